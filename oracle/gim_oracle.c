@@ -1,0 +1,494 @@
+/* oracle/gim_oracle.c — the parity ORACLE for the gIM / IMM hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY. Nothing outside tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load or call this code. It shares no code, header,
+ * table or constant generator with the CUDA library (paper_2009_07325_b200/); neither side
+ * includes or links the other. Inputs come from gim_inputs/ (graph generator, no method
+ * arithmetic).
+ *
+ * A plain, slow, obviously-correct, single-threaded implementation of what the GPU path must
+ * reproduce bit for bit. Citations: "P:n" = /root/reference/PAPER.md line n (gIM paper,
+ * arXiv 2009.07325); "O1..O9" and "R1..R25" = SURVEY.md §8(c) oracle steps and readings
+ * (restated in DESIGN.md). Parity status of every function: pinned (see tests/test_oracle_*.py
+ * and DESIGN.md "Oracle pins"); none is "parity unpinned".
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fPIC -shared gim_oracle.c -lm  (no -ffast-math)
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------------------
+ * O2. Philox4x32-10 (Salmon et al., SC'11 "Parallel random numbers: as easy as 1, 2, 3").
+ * The paper only says "p = U(0,1)" (Alg. 3 l.18) — reading R16 fixes the generator.
+ * ------------------------------------------------------------------------------------------ */
+void og_philox(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+  uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+  uint32_t k0 = key_in[0], k1 = key_in[1];
+  int r;
+  for (r = 0; r < 10; ++r) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n1 = lo1;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    uint32_t n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Key scheme (O2): key = (seed_lo, seed_hi); counter = (id_lo, id_hi, s_lo, s_hi). */
+static void keyed(uint64_t seed, uint64_t id, uint64_t slot, uint32_t out[4]) {
+  uint32_t ctr[4], key[2];
+  ctr[0] = (uint32_t)id;   ctr[1] = (uint32_t)(id >> 32);
+  ctr[2] = (uint32_t)slot; ctr[3] = (uint32_t)(slot >> 32);
+  key[0] = (uint32_t)seed; key[1] = (uint32_t)(seed >> 32);
+  og_philox(ctr, key, out);
+}
+
+#define SLOT_ROOT (((uint64_t)1) << 63)          /* tag 10 */
+#define SLOT_LT (((uint64_t)1) << 62)            /* tag 01 */
+#define SLOT_MC (((uint64_t)3) << 62)            /* tag 11: oracle-only forward Monte-Carlo */
+
+/* O3. root_i = floor(u64 * n / 2^64) — "u = randSelect(V)" (Alg. 3 l.5; reading R17). */
+uint32_t og_root(uint64_t seed, uint64_t id, uint32_t n) {
+  uint32_t o[4];
+  uint64_t u64;
+  keyed(seed, id, SLOT_ROOT, o);
+  u64 = (uint64_t)o[0] | ((uint64_t)o[1] << 32);
+  return (uint32_t)(((unsigned __int128)u64 * (unsigned __int128)n) >> 64);
+}
+
+/* O4. coin(i, e) = word (e & 3) of Philox(seed; i, e >> 2). */
+uint32_t og_coin(uint64_t seed, uint64_t id, uint64_t e) {
+  uint32_t o[4];
+  keyed(seed, id, e >> 2, o);
+  return o[e & 3];
+}
+
+/* LT draw at node v (O5). */
+uint32_t og_lt_draw(uint64_t seed, uint64_t id, uint32_t v) {
+  uint32_t o[4];
+  keyed(seed, id, SLOT_LT | (uint64_t)v, o);
+  return o[0];
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Context: graph (O1) + pool (O6).
+ * ------------------------------------------------------------------------------------------ */
+enum { OG_IC = 0, OG_LT = 1 };
+enum { OG_W_EXPLICIT = 0, OG_W_WC = 1, OG_W_UNIFORM = 2 };
+
+typedef struct og_ctx {
+  uint32_t n;
+  uint64_t m;
+  uint64_t* row_ptr;      /* in-CSR, n+1 */
+  uint32_t* src;          /* m */
+  float* w;               /* m or NULL */
+  int model, scheme;
+  float p_uniform;
+  uint64_t thr_uniform;   /* ceil(p * 2^32) */
+  uint64_t* thr_edge;     /* explicit IC: ceil(w_e * 2^32); explicit LT: floor(w_e * 2^32) */
+  /* out-CSR for the forward Monte-Carlo check only */
+  uint64_t* out_ptr;
+  uint32_t* out_dst;
+  uint64_t* out_in_slot;  /* in-CSR slot of each out-edge (to read its weight) */
+  /* scratch */
+  uint8_t* visited;
+  uint32_t* queue;
+  /* pool (O6) */
+  uint64_t seed;
+  int have_seed;
+  uint64_t nsets, pool_len, cap_sets, cap_pool;
+  uint64_t* offsets;      /* nsets+1 */
+  uint32_t* nodes;
+  uint32_t* count;        /* n */
+  /* workload statistics */
+  uint64_t stat_coins, stat_live;
+} og_ctx;
+
+static int cmp_u32(const void* a, const void* b) {
+  uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  return (x > y) - (x < y);
+}
+
+void og_destroy(og_ctx* c) {
+  if (!c) return;
+  free(c->row_ptr); free(c->src); free(c->w); free(c->thr_edge);
+  free(c->out_ptr); free(c->out_dst); free(c->out_in_slot);
+  free(c->visited); free(c->queue);
+  free(c->offsets); free(c->nodes); free(c->count);
+  free(c);
+}
+
+/* Graph arrays are copied. Returns NULL on invalid input. */
+og_ctx* og_create(uint32_t n, uint64_t m, const uint64_t* row_ptr, const uint32_t* src,
+                  const float* w, int model, int scheme, float p_uniform) {
+  og_ctx* c;
+  uint64_t e;
+  uint32_t v;
+  if (n < 1) return NULL;
+  if (scheme == OG_W_EXPLICIT && !w) return NULL;
+  c = (og_ctx*)calloc(1, sizeof(og_ctx));
+  c->n = n; c->m = m; c->model = model; c->scheme = scheme; c->p_uniform = p_uniform;
+  c->row_ptr = (uint64_t*)malloc(sizeof(uint64_t) * (n + 1));
+  c->src = (uint32_t*)malloc(sizeof(uint32_t) * (m ? m : 1));
+  memcpy(c->row_ptr, row_ptr, sizeof(uint64_t) * (n + 1));
+  if (m) memcpy(c->src, src, sizeof(uint32_t) * m);
+  /* O4: live iff coin * 2^-32 < p, exactly: coin < ceil(p * 2^32). p*2^32 is exact in double
+   * for a float32 p. */
+  c->thr_uniform = (uint64_t)ceil((double)p_uniform * 4294967296.0);
+  if (scheme == OG_W_EXPLICIT) {
+    c->w = (float*)malloc(sizeof(float) * (m ? m : 1));
+    c->thr_edge = (uint64_t*)malloc(sizeof(uint64_t) * (m ? m : 1));
+    if (m) memcpy(c->w, w, sizeof(float) * m);
+    for (e = 0; e < m; ++e) {
+      double x = (double)w[e] * 4294967296.0;
+      c->thr_edge[e] = (model == OG_LT) ? (uint64_t)floor(x) : (uint64_t)ceil(x);
+    }
+  }
+  /* out-CSR (transpose), used only by og_mc_spread */
+  c->out_ptr = (uint64_t*)calloc(n + 1, sizeof(uint64_t));
+  c->out_dst = (uint32_t*)malloc(sizeof(uint32_t) * (m ? m : 1));
+  c->out_in_slot = (uint64_t*)malloc(sizeof(uint64_t) * (m ? m : 1));
+  for (e = 0; e < m; ++e) c->out_ptr[src[e] + 1]++;
+  for (v = 0; v < n; ++v) c->out_ptr[v + 1] += c->out_ptr[v];
+  {
+    uint64_t* cur = (uint64_t*)malloc(sizeof(uint64_t) * n);
+    memcpy(cur, c->out_ptr, sizeof(uint64_t) * n);
+    for (v = 0; v < n; ++v)
+      for (e = row_ptr[v]; e < row_ptr[v + 1]; ++e) {
+        uint64_t pos = cur[src[e]]++;
+        c->out_dst[pos] = v;
+        c->out_in_slot[pos] = e;
+      }
+    free(cur);
+  }
+  c->visited = (uint8_t*)calloc(n, 1);
+  c->queue = (uint32_t*)malloc(sizeof(uint32_t) * n);
+  c->cap_sets = 1024;
+  c->offsets = (uint64_t*)calloc(c->cap_sets + 1, sizeof(uint64_t));
+  c->cap_pool = 4096;
+  c->nodes = (uint32_t*)malloc(sizeof(uint32_t) * c->cap_pool);
+  c->count = (uint32_t*)calloc(n, sizeof(uint32_t));
+  return c;
+}
+
+static uint64_t deg_in(const og_ctx* c, uint32_t v) { return c->row_ptr[v + 1] - c->row_ptr[v]; }
+
+/* O4: edge e (an in-edge of v) is live in RR set `id`. */
+static int ic_live(og_ctx* c, uint64_t seed, uint64_t id, uint64_t e, uint32_t v) {
+  uint64_t coin = og_coin(seed, id, e);
+  c->stat_coins++;
+  if (c->scheme == OG_W_WC) return coin * deg_in(c, v) < ((uint64_t)1 << 32);   /* p = 1/d_in(v) */
+  if (c->scheme == OG_W_UNIFORM) return coin < c->thr_uniform;
+  return coin < c->thr_edge[e];
+}
+
+/* O4. IC RR set: reverse BFS over live in-edges from a uniform root — the RR set definition of
+ * P:166-168 realised as the randomized BFS of P:260 / Alg. 3 l.8-22, with the root
+ * marked visited (R12) and exact set semantics (R13). Writes the set, ascending, to out[];
+ * returns its size. */
+static uint32_t rr_ic(og_ctx* c, uint64_t seed, uint64_t id, uint32_t* out) {
+  uint32_t head = 0, tail = 0, i;
+  uint32_t root = og_root(seed, id, c->n);
+  c->visited[root] = 1;
+  c->queue[tail++] = root;
+  while (head < tail) {
+    uint32_t v = c->queue[head++];
+    uint64_t e;
+    for (e = c->row_ptr[v]; e < c->row_ptr[v + 1]; ++e) {
+      if (ic_live(c, seed, id, e, v)) {
+        uint32_t u = c->src[e];
+        c->stat_live++;
+        if (!c->visited[u]) {
+          c->visited[u] = 1;
+          c->queue[tail++] = u;
+        }
+      }
+    }
+  }
+  for (i = 0; i < tail; ++i) { c->visited[c->queue[i]] = 0; out[i] = c->queue[i]; }
+  qsort(out, tail, sizeof(uint32_t), cmp_u32);
+  return tail;
+}
+
+/* O5. LT RR set: reverse random walk choosing at most one in-edge per node according to the
+ * edge weights, frontier <= 1, stopping at a node with no chosen edge or at an
+ * already-visited node (R19). Half-open fixed-point intervals (R18). */
+static uint32_t rr_lt(og_ctx* c, uint64_t seed, uint64_t id, uint32_t* out) {
+  uint32_t len = 0, i;
+  uint32_t v = og_root(seed, id, c->n);
+  c->visited[v] = 1;
+  c->queue[len++] = v;
+  for (;;) {
+    uint64_t d = deg_in(c, v);
+    uint64_t r, j;
+    uint32_t u;
+    if (d == 0) break;
+    r = og_lt_draw(seed, id, v);
+    c->stat_coins++;
+    if (c->scheme == OG_W_WC) {
+      j = (r * d) >> 32;                     /* uniform in-neighbour: weights 1/d */
+    } else {
+      uint64_t acc = 0, t;
+      j = d;
+      for (t = 0; t < d; ++t) {
+        acc += c->thr_edge[c->row_ptr[v] + t];
+        if (r < acc) { j = t; break; }
+      }
+      if (j == d) break;                     /* r beyond the total weight: no live in-edge */
+    }
+    c->stat_live++;
+    u = c->src[c->row_ptr[v] + j];
+    if (c->visited[u]) break;
+    c->visited[u] = 1;
+    c->queue[len++] = u;
+    v = u;
+  }
+  for (i = 0; i < len; ++i) { c->visited[c->queue[i]] = 0; out[i] = c->queue[i]; }
+  qsort(out, len, sizeof(uint32_t), cmp_u32);
+  return len;
+}
+
+uint32_t og_rr_set(og_ctx* c, uint64_t seed, uint64_t id, uint32_t* out) {
+  return (c->model == OG_LT) ? rr_lt(c, seed, id, out) : rr_ic(c, seed, id, out);
+}
+
+/* O6. Extend (or truncate) the pool to exactly { RR(seed, i) : 0 <= i < T } in id order, with
+ * count[v] = #{i : v in RR_i} — Occur of P:285 / Alg. 3 l.13, RR + Offsets_RR of Alg. 6
+ * (P:435-445), except that sets are stored in id order (R20). A different seed restarts. */
+int og_generate(og_ctx* c, uint64_t T, uint64_t seed) {
+  uint64_t i, j;
+  if (!c->have_seed || c->seed != seed) {
+    c->nsets = 0; c->pool_len = 0; c->offsets[0] = 0;
+    memset(c->count, 0, sizeof(uint32_t) * c->n);
+    c->seed = seed; c->have_seed = 1;
+  }
+  while (c->nsets > T) {                      /* truncate */
+    uint64_t a = c->offsets[c->nsets - 1], b = c->offsets[c->nsets];
+    for (j = a; j < b; ++j) c->count[c->nodes[j]]--;
+    c->nsets--; c->pool_len = a;
+  }
+  for (i = c->nsets; i < T; ++i) {
+    uint32_t len;
+    if (c->nsets + 1 > c->cap_sets) {
+      c->cap_sets *= 2;
+      c->offsets = (uint64_t*)realloc(c->offsets, sizeof(uint64_t) * (c->cap_sets + 1));
+    }
+    if (c->pool_len + c->n > c->cap_pool) {
+      while (c->pool_len + c->n > c->cap_pool) c->cap_pool *= 2;
+      c->nodes = (uint32_t*)realloc(c->nodes, sizeof(uint32_t) * c->cap_pool);
+    }
+    len = og_rr_set(c, seed, i, c->nodes + c->pool_len);
+    for (j = 0; j < len; ++j) c->count[c->nodes[c->pool_len + j]]++;
+    c->pool_len += len;
+    c->nsets++;
+    c->offsets[c->nsets] = c->pool_len;
+  }
+  return 0;
+}
+
+uint64_t og_num_sets(const og_ctx* c) { return c->nsets; }
+uint64_t og_pool_len(const og_ctx* c) { return c->pool_len; }
+void og_export(const og_ctx* c, uint64_t* offsets_out, uint32_t* nodes_out, uint32_t* count_out) {
+  if (offsets_out) memcpy(offsets_out, c->offsets, sizeof(uint64_t) * (c->nsets + 1));
+  if (nodes_out && c->pool_len) memcpy(nodes_out, c->nodes, sizeof(uint32_t) * c->pool_len);
+  if (count_out) memcpy(count_out, c->count, sizeof(uint32_t) * c->n);
+}
+void og_stats(const og_ctx* c, uint64_t out[2]) { out[0] = c->stat_coins; out[1] = c->stat_live; }
+
+/* ------------------------------------------------------------------------------------------
+ * O7. NodeSelection: greedy max coverage over a pool of ascending sets — Alg. 1 l.6-10
+ * with the counter method of §3.8 and Alg. 7 literally:
+ * for each pick, scan every uncovered set for u; if found, flag it covered and decrement the
+ * counter of every member (u included, R11). Argmax over unselected nodes, ties -> lowest id,
+ * zero maximum allowed (R10). Non-destructive (R9): starts from the given counts.
+ * ------------------------------------------------------------------------------------------ */
+static int contains_sorted(const uint32_t* a, uint64_t len, uint32_t u) {
+  uint64_t lo = 0, hi = len;
+  while (lo < hi) {
+    uint64_t mid = lo + (hi - lo) / 2;
+    if (a[mid] < u) lo = mid + 1; else hi = mid;
+  }
+  return lo < len && a[lo] == u;
+}
+
+int og_select_pool(uint32_t n, uint64_t nsets, const uint64_t* offsets, const uint32_t* nodes,
+                   const uint32_t* count, uint32_t k, uint32_t* seeds_out, uint64_t* gains_out,
+                   uint64_t* cov_out) {
+  int64_t* cnt;
+  uint8_t *covered, *selected;
+  uint64_t i, w, cov = 0;
+  uint32_t j, v;
+  if (k < 1 || k > n) return 1;
+  cnt = (int64_t*)malloc(sizeof(int64_t) * n);
+  covered = (uint8_t*)calloc(nsets ? nsets : 1, 1);
+  selected = (uint8_t*)calloc(n, 1);
+  for (v = 0; v < n; ++v) cnt[v] = count[v];
+  for (j = 0; j < k; ++j) {
+    int64_t best = -1;
+    uint32_t u = 0;
+    for (v = 0; v < n; ++v)
+      if (!selected[v] && cnt[v] > best) { best = cnt[v]; u = v; }
+    selected[u] = 1;
+    seeds_out[j] = u;
+    if (gains_out) gains_out[j] = (uint64_t)best;
+    cov += (uint64_t)best;
+    for (i = 0; i < nsets; ++i) {                       /* Alg. 7 l.1 */
+      uint64_t off = offsets[i], len = offsets[i + 1] - offsets[i];
+      if (covered[i]) continue;                          /* l.2 */
+      if (!contains_sorted(nodes + off, len, u)) continue;  /* l.3-10 */
+      covered[i] = 1;                                    /* l.12 */
+      for (w = 0; w < len; ++w) cnt[nodes[off + w]]--;   /* l.13-15 */
+    }
+  }
+  if (cov_out) *cov_out = cov;
+  free(cnt); free(covered); free(selected);
+  return 0;
+}
+
+int og_select(og_ctx* c, uint32_t k, uint32_t* seeds_out, uint64_t* gains_out, uint64_t* cov_out) {
+  if (c->nsets == 0) return 2;
+  return og_select_pool(c->n, c->nsets, c->offsets, c->nodes, c->count, k, seeds_out, gains_out,
+                        cov_out);
+}
+
+/* ------------------------------------------------------------------------------------------
+ * O8. IMM constants. The paper defers f(n, eps, k) and lambda to IMM (
+ * readings R1-R3): lambda' and lambda* of Tang, Shi, Xiao (SIGMOD'15). Double, contraction off,
+ * expression order fixed.
+ * out = { ell_eff, eps_prime, lnC, lambda_prime, alpha, beta, lambda_star }
+ * ------------------------------------------------------------------------------------------ */
+int og_imm_constants(uint32_t n, uint32_t k, double eps, double ell, double out[7]) {
+  double ln_n, log2n, ell_eff, eps_p, lnC = 0.0, lambda_p, alpha, beta, lambda_s, e = M_E;
+  uint32_t t;
+  if (n < 2 || k < 1 || k > n || !(eps > 0.0 && eps < 1.0) || !(ell > 0.0)) return 1;
+  ln_n = log((double)n);
+  log2n = log2((double)n);
+  ell_eff = ell * (1.0 + log(2.0) / ln_n);
+  eps_p = sqrt(2.0) * eps;
+  for (t = 1; t <= k; ++t) lnC += log((double)(n - k + t)) - log((double)t);
+  lambda_p = (2.0 + 2.0 / 3.0 * eps_p) * (lnC + ell_eff * ln_n + log(log2n)) * (double)n / (eps_p * eps_p);
+  alpha = sqrt(ell_eff * ln_n + log(2.0));
+  beta = sqrt((1.0 - 1.0 / e) * (lnC + ell_eff * ln_n + log(2.0)));
+  {
+    double s = (1.0 - 1.0 / e) * alpha + beta;
+    lambda_s = 2.0 * (double)n * (s * s) / (eps * eps);
+  }
+  out[0] = ell_eff; out[1] = eps_p; out[2] = lnC; out[3] = lambda_p;
+  out[4] = alpha; out[5] = beta; out[6] = lambda_s;
+  return 0;
+}
+
+/* O8 driver: Alg. 2 rounds, then theta = lambda_star / LB and the final selection
+ * (Alg. 1). Readings R4-R8. Cumulative pool (IMM reuses the estimation sets).
+ * dres = { LB, theta, spread_est, ell_eff, eps_prime, lambda_prime, lambda_star }
+ * tr_theta[i] = theta_i (double), tr_T[i] = ceil(theta_i), tr_cov[i] = covered count of round i.
+ * ures = { rounds, R_final, cov_final }. */
+int og_imm(og_ctx* c, uint32_t k, double eps, double ell, uint64_t seed, uint32_t* seeds_out,
+           uint64_t* gains_out, double dres[7], double tr_theta[64], uint64_t tr_T[64],
+           uint64_t tr_cov[64], uint64_t ures[3]) {
+  double K[7], n = (double)c->n, LB = 1.0, theta, log2n;
+  uint64_t cov = 0, T, R;
+  int i, i_max, rounds = 0;
+  uint32_t* tmp_seeds;
+  if (og_imm_constants(c->n, k, eps, ell, K)) return 1;
+  tmp_seeds = (uint32_t*)malloc(sizeof(uint32_t) * k);
+  c->have_seed = 0;                                      /* IMM starts from R = {} */
+  og_generate(c, 0, seed);
+  log2n = log2(n);
+  i_max = (int)floor(log2n) - 1;                         /* R5 */
+  for (i = 1; i <= i_max && i <= 64; ++i) {
+    double x = n / ldexp(1.0, i);                        /* Alg. 2 l.3 */
+    double theta_i = K[3] / x;                           /* l.4 */
+    T = (uint64_t)ceil(theta_i);
+    R = c->nsets > T ? c->nsets : T;                     /* l.5, R4 */
+    og_generate(c, R, seed);
+    og_select(c, k, tmp_seeds, NULL, &cov);              /* l.6, R9 */
+    tr_theta[i - 1] = theta_i; tr_T[i - 1] = T; tr_cov[i - 1] = cov;
+    rounds = i;
+    if ((n * (double)cov) / (double)c->nsets >= (1.0 + K[1]) * x) {   /* l.7, R7 */
+      LB = (n * (double)cov) / (double)c->nsets / (1.0 + K[1]);       /* l.8 */
+      break;
+    }
+  }
+  theta = K[6] / LB;                                     /* R2 */
+  T = (uint64_t)ceil(theta);
+  R = c->nsets > T ? c->nsets : T;                       /* R8: reuse, no truncation */
+  og_generate(c, R, seed);
+  og_select(c, k, seeds_out, gains_out, &cov);
+  dres[0] = LB; dres[1] = theta; dres[2] = n * (double)cov / (double)c->nsets;   /* Eq. 3 */
+  dres[3] = K[0]; dres[4] = K[1]; dres[5] = K[3]; dres[6] = K[6];
+  ures[0] = (uint64_t)rounds; ures[1] = c->nsets; ures[2] = cov;
+  free(tmp_seeds);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Forward Monte-Carlo spread (verification only; uses none of the reverse machinery).
+ * IC per P:120: each newly active u tries each out-edge once with probability p_uv.
+ * LT per Eq. 1: thresholds tau_v ~ U(0,1); v activates when the summed weight of
+ * its active in-neighbours reaches tau_v (iterated to the fixpoint, which is order-free).
+ * Randomness: Philox keyed (mc_seed; trial, tag-11 slot), independent of any RR stream.
+ * ------------------------------------------------------------------------------------------ */
+static double edge_p(const og_ctx* c, uint64_t in_slot, uint32_t v) {
+  if (c->scheme == OG_W_WC) return 1.0 / (double)deg_in(c, v);
+  if (c->scheme == OG_W_UNIFORM) return (double)c->p_uniform;
+  return (double)c->w[in_slot];
+}
+
+int og_mc_spread(og_ctx* c, const uint32_t* S, uint32_t k, uint64_t trials, uint64_t mc_seed,
+                 double* mean_out, double* stderr_out) {
+  uint32_t* q = (uint32_t*)malloc(sizeof(uint32_t) * c->n);
+  uint8_t* act = (uint8_t*)calloc(c->n, 1);
+  double* acc = (double*)calloc(c->n, sizeof(double));
+  uint32_t* touched = (uint32_t*)malloc(sizeof(uint32_t) * (c->m + c->n + 1));
+  double sum = 0.0, sum2 = 0.0;
+  uint64_t t;
+  for (t = 0; t < trials; ++t) {
+    uint32_t head = 0, tail = 0, ntouch = 0, i;
+    for (i = 0; i < k; ++i)
+      if (!act[S[i]]) { act[S[i]] = 1; q[tail++] = S[i]; }
+    while (head < tail) {
+      uint32_t u = q[head++];
+      uint64_t e;
+      for (e = c->out_ptr[u]; e < c->out_ptr[u + 1]; ++e) {
+        uint32_t v = c->out_dst[e];
+        double p;
+        if (act[v]) continue;
+        p = edge_p(c, c->out_in_slot[e], v);
+        if (c->model == OG_IC) {
+          uint32_t o[4];
+          keyed(mc_seed, t, SLOT_MC | (e >> 2), o);
+          if ((double)o[e & 3] < p * 4294967296.0) { act[v] = 1; q[tail++] = v; }
+        } else {
+          uint32_t o[4];
+          double tau;
+          keyed(mc_seed, t, SLOT_MC | (((uint64_t)1) << 40) | (uint64_t)v, o);
+          tau = ((double)o[0] + 0.5) / 4294967296.0;      /* tau_v ~ U(0,1) */
+          if (acc[v] == 0.0) touched[ntouch++] = v;
+          acc[v] += p;
+          if (acc[v] >= tau) { act[v] = 1; q[tail++] = v; }
+        }
+      }
+    }
+    sum += (double)tail;
+    sum2 += (double)tail * (double)tail;
+    for (i = 0; i < tail; ++i) act[q[i]] = 0;
+    for (i = 0; i < ntouch; ++i) acc[touched[i]] = 0.0;
+  }
+  *mean_out = sum / (double)trials;
+  {
+    double var = sum2 / (double)trials - (*mean_out) * (*mean_out);
+    *stderr_out = sqrt((var > 0 ? var : 0) / (double)trials);
+  }
+  free(q); free(act); free(acc); free(touched);
+  return 0;
+}

@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""bench.py — RR sets/s & IMM time of the gIM/IMM hot path on B200 (BASELINE.json metric).
+
+One step = one full IMM run (gim_imm: every Alg. 2 round of RR sampling + NodeSelection, then
+theta = lambda*/LB, the final sampling and the final NodeSelection) on the workload named by
+--workload (default C3: LiveJournal-shaped synthetic graph, IC weighted cascade, k=50,
+eps=0.1, ell=1), with the graph resident in HBM. value = RR sets generated (global R_final,
+summed over steps) / device time of the K timed steps (max over ranks). Every rank holds the
+replicated graph and generates its contiguous slice of every RR-id range (weak-by-ids
+sharding, "scaling": "strong" since the per-job work is fixed); selection all-reduces counts
+over NCCL.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gim|reference] [--workload C3]
+
+--impl reference times the oracle (oracle/, single-threaded C, as it stands) on a bounded
+sample of the same workload on the host cores.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import gim_inputs as gi  # noqa: E402
+
+METRIC = "RR sets/s & IMM time (k=50, ε=0.1) at 1/2/4/8 B200; HBM GB/s vs peak"
+UNIT = "RR sets/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gim", choices=["gim", "reference"])
+    ap.add_argument("--workload", default="C3", choices=sorted(gi.WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def config_of(w, world):
+    return {"workload": f"{w.key}: {w.desc}", "n": w.n, "m": w.m, "k": w.k, "eps": w.eps,
+            "ell": w.ell, "model": "IC" if w.model == gi.IC else "LT",
+            "weights": {gi.W_WC: "weighted cascade 1/d_in", gi.W_UNIFORM: f"uniform p={w.p_uniform}",
+                        gi.W_EXPLICIT: "explicit"}[w.scheme],
+            "generator": f"plg gamma={w.gamma} rho={w.rho} d_cap={w.d_cap} graph_seed={w.graph_seed}",
+            "rr_seed": w.rr_seed, "parallelism": f"dp{world} (RR-id slices, replicated graph)",
+            "l2": "inputs larger than L2 (C3/C4/C5 graphs exceed the 126 MB L2)" if w.m > 30_000_000
+            else "graph is L2-resident (no flush between steps)"}
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(gpu_index), "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for nm, val in zip(names, r[5:9]):
+                    if val.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                pass
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# reference arm: the oracle on the host cores
+# ------------------------------------------------------------------------------------------
+def oracle_sample(w, g, seconds, k):
+    """Oracle RR generation (ids 0..T-1, grown in chunks until `seconds` elapse) followed by one
+    NodeSelection (k) over that sample; returns (sets, wall seconds)."""
+    import oracle
+    o = oracle.Oracle(g, w.model, w.scheme, w.p_uniform)
+    t0 = time.perf_counter()
+    T, chunk = 0, 2000
+    while time.perf_counter() - t0 < seconds:
+        T += chunk
+        o.generate(T, w.rr_seed)
+    o.select(k)
+    return T, time.perf_counter() - t0
+
+
+def run_reference(args, w):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    g = gi.workload_graph(w.key)
+    per_step = max(1.0, min(10.0, 60.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(w, g, per_step / 4, w.k)
+    tot_sets, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        T, s = oracle_sample(w, g, per_step, w.k)
+        tot_sets += T
+        tot_s += s
+    v = tot_sets / tot_s
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_s / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": config_of(w, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"per step: oracle RR sets of ids 0..T-1 for ~{per_step:.1f}s, "
+                                       f"then one k={w.k} NodeSelection over them"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------
+def alu_peak_gcoins(sm_mhz, sms=148):
+    """ALU roof of IC sampling: one Philox4x32-10 = 20 IMAD.WIDE.U32 on
+    the FMA pipe (reciprocal throughput 2 cycles per warp instruction per SM sub-partition,
+    B300_MICROARCH.md "Pipe rates"), 4 SMSPs per SM -> 3.2 Philox = 12.8 coins per cycle per SM."""
+    return 12.8 * sms * sm_mhz * 1e6 / 1e9
+
+
+def load_profile_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+def run_gim(args, w):
+    import torch
+    import torch.distributed as dist
+    import paper_2009_07325_b200 as P
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    g = gi.workload_graph(w.key)
+    stream = torch.cuda.Stream(local)
+    ctx = P.Gim(local, stream=stream.cuda_stream)
+    ctx.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme, weights=g.weights, p_uniform=w.p_uniform)
+    if world > 1:
+        ctx.set_shard(rank, world)
+        ctx.set_allreduce(P.torch_allreduce())
+    ctx.set_option(P.OPT_PROFILE, 1)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 0)):
+        ctx.imm(w.k, w.eps, w.ell, w.rr_seed)
+    ctx.reset_stats()
+    barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local) if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    results = [ctx.imm(w.k, w.eps, w.ell, w.rr_seed) for _ in range(args.steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop() if clk else None
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    st = ctx.stats()
+    total_sets = sum(r.R_final for r in results)
+    value = total_sets / (ms / 1000.0)
+    r0 = results[-1]
+
+    # ---- dominant kernel roofline: K-RR (warp-per-RR sampling), ALU-bound by Philox ----------
+    rr_ms = st["ms_rr"]
+    n_rr = max(st["n_rr_launches"], 1)
+    coins = st["coins"]
+    sm_max = (clocks or {}).get("sm_max_mhz") or 1965.0
+    peak = alu_peak_gcoins(sm_max)
+    achieved = coins / (rr_ms / 1000.0) / 1e9 if rr_ms > 0 else 0.0
+    # algorithmic bytes of K-RR: 12 B per set (size+offset) + 8 B row_ptr pair and 4 B staging
+    # write per visited node + 4 B src per live in-edge (coins are drawn before any load)
+    warp_elems = st["rr_elements"]
+    alg_bytes = 12 * st["rr_sets"] + 12 * warp_elems + 4 * st["live_edges"]
+    traffic = load_profile_traffic().get(f"{w.key}:k_rr_warp")
+    measured_philox = None
+    try:
+        groups = 1 << 30
+        mb_ms = ctx.microbench_philox(groups)
+        measured_philox = 4 * groups / (mb_ms / 1000.0) / 1e9
+    except Exception:
+        pass
+    mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = mp.get("hbm_gbs", 6650.0)
+    roofline = {
+        "kernel": "k_rr_warp (K-IC warp-per-RR sampling)" if w.model == gi.IC else "k_rr_warp (K-LT)",
+        "bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gcoin/s",
+        "frac": achieved / peak if peak else None,
+        "traffic": traffic,
+        "per_launch_ms": rr_ms / n_rr, "launches": n_rr,
+        "coins_per_launch": coins / n_rr,
+        "peak_basis": f"derived: 12.8 coins/cycle/SM x 148 SMs x {sm_max:.0f} MHz (Philox4x32-10 = 20 IMAD.WIDE on the FMA pipe)",
+        "philox_microbench_gcoins": measured_philox,
+        "frac_of_microbench": (achieved / measured_philox) if measured_philox else None,
+        "algorithmic_gbs": alg_bytes / (rr_ms / 1000.0) / 1e9 if rr_ms > 0 else None,
+        "hbm_peak_gbs": hbm_peak,
+        "hbm_frac": (alg_bytes / (rr_ms / 1000.0) / 1e9) / hbm_peak if rr_ms > 0 else None,
+        "hbm_peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy)" if mp else "fallback 6.65 TB/s",
+    }
+    phases = {"ms_rr": st["ms_rr"] / args.steps, "ms_giant": st["ms_giant"] / args.steps,
+              "ms_store": st["ms_store"] / args.steps, "ms_inv": st["ms_inv"] / args.steps,
+              "ms_select": st["ms_select"] / args.steps}
+    gen_ms = st["ms_rr"] + st["ms_giant"] + st["ms_store"]
+
+    # ---- end to end through the public API with host buffers -------------------------------
+    e2e = None
+    if not args.no_e2e:
+        rp_h = torch.from_numpy(g.row_ptr).pin_memory()
+        src_h = torch.from_numpy(g.src).pin_memory()
+        ctx2 = P.Gim(local, stream=stream.cuda_stream)
+        if world > 1:
+            ctx2.set_shard(rank, world)
+            ctx2.set_allreduce(P.torch_allreduce())
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        e2e_sets = 0
+        for _ in range(args.steps):
+            ctx2.load_graph(g.n, rp_h.numpy(), src_h.numpy(), w.model, w.scheme, weights=g.weights,
+                            p_uniform=w.p_uniform)
+            if world > 1:
+                ctx2.set_shard(rank, world)
+            r = ctx2.imm(w.k, w.eps, w.ell, w.rr_seed)
+            e2e_sets += r.R_final
+        f1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms2 = max_over_ranks(f0.elapsed_time(f1))
+        e2e = {"value": e2e_sets / (ms2 / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(g.row_ptr.nbytes + g.src.nbytes),
+               "d2h_bytes_per_step": int(4 * w.k + 8 * w.k * (r.rounds + 1)),
+               "ms_per_step": ms2 / args.steps,
+               "note": "gim_load_graph (host validation + H2D from pinned host buffers) + gim_imm + seeds D2H per step"}
+        ctx2.close()
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) --------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        T, s = oracle_sample(w, g, args.cpu_seconds, w.k)
+        cpu = {"value": T / s, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"oracle RR sets of ids 0..{T - 1} ({s:.1f}s) + one k={w.k} NodeSelection over them, "
+                         "single-threaded C"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                "config": config_of(w, world),
+                "imm_time_s": ms / args.steps / 1000.0,
+                "rr_sets_per_step": r0.R_final, "theta": r0.theta, "LB": r0.LB, "rounds": r0.rounds,
+                "spread_est": r0.spread_est,
+                "rr_gen_sets_per_s": (st["rr_sets"] * world) / (gen_ms / 1000.0) if gen_ms > 0 else None,
+                "phase_ms_per_step": phases,
+                "rr_stats": {"mean_len": st["rr_elements"] / max(st["rr_sets"], 1),
+                             "coins_per_set": (st["coins"] + st["coins_giant"]) / max(st["rr_sets"], 1),
+                             "giant_frac": st["giant_sets"] / max(st["rr_sets"], 1)},
+                "gpu_launches": st["launches"],
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+                "seeds_head": r0.seeds[:8].tolist()}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    w = gi.WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, w)
+    else:
+        run_gim(args, w)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+/* gim.h — C ABI of the B200-native gIM/IMM hot path (libgim.so, sm_100a).
+ *
+ * The calls follow the problem statement of the paper (§2.3, Eq. 2): given
+ * a graph G, influence probabilities p_uv, a diffusion model and k, find a seed set S with
+ * |S| = k maximising E[I(S)]. The method is IMM's two steps as gIM accelerates them (Alg. 1,
+ * P:178-198; Alg. 2): RR-set sampling (Alg. 3/6) and greedy
+ * max-coverage NodeSelection (§3.8, Alg. 7). "P:n" = line n of the paper
+ * (/root/reference/PAPER.md); "R1..R25" = readings of the paper listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns gim_status (GIM_OK = 0). On error gim_last_error(ctx) returns a
+ *    NUL-terminated message owned by ctx, valid until the next call on ctx. No exceptions
+ *    cross the ABI; no CPU fallback exists: without a usable CUDA device gim_create fails with
+ *    GIM_ECUDA.
+ *  - Node ids are dense uint32 in [0, n). Host arrays passed in are copied; the caller keeps
+ *    ownership. Output arrays are caller-allocated host memory.
+ *  - A ctx is bound to one device and one CUDA stream; it is not thread-safe. All device work
+ *    is enqueued on the ctx stream, and every call returns after its results are host-visible.
+ *  - The RR-set randomness is a pure function of (seed, RR id): Philox4x32-10 with key
+ *    (seed_lo, seed_hi) and counter (id_lo, id_hi, slot_lo, slot_hi) (reading R16; DESIGN.md
+ *    "RNG contract"), so every RR set is reproducible bit for bit on any number of GPUs.
+ */
+#ifndef GIM_H_
+#define GIM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GIM_OK = 0,
+  GIM_EINVAL = 1,      /* invalid argument (sizes, ranges, non-canonical CSR, k, eps, ell) */
+  GIM_ESTATE = 2,      /* call not valid in the current state (no graph, empty pool)     */
+  GIM_ENOMEM = 3,      /* device allocation failed                                        */
+  GIM_ECUDA = 4,       /* CUDA runtime / kernel error, or no device                       */
+  GIM_ECOLL = 5,       /* the all-reduce callback returned non-zero                       */
+  GIM_ELTWEIGHT = 6    /* LT with explicit weights whose in-sum exceeds 1 at some node    */
+} gim_status;
+
+typedef enum { GIM_IC = 0, GIM_LT = 1 } gim_model;          /* PAPER.md §2.2 */
+typedef enum { GIM_W_EXPLICIT = 0, GIM_W_WC = 1, GIM_W_UNIFORM = 2 } gim_weights;
+
+typedef struct gim_ctx gim_ctx;   /* opaque; one per (process, device) */
+
+/* Create a context on CUDA device `device`. cuda_stream is a cudaStream_t (may be NULL: the
+ * library creates its own non-blocking stream). Errors: GIM_ECUDA (no device / bad id). */
+gim_status gim_create(int device, void* cuda_stream, gim_ctx** out);
+
+/* Free every device allocation of ctx and ctx itself. NULL is a no-op. */
+void gim_destroy(gim_ctx* ctx);
+
+/* Last error message of ctx (never NULL; "" after success). */
+const char* gim_last_error(const gim_ctx* ctx);
+
+/* Load the graph (§3.2 "Graph Representation", as an in-CSR: reading R14).
+ *  in_row_ptr[n+1], in_src[m]: row v lists the sources u of edges u->v; canonical form is
+ *    required — in_row_ptr[0] = 0, in_row_ptr[n] = m, non-decreasing; each row strictly
+ *    ascending, every u < n, no u == v (reading R15). Violations: GIM_EINVAL.
+ *  weights[m] (float32 in [0,1], slot-aligned with in_src) is required iff scheme ==
+ *    GIM_W_EXPLICIT, else ignored. GIM_W_WC: p_uv = 1/d_in(v) (weighted cascade).
+ *    GIM_W_UNIFORM: p_uv = p_uniform in [0,1] (IC only).
+ *  model GIM_LT requires GIM_W_WC or GIM_W_EXPLICIT with sum_u w_uv <= 1 at every v
+ *    (P:125), else GIM_ELTWEIGHT (or GIM_EINVAL for LT + uniform, reading R23).
+ *  Limits: 1 <= n < 2^32 - 1, m < 2^32 (row pointers are held as uint32 on the device).
+ * Replaces any previous graph and clears the RR pool. */
+gim_status gim_load_graph(gim_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* in_row_ptr,
+                          const uint32_t* in_src, const float* weights, gim_model model,
+                          gim_weights scheme, float p_uniform);
+
+/* Data-parallel sharding of RR ids (default rank 0 of 1). For any id range [a, b) this rank
+ * generates and holds the contiguous slice [a + r(b-a)/P, a + (r+1)(b-a)/P) (integer floor).
+ * Must be called before gim_generate_rr / gim_imm; clears the pool. GIM_EINVAL unless
+ * 0 <= rank < world. */
+gim_status gim_set_shard(gim_ctx* ctx, int rank, int world);
+
+/* In-place SUM all-reduce over the world of int32 (two's complement) elements living in device
+ * memory on the ctx device, enqueued on / ordered with cuda_stream. Returns 0 on success. Used
+ * by gim_select when world > 1 (the count vector once, then one decrement
+ * vector per greedy step). Required before gim_select/gim_imm when world > 1. */
+typedef int (*gim_allreduce_fn)(void* dev_buf, uint64_t count, void* cuda_stream, void* user);
+gim_status gim_set_allreduce(gim_ctx* ctx, gim_allreduce_fn fn, void* user);
+
+/* Route every device allocation of ctx through the caller (e.g. torch's caching allocator).
+ * Must be called before gim_load_graph. alloc_fn returns NULL on failure. */
+typedef void* (*gim_alloc_fn)(uint64_t bytes, void* cuda_stream, void* user);
+typedef void (*gim_free_fn)(void* ptr, void* cuda_stream, void* user);
+gim_status gim_set_allocator(gim_ctx* ctx, gim_alloc_fn alloc_fn, gim_free_fn free_fn,
+                             void* user);
+
+/* RR-set sampling (Alg. 1 l.3-4; Alg. 3/6). Afterwards the global pool is exactly
+ * { RR(seed, i) : 0 <= i < theta } (reading R20), this rank holding its slices. Same seed and a
+ * larger theta extends the pool (Alg. 2 reuses sets, reading R8); a smaller theta truncates;
+ * a different seed discards and regenerates. RR(seed, i): root = floor(u64 * n / 2^64) with
+ * u64 from Philox slot 2^63 (R17); IC keeps in-edge slot e iff coin(i, e) * 2^-32 < p_e where
+ * coin = word (e & 3) of Philox slot (e >> 2) (R16); LT walks one in-edge per node chosen by
+ * Philox slot 2^62 | v (R18-R19). Also maintains count[v] = #{local i : v in RR_i}
+ * (Occur). Errors: GIM_ESTATE (no graph), GIM_ENOMEM, GIM_ECUDA. */
+gim_status gim_generate_rr(gim_ctx* ctx, uint64_t theta, uint64_t seed);
+
+/* Greedy max coverage over the current (global) pool, non-destructive (reading R9): k steps of
+ * u_j = argmax_{v not in S} count[v] (ties -> lowest id, zero maximum allowed: R10), then
+ * every uncovered RR set containing u_j is covered and count[w] -= 1 for each member (Alg. 7,
+ * P:541-561; R11). seeds_out[k] required; gains_out[k] (marginal coverage) and covered_out
+ * (sum of gains = |{i : S cap RR_i != {}}|) may be NULL. Errors: GIM_EINVAL (k < 1 or k > n),
+ * GIM_ESTATE (empty pool / missing all-reduce), GIM_ECOLL, GIM_ECUDA. */
+gim_status gim_select(gim_ctx* ctx, uint32_t k, uint32_t* seeds_out, uint64_t* gains_out,
+                      uint64_t* covered_out);
+
+/* IMM result / trace (reading R1-R8, R21). theta_i[r] are the round targets ceil(theta_i)
+ * actually sampled, cov_i[r] the covered count of round r's selection. */
+typedef struct {
+  double ell_eff, eps_prime, lambda_prime, lambda_star, LB, theta;
+  uint32_t rounds;
+  uint64_t theta_i[64], cov_i[64];
+  double theta_i_real[64];
+  uint64_t R_final;
+  uint64_t covered;
+  double spread_est;   /* n * covered / R_final (Eq. 3) */
+} gim_imm_result;
+
+/* Full IMM (Alg. 2 bootstrap of LB, then theta = lambda_star / LB and the final NodeSelection):
+ * starts from an empty pool. seeds_out[k] required; res may be NULL. GIM_EINVAL unless n >= 2,
+ * 1 <= k <= n, 0 < eps < 1, ell > 0 (reading R25). */
+gim_status gim_imm(gim_ctx* ctx, uint32_t k, double eps, double ell, uint64_t seed,
+                   uint32_t* seeds_out, gim_imm_result* res);
+
+/* Parity/debug export of this rank's local slice (caller-allocated; pass NULL buffers to query
+ * n_sets / pool_len only). ids_out[n_sets]: global RR id of each local set; offsets_out
+ * [n_sets+1]: local offsets into nodes_out[pool_len]. sort_each_set != 0 sorts every set
+ * ascending (the device stores sets in discovery order, which is not part of the contract). */
+gim_status gim_rr_export(gim_ctx* ctx, uint64_t* n_sets, uint64_t* pool_len, uint64_t* ids_out,
+                         uint64_t* offsets_out, uint32_t* nodes_out, int sort_each_set);
+
+/* count_out[n]: this rank's local occurrence counts (Occur). */
+gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
+
+/* Tunables (test / ablation hooks; the defaults are the tuned configuration):
+ *  GIM_OPT_FORCE_GIANT  = 1: every RR set goes through the block-per-RR giant kernel.
+ *  GIM_OPT_QUEUE_CAP    = Q: shared-memory queue capacity per RR (power of two, 32..1024);
+ *                          sets larger than Q are replayed by the giant kernel.
+ *  GIM_OPT_PROFILE      = 1: time every kernel class with CUDA events (see gim_get_stats).
+ *  GIM_OPT_STAGING_CAP  = elements of staging memory to start from (forces retries if tiny). */
+typedef enum {
+  GIM_OPT_FORCE_GIANT = 1,
+  GIM_OPT_QUEUE_CAP = 2,
+  GIM_OPT_PROFILE = 3,
+  GIM_OPT_STAGING_CAP = 4
+} gim_option;
+gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
+
+/* Counters since the last gim_reset_stats. Kernel times (ms, CUDA events on the ctx stream)
+ * are only collected with GIM_OPT_PROFILE = 1. */
+typedef struct {
+  uint64_t launches;          /* kernels launched by the library                      */
+  uint64_t rr_sets;           /* RR sets generated (local)                             */
+  uint64_t rr_elements;       /* pool elements appended (local)                        */
+  uint64_t giant_sets;        /* sets replayed by the giant kernel                     */
+  uint64_t coins;             /* in-edge slots examined (IC) / draws (LT), warp kernel */
+  uint64_t live_edges;        /* live in-edges found, warp kernel                      */
+  uint64_t coins_giant;       /* same, giant kernel                                    */
+  uint64_t live_giant;
+  uint64_t selects;           /* NodeSelection calls                                   */
+  uint64_t allreduces;        /* all-reduce callback invocations                       */
+  double ms_rr, ms_giant, ms_store, ms_inv, ms_select; /* kernel time per class        */
+  uint64_t n_rr_launches, n_giant_launches;
+} gim_stats;
+gim_status gim_get_stats(gim_ctx* ctx, gim_stats* out);
+gim_status gim_reset_stats(gim_ctx* ctx);
+
+/* Diagnostic: time `groups` Philox4x32-10 slot-group evaluations (4 coins each, the per-group
+ * ALU work of the IC kernel without memory traffic) on the ctx stream; *ms = kernel time. Used
+ * to check the ALU roofline of the sampling kernel. */
+gim_status gim_microbench_philox(gim_ctx* ctx, uint64_t groups, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GIM_H_ */

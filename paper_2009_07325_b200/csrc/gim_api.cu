@@ -1,0 +1,821 @@
+// gim_api.cu — C-ABI entry points, device memory management and the host IMM driver of
+// libgim (declared in include/gim.h). Host code is compiled with -ffp-contract=off so that the
+// IMM doubles follow the evaluation order fixed in DESIGN.md (reading R21).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gim.h"
+#include "gim_device.cuh"
+#include "gim_internal.h"
+
+using namespace gim;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  uint64_t bytes = 0;
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct Seg {
+  uint64_t gstart, lstart, count;   // global id range [gstart, gstart+count) at local index lstart
+};
+
+enum { CLS_RR = 0, CLS_GIANT, CLS_STORE, CLS_INV, CLS_SELECT, CLS_N };
+
+constexpr uint32_t kChunk = 1u << 22;   // RR ids per generation chunk (bounds staging)
+
+}  // namespace
+
+struct gim_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  std::string err;
+  gim_alloc_fn afn = nullptr;
+  gim_free_fn ffn = nullptr;
+  void* auser = nullptr;
+  // graph (O1)
+  bool graph = false;
+  uint32_t n = 0;
+  uint64_t m = 0;
+  int model = 0, scheme = 0;
+  float p_uniform = 0.f;
+  uint64_t thr_uniform = 0;
+  DevBuf row_ptr, src, thr_edge;
+  // sharding
+  int rank = 0, world = 1;
+  gim_allreduce_fn arfn = nullptr;
+  void* aruser = nullptr;
+  // pool (O6)
+  bool have_seed = false;
+  uint64_t seed = 0, T_global = 0, nsets = 0, pool_len = 0;
+  std::vector<Seg> segs;
+  DevBuf pool, offsets, count_total;
+  // generation scratch
+  DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr;
+  DevBuf bitmaps, gqueues;
+  uint32_t giant_slots = 0;
+  uint64_t stage_cap = 0;
+  GenCounters* h_ctr = nullptr;   // pinned
+  uint64_t* h_u64 = nullptr;      // pinned scratch
+  // selection scratch
+  DevBuf cnt, inv_off, cursor, inv, covered, keys, dec;
+  // options
+  int force_giant = 0, profile = 0;
+  uint32_t qcap = kQMax;
+  uint64_t staging_init = 0;
+  gim_stats st{};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[CLS_N];
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+gim_status fail(gim_ctx* c, gim_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+gim_status fail_cuda(gim_ctx* c, const char* what, cudaError_t e) {
+  cudaGetLastError();
+  return fail(c, GIM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return fail_cuda(c, #call, _e); \
+  } while (0)
+#define TRY(call)                      \
+  do {                                 \
+    gim_status _s = (call);            \
+    if (_s != GIM_OK) return _s;       \
+  } while (0)
+
+void dfree(gim_ctx* c, DevBuf& b) {
+  if (b.p) {
+    if (c->ffn) c->ffn(b.p, c->stream, c->auser);
+    else cudaFreeAsync(b.p, c->stream);
+  }
+  b = DevBuf{};
+}
+
+gim_status dalloc(gim_ctx* c, DevBuf& b, uint64_t bytes) {
+  dfree(c, b);
+  bytes = std::max<uint64_t>((bytes + 255) & ~uint64_t(255), 256);
+  void* p = nullptr;
+  if (c->afn) {
+    p = c->afn(bytes, c->stream, c->auser);
+    if (!p) return fail(c, GIM_ENOMEM, "allocator callback failed for " + std::to_string(bytes) + " bytes");
+  } else {
+    cudaError_t e = cudaMallocAsync(&p, bytes, c->stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, GIM_ENOMEM, "cudaMallocAsync(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    }
+  }
+  b.p = p;
+  b.bytes = bytes;
+  return GIM_OK;
+}
+
+// Capacity >= bytes; contents are NOT preserved.
+gim_status ensure(gim_ctx* c, DevBuf& b, uint64_t bytes) {
+  if (b.bytes >= bytes && b.p) return GIM_OK;
+  return dalloc(c, b, std::max<uint64_t>(bytes, b.bytes + b.bytes / 2));
+}
+
+// Capacity >= bytes; the first `keep` bytes are preserved.
+gim_status grow_keep(gim_ctx* c, DevBuf& b, uint64_t bytes, uint64_t keep) {
+  if (b.bytes >= bytes && b.p) return GIM_OK;
+  DevBuf nb;
+  TRY(dalloc(c, nb, std::max<uint64_t>(bytes, b.bytes * 2)));
+  if (keep && b.p) CK(cudaMemcpyAsync(nb.p, b.p, keep, cudaMemcpyDeviceToDevice, c->stream));
+  dfree(c, b);
+  b = nb;
+  return GIM_OK;
+}
+
+// ---- profiling (CUDA events on the ctx stream, resolved at sync points) ----------------------
+struct Prof {
+  gim_ctx* c;
+  int cls;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Prof(gim_ctx* c_, int cls_) : c(c_), cls(cls_) {
+    if (c->profile) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~Prof() {
+    if (a) {
+      cudaEventRecord(b, c->stream);
+      c->ev[cls].emplace_back(a, b);
+    }
+  }
+};
+
+gim_status sync(gim_ctx* c) {
+  CK(cudaStreamSynchronize(c->stream));
+  double* acc[CLS_N] = {&c->st.ms_rr, &c->st.ms_giant, &c->st.ms_store, &c->st.ms_inv, &c->st.ms_select};
+  for (int k = 0; k < CLS_N; ++k) {
+    for (auto& pr : c->ev[k]) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) *acc[k] += ms;
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    c->ev[k].clear();
+  }
+  cudaGetLastError();
+  return GIM_OK;
+}
+
+gim_status launched(gim_ctx* c, cudaError_t e, const char* what, int n = 1) {
+  c->st.launches += n;
+  if (e != cudaSuccess) return fail_cuda(c, what, e);
+  return GIM_OK;
+}
+
+// ---- pool management ------------------------------------------------------------------------
+gim_status reset_pool(gim_ctx* c, uint64_t seed) {
+  c->have_seed = true;
+  c->seed = seed;
+  c->T_global = 0;
+  c->nsets = 0;
+  c->pool_len = 0;
+  c->segs.clear();
+  TRY(ensure(c, c->count_total, (uint64_t)c->n * 4));
+  CK(cudaMemsetAsync(c->count_total.p, 0, (uint64_t)c->n * 4, c->stream));
+  TRY(ensure(c, c->offsets, 8 * 1024));
+  CK(cudaMemsetAsync(c->offsets.p, 0, 8, c->stream));
+  return GIM_OK;
+}
+
+gim_status ensure_giant_slots(gim_ctx* c, uint32_t want) {
+  const uint64_t words = ((uint64_t)c->n + 31) / 32;
+  const uint64_t per_slot = words * 4 + (uint64_t)c->n * 4;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  uint64_t cap = std::max<uint64_t>(1, (uint64_t)(free_b / 8) / std::max<uint64_t>(per_slot, 1));
+  uint32_t slots = (uint32_t)std::min<uint64_t>({(uint64_t)want, (uint64_t)2 * c->num_sms, cap});
+  if (slots <= c->giant_slots) return GIM_OK;
+  TRY(dalloc(c, c->bitmaps, words * 4 * slots));
+  CK(cudaMemsetAsync(c->bitmaps.p, 0, words * 4 * slots, c->stream));
+  TRY(dalloc(c, c->gqueues, (uint64_t)c->n * 4 * slots));
+  c->giant_slots = slots;
+  return GIM_OK;
+}
+
+RRParams base_params(gim_ctx* c) {
+  RRParams p{};
+  p.n = c->n;
+  p.row_ptr = c->row_ptr.as<uint32_t>();
+  p.src = c->src.as<uint32_t>();
+  p.thr_edge = c->thr_edge.as<uint64_t>();
+  p.thr_uniform = c->thr_uniform;
+  p.seed = c->seed;
+  p.sizes = c->sizes.as<uint32_t>();
+  p.soff = c->soff.as<uint64_t>();
+  p.staging = c->staging.as<uint32_t>();
+  p.stage_cap = c->stage_cap;
+  p.ctr = c->ctr.as<GenCounters>();
+  p.giant_list = c->giant_list.as<uint32_t>();
+  p.retry_list = c->retry_list.as<uint32_t>();
+  p.qcap = c->qcap;
+  p.force_giant = c->force_giant;
+  return p;
+}
+
+gim_status read_ctr(gim_ctx* c) {
+  CK(cudaMemcpyAsync(c->h_ctr, c->ctr.p, sizeof(GenCounters), cudaMemcpyDeviceToHost, c->stream));
+  return sync(c);
+}
+
+// Generate local RR sets for global ids [gstart, gstart + cnt) and append them to the pool.
+gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
+  TRY(ensure(c, c->sizes, (uint64_t)cnt * 4));
+  TRY(ensure(c, c->soff, (uint64_t)cnt * 8));
+  TRY(ensure(c, c->giant_list, (uint64_t)cnt * 4));
+  TRY(ensure(c, c->retry_list, (uint64_t)cnt * 4));
+  TRY(ensure(c, c->item_list, (uint64_t)cnt * 4));
+  TRY(ensure(c, c->scan_out, ((uint64_t)cnt + 1) * 8));
+  TRY(ensure(c, c->scan_tmp, (scan_tiles(cnt) + 2) * 8));
+  TRY(ensure(c, c->ctr, sizeof(GenCounters)));
+  if (c->stage_cap == 0 && c->staging_init) {
+    TRY(dalloc(c, c->staging, c->staging_init * 4));
+    c->stage_cap = c->staging_init;
+  } else {
+    const double mean = c->nsets ? (double)c->pool_len / (double)c->nsets : 32.0;
+    const uint64_t want = (uint64_t)(mean * (double)cnt * 1.25) + (1u << 20);
+    if (c->stage_cap < want && !c->staging_init) {
+      TRY(dalloc(c, c->staging, want * 4));
+      c->stage_cap = c->staging.bytes / 4;
+    }
+  }
+  CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(GenCounters), c->stream));
+  RRParams p = base_params(c);
+  p.id_base = gstart;
+  p.count = cnt;
+  p.item_list = nullptr;
+  const int rr_grid = c->num_sms * 4;   // 4 CTAs x 8 warps per SM (smem-limited)
+  {
+    Prof pf(c, CLS_RR);
+    TRY(launched(c, launch_rr_warp(c->model, c->scheme, p, rr_grid, c->stream), "k_rr_warp"));
+    c->st.n_rr_launches++;
+  }
+  TRY(read_ctr(c));
+  for (int iter = 0;; ++iter) {
+    const uint32_t giants = c->h_ctr->giant_count;
+    if (giants) {
+      TRY(ensure_giant_slots(c, giants));
+      {
+        Prof pf(c, CLS_GIANT);
+        TRY(launched(c, launch_rr_giant(c->model, c->scheme, p, (int)std::min(giants, c->giant_slots),
+                                        c->bitmaps.as<uint32_t>(), c->gqueues.as<uint32_t>(),
+                                        ((uint64_t)c->n + 31) / 32, c->stream), "k_rr_giant"));
+        c->st.n_giant_launches++;
+      }
+      c->st.giant_sets += giants;
+      TRY(read_ctr(c));
+    }
+    const uint32_t retries = c->h_ctr->retry_count;
+    if (!retries) break;
+    if (iter > 40) return fail(c, GIM_ENOMEM, "staging retry loop did not converge");
+    // staging overflow: grow (keep the part already written) and replay the failed items
+    const uint64_t old_cap = c->stage_cap;
+    TRY(grow_keep(c, c->staging, old_cap * 4 * 2, old_cap * 4));
+    c->stage_cap = c->staging.bytes / 4;
+    CK(cudaMemcpyAsync(c->item_list.p, c->retry_list.p, (uint64_t)retries * 4, cudaMemcpyDeviceToDevice, c->stream));
+    GenCounters h = *c->h_ctr;
+    h.stage_tail = old_cap;
+    h.claim = h.claim_giant = h.giant_count = h.retry_count = 0;
+    *c->h_ctr = h;
+    CK(cudaMemcpyAsync(c->ctr.p, c->h_ctr, sizeof(GenCounters), cudaMemcpyHostToDevice, c->stream));
+    p = base_params(c);
+    p.id_base = gstart;
+    p.count = retries;
+    p.item_list = c->item_list.as<uint32_t>();
+    {
+      Prof pf(c, CLS_RR);
+      TRY(launched(c, launch_rr_warp(c->model, c->scheme, p, rr_grid, c->stream), "k_rr_warp(retry)"));
+      c->st.n_rr_launches++;
+    }
+    TRY(read_ctr(c));
+  }
+  c->st.coins += c->h_ctr->coins;
+  c->st.live_edges += c->h_ctr->live;
+  c->st.coins_giant += c->h_ctr->coins_giant;
+  c->st.live_giant += c->h_ctr->live_giant;
+  // two-pass storage: exclusive scan of sizes, then compacting copy + count_total
+  {
+    Prof pf(c, CLS_STORE);
+    int nl = 0;
+    cudaError_t e = launch_scan_u32(c->sizes.as<uint32_t>(), cnt, c->scan_out.as<uint64_t>(),
+                                    c->scan_tmp.as<uint64_t>(), c->scan_tmp.as<uint64_t>() + scan_tiles(cnt) + 1,
+                                    c->stream, &nl);
+    TRY(launched(c, e, "scan(sizes)", nl));
+  }
+  CK(cudaMemcpyAsync(c->h_u64, c->scan_out.as<uint64_t>() + cnt, 8, cudaMemcpyDeviceToHost, c->stream));
+  TRY(sync(c));
+  const uint64_t total = c->h_u64[0];
+  TRY(grow_keep(c, c->pool, (c->pool_len + total) * 4, c->pool_len * 4));
+  TRY(grow_keep(c, c->offsets, (c->nsets + cnt + 1) * 8, (c->nsets + 1) * 8));
+  {
+    Prof pf(c, CLS_STORE);
+    TRY(launched(c, launch_store(c->staging.as<uint32_t>(), c->sizes.as<uint32_t>(), c->soff.as<uint64_t>(),
+                                 c->scan_out.as<uint64_t>(), cnt, c->pool_len, c->pool.as<uint32_t>(),
+                                 c->offsets.as<uint64_t>() + c->nsets, c->count_total.as<uint32_t>(),
+                                 c->num_sms * 8, c->stream), "k_store"));
+  }
+  c->segs.push_back(Seg{gstart, c->nsets, cnt});
+  c->nsets += cnt;
+  c->pool_len += total;
+  c->st.rr_sets += cnt;
+  c->st.rr_elements += total;
+  return GIM_OK;
+}
+
+gim_status truncate_pool(gim_ctx* c, uint64_t theta) {
+  uint64_t keep_sets = 0;
+  std::vector<Seg> kept;
+  for (const Seg& s : c->segs) {
+    if (s.gstart >= theta) break;
+    const uint64_t k = std::min<uint64_t>(s.count, theta - s.gstart);
+    kept.push_back(Seg{s.gstart, s.lstart, k});
+    keep_sets = s.lstart + k;
+    if (k < s.count) break;
+  }
+  CK(cudaMemcpyAsync(c->h_u64, c->offsets.as<uint64_t>() + keep_sets, 8, cudaMemcpyDeviceToHost, c->stream));
+  TRY(sync(c));
+  const uint64_t e0 = c->h_u64[0];
+  if (c->pool_len > e0)
+    TRY(launched(c, launch_count_sub(c->pool.as<uint32_t>(), e0, c->pool_len, c->count_total.as<uint32_t>(),
+                                     c->num_sms * 8, c->stream), "k_count_sub"));
+  c->segs = kept;
+  c->nsets = keep_sets;
+  c->pool_len = e0;
+  c->T_global = theta;
+  return GIM_OK;
+}
+
+gim_status generate(gim_ctx* c, uint64_t theta, uint64_t seed) {
+  if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
+  if (theta >= (1ull << 32)) return fail(c, GIM_EINVAL, "theta must be < 2^32");
+  if (!c->have_seed || c->seed != seed) TRY(reset_pool(c, seed));
+  if (theta < c->T_global) {
+    TRY(truncate_pool(c, theta));
+  } else if (theta > c->T_global) {
+    const uint64_t a = c->T_global, len = theta - a;
+    const uint64_t lo = a + (uint64_t)((unsigned __int128)len * c->rank / c->world);
+    const uint64_t hi = a + (uint64_t)((unsigned __int128)len * (c->rank + 1) / c->world);
+    for (uint64_t s = lo; s < hi; s += kChunk) TRY(gen_chunk(c, s, (uint32_t)std::min<uint64_t>(kChunk, hi - s)));
+    c->T_global = theta;
+  }
+  return sync(c);
+}
+
+// ---- NodeSelection (O7) ---------------------------------------------------------------------
+gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains, uint64_t* covered) {
+  if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
+  if (k < 1 || k > c->n) return fail(c, GIM_EINVAL, "k must satisfy 1 <= k <= n");
+  if (!c->have_seed || c->T_global == 0) return fail(c, GIM_ESTATE, "RR pool is empty");
+  if (c->world > 1 && !c->arfn) return fail(c, GIM_ESTATE, "world > 1 requires gim_set_allreduce");
+  const uint64_t n = c->n;
+  TRY(ensure(c, c->cnt, n * 4));
+  TRY(ensure(c, c->inv_off, (n + 1) * 8));
+  TRY(ensure(c, c->cursor, n * 4));
+  TRY(ensure(c, c->inv, std::max<uint64_t>(c->pool_len, 1) * 4));
+  TRY(ensure(c, c->covered, std::max<uint64_t>(c->nsets, 1)));
+  TRY(ensure(c, c->keys, (uint64_t)k * 8));
+  TRY(ensure(c, c->scan_tmp, (scan_tiles(n) + 2) * 8));
+  if (c->world > 1) TRY(ensure(c, c->dec, n * 4));
+  int32_t* dec = c->world > 1 ? c->dec.as<int32_t>() : nullptr;
+  {
+    Prof pf(c, CLS_INV);
+    int nl = 0;
+    cudaError_t e = launch_scan_u32(c->count_total.as<uint32_t>(), n, c->inv_off.as<uint64_t>(),
+                                    c->scan_tmp.as<uint64_t>(), c->scan_tmp.as<uint64_t>() + scan_tiles(n) + 1,
+                                    c->stream, &nl);
+    TRY(launched(c, e, "scan(count_total)", nl));
+    CK(cudaMemsetAsync(c->cursor.p, 0, n * 4, c->stream));
+    if (c->nsets)
+      TRY(launched(c, launch_inv_scatter(c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), (uint32_t)c->nsets,
+                                         c->inv_off.as<uint64_t>(), c->cursor.as<uint32_t>(), c->inv.as<uint32_t>(),
+                                         c->num_sms * 8, c->stream), "k_inv_scatter"));
+  }
+  CK(cudaMemcpyAsync(c->cnt.p, c->count_total.p, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemsetAsync(c->covered.p, 0, std::max<uint64_t>(c->nsets, 1), c->stream));
+  CK(cudaMemsetAsync(c->keys.p, 0, (uint64_t)k * 8, c->stream));
+  if (dec) {
+    CK(cudaMemsetAsync(dec, 0, n * 4, c->stream));
+    c->st.allreduces++;
+    if (c->arfn(c->cnt.p, n, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(count) failed");
+  }
+  auto* keys = reinterpret_cast<unsigned long long*>(c->keys.p);
+  for (uint32_t j = 0; j < k; ++j) {
+    {
+      Prof pf(c, CLS_SELECT);
+      TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, c->n, keys, (int)j, c->num_sms * 4, c->stream),
+                   "k_argmax"));
+      TRY(launched(c, launch_cover(keys, (int)j, c->inv_off.as<uint64_t>(), c->inv.as<uint32_t>(),
+                                   c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), c->covered.as<uint8_t>(),
+                                   c->cnt.as<uint32_t>(), dec, c->num_sms * 8, c->stream), "k_cover"));
+    }
+    if (dec && j + 1 < k) {
+      c->st.allreduces++;
+      if (c->arfn(dec, n, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(dec) failed");
+    }
+  }
+  std::vector<unsigned long long> hk(k);
+  CK(cudaMemcpyAsync(hk.data(), keys, (uint64_t)k * 8, cudaMemcpyDeviceToHost, c->stream));
+  TRY(sync(c));
+  uint64_t cov = 0;
+  for (uint32_t j = 0; j < k; ++j) {
+    seeds[j] = ~(uint32_t)(hk[j] & 0xFFFFFFFFull);
+    const uint64_t g = hk[j] >> 32;
+    if (gains) gains[j] = g;
+    cov += g;
+  }
+  if (covered) *covered = cov;
+  c->st.selects++;
+  return GIM_OK;
+}
+
+// ---- IMM constants (O8; readings R1-R3, R21) -----------------------------------------------
+struct ImmConst {
+  double ell_eff, eps_p, lnC, lambda_p, alpha, beta, lambda_s;
+};
+
+ImmConst imm_constants(uint32_t n_, uint32_t k, double eps, double ell) {
+  ImmConst K;
+  const double n = (double)n_;
+  const double ln_n = std::log(n);
+  const double log2n = std::log2(n);
+  K.ell_eff = ell * (1.0 + std::log(2.0) / ln_n);
+  K.eps_p = std::sqrt(2.0) * eps;
+  K.lnC = 0.0;
+  for (uint32_t t = 1; t <= k; ++t) K.lnC += std::log((double)(n_ - k + t)) - std::log((double)t);
+  K.lambda_p = (2.0 + 2.0 / 3.0 * K.eps_p) * (K.lnC + K.ell_eff * ln_n + std::log(log2n)) * n / (K.eps_p * K.eps_p);
+  K.alpha = std::sqrt(K.ell_eff * ln_n + std::log(2.0));
+  K.beta = std::sqrt((1.0 - 1.0 / M_E) * (K.lnC + K.ell_eff * ln_n + std::log(2.0)));
+  const double s = (1.0 - 1.0 / M_E) * K.alpha + K.beta;
+  K.lambda_s = 2.0 * n * (s * s) / (eps * eps);
+  return K;
+}
+
+}  // namespace
+
+// =============================================================================================
+// C ABI
+// =============================================================================================
+extern "C" {
+
+gim_status gim_create(int device, void* cuda_stream, gim_ctx** out) {
+  if (!out) return GIM_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return GIM_ECUDA;
+  }
+  if (device < 0 || device >= ndev) return GIM_ECUDA;
+  DeviceGuard g(device);
+  gim_ctx* c = new gim_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cuda_stream) {
+    c->stream = static_cast<cudaStream_t>(cuda_stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      return GIM_ECUDA;
+    }
+    c->own_stream = true;
+  }
+  cudaMemPool_t mp;
+  if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (cudaMallocHost(&c->h_ctr, sizeof(GenCounters)) != cudaSuccess ||
+      cudaMallocHost(&c->h_u64, 64) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return GIM_ECUDA;
+  }
+  *out = c;
+  return GIM_OK;
+}
+
+void gim_destroy(gim_ctx* c) {
+  if (!c) return;
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->stream);
+  DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
+                    &c->sizes, &c->soff, &c->giant_list, &c->retry_list, &c->item_list, &c->scan_out,
+                    &c->scan_tmp, &c->staging, &c->ctr, &c->bitmaps, &c->gqueues, &c->cnt, &c->inv_off,
+                    &c->cursor, &c->inv, &c->covered, &c->keys, &c->dec};
+  for (DevBuf* b : bufs) dfree(c, *b);
+  cudaStreamSynchronize(c->stream);
+  for (auto& v : c->ev)
+    for (auto& pr : v) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+  if (c->h_ctr) cudaFreeHost(c->h_ctr);
+  if (c->h_u64) cudaFreeHost(c->h_u64);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  cudaGetLastError();
+  delete c;
+}
+
+const char* gim_last_error(const gim_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+gim_status gim_set_allocator(gim_ctx* c, gim_alloc_fn a, gim_free_fn f, void* user) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  if (c->graph) return fail(c, GIM_ESTATE, "gim_set_allocator must precede gim_load_graph");
+  if ((a == nullptr) != (f == nullptr)) return fail(c, GIM_EINVAL, "alloc and free must both be set");
+  c->afn = a;
+  c->ffn = f;
+  c->auser = user;
+  return GIM_OK;
+}
+
+gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp, const uint32_t* src,
+                          const float* w, gim_model model, gim_weights scheme, float p_uniform) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  DeviceGuard g(c->device);
+  if (n < 1 || n == 0xFFFFFFFFu) return fail(c, GIM_EINVAL, "n must be in [1, 2^32-2]");
+  if (m >= 0xFFFFFFF0ull) return fail(c, GIM_EINVAL, "m must be < 2^32 - 16");
+  if (!rp || (m && !src)) return fail(c, GIM_EINVAL, "row_ptr/src missing");
+  if (model != GIM_IC && model != GIM_LT) return fail(c, GIM_EINVAL, "bad model");
+  if (scheme != GIM_W_EXPLICIT && scheme != GIM_W_WC && scheme != GIM_W_UNIFORM) return fail(c, GIM_EINVAL, "bad scheme");
+  if (scheme == GIM_W_EXPLICIT && m && !w) return fail(c, GIM_EINVAL, "explicit weights required");
+  if (model == GIM_LT && scheme == GIM_W_UNIFORM) return fail(c, GIM_EINVAL, "LT with uniform p is not supported (reading R23)");
+  if (scheme == GIM_W_UNIFORM && !(p_uniform >= 0.f && p_uniform <= 1.f)) return fail(c, GIM_EINVAL, "p_uniform must be in [0,1]");
+  // canonical in-CSR validation (reading R15)
+  if (rp[0] != 0 || rp[n] != m) return fail(c, GIM_EINVAL, "row_ptr[0] must be 0 and row_ptr[n] must be m");
+  std::vector<uint32_t> rp32(n + 1);
+  for (uint32_t v = 0; v < n; ++v) {
+    if (rp[v + 1] < rp[v]) return fail(c, GIM_EINVAL, "row_ptr must be non-decreasing");
+    rp32[v] = (uint32_t)rp[v];
+    for (uint64_t e = rp[v]; e < rp[v + 1]; ++e) {
+      const uint32_t u = src[e];
+      if (u >= n) return fail(c, GIM_EINVAL, "src out of range");
+      if (u == v) return fail(c, GIM_EINVAL, "self-loop in row " + std::to_string(v));
+      if (e > rp[v] && src[e - 1] >= u) return fail(c, GIM_EINVAL, "row " + std::to_string(v) + " not strictly ascending");
+    }
+  }
+  rp32[n] = (uint32_t)m;
+  std::vector<uint64_t> thr;
+  if (scheme == GIM_W_EXPLICIT) {
+    thr.resize(std::max<uint64_t>(m, 1));
+    for (uint32_t v = 0; v < n; ++v) {
+      uint64_t acc = 0;
+      for (uint64_t e = rp[v]; e < rp[v + 1]; ++e) {
+        const float x = w[e];
+        if (!(x >= 0.f && x <= 1.f)) return fail(c, GIM_EINVAL, "weights must be in [0,1]");
+        const double t = (double)x * 4294967296.0;   // exact for float32
+        thr[e] = (model == GIM_LT) ? (uint64_t)std::floor(t) : (uint64_t)std::ceil(t);
+        acc += thr[e];
+      }
+      if (model == GIM_LT && acc > 4294967296ull)
+        return fail(c, GIM_ELTWEIGHT, "LT in-weights of node " + std::to_string(v) + " sum above 1");
+    }
+  }
+  // release the previous graph and pool
+  dfree(c, c->row_ptr);
+  dfree(c, c->src);
+  dfree(c, c->thr_edge);
+  dfree(c, c->bitmaps);
+  dfree(c, c->gqueues);
+  c->giant_slots = 0;
+  c->graph = false;
+  c->n = n;
+  c->m = m;
+  c->model = model;
+  c->scheme = scheme;
+  c->p_uniform = p_uniform;
+  c->thr_uniform = (uint64_t)std::ceil((double)p_uniform * 4294967296.0);
+  TRY(dalloc(c, c->row_ptr, ((uint64_t)n + 1) * 4));
+  TRY(dalloc(c, c->src, std::max<uint64_t>(m, 1) * 4));
+  CK(cudaMemcpyAsync(c->row_ptr.p, rp32.data(), ((uint64_t)n + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+  if (m) CK(cudaMemcpyAsync(c->src.p, src, m * 4, cudaMemcpyHostToDevice, c->stream));
+  if (scheme == GIM_W_EXPLICIT) {
+    TRY(dalloc(c, c->thr_edge, thr.size() * 8));
+    CK(cudaMemcpyAsync(c->thr_edge.p, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, c->stream));
+  }
+  c->graph = true;
+  c->have_seed = false;
+  TRY(reset_pool(c, 0));
+  c->have_seed = false;
+  return sync(c);
+}
+
+gim_status gim_set_shard(gim_ctx* c, int rank, int world) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  if (world < 1 || rank < 0 || rank >= world) return fail(c, GIM_EINVAL, "need 0 <= rank < world");
+  c->rank = rank;
+  c->world = world;
+  c->have_seed = false;
+  c->T_global = c->nsets = c->pool_len = 0;
+  c->segs.clear();
+  return GIM_OK;
+}
+
+gim_status gim_set_allreduce(gim_ctx* c, gim_allreduce_fn fn, void* user) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  c->arfn = fn;
+  c->aruser = user;
+  return GIM_OK;
+}
+
+gim_status gim_generate_rr(gim_ctx* c, uint64_t theta, uint64_t seed) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  DeviceGuard g(c->device);
+  return generate(c, theta, seed);
+}
+
+gim_status gim_select(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains, uint64_t* covered) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  if (!seeds) return fail(c, GIM_EINVAL, "seeds_out required");
+  DeviceGuard g(c->device);
+  return select_impl(c, k, seeds, gains, covered);
+}
+
+gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed, uint32_t* seeds,
+                   gim_imm_result* res) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  if (!seeds) return fail(c, GIM_EINVAL, "seeds_out required");
+  if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
+  if (c->n < 2) return fail(c, GIM_EINVAL, "IMM needs n >= 2 (reading R25)");
+  if (k < 1 || k > c->n) return fail(c, GIM_EINVAL, "k must satisfy 1 <= k <= n");
+  if (!(eps > 0.0 && eps < 1.0)) return fail(c, GIM_EINVAL, "eps must be in (0,1)");
+  if (!(ell > 0.0)) return fail(c, GIM_EINVAL, "ell must be > 0");
+  DeviceGuard g(c->device);
+  const ImmConst K = imm_constants(c->n, k, eps, ell);
+  gim_imm_result r;
+  std::memset(&r, 0, sizeof(r));
+  r.ell_eff = K.ell_eff;
+  r.eps_prime = K.eps_p;
+  r.lambda_prime = K.lambda_p;
+  r.lambda_star = K.lambda_s;
+  const double n = (double)c->n;
+  c->have_seed = false;                                      // IMM starts from R = {}
+  TRY(generate(c, 0, seed));
+  double LB = 1.0;                                           // reading R6
+  uint64_t cov = 0;
+  std::vector<uint32_t> tmp(k);
+  const int i_max = (int)std::floor(std::log2(n)) - 1;       // reading R5
+  for (int i = 1; i <= i_max && i <= 64; ++i) {              // Alg. 2 l.2
+    const double x = n / std::ldexp(1.0, i);                 // l.3
+    const double theta_i = K.lambda_p / x;                   // l.4 (f = lambda', reading R1)
+    const uint64_t T = (uint64_t)std::ceil(theta_i);
+    TRY(generate(c, std::max<uint64_t>(c->T_global, T), seed));   // l.5 (reading R4)
+    TRY(select_impl(c, k, tmp.data(), nullptr, &cov));       // l.6 (reading R9)
+    r.theta_i[i - 1] = T;
+    r.theta_i_real[i - 1] = theta_i;
+    r.cov_i[i - 1] = cov;
+    r.rounds = (uint32_t)i;
+    if ((n * (double)cov) / (double)c->T_global >= (1.0 + K.eps_p) * x) {   // l.7 (reading R7)
+      LB = (n * (double)cov) / (double)c->T_global / (1.0 + K.eps_p);       // l.8
+      break;
+    }
+  }
+  const double theta = K.lambda_s / LB;                      // reading R2
+  const uint64_t T = (uint64_t)std::ceil(theta);
+  TRY(generate(c, std::max<uint64_t>(c->T_global, T), seed));    // reading R8
+  std::vector<uint64_t> gains(k);
+  TRY(select_impl(c, k, seeds, gains.data(), &cov));
+  r.LB = LB;
+  r.theta = theta;
+  r.R_final = c->T_global;
+  r.covered = cov;
+  r.spread_est = n * (double)cov / (double)c->T_global;     // Eq. 3
+  if (res) *res = r;
+  return GIM_OK;
+}
+
+gim_status gim_rr_export(gim_ctx* c, uint64_t* n_sets, uint64_t* pool_len, uint64_t* ids, uint64_t* offs,
+                         uint32_t* nodes, int sort_each_set) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  DeviceGuard g(c->device);
+  if (n_sets) *n_sets = c->nsets;
+  if (pool_len) *pool_len = c->pool_len;
+  if (ids)
+    for (const Seg& s : c->segs)
+      for (uint64_t i = 0; i < s.count; ++i) ids[s.lstart + i] = s.gstart + i;
+  std::vector<uint64_t> tmp;
+  uint64_t* o = offs;
+  if (!o && nodes && sort_each_set) {
+    tmp.resize(c->nsets + 1);
+    o = tmp.data();
+  }
+  if (o) {
+    if (c->nsets == 0) o[0] = 0;
+    else CK(cudaMemcpyAsync(o, c->offsets.p, (c->nsets + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (nodes && c->pool_len) CK(cudaMemcpyAsync(nodes, c->pool.p, c->pool_len * 4, cudaMemcpyDeviceToHost, c->stream));
+  TRY(sync(c));
+  if (nodes && sort_each_set)
+    for (uint64_t i = 0; i < c->nsets; ++i) std::sort(nodes + o[i], nodes + o[i + 1]);
+  return GIM_OK;
+}
+
+gim_status gim_counts_export(gim_ctx* c, uint32_t* count_out) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  if (!count_out) return fail(c, GIM_EINVAL, "count_out required");
+  if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
+  DeviceGuard g(c->device);
+  CK(cudaMemcpyAsync(count_out, c->count_total.p, (uint64_t)c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+  return sync(c);
+}
+
+gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  switch (opt) {
+    case GIM_OPT_FORCE_GIANT: c->force_giant = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_QUEUE_CAP:
+      if (value < 1 || value > kQMax) return fail(c, GIM_EINVAL, "queue cap must be in [1, 512]");
+      c->qcap = (uint32_t)value;
+      return GIM_OK;
+    case GIM_OPT_PROFILE: c->profile = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_STAGING_CAP:
+      if (value < 0) return fail(c, GIM_EINVAL, "staging cap must be >= 0");
+      c->staging_init = (uint64_t)value;
+      c->stage_cap = 0;
+      return GIM_OK;
+  }
+  return fail(c, GIM_EINVAL, "unknown option");
+}
+
+gim_status gim_get_stats(gim_ctx* c, gim_stats* out) {
+  if (!c || !out) return GIM_EINVAL;
+  *out = c->st;
+  return GIM_OK;
+}
+
+gim_status gim_reset_stats(gim_ctx* c) {
+  if (!c) return GIM_EINVAL;
+  c->st = gim_stats{};
+  return GIM_OK;
+}
+
+gim_status gim_microbench_philox(gim_ctx* c, uint64_t groups, double* ms) {
+  if (!c || !ms || groups == 0) return GIM_EINVAL;
+  c->err.clear();
+  DeviceGuard g(c->device);
+  const int grid = c->num_sms * 8;
+  const uint64_t threads = (uint64_t)grid * 256;
+  const uint32_t per = (uint32_t)std::max<uint64_t>(1, groups / threads);
+  DevBuf sink;
+  TRY(dalloc(c, sink, 256));
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  CK(launch_philox_bench(1, per, sink.as<uint32_t>(), grid, c->stream));   // warm-up
+  CK(cudaEventRecord(a, c->stream));
+  CK(launch_philox_bench(2, per, sink.as<uint32_t>(), grid, c->stream));
+  CK(cudaEventRecord(b, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  float t = 0.f;
+  CK(cudaEventElapsedTime(&t, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  dfree(c, sink);
+  c->st.launches += 2;
+  *ms = (double)t * ((double)groups / (double)(threads * per));   // normalised to `groups`
+  return sync(c);
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// gim_device.cuh — device-side building blocks of libgim (sm_100a).
+//
+// Philox4x32-10 and the (seed; RR id, slot) key scheme (reading R16, DESIGN.md "RNG
+// contract"), kernel parameter blocks and launch wrappers shared by rr.cu / select.cu /
+// gim_api.cu. Independent of oracle/ (no shared code; both sides are pinned separately to the
+// Random123 known-answer vectors).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gim {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;   // empty hash slot / "no node"
+constexpr uint32_t kSent = 0xFFFFFFFFu;    // count sentinel of an already-selected node
+
+enum { MODEL_IC = 0, MODEL_LT = 1 };
+enum { W_EXPLICIT = 0, W_WC = 1, W_UNIFORM = 2 };
+
+// Slot tags of the counter's high word.
+constexpr uint32_t kSlotRootHi = 0x80000000u;   // 2^63: root draw
+constexpr uint32_t kSlotLtHi = 0x40000000u;     // 2^62 | v: LT in-edge draw at node v
+
+// Philox4x32-10 (Salmon et al. SC'11): 10 rounds, key bumped after every round.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// Root of RR set `id`: floor(u64 * n / 2^64), u64 = out0 | out1 << 32 of slot 2^63
+// ("u = randSelect(V)", Alg. 3 l.5; reading R17).
+__device__ __forceinline__ uint32_t rr_root(uint64_t seed, uint64_t id, uint32_t n) {
+  const uint4 o = philox4x32_10(make_uint4((uint32_t)id, (uint32_t)(id >> 32), 0u, kSlotRootHi),
+                                (uint32_t)seed, (uint32_t)(seed >> 32));
+  const uint64_t u64 = (uint64_t)o.x | ((uint64_t)o.y << 32);
+  return (uint32_t)__umul64hi(u64, (uint64_t)n);
+}
+
+// Device counters of one generation launch sequence (zeroed by the host per chunk).
+struct GenCounters {
+  unsigned long long stage_tail;   // staging bump allocator (elements)
+  unsigned long long coins;        // in-edge slots examined / LT draws
+  unsigned long long live;         // live in-edges found
+  unsigned long long coins_giant;  // same, giant kernel
+  unsigned long long live_giant;
+  unsigned int claim;              // warp-kernel work claim
+  unsigned int claim_giant;        // giant-kernel work claim
+  unsigned int giant_count;        // ids pushed to the giant list
+  unsigned int retry_count;        // ids whose staging write did not fit
+};
+
+// Parameters of the RR-generation kernels.
+struct RRParams {
+  uint32_t n;
+  const uint32_t* row_ptr;     // in-CSR row pointers (uint32, m < 2^32)
+  const uint32_t* src;         // in-CSR sources
+  const uint64_t* thr_edge;    // explicit weights: IC ceil(w*2^32), LT floor(w*2^32)
+  uint64_t thr_uniform;        // uniform p: ceil(p*2^32)
+  uint64_t seed;
+  uint64_t id_base;            // global RR id = id_base + item
+  uint32_t count;              // items to process
+  const uint32_t* item_list;   // nullptr: items are 0..count-1; else item = item_list[i]
+  uint32_t* sizes;             // [chunk] RR size per item
+  uint64_t* soff;              // [chunk] staging offset per item
+  uint32_t* staging;
+  uint64_t stage_cap;
+  GenCounters* ctr;
+  uint32_t* giant_list;        // items replayed by the giant kernel
+  uint32_t* retry_list;        // items whose staging write failed
+  uint32_t qcap;               // shared-memory queue capacity (<= kQMax)
+  int force_giant;
+};
+
+// Shared-memory layout of the warp-per-RR kernel.
+constexpr int kRRWarps = 8;          // warps per CTA
+constexpr int kQMax = 512;           // queue capacity (the queue doubles as the RR buffer)
+constexpr int kHLog = 10;            // visited hash: 1024 slots (load <= 0.63)
+constexpr int kHSize = 1 << kHLog;
+constexpr int kRRSmemPerWarp = (kQMax + kHSize) * 4;
+constexpr int kGiantThreads = 512;
+
+}  // namespace gim

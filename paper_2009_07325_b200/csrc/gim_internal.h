@@ -1,0 +1,31 @@
+// gim_internal.h — host-side declarations of the kernel launch wrappers (libgim internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gim {
+struct RRParams;
+
+cudaError_t launch_rr_warp(int model, int scheme, const RRParams& p, int grid, cudaStream_t s);
+cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
+                            uint32_t* gqueues, uint64_t bm_words, cudaStream_t s);
+cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const uint64_t* soff,
+                         const uint64_t* scan, uint32_t count, uint64_t pool_base, uint32_t* pool,
+                         uint64_t* offsets_out, uint32_t* count_total, int grid, cudaStream_t s);
+cudaError_t launch_count_sub(const uint32_t* pool, uint64_t e0, uint64_t e1, uint32_t* count_total,
+                             int grid, cudaStream_t s);
+
+cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* sink, int grid, cudaStream_t s);
+
+uint64_t scan_tiles(uint64_t count);
+cudaError_t launch_scan_u32(const uint32_t* in, uint64_t count, uint64_t* out, uint64_t* tile_tmp,
+                            uint64_t* total_tmp, cudaStream_t s, int* launches);
+cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, uint32_t nsets,
+                               const uint64_t* inv_off, uint32_t* cursor, uint32_t* inv, int grid,
+                               cudaStream_t s);
+cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
+                          int grid, cudaStream_t s);
+cudaError_t launch_cover(const unsigned long long* keys, int j, const uint64_t* inv_off,
+                         const uint32_t* inv, const uint64_t* offsets, const uint32_t* pool,
+                         uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s);
+}  // namespace gim

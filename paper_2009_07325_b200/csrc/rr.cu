@@ -1,0 +1,428 @@
+// rr.cu — RR-set generation kernels (K-IC/K-LT warp kernel, K-GIANT fallback, K-STORE).
+//
+// What they compute: RR_i = {u : u reaches root_i in the instance graph g_i}
+// by a randomized reverse BFS over the in-CSR (Alg. 3), IC coin per in-edge
+// slot, LT one in-edge per node (§3.7). B200 design:
+//  * persistent warps claim RR ids dynamically (Alg. 6's N_b persistent blocks, P:449-478,
+//    with ids pre-assigned instead of the N_RR/tail_RR mutex, reading R20);
+//  * one warp per RR set (N_th = 32), frontier queue + visited hash in shared memory
+//    (Q_shr; Visited as an exact-set hash, readings R12-R13);
+//  * coins are drawn BEFORE the source column is loaded: lane l evaluates one Philox call = the
+//    4 coins of slot group g = e >> 2, and only live edges read src[e];
+//  * ballot/scan compaction of newly visited nodes into the append-only queue, which is also
+//    the RR buffer (replaces RR_tmp);
+//  * a set that outgrows the queue is aborted and replayed exactly by the block-per-RR giant
+//    kernel with a global bitmap (replaces offloadQueue/reloadQueue, Alg. 4/5: the
+//    keyed RNG makes the replay draw the same coins);
+//  * two-pass storage: bump-allocated staging + sizes, then exclusive scan and a compacting
+//    copy that also builds count_total (Occur; Alg. 6 l.4-11).
+#include "gim_device.cuh"
+#include "gim_internal.h"
+
+namespace gim {
+
+__device__ __forceinline__ uint32_t hash_slot(uint32_t u) { return (u * 0x9E3779B1u) >> (32 - kHLog); }
+
+// Exact-set test-and-set in the shared-memory visited hash. Returns true iff u was absent.
+__device__ __forceinline__ bool hash_insert(uint32_t* h, uint32_t u) {
+  uint32_t s = hash_slot(u);
+  while (true) {
+    const uint32_t old = atomicCAS(&h[s], kEmpty, u);
+    if (old == kEmpty) return true;
+    if (old == u) return false;
+    s = (s + 1) & (kHSize - 1);
+  }
+}
+
+template <int SCHEME>
+__device__ __forceinline__ bool ic_live(uint32_t coin, uint32_t thr_wc, uint64_t thr_uniform,
+                                        const uint64_t* thr_edge, uint32_t e) {
+  if (SCHEME == W_WC) return coin <= thr_wc;              // coin < ceil(2^32/d)  <=>  coin*d < 2^32
+  if (SCHEME == W_UNIFORM) return (uint64_t)coin < thr_uniform;
+  return (uint64_t)coin < thr_edge[e];
+}
+
+// LT: index of the chosen in-edge of v (0..d-1) or d if none (reading R18). Warp-collective.
+template <int SCHEME>
+__device__ __forceinline__ uint32_t lt_choose(const RRParams& p, uint64_t id, uint32_t v,
+                                              uint32_t a, uint32_t d, int lane) {
+  const uint4 o = philox4x32_10(make_uint4((uint32_t)id, (uint32_t)(id >> 32), v, kSlotLtHi),
+                                (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+  const uint32_t r = o.x;
+  if (SCHEME == W_WC) return __umulhi(r, d);            // floor(r * d / 2^32): uniform in-neighbour
+  // explicit weights: first t with r < sum_{s<=t} W_s, warp prefix scan
+  uint64_t carry = 0;
+  for (uint32_t base = 0; base < d; base += 32) {
+    const uint32_t t = base + lane;
+    uint64_t x = (t < d) ? p.thr_edge[a + t] : 0ull;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint64_t y = __shfl_up_sync(kFull, x, off);
+      if (lane >= off) x += y;
+    }
+    x += carry;
+    const uint32_t hit = __ballot_sync(kFull, t < d && (uint64_t)r < x);
+    if (hit) return base + (__ffs(hit) - 1);
+    carry = __shfl_sync(kFull, x, 31);
+  }
+  return d;
+}
+
+
+// One lane's share of an IC expansion step: the 4 coins of slot group g (one Philox call),
+// live test against the exact integer threshold, and — for live edges only — the src[e] load
+// and the visited test-and-set `visit(u)`. uu[j] receives the newly visited node or kEmpty.
+template <int SCHEME, class Visit>
+__device__ __forceinline__ void ic_group(const RRParams& p, uint32_t id_lo, uint32_t id_hi,
+                                         uint32_t k0, uint32_t k1, uint32_t g, uint32_t a,
+                                         uint32_t b, uint32_t thr_wc, uint32_t (&uu)[4],
+                                         unsigned long long& coins, unsigned long long& lives,
+                                         Visit visit) {
+  const uint4 w = philox4x32_10(make_uint4(id_lo, id_hi, g, 0u), k0, k1);
+  const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+  const uint32_t e0 = g << 2;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t e = e0 + j;
+    if (e >= a && e < b) {
+      ++coins;
+      if (ic_live<SCHEME>(words[j], thr_wc, p.thr_uniform, p.thr_edge, e)) {
+        ++lives;
+        const uint32_t u = __ldg(p.src + e);
+        if (visit(u)) uu[j] = u;
+      }
+    }
+  }
+}
+
+// Warp-inclusive scan of the number of new nodes per lane; returns (exclusive offset, total).
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t cnt, int lane, uint32_t& total) {
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, off);
+    if (lane >= off) incl += y;
+  }
+  total = __shfl_sync(kFull, incl, 31);
+  return incl - cnt;
+}
+
+// ------------------------------------------------------------------------------------------
+// K-RR: warp-per-RR persistent kernel.
+// ------------------------------------------------------------------------------------------
+template <int MODEL, int SCHEME>
+__global__ void __launch_bounds__(kRRWarps * 32) k_rr_warp(RRParams p) {
+  extern __shared__ uint32_t smem[];
+  const int lane = threadIdx.x & 31;
+  uint32_t* q = smem + (threadIdx.x >> 5) * (kQMax + kHSize);
+  uint32_t* h = q + kQMax;
+  for (int i = lane; i < kHSize; i += 32) h[i] = kEmpty;
+  __syncwarp();
+  const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
+  unsigned long long coins = 0, lives = 0;
+
+  while (true) {
+    uint32_t i = 0;
+    if (lane == 0) i = atomicAdd(&p.ctr->claim, 1u);
+    i = __shfl_sync(kFull, i, 0);
+    if (i >= p.count) break;
+    const uint32_t item = p.item_list ? p.item_list[i] : i;
+    if (p.force_giant) {
+      if (lane == 0) p.giant_list[atomicAdd(&p.ctr->giant_count, 1u)] = item;
+      continue;
+    }
+    const uint64_t id = p.id_base + item;
+    const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
+    const uint32_t root = rr_root(p.seed, id, p.n);
+    if (lane == 0) {
+      q[0] = root;
+      h[hash_slot(root)] = root;     // table is empty here
+    }
+    __syncwarp();
+    uint32_t head = 0, tail = 1;
+    bool overflow = false;
+    while (head < tail) {
+      const uint32_t v = q[head++];
+      const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
+      if (b <= a) continue;
+      if (MODEL == MODEL_IC) {
+        const uint32_t thr_wc = (SCHEME == W_WC) ? 0xFFFFFFFFu / (b - a) : 0u;
+        const uint32_t g_lo = a >> 2, g_hi = (b - 1) >> 2;
+        for (uint32_t gb = g_lo; gb <= g_hi; gb += 32) {
+          const uint32_t g = gb + lane;
+          uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
+          if (g <= g_hi)
+            ic_group<SCHEME>(p, id_lo, id_hi, k0, k1, g, a, b, thr_wc, uu, coins, lives,
+                             [h](uint32_t u) { return hash_insert(h, u); });
+          const uint32_t cnt = (uu[0] != kEmpty) + (uu[1] != kEmpty) + (uu[2] != kEmpty) + (uu[3] != kEmpty);
+          uint32_t total;
+          uint32_t pos = tail + warp_excl_scan(cnt, lane, total);
+          if (tail + total > p.qcap) { overflow = true; break; }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (uu[j] != kEmpty) q[pos++] = uu[j];
+          tail += total;
+        }
+      } else {  // LT: frontier <= 1
+        const uint32_t d = b - a;
+        const uint32_t j = lt_choose<SCHEME>(p, id, v, a, d, lane);
+        if (lane == 0) { coins += 1; lives += (j < d); }
+        if (j < d) {
+          uint32_t isnew = 0, u = 0;
+          if (lane == 0) {
+            u = __ldg(p.src + a + j);
+            isnew = hash_insert(h, u);
+          }
+          isnew = __shfl_sync(kFull, isnew, 0);
+          u = __shfl_sync(kFull, u, 0);
+          if (isnew) {
+            if (tail + 1 > p.qcap) { overflow = true; }
+            else {
+              if (lane == 0) q[tail] = u;
+              tail += 1;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (overflow) break;
+    }
+    if (overflow) {
+      if (lane == 0) p.giant_list[atomicAdd(&p.ctr->giant_count, 1u)] = item;
+    } else {
+      unsigned long long off = 0;
+      if (lane == 0) off = atomicAdd(&p.ctr->stage_tail, (unsigned long long)tail);
+      off = __shfl_sync(kFull, off, 0);
+      if (off + tail > p.stage_cap) {
+        if (lane == 0) p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = item;
+      } else {
+        for (uint32_t t = lane; t < tail; t += 32) p.staging[off + t] = q[t];
+        if (lane == 0) { p.sizes[item] = tail; p.soff[item] = off; }
+      }
+    }
+    // clear the visited hash (vectorised; 4 KB)
+    uint4* h4 = reinterpret_cast<uint4*>(h);
+    for (int t = lane; t < kHSize / 4; t += 32) h4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    __syncwarp();
+  }
+  // per-warp statistics
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    coins += __shfl_xor_sync(kFull, coins, off);
+    lives += __shfl_xor_sync(kFull, lives, off);
+  }
+  if (lane == 0) {
+    atomicAdd(&p.ctr->coins, coins);
+    atomicAdd(&p.ctr->live, lives);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K-GIANT: block-per-RR replay for sets that outgrew the warp queue. Level-synchronous over
+// the frontier with a per-block global bitmap (Visited[n]) and a global queue of
+// capacity n; warps expand frontier nodes in parallel, bitmap test-and-set by atomicOr.
+// ------------------------------------------------------------------------------------------
+template <int MODEL, int SCHEME>
+__global__ void __launch_bounds__(kGiantThreads) k_rr_giant(RRParams p, uint32_t* bitmaps,
+                                                            uint32_t* gqueues, uint64_t bm_words) {
+  __shared__ uint32_t s_item, s_tail;
+  __shared__ unsigned long long s_off;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kGiantThreads / 32;
+  uint32_t* bm = bitmaps + (uint64_t)blockIdx.x * bm_words;
+  uint32_t* Q = gqueues + (uint64_t)blockIdx.x * p.n;
+  const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
+  const uint32_t giant_count = *(volatile unsigned int*)&p.ctr->giant_count;
+  unsigned long long coins = 0, lives = 0;
+
+  while (true) {
+    if (threadIdx.x == 0) {
+      const uint32_t r = atomicAdd(&p.ctr->claim_giant, 1u);
+      s_item = (r < giant_count) ? p.giant_list[r] : kEmpty;
+    }
+    __syncthreads();
+    const uint32_t item = s_item;
+    if (item == kEmpty) break;
+    const uint64_t id = p.id_base + item;
+    const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
+    if (threadIdx.x == 0) {
+      const uint32_t root = rr_root(p.seed, id, p.n);
+      Q[0] = root;
+      atomicOr(&bm[root >> 5], 1u << (root & 31));
+      s_tail = 1;
+    }
+    __syncthreads();
+    uint32_t head = 0, lvl_end = 1;
+    while (head < lvl_end) {
+      for (uint32_t f = head + warp; f < lvl_end; f += nw) {
+        const uint32_t v = Q[f];
+        const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
+        if (b <= a) continue;
+        if (MODEL == MODEL_IC) {
+          const uint32_t thr_wc = (SCHEME == W_WC) ? 0xFFFFFFFFu / (b - a) : 0u;
+          const uint32_t g_lo = a >> 2, g_hi = (b - 1) >> 2;
+          for (uint32_t gb = g_lo; gb <= g_hi; gb += 32) {
+            const uint32_t g = gb + lane;
+            uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
+            if (g <= g_hi)
+              ic_group<SCHEME>(p, id_lo, id_hi, k0, k1, g, a, b, thr_wc, uu, coins, lives,
+                               [bm](uint32_t u) {
+                                 const uint32_t bit = 1u << (u & 31);
+                                 return !(atomicOr(&bm[u >> 5], bit) & bit);
+                               });
+            const uint32_t cnt = (uu[0] != kEmpty) + (uu[1] != kEmpty) + (uu[2] != kEmpty) + (uu[3] != kEmpty);
+            uint32_t total;
+            const uint32_t excl = warp_excl_scan(cnt, lane, total);
+            uint32_t base = 0;
+            if (lane == 0 && total) base = atomicAdd(&s_tail, total);
+            uint32_t pos = __shfl_sync(kFull, base, 0) + excl;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (uu[j] != kEmpty) Q[pos++] = uu[j];
+          }
+        } else {
+          const uint32_t d = b - a;
+          const uint32_t j = lt_choose<SCHEME>(p, id, v, a, d, lane);
+          if (lane == 0) coins += 1;
+          if (j < d && lane == 0) {
+            ++lives;
+            const uint32_t u = __ldg(p.src + a + j);
+            const uint32_t bit = 1u << (u & 31);
+            if (!(atomicOr(&bm[u >> 5], bit) & bit)) Q[atomicAdd(&s_tail, 1u)] = u;
+          }
+        }
+      }
+      __syncthreads();
+      head = lvl_end;
+      lvl_end = s_tail;
+      __syncthreads();
+    }
+    const uint32_t size = lvl_end;
+    if (threadIdx.x == 0) s_off = atomicAdd(&p.ctr->stage_tail, (unsigned long long)size);
+    __syncthreads();
+    const unsigned long long off = s_off;
+    if (off + size > p.stage_cap) {
+      if (threadIdx.x == 0) p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = item;
+    } else {
+      for (uint32_t t = threadIdx.x; t < size; t += kGiantThreads) p.staging[off + t] = Q[t];
+      if (threadIdx.x == 0) { p.sizes[item] = size; p.soff[item] = off; }
+    }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < size; t += kGiantThreads) bm[Q[t] >> 5] = 0u;
+    __syncthreads();
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    coins += __shfl_xor_sync(kFull, coins, off);
+    lives += __shfl_xor_sync(kFull, lives, off);
+  }
+  if (lane == 0) {
+    atomicAdd(&p.ctr->coins_giant, coins);
+    atomicAdd(&p.ctr->live_giant, lives);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K-STORE: compacting copy staging -> pool in item order + count_total histogram.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_store(const uint32_t* __restrict__ staging,
+                                               const uint32_t* __restrict__ sizes,
+                                               const uint64_t* __restrict__ soff,
+                                               const uint64_t* __restrict__ scan, uint32_t count,
+                                               uint64_t pool_base, uint32_t* __restrict__ pool,
+                                               uint64_t* __restrict__ offsets_out,
+                                               uint32_t* __restrict__ count_total) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < count; i += nwarps) {
+    const uint32_t sz = sizes[i];
+    const uint64_t from = soff[i], to = pool_base + scan[i];
+    for (uint32_t t = lane; t < sz; t += 32) {
+      const uint32_t v = staging[from + t];
+      pool[to + t] = v;
+      atomicAdd(count_total + v, 1u);
+    }
+    if (lane == 0) offsets_out[i] = to;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) offsets_out[count] = pool_base + scan[count];
+}
+
+// count_total[v] -= 1 for every member of local sets [s0, s1) (pool truncation).
+__global__ void k_count_sub(const uint32_t* __restrict__ pool, uint64_t e0, uint64_t e1,
+                            uint32_t* __restrict__ count_total) {
+  for (uint64_t t = e0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < e1;
+       t += (uint64_t)gridDim.x * blockDim.x)
+    atomicSub(count_total + pool[t], 1u);
+}
+
+// ------------------------------------------------------------------------------------------
+// Host launch wrappers
+// ------------------------------------------------------------------------------------------
+template <int MODEL, int SCHEME>
+static cudaError_t launch_rr_t(const RRParams& p, int grid, cudaStream_t s) {
+  const int smem = kRRWarps * kRRSmemPerWarp;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_rr_warp<MODEL, SCHEME>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_rr_warp<MODEL, SCHEME><<<grid, kRRWarps * 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rr_warp(int model, int scheme, const RRParams& p, int grid, cudaStream_t s) {
+  if (model == MODEL_IC) {
+    if (scheme == W_WC) return launch_rr_t<MODEL_IC, W_WC>(p, grid, s);
+    if (scheme == W_UNIFORM) return launch_rr_t<MODEL_IC, W_UNIFORM>(p, grid, s);
+    return launch_rr_t<MODEL_IC, W_EXPLICIT>(p, grid, s);
+  }
+  if (scheme == W_WC) return launch_rr_t<MODEL_LT, W_WC>(p, grid, s);
+  return launch_rr_t<MODEL_LT, W_EXPLICIT>(p, grid, s);
+}
+
+cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
+                            uint32_t* gqueues, uint64_t bm_words, cudaStream_t s) {
+  if (model == MODEL_IC) {
+    if (scheme == W_WC) k_rr_giant<MODEL_IC, W_WC><<<grid, kGiantThreads, 0, s>>>(p, bitmaps, gqueues, bm_words);
+    else if (scheme == W_UNIFORM) k_rr_giant<MODEL_IC, W_UNIFORM><<<grid, kGiantThreads, 0, s>>>(p, bitmaps, gqueues, bm_words);
+    else k_rr_giant<MODEL_IC, W_EXPLICIT><<<grid, kGiantThreads, 0, s>>>(p, bitmaps, gqueues, bm_words);
+  } else {
+    if (scheme == W_WC) k_rr_giant<MODEL_LT, W_WC><<<grid, kGiantThreads, 0, s>>>(p, bitmaps, gqueues, bm_words);
+    else k_rr_giant<MODEL_LT, W_EXPLICIT><<<grid, kGiantThreads, 0, s>>>(p, bitmaps, gqueues, bm_words);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const uint64_t* soff,
+                         const uint64_t* scan, uint32_t count, uint64_t pool_base, uint32_t* pool,
+                         uint64_t* offsets_out, uint32_t* count_total, int grid, cudaStream_t s) {
+  k_store<<<grid, 256, 0, s>>>(staging, sizes, soff, scan, count, pool_base, pool, offsets_out,
+                               count_total);
+  return cudaGetLastError();
+}
+
+// Philox microbenchmark (diagnostic, gim_microbench_philox): each thread evaluates `per_thread`
+// slot groups of one RR id, exactly the per-group work of the IC kernel without memory traffic.
+__global__ void __launch_bounds__(256) k_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* sink) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t acc = 0;
+  for (uint32_t i = 0; i < per_thread; ++i) {
+    const uint4 w = philox4x32_10(make_uint4(tid, 0u, i, 0u), (uint32_t)seed, (uint32_t)(seed >> 32));
+    acc += (w.x <= 0x1000u) + (w.y <= 0x1000u) + (w.z <= 0x1000u) + (w.w <= 0x1000u);
+  }
+  if (acc == 0xFFFFFFFFu) sink[0] = acc;
+}
+
+cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* sink, int grid, cudaStream_t s) {
+  k_philox_bench<<<grid, 256, 0, s>>>(seed, per_thread, sink);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_sub(const uint32_t* pool, uint64_t e0, uint64_t e1, uint32_t* count_total,
+                             int grid, cudaStream_t s) {
+  k_count_sub<<<grid, 256, 0, s>>>(pool, e0, e1, count_total);
+  return cudaGetLastError();
+}
+
+}  // namespace gim

@@ -1,0 +1,259 @@
+"""Thin Python binding of libgim.so (include/gim.h) — argument marshalling only.
+
+Every step of the hot path (RR sampling, storage, inverted index, NodeSelection, the IMM
+driver) runs inside libgim.so; this module only converts arrays and calls the C ABI. PyTorch is
+used for plumbing: device memory (the caching allocator backs every library allocation), the
+CUDA stream, and torch.distributed process groups for the selection all-reduce.
+
+Method names follow the C names without the ``gim_`` prefix (``gim_load_graph`` ->
+``Gim.load_graph`` ...). There is no fallback: if libgim.so is missing or no CUDA device is
+present, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+from typing import Callable, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgim.so")
+
+GIM_OK, GIM_EINVAL, GIM_ESTATE, GIM_ENOMEM, GIM_ECUDA, GIM_ECOLL, GIM_ELTWEIGHT = range(7)
+IC, LT = 0, 1
+W_EXPLICIT, W_WC, W_UNIFORM = 0, 1, 2
+OPT_FORCE_GIANT, OPT_QUEUE_CAP, OPT_PROFILE, OPT_STAGING_CAP = 1, 2, 3, 4
+
+_STATUS = {0: "GIM_OK", 1: "GIM_EINVAL", 2: "GIM_ESTATE", 3: "GIM_ENOMEM", 4: "GIM_ECUDA",
+           5: "GIM_ECOLL", 6: "GIM_ELTWEIGHT"}
+
+_p, _u32, _u64, _i32, _i64, _dbl = (ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64,
+                                    ctypes.c_int, ctypes.c_int64, ctypes.c_double)
+
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, _p, _u64, _p, _p)
+ALLOC_FN = ctypes.CFUNCTYPE(_p, _u64, _p, _p)
+FREE_FN = ctypes.CFUNCTYPE(None, _p, _p, _p)
+
+
+class ImmResultC(ctypes.Structure):
+    _fields_ = [("ell_eff", _dbl), ("eps_prime", _dbl), ("lambda_prime", _dbl),
+                ("lambda_star", _dbl), ("LB", _dbl), ("theta", _dbl), ("rounds", _u32),
+                ("theta_i", _u64 * 64), ("cov_i", _u64 * 64), ("theta_i_real", _dbl * 64),
+                ("R_final", _u64), ("covered", _u64), ("spread_est", _dbl)]
+
+
+class StatsC(ctypes.Structure):
+    _fields_ = [("launches", _u64), ("rr_sets", _u64), ("rr_elements", _u64),
+                ("giant_sets", _u64), ("coins", _u64), ("live_edges", _u64), ("coins_giant", _u64),
+                ("live_giant", _u64), ("selects", _u64),
+                ("allreduces", _u64), ("ms_rr", _dbl), ("ms_giant", _dbl), ("ms_store", _dbl),
+                ("ms_inv", _dbl), ("ms_select", _dbl), ("n_rr_launches", _u64),
+                ("n_giant_launches", _u64)]
+
+
+# name -> (restype, argtypes); exactly the functions declared in include/gim.h
+SIGNATURES = {
+    "gim_create": (_i32, [_i32, _p, ctypes.POINTER(_p)]),
+    "gim_destroy": (None, [_p]),
+    "gim_last_error": (ctypes.c_char_p, [_p]),
+    "gim_load_graph": (_i32, [_p, _u32, _u64, _p, _p, _p, _i32, _i32, ctypes.c_float]),
+    "gim_set_shard": (_i32, [_p, _i32, _i32]),
+    "gim_set_allreduce": (_i32, [_p, ALLREDUCE_FN, _p]),
+    "gim_set_allocator": (_i32, [_p, ALLOC_FN, FREE_FN, _p]),
+    "gim_generate_rr": (_i32, [_p, _u64, _u64]),
+    "gim_select": (_i32, [_p, _u32, _p, _p, _p]),
+    "gim_imm": (_i32, [_p, _u32, _dbl, _dbl, _u64, _p, ctypes.POINTER(ImmResultC)]),
+    "gim_rr_export": (_i32, [_p, _p, _p, _p, _p, _p, _i32]),
+    "gim_counts_export": (_i32, [_p, _p]),
+    "gim_set_option": (_i32, [_p, _i32, _i64]),
+    "gim_get_stats": (_i32, [_p, ctypes.POINTER(StatsC)]),
+    "gim_reset_stats": (_i32, [_p]),
+    "gim_microbench_philox": (_i32, [_p, _u64, ctypes.POINTER(_dbl)]),
+}
+
+_lib_handle = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libgim.so (raises if it is missing — there is no fallback path)."""
+    global _lib_handle
+    if _lib_handle is None:
+        if not os.path.exists(path):
+            raise RuntimeError(f"libgim.so not built ({path}); run `make` / __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(lib, name)
+            f.restype, f.argtypes = res, args
+        _lib_handle = lib
+    return _lib_handle
+
+
+class GimError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+@dataclasses.dataclass
+class ImmResult:
+    seeds: np.ndarray
+    ell_eff: float
+    eps_prime: float
+    lambda_prime: float
+    lambda_star: float
+    LB: float
+    theta: float
+    rounds: int
+    theta_i: np.ndarray
+    theta_i_real: np.ndarray
+    cov_i: np.ndarray
+    R_final: int
+    covered: int
+    spread_est: float
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+class Gim:
+    """One libgim context (one device, one stream)."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None, torch_allocator: bool = True):
+        self._lib = load_library()
+        self._keep = []
+        h = _p()
+        st = self._lib.gim_create(device, stream, ctypes.byref(h))
+        if st != GIM_OK:
+            raise GimError(st, "gim_create failed (no usable CUDA device?)")
+        self._h = h
+        self.device = device
+        if torch_allocator:
+            self._use_torch_allocator(device)
+
+    # -- plumbing -------------------------------------------------------------------------
+    def _check(self, st: int):
+        if st != GIM_OK:
+            raise GimError(st, self._lib.gim_last_error(self._h).decode())
+
+    def _use_torch_allocator(self, device: int):
+        import torch
+
+        def _alloc(nbytes, stream, user):
+            try:
+                return torch.cuda.caching_allocator_alloc(int(nbytes), device, int(stream or 0))
+            except Exception:
+                return None
+
+        def _free(ptr, stream, user):
+            torch.cuda.caching_allocator_delete(ptr)
+
+        a, f = ALLOC_FN(_alloc), FREE_FN(_free)
+        self._keep += [a, f]
+        self._check(self._lib.gim_set_allocator(self._h, a, f, None))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.gim_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- C ABI ----------------------------------------------------------------------------
+    def load_graph(self, n: int, row_ptr: np.ndarray, src: np.ndarray, model: int, scheme: int,
+                   weights: Optional[np.ndarray] = None, p_uniform: float = 0.0):
+        rp = np.ascontiguousarray(row_ptr, dtype=np.uint64)
+        s = np.ascontiguousarray(src, dtype=np.uint32)
+        w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float32)
+        self._check(self._lib.gim_load_graph(self._h, n, len(s), _ptr(rp), _ptr(s) if len(s) else None,
+                                             _ptr(w), model, scheme, p_uniform))
+
+    def set_shard(self, rank: int, world: int):
+        self._check(self._lib.gim_set_shard(self._h, rank, world))
+
+    def set_allreduce(self, fn: Callable[[int, int, int], int]):
+        """fn(dev_ptr, count_int32, cuda_stream) -> 0 on success (in-place SUM)."""
+        cb = ALLREDUCE_FN(lambda buf, count, stream, user: int(fn(buf, count, stream or 0)))
+        self._keep.append(cb)
+        self._check(self._lib.gim_set_allreduce(self._h, cb, None))
+
+    def generate_rr(self, theta: int, seed: int):
+        self._check(self._lib.gim_generate_rr(self._h, theta, seed))
+
+    def select(self, k: int):
+        seeds = np.zeros(k, dtype=np.uint32)
+        gains = np.zeros(k, dtype=np.uint64)
+        cov = np.zeros(1, dtype=np.uint64)
+        self._check(self._lib.gim_select(self._h, k, _ptr(seeds), _ptr(gains), _ptr(cov)))
+        return seeds, gains, int(cov[0])
+
+    def imm(self, k: int, eps: float, ell: float, seed: int) -> ImmResult:
+        seeds = np.zeros(k, dtype=np.uint32)
+        r = ImmResultC()
+        self._check(self._lib.gim_imm(self._h, k, eps, ell, seed, _ptr(seeds), ctypes.byref(r)))
+        nr = int(r.rounds)
+        return ImmResult(seeds=seeds, ell_eff=r.ell_eff, eps_prime=r.eps_prime,
+                         lambda_prime=r.lambda_prime, lambda_star=r.lambda_star, LB=r.LB,
+                         theta=r.theta, rounds=nr, theta_i=np.array(r.theta_i[:nr], dtype=np.uint64),
+                         theta_i_real=np.array(r.theta_i_real[:nr]),
+                         cov_i=np.array(r.cov_i[:nr], dtype=np.uint64), R_final=int(r.R_final),
+                         covered=int(r.covered), spread_est=r.spread_est)
+
+    def rr_export(self, sort_each_set: bool = True):
+        ns, pl = _u64(), _u64()
+        self._check(self._lib.gim_rr_export(self._h, ctypes.byref(ns), ctypes.byref(pl), None, None,
+                                            None, 0))
+        ids = np.zeros(max(ns.value, 1), dtype=np.uint64)
+        off = np.zeros(ns.value + 1, dtype=np.uint64)
+        nodes = np.zeros(max(pl.value, 1), dtype=np.uint32)
+        self._check(self._lib.gim_rr_export(self._h, ctypes.byref(ns), ctypes.byref(pl), _ptr(ids),
+                                            _ptr(off), _ptr(nodes), int(sort_each_set)))
+        return ids[:ns.value], off, nodes[:pl.value]
+
+    def counts_export(self, n: int) -> np.ndarray:
+        out = np.zeros(n, dtype=np.uint32)
+        self._check(self._lib.gim_counts_export(self._h, _ptr(out)))
+        return out
+
+    def set_option(self, opt: int, value: int):
+        self._check(self._lib.gim_set_option(self._h, opt, value))
+
+    def stats(self) -> dict:
+        s = StatsC()
+        self._check(self._lib.gim_get_stats(self._h, ctypes.byref(s)))
+        return {name: getattr(s, name) for name, _ in StatsC._fields_}
+
+    def reset_stats(self):
+        self._check(self._lib.gim_reset_stats(self._h))
+
+    def microbench_philox(self, groups: int) -> float:
+        ms = _dbl()
+        self._check(self._lib.gim_microbench_philox(self._h, groups, ctypes.byref(ms)))
+        return ms.value
+
+
+def torch_allreduce(group=None):
+    """all-reduce callback for Gim.set_allreduce: wraps the library's int32 device buffer as a
+    torch tensor (``__cuda_array_interface__``) and runs torch.distributed.all_reduce (SUM) on
+    the library's stream (NCCL over NVLink when the group's backend is nccl)."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(ptr: int, count: int, stream: int) -> int:
+        class _View:
+            __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<i4",
+                                        "data": (int(ptr), False), "version": 3, "strides": None,
+                                        "stream": None}
+        t = torch.as_tensor(_View(), device="cuda")
+        s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return 0
+
+    return fn

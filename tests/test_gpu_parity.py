@@ -1,0 +1,297 @@
+"""Parity of the CUDA path (through the C ABI, libgim.so) with the oracle, element by element.
+
+Bar: RR sets (sorted), offsets, ids, counts, seeds and gains bit-exact;
+IMM doubles (lambda', lambda*, theta_i, LB, theta) within 1e-12 relative. Sizes: tiny graphs,
+C1/C2 pools spanning many warps and a ragged tail, and C3/C4 at full size on sampled ids.
+"""
+import math
+import threading
+
+import numpy as np
+import pytest
+
+import gim_inputs as gi
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2009_07325_b200")
+
+
+def _ctx(g, model, scheme, p_uniform=0.0, **opts):
+    c = P.Gim(0)
+    c.load_graph(g.n, g.row_ptr, g.src, model, scheme, weights=g.weights, p_uniform=p_uniform)
+    for k, v in opts.items():
+        c.set_option(k, v)
+    return c
+
+
+def _same_pool(c, o, T):
+    ids, off, nodes = c.rr_export(sort_each_set=True)
+    ooff, onodes, ocnt = o.export()
+    assert len(ids) == T and np.array_equal(ids, np.arange(T, dtype=np.uint64))
+    assert np.array_equal(off, ooff), "offsets"
+    assert np.array_equal(nodes, onodes), "pool contents"
+    assert np.array_equal(c.counts_export(o.n), ocnt), "counts"
+
+
+def _variants(g):
+    rng = np.random.default_rng(g.n)
+    din = g.in_degree()
+    dst = np.repeat(np.arange(g.n), din)
+    w_ic = rng.choice([0.0, 0.2, 0.5, 1.0], size=g.m).astype(np.float32)
+    w_lt = (rng.uniform(0.1, 1.0, size=g.m) / np.maximum(din[dst], 1)).astype(np.float32)
+    return [("ic_wc", g, gi.IC, gi.W_WC, 0.0), ("ic_uni", g, gi.IC, gi.W_UNIFORM, 0.3),
+            ("ic_exp", gi.with_weights(g, w_ic), gi.IC, gi.W_EXPLICIT, 0.0),
+            ("lt_wc", g, gi.LT, gi.W_WC, 0.0), ("lt_exp", gi.with_weights(g, w_lt), gi.LT, gi.W_EXPLICIT, 0.0)]
+
+
+def test_keyscheme_golden_diamond():
+    import json, os
+    gd = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "diamond_keyscheme.json")))
+    d = gi.diamond()
+    for case, g, model, scheme in [("ic_wc", d, gi.IC, gi.W_WC),
+                                   ("ic_half", gi.with_weights(d, np.full(4, 0.5)), gi.IC, gi.W_EXPLICIT),
+                                   ("lt_wc", d, gi.LT, gi.W_WC)]:
+        c = _ctx(g, model, scheme)
+        c.generate_rr(16, gd["seed"])
+        ids, off, nodes = c.rr_export()
+        sets = ["".join(str(int(v)) for v in nodes[off[i]:off[i + 1]]) for i in range(16)]
+        assert sets == gd[case + "_sets"]
+        assert c.counts_export(4).tolist() == gd[case + "_counts"]
+        seeds, gains, cov = c.select(2)
+        assert seeds.tolist() == gd[case + "_greedy_k2"]["seeds"]
+        assert gains.tolist() == gd[case + "_greedy_k2"]["gains"]
+
+
+@pytest.mark.parametrize("gname", ["diamond", "chain", "star", "cycle", "rand0", "rand1", "rand2"])
+def test_pool_parity_tiny(gname):
+    g = {"diamond": gi.diamond(), "chain": gi.chain(6), "star": gi.star_in(40),
+         "cycle": gi.cycle_plus(), "rand0": gi.random_small(9, 30, 0),
+         "rand1": gi.random_small(12, 60, 1), "rand2": gi.random_small(30, 200, 2)}[gname]
+    for name, gg, model, scheme, pu in _variants(g):
+        T = 3001                       # many warps + a ragged tail
+        c = _ctx(gg, model, scheme, pu)
+        c.generate_rr(T, 4242)
+        o = oracle.Oracle(gg, model, scheme, pu)
+        o.generate(T, 4242)
+        _same_pool(c, o, T)
+        k = min(3, g.n)
+        assert [x.tolist() if hasattr(x, "tolist") else x for x in c.select(k)] == \
+               [x.tolist() if hasattr(x, "tolist") else x for x in o.select(k)], name
+
+
+@pytest.mark.parametrize("opts", [{}, {P.OPT_FORCE_GIANT: 1}, {P.OPT_QUEUE_CAP: 4},
+                                  {P.OPT_STAGING_CAP: 64}, {P.OPT_QUEUE_CAP: 32, P.OPT_STAGING_CAP: 1000}])
+def test_pool_parity_C1_invariance(opts):
+    """Same pool whatever the queue capacity, forced fallback or staging retries."""
+    w = gi.WORKLOADS["C1"]
+    g = gi.workload_graph("C1")
+    T = 40013
+    c = _ctx(g, w.model, w.scheme, **opts)
+    c.generate_rr(T, w.rr_seed)
+    o = oracle.Oracle(g, w.model, w.scheme)
+    o.generate(T, w.rr_seed)
+    _same_pool(c, o, T)
+    if opts.get(P.OPT_FORCE_GIANT):
+        assert c.stats()["giant_sets"] == T
+
+
+def test_pool_parity_C2_and_select():
+    w = gi.WORKLOADS["C2"]
+    g = gi.workload_graph("C2")
+    T = 30011
+    c = _ctx(g, w.model, w.scheme)
+    c.generate_rr(T, w.rr_seed)
+    o = oracle.Oracle(g, w.model, w.scheme)
+    o.generate(T, w.rr_seed)
+    _same_pool(c, o, T)
+    s, gns, cov = c.select(50)
+    os_, ogn, ocov = o.select(50)
+    assert np.array_equal(s, os_) and np.array_equal(gns, ogn) and cov == ocov
+    st = c.stats()
+    assert st["coins"] == o.stats()["coins"] or st["giant_sets"] > 0   # aborted work is recounted
+    assert st["rr_elements"] == len(o.export()[1])
+
+
+def test_extend_truncate_reseed():
+    g = gi.random_small(40, 300, 5)
+    c = _ctx(g, gi.IC, gi.W_WC)
+    o = oracle.Oracle(g, gi.IC, gi.W_WC)
+    for T, seed in [(1000, 1), (5000, 1), (777, 1), (4000, 1), (4000, 2), (0, 2), (10, 2)]:
+        c.generate_rr(T, seed)
+        o.generate(T, seed)
+        _same_pool(c, o, T)
+
+
+def test_select_zero_gain_and_k_eq_n():
+    g = gi.diamond()
+    c = _ctx(g, gi.LT, gi.W_WC)
+    c.generate_rr(16, 200907325)
+    s, gns, cov = c.select(4)
+    o = oracle.Oracle(g, gi.LT, gi.W_WC)
+    o.generate(16, 200907325)
+    os_, ogn, ocov = o.select(4)
+    assert s.tolist() == os_.tolist() and gns.tolist() == ogn.tolist() and cov == ocov == 16
+
+
+def test_errors():
+    g = gi.diamond()
+    c = P.Gim(0)
+    with pytest.raises(P.GimError) as e:
+        c.generate_rr(10, 1)
+    assert e.value.status == 2                     # no graph
+    with pytest.raises(P.GimError) as e:
+        c.load_graph(4, np.array([0, 0, 1, 2, 4], np.uint64), np.array([0, 0, 2, 1], np.uint32), gi.IC, gi.W_WC)
+    assert e.value.status == 1                     # row 3 not ascending
+    with pytest.raises(P.GimError) as e:
+        c.load_graph(2, np.array([0, 1, 1], np.uint64), np.array([0], np.uint32), gi.IC, gi.W_WC)
+    assert e.value.status == 1                     # self-loop
+    with pytest.raises(P.GimError) as e:
+        c.load_graph(g.n, g.row_ptr, g.src, gi.LT, gi.W_EXPLICIT, weights=np.full(4, 0.6, np.float32))
+    assert e.value.status == 6                     # LT in-weights of node 3 sum to 1.2
+    c.load_graph(g.n, g.row_ptr, g.src, gi.IC, gi.W_WC)
+    with pytest.raises(P.GimError) as e:
+        c.select(1)
+    assert e.value.status == 2                     # empty pool
+    c.generate_rr(10, 1)
+    for k in (0, 5):
+        with pytest.raises(P.GimError) as e:
+            c.select(k)
+        assert e.value.status == 1
+    with pytest.raises(P.GimError):
+        c.imm(2, 0.0, 1.0, 1)
+    g1 = gi.from_edges(1, [])
+    c.load_graph(1, g1.row_ptr, g1.src, gi.IC, gi.W_WC)
+    c.generate_rr(5, 3)
+    ids, off, nodes = c.rr_export()
+    assert off.tolist() == [0, 1, 2, 3, 4, 5] and c.counts_export(1).tolist() == [5]
+    with pytest.raises(P.GimError) as e:
+        c.imm(1, 0.1, 1.0, 1)
+    assert e.value.status == 1                     # n = 1 (reading R25)
+
+
+def _imm_parity(key, k=None, eps=None):
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    k = k or w.k
+    eps = eps or w.eps
+    c = _ctx(g, w.model, w.scheme, w.p_uniform)
+    r = c.imm(k, eps, w.ell, w.rr_seed)
+    o = oracle.Oracle(g, w.model, w.scheme, w.p_uniform)
+    ro = o.imm(k, eps, w.ell, w.rr_seed)
+    rel = lambda a, b: abs(a - b) <= 1e-12 * max(abs(b), 1e-300)
+    assert rel(r.lambda_prime, ro.lambda_prime) and rel(r.lambda_star, ro.lambda_star)
+    assert rel(r.ell_eff, ro.ell_eff) and rel(r.eps_prime, ro.eps_prime)
+    assert r.rounds == ro.rounds
+    assert all(rel(a, b) for a, b in zip(r.theta_i_real, ro.theta_i))
+    assert np.array_equal(r.theta_i, ro.T_i) and np.array_equal(r.cov_i, ro.cov_i)
+    assert rel(r.LB, ro.LB) and rel(r.theta, ro.theta)
+    assert r.R_final == ro.R_final and r.covered == ro.cov
+    assert np.array_equal(r.seeds, ro.seeds), (r.seeds, ro.seeds)
+    assert rel(r.spread_est, ro.spread_est)
+    return r
+
+
+def test_imm_parity_C1():
+    _imm_parity("C1")
+
+
+def test_imm_parity_C2():
+    _imm_parity("C2")
+
+
+def test_imm_parity_C1_LT():
+    w = gi.WORKLOADS["C1"]
+    g = gi.workload_graph("C1")
+    c = _ctx(g, gi.LT, gi.W_WC)
+    r = c.imm(w.k, w.eps, w.ell, w.rr_seed)
+    o = oracle.Oracle(g, gi.LT, gi.W_WC)
+    ro = o.imm(w.k, w.eps, w.ell, w.rr_seed)
+    assert np.array_equal(r.seeds, ro.seeds) and r.R_final == ro.R_final and r.covered == ro.cov
+
+
+@pytest.mark.parametrize("key", ["C3", "C4"])
+def test_full_size_sampled(key):
+    """BASELINE.json full size: 2^21 RR sets in the launch configuration bench.py times; sampled
+    ids recomputed one by one by the oracle; counts checked by the size-free identities."""
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    c = _ctx(g, w.model, w.scheme)
+    T = 1 << 21
+    c.generate_rr(T, w.rr_seed)
+    ids, off, nodes = c.rr_export(sort_each_set=True)
+    assert np.array_equal(ids, np.arange(T, dtype=np.uint64))
+    o = oracle.Oracle(g, w.model, w.scheme)
+    rng = np.random.default_rng(1)
+    sample = np.concatenate([[0, 1, T - 1], rng.choice(T, 300, replace=False)])
+    sizes = np.diff(off.astype(np.int64))
+    sample = np.concatenate([sample, np.argsort(sizes)[-5:]])       # include the largest sets
+    for i in sample:
+        assert np.array_equal(nodes[off[i]:off[i + 1]], o.rr_set(w.rr_seed, int(i))), int(i)
+    cnt = c.counts_export(g.n)
+    assert int(cnt.sum()) == len(nodes)
+    assert np.array_equal(np.bincount(nodes, minlength=g.n).astype(np.uint32), cnt)
+    assert np.all(sizes >= 1)
+    d = np.diff(nodes.astype(np.int64))
+    starts = off[1:-1].astype(np.int64)
+    mask = np.ones(len(d), dtype=bool)
+    mask[starts - 1] = False
+    assert np.all(d[mask] > 0)                                       # distinct members
+
+
+def test_sharded_emulation_equals_single():
+    """P contexts (one per emulated rank) with a host-side summing all-reduce: pools are the
+    slices of the P=1 pool and the selection is identical (SURVEY.md §4 "multi-GPU without a
+    cluster")."""
+    import torch
+    w = gi.WORKLOADS["C2"]
+    g = gi.workload_graph("C2")
+    T, k = 50021, 50
+    ref = _ctx(g, w.model, w.scheme)
+    ref.generate_rr(T, w.rr_seed)
+    rseeds, rgains, rcov = ref.select(k)
+    _, roff, rnodes = ref.rr_export()
+    for Pn in (2, 3):
+        bar = threading.Barrier(Pn)
+        bufs = [None] * Pn
+        ctxs = []
+
+        def make_cb(r):
+            def cb(ptr, count, stream):
+                class V:
+                    __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<i4",
+                                                "data": (int(ptr), False), "version": 3,
+                                                "strides": None, "stream": None}
+                t = torch.as_tensor(V(), device="cuda")
+                torch.cuda.ExternalStream(stream).synchronize()
+                bufs[r] = t.cpu()
+                bar.wait()
+                tot = sum(bufs)
+                bar.wait()
+                t.copy_(tot.cuda())
+                torch.cuda.synchronize()
+                return 0
+            return cb
+
+        for r in range(Pn):
+            c = _ctx(g, w.model, w.scheme)
+            c.set_shard(r, Pn)
+            c.set_allreduce(make_cb(r))
+            ctxs.append(c)
+        out = [None] * Pn
+
+        def run(r):
+            ctxs[r].generate_rr(T, w.rr_seed)
+            out[r] = ctxs[r].select(k)
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(Pn)]
+        [t.start() for t in th]
+        [t.join() for t in th]
+        for r in range(Pn):
+            assert np.array_equal(out[r][0], rseeds) and np.array_equal(out[r][1], rgains)
+            assert out[r][2] == rcov
+            ids, off, nodes = ctxs[r].rr_export()
+            lo, hi = r * T // Pn, (r + 1) * T // Pn
+            assert np.array_equal(ids, np.arange(lo, hi, dtype=np.uint64))
+            assert np.array_equal(nodes, rnodes[roff[lo]:roff[hi]])

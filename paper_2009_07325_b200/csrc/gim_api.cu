@@ -59,7 +59,7 @@ struct gim_ctx {
   std::vector<Seg> segs;
   DevBuf pool, offsets, count_total;
   // generation scratch
-  DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr;
+  DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr, dump;
   DevBuf bitmaps, gqueues;
   uint32_t giant_slots = 0;
   uint64_t stage_cap = 0;
@@ -239,7 +239,9 @@ RRParams base_params(gim_ctx* c) {
   p.staging = c->staging.as<uint32_t>();
   p.stage_cap = c->stage_cap;
   p.ctr = c->ctr.as<GenCounters>();
-  p.giant_list = c->giant_list.as<uint32_t>();
+  p.giant_recs = c->giant_list.as<GiantRec>();
+  p.dump = c->dump.as<uint32_t>();
+  p.dump_cap = c->dump.bytes / 4;
   p.retry_list = c->retry_list.as<uint32_t>();
   p.qcap = c->qcap;
   p.force_giant = c->force_giant;
@@ -255,7 +257,8 @@ gim_status read_ctr(gim_ctx* c) {
 gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   TRY(ensure(c, c->sizes, (uint64_t)cnt * 4));
   TRY(ensure(c, c->soff, (uint64_t)cnt * 8));
-  TRY(ensure(c, c->giant_list, (uint64_t)cnt * 4));
+  TRY(ensure(c, c->giant_list, (uint64_t)cnt * sizeof(GiantRec)));
+  TRY(ensure(c, c->dump, std::max<uint64_t>((uint64_t)cnt * 8, 1u << 20) * 4));
   TRY(ensure(c, c->retry_list, (uint64_t)cnt * 4));
   TRY(ensure(c, c->item_list, (uint64_t)cnt * 4));
   TRY(ensure(c, c->scan_out, ((uint64_t)cnt + 1) * 8));
@@ -309,6 +312,7 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     GenCounters h = *c->h_ctr;
     h.stage_tail = old_cap;
     h.claim = h.claim_giant = h.giant_count = h.retry_count = 0;
+    h.dump_tail = 0;
     *c->h_ctr = h;
     CK(cudaMemcpyAsync(c->ctr.p, c->h_ctr, sizeof(GenCounters), cudaMemcpyHostToDevice, c->stream));
     p = base_params(c);
@@ -533,7 +537,7 @@ void gim_destroy(gim_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
                     &c->sizes, &c->soff, &c->giant_list, &c->retry_list, &c->item_list, &c->scan_out,
-                    &c->scan_tmp, &c->staging, &c->ctr, &c->bitmaps, &c->gqueues, &c->cnt, &c->inv_off,
+                    &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->bitmaps, &c->gqueues, &c->cnt, &c->inv_off,
                     &c->cursor, &c->inv, &c->covered, &c->keys, &c->dec};
   for (DevBuf* b : bufs) dfree(c, *b);
   cudaStreamSynchronize(c->stream);

@@ -50,10 +50,19 @@ struct GenCounters {
   unsigned long long live;         // live in-edges found
   unsigned long long coins_giant;  // same, giant kernel
   unsigned long long live_giant;
+  unsigned long long dump_tail;    // partial-BFS dump allocator (elements)
   unsigned int claim;              // warp-kernel work claim
   unsigned int claim_giant;        // giant-kernel work claim
   unsigned int giant_count;        // ids pushed to the giant list
   unsigned int retry_count;        // ids whose staging write did not fit
+};
+
+// A set handed from the warp kernel to the giant kernel: the warp's partial BFS (queue
+// q[0..qlen) of which q[0..head) are fully expanded) is dumped at dump[dump_off..] so the giant
+// kernel resumes instead of replaying. qlen == 0: start from the root.
+struct GiantRec {
+  uint32_t item, qlen, head, pad;
+  unsigned long long dump_off;
 };
 
 // Parameters of the RR-generation kernels.
@@ -72,7 +81,9 @@ struct RRParams {
   uint32_t* staging;
   uint64_t stage_cap;
   GenCounters* ctr;
-  uint32_t* giant_list;        // items replayed by the giant kernel
+  GiantRec* giant_recs;        // sets handed to the giant kernel
+  uint32_t* dump;              // partial-BFS dumps
+  uint64_t dump_cap;
   uint32_t* retry_list;        // items whose staging write failed
   uint32_t qcap;               // shared-memory queue capacity (<= kQMax)
   int force_giant;
@@ -85,5 +96,6 @@ constexpr int kHLog = 10;            // visited hash: 1024 slots (load <= 0.63)
 constexpr int kHSize = 1 << kHLog;
 constexpr int kRRSmemPerWarp = (kQMax + kHSize) * 4;
 constexpr int kGiantThreads = 512;
+constexpr int kGiantWin = 2048;      // frontier window of the giant kernel (smem)
 
 }  // namespace gim

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kRRWarps * 32) k_rr_warp(RRParams p) {
     if (i >= p.count) break;
     const uint32_t item = p.item_list ? p.item_list[i] : i;
     if (p.force_giant) {
-      if (lane == 0) p.giant_list[atomicAdd(&p.ctr->giant_count, 1u)] = item;
+      if (lane == 0) p.giant_recs[atomicAdd(&p.ctr->giant_count, 1u)] = GiantRec{item, 0u, 0u, 0u, 0ull};
       continue;
     }
     const uint64_t id = p.id_base + item;
@@ -188,7 +188,17 @@ __global__ void __launch_bounds__(kRRWarps * 32) k_rr_warp(RRParams p) {
       if (overflow) break;
     }
     if (overflow) {
-      if (lane == 0) p.giant_list[atomicAdd(&p.ctr->giant_count, 1u)] = item;
+      // hand the partial BFS to the giant kernel: q[0..tail) are visited, q[0..head-1) fully
+      // expanded; the node being expanded (q[head-1]) is re-expanded there (same coins).
+      unsigned long long off = 0;
+      if (lane == 0) off = atomicAdd(&p.ctr->dump_tail, (unsigned long long)tail);
+      off = __shfl_sync(kFull, off, 0);
+      const bool fits = off + tail <= p.dump_cap;
+      if (fits)
+        for (uint32_t t = lane; t < tail; t += 32) p.dump[off + t] = q[t];
+      if (lane == 0)
+        p.giant_recs[atomicAdd(&p.ctr->giant_count, 1u)] =
+            fits ? GiantRec{item, tail, head - 1, 0u, off} : GiantRec{item, 0u, 0u, 0u, 0ull};
     } else {
       unsigned long long off = 0;
       if (lane == 0) off = atomicAdd(&p.ctr->stage_tail, (unsigned long long)tail);
@@ -218,95 +228,165 @@ __global__ void __launch_bounds__(kRRWarps * 32) k_rr_warp(RRParams p) {
 }
 
 // ------------------------------------------------------------------------------------------
-// K-GIANT: block-per-RR replay for sets that outgrew the warp queue. Level-synchronous over
-// the frontier with a per-block global bitmap (Visited[n]) and a global queue of
-// capacity n; warps expand frontier nodes in parallel, bitmap test-and-set by atomicOr.
+// K-GIANT: block-per-RR continuation for sets that outgrew the warp queue (the role of the
+// paper's reservoir queue Q_res, Alg. 4/5). Per-block global bitmap (Visited[n])
+// and global queue (capacity n). The frontier is processed in windows of up to kGiantWin
+// nodes; each window is flattened into 32-slot-group chunks (a hub of in-degree d gives
+// ceil(d/128) chunks) which the 16 warps of the block split into contiguous ranges, so a
+// narrow frontier of hubs still occupies the whole block.
 // ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t block_incl_scan_512(uint32_t x, uint32_t* s_w, uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = (lane < kGiantThreads / 32) ? s_w[lane] : 0u;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, w, off);
+      if (lane >= off) w += y;
+    }
+    if (lane < kGiantThreads / 32) s_w[lane] = w;
+  }
+  __syncthreads();
+  total = s_w[kGiantThreads / 32 - 1];
+  const uint32_t r = x + (warp ? s_w[warp - 1] : 0u);
+  __syncthreads();
+  return r;
+}
+
 template <int MODEL, int SCHEME>
 __global__ void __launch_bounds__(kGiantThreads) k_rr_giant(RRParams p, uint32_t* bitmaps,
                                                             uint32_t* gqueues, uint64_t bm_words) {
-  __shared__ uint32_t s_item, s_tail;
+  constexpr int NW = kGiantThreads / 32;
+  __shared__ uint32_t s_cp[kGiantWin];     // inclusive chunk prefix over the window
+  __shared__ uint32_t s_a[kGiantWin], s_b[kGiantWin];
+  __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_tail, s_r;
   __shared__ unsigned long long s_off;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kGiantThreads / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t* bm = bitmaps + (uint64_t)blockIdx.x * bm_words;
   uint32_t* Q = gqueues + (uint64_t)blockIdx.x * p.n;
   const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
   const uint32_t giant_count = *(volatile unsigned int*)&p.ctr->giant_count;
   unsigned long long coins = 0, lives = 0;
+  auto visit = [bm](uint32_t u) {
+    const uint32_t bit = 1u << (u & 31);
+    return !(atomicOr(&bm[u >> 5], bit) & bit);
+  };
 
   while (true) {
-    if (threadIdx.x == 0) {
-      const uint32_t r = atomicAdd(&p.ctr->claim_giant, 1u);
-      s_item = (r < giant_count) ? p.giant_list[r] : kEmpty;
-    }
+    if (threadIdx.x == 0) s_r = atomicAdd(&p.ctr->claim_giant, 1u);
     __syncthreads();
-    const uint32_t item = s_item;
-    if (item == kEmpty) break;
-    const uint64_t id = p.id_base + item;
+    const uint32_t r = s_r;
+    if (r >= giant_count) break;
+    const GiantRec rec = p.giant_recs[r];
+    const uint64_t id = p.id_base + rec.item;
     const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
-    if (threadIdx.x == 0) {
-      const uint32_t root = rr_root(p.seed, id, p.n);
-      Q[0] = root;
-      atomicOr(&bm[root >> 5], 1u << (root & 31));
-      s_tail = 1;
+    uint32_t head;
+    if (rec.qlen == 0) {
+      if (threadIdx.x == 0) {
+        const uint32_t root = rr_root(p.seed, id, p.n);
+        Q[0] = root;
+        atomicOr(&bm[root >> 5], 1u << (root & 31));
+        s_tail = 1;
+      }
+      head = 0;
+    } else {                                   // resume the warp kernel's partial BFS
+      for (uint32_t t = threadIdx.x; t < rec.qlen; t += kGiantThreads) {
+        const uint32_t u = p.dump[rec.dump_off + t];
+        Q[t] = u;
+        atomicOr(&bm[u >> 5], 1u << (u & 31));
+      }
+      if (threadIdx.x == 0) s_tail = rec.qlen;
+      head = rec.head;
     }
     __syncthreads();
-    uint32_t head = 0, lvl_end = 1;
-    while (head < lvl_end) {
-      for (uint32_t f = head + warp; f < lvl_end; f += nw) {
-        const uint32_t v = Q[f];
-        const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
-        if (b <= a) continue;
-        if (MODEL == MODEL_IC) {
-          const uint32_t thr_wc = (SCHEME == W_WC) ? 0xFFFFFFFFu / (b - a) : 0u;
-          const uint32_t g_lo = a >> 2, g_hi = (b - 1) >> 2;
-          for (uint32_t gb = g_lo; gb <= g_hi; gb += 32) {
-            const uint32_t g = gb + lane;
+    while (true) {
+      const uint32_t tail = s_tail;
+      if (head >= tail) break;
+      const uint32_t L = min(tail - head, (uint32_t)kGiantWin);
+      // phase 1: row ranges and chunk counts of the window, block prefix scan
+      uint32_t carry = 0;
+      for (uint32_t base = 0; base < L; base += kGiantThreads) {
+        const uint32_t f = base + threadIdx.x;
+        uint32_t nc = 0;
+        if (f < L) {
+          const uint32_t v = Q[head + f];
+          const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
+          s_a[f] = a;
+          s_b[f] = b;
+          if (b > a) nc = (MODEL == MODEL_IC) ? ((((b - 1) >> 2) - (a >> 2)) >> 5) + 1 : 1u;
+        }
+        uint32_t tot;
+        const uint32_t incl = block_incl_scan_512(nc, s_w, tot);
+        if (f < L) s_cp[f] = carry + incl;
+        carry += tot;
+      }
+      __syncthreads();
+      const uint32_t total = carry;
+      // phase 2: warp `warp` takes chunks [c0, c1)
+      const uint32_t c0 = (uint32_t)(((uint64_t)total * warp) / NW);
+      const uint32_t c1 = (uint32_t)(((uint64_t)total * (warp + 1)) / NW);
+      if (c0 < c1) {
+        uint32_t lo = 0, hi = L - 1;           // first f with s_cp[f] > c0
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (s_cp[mid] > c0) hi = mid; else lo = mid + 1;
+        }
+        uint32_t f = lo;
+        for (uint32_t c = c0; c < c1; ++c) {
+          while (s_cp[f] <= c) ++f;
+          const uint32_t cin = c - (f ? s_cp[f - 1] : 0u);
+          const uint32_t a = s_a[f], b = s_b[f];
+          if (MODEL == MODEL_IC) {
+            const uint32_t thr_wc = (SCHEME == W_WC) ? 0xFFFFFFFFu / (b - a) : 0u;
+            const uint32_t g_hi = (b - 1) >> 2;
+            const uint32_t g = (a >> 2) + (cin << 5) + lane;
             uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
-            if (g <= g_hi)
-              ic_group<SCHEME>(p, id_lo, id_hi, k0, k1, g, a, b, thr_wc, uu, coins, lives,
-                               [bm](uint32_t u) {
-                                 const uint32_t bit = 1u << (u & 31);
-                                 return !(atomicOr(&bm[u >> 5], bit) & bit);
-                               });
+            if (g <= g_hi) ic_group<SCHEME>(p, id_lo, id_hi, k0, k1, g, a, b, thr_wc, uu, coins, lives, visit);
             const uint32_t cnt = (uu[0] != kEmpty) + (uu[1] != kEmpty) + (uu[2] != kEmpty) + (uu[3] != kEmpty);
-            uint32_t total;
-            const uint32_t excl = warp_excl_scan(cnt, lane, total);
+            uint32_t tot;
+            const uint32_t excl = warp_excl_scan(cnt, lane, tot);
             uint32_t base = 0;
-            if (lane == 0 && total) base = atomicAdd(&s_tail, total);
+            if (lane == 0 && tot) base = atomicAdd(&s_tail, tot);
             uint32_t pos = __shfl_sync(kFull, base, 0) + excl;
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               if (uu[j] != kEmpty) Q[pos++] = uu[j];
-          }
-        } else {
-          const uint32_t d = b - a;
-          const uint32_t j = lt_choose<SCHEME>(p, id, v, a, d, lane);
-          if (lane == 0) coins += 1;
-          if (j < d && lane == 0) {
-            ++lives;
-            const uint32_t u = __ldg(p.src + a + j);
-            const uint32_t bit = 1u << (u & 31);
-            if (!(atomicOr(&bm[u >> 5], bit) & bit)) Q[atomicAdd(&s_tail, 1u)] = u;
+          } else {
+            const uint32_t v = Q[head + f];
+            const uint32_t d = b - a;
+            const uint32_t j = lt_choose<SCHEME>(p, id, v, a, d, lane);
+            if (lane == 0) {
+              coins += 1;
+              if (j < d) {
+                ++lives;
+                const uint32_t u = __ldg(p.src + a + j);
+                if (visit(u)) Q[atomicAdd(&s_tail, 1u)] = u;
+              }
+            }
           }
         }
       }
-      __syncthreads();
-      head = lvl_end;
-      lvl_end = s_tail;
+      head += L;
       __syncthreads();
     }
-    const uint32_t size = lvl_end;
+    const uint32_t size = s_tail;
     if (threadIdx.x == 0) s_off = atomicAdd(&p.ctr->stage_tail, (unsigned long long)size);
     __syncthreads();
     const unsigned long long off = s_off;
     if (off + size > p.stage_cap) {
-      if (threadIdx.x == 0) p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = item;
+      if (threadIdx.x == 0) p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = rec.item;
     } else {
       for (uint32_t t = threadIdx.x; t < size; t += kGiantThreads) p.staging[off + t] = Q[t];
-      if (threadIdx.x == 0) { p.sizes[item] = size; p.soff[item] = off; }
+      if (threadIdx.x == 0) { p.sizes[rec.item] = size; p.soff[rec.item] = off; }
     }
-    __syncthreads();
     for (uint32_t t = threadIdx.x; t < size; t += kGiantThreads) bm[Q[t] >> 5] = 0u;
     __syncthreads();
   }

@@ -18,10 +18,10 @@ pytestmark = pytest.mark.gpu
 P = pytest.importorskip("paper_2009_07325_b200")
 
 
-def _ctx(g, model, scheme, p_uniform=0.0, **opts):
+def _ctx(g, model, scheme, p_uniform=0.0, opts=None):
     c = P.Gim(0)
     c.load_graph(g.n, g.row_ptr, g.src, model, scheme, weights=g.weights, p_uniform=p_uniform)
-    for k, v in opts.items():
+    for k, v in (opts or {}).items():
         c.set_option(k, v)
     return c
 
@@ -88,7 +88,7 @@ def test_pool_parity_C1_invariance(opts):
     w = gi.WORKLOADS["C1"]
     g = gi.workload_graph("C1")
     T = 40013
-    c = _ctx(g, w.model, w.scheme, **opts)
+    c = _ctx(g, w.model, w.scheme, opts=opts)
     c.generate_rr(T, w.rr_seed)
     o = oracle.Oracle(g, w.model, w.scheme)
     o.generate(T, w.rr_seed)

@@ -21,6 +21,11 @@ oracle/liboracle.so: oracle/gim_oracle.c
 gim_inputs/libplg.so: gim_inputs/plg.cpp
 	g++ -O3 -std=c++17 -fopenmp -shared -fPIC $< -o $@
 
+# tuning variants (A/B on the GPU box via GIM_LIB_PATH): make variant NAME=x VFLAGS="-DGIM_RR_BLOCKS=5"
+variant: $(SRCS) $(HDRS)
+	mkdir -p build
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -shared -o build/libgim_$(NAME).so $(SRCS)
+
 ptxas: $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /dev/null $(PKG)/csrc/rr.cu
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /dev/null $(PKG)/csrc/select.cu

@@ -63,7 +63,7 @@ const char* gim_last_error(const gim_ctx* ctx);
  *    GIM_W_UNIFORM: p_uv = p_uniform in [0,1] (IC only).
  *  model GIM_LT requires GIM_W_WC or GIM_W_EXPLICIT with sum_u w_uv <= 1 at every v
  *    (P:125), else GIM_ELTWEIGHT (or GIM_EINVAL for LT + uniform, reading R23).
- *  Limits: 1 <= n < 2^32 - 1, m < 2^32 (row pointers are held as uint32 on the device).
+ *  Limits: 1 <= n < 2^32 - 1, m < 2^32 - 256 (row pointers are held as uint32 on the device).
  * Replaces any previous graph and clears the RR pool. */
 gim_status gim_load_graph(gim_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* in_row_ptr,
                           const uint32_t* in_src, const float* weights, gim_model model,

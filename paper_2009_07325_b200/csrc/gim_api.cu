@@ -234,6 +234,15 @@ RRParams base_params(gim_ctx* c) {
   p.thr_edge = c->thr_edge.as<uint64_t>();
   p.thr_uniform = c->thr_uniform;
   p.seed = c->seed;
+  {
+    uint32_t k0 = (uint32_t)c->seed, k1 = (uint32_t)(c->seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+      p.rk[2 * r] = k0;
+      p.rk[2 * r + 1] = k1;
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+  }
   p.sizes = c->sizes.as<uint32_t>();
   p.soff = c->soff.as<uint64_t>();
   p.staging = c->staging.as<uint32_t>();
@@ -280,7 +289,7 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   p.id_base = gstart;
   p.count = cnt;
   p.item_list = nullptr;
-  const int rr_grid = c->num_sms * 4;   // 4 CTAs x 8 warps per SM (smem-limited)
+  const int rr_grid = c->num_sms * kRRBlocksPerSM;   // persistent: 6 CTAs x 8 warps per SM
   {
     Prof pf(c, CLS_RR);
     TRY(launched(c, launch_rr_warp(c->model, c->scheme, p, rr_grid, c->stream), "k_rr_warp"));
@@ -572,7 +581,7 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
   c->err.clear();
   DeviceGuard g(c->device);
   if (n < 1 || n == 0xFFFFFFFFu) return fail(c, GIM_EINVAL, "n must be in [1, 2^32-2]");
-  if (m >= 0xFFFFFFF0ull) return fail(c, GIM_EINVAL, "m must be < 2^32 - 16");
+  if (m >= 0xFFFFFF00ull) return fail(c, GIM_EINVAL, "m must be < 2^32 - 256");
   if (!rp || (m && !src)) return fail(c, GIM_EINVAL, "row_ptr/src missing");
   if (model != GIM_IC && model != GIM_LT) return fail(c, GIM_EINVAL, "bad model");
   if (scheme != GIM_W_EXPLICIT && scheme != GIM_W_WC && scheme != GIM_W_UNIFORM) return fail(c, GIM_EINVAL, "bad scheme");
@@ -770,7 +779,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
   switch (opt) {
     case GIM_OPT_FORCE_GIANT: c->force_giant = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_QUEUE_CAP:
-      if (value < 1 || value > kQMax) return fail(c, GIM_EINVAL, "queue cap must be in [1, 512]");
+      if (value < 1 || value > kQMax) return fail(c, GIM_EINVAL, "queue cap must be in [1, 384]");
       c->qcap = (uint32_t)value;
       return GIM_OK;
     case GIM_OPT_PROFILE: c->profile = value ? 1 : 0; return GIM_OK;

@@ -34,6 +34,18 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
+// Same, with the 20 round keys precomputed (rk[2r], rk[2r+1] = key of round r): kernels pass
+// them in the parameter (constant) bank so every key XOR is one LOP3 with a constant operand.
+__device__ __forceinline__ uint4 philox4x32_10_rk(uint4 c, const uint32_t* rk) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ rk[2 * r], lo1, hi0 ^ c.w ^ rk[2 * r + 1], lo0);
+  }
+  return c;
+}
+
 // Root of RR set `id`: floor(u64 * n / 2^64), u64 = out0 | out1 << 32 of slot 2^63
 // ("u = randSelect(V)", Alg. 3 l.5; reading R17).
 __device__ __forceinline__ uint32_t rr_root(uint64_t seed, uint64_t id, uint32_t n) {
@@ -73,6 +85,7 @@ struct RRParams {
   const uint64_t* thr_edge;    // explicit weights: IC ceil(w*2^32), LT floor(w*2^32)
   uint64_t thr_uniform;        // uniform p: ceil(p*2^32)
   uint64_t seed;
+  uint32_t rk[20];             // Philox round keys of `seed` (host-computed)
   uint64_t id_base;            // global RR id = id_base + item
   uint32_t count;              // items to process
   const uint32_t* item_list;   // nullptr: items are 0..count-1; else item = item_list[i]
@@ -91,10 +104,22 @@ struct RRParams {
 
 // Shared-memory layout of the warp-per-RR kernel.
 constexpr int kRRWarps = 8;          // warps per CTA
-constexpr int kQMax = 512;           // queue capacity (the queue doubles as the RR buffer)
-constexpr int kHLog = 10;            // visited hash: 1024 slots (load <= 0.63)
-constexpr int kHSize = 1 << kHLog;
-constexpr int kRRSmemPerWarp = (kQMax + kHSize) * 4;
+constexpr int kQMax = 384;           // queue capacity (the queue doubles as the RR buffer)
+constexpr int kHSize = 768;          // visited hash slots (load <= (384 + 256) / 768)
+constexpr int kRRSmemPerWarp = (kQMax + kHSize) * 4;   // 4.5 KB -> 6 CTAs x 8 warps per SM
+#ifndef GIM_RR_BLOCKS
+#define GIM_RR_BLOCKS 6
+#endif
+#ifndef GIM_RR_ILP
+#define GIM_RR_ILP 2
+#endif
+constexpr int kRRBlocksPerSM = GIM_RR_BLOCKS;
+constexpr int kRRIlp = GIM_RR_ILP;    // Philox chains per lane per iteration (1 or 2)
+#ifndef GIM_HUB_ILP
+#define GIM_HUB_ILP 4
+#endif
+constexpr int kHubIlp = GIM_HUB_ILP;  // Philox chains per lane per step on a hub node
+constexpr uint32_t kHubGroups = 32u * GIM_HUB_ILP;   // nodes with >= this many slot groups are hubs
 constexpr int kGiantThreads = 512;
 constexpr int kGiantWin = 2048;      // frontier window of the giant kernel (smem)
 

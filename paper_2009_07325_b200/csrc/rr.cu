@@ -21,7 +21,7 @@
 
 namespace gim {
 
-__device__ __forceinline__ uint32_t hash_slot(uint32_t u) { return (u * 0x9E3779B1u) >> (32 - kHLog); }
+__device__ __forceinline__ uint32_t hash_slot(uint32_t u) { return __umulhi(u * 0x9E3779B1u, (uint32_t)kHSize); }
 
 // Exact-set test-and-set in the shared-memory visited hash. Returns true iff u was absent.
 __device__ __forceinline__ bool hash_insert(uint32_t* h, uint32_t u) {
@@ -30,16 +30,8 @@ __device__ __forceinline__ bool hash_insert(uint32_t* h, uint32_t u) {
     const uint32_t old = atomicCAS(&h[s], kEmpty, u);
     if (old == kEmpty) return true;
     if (old == u) return false;
-    s = (s + 1) & (kHSize - 1);
+    s = (s + 1 == (uint32_t)kHSize) ? 0u : s + 1;
   }
-}
-
-template <int SCHEME>
-__device__ __forceinline__ bool ic_live(uint32_t coin, uint32_t thr_wc, uint64_t thr_uniform,
-                                        const uint64_t* thr_edge, uint32_t e) {
-  if (SCHEME == W_WC) return coin <= thr_wc;              // coin < ceil(2^32/d)  <=>  coin*d < 2^32
-  if (SCHEME == W_UNIFORM) return (uint64_t)coin < thr_uniform;
-  return (uint64_t)coin < thr_edge[e];
 }
 
 // LT: index of the chosen in-edge of v (0..d-1) or d if none (reading R18). Warp-collective.
@@ -69,30 +61,52 @@ __device__ __forceinline__ uint32_t lt_choose(const RRParams& p, uint64_t id, ui
 }
 
 
-// One lane's share of an IC expansion step: the 4 coins of slot group g (one Philox call),
-// live test against the exact integer threshold, and — for live edges only — the src[e] load
-// and the visited test-and-set `visit(u)`. uu[j] receives the newly visited node or kEmpty.
-template <int SCHEME, class Visit>
-__device__ __forceinline__ void ic_group(const RRParams& p, uint32_t id_lo, uint32_t id_hi,
-                                         uint32_t k0, uint32_t k1, uint32_t g, uint32_t a,
-                                         uint32_t b, uint32_t thr_wc, uint32_t (&uu)[4],
-                                         unsigned long long& coins, unsigned long long& lives,
-                                         Visit visit) {
-  const uint4 w = philox4x32_10(make_uint4(id_lo, id_hi, g, 0u), k0, k1);
-  const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+// Fast path of one IC expansion step: lane evaluates the 4 coins of slot group g (one Philox
+// call) and returns the 4-bit mask of LIVE in-edge slots inside [a, b). No memory is touched.
+template <int SCHEME>
+__device__ __forceinline__ uint32_t ic_live_mask(const RRParams& p, uint32_t id_lo, uint32_t id_hi,
+                                                 uint32_t k0, uint32_t k1, uint32_t g, uint32_t a,
+                                                 uint32_t b, uint32_t thr) {
+  const uint4 w = philox4x32_10_rk(make_uint4(id_lo, id_hi, g, 0u), p.rk);
+  const uint32_t e0 = g << 2;
+  uint32_t m;
+  if (SCHEME == W_EXPLICIT) {
+    m = 0;
+    const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (e0 + j >= a && e0 + j < b && (uint64_t)words[j] < p.thr_edge[e0 + j]) m |= 1u << j;
+    return m;
+  }
+  // WC: coin <= floor((2^32-1)/d)  <=>  coin * d < 2^32;  UNIFORM: coin <= ceil(p 2^32) - 1
+  m = (uint32_t)(w.x <= thr) | ((uint32_t)(w.y <= thr) << 1) | ((uint32_t)(w.z <= thr) << 2) |
+      ((uint32_t)(w.w <= thr) << 3);
+  const uint32_t lo = a > e0 ? a - e0 : 0u;          // first valid word (group g_lo)
+  const uint32_t hi = (b - e0) < 4u ? b - e0 : 4u;   // one past the last valid word (group g_hi)
+  return m & (0xFu << lo) & (0xFu >> (4u - hi));
+}
+
+// Slow path (some lane of the warp has a live slot): load src[e] for live slots only and
+// test-and-set them in the visited structure; uu[j] = newly visited node or kEmpty.
+template <class Visit>
+__device__ __forceinline__ void ic_take_live(const RRParams& p, uint32_t g, uint32_t m,
+                                             uint32_t (&uu)[4], Visit visit) {
   const uint32_t e0 = g << 2;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t e = e0 + j;
-    if (e >= a && e < b) {
-      ++coins;
-      if (ic_live<SCHEME>(words[j], thr_wc, p.thr_uniform, p.thr_edge, e)) {
-        ++lives;
-        const uint32_t u = __ldg(p.src + e);
-        if (visit(u)) uu[j] = u;
-      }
+    if (m & (1u << j)) {
+      const uint32_t u = __ldg(p.src + e0 + j);
+      if (visit(u)) uu[j] = u;
     }
   }
+}
+
+// Per-node live threshold of the 32-bit fast test (WC and UNIFORM).
+template <int SCHEME>
+__device__ __forceinline__ uint32_t node_thr(const RRParams& p, uint32_t d) {
+  if (SCHEME == W_WC) return 0xFFFFFFFFu / d;
+  if (SCHEME == W_UNIFORM) return p.thr_uniform ? (uint32_t)(p.thr_uniform - 1) : 0u;
+  return 0u;
 }
 
 // Warp-inclusive scan of the number of new nodes per lane; returns (exclusive offset, total).
@@ -107,11 +121,31 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t cnt, int lane, uint3
   return incl - cnt;
 }
 
+
+// Slow path of the warp kernel: load src[e] for this lane's live slots of group g, test-and-set
+// them in the smem visited hash and append the new nodes to the queue (warp-collective).
+// Returns false (nothing appended) if the queue would overflow.
+template <class Visit>
+__device__ __forceinline__ bool append_live(const RRParams& p, uint32_t g, uint32_t m, uint32_t* q,
+                                            uint32_t& tail, int lane, Visit vis) {
+  uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
+  if (m) ic_take_live(p, g, m, uu, vis);
+  const uint32_t cnt = (uu[0] != kEmpty) + (uu[1] != kEmpty) + (uu[2] != kEmpty) + (uu[3] != kEmpty);
+  uint32_t total;
+  uint32_t pos = tail + warp_excl_scan(cnt, lane, total);
+  if (tail + total > p.qcap) return false;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (uu[j] != kEmpty) q[pos++] = uu[j];
+  tail += total;
+  return true;
+}
+
 // ------------------------------------------------------------------------------------------
 // K-RR: warp-per-RR persistent kernel.
 // ------------------------------------------------------------------------------------------
 template <int MODEL, int SCHEME>
-__global__ void __launch_bounds__(kRRWarps * 32) k_rr_warp(RRParams p) {
+__global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRParams p) {
   extern __shared__ uint32_t smem[];
   const int lane = threadIdx.x & 31;
   uint32_t* q = smem + (threadIdx.x >> 5) * (kQMax + kHSize);
@@ -119,7 +153,7 @@ __global__ void __launch_bounds__(kRRWarps * 32) k_rr_warp(RRParams p) {
   for (int i = lane; i < kHSize; i += 32) h[i] = kEmpty;
   __syncwarp();
   const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
-  unsigned long long coins = 0, lives = 0;
+  uint32_t coins = 0, lives = 0;    // 32-bit per-warp counters, flushed before they can wrap
 
   while (true) {
     uint32_t i = 0;
@@ -139,31 +173,93 @@ __global__ void __launch_bounds__(kRRWarps * 32) k_rr_warp(RRParams p) {
       h[hash_slot(root)] = root;     // table is empty here
     }
     __syncwarp();
-    uint32_t head = 0, tail = 1;
+    uint32_t head = 0, tail = 1, resume = 0;
     bool overflow = false;
-    while (head < tail) {
-      const uint32_t v = q[head++];
-      const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
-      if (b <= a) continue;
-      if (MODEL == MODEL_IC) {
-        const uint32_t thr_wc = (SCHEME == W_WC) ? 0xFFFFFFFFu / (b - a) : 0u;
-        const uint32_t g_lo = a >> 2, g_hi = (b - 1) >> 2;
-        for (uint32_t gb = g_lo; gb <= g_hi; gb += 32) {
-          const uint32_t g = gb + lane;
-          uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
-          if (g <= g_hi)
-            ic_group<SCHEME>(p, id_lo, id_hi, k0, k1, g, a, b, thr_wc, uu, coins, lives,
-                             [h](uint32_t u) { return hash_insert(h, u); });
-          const uint32_t cnt = (uu[0] != kEmpty) + (uu[1] != kEmpty) + (uu[2] != kEmpty) + (uu[3] != kEmpty);
-          uint32_t total;
-          uint32_t pos = tail + warp_excl_scan(cnt, lane, total);
-          if (tail + total > p.qcap) { overflow = true; break; }
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (uu[j] != kEmpty) q[pos++] = uu[j];
-          tail += total;
+    if (MODEL == MODEL_IC) {
+      const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
+      auto vis = [h](uint32_t u) { return hash_insert(h, u); };
+      // Expand every pending frontier node of this RR set together: lane i holds node
+      // q[head + i] of the batch (row range, live threshold, group count), the warp sweeps the
+      // concatenation of their slot-group ranges 32 groups at a time, and live in-edges found
+      // anywhere in a sweep step are appended in one warp-wide step.
+      while (head < tail) {
+        const uint32_t nb = min(tail - head, 32u);
+        uint32_t a = 0, b = 0, thr = 0, ng = 0;
+        if (lane < nb) {
+          const uint32_t v = q[head + lane];
+          a = __ldg(p.row_ptr + v);
+          b = __ldg(p.row_ptr + v + 1);
+          if (b > a) {
+            ng = ((b - 1) >> 2) - (a >> 2) + 1;
+            thr = node_thr<SCHEME>(p, b - a);
+          }
         }
-      } else {  // LT: frontier <= 1
+        if (coins >= 0x80000000u) { atomicAdd(&p.ctr->coins, (unsigned long long)coins); coins = 0; }
+        coins += b - a;
+        resume = head;                                  // batch start: re-expanded on overflow
+        head += nb;
+        // hubs (>= kHubGroups slot groups) are swept alone below; the rest are flattened here
+        const uint32_t hubs = __ballot_sync(kFull, ng >= kHubGroups);
+        const uint32_t ngf = (ng >= kHubGroups) ? 0u : ng;
+        uint32_t total_g;
+        const uint32_t E = warp_excl_scan(ngf, lane, total_g);   // exclusive group prefix
+        const uint32_t P = E + ngf;
+        for (uint32_t base = 0; base < total_g; base += 32) {
+          const uint32_t gi = base + lane;
+          uint32_t k = 0;                               // node of flattened group gi
+          if (nb > 1) {
+#pragma unroll
+            for (uint32_t step = 16; step >= 1; step >>= 1) {
+              const uint32_t pv = __shfl_sync(kFull, P, k + step - 1);
+              if (pv <= gi) k += step;
+            }
+          }
+          const uint32_t ak = __shfl_sync(kFull, a, k), bk = __shfl_sync(kFull, b, k);
+          const uint32_t tk = __shfl_sync(kFull, thr, k), ek = __shfl_sync(kFull, E, k);
+          const uint32_t g = (ak >> 2) + (gi - ek);
+          uint32_t m = 0;
+          if (gi < total_g && !never) m = ic_live_mask<SCHEME>(p, id_lo, id_hi, k0, k1, g, ak, bk, tk);
+          if (!__any_sync(kFull, m)) continue;          // no live in-edge in these 128 slots
+          lives += __popc(m);
+          if (!append_live(p, g, m, q, tail, lane, vis)) { overflow = true; break; }
+        }
+        // hub sweep: kHubIlp independent Philox chains per lane, 128 x kHubIlp slots per step
+        for (uint32_t hm = overflow ? 0u : hubs; hm; hm &= hm - 1) {
+          const uint32_t k = __ffs(hm) - 1;
+          const uint32_t ak = __shfl_sync(kFull, a, k), bk = __shfl_sync(kFull, b, k);
+          const uint32_t tk = __shfl_sync(kFull, thr, k);
+          const uint32_t g_lo = ak >> 2, g_hi = (bk - 1) >> 2;
+          for (uint32_t gb = g_lo; gb <= g_hi && !overflow; gb += kHubGroups) {
+            uint32_t m[kHubIlp];
+#pragma unroll
+            for (int r = 0; r < kHubIlp; ++r) {
+              const uint32_t g = gb + 32u * r + lane;
+              m[r] = (g <= g_hi && !never) ? ic_live_mask<SCHEME>(p, id_lo, id_hi, k0, k1, g, ak, bk, tk) : 0u;
+            }
+            uint32_t any = 0;
+#pragma unroll
+            for (int r = 0; r < kHubIlp; ++r) any |= m[r];
+            if (!__any_sync(kFull, any)) continue;
+#pragma unroll 1
+            for (int r = 0; r < kHubIlp; ++r) {
+              uint32_t mr = 0;
+#pragma unroll
+              for (int t = 0; t < kHubIlp; ++t) mr = (t == r) ? m[t] : mr;
+              if (!__any_sync(kFull, mr)) continue;
+              lives += __popc(mr);
+              if (!append_live(p, gb + 32u * r + lane, mr, q, tail, lane, vis)) { overflow = true; break; }
+            }
+          }
+        }
+        __syncwarp();
+        if (overflow) break;
+      }
+    } else {  // LT: frontier <= 1
+      while (head < tail) {
+        const uint32_t v = q[head++];
+        const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
+        if (b <= a) continue;
+        resume = head - 1;
         const uint32_t d = b - a;
         const uint32_t j = lt_choose<SCHEME>(p, id, v, a, d, lane);
         if (lane == 0) { coins += 1; lives += (j < d); }
@@ -183,13 +279,14 @@ __global__ void __launch_bounds__(kRRWarps * 32) k_rr_warp(RRParams p) {
             }
           }
         }
+        __syncwarp();
+        if (overflow) break;
       }
-      __syncwarp();
-      if (overflow) break;
     }
     if (overflow) {
-      // hand the partial BFS to the giant kernel: q[0..tail) are visited, q[0..head-1) fully
-      // expanded; the node being expanded (q[head-1]) is re-expanded there (same coins).
+      // hand the partial BFS to the giant kernel: q[0..tail) are visited and q[0..resume) are
+      // fully expanded; the batch being expanded (q[resume..]) is re-expanded there with the
+      // same coins, so the continuation is exact.
       unsigned long long off = 0;
       if (lane == 0) off = atomicAdd(&p.ctr->dump_tail, (unsigned long long)tail);
       off = __shfl_sync(kFull, off, 0);
@@ -198,7 +295,7 @@ __global__ void __launch_bounds__(kRRWarps * 32) k_rr_warp(RRParams p) {
         for (uint32_t t = lane; t < tail; t += 32) p.dump[off + t] = q[t];
       if (lane == 0)
         p.giant_recs[atomicAdd(&p.ctr->giant_count, 1u)] =
-            fits ? GiantRec{item, tail, head - 1, 0u, off} : GiantRec{item, 0u, 0u, 0u, 0ull};
+            fits ? GiantRec{item, tail, resume, 0u, off} : GiantRec{item, 0u, 0u, 0u, 0ull};
     } else {
       unsigned long long off = 0;
       if (lane == 0) off = atomicAdd(&p.ctr->stage_tail, (unsigned long long)tail);
@@ -216,14 +313,15 @@ __global__ void __launch_bounds__(kRRWarps * 32) k_rr_warp(RRParams p) {
     __syncwarp();
   }
   // per-warp statistics
+  unsigned long long c64 = coins, l64 = lives;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    coins += __shfl_xor_sync(kFull, coins, off);
-    lives += __shfl_xor_sync(kFull, lives, off);
+    c64 += __shfl_xor_sync(kFull, c64, off);
+    l64 += __shfl_xor_sync(kFull, l64, off);
   }
   if (lane == 0) {
-    atomicAdd(&p.ctr->coins, coins);
-    atomicAdd(&p.ctr->live, lives);
+    atomicAdd(&p.ctr->coins, c64);
+    atomicAdd(&p.ctr->live, l64);
   }
 }
 
@@ -345,11 +443,17 @@ __global__ void __launch_bounds__(kGiantThreads) k_rr_giant(RRParams p, uint32_t
           const uint32_t cin = c - (f ? s_cp[f - 1] : 0u);
           const uint32_t a = s_a[f], b = s_b[f];
           if (MODEL == MODEL_IC) {
-            const uint32_t thr_wc = (SCHEME == W_WC) ? 0xFFFFFFFFu / (b - a) : 0u;
+            const uint32_t thr = node_thr<SCHEME>(p, b - a);
+            const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
             const uint32_t g_hi = (b - 1) >> 2;
             const uint32_t g = (a >> 2) + (cin << 5) + lane;
+            if (lane == 0) coins += min(b, (g - lane + 32) << 2) - max(a, (g - lane) << 2);
+            uint32_t m = 0;
+            if (g <= g_hi && !never) m = ic_live_mask<SCHEME>(p, id_lo, id_hi, k0, k1, g, a, b, thr);
+            if (!__any_sync(kFull, m)) continue;
+            lives += __popc(m);
             uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
-            if (g <= g_hi) ic_group<SCHEME>(p, id_lo, id_hi, k0, k1, g, a, b, thr_wc, uu, coins, lives, visit);
+            ic_take_live(p, g, m, uu, visit);
             const uint32_t cnt = (uu[0] != kEmpty) + (uu[1] != kEmpty) + (uu[2] != kEmpty) + (uu[3] != kEmpty);
             uint32_t tot;
             const uint32_t excl = warp_excl_scan(cnt, lane, tot);

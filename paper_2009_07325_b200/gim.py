@@ -238,14 +238,20 @@ class Gim:
         return ms.value
 
 
-def torch_allreduce(group=None):
-    """all-reduce callback for Gim.set_allreduce: wraps the library's int32 device buffer as a
-    torch tensor (``__cuda_array_interface__``) and runs torch.distributed.all_reduce (SUM) on
-    the library's stream (NCCL over NVLink when the group's backend is nccl)."""
+def torch_allreduce(group=None, device: str = "cuda"):
+    """all-reduce callback for Gim.set_allreduce: wraps the library's int32 buffer as a torch
+    tensor and runs torch.distributed.all_reduce (SUM) ordered on the library's stream (NCCL over
+    NVLink when the group's backend is nccl). device="cpu" wraps a host pointer instead (used by
+    the multi-process gloo tests of this plumbing)."""
     import torch
     import torch.distributed as dist
 
     def fn(ptr: int, count: int, stream: int) -> int:
+        if device == "cpu":
+            arr = np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_int32)), shape=(int(count),))
+            dist.all_reduce(torch.from_numpy(arr), op=dist.ReduceOp.SUM, group=group)
+            return 0
+
         class _View:
             __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<i4",
                                         "data": (int(ptr), False), "version": 3, "strides": None,
@@ -257,3 +263,9 @@ def torch_allreduce(group=None):
         return 0
 
     return fn
+
+
+def shard_slice(a: int, b: int, rank: int, world: int):
+    """This rank's contiguous slice of RR ids [a, b) (include/gim.h gim_set_shard)."""
+    ln = b - a
+    return a + ln * rank // world, a + ln * (rank + 1) // world

@@ -1,0 +1,123 @@
+"""Multi-process (world_size 2 and 3, gloo on CPU) tests of the N > 1 host logic: the all-reduce
+callback plumbing of the binding, the RR-id slicing, and the sharded NodeSelection protocol the
+library runs per greedy step (count all-reduce once, then decrement all-reduce per step) —
+executed here on oracle pools split by rank, which must reproduce the single-process selection."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import gim_inputs as gi
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _init(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _worker_callback(rank, world, port, q):
+    _init(rank, world, port)
+    import paper_2009_07325_b200 as P
+    fn = P.torch_allreduce(device="cpu")
+    buf = np.arange(10, dtype=np.int32) * (rank + 1)
+    rc = fn(buf.ctypes.data, len(buf), 0)
+    q.put((rank, rc, buf.tolist()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_allreduce_callback_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker_callback, args=(r, world, port, q)) for r in range(world)]
+    [p.start() for p in procs]
+    out = [q.get(timeout=120) for _ in range(world)]
+    [p.join(60) for p in procs]
+    tot = sum(range(1, world + 1))
+    for rank, rc, buf in out:
+        assert rc == 0 and buf == [i * tot for i in range(10)]
+
+
+def test_shard_slices_partition():
+    from paper_2009_07325_b200 import shard_slice
+    for a, b in [(0, 10), (5, 6), (100, 1000003), (7, 7)]:
+        for world in (1, 2, 3, 8):
+            parts = [shard_slice(a, b, r, world) for r in range(world)]
+            assert parts[0][0] == a and parts[-1][1] == b
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(world - 1))
+
+
+def _sharded_select(rank, world, port, q, key, T, k):
+    """The library's P > 1 selection protocol, on the oracle pool slices of this rank."""
+    _init(rank, world, port)
+    import oracle
+    from paper_2009_07325_b200 import shard_slice
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    o = oracle.Oracle(g, w.model, w.scheme)
+    o.generate(T, w.rr_seed)
+    off, nodes, _ = o.export()
+    lo, hi = shard_slice(0, T, rank, world)
+    sets = [nodes[off[i]:off[i + 1]] for i in range(lo, hi)]
+    local = np.zeros(g.n, dtype=np.int64)
+    for s in sets:
+        local[s] += 1
+    cnt = torch.from_numpy(local.copy())
+    dist.all_reduce(cnt)                                   # count: once per selection
+    cnt = cnt.numpy()
+    inv = {}
+    for r, s in enumerate(sets):
+        for v in s:
+            inv.setdefault(int(v), []).append(r)
+    covered = np.zeros(len(sets), dtype=bool)
+    selected = np.zeros(g.n, dtype=bool)
+    seeds, gains = [], []
+    for _ in range(k):
+        key_ = np.where(selected, -1, cnt)
+        u = int(np.argmax(key_))                           # lowest id among maxima
+        seeds.append(u)
+        gains.append(int(cnt[u]))
+        selected[u] = True
+        dec = np.zeros(g.n, dtype=np.int64)
+        for r in inv.get(u, []):
+            if not covered[r]:
+                covered[r] = True
+                dec[sets[r]] += 1
+        d = torch.from_numpy(dec)
+        dist.all_reduce(d)                                  # decrement: once per step
+        cnt = cnt - d.numpy()
+    q.put((rank, seeds, gains))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_selection_protocol_equals_single(world):
+    import oracle
+    key, T, k = "C1", 20000, 20
+    w = gi.WORKLOADS[key]
+    o = oracle.Oracle(gi.workload_graph(key), w.model, w.scheme)
+    o.generate(T, w.rr_seed)
+    rs, rg, _ = o.select(k)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_sharded_select, args=(r, world, port, q, key, T, k)) for r in range(world)]
+    [p.start() for p in procs]
+    out = [q.get(timeout=300) for _ in range(world)]
+    [p.join(60) for p in procs]
+    for rank, seeds, gains in out:
+        assert seeds == rs.tolist() and gains == rg.tolist()

@@ -211,7 +211,11 @@ def run_gim(args, w):
     clk = Clocks(local) if rank == 0 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    results = [ctx.imm(w.k, w.eps, w.ell, w.rr_seed) for _ in range(args.steps)]
+    results, step_wall = [], []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        results.append(ctx.imm(w.k, w.eps, w.ell, w.rr_seed))
+        step_wall.append(1000 * (time.perf_counter() - t0))
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -318,6 +322,11 @@ def run_gim(args, w):
                              "coins_per_set": (st["coins"] + st["coins_giant"]) / max(st["rr_sets"], 1),
                              "giant_frac": st["giant_sets"] / max(st["rr_sets"], 1)},
                 "gpu_launches": st["launches"],
+                "step_wall_ms": [round(x, 3) for x in step_wall],
+                "host": {"api_ms_per_step": st["host_ms_api"] / args.steps,
+                         "sync_ms_per_step": st["host_ms_sync"] / args.steps,
+                         "syncs_per_step": st["n_syncs"] / args.steps,
+                         "allocs_in_timed_region": st["n_allocs"]},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "seeds_head": r0.seeds[:8].tolist()}
         print(json.dumps(line), flush=True)

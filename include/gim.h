@@ -141,17 +141,22 @@ gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
  *  GIM_OPT_QUEUE_CAP    = Q: shared-memory queue capacity per RR (power of two, 32..1024);
  *                          sets larger than Q are replayed by the giant kernel.
  *  GIM_OPT_PROFILE      = 1: time every kernel class with CUDA events (see gim_get_stats).
- *  GIM_OPT_STAGING_CAP  = elements of staging memory to start from (forces retries if tiny). */
+ *  GIM_OPT_STAGING_CAP  = elements of staging memory to start from (forces retries if tiny).
+ *  GIM_OPT_SELECT_STEPS = 1 (default): one argmax + one cover launch per greedy step;
+ *                          0: P = 1 selections run all k steps in one cooperative persistent
+ *                          kernel with grid-wide barriers (ablation; slower on C3). */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
   GIM_OPT_PROFILE = 3,
-  GIM_OPT_STAGING_CAP = 4
+  GIM_OPT_STAGING_CAP = 4,
+  GIM_OPT_SELECT_STEPS = 5
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 
 /* Counters since the last gim_reset_stats. Kernel times (ms, CUDA events on the ctx stream)
- * are only collected with GIM_OPT_PROFILE = 1. */
+ * are only collected with GIM_OPT_PROFILE = 1. gim_imm time counts once (its inner
+ * generate/select calls are internal). */
 typedef struct {
   uint64_t launches;          /* kernels launched by the library                      */
   uint64_t rr_sets;           /* RR sets generated (local)                             */
@@ -165,6 +170,9 @@ typedef struct {
   uint64_t allreduces;        /* all-reduce callback invocations                       */
   double ms_rr, ms_giant, ms_store, ms_inv, ms_select; /* kernel time per class        */
   uint64_t n_rr_launches, n_giant_launches;
+  uint64_t n_syncs, n_allocs;   /* host<->device syncs, device allocations                */
+  double host_ms_sync;          /* host wall time blocked in stream synchronisation       */
+  double host_ms_api;           /* host wall time inside gim_generate_rr/select/imm       */
 } gim_stats;
 gim_status gim_get_stats(gim_ctx* ctx, gim_stats* out);
 gim_status gim_reset_stats(gim_ctx* ctx);

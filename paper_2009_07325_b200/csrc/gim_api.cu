@@ -2,6 +2,7 @@
 // libgim (declared in include/gim.h). Host code is compiled with -ffp-contract=off so that the
 // IMM doubles follow the evaluation order fixed in DESIGN.md (reading R21).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -29,6 +30,9 @@ struct Seg {
 enum { CLS_RR = 0, CLS_GIANT, CLS_STORE, CLS_INV, CLS_SELECT, CLS_N };
 
 constexpr uint32_t kChunk = 1u << 22;   // RR ids per generation chunk (bounds staging)
+#ifndef GIM_DEFAULT_SELECT_STEPS
+#define GIM_DEFAULT_SELECT_STEPS 1
+#endif
 
 }  // namespace
 
@@ -66,13 +70,14 @@ struct gim_ctx {
   GenCounters* h_ctr = nullptr;   // pinned
   uint64_t* h_u64 = nullptr;      // pinned scratch
   // selection scratch
-  DevBuf cnt, inv_off, cursor, inv, covered, keys, dec;
+  DevBuf cnt, inv_off, cursor, inv, covered, keys, dec, bound;
   // options
-  int force_giant = 0, profile = 0;
+  int force_giant = 0, profile = 0, select_steps = GIM_DEFAULT_SELECT_STEPS;
   uint32_t qcap = kQMax;
   uint64_t staging_init = 0;
   gim_stats st{};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[CLS_N];
+  std::vector<cudaEvent_t> ev_free;   // recycled timing events
 };
 
 namespace {
@@ -134,6 +139,7 @@ gim_status dalloc(gim_ctx* c, DevBuf& b, uint64_t bytes) {
   }
   b.p = p;
   b.bytes = bytes;
+  c->st.n_allocs++;
   return GIM_OK;
 }
 
@@ -159,10 +165,20 @@ struct Prof {
   gim_ctx* c;
   int cls;
   cudaEvent_t a = nullptr, b = nullptr;
+  static cudaEvent_t take(gim_ctx* c) {
+    cudaEvent_t e = nullptr;
+    if (!c->ev_free.empty()) {
+      e = c->ev_free.back();
+      c->ev_free.pop_back();
+    } else {
+      cudaEventCreate(&e);
+    }
+    return e;
+  }
   Prof(gim_ctx* c_, int cls_) : c(c_), cls(cls_) {
     if (c->profile) {
-      cudaEventCreate(&a);
-      cudaEventCreate(&b);
+      a = take(c);
+      b = take(c);
       cudaEventRecord(a, c->stream);
     }
   }
@@ -174,15 +190,23 @@ struct Prof {
   }
 };
 
+double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 gim_status sync(gim_ctx* c) {
-  CK(cudaStreamSynchronize(c->stream));
+  const double t0 = now_ms();
+  const cudaError_t se = cudaStreamSynchronize(c->stream);
+  c->st.host_ms_sync += now_ms() - t0;
+  c->st.n_syncs++;
+  CK(se);
   double* acc[CLS_N] = {&c->st.ms_rr, &c->st.ms_giant, &c->st.ms_store, &c->st.ms_inv, &c->st.ms_select};
   for (int k = 0; k < CLS_N; ++k) {
     for (auto& pr : c->ev[k]) {
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) *acc[k] += ms;
-      cudaEventDestroy(pr.first);
-      cudaEventDestroy(pr.second);
+      c->ev_free.push_back(pr.first);
+      c->ev_free.push_back(pr.second);
     }
     c->ev[k].clear();
   }
@@ -217,7 +241,7 @@ gim_status ensure_giant_slots(gim_ctx* c, uint32_t want) {
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   uint64_t cap = std::max<uint64_t>(1, (uint64_t)(free_b / 8) / std::max<uint64_t>(per_slot, 1));
-  uint32_t slots = (uint32_t)std::min<uint64_t>({(uint64_t)want, (uint64_t)2 * c->num_sms, cap});
+  uint32_t slots = (uint32_t)std::min<uint64_t>({(uint64_t)want, cap});
   if (slots <= c->giant_slots) return GIM_OK;
   TRY(dalloc(c, c->bitmaps, words * 4 * slots));
   CK(cudaMemsetAsync(c->bitmaps.p, 0, words * 4 * slots, c->stream));
@@ -289,31 +313,41 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   p.id_base = gstart;
   p.count = cnt;
   p.item_list = nullptr;
-  const int rr_grid = c->num_sms * kRRBlocksPerSM;   // persistent: 6 CTAs x 8 warps per SM
-  {
-    Prof pf(c, CLS_RR);
-    TRY(launched(c, launch_rr_warp(c->model, c->scheme, p, rr_grid, c->stream), "k_rr_warp"));
-    c->st.n_rr_launches++;
-  }
-  TRY(read_ctr(c));
-  for (int iter = 0;; ++iter) {
-    const uint32_t giants = c->h_ctr->giant_count;
-    if (giants) {
-      TRY(ensure_giant_slots(c, giants));
-      {
-        Prof pf(c, CLS_GIANT);
-        TRY(launched(c, launch_rr_giant(c->model, c->scheme, p, (int)std::min(giants, c->giant_slots),
-                                        c->bitmaps.as<uint32_t>(), c->gqueues.as<uint32_t>(),
-                                        ((uint64_t)c->n + 31) / 32, c->stream), "k_rr_giant"));
-        c->st.n_giant_launches++;
-      }
-      c->st.giant_sets += giants;
-      TRY(read_ctr(c));
+  const int rr_grid = c->num_sms * kRRBlocksPerSM;   // persistent CTAs, 8 warps each
+  TRY(ensure_giant_slots(c, 2u * (uint32_t)c->num_sms));
+  const uint64_t bm_words = ((uint64_t)c->n + 31) / 32;
+  // warp kernel, then the giant kernel unconditionally (it reads the giant count on the device
+  // and exits at once when there is none), then the size scan: one host sync per chunk.
+  auto run_pass = [&](const RRParams& pp) -> gim_status {
+    {
+      Prof pf(c, CLS_RR);
+      TRY(launched(c, launch_rr_warp(c->model, c->scheme, pp, rr_grid, c->stream), "k_rr_warp"));
+      c->st.n_rr_launches++;
     }
-    const uint32_t retries = c->h_ctr->retry_count;
-    if (!retries) break;
+    {
+      Prof pf(c, CLS_GIANT);
+      TRY(launched(c, launch_rr_giant(c->model, c->scheme, pp, (int)c->giant_slots, c->bitmaps.as<uint32_t>(),
+                                      c->gqueues.as<uint32_t>(), bm_words, c->stream), "k_rr_giant"));
+      c->st.n_giant_launches++;
+    }
+    return GIM_OK;
+  };
+  TRY(run_pass(p));
+  {
+    Prof pf(c, CLS_STORE);
+    int nl = 0;
+    cudaError_t e = launch_scan_u32(c->sizes.as<uint32_t>(), cnt, c->scan_out.as<uint64_t>(),
+                                    c->scan_tmp.as<uint64_t>(), c->scan_tmp.as<uint64_t>() + scan_tiles(cnt) + 1,
+                                    c->stream, &nl);
+    TRY(launched(c, e, "scan(sizes)", nl));
+  }
+  CK(cudaMemcpyAsync(c->h_u64, c->scan_out.as<uint64_t>() + cnt, 8, cudaMemcpyDeviceToHost, c->stream));
+  TRY(read_ctr(c));
+  c->st.giant_sets += c->h_ctr->giant_count;
+  for (int iter = 0; c->h_ctr->retry_count; ++iter) {
     if (iter > 40) return fail(c, GIM_ENOMEM, "staging retry loop did not converge");
-    // staging overflow: grow (keep the part already written) and replay the failed items
+    // staging overflow: grow (keep the part already written) and redo the failed items
+    const uint32_t retries = c->h_ctr->retry_count;
     const uint64_t old_cap = c->stage_cap;
     TRY(grow_keep(c, c->staging, old_cap * 4 * 2, old_cap * 4));
     c->stage_cap = c->staging.bytes / 4;
@@ -324,32 +358,29 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     h.dump_tail = 0;
     *c->h_ctr = h;
     CK(cudaMemcpyAsync(c->ctr.p, c->h_ctr, sizeof(GenCounters), cudaMemcpyHostToDevice, c->stream));
-    p = base_params(c);
-    p.id_base = gstart;
-    p.count = retries;
-    p.item_list = c->item_list.as<uint32_t>();
-    {
-      Prof pf(c, CLS_RR);
-      TRY(launched(c, launch_rr_warp(c->model, c->scheme, p, rr_grid, c->stream), "k_rr_warp(retry)"));
-      c->st.n_rr_launches++;
-    }
+    RRParams pr = base_params(c);
+    pr.id_base = gstart;
+    pr.count = retries;
+    pr.item_list = c->item_list.as<uint32_t>();
+    TRY(run_pass(pr));
     TRY(read_ctr(c));
+    c->st.giant_sets += c->h_ctr->giant_count;
+    if (!c->h_ctr->retry_count) {             // sizes complete: redo the scan
+      Prof pf(c, CLS_STORE);
+      int nl = 0;
+      cudaError_t e = launch_scan_u32(c->sizes.as<uint32_t>(), cnt, c->scan_out.as<uint64_t>(),
+                                      c->scan_tmp.as<uint64_t>(), c->scan_tmp.as<uint64_t>() + scan_tiles(cnt) + 1,
+                                      c->stream, &nl);
+      TRY(launched(c, e, "scan(sizes)", nl));
+      CK(cudaMemcpyAsync(c->h_u64, c->scan_out.as<uint64_t>() + cnt, 8, cudaMemcpyDeviceToHost, c->stream));
+      TRY(sync(c));
+    }
   }
   c->st.coins += c->h_ctr->coins;
   c->st.live_edges += c->h_ctr->live;
   c->st.coins_giant += c->h_ctr->coins_giant;
   c->st.live_giant += c->h_ctr->live_giant;
-  // two-pass storage: exclusive scan of sizes, then compacting copy + count_total
-  {
-    Prof pf(c, CLS_STORE);
-    int nl = 0;
-    cudaError_t e = launch_scan_u32(c->sizes.as<uint32_t>(), cnt, c->scan_out.as<uint64_t>(),
-                                    c->scan_tmp.as<uint64_t>(), c->scan_tmp.as<uint64_t>() + scan_tiles(cnt) + 1,
-                                    c->stream, &nl);
-    TRY(launched(c, e, "scan(sizes)", nl));
-  }
-  CK(cudaMemcpyAsync(c->h_u64, c->scan_out.as<uint64_t>() + cnt, 8, cudaMemcpyDeviceToHost, c->stream));
-  TRY(sync(c));
+  // two-pass storage: sizes were scanned above; compacting copy + count_total
   const uint64_t total = c->h_u64[0];
   TRY(grow_keep(c, c->pool, (c->pool_len + total) * 4, c->pool_len * 4));
   TRY(grow_keep(c, c->offsets, (c->nsets + cnt + 1) * 8, (c->nsets + 1) * 8));
@@ -445,18 +476,27 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
     if (c->arfn(c->cnt.p, n, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(count) failed");
   }
   auto* keys = reinterpret_cast<unsigned long long*>(c->keys.p);
-  for (uint32_t j = 0; j < k; ++j) {
-    {
-      Prof pf(c, CLS_SELECT);
-      TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, c->n, keys, (int)j, c->num_sms * 4, c->stream),
-                   "k_argmax"));
-      TRY(launched(c, launch_cover(keys, (int)j, c->inv_off.as<uint64_t>(), c->inv.as<uint32_t>(),
-                                   c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), c->covered.as<uint8_t>(),
-                                   c->cnt.as<uint32_t>(), dec, c->num_sms * 8, c->stream), "k_cover"));
-    }
-    if (dec && j + 1 < k) {
-      c->st.allreduces++;
-      if (c->arfn(dec, n, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(dec) failed");
+  if (!dec && !c->select_steps) {
+    // P = 1: all k steps on-device in one cooperative persistent kernel
+    Prof pf(c, CLS_SELECT);
+    TRY(launched(c, launch_select_coop(c->cnt.as<uint32_t>(), c->n, c->inv_off.as<uint64_t>(), c->inv.as<uint32_t>(),
+                                       c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), c->covered.as<uint8_t>(),
+                                       keys, (int)k, c->num_sms, c->stream),
+                 "k_select_coop"));
+  } else {
+    for (uint32_t j = 0; j < k; ++j) {
+      {
+        Prof pf(c, CLS_SELECT);
+        TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, c->n, keys, (int)j, c->num_sms * 4, c->stream),
+                     "k_argmax"));
+        TRY(launched(c, launch_cover(keys, (int)j, c->inv_off.as<uint64_t>(), c->inv.as<uint32_t>(),
+                                     c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), c->covered.as<uint8_t>(),
+                                     c->cnt.as<uint32_t>(), dec, c->num_sms * 8, c->stream), "k_cover"));
+      }
+      if (dec && j + 1 < k) {
+        c->st.allreduces++;
+        if (c->arfn(dec, n, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(dec) failed");
+      }
     }
   }
   std::vector<unsigned long long> hk(k);
@@ -547,7 +587,7 @@ void gim_destroy(gim_ctx* c) {
   DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
                     &c->sizes, &c->soff, &c->giant_list, &c->retry_list, &c->item_list, &c->scan_out,
                     &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->bitmaps, &c->gqueues, &c->cnt, &c->inv_off,
-                    &c->cursor, &c->inv, &c->covered, &c->keys, &c->dec};
+                    &c->cursor, &c->inv, &c->covered, &c->keys, &c->dec, &c->bound};
   for (DevBuf* b : bufs) dfree(c, *b);
   cudaStreamSynchronize(c->stream);
   for (auto& v : c->ev)
@@ -555,6 +595,7 @@ void gim_destroy(gim_ctx* c) {
       cudaEventDestroy(pr.first);
       cudaEventDestroy(pr.second);
     }
+  for (cudaEvent_t e : c->ev_free) cudaEventDestroy(e);
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
   if (c->h_u64) cudaFreeHost(c->h_u64);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -671,7 +712,10 @@ gim_status gim_generate_rr(gim_ctx* c, uint64_t theta, uint64_t seed) {
   if (!c) return GIM_EINVAL;
   c->err.clear();
   DeviceGuard g(c->device);
-  return generate(c, theta, seed);
+  const double t0 = now_ms();
+  const gim_status s = generate(c, theta, seed);
+  c->st.host_ms_api += now_ms() - t0;
+  return s;
 }
 
 gim_status gim_select(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains, uint64_t* covered) {
@@ -679,7 +723,10 @@ gim_status gim_select(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains, 
   c->err.clear();
   if (!seeds) return fail(c, GIM_EINVAL, "seeds_out required");
   DeviceGuard g(c->device);
-  return select_impl(c, k, seeds, gains, covered);
+  const double t0 = now_ms();
+  const gim_status s = select_impl(c, k, seeds, gains, covered);
+  c->st.host_ms_api += now_ms() - t0;
+  return s;
 }
 
 gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed, uint32_t* seeds,
@@ -693,6 +740,7 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
   if (!(eps > 0.0 && eps < 1.0)) return fail(c, GIM_EINVAL, "eps must be in (0,1)");
   if (!(ell > 0.0)) return fail(c, GIM_EINVAL, "ell must be > 0");
   DeviceGuard g(c->device);
+  const double t_api = now_ms();
   const ImmConst K = imm_constants(c->n, k, eps, ell);
   gim_imm_result r;
   std::memset(&r, 0, sizeof(r));
@@ -733,6 +781,7 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
   r.covered = cov;
   r.spread_est = n * (double)cov / (double)c->T_global;     // Eq. 3
   if (res) *res = r;
+  c->st.host_ms_api += now_ms() - t_api;
   return GIM_OK;
 }
 
@@ -779,10 +828,11 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
   switch (opt) {
     case GIM_OPT_FORCE_GIANT: c->force_giant = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_QUEUE_CAP:
-      if (value < 1 || value > kQMax) return fail(c, GIM_EINVAL, "queue cap must be in [1, 384]");
+      if (value < 1 || value > kQMax) return fail(c, GIM_EINVAL, "queue cap must be in [1, kQMax]");
       c->qcap = (uint32_t)value;
       return GIM_OK;
     case GIM_OPT_PROFILE: c->profile = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_SELECT_STEPS: c->select_steps = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_STAGING_CAP:
       if (value < 0) return fail(c, GIM_EINVAL, "staging cap must be >= 0");
       c->staging_init = (uint64_t)value;

@@ -104,8 +104,14 @@ struct RRParams {
 
 // Shared-memory layout of the warp-per-RR kernel.
 constexpr int kRRWarps = 8;          // warps per CTA
-constexpr int kQMax = 384;           // queue capacity (the queue doubles as the RR buffer)
-constexpr int kHSize = 768;          // visited hash slots (load <= (384 + 256) / 768)
+#ifndef GIM_QMAX
+#define GIM_QMAX 384
+#endif
+#ifndef GIM_HSIZE
+#define GIM_HSIZE 768
+#endif
+constexpr int kQMax = GIM_QMAX;      // queue capacity (the queue doubles as the RR buffer)
+constexpr int kHSize = GIM_HSIZE;    // visited hash slots (load <= (Q + 128) / H)
 constexpr int kRRSmemPerWarp = (kQMax + kHSize) * 4;   // 4.5 KB -> 6 CTAs x 8 warps per SM
 #ifndef GIM_RR_BLOCKS
 #define GIM_RR_BLOCKS 6

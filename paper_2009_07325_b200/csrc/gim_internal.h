@@ -28,4 +28,7 @@ cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long
 cudaError_t launch_cover(const unsigned long long* keys, int j, const uint64_t* inv_off,
                          const uint32_t* inv, const uint64_t* offsets, const uint32_t* pool,
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s);
+cudaError_t launch_select_coop(uint32_t* cnt, uint32_t n, const uint64_t* inv_off, const uint32_t* inv,
+                               const uint64_t* offsets, const uint32_t* pool, uint8_t* covered,
+                               unsigned long long* keys, int k, int num_sms, cudaStream_t s);
 }  // namespace gim

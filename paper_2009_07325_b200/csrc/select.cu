@@ -125,24 +125,60 @@ __global__ void __launch_bounds__(256) k_inv_scatter(const uint64_t* __restrict_
 // ------------------------------------------------------------------------------------------
 // K-ARGMAX: keys[j] = max over v of (selected ? 0 : count[v] << 32 | ~v). Applies the
 // all-reduced decrements of the previous step first (P > 1) and retires the previous pick.
+// Streams count as uint4 (4 nodes per load) with 4 independent loads in flight per thread.
 // ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void argmax_one(uint32_t c, uint32_t v, unsigned long long& best) {
+  const unsigned long long key = (c == kSent) ? 0ull : (((unsigned long long)c << 32) | (unsigned long long)(~v));
+  best = key > best ? key : best;
+}
+
 __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int32_t* __restrict__ dec,
                                                 uint32_t n, unsigned long long* __restrict__ keys, int j) {
+  (void)j;
   __shared__ unsigned long long s_best[8];
-  const uint32_t uprev = (j > 0) ? ~(uint32_t)keys[j - 1] : kEmpty;
   unsigned long long best = 0;
+  const uint32_t n4 = n >> 2;
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
-    uint32_t c = cnt[v];
-    bool dirty = false;
-    if (dec != nullptr) {
-      const int32_t d = dec[v];
-      if (d) { c -= (uint32_t)d; dec[v] = 0; dirty = true; }
+  uint4* c4 = reinterpret_cast<uint4*>(cnt);
+  int4* d4 = reinterpret_cast<int4*>(dec);
+  for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += 4 * stride) {
+    uint4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * stride;
+      x[u] = (i < n4) ? c4[i] : make_uint4(kSent, kSent, kSent, kSent);
     }
-    if (v == uprev) { c = kSent; dirty = true; }
-    if (dirty) cnt[v] = c;
-    const unsigned long long key = (c == kSent) ? 0ull : (((unsigned long long)c << 32) | (unsigned long long)(~v));
-    best = key > best ? key : best;
+    if (dec != nullptr) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = i0 + u * stride;
+        if (i < n4) {
+          const int4 d = d4[i];
+          if (d.x | d.y | d.z | d.w) {
+            if (x[u].x != kSent) x[u].x -= (uint32_t)d.x;
+            if (x[u].y != kSent) x[u].y -= (uint32_t)d.y;
+            if (x[u].z != kSent) x[u].z -= (uint32_t)d.z;
+            if (x[u].w != kSent) x[u].w -= (uint32_t)d.w;
+            c4[i] = x[u];
+            d4[i] = make_int4(0, 0, 0, 0);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t v = (i0 + u * stride) << 2;
+      argmax_one(x[u].x, v, best);
+      argmax_one(x[u].y, v + 1, best);
+      argmax_one(x[u].z, v + 2, best);
+      argmax_one(x[u].w, v + 3, best);
+    }
+  }
+  // tail (n % 4 nodes)
+  for (uint32_t v = (n4 << 2) + blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    uint32_t c = cnt[v];
+    if (dec != nullptr && c != kSent && dec[v]) { c -= (uint32_t)dec[v]; dec[v] = 0; cnt[v] = c; }
+    argmax_one(c, v, best);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -164,7 +200,8 @@ __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int3
 
 // ------------------------------------------------------------------------------------------
 // K-COVER: for every local set r in inv[u_j] not yet covered: covered[r] = 1 and, for each
-// member w, count[w] -= 1 (P = 1) or dec[w] += 1 (P > 1, all-reduced before the next argmax).
+// member w != u_j, count[w] -= 1 (P = 1) or dec[w] += 1 (P > 1, all-reduced before the next
+// argmax). One 8-lane group per inverted-index entry (RR sets average ~18 members).
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restrict__ keys, int j,
                                                const uint64_t* __restrict__ inv_off,
@@ -173,20 +210,26 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
                                                const uint32_t* __restrict__ pool,
                                                uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
                                                int32_t* __restrict__ dec) {
-  const int lane = threadIdx.x & 31;
+  const uint32_t sub = threadIdx.x & 7;
   const uint32_t u = ~(uint32_t)keys[j];
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[u] = kSent;   // retire the pick (never decremented)
   const uint64_t lo = inv_off[u], hi = inv_off[u + 1];
-  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-  for (uint64_t t = lo + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < hi; t += nwarps) {
+  const uint64_t ngroups = (uint64_t)gridDim.x * (blockDim.x >> 3);
+  for (uint64_t t = lo + blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); t < hi; t += ngroups) {
     const uint32_t r = inv[t];
     if (covered[r]) continue;
-    __syncwarp();
-    if (lane == 0) covered[r] = 1;
+    if (sub == 0) covered[r] = 1;      // each r appears once in inv[u]: no race
     const uint64_t a = offsets[r], b = offsets[r + 1];
     if (dec == nullptr) {
-      for (uint64_t e = a + lane; e < b; e += 32) atomicSub(cnt + pool[e], 1u);
+      for (uint64_t e = a + sub; e < b; e += 8) {
+        const uint32_t w = pool[e];
+        if (w != u) atomicSub(cnt + w, 1u);
+      }
     } else {
-      for (uint64_t e = a + lane; e < b; e += 32) atomicAdd(dec + pool[e], 1);
+      for (uint64_t e = a + sub; e < b; e += 8) {
+        const uint32_t w = pool[e];
+        if (w != u) atomicAdd(dec + w, 1);
+      }
     }
   }
 }
@@ -228,6 +271,112 @@ cudaError_t launch_cover(const unsigned long long* keys, int j, const uint64_t* 
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s) {
   k_cover<<<grid, 256, 0, s>>>(keys, j, inv_off, inv, offsets, pool, covered, cnt, dec);
   return cudaGetLastError();
+}
+
+
+// ==========================================================================================
+// K-SELECT: the whole k-step NodeSelection (P = 1) in ONE cooperative persistent kernel — the
+// k greedy steps iterate on-device without host round trips or per-step launches:
+//   phase A (all CTAs): streaming argmax of (count << 32 | ~v) over unselected nodes (lowest id
+//       wins ties, reading R10), one atomicMax per CTA into keys[j];   grid.sync();
+//   phase B (all warps): cover inv[u_j]: flag each uncovered set and decrement its members
+//       (Alg. 7 l.11-16, via the inverted index); CTA 0 retires u_j (sentinel);   grid.sync().
+// The count vector (4n bytes, 19 MB on C3) stays L2-resident across steps.
+// ==========================================================================================
+}  // namespace gim
+#include <cooperative_groups.h>
+namespace gim {
+namespace cg = cooperative_groups;
+
+constexpr int kSelThreads = 512;
+
+struct SelParams {
+  uint32_t* cnt;
+  uint32_t n;
+  const uint64_t* inv_off;
+  const uint32_t* inv;
+  const uint64_t* offsets;
+  const uint32_t* pool;
+  uint8_t* covered;
+  unsigned long long* keys;   // zeroed, k entries
+  int k;
+};
+
+__global__ void __launch_bounds__(kSelThreads) k_select_coop(SelParams p) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ unsigned long long s_red[kSelThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t gtid = blockIdx.x * kSelThreads + threadIdx.x;
+  const uint32_t gthreads = gridDim.x * kSelThreads;
+  const uint32_t n4 = p.n >> 2;
+  const uint4* c4 = reinterpret_cast<const uint4*>(p.cnt);   // read with __ldcg: mutated in-kernel
+  const uint32_t sub = threadIdx.x & 7;
+  const uint64_t ngroups = (uint64_t)gridDim.x * (kSelThreads / 8);
+  const uint64_t gg = (uint64_t)blockIdx.x * (kSelThreads / 8) + (threadIdx.x >> 3);
+  for (int j = 0; j < p.k; ++j) {
+    unsigned long long best = 0;
+    for (uint32_t i0 = gtid; i0 < n4; i0 += 4 * gthreads) {
+      uint4 x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t i = i0 + q * gthreads;
+        x[q] = (i < n4) ? __ldcg(c4 + i) : make_uint4(kSent, kSent, kSent, kSent);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t v = (i0 + q * gthreads) << 2;
+        argmax_one(x[q].x, v, best);
+        argmax_one(x[q].y, v + 1, best);
+        argmax_one(x[q].z, v + 2, best);
+        argmax_one(x[q].w, v + 3, best);
+      }
+    }
+    for (uint32_t v = (n4 << 2) + gtid; v < p.n; v += gthreads) argmax_one(__ldcg(p.cnt + v), v, best);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+      best = o > best ? o : best;
+    }
+    if (lane == 0) s_red[warp] = best;
+    __syncthreads();
+    if (warp == 0) {
+      best = (lane < kSelThreads / 32) ? s_red[lane] : 0ull;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+        best = o > best ? o : best;
+      }
+      if (lane == 0 && best) atomicMax(p.keys + j, best);
+    }
+    grid.sync();
+    const uint32_t u = ~(uint32_t)__ldcg(p.keys + j);
+    if (gtid == 0) p.cnt[u] = kSent;          // retire the pick (never decremented by cover)
+    const uint64_t lo = p.inv_off[u], hi = p.inv_off[u + 1];
+    for (uint64_t t = lo + gg; t < hi; t += ngroups) {
+      const uint32_t r = p.inv[t];
+      if (__ldcg(p.covered + r)) continue;
+      if (sub == 0) p.covered[r] = 1;
+      const uint64_t a = p.offsets[r], b = p.offsets[r + 1];
+      for (uint64_t e = a + sub; e < b; e += 8) {
+        const uint32_t w = p.pool[e];
+        if (w != u) atomicSub(p.cnt + w, 1u);
+      }
+    }
+    grid.sync();
+  }
+}
+
+cudaError_t launch_select_coop(uint32_t* cnt, uint32_t n, const uint64_t* inv_off, const uint32_t* inv,
+                               const uint64_t* offsets, const uint32_t* pool, uint8_t* covered,
+                               unsigned long long* keys, int k, int num_sms, cudaStream_t s) {
+  SelParams p{cnt, n, inv_off, inv, offsets, pool, covered, keys, k};
+  int bps = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_select_coop, kSelThreads, 0);
+  if (e != cudaSuccess) return e;
+  if (bps < 1) return cudaErrorCooperativeLaunchTooLarge;
+  dim3 grid(num_sms * (bps < 4 ? bps : 4)), block(kSelThreads);
+  void* args[] = {&p};
+  return cudaLaunchCooperativeKernel((void*)k_select_coop, grid, block, args, 0, s);
 }
 
 }  // namespace gim

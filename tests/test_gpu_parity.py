@@ -97,11 +97,14 @@ def test_pool_parity_C1_invariance(opts):
         assert c.stats()["giant_sets"] == T
 
 
-def test_pool_parity_C2_and_select():
+@pytest.mark.parametrize("steps", [1, 0])
+def test_pool_parity_C2_and_select(steps):
+    """k = 50 selection through the cooperative k-step kernel (steps=0) and the per-step
+    argmax/cover launches (steps=1)."""
     w = gi.WORKLOADS["C2"]
     g = gi.workload_graph("C2")
     T = 30011
-    c = _ctx(g, w.model, w.scheme)
+    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_STEPS: steps})
     c.generate_rr(T, w.rr_seed)
     o = oracle.Oracle(g, w.model, w.scheme)
     o.generate(T, w.rr_seed)
@@ -109,6 +112,8 @@ def test_pool_parity_C2_and_select():
     s, gns, cov = c.select(50)
     os_, ogn, ocov = o.select(50)
     assert np.array_equal(s, os_) and np.array_equal(gns, ogn) and cov == ocov
+    s2, g2, c2 = c.select(50)                          # non-destructive (reading R9)
+    assert np.array_equal(s2, s) and np.array_equal(g2, gns) and c2 == cov
     st = c.stats()
     assert st["coins"] == o.stats()["coins"] or st["giant_sets"] > 0   # aborted work is recounted
     assert st["rr_elements"] == len(o.export()[1])
@@ -124,9 +129,10 @@ def test_extend_truncate_reseed():
         _same_pool(c, o, T)
 
 
-def test_select_zero_gain_and_k_eq_n():
+@pytest.mark.parametrize("steps", [0, 1])
+def test_select_zero_gain_and_k_eq_n(steps):
     g = gi.diamond()
-    c = _ctx(g, gi.LT, gi.W_WC)
+    c = _ctx(g, gi.LT, gi.W_WC, opts={P.OPT_SELECT_STEPS: steps})
     c.generate_rr(16, 200907325)
     s, gns, cov = c.select(4)
     o = oracle.Oracle(g, gi.LT, gi.W_WC)
@@ -238,6 +244,19 @@ def test_full_size_sampled(key):
     mask = np.ones(len(d), dtype=bool)
     mask[starts - 1] = False
     assert np.all(d[mask] > 0)                                       # distinct members
+    # NodeSelection at full size: cooperative k-step kernel == per-step launches; properties
+    # that hold at any size: first pick is the lowest-id argmax of the counts, gains are
+    # non-increasing (greedy on a coverage function), covered = #sets hit by the seeds.
+    seeds, gains, cov = c.select(w.k)
+    c.set_option(P.OPT_SELECT_STEPS, 0)
+    s2, g2, c2 = c.select(w.k)
+    assert np.array_equal(seeds, s2) and np.array_equal(gains, g2) and cov == c2
+    assert seeds[0] == int(np.argmax(cnt)) and gains[0] == int(cnt.max())
+    assert np.all(np.diff(gains.astype(np.int64)) <= 0) and len(set(seeds.tolist())) == w.k
+    hit = np.zeros(T, dtype=bool)
+    set_of = np.repeat(np.arange(T), sizes)
+    hit[set_of[np.isin(nodes, seeds)]] = True
+    assert int(hit.sum()) == cov == int(gains.sum())
 
 
 def test_sharded_emulation_equals_single():

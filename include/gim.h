@@ -64,7 +64,8 @@ const char* gim_last_error(const gim_ctx* ctx);
  *  model GIM_LT requires GIM_W_WC or GIM_W_EXPLICIT with sum_u w_uv <= 1 at every v
  *    (P:125), else GIM_ELTWEIGHT (or GIM_EINVAL for LT + uniform, reading R23).
  *  Limits: 1 <= n < 2^32 - 1, m < 2^32 - 256 (row pointers are held as uint32 on the device).
- * Replaces any previous graph and clears the RR pool. */
+ * Replaces any previous graph and clears the RR pool; after an error no graph is loaded.
+ * Validation and the row-pointer conversion run on the device (pinned host arrays are DMA'd). */
 gim_status gim_load_graph(gim_ctx* ctx, uint32_t n, uint64_t m, const uint64_t* in_row_ptr,
                           const uint32_t* in_src, const float* weights, gim_model model,
                           gim_weights scheme, float p_uniform);
@@ -144,13 +145,16 @@ gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
  *  GIM_OPT_STAGING_CAP  = elements of staging memory to start from (forces retries if tiny).
  *  GIM_OPT_SELECT_STEPS = 1 (default): one argmax + one cover launch per greedy step;
  *                          0: P = 1 selections run all k steps in one cooperative persistent
- *                          kernel with grid-wide barriers (ablation; slower on C3). */
+ *                          kernel with grid-wide barriers (ablation; slower on C3).
+ *  GIM_OPT_SELECT_GRAPH = 1 (default): with per-step launches and P = 1, replay the 2k launches
+ *                          from a captured CUDA graph; 0: launch them one by one. */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
   GIM_OPT_PROFILE = 3,
   GIM_OPT_STAGING_CAP = 4,
-  GIM_OPT_SELECT_STEPS = 5
+  GIM_OPT_SELECT_STEPS = 5,
+  GIM_OPT_SELECT_GRAPH = 6
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

@@ -66,9 +66,12 @@ struct gim_ctx {
   DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr, dump;
   DevBuf bitmaps, gqueues;
   uint32_t giant_slots = 0;
+  bool giant_cap_reached = false;
   uint64_t stage_cap = 0;
   GenCounters* h_ctr = nullptr;   // pinned
   uint64_t* h_u64 = nullptr;      // pinned scratch
+  unsigned long long* h_keys = nullptr;   // pinned selection keys
+  uint32_t h_keys_cap = 0;
   // selection scratch
   DevBuf cnt, inv_off, cursor, inv, covered, keys, dec, bound;
   // options
@@ -78,6 +81,10 @@ struct gim_ctx {
   gim_stats st{};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[CLS_N];
   std::vector<cudaEvent_t> ev_free;   // recycled timing events
+  // CUDA graph of the k-step selection loop (P = 1), valid while its key is unchanged
+  cudaGraphExec_t sel_exec = nullptr;
+  std::vector<uintptr_t> sel_key;
+  int use_graph = 1;
 };
 
 namespace {
@@ -236,12 +243,14 @@ gim_status reset_pool(gim_ctx* c, uint64_t seed) {
 }
 
 gim_status ensure_giant_slots(gim_ctx* c, uint32_t want) {
+  if (c->giant_slots >= want || c->giant_cap_reached) return GIM_OK;
   const uint64_t words = ((uint64_t)c->n + 31) / 32;
   const uint64_t per_slot = words * 4 + (uint64_t)c->n * 4;
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   uint64_t cap = std::max<uint64_t>(1, (uint64_t)(free_b / 8) / std::max<uint64_t>(per_slot, 1));
   uint32_t slots = (uint32_t)std::min<uint64_t>({(uint64_t)want, cap});
+  if (slots < want) c->giant_cap_reached = true;
   if (slots <= c->giant_slots) return GIM_OK;
   TRY(dalloc(c, c->bitmaps, words * 4 * slots));
   CK(cudaMemsetAsync(c->bitmaps.p, 0, words * 4 * slots, c->stream));
@@ -483,6 +492,31 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
                                        c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), c->covered.as<uint8_t>(),
                                        keys, (int)k, c->num_sms, c->stream),
                  "k_select_coop"));
+  } else if (!dec && c->use_graph) {
+    // P = 1: the 2k argmax/cover launches replayed from a CUDA graph (captured once per set of
+    // buffer pointers; steady-state IMM runs reuse it), so the GPU runs them back to back.
+    const std::vector<uintptr_t> key = {(uintptr_t)c->cnt.p, (uintptr_t)c->inv_off.p, (uintptr_t)c->inv.p,
+                                        (uintptr_t)c->offsets.p, (uintptr_t)c->pool.p, (uintptr_t)c->covered.p,
+                                        (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n};
+    if (!c->sel_exec || key != c->sel_key) {
+      if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
+      c->sel_exec = nullptr;
+      cudaGraph_t graph = nullptr;
+      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      for (uint32_t j = 0; j < k; ++j) {
+        launch_argmax(c->cnt.as<uint32_t>(), nullptr, c->n, keys, (int)j, c->num_sms * 4, c->stream);
+        launch_cover(keys, (int)j, c->inv_off.as<uint64_t>(), c->inv.as<uint32_t>(), c->offsets.as<uint64_t>(),
+                     c->pool.as<uint32_t>(), c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr,
+                     c->num_sms * 8, c->stream);
+      }
+      CK(cudaStreamEndCapture(c->stream, &graph));
+      const cudaError_t ie = cudaGraphInstantiate(&c->sel_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) return fail_cuda(c, "cudaGraphInstantiate", ie);
+      c->sel_key = key;
+    }
+    Prof pf(c, CLS_SELECT);
+    TRY(launched(c, cudaGraphLaunch(c->sel_exec, c->stream), "selection graph", 2 * (int)k));
   } else {
     for (uint32_t j = 0; j < k; ++j) {
       {
@@ -499,8 +533,14 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
       }
     }
   }
-  std::vector<unsigned long long> hk(k);
-  CK(cudaMemcpyAsync(hk.data(), keys, (uint64_t)k * 8, cudaMemcpyDeviceToHost, c->stream));
+  if (c->h_keys_cap < k) {
+    if (c->h_keys) cudaFreeHost(c->h_keys);
+    c->h_keys = nullptr;
+    CK(cudaMallocHost(&c->h_keys, (uint64_t)k * 8));
+    c->h_keys_cap = k;
+  }
+  unsigned long long* hk = c->h_keys;
+  CK(cudaMemcpyAsync(hk, keys, (uint64_t)k * 8, cudaMemcpyDeviceToHost, c->stream));
   TRY(sync(c));
   uint64_t cov = 0;
   for (uint32_t j = 0; j < k; ++j) {
@@ -596,8 +636,10 @@ void gim_destroy(gim_ctx* c) {
       cudaEventDestroy(pr.second);
     }
   for (cudaEvent_t e : c->ev_free) cudaEventDestroy(e);
+  if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
   if (c->h_u64) cudaFreeHost(c->h_u64);
+  if (c->h_keys) cudaFreeHost(c->h_keys);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   cudaGetLastError();
   delete c;
@@ -629,36 +671,8 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
   if (scheme == GIM_W_EXPLICIT && m && !w) return fail(c, GIM_EINVAL, "explicit weights required");
   if (model == GIM_LT && scheme == GIM_W_UNIFORM) return fail(c, GIM_EINVAL, "LT with uniform p is not supported (reading R23)");
   if (scheme == GIM_W_UNIFORM && !(p_uniform >= 0.f && p_uniform <= 1.f)) return fail(c, GIM_EINVAL, "p_uniform must be in [0,1]");
-  // canonical in-CSR validation (reading R15)
+  // canonical in-CSR (reading R15): the end points here, everything else on the device below
   if (rp[0] != 0 || rp[n] != m) return fail(c, GIM_EINVAL, "row_ptr[0] must be 0 and row_ptr[n] must be m");
-  std::vector<uint32_t> rp32(n + 1);
-  for (uint32_t v = 0; v < n; ++v) {
-    if (rp[v + 1] < rp[v]) return fail(c, GIM_EINVAL, "row_ptr must be non-decreasing");
-    rp32[v] = (uint32_t)rp[v];
-    for (uint64_t e = rp[v]; e < rp[v + 1]; ++e) {
-      const uint32_t u = src[e];
-      if (u >= n) return fail(c, GIM_EINVAL, "src out of range");
-      if (u == v) return fail(c, GIM_EINVAL, "self-loop in row " + std::to_string(v));
-      if (e > rp[v] && src[e - 1] >= u) return fail(c, GIM_EINVAL, "row " + std::to_string(v) + " not strictly ascending");
-    }
-  }
-  rp32[n] = (uint32_t)m;
-  std::vector<uint64_t> thr;
-  if (scheme == GIM_W_EXPLICIT) {
-    thr.resize(std::max<uint64_t>(m, 1));
-    for (uint32_t v = 0; v < n; ++v) {
-      uint64_t acc = 0;
-      for (uint64_t e = rp[v]; e < rp[v + 1]; ++e) {
-        const float x = w[e];
-        if (!(x >= 0.f && x <= 1.f)) return fail(c, GIM_EINVAL, "weights must be in [0,1]");
-        const double t = (double)x * 4294967296.0;   // exact for float32
-        thr[e] = (model == GIM_LT) ? (uint64_t)std::floor(t) : (uint64_t)std::ceil(t);
-        acc += thr[e];
-      }
-      if (model == GIM_LT && acc > 4294967296ull)
-        return fail(c, GIM_ELTWEIGHT, "LT in-weights of node " + std::to_string(v) + " sum above 1");
-    }
-  }
   // release the previous graph and pool
   dfree(c, c->row_ptr);
   dfree(c, c->src);
@@ -666,6 +680,7 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
   dfree(c, c->bitmaps);
   dfree(c, c->gqueues);
   c->giant_slots = 0;
+  c->giant_cap_reached = false;
   c->graph = false;
   c->n = n;
   c->m = m;
@@ -675,8 +690,52 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
   c->thr_uniform = (uint64_t)std::ceil((double)p_uniform * 4294967296.0);
   TRY(dalloc(c, c->row_ptr, ((uint64_t)n + 1) * 4));
   TRY(dalloc(c, c->src, std::max<uint64_t>(m, 1) * 4));
-  CK(cudaMemcpyAsync(c->row_ptr.p, rp32.data(), ((uint64_t)n + 1) * 4, cudaMemcpyHostToDevice, c->stream));
-  if (m) CK(cudaMemcpyAsync(c->src.p, src, m * 4, cudaMemcpyHostToDevice, c->stream));
+  {
+    // upload (pinned host buffers DMA directly), validate + convert row pointers on the device
+    DevBuf rp64;
+    TRY(dalloc(c, rp64, ((uint64_t)n + 1) * 8 + 16));
+    uint32_t* flags = reinterpret_cast<uint32_t*>(rp64.as<uint64_t>() + n + 1);
+    CK(cudaMemcpyAsync(rp64.p, rp, ((uint64_t)n + 1) * 8, cudaMemcpyHostToDevice, c->stream));
+    if (m) CK(cudaMemcpyAsync(c->src.p, src, m * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(flags, 0, 4, c->stream));
+    CK(cudaMemsetAsync(flags + 1, 0xFF, 4, c->stream));
+    TRY(launched(c, launch_validate_csr(rp64.as<uint64_t>(), n, m, c->src.as<uint32_t>(), c->row_ptr.as<uint32_t>(),
+                                        flags, flags + 1, c->num_sms * 8, c->stream), "k_validate_csr"));
+    CK(cudaMemcpyAsync(c->h_u64, flags, 8, cudaMemcpyDeviceToHost, c->stream));
+    TRY(sync(c));
+    dfree(c, rp64);
+    const uint32_t err = (uint32_t)c->h_u64[0], row = (uint32_t)(c->h_u64[0] >> 32);
+    if (err) {
+      dfree(c, c->row_ptr);
+      dfree(c, c->src);
+      const char* what = (err & 1) ? "row_ptr must be non-decreasing and <= m"
+                         : (err & 2) ? "src out of range"
+                         : (err & 4) ? "self-loop"
+                                     : "row not strictly ascending";
+      return fail(c, GIM_EINVAL, std::string(what) + " (row " + std::to_string(row) + ")");
+    }
+  }
+  // explicit weights: thresholds on the host, rows now known to be valid
+  std::vector<uint64_t> thr;
+  if (scheme == GIM_W_EXPLICIT) {
+    thr.resize(std::max<uint64_t>(m, 1));
+    for (uint32_t v = 0; v < n; ++v) {
+      uint64_t acc = 0;
+      for (uint64_t e = rp[v]; e < rp[v + 1]; ++e) {
+        const float x = w[e];
+        if (!(x >= 0.f && x <= 1.f)) { dfree(c, c->row_ptr); dfree(c, c->src); return fail(c, GIM_EINVAL, "weights must be in [0,1]"); }
+        const double t = (double)x * 4294967296.0;   // exact for float32
+        thr[e] = (model == GIM_LT) ? (uint64_t)std::floor(t) : (uint64_t)std::ceil(t);
+        acc += thr[e];
+      }
+      if (model == GIM_LT && acc > 4294967296ull)
+      {
+        dfree(c, c->row_ptr);
+        dfree(c, c->src);
+        return fail(c, GIM_ELTWEIGHT, "LT in-weights of node " + std::to_string(v) + " sum above 1");
+      }
+    }
+  }
   if (scheme == GIM_W_EXPLICIT) {
     TRY(dalloc(c, c->thr_edge, thr.size() * 8));
     CK(cudaMemcpyAsync(c->thr_edge.p, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, c->stream));
@@ -833,6 +892,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
       return GIM_OK;
     case GIM_OPT_PROFILE: c->profile = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_SELECT_STEPS: c->select_steps = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_SELECT_GRAPH: c->use_graph = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_STAGING_CAP:
       if (value < 0) return fail(c, GIM_EINVAL, "staging cap must be >= 0");
       c->staging_init = (uint64_t)value;

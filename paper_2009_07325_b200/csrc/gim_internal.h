@@ -31,4 +31,6 @@ cudaError_t launch_cover(const unsigned long long* keys, int j, const uint64_t* 
 cudaError_t launch_select_coop(uint32_t* cnt, uint32_t n, const uint64_t* inv_off, const uint32_t* inv,
                                const uint64_t* offsets, const uint32_t* pool, uint8_t* covered,
                                unsigned long long* keys, int k, int num_sms, cudaStream_t s);
+cudaError_t launch_validate_csr(const uint64_t* rp64, uint32_t n, uint64_t m, const uint32_t* src,
+                                uint32_t* rp32, uint32_t* err, uint32_t* bad_row, int grid, cudaStream_t s);
 }  // namespace gim

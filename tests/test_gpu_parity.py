@@ -97,14 +97,14 @@ def test_pool_parity_C1_invariance(opts):
         assert c.stats()["giant_sets"] == T
 
 
-@pytest.mark.parametrize("steps", [1, 0])
-def test_pool_parity_C2_and_select(steps):
-    """k = 50 selection through the cooperative k-step kernel (steps=0) and the per-step
-    argmax/cover launches (steps=1)."""
+@pytest.mark.parametrize("steps,graph", [(1, 1), (1, 0), (0, 0)])
+def test_pool_parity_C2_and_select(steps, graph):
+    """k = 50 selection through the per-step argmax/cover launches replayed from a CUDA graph
+    (default), launched one by one, and the cooperative k-step kernel."""
     w = gi.WORKLOADS["C2"]
     g = gi.workload_graph("C2")
     T = 30011
-    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_STEPS: steps})
+    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_STEPS: steps, P.OPT_SELECT_GRAPH: graph})
     c.generate_rr(T, w.rr_seed)
     o = oracle.Oracle(g, w.model, w.scheme)
     o.generate(T, w.rr_seed)

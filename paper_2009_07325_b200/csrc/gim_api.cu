@@ -255,6 +255,7 @@ gim_status ensure_giant_slots(gim_ctx* c, uint32_t want) {
   TRY(dalloc(c, c->bitmaps, words * 4 * slots));
   CK(cudaMemsetAsync(c->bitmaps.p, 0, words * 4 * slots, c->stream));
   TRY(dalloc(c, c->gqueues, (uint64_t)c->n * 4 * slots));
+  CK(cudaMemsetAsync(c->gqueues.p, 0xFF, (uint64_t)c->n * 4 * slots, c->stream));   // kEmpty
   c->giant_slots = slots;
   return GIM_OK;
 }

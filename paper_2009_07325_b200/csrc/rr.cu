@@ -328,54 +328,37 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
 // ------------------------------------------------------------------------------------------
 // K-GIANT: block-per-RR continuation for sets that outgrew the warp queue (the role of the
 // paper's reservoir queue Q_res, Alg. 4/5). Per-block global bitmap (Visited[n])
-// and global queue (capacity n). The frontier is processed in windows of up to kGiantWin
-// nodes; each window is flattened into 32-slot-group chunks (a hub of in-degree d gives
-// ceil(d/128) chunks) which the 16 warps of the block split into contiguous ranges, so a
-// narrow frontier of hubs still occupies the whole block.
+// and global queue (capacity n, entries kEmpty when unused). No level barriers: the 16 warps
+// of the block claim queued nodes from a shared head counter, expand each with the 4-chain
+// sweep of the hub path, and append new nodes with an atomic tail; the set is complete when no
+// node is pending and no warp is busy (the order of expansion cannot change the set).
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t block_incl_scan_512(uint32_t x, uint32_t* s_w, uint32_t& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, x, off);
-    if (lane >= off) x += y;
-  }
-  if (lane == 31) s_w[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t w = (lane < kGiantThreads / 32) ? s_w[lane] : 0u;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, w, off);
-      if (lane >= off) w += y;
-    }
-    if (lane < kGiantThreads / 32) s_w[lane] = w;
-  }
-  __syncthreads();
-  total = s_w[kGiantThreads / 32 - 1];
-  const uint32_t r = x + (warp ? s_w[warp - 1] : 0u);
-  __syncthreads();
-  return r;
-}
-
 template <int MODEL, int SCHEME>
 __global__ void __launch_bounds__(kGiantThreads) k_rr_giant(RRParams p, uint32_t* bitmaps,
                                                             uint32_t* gqueues, uint64_t bm_words) {
-  constexpr int NW = kGiantThreads / 32;
-  __shared__ uint32_t s_cp[kGiantWin];     // inclusive chunk prefix over the window
-  __shared__ uint32_t s_a[kGiantWin], s_b[kGiantWin];
-  __shared__ uint32_t s_w[32];
-  __shared__ uint32_t s_tail, s_r;
+  __shared__ uint32_t s_head, s_tail, s_busy, s_r;
   __shared__ unsigned long long s_off;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   uint32_t* bm = bitmaps + (uint64_t)blockIdx.x * bm_words;
-  uint32_t* Q = gqueues + (uint64_t)blockIdx.x * p.n;
-  const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
+  uint32_t* Q = gqueues + (uint64_t)blockIdx.x * p.n;     // entries are kEmpty when unused
   const uint32_t giant_count = *(volatile unsigned int*)&p.ctr->giant_count;
-  unsigned long long coins = 0, lives = 0;
+  const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
+  uint32_t coins = 0, lives = 0;
   auto visit = [bm](uint32_t u) {
     const uint32_t bit = 1u << (u & 31);
     return !(atomicOr(&bm[u >> 5], bit) & bit);
+  };
+  // append this lane's new nodes uu[] to the block queue (warp-collective)
+  auto append = [&](const uint32_t (&uu)[4]) {
+    const uint32_t cnt = (uu[0] != kEmpty) + (uu[1] != kEmpty) + (uu[2] != kEmpty) + (uu[3] != kEmpty);
+    uint32_t tot;
+    const uint32_t excl = warp_excl_scan(cnt, lane, tot);
+    uint32_t base = 0;
+    if (lane == 0 && tot) base = atomicAdd(&s_tail, tot);
+    uint32_t pos = __shfl_sync(kFull, base, 0) + excl;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (uu[j] != kEmpty) Q[pos++] = uu[j];
   };
 
   while (true) {
@@ -386,122 +369,136 @@ __global__ void __launch_bounds__(kGiantThreads) k_rr_giant(RRParams p, uint32_t
     const GiantRec rec = p.giant_recs[r];
     const uint64_t id = p.id_base + rec.item;
     const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
-    uint32_t head;
     if (rec.qlen == 0) {
       if (threadIdx.x == 0) {
         const uint32_t root = rr_root(p.seed, id, p.n);
         Q[0] = root;
         atomicOr(&bm[root >> 5], 1u << (root & 31));
         s_tail = 1;
+        s_head = 0;
       }
-      head = 0;
     } else {                                   // resume the warp kernel's partial BFS
       for (uint32_t t = threadIdx.x; t < rec.qlen; t += kGiantThreads) {
         const uint32_t u = p.dump[rec.dump_off + t];
         Q[t] = u;
         atomicOr(&bm[u >> 5], 1u << (u & 31));
       }
-      if (threadIdx.x == 0) s_tail = rec.qlen;
-      head = rec.head;
-    }
-    __syncthreads();
-    while (true) {
-      const uint32_t tail = s_tail;
-      if (head >= tail) break;
-      const uint32_t L = min(tail - head, (uint32_t)kGiantWin);
-      // phase 1: row ranges and chunk counts of the window, block prefix scan
-      uint32_t carry = 0;
-      for (uint32_t base = 0; base < L; base += kGiantThreads) {
-        const uint32_t f = base + threadIdx.x;
-        uint32_t nc = 0;
-        if (f < L) {
-          const uint32_t v = Q[head + f];
-          const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
-          s_a[f] = a;
-          s_b[f] = b;
-          if (b > a) nc = (MODEL == MODEL_IC) ? ((((b - 1) >> 2) - (a >> 2)) >> 5) + 1 : 1u;
-        }
-        uint32_t tot;
-        const uint32_t incl = block_incl_scan_512(nc, s_w, tot);
-        if (f < L) s_cp[f] = carry + incl;
-        carry += tot;
+      if (threadIdx.x == 0) {
+        s_tail = rec.qlen;
+        s_head = rec.head;
       }
-      __syncthreads();
-      const uint32_t total = carry;
-      // phase 2: warp `warp` takes chunks [c0, c1)
-      const uint32_t c0 = (uint32_t)(((uint64_t)total * warp) / NW);
-      const uint32_t c1 = (uint32_t)(((uint64_t)total * (warp + 1)) / NW);
-      if (c0 < c1) {
-        uint32_t lo = 0, hi = L - 1;           // first f with s_cp[f] > c0
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (s_cp[mid] > c0) hi = mid; else lo = mid + 1;
+    }
+    if (threadIdx.x == 0) s_busy = 0;
+    __syncthreads();
+    // asynchronous expansion: warps claim queued nodes until none is pending and none is busy
+    while (true) {
+      uint32_t f = 0, state = 0;                 // state: 1 = got a node, 2 = done
+      if (lane == 0) {
+        atomicAdd(&s_busy, 1u);
+        while (true) {
+          const uint32_t h = *(volatile uint32_t*)&s_head;
+          const uint32_t t = *(volatile uint32_t*)&s_tail;
+          if (h < t) {
+            if (atomicCAS(&s_head, h, h + 1) == h) { f = h; state = 1; break; }
+            continue;
+          }
+          atomicSub(&s_busy, 1u);
+          while (true) {                        // idle: wait for work or global quiescence
+            const uint32_t b0 = *(volatile uint32_t*)&s_busy;
+            __threadfence_block();
+            const uint32_t h2 = *(volatile uint32_t*)&s_head;
+            const uint32_t t2 = *(volatile uint32_t*)&s_tail;
+            if (h2 < t2) { atomicAdd(&s_busy, 1u); break; }
+            if (b0 == 0) { state = 2; break; }
+            __nanosleep(64);
+          }
+          if (state == 2) break;
         }
-        uint32_t f = lo;
-        for (uint32_t c = c0; c < c1; ++c) {
-          while (s_cp[f] <= c) ++f;
-          const uint32_t cin = c - (f ? s_cp[f - 1] : 0u);
-          const uint32_t a = s_a[f], b = s_b[f];
-          if (MODEL == MODEL_IC) {
-            const uint32_t thr = node_thr<SCHEME>(p, b - a);
-            const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
-            const uint32_t g_hi = (b - 1) >> 2;
-            const uint32_t g = (a >> 2) + (cin << 5) + lane;
-            if (lane == 0) coins += min(b, (g - lane + 32) << 2) - max(a, (g - lane) << 2);
-            uint32_t m = 0;
-            if (g <= g_hi && !never) m = ic_live_mask<SCHEME>(p, id_lo, id_hi, k0, k1, g, a, b, thr);
-            if (!__any_sync(kFull, m)) continue;
-            lives += __popc(m);
-            uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
-            ic_take_live(p, g, m, uu, visit);
-            const uint32_t cnt = (uu[0] != kEmpty) + (uu[1] != kEmpty) + (uu[2] != kEmpty) + (uu[3] != kEmpty);
-            uint32_t tot;
-            const uint32_t excl = warp_excl_scan(cnt, lane, tot);
-            uint32_t base = 0;
-            if (lane == 0 && tot) base = atomicAdd(&s_tail, tot);
-            uint32_t pos = __shfl_sync(kFull, base, 0) + excl;
+      }
+      state = __shfl_sync(kFull, state, 0);
+      if (state == 2) break;
+      f = __shfl_sync(kFull, f, 0);
+      // the appender may still be writing the entry: read it at L2 (atomic), sleep while empty
+      uint32_t v = atomicOr(Q + f, 0u);
+      while (v == kEmpty) {
+        __nanosleep(32);
+        v = atomicOr(Q + f, 0u);
+      }
+      const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
+      if (b > a) {
+        if (MODEL == MODEL_IC) {
+          const uint32_t thr = node_thr<SCHEME>(p, b - a);
+          const uint32_t g_lo = a >> 2, g_hi = (b - 1) >> 2;
+          if (lane == 0) coins += b - a;
+          for (uint32_t gb = g_lo; gb <= g_hi; gb += kHubGroups) {
+            uint32_t m[kHubIlp];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (uu[j] != kEmpty) Q[pos++] = uu[j];
-          } else {
-            const uint32_t v = Q[head + f];
-            const uint32_t d = b - a;
-            const uint32_t j = lt_choose<SCHEME>(p, id, v, a, d, lane);
-            if (lane == 0) {
-              coins += 1;
-              if (j < d) {
-                ++lives;
-                const uint32_t u = __ldg(p.src + a + j);
-                if (visit(u)) Q[atomicAdd(&s_tail, 1u)] = u;
-              }
+            for (int q = 0; q < kHubIlp; ++q) {
+              const uint32_t g = gb + 32u * q + lane;
+              m[q] = (g <= g_hi && !never) ? ic_live_mask<SCHEME>(p, id_lo, id_hi, 0u, 0u, g, a, b, thr) : 0u;
+            }
+            uint32_t any = 0;
+#pragma unroll
+            for (int q = 0; q < kHubIlp; ++q) any |= m[q];
+            if (!__any_sync(kFull, any)) continue;
+#pragma unroll 1
+            for (int q = 0; q < kHubIlp; ++q) {
+              uint32_t mq = 0;
+#pragma unroll
+              for (int t = 0; t < kHubIlp; ++t) mq = (t == q) ? m[t] : mq;
+              if (!__any_sync(kFull, mq)) continue;
+              lives += __popc(mq);
+              uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
+              if (mq) ic_take_live(p, gb + 32u * q + lane, mq, uu, visit);
+              append(uu);
             }
           }
+        } else {
+          const uint32_t d = b - a;
+          const uint32_t j = lt_choose<SCHEME>(p, id, v, a, d, lane);
+          uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
+          if (lane == 0) {
+            coins += 1;
+            if (j < d) {
+              ++lives;
+              const uint32_t u = __ldg(p.src + a + j);
+              if (visit(u)) uu[0] = u;
+            }
+          }
+          append(uu);
         }
       }
-      head += L;
-      __syncthreads();
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        atomicSub(&s_busy, 1u);
+      }
     }
+    __syncthreads();
     const uint32_t size = s_tail;
     if (threadIdx.x == 0) s_off = atomicAdd(&p.ctr->stage_tail, (unsigned long long)size);
     __syncthreads();
     const unsigned long long off = s_off;
-    if (off + size > p.stage_cap) {
-      if (threadIdx.x == 0) p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = rec.item;
-    } else {
-      for (uint32_t t = threadIdx.x; t < size; t += kGiantThreads) p.staging[off + t] = Q[t];
-      if (threadIdx.x == 0) { p.sizes[rec.item] = size; p.soff[rec.item] = off; }
+    const bool fits = off + size <= p.stage_cap;
+    if (!fits && threadIdx.x == 0) p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = rec.item;
+    if (fits && threadIdx.x == 0) { p.sizes[rec.item] = size; p.soff[rec.item] = off; }
+    for (uint32_t t = threadIdx.x; t < size; t += kGiantThreads) {
+      const uint32_t u = Q[t];
+      if (fits) p.staging[off + t] = u;
+      bm[u >> 5] = 0u;
+      Q[t] = kEmpty;
     }
-    for (uint32_t t = threadIdx.x; t < size; t += kGiantThreads) bm[Q[t] >> 5] = 0u;
     __syncthreads();
   }
+  unsigned long long c64 = coins, l64 = lives;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    coins += __shfl_xor_sync(kFull, coins, off);
-    lives += __shfl_xor_sync(kFull, lives, off);
+    c64 += __shfl_xor_sync(kFull, c64, off);
+    l64 += __shfl_xor_sync(kFull, l64, off);
   }
   if (lane == 0) {
-    atomicAdd(&p.ctr->coins_giant, coins);
-    atomicAdd(&p.ctr->live_giant, lives);
+    atomicAdd(&p.ctr->coins_giant, c64);
+    atomicAdd(&p.ctr->live_giant, l64);
   }
 }
 

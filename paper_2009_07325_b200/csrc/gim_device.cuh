@@ -46,6 +46,22 @@ __device__ __forceinline__ uint4 philox4x32_10_rk(uint4 c, const uint32_t* rk) {
   return c;
 }
 
+// N independent Philox4x32-10 evaluations interleaved round by round (same key): each round key
+// is fetched once for all N states and the N dependency chains give the scheduler ILP.
+template <int N>
+__device__ __forceinline__ void philox4x32_10_rk_xn(uint4 (&c)[N], const uint32_t* rk) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t ka = rk[2 * r], kb = rk[2 * r + 1];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const uint32_t lo0 = 0xD2511F53u * c[i].x, hi0 = __umulhi(0xD2511F53u, c[i].x);
+      const uint32_t lo1 = 0xCD9E8D57u * c[i].z, hi1 = __umulhi(0xCD9E8D57u, c[i].z);
+      c[i] = make_uint4(hi1 ^ c[i].y ^ ka, lo1, hi0 ^ c[i].w ^ kb, lo0);
+    }
+  }
+}
+
 // Root of RR set `id`: floor(u64 * n / 2^64), u64 = out0 | out1 << 32 of slot 2^63
 // ("u = randSelect(V)", Alg. 3 l.5; reading R17).
 __device__ __forceinline__ uint32_t rr_root(uint64_t seed, uint64_t id, uint32_t n) {
@@ -105,16 +121,16 @@ struct RRParams {
 // Shared-memory layout of the warp-per-RR kernel.
 constexpr int kRRWarps = 8;          // warps per CTA
 #ifndef GIM_QMAX
-#define GIM_QMAX 384
+#define GIM_QMAX 512
 #endif
 #ifndef GIM_HSIZE
-#define GIM_HSIZE 768
+#define GIM_HSIZE 1024
 #endif
 constexpr int kQMax = GIM_QMAX;      // queue capacity (the queue doubles as the RR buffer)
 constexpr int kHSize = GIM_HSIZE;    // visited hash slots (load <= (Q + 128) / H)
-constexpr int kRRSmemPerWarp = (kQMax + kHSize) * 4;   // 4.5 KB -> 6 CTAs x 8 warps per SM
+constexpr int kRRSmemPerWarp = (kQMax + kHSize) * 4;   // 6 KB -> 4 CTAs x 8 warps per SM
 #ifndef GIM_RR_BLOCKS
-#define GIM_RR_BLOCKS 6
+#define GIM_RR_BLOCKS 4
 #endif
 #ifndef GIM_RR_ILP
 #define GIM_RR_ILP 2

@@ -61,13 +61,12 @@ __device__ __forceinline__ uint32_t lt_choose(const RRParams& p, uint64_t id, ui
 }
 
 
-// Fast path of one IC expansion step: lane evaluates the 4 coins of slot group g (one Philox
-// call) and returns the 4-bit mask of LIVE in-edge slots inside [a, b). No memory is touched.
+// Live-slot mask of slot group g from its 4 coins w: bit j set iff slot e = 4g + j lies in
+// [a, b) and is live. WC: coin <= floor((2^32-1)/d) <=> coin * d < 2^32; UNIFORM: coin <=
+// ceil(p 2^32) - 1; EXPLICIT: coin < ceil(w_e 2^32).
 template <int SCHEME>
-__device__ __forceinline__ uint32_t ic_live_mask(const RRParams& p, uint32_t id_lo, uint32_t id_hi,
-                                                 uint32_t k0, uint32_t k1, uint32_t g, uint32_t a,
-                                                 uint32_t b, uint32_t thr) {
-  const uint4 w = philox4x32_10_rk(make_uint4(id_lo, id_hi, g, 0u), p.rk);
+__device__ __forceinline__ uint32_t live_mask_words(const RRParams& p, uint4 w, uint32_t g, uint32_t a,
+                                                    uint32_t b, uint32_t thr) {
   const uint32_t e0 = g << 2;
   uint32_t m;
   if (SCHEME == W_EXPLICIT) {
@@ -78,12 +77,20 @@ __device__ __forceinline__ uint32_t ic_live_mask(const RRParams& p, uint32_t id_
       if (e0 + j >= a && e0 + j < b && (uint64_t)words[j] < p.thr_edge[e0 + j]) m |= 1u << j;
     return m;
   }
-  // WC: coin <= floor((2^32-1)/d)  <=>  coin * d < 2^32;  UNIFORM: coin <= ceil(p 2^32) - 1
   m = (uint32_t)(w.x <= thr) | ((uint32_t)(w.y <= thr) << 1) | ((uint32_t)(w.z <= thr) << 2) |
       ((uint32_t)(w.w <= thr) << 3);
   const uint32_t lo = a > e0 ? a - e0 : 0u;          // first valid word (group g_lo)
   const uint32_t hi = (b - e0) < 4u ? b - e0 : 4u;   // one past the last valid word (group g_hi)
-  return m & (0xFu << lo) & (0xFu >> (4u - hi));
+  return m & (0xFFFFFFFFu << lo) & (0xFu >> (4u - hi));
+}
+
+// One lane's coins of slot group g (one Philox call) as a live mask. No memory is touched.
+template <int SCHEME>
+__device__ __forceinline__ uint32_t ic_live_mask(const RRParams& p, uint32_t id_lo, uint32_t id_hi,
+                                                 uint32_t k0, uint32_t k1, uint32_t g, uint32_t a,
+                                                 uint32_t b, uint32_t thr) {
+  (void)k0; (void)k1;
+  return live_mask_words<SCHEME>(p, philox4x32_10_rk(make_uint4(id_lo, id_hi, g, 0u), p.rk), g, a, b, thr);
 }
 
 // Slow path (some lane of the warp has a live slot): load src[e] for live slots only and
@@ -138,6 +145,45 @@ __device__ __forceinline__ bool append_live(const RRParams& p, uint32_t g, uint3
   for (int j = 0; j < 4; ++j)
     if (uu[j] != kEmpty) q[pos++] = uu[j];
   tail += total;
+  return true;
+}
+
+
+// Sweep of one node's slot groups [a>>2, (b-1)>>2] with kHubIlp independent Philox chains per
+// lane (128 x kHubIlp slots per warp step). Fast path: only "could any coin be live?" — the
+// minimum of a lane's 4*kHubIlp coins against the node threshold — then one warp vote; the
+// exact masks are built from the same registers only when some lane may hold a live slot.
+// on_live(g, mask) is warp-collective and returns false to abort the sweep.
+template <int SCHEME, class OnLive>
+__device__ __forceinline__ bool hub_sweep(const RRParams& p, uint32_t id_lo, uint32_t id_hi, uint32_t a,
+                                          uint32_t b, uint32_t thr, bool never, int lane,
+                                          uint32_t& lives, OnLive on_live) {
+  const uint32_t g_lo = a >> 2, g_hi = (b - 1) >> 2;
+  for (uint32_t gb = g_lo; gb <= g_hi; gb += kHubGroups) {
+    uint4 w[kHubIlp];
+#pragma unroll
+    for (int r = 0; r < kHubIlp; ++r) w[r] = make_uint4(id_lo, id_hi, gb + 32u * r + lane, 0u);
+    philox4x32_10_rk_xn<kHubIlp>(w, p.rk);        // groups past g_hi are computed and ignored
+    uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+    for (int r = 0; r < kHubIlp; ++r) {
+      if (gb + 32u * r + lane > g_hi) w[r] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+      mn = min(mn, min(min(w[r].x, w[r].y), min(w[r].z, w[r].w)));
+    }
+    const bool maybe = !never && (SCHEME == W_EXPLICIT || mn <= thr || (g_hi - gb) < 32u * kHubIlp);
+    if (!__any_sync(kFull, maybe)) continue;
+#pragma unroll 1
+    for (int r = 0; r < kHubIlp; ++r) {
+      uint4 wr = w[0];
+#pragma unroll
+      for (int t = 1; t < kHubIlp; ++t) wr = (t == r) ? w[t] : wr;
+      const uint32_t g = gb + 32u * r + lane;
+      const uint32_t m = (g <= g_hi && !never) ? live_mask_words<SCHEME>(p, wr, g, a, b, thr) : 0u;
+      if (!__any_sync(kFull, m)) continue;
+      lives += __popc(m);
+      if (!on_live(g, m)) return false;
+    }
+  }
   return true;
 }
 
@@ -228,28 +274,9 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
           const uint32_t k = __ffs(hm) - 1;
           const uint32_t ak = __shfl_sync(kFull, a, k), bk = __shfl_sync(kFull, b, k);
           const uint32_t tk = __shfl_sync(kFull, thr, k);
-          const uint32_t g_lo = ak >> 2, g_hi = (bk - 1) >> 2;
-          for (uint32_t gb = g_lo; gb <= g_hi && !overflow; gb += kHubGroups) {
-            uint32_t m[kHubIlp];
-#pragma unroll
-            for (int r = 0; r < kHubIlp; ++r) {
-              const uint32_t g = gb + 32u * r + lane;
-              m[r] = (g <= g_hi && !never) ? ic_live_mask<SCHEME>(p, id_lo, id_hi, k0, k1, g, ak, bk, tk) : 0u;
-            }
-            uint32_t any = 0;
-#pragma unroll
-            for (int r = 0; r < kHubIlp; ++r) any |= m[r];
-            if (!__any_sync(kFull, any)) continue;
-#pragma unroll 1
-            for (int r = 0; r < kHubIlp; ++r) {
-              uint32_t mr = 0;
-#pragma unroll
-              for (int t = 0; t < kHubIlp; ++t) mr = (t == r) ? m[t] : mr;
-              if (!__any_sync(kFull, mr)) continue;
-              lives += __popc(mr);
-              if (!append_live(p, gb + 32u * r + lane, mr, q, tail, lane, vis)) { overflow = true; break; }
-            }
-          }
+          if (!hub_sweep<SCHEME>(p, id_lo, id_hi, ak, bk, tk, never, lane, lives,
+                                 [&](uint32_t g, uint32_t m) { return append_live(p, g, m, q, tail, lane, vis); }))
+            overflow = true;
         }
         __syncwarp();
         if (overflow) break;
@@ -334,7 +361,7 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
 // node is pending and no warp is busy (the order of expansion cannot change the set).
 // ------------------------------------------------------------------------------------------
 template <int MODEL, int SCHEME>
-__global__ void __launch_bounds__(kGiantThreads) k_rr_giant(RRParams p, uint32_t* bitmaps,
+__global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint32_t* bitmaps,
                                                             uint32_t* gqueues, uint64_t bm_words) {
   __shared__ uint32_t s_head, s_tail, s_busy, s_r;
   __shared__ unsigned long long s_off;
@@ -428,31 +455,13 @@ __global__ void __launch_bounds__(kGiantThreads) k_rr_giant(RRParams p, uint32_t
       if (b > a) {
         if (MODEL == MODEL_IC) {
           const uint32_t thr = node_thr<SCHEME>(p, b - a);
-          const uint32_t g_lo = a >> 2, g_hi = (b - 1) >> 2;
           if (lane == 0) coins += b - a;
-          for (uint32_t gb = g_lo; gb <= g_hi; gb += kHubGroups) {
-            uint32_t m[kHubIlp];
-#pragma unroll
-            for (int q = 0; q < kHubIlp; ++q) {
-              const uint32_t g = gb + 32u * q + lane;
-              m[q] = (g <= g_hi && !never) ? ic_live_mask<SCHEME>(p, id_lo, id_hi, 0u, 0u, g, a, b, thr) : 0u;
-            }
-            uint32_t any = 0;
-#pragma unroll
-            for (int q = 0; q < kHubIlp; ++q) any |= m[q];
-            if (!__any_sync(kFull, any)) continue;
-#pragma unroll 1
-            for (int q = 0; q < kHubIlp; ++q) {
-              uint32_t mq = 0;
-#pragma unroll
-              for (int t = 0; t < kHubIlp; ++t) mq = (t == q) ? m[t] : mq;
-              if (!__any_sync(kFull, mq)) continue;
-              lives += __popc(mq);
-              uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
-              if (mq) ic_take_live(p, gb + 32u * q + lane, mq, uu, visit);
-              append(uu);
-            }
-          }
+          hub_sweep<SCHEME>(p, id_lo, id_hi, a, b, thr, never, lane, lives, [&](uint32_t g, uint32_t m) {
+            uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
+            if (m) ic_take_live(p, g, m, uu, visit);
+            append(uu);
+            return true;
+          });
         } else {
           const uint32_t d = b - a;
           const uint32_t j = lt_choose<SCHEME>(p, id, v, a, d, lane);

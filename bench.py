@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--opt", action="append", default=[], help="library option NAME=VALUE (ablations)")
     return ap.parse_args()
 
 
@@ -70,46 +71,50 @@ def config_of(w, world):
 # clocks sampling (nvidia-smi during the timed region)
 # ------------------------------------------------------------------------------------------
 class Clocks:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clock and clock-event (throttle) reasons through NVML every 5 ms in a
+    background thread while the timed region runs (falls back to nothing if NVML is absent)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, gpu_index):
-        self.idx = gpu_index
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        import threading
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-i", str(gpu_index), "-lms", "200"], stdout=self.f,
-                                      stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.p = None
+            self.nv = None
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.005)
 
     def stop(self):
-        if self.p is None:
+        if self.nv is None:
             return None
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.flush()
-        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
-        os.unlink(self.f.name)
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            try:
-                sm.append(float(r[1]))
-                mx = max(mx, float(r[2]))
-                for nm, val in zip(names, r[5:9]):
-                    if val.strip().lower() == "active":
-                        reasons.add(nm)
-            except (ValueError, IndexError):
-                pass
-        if not sm:
+        self._stop.set()
+        self.t.join(timeout=2)
+        if not self.samples:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml 5 ms"}
 
 
 # ------------------------------------------------------------------------------------------
@@ -191,6 +196,9 @@ def run_gim(args, w):
         ctx.set_shard(rank, world)
         ctx.set_allreduce(P.torch_allreduce())
     ctx.set_option(P.OPT_PROFILE, 1)
+    for o in args.opt:
+        name, val = o.split("=")
+        ctx.set_option(getattr(P, name), int(val))
 
     def barrier():
         if world > 1:
@@ -238,6 +246,9 @@ def run_gim(args, w):
     warp_elems = st["rr_elements"]
     alg_bytes = 12 * st["rr_sets"] + 12 * warp_elems + 4 * st["live_edges"]
     traffic = load_profile_traffic().get(f"{w.key}:k_rr_warp")
+    mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = mp.get("hbm_gbs", 6650.0)
     measured_philox = None
     try:
         groups = 1 << 30
@@ -245,22 +256,25 @@ def run_gim(args, w):
         measured_philox = 4 * groups / (mb_ms / 1000.0) / 1e9
     except Exception:
         pass
-    mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
-    hbm_peak = mp.get("hbm_gbs", 6650.0)
+    alg_gbs = alg_bytes / (rr_ms / 1000.0) / 1e9 if rr_ms > 0 else 0.0
+    if w.model == gi.IC:
+        head = {"kernel": "k_rr_warp (K-IC warp-per-RR sampling)", "bound": "alu", "achieved": achieved,
+                "peak": peak, "unit": "Gcoin/s", "frac": achieved / peak if peak else None}
+    else:   # LT: one draw per visited node, dependent loads -> reported against HBM
+        head = {"kernel": "k_rr_warp (K-LT reverse walk)", "bound": "hbm", "achieved": alg_gbs,
+                "peak": hbm_peak, "unit": "GB/s", "frac": alg_gbs / hbm_peak}
     roofline = {
-        "kernel": "k_rr_warp (K-IC warp-per-RR sampling)" if w.model == gi.IC else "k_rr_warp (K-LT)",
-        "bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gcoin/s",
-        "frac": achieved / peak if peak else None,
+        **head,
         "traffic": traffic,
         "per_launch_ms": rr_ms / n_rr, "launches": n_rr,
         "coins_per_launch": coins / n_rr,
         "peak_basis": f"derived: 12.8 coins/cycle/SM x 148 SMs x {sm_max:.0f} MHz (Philox4x32-10 = 20 IMAD.WIDE on the FMA pipe)",
         "philox_microbench_gcoins": measured_philox,
         "frac_of_microbench": (achieved / measured_philox) if measured_philox else None,
-        "algorithmic_gbs": alg_bytes / (rr_ms / 1000.0) / 1e9 if rr_ms > 0 else None,
+        "traffic_note": "DRAM bytes of one captured launch (profiles/ncu_traffic.json), not averaged",
+        "algorithmic_gbs": alg_gbs,
         "hbm_peak_gbs": hbm_peak,
-        "hbm_frac": (alg_bytes / (rr_ms / 1000.0) / 1e9) / hbm_peak if rr_ms > 0 else None,
+        "hbm_frac": alg_gbs / hbm_peak,
         "hbm_peak_basis": "MEASURED_PEAKS.json hbm_gbs (copy)" if mp else "fallback 6.65 TB/s",
     }
     phases = {"ms_rr": st["ms_rr"] / args.steps, "ms_giant": st["ms_giant"] / args.steps,
@@ -277,17 +291,21 @@ def run_gim(args, w):
         if world > 1:
             ctx2.set_shard(rank, world)
             ctx2.set_allreduce(P.torch_allreduce())
+        def e2e_step():
+            ctx2.load_graph(g.n, rp_h.numpy(), src_h.numpy(), w.model, w.scheme, weights=g.weights,
+                            p_uniform=w.p_uniform)
+            if world > 1:
+                ctx2.set_shard(rank, world)
+            return ctx2.imm(w.k, w.eps, w.ell, w.rr_seed)
+        for _ in range(max(args.warmup, 1)):
+            e2e_step()
         barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         e2e_sets = 0
         for _ in range(args.steps):
-            ctx2.load_graph(g.n, rp_h.numpy(), src_h.numpy(), w.model, w.scheme, weights=g.weights,
-                            p_uniform=w.p_uniform)
-            if world > 1:
-                ctx2.set_shard(rank, world)
-            r = ctx2.imm(w.k, w.eps, w.ell, w.rr_seed)
+            r = e2e_step()
             e2e_sets += r.R_final
         f1.record(stream)
         torch.cuda.synchronize()
@@ -297,7 +315,7 @@ def run_gim(args, w):
                "h2d_bytes_per_step": int(g.row_ptr.nbytes + g.src.nbytes),
                "d2h_bytes_per_step": int(4 * w.k + 8 * w.k * (r.rounds + 1)),
                "ms_per_step": ms2 / args.steps,
-               "note": "gim_load_graph (host validation + H2D from pinned host buffers) + gim_imm + seeds D2H per step"}
+               "note": "per step: gim_load_graph (H2D of the in-CSR from pinned host buffers + on-device validation) + gim_imm + seeds D2H"}
         ctx2.close()
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) --------------------

@@ -143,18 +143,18 @@ gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
  *                          sets larger than Q are replayed by the giant kernel.
  *  GIM_OPT_PROFILE      = 1: time every kernel class with CUDA events (see gim_get_stats).
  *  GIM_OPT_STAGING_CAP  = elements of staging memory to start from (forces retries if tiny).
- *  GIM_OPT_SELECT_STEPS = 1 (default): one argmax + one cover launch per greedy step;
- *                          0: P = 1 selections run all k steps in one cooperative persistent
- *                          kernel with grid-wide barriers (ablation; slower on C3).
- *  GIM_OPT_SELECT_GRAPH = 1 (default): with per-step launches and P = 1, replay the 2k launches
- *                          from a captured CUDA graph; 0: launch them one by one. */
+ *  GIM_OPT_SELECT_GRAPH = 1 (default): for P = 1 replay the 2k argmax/cover launches of a
+ *                          NodeSelection from a captured CUDA graph; 0: launch them one by one.
+ *  GIM_OPT_INV_SEGMENTS = 1 (default): index each generation chunk's sets as it is stored (one
+ *                          inverted-index segment per chunk); 0: rebuild one index over the
+ *                          whole pool at every selection (ablation). */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
   GIM_OPT_PROFILE = 3,
   GIM_OPT_STAGING_CAP = 4,
-  GIM_OPT_SELECT_STEPS = 5,
-  GIM_OPT_SELECT_GRAPH = 6
+  GIM_OPT_SELECT_GRAPH = 6,
+  GIM_OPT_INV_SEGMENTS = 7
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

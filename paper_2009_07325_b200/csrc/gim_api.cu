@@ -30,9 +30,7 @@ struct Seg {
 enum { CLS_RR = 0, CLS_GIANT, CLS_STORE, CLS_INV, CLS_SELECT, CLS_N };
 
 constexpr uint32_t kChunk = 1u << 22;   // RR ids per generation chunk (bounds staging)
-#ifndef GIM_DEFAULT_SELECT_STEPS
-#define GIM_DEFAULT_SELECT_STEPS 1
-#endif
+
 
 }  // namespace
 
@@ -63,7 +61,7 @@ struct gim_ctx {
   std::vector<Seg> segs;
   DevBuf pool, offsets, count_total;
   // generation scratch
-  DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr, dump;
+  DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr, dump, lt_spill;
   DevBuf bitmaps, gqueues;
   uint32_t giant_slots = 0;
   bool giant_cap_reached = false;
@@ -73,9 +71,19 @@ struct gim_ctx {
   unsigned long long* h_keys = nullptr;   // pinned selection keys
   uint32_t h_keys_cap = 0;
   // selection scratch
-  DevBuf cnt, inv_off, cursor, inv, covered, keys, dec, bound;
+  DevBuf cnt, cursor, covered, keys, dec;
+  // segmented inverted index (one segment per generation chunk; rebuilt whole when invalid)
+  struct InvSeg {
+    DevBuf off, inv;
+  };
+  std::vector<InvSeg> iseg;
+  bool inv_valid = true;
+  int inv_segmented = 1;        // GIM_OPT_INV_SEGMENTS
+  DevBuf cnt_snap;              // count_total at the last indexed chunk
+  DevBuf seg_desc;              // device InvSegDev[kMaxInvSeg] + uint32 nseg
+  InvSegDev* h_desc = nullptr;  // pinned mirror
   // options
-  int force_giant = 0, profile = 0, select_steps = GIM_DEFAULT_SELECT_STEPS;
+  int force_giant = 0, profile = 0;
   uint32_t qcap = kQMax;
   uint64_t staging_init = 0;
   gim_stats st{};
@@ -227,6 +235,40 @@ gim_status launched(gim_ctx* c, cudaError_t e, const char* what, int n = 1) {
   return GIM_OK;
 }
 
+// ---- segmented inverted index ----------------------------------------------------------------
+void drop_inv(gim_ctx* c) {
+  for (auto& sg : c->iseg) {
+    dfree(c, sg.off);
+    dfree(c, sg.inv);
+  }
+  c->iseg.clear();
+}
+
+// Index local sets [set0, set1) (pool elements [e0, e1)) as a new segment; the per-node
+// histogram is count_total - cnt_snap (no extra atomics), then scan + cursor scatter.
+gim_status build_inv_segment(gim_ctx* c, uint64_t set0, uint64_t set1, uint64_t e0, uint64_t e1) {
+  const uint64_t n = c->n;
+  gim_ctx::InvSeg sg;
+  TRY(dalloc(c, sg.off, (n + 1) * 8));
+  TRY(dalloc(c, sg.inv, std::max<uint64_t>(e1 - e0, 1) * 4));
+  TRY(ensure(c, c->cursor, n * 4));
+  TRY(ensure(c, c->scan_tmp, (scan_tiles(n) + 2) * 8));
+  Prof pf(c, CLS_INV);
+  TRY(launched(c, launch_count_delta(c->count_total.as<uint32_t>(), c->cnt_snap.as<uint32_t>(),
+                                     c->cursor.as<uint32_t>(), c->n, c->num_sms * 8, c->stream), "k_count_delta"));
+  int nl = 0;
+  cudaError_t e = launch_scan_u32(c->cursor.as<uint32_t>(), n, sg.off.as<uint64_t>(), c->scan_tmp.as<uint64_t>(),
+                                  c->scan_tmp.as<uint64_t>() + scan_tiles(n) + 1, c->stream, &nl);
+  TRY(launched(c, e, "scan(segment counts)", nl));
+  CK(cudaMemsetAsync(c->cursor.p, 0, n * 4, c->stream));
+  if (set1 > set0)
+    TRY(launched(c, launch_inv_scatter(c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), (uint32_t)set0,
+                                       (uint32_t)set1, sg.off.as<uint64_t>(), c->cursor.as<uint32_t>(),
+                                       sg.inv.as<uint32_t>(), c->num_sms * 8, c->stream), "k_inv_scatter"));
+  c->iseg.push_back(std::move(sg));
+  return GIM_OK;
+}
+
 // ---- pool management ------------------------------------------------------------------------
 gim_status reset_pool(gim_ctx* c, uint64_t seed) {
   c->have_seed = true;
@@ -239,6 +281,10 @@ gim_status reset_pool(gim_ctx* c, uint64_t seed) {
   CK(cudaMemsetAsync(c->count_total.p, 0, (uint64_t)c->n * 4, c->stream));
   TRY(ensure(c, c->offsets, 8 * 1024));
   CK(cudaMemsetAsync(c->offsets.p, 0, 8, c->stream));
+  drop_inv(c);
+  c->inv_valid = true;
+  TRY(ensure(c, c->cnt_snap, (uint64_t)c->n * 4));
+  CK(cudaMemsetAsync(c->cnt_snap.p, 0, (uint64_t)c->n * 4, c->stream));
   return GIM_OK;
 }
 
@@ -287,6 +333,7 @@ RRParams base_params(gim_ctx* c) {
   p.dump_cap = c->dump.bytes / 4;
   p.retry_list = c->retry_list.as<uint32_t>();
   p.qcap = c->qcap;
+  p.lt_spill = c->lt_spill.as<uint32_t>();
   p.force_giant = c->force_giant;
   return p;
 }
@@ -323,7 +370,14 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   p.id_base = gstart;
   p.count = cnt;
   p.item_list = nullptr;
-  const int rr_grid = c->num_sms * kRRBlocksPerSM;   // persistent CTAs, 8 warps each
+  int rr_grid = c->num_sms * kRRBlocksPerSM;   // persistent CTAs, 8 warps each
+  if (c->model == MODEL_LT) {
+    static int lt_bps = 0;
+    if (!lt_bps) lt_bps = lt_blocks_per_sm();
+    rr_grid = c->num_sms * lt_bps;
+    TRY(ensure(c, c->lt_spill, (uint64_t)rr_grid * kLtWarps * (kLtCap2 - kLtCap) * 32 * 4));
+    p.lt_spill = c->lt_spill.as<uint32_t>();
+  }
   TRY(ensure_giant_slots(c, 2u * (uint32_t)c->num_sms));
   const uint64_t bm_words = ((uint64_t)c->n + 31) / 32;
   // warp kernel, then the giant kernel unconditionally (it reads the giant count on the device
@@ -369,6 +423,7 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     *c->h_ctr = h;
     CK(cudaMemcpyAsync(c->ctr.p, c->h_ctr, sizeof(GenCounters), cudaMemcpyHostToDevice, c->stream));
     RRParams pr = base_params(c);
+    pr.lt_spill = c->lt_spill.as<uint32_t>();
     pr.id_base = gstart;
     pr.count = retries;
     pr.item_list = c->item_list.as<uint32_t>();
@@ -402,6 +457,10 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
                                  c->num_sms * 8, c->stream), "k_store"));
   }
   c->segs.push_back(Seg{gstart, c->nsets, cnt});
+  if (c->inv_segmented && c->inv_valid && c->iseg.size() < (size_t)kMaxInvSeg)
+    TRY(build_inv_segment(c, c->nsets, c->nsets + cnt, c->pool_len, c->pool_len + total));
+  else
+    c->inv_valid = false;                      // rebuilt as one segment at the next selection
   c->nsets += cnt;
   c->pool_len += total;
   c->st.rr_sets += cnt;
@@ -429,6 +488,7 @@ gim_status truncate_pool(gim_ctx* c, uint64_t theta) {
   c->nsets = keep_sets;
   c->pool_len = e0;
   c->T_global = theta;
+  c->inv_valid = false;
   return GIM_OK;
 }
 
@@ -456,27 +516,26 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
   if (c->world > 1 && !c->arfn) return fail(c, GIM_ESTATE, "world > 1 requires gim_set_allreduce");
   const uint64_t n = c->n;
   TRY(ensure(c, c->cnt, n * 4));
-  TRY(ensure(c, c->inv_off, (n + 1) * 8));
-  TRY(ensure(c, c->cursor, n * 4));
-  TRY(ensure(c, c->inv, std::max<uint64_t>(c->pool_len, 1) * 4));
   TRY(ensure(c, c->covered, std::max<uint64_t>(c->nsets, 1)));
   TRY(ensure(c, c->keys, (uint64_t)k * 8));
-  TRY(ensure(c, c->scan_tmp, (scan_tiles(n) + 2) * 8));
   if (c->world > 1) TRY(ensure(c, c->dec, n * 4));
   int32_t* dec = c->world > 1 ? c->dec.as<int32_t>() : nullptr;
-  {
-    Prof pf(c, CLS_INV);
-    int nl = 0;
-    cudaError_t e = launch_scan_u32(c->count_total.as<uint32_t>(), n, c->inv_off.as<uint64_t>(),
-                                    c->scan_tmp.as<uint64_t>(), c->scan_tmp.as<uint64_t>() + scan_tiles(n) + 1,
-                                    c->stream, &nl);
-    TRY(launched(c, e, "scan(count_total)", nl));
-    CK(cudaMemsetAsync(c->cursor.p, 0, n * 4, c->stream));
-    if (c->nsets)
-      TRY(launched(c, launch_inv_scatter(c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), (uint32_t)c->nsets,
-                                         c->inv_off.as<uint64_t>(), c->cursor.as<uint32_t>(), c->inv.as<uint32_t>(),
-                                         c->num_sms * 8, c->stream), "k_inv_scatter"));
+  if (!c->inv_valid) {                          // one segment over the whole local pool
+    drop_inv(c);
+    CK(cudaMemsetAsync(c->cnt_snap.p, 0, n * 4, c->stream));
+    TRY(build_inv_segment(c, 0, c->nsets, 0, c->pool_len));
+    c->inv_valid = true;
   }
+  TRY(ensure(c, c->seg_desc, sizeof(InvSegDev) * kMaxInvSeg + 16));
+  if (!c->h_desc) CK(cudaMallocHost(&c->h_desc, sizeof(InvSegDev) * kMaxInvSeg + 16));
+  for (size_t q = 0; q < (size_t)kMaxInvSeg; ++q)
+    c->h_desc[q] = q < c->iseg.size() ? InvSegDev{c->iseg[q].off.as<uint64_t>(), c->iseg[q].inv.as<uint32_t>()}
+                                      : InvSegDev{nullptr, nullptr};
+  *reinterpret_cast<uint32_t*>(c->h_desc + kMaxInvSeg) = (uint32_t)c->iseg.size();
+  CK(cudaMemcpyAsync(c->seg_desc.p, c->h_desc, sizeof(InvSegDev) * kMaxInvSeg + 4, cudaMemcpyHostToDevice,
+                     c->stream));
+  const InvSegDev* segd = c->seg_desc.as<InvSegDev>();
+  const uint32_t* nsegd = reinterpret_cast<const uint32_t*>(segd + kMaxInvSeg);
   CK(cudaMemcpyAsync(c->cnt.p, c->count_total.p, n * 4, cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaMemsetAsync(c->covered.p, 0, std::max<uint64_t>(c->nsets, 1), c->stream));
   CK(cudaMemsetAsync(c->keys.p, 0, (uint64_t)k * 8, c->stream));
@@ -486,17 +545,10 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
     if (c->arfn(c->cnt.p, n, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(count) failed");
   }
   auto* keys = reinterpret_cast<unsigned long long*>(c->keys.p);
-  if (!dec && !c->select_steps) {
-    // P = 1: all k steps on-device in one cooperative persistent kernel
-    Prof pf(c, CLS_SELECT);
-    TRY(launched(c, launch_select_coop(c->cnt.as<uint32_t>(), c->n, c->inv_off.as<uint64_t>(), c->inv.as<uint32_t>(),
-                                       c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), c->covered.as<uint8_t>(),
-                                       keys, (int)k, c->num_sms, c->stream),
-                 "k_select_coop"));
-  } else if (!dec && c->use_graph) {
+  if (!dec && c->use_graph) {
     // P = 1: the 2k argmax/cover launches replayed from a CUDA graph (captured once per set of
     // buffer pointers; steady-state IMM runs reuse it), so the GPU runs them back to back.
-    const std::vector<uintptr_t> key = {(uintptr_t)c->cnt.p, (uintptr_t)c->inv_off.p, (uintptr_t)c->inv.p,
+    const std::vector<uintptr_t> key = {(uintptr_t)c->cnt.p, (uintptr_t)segd,
                                         (uintptr_t)c->offsets.p, (uintptr_t)c->pool.p, (uintptr_t)c->covered.p,
                                         (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n};
     if (!c->sel_exec || key != c->sel_key) {
@@ -506,9 +558,8 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
       CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       for (uint32_t j = 0; j < k; ++j) {
         launch_argmax(c->cnt.as<uint32_t>(), nullptr, c->n, keys, (int)j, c->num_sms * 4, c->stream);
-        launch_cover(keys, (int)j, c->inv_off.as<uint64_t>(), c->inv.as<uint32_t>(), c->offsets.as<uint64_t>(),
-                     c->pool.as<uint32_t>(), c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr,
-                     c->num_sms * 8, c->stream);
+        launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
+                     c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * 8, c->stream);
       }
       CK(cudaStreamEndCapture(c->stream, &graph));
       const cudaError_t ie = cudaGraphInstantiate(&c->sel_exec, graph, 0);
@@ -524,9 +575,9 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
         Prof pf(c, CLS_SELECT);
         TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, c->n, keys, (int)j, c->num_sms * 4, c->stream),
                      "k_argmax"));
-        TRY(launched(c, launch_cover(keys, (int)j, c->inv_off.as<uint64_t>(), c->inv.as<uint32_t>(),
-                                     c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), c->covered.as<uint8_t>(),
-                                     c->cnt.as<uint32_t>(), dec, c->num_sms * 8, c->stream), "k_cover"));
+        TRY(launched(c, launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
+                                     c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * 8,
+                                     c->stream), "k_cover"));
       }
       if (dec && j + 1 < k) {
         c->st.allreduces++;
@@ -536,6 +587,7 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
   }
   if (c->h_keys_cap < k) {
     if (c->h_keys) cudaFreeHost(c->h_keys);
+  if (c->h_desc) cudaFreeHost(c->h_desc);
     c->h_keys = nullptr;
     CK(cudaMallocHost(&c->h_keys, (uint64_t)k * 8));
     c->h_keys_cap = k;
@@ -627,8 +679,12 @@ void gim_destroy(gim_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
                     &c->sizes, &c->soff, &c->giant_list, &c->retry_list, &c->item_list, &c->scan_out,
-                    &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->bitmaps, &c->gqueues, &c->cnt, &c->inv_off,
-                    &c->cursor, &c->inv, &c->covered, &c->keys, &c->dec, &c->bound};
+                    &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->bitmaps, &c->gqueues, &c->cnt,
+                    &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc};
+  for (auto& sg : c->iseg) {
+    dfree(c, sg.off);
+    dfree(c, sg.inv);
+  }
   for (DevBuf* b : bufs) dfree(c, *b);
   cudaStreamSynchronize(c->stream);
   for (auto& v : c->ev)
@@ -641,6 +697,7 @@ void gim_destroy(gim_ctx* c) {
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
   if (c->h_u64) cudaFreeHost(c->h_u64);
   if (c->h_keys) cudaFreeHost(c->h_keys);
+  if (c->h_desc) cudaFreeHost(c->h_desc);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   cudaGetLastError();
   delete c;
@@ -892,8 +949,8 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
       c->qcap = (uint32_t)value;
       return GIM_OK;
     case GIM_OPT_PROFILE: c->profile = value ? 1 : 0; return GIM_OK;
-    case GIM_OPT_SELECT_STEPS: c->select_steps = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_SELECT_GRAPH: c->use_graph = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_INV_SEGMENTS: c->inv_segmented = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_STAGING_CAP:
       if (value < 0) return fail(c, GIM_EINVAL, "staging cap must be >= 0");
       c->staging_init = (uint64_t)value;

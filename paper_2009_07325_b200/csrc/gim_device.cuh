@@ -93,6 +93,14 @@ struct GiantRec {
   unsigned long long dump_off;
 };
 
+// One segment of the inverted node -> RR index (built per generation chunk): the local set ids
+// containing v are inv[off[v] .. off[v+1]).
+struct InvSegDev {
+  const uint64_t* off;
+  const uint32_t* inv;
+};
+constexpr int kMaxInvSeg = 16;
+
 // Parameters of the RR-generation kernels.
 struct RRParams {
   uint32_t n;
@@ -115,6 +123,7 @@ struct RRParams {
   uint64_t dump_cap;
   uint32_t* retry_list;        // items whose staging write failed
   uint32_t qcap;               // shared-memory queue capacity (<= kQMax)
+  uint32_t* lt_spill;          // LT: per-warp spill of walks longer than kLtCap (lane-interleaved)
   int force_giant;
 };
 
@@ -143,6 +152,9 @@ constexpr int kRRIlp = GIM_RR_ILP;    // Philox chains per lane per iteration (1
 constexpr int kHubIlp = GIM_HUB_ILP;  // Philox chains per lane per step on a hub node
 constexpr uint32_t kHubGroups = 32u * GIM_HUB_ILP;   // nodes with >= this many slot groups are hubs
 constexpr int kGiantThreads = 512;
+constexpr int kLtWarps = 8;          // K-LT: warps per CTA
+constexpr int kLtCap = 64;           // K-LT: path entries per lane in shared memory
+constexpr int kLtCap2 = 512;         // K-LT: max path per lane (shared + global spill)
 constexpr int kGiantWin = 2048;      // frontier window of the giant kernel (smem)
 
 }  // namespace gim

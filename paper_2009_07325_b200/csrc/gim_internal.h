@@ -6,6 +6,7 @@
 namespace gim {
 struct RRParams;
 
+int lt_blocks_per_sm();
 cudaError_t launch_rr_warp(int model, int scheme, const RRParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
                             uint32_t* gqueues, uint64_t bm_words, cudaStream_t s);
@@ -20,17 +21,17 @@ cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* si
 uint64_t scan_tiles(uint64_t count);
 cudaError_t launch_scan_u32(const uint32_t* in, uint64_t count, uint64_t* out, uint64_t* tile_tmp,
                             uint64_t* total_tmp, cudaStream_t s, int* launches);
-cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, uint32_t nsets,
+cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, uint32_t set0, uint32_t set1,
                                const uint64_t* inv_off, uint32_t* cursor, uint32_t* inv, int grid,
+                               cudaStream_t s);
+cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* delta, uint32_t n, int grid,
                                cudaStream_t s);
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
                           int grid, cudaStream_t s);
-cudaError_t launch_cover(const unsigned long long* keys, int j, const uint64_t* inv_off,
-                         const uint32_t* inv, const uint64_t* offsets, const uint32_t* pool,
+struct InvSegDev;
+cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,
+                         const uint64_t* offsets, const uint32_t* pool,
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s);
-cudaError_t launch_select_coop(uint32_t* cnt, uint32_t n, const uint64_t* inv_off, const uint32_t* inv,
-                               const uint64_t* offsets, const uint32_t* pool, uint8_t* covered,
-                               unsigned long long* keys, int k, int num_sms, cudaStream_t s);
 cudaError_t launch_validate_csr(const uint64_t* rp64, uint32_t n, uint64_t m, const uint32_t* src,
                                 uint32_t* rp32, uint32_t* err, uint32_t* bad_row, int grid, cudaStream_t s);
 }  // namespace gim

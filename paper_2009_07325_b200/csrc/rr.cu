@@ -353,6 +353,148 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
 }
 
 // ------------------------------------------------------------------------------------------
+// K-LT: lane-per-walk LT sampling (§3.7: at most one live in-edge per node, so the
+// "frontier" is one node and the RR set is a reverse walk). Each lane owns one RR set; 32 walks
+// per warp hide each other's dependent-load latency (row_ptr -> draw -> src -> membership).
+// The lane's path sits in shared memory (lane-interleaved, conflict-free) and is also the
+// membership set: a walk stops at a node with no chosen in-edge or at a node already on the
+// path (R19). Walks longer than kLtCap hand their path to K-GIANT (exact resume at the last
+// node: same draw, same chosen edge).
+// ------------------------------------------------------------------------------------------
+
+template <int SCHEME>
+__device__ __forceinline__ uint32_t lt_choose_lane(const RRParams& p, uint64_t id, uint32_t v, uint32_t a,
+                                                   uint32_t d) {
+  const uint4 o = philox4x32_10_rk(make_uint4((uint32_t)id, (uint32_t)(id >> 32), v, kSlotLtHi), p.rk);
+  const uint32_t r = o.x;
+  if (SCHEME == W_WC) return __umulhi(r, d);           // floor(r * d / 2^32)
+  uint64_t acc = 0;                                      // explicit: half-open fixed-point intervals
+  for (uint32_t t = 0; t < d; ++t) {
+    acc += p.thr_edge[a + t];
+    if ((uint64_t)r < acc) return t;
+  }
+  return d;
+}
+
+template <int SCHEME>
+__global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
+  extern __shared__ uint32_t smem[];
+  const int lane = threadIdx.x & 31;
+  uint32_t* path = smem + (threadIdx.x >> 5) * (kLtCap * 32);   // path[i * 32 + lane]
+  const uint64_t gwarp = (uint64_t)blockIdx.x * kLtWarps + (threadIdx.x >> 5);
+  uint32_t* spill = p.lt_spill + gwarp * (uint64_t)((kLtCap2 - kLtCap) * 32);   // entries >= kLtCap
+  auto at = [&](uint32_t t) -> uint32_t& {
+    return t < (uint32_t)kLtCap ? path[t * 32 + lane] : spill[(t - kLtCap) * 32 + lane];
+  };
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  uint32_t item = 0, v = 0, len = 0;
+  uint64_t id = 0;
+  bool active = false, want = true;       // want: lane needs a new walk
+  uint32_t coins = 0, lives = 0;
+  const uint32_t cap = min((uint32_t)kLtCap2, p.qcap);
+  while (true) {
+    // refill lanes that finished (one claim per warp)
+    const uint32_t need = __ballot_sync(kFull, want);
+    if (need) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&p.ctr->claim, (uint32_t)__popc(need));
+      base = __shfl_sync(kFull, base, 0);
+      if (want) {
+        const uint32_t i = base + __popc(need & lt_mask);
+        want = false;
+        active = i < p.count;
+        if (active) {
+          item = p.item_list ? p.item_list[i] : i;
+          id = p.id_base + item;
+          v = rr_root(p.seed, id, p.n);
+          path[lane] = v;
+          len = 1;
+          if (p.force_giant) {
+            p.giant_recs[atomicAdd(&p.ctr->giant_count, 1u)] = GiantRec{item, 0u, 0u, 0u, 0ull};
+            active = false;
+            want = true;
+          }
+        }
+      }
+    }
+    if (!__any_sync(kFull, active)) {
+      if (!__any_sync(kFull, want)) break;      // claims exhausted and no walk in flight
+      continue;
+    }
+    bool finish = false, overflow = false;
+    if (active) {
+      const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
+      const uint32_t d = b - a;
+      if (d == 0) {
+        finish = true;
+      } else {
+        const uint32_t j = lt_choose_lane<SCHEME>(p, id, v, a, d);
+        ++coins;
+        if (j >= d) {
+          finish = true;                       // r beyond the total weight: no live in-edge
+        } else {
+          ++lives;
+          const uint32_t u = __ldg(p.src + a + j);
+          bool seen = false;
+          const uint32_t ls = min(len, (uint32_t)kLtCap);
+          for (uint32_t t = 0; t < ls; ++t) seen |= (path[t * 32 + lane] == u);
+          for (uint32_t t = kLtCap; t < len; ++t) seen |= (spill[(t - kLtCap) * 32 + lane] == u);
+          if (seen) finish = true;
+          else if (len == cap) overflow = true;
+          else { at(len) = u; ++len; v = u; }
+        }
+      }
+    }
+    // finished walks: warp-aggregated staging reservation, then per-lane copy
+    const uint32_t fin = __ballot_sync(kFull, finish);
+    if (fin) {
+      uint32_t incl = finish ? len : 0u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += y;
+      }
+      const uint32_t tot = __shfl_sync(kFull, incl, 31);
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(&p.ctr->stage_tail, (unsigned long long)tot);
+      base = __shfl_sync(kFull, base, 0);
+      if (finish) {
+        const unsigned long long off = base + incl - len;
+        if (off + len > p.stage_cap) {
+          p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = item;
+        } else {
+          for (uint32_t t = 0; t < len; ++t) p.staging[off + t] = at(t);
+          p.sizes[item] = len;
+          p.soff[item] = off;
+        }
+        active = false;
+        want = true;
+      }
+    }
+    if (overflow) {                          // rare: hand the path to the giant kernel
+      const unsigned long long off = atomicAdd(&p.ctr->dump_tail, (unsigned long long)len);
+      const bool fits = off + len <= p.dump_cap;
+      if (fits)
+        for (uint32_t t = 0; t < len; ++t) p.dump[off + t] = at(t);
+      p.giant_recs[atomicAdd(&p.ctr->giant_count, 1u)] =
+          fits ? GiantRec{item, len, len - 1, 0u, off} : GiantRec{item, 0u, 0u, 0u, 0ull};
+      active = false;
+      want = true;
+    }
+  }
+  unsigned long long c64 = coins, l64 = lives;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    c64 += __shfl_xor_sync(kFull, c64, off);
+    l64 += __shfl_xor_sync(kFull, l64, off);
+  }
+  if (lane == 0) {
+    atomicAdd(&p.ctr->coins, c64);
+    atomicAdd(&p.ctr->live, l64);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // K-GIANT: block-per-RR continuation for sets that outgrew the warp queue (the role of the
 // paper's reservoir queue Q_res, Alg. 4/5). Per-block global bitmap (Visited[n])
 // and global queue (capacity n, entries kEmpty when unused). No level barriers: the 16 warps
@@ -561,14 +703,40 @@ static cudaError_t launch_rr_t(const RRParams& p, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int SCHEME>
+static cudaError_t launch_lt_t(const RRParams& p, int grid, cudaStream_t s) {
+  const int smem = kLtWarps * kLtCap * 32 * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_rr_lt_lane<SCHEME>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_rr_lt_lane<SCHEME><<<grid, kLtWarps * 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_rr_lt(int scheme, const RRParams& p, int grid, cudaStream_t s) {
+  if (scheme == W_WC) return launch_lt_t<W_WC>(p, grid, s);
+  return launch_lt_t<W_EXPLICIT>(p, grid, s);
+}
+
+// resident CTAs per SM of the LT lane kernel (the host sizes the spill buffer from it)
+int lt_blocks_per_sm() {
+  int bps = 1;
+  const int smem = kLtWarps * kLtCap * 32 * 4;
+  cudaFuncSetAttribute(k_rr_lt_lane<W_WC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_rr_lt_lane<W_WC>, kLtWarps * 32, smem);
+  return bps > 0 ? bps : 1;
+}
+
 cudaError_t launch_rr_warp(int model, int scheme, const RRParams& p, int grid, cudaStream_t s) {
   if (model == MODEL_IC) {
     if (scheme == W_WC) return launch_rr_t<MODEL_IC, W_WC>(p, grid, s);
     if (scheme == W_UNIFORM) return launch_rr_t<MODEL_IC, W_UNIFORM>(p, grid, s);
     return launch_rr_t<MODEL_IC, W_EXPLICIT>(p, grid, s);
   }
-  if (scheme == W_WC) return launch_rr_t<MODEL_LT, W_WC>(p, grid, s);
-  return launch_rr_t<MODEL_LT, W_EXPLICIT>(p, grid, s);
+  return launch_rr_lt(scheme, p, grid, s);
 }
 
 cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,

@@ -130,13 +130,15 @@ __device__ __forceinline__ uint32_t warp_owner(uint32_t P, uint32_t i) {
 // time; the owning set of a member is found with a 5-step shuffle search.
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_inv_scatter(const uint64_t* __restrict__ offsets,
-                                                     const uint32_t* __restrict__ pool, uint32_t nsets,
+                                                     const uint32_t* __restrict__ pool, uint32_t set0,
+                                                     uint32_t nsets_end,
                                                      const uint64_t* __restrict__ inv_off,
                                                      uint32_t* __restrict__ cursor,
                                                      uint32_t* __restrict__ inv) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t r0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u; r0 < nsets;
+  const uint32_t nsets = nsets_end;
+  for (uint32_t r0 = set0 + (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u; r0 < nsets;
        r0 += nwarps * 32u) {
     const uint32_t nr = min(32u, nsets - r0);
     const uint64_t base = offsets[r0];
@@ -152,6 +154,16 @@ __global__ void __launch_bounds__(256) k_inv_scatter(const uint64_t* __restrict_
         inv[inv_off[v] + pos] = r0 + k;
       }
     }
+  }
+}
+
+// Per-segment histogram without atomics: delta[v] = count_total[v] - snap[v]; snap := count_total.
+__global__ void __launch_bounds__(256) k_count_delta(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ snap,
+                                                     uint32_t* __restrict__ delta, uint32_t n) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t c = cnt[v];
+    delta[v] = c - snap[v];
+    snap[v] = c;
   }
 }
 
@@ -239,22 +251,54 @@ __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int3
 // flattening members within a warp (measured 19 vs 94 us per step on C3).
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restrict__ keys, int j,
-                                               const uint64_t* __restrict__ inv_off,
-                                               const uint32_t* __restrict__ inv,
+                                               const InvSegDev* __restrict__ segs,
+                                               const uint32_t* __restrict__ nseg_ptr_unused,
                                                const uint64_t* __restrict__ offsets,
                                                const uint32_t* __restrict__ pool,
                                                uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
                                                int32_t* __restrict__ dec) {
+  __shared__ uint64_t s_lo[kMaxInvSeg], s_end[kMaxInvSeg];   // list start, inclusive prefix end
+  __shared__ const uint32_t* s_inv[kMaxInvSeg];
+  __shared__ uint32_t s_nseg;
   const uint32_t sub = threadIdx.x & 7;
   const uint32_t u = ~(uint32_t)keys[j];
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[u] = kSent;   // retire the pick (never decremented)
-  const uint64_t lo = inv_off[u], hi = inv_off[u + 1];
+  if (threadIdx.x < 32) {                     // lanes load the segments' list bounds in parallel
+    const uint32_t l = threadIdx.x;
+    InvSegDev sg{nullptr, nullptr};
+    if (l < (uint32_t)kMaxInvSeg) sg = segs[l];  // unused slots are null: no dependency on nseg
+    uint64_t lo = 0, len = 0;
+    if (sg.off) {
+      lo = sg.off[u];
+      len = sg.off[u + 1] - lo;
+    }
+    uint64_t incl = len;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint64_t y = __shfl_up_sync(kFull, incl, off);
+      if (l >= (uint32_t)off) incl += y;
+    }
+    if (l < (uint32_t)kMaxInvSeg) {
+      s_lo[l] = lo;
+      s_end[l] = incl;
+      s_inv[l] = sg.inv;
+    }
+    const uint32_t used = __ballot_sync(kFull, sg.off != nullptr);   // warp-wide vote
+    if (l == 0) s_nseg = __popc(used);
+  }
+  __syncthreads();
+  const uint32_t ns = s_nseg;
+  const uint64_t total = ns ? s_end[kMaxInvSeg - 1] : 0;
   const uint64_t ngroups = (uint64_t)gridDim.x * (blockDim.x >> 3);
-  for (uint64_t t = lo + blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); t < hi; t += ngroups) {
-    const uint32_t r = inv[t];
-    if (covered[r]) continue;
-    if (sub == 0) covered[r] = 1;      // each r appears once in inv[u]: no race
+  uint32_t q = 0;
+  for (uint64_t t = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); t < total; t += ngroups) {
+    while (t >= s_end[q]) ++q;                 // t increases monotonically per group
+    const uint64_t pos = s_lo[q] + (t - (q ? s_end[q - 1] : 0));
+    const uint32_t r = s_inv[q][pos];
+    const uint8_t cov = covered[r];            // flag and offsets loaded together
     const uint64_t a = offsets[r], b = offsets[r + 1];
+    if (cov) continue;
+    if (sub == 0) covered[r] = 1;      // each r appears once across the lists of u: no race
     if (dec == nullptr) {
       for (uint64_t e = a + sub; e < b; e += 8) {
         const uint32_t w = pool[e];
@@ -288,10 +332,16 @@ cudaError_t launch_scan_u32(const uint32_t* in, uint64_t count, uint64_t* out, u
   return cudaGetLastError();
 }
 
-cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, uint32_t nsets,
+cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, uint32_t set0, uint32_t set1,
                                const uint64_t* inv_off, uint32_t* cursor, uint32_t* inv, int grid,
                                cudaStream_t s) {
-  k_inv_scatter<<<grid, 256, 0, s>>>(offsets, pool, nsets, inv_off, cursor, inv);
+  k_inv_scatter<<<grid, 256, 0, s>>>(offsets, pool, set0, set1, inv_off, cursor, inv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* delta, uint32_t n, int grid,
+                               cudaStream_t s) {
+  k_count_delta<<<grid, 256, 0, s>>>(cnt, snap, delta, n);
   return cudaGetLastError();
 }
 
@@ -301,117 +351,11 @@ cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long
   return cudaGetLastError();
 }
 
-cudaError_t launch_cover(const unsigned long long* keys, int j, const uint64_t* inv_off,
-                         const uint32_t* inv, const uint64_t* offsets, const uint32_t* pool,
+cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,
+                         const uint64_t* offsets, const uint32_t* pool,
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s) {
-  k_cover<<<grid, 256, 0, s>>>(keys, j, inv_off, inv, offsets, pool, covered, cnt, dec);
+  k_cover<<<grid, 256, 0, s>>>(keys, j, segs, nseg, offsets, pool, covered, cnt, dec);
   return cudaGetLastError();
-}
-
-
-// ==========================================================================================
-// K-SELECT: the whole k-step NodeSelection (P = 1) in ONE cooperative persistent kernel — the
-// k greedy steps iterate on-device without host round trips or per-step launches:
-//   phase A (all CTAs): streaming argmax of (count << 32 | ~v) over unselected nodes (lowest id
-//       wins ties, reading R10), one atomicMax per CTA into keys[j];   grid.sync();
-//   phase B (all warps): cover inv[u_j]: flag each uncovered set and decrement its members
-//       (Alg. 7 l.11-16, via the inverted index); CTA 0 retires u_j (sentinel);   grid.sync().
-// The count vector (4n bytes, 19 MB on C3) stays L2-resident across steps.
-// ==========================================================================================
-}  // namespace gim
-#include <cooperative_groups.h>
-namespace gim {
-namespace cg = cooperative_groups;
-
-constexpr int kSelThreads = 512;
-
-struct SelParams {
-  uint32_t* cnt;
-  uint32_t n;
-  const uint64_t* inv_off;
-  const uint32_t* inv;
-  const uint64_t* offsets;
-  const uint32_t* pool;
-  uint8_t* covered;
-  unsigned long long* keys;   // zeroed, k entries
-  int k;
-};
-
-__global__ void __launch_bounds__(kSelThreads) k_select_coop(SelParams p) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ unsigned long long s_red[kSelThreads / 32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t gtid = blockIdx.x * kSelThreads + threadIdx.x;
-  const uint32_t gthreads = gridDim.x * kSelThreads;
-  const uint32_t n4 = p.n >> 2;
-  const uint4* c4 = reinterpret_cast<const uint4*>(p.cnt);   // read with __ldcg: mutated in-kernel
-  const uint32_t sub = threadIdx.x & 7;
-  const uint64_t ngroups = (uint64_t)gridDim.x * (kSelThreads / 8);
-  const uint64_t gg = (uint64_t)blockIdx.x * (kSelThreads / 8) + (threadIdx.x >> 3);
-  for (int j = 0; j < p.k; ++j) {
-    unsigned long long best = 0;
-    for (uint32_t i0 = gtid; i0 < n4; i0 += 4 * gthreads) {
-      uint4 x[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t i = i0 + q * gthreads;
-        x[q] = (i < n4) ? __ldcg(c4 + i) : make_uint4(kSent, kSent, kSent, kSent);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t v = (i0 + q * gthreads) << 2;
-        argmax_one(x[q].x, v, best);
-        argmax_one(x[q].y, v + 1, best);
-        argmax_one(x[q].z, v + 2, best);
-        argmax_one(x[q].w, v + 3, best);
-      }
-    }
-    for (uint32_t v = (n4 << 2) + gtid; v < p.n; v += gthreads) argmax_one(__ldcg(p.cnt + v), v, best);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const unsigned long long o = __shfl_xor_sync(kFull, best, off);
-      best = o > best ? o : best;
-    }
-    if (lane == 0) s_red[warp] = best;
-    __syncthreads();
-    if (warp == 0) {
-      best = (lane < kSelThreads / 32) ? s_red[lane] : 0ull;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const unsigned long long o = __shfl_xor_sync(kFull, best, off);
-        best = o > best ? o : best;
-      }
-      if (lane == 0 && best) atomicMax(p.keys + j, best);
-    }
-    grid.sync();
-    const uint32_t u = ~(uint32_t)__ldcg(p.keys + j);
-    if (gtid == 0) p.cnt[u] = kSent;          // retire the pick (never decremented by cover)
-    const uint64_t lo = p.inv_off[u], hi = p.inv_off[u + 1];
-    for (uint64_t t = lo + gg; t < hi; t += ngroups) {
-      const uint32_t r = p.inv[t];
-      if (__ldcg(p.covered + r)) continue;
-      if (sub == 0) p.covered[r] = 1;
-      const uint64_t a = p.offsets[r], b = p.offsets[r + 1];
-      for (uint64_t e = a + sub; e < b; e += 8) {
-        const uint32_t w = p.pool[e];
-        if (w != u) atomicSub(p.cnt + w, 1u);
-      }
-    }
-    grid.sync();
-  }
-}
-
-cudaError_t launch_select_coop(uint32_t* cnt, uint32_t n, const uint64_t* inv_off, const uint32_t* inv,
-                               const uint64_t* offsets, const uint32_t* pool, uint8_t* covered,
-                               unsigned long long* keys, int k, int num_sms, cudaStream_t s) {
-  SelParams p{cnt, n, inv_off, inv, offsets, pool, covered, keys, k};
-  int bps = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_select_coop, kSelThreads, 0);
-  if (e != cudaSuccess) return e;
-  if (bps < 1) return cudaErrorCooperativeLaunchTooLarge;
-  dim3 grid(num_sms * (bps < 4 ? bps : 4)), block(kSelThreads);
-  void* args[] = {&p};
-  return cudaLaunchCooperativeKernel((void*)k_select_coop, grid, block, args, 0, s);
 }
 
 }  // namespace gim

@@ -97,14 +97,16 @@ def test_pool_parity_C1_invariance(opts):
         assert c.stats()["giant_sets"] == T
 
 
-@pytest.mark.parametrize("steps,graph", [(1, 1), (1, 0), (0, 0)])
-def test_pool_parity_C2_and_select(steps, graph):
-    """k = 50 selection through the per-step argmax/cover launches replayed from a CUDA graph
-    (default), launched one by one, and the cooperative k-step kernel."""
+@pytest.mark.parametrize("graph,segs", [(1, 1), (0, 1), (1, 0)])
+def test_pool_parity_C2_and_select(graph, segs):
+    """k = 50 selection through the argmax/cover launches replayed from a CUDA graph (default)
+    and launched one by one; pool generated in several calls (several index segments)."""
     w = gi.WORKLOADS["C2"]
     g = gi.workload_graph("C2")
     T = 30011
-    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_STEPS: steps, P.OPT_SELECT_GRAPH: graph})
+    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_GRAPH: graph, P.OPT_INV_SEGMENTS: segs})
+    for t in (1000, 7000, 7001, 20000):
+        c.generate_rr(t, w.rr_seed)
     c.generate_rr(T, w.rr_seed)
     o = oracle.Oracle(g, w.model, w.scheme)
     o.generate(T, w.rr_seed)
@@ -129,10 +131,10 @@ def test_extend_truncate_reseed():
         _same_pool(c, o, T)
 
 
-@pytest.mark.parametrize("steps", [0, 1])
-def test_select_zero_gain_and_k_eq_n(steps):
+@pytest.mark.parametrize("graph", [1, 0])
+def test_select_zero_gain_and_k_eq_n(graph):
     g = gi.diamond()
-    c = _ctx(g, gi.LT, gi.W_WC, opts={P.OPT_SELECT_STEPS: steps})
+    c = _ctx(g, gi.LT, gi.W_WC, opts={P.OPT_SELECT_GRAPH: graph})
     c.generate_rr(16, 200907325)
     s, gns, cov = c.select(4)
     o = oracle.Oracle(g, gi.LT, gi.W_WC)
@@ -244,11 +246,11 @@ def test_full_size_sampled(key):
     mask = np.ones(len(d), dtype=bool)
     mask[starts - 1] = False
     assert np.all(d[mask] > 0)                                       # distinct members
-    # NodeSelection at full size: cooperative k-step kernel == per-step launches; properties
+    # NodeSelection at full size: graph replay == one-by-one launches; properties
     # that hold at any size: first pick is the lowest-id argmax of the counts, gains are
     # non-increasing (greedy on a coverage function), covered = #sets hit by the seeds.
     seeds, gains, cov = c.select(w.k)
-    c.set_option(P.OPT_SELECT_STEPS, 0)
+    c.set_option(P.OPT_SELECT_GRAPH, 0)
     s2, g2, c2 = c.select(w.k)
     assert np.array_equal(seeds, s2) and np.array_equal(gains, g2) and cov == c2
     assert seeds[0] == int(np.argmax(cnt)) and gains[0] == int(cnt.max())

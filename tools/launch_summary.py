@@ -9,7 +9,7 @@ for d in data:
     if d['Metric Name']!='gpu__time_duration.sum': continue
     k=d['Kernel Name'].split('(')[0].replace('void ','')[:40]
     v=float(d['Metric Value'].replace(',',''))
-    u=d['Metric Unit']; v*= {'nsecond':1e-3,'usecond':1,'msecond':1e3,'second':1e6}.get(u,1)
+    u=d['Metric Unit']; v*= {'ns':1e-3,'nsecond':1e-3,'us':1,'usecond':1,'ms':1e3,'msecond':1e3}.get(u,1)
     agg[k][0]+=1; agg[k][1]+=v
 tot=sum(v[1] for v in agg.values())
 print(f"{'kernel':40s} {'launches':>8s} {'total_us':>10s} {'avg_us':>8s} {'share':>6s}")

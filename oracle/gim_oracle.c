@@ -153,23 +153,7 @@ og_ctx* og_create(uint32_t n, uint64_t m, const uint64_t* row_ptr, const uint32_
       c->thr_edge[e] = (model == OG_LT) ? (uint64_t)floor(x) : (uint64_t)ceil(x);
     }
   }
-  /* out-CSR (transpose), used only by og_mc_spread */
-  c->out_ptr = (uint64_t*)calloc(n + 1, sizeof(uint64_t));
-  c->out_dst = (uint32_t*)malloc(sizeof(uint32_t) * (m ? m : 1));
-  c->out_in_slot = (uint64_t*)malloc(sizeof(uint64_t) * (m ? m : 1));
-  for (e = 0; e < m; ++e) c->out_ptr[src[e] + 1]++;
-  for (v = 0; v < n; ++v) c->out_ptr[v + 1] += c->out_ptr[v];
-  {
-    uint64_t* cur = (uint64_t*)malloc(sizeof(uint64_t) * n);
-    memcpy(cur, c->out_ptr, sizeof(uint64_t) * n);
-    for (v = 0; v < n; ++v)
-      for (e = row_ptr[v]; e < row_ptr[v + 1]; ++e) {
-        uint64_t pos = cur[src[e]]++;
-        c->out_dst[pos] = v;
-        c->out_in_slot[pos] = e;
-      }
-    free(cur);
-  }
+  /* the out-CSR (transpose) used by og_mc_spread is built on first use */
   c->visited = (uint8_t*)calloc(n, 1);
   c->queue = (uint32_t*)malloc(sizeof(uint32_t) * n);
   c->cap_sets = 1024;
@@ -438,6 +422,26 @@ int og_imm(og_ctx* c, uint32_t k, double eps, double ell, uint64_t seed, uint32_
  * its active in-neighbours reaches tau_v (iterated to the fixpoint, which is order-free).
  * Randomness: Philox keyed (mc_seed; trial, tag-11 slot), independent of any RR stream.
  * ------------------------------------------------------------------------------------------ */
+static void build_out_csr(og_ctx* c) {
+  uint64_t e, *cur;
+  uint32_t v, n = c->n;
+  if (c->out_ptr) return;
+  c->out_ptr = (uint64_t*)calloc(n + 1, sizeof(uint64_t));
+  c->out_dst = (uint32_t*)malloc(sizeof(uint32_t) * (c->m ? c->m : 1));
+  c->out_in_slot = (uint64_t*)malloc(sizeof(uint64_t) * (c->m ? c->m : 1));
+  for (e = 0; e < c->m; ++e) c->out_ptr[c->src[e] + 1]++;
+  for (v = 0; v < n; ++v) c->out_ptr[v + 1] += c->out_ptr[v];
+  cur = (uint64_t*)malloc(sizeof(uint64_t) * n);
+  memcpy(cur, c->out_ptr, sizeof(uint64_t) * n);
+  for (v = 0; v < n; ++v)
+    for (e = c->row_ptr[v]; e < c->row_ptr[v + 1]; ++e) {
+      uint64_t pos = cur[c->src[e]]++;
+      c->out_dst[pos] = v;
+      c->out_in_slot[pos] = e;
+    }
+  free(cur);
+}
+
 static double edge_p(const og_ctx* c, uint64_t in_slot, uint32_t v) {
   if (c->scheme == OG_W_WC) return 1.0 / (double)deg_in(c, v);
   if (c->scheme == OG_W_UNIFORM) return (double)c->p_uniform;
@@ -452,6 +456,7 @@ int og_mc_spread(og_ctx* c, const uint32_t* S, uint32_t k, uint64_t trials, uint
   uint32_t* touched = (uint32_t*)malloc(sizeof(uint32_t) * (c->m + c->n + 1));
   double sum = 0.0, sum2 = 0.0;
   uint64_t t;
+  build_out_csr(c);
   for (t = 0; t < trials; ++t) {
     uint32_t head = 0, tail = 0, ntouch = 0, i;
     for (i = 0; i < k; ++i)

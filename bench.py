@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--opt", action="append", default=[], help="library option NAME=VALUE (ablations)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo + --same-device: functional multi-rank test on 1 GPU)")
+    ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (functional testing)")
     return ap.parse_args()
 
 
@@ -185,8 +188,13 @@ def run_gim(args, w):
     import paper_2009_07325_b200 as P
 
     world, rank, local = dist_env()
+    if args.same_device:
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     g = gi.workload_graph(w.key)
     stream = torch.cuda.Stream(local)
@@ -207,7 +215,7 @@ def run_gim(args, w):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if args.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

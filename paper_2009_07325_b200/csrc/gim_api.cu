@@ -81,7 +81,6 @@ struct gim_ctx {
   int inv_segmented = 1;        // GIM_OPT_INV_SEGMENTS
   DevBuf cnt_snap;              // count_total at the last indexed chunk
   DevBuf seg_desc;              // device InvSegDev[kMaxInvSeg] + uint32 nseg
-  InvSegDev* h_desc = nullptr;  // pinned mirror
   // options
   int force_giant = 0, profile = 0;
   uint32_t qcap = kQMax;
@@ -527,13 +526,14 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
     c->inv_valid = true;
   }
   TRY(ensure(c, c->seg_desc, sizeof(InvSegDev) * kMaxInvSeg + 16));
-  if (!c->h_desc) CK(cudaMallocHost(&c->h_desc, sizeof(InvSegDev) * kMaxInvSeg + 16));
-  for (size_t q = 0; q < (size_t)kMaxInvSeg; ++q)
-    c->h_desc[q] = q < c->iseg.size() ? InvSegDev{c->iseg[q].off.as<uint64_t>(), c->iseg[q].inv.as<uint32_t>()}
-                                      : InvSegDev{nullptr, nullptr};
-  *reinterpret_cast<uint32_t*>(c->h_desc + kMaxInvSeg) = (uint32_t)c->iseg.size();
-  CK(cudaMemcpyAsync(c->seg_desc.p, c->h_desc, sizeof(InvSegDev) * kMaxInvSeg + 4, cudaMemcpyHostToDevice,
-                     c->stream));
+  {
+    InvSegDev tab[kMaxInvSeg];
+    for (size_t q = 0; q < c->iseg.size(); ++q)
+      tab[q] = InvSegDev{c->iseg[q].off.as<uint64_t>(), c->iseg[q].inv.as<uint32_t>()};
+    TRY(launched(c, launch_set_segs(tab, (uint32_t)c->iseg.size(), c->seg_desc.as<InvSegDev>(),
+                                    reinterpret_cast<uint32_t*>(c->seg_desc.as<InvSegDev>() + kMaxInvSeg),
+                                    c->stream), "k_set_segs"));
+  }
   const InvSegDev* segd = c->seg_desc.as<InvSegDev>();
   const uint32_t* nsegd = reinterpret_cast<const uint32_t*>(segd + kMaxInvSeg);
   CK(cudaMemcpyAsync(c->cnt.p, c->count_total.p, n * 4, cudaMemcpyDeviceToDevice, c->stream));
@@ -587,7 +587,6 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
   }
   if (c->h_keys_cap < k) {
     if (c->h_keys) cudaFreeHost(c->h_keys);
-  if (c->h_desc) cudaFreeHost(c->h_desc);
     c->h_keys = nullptr;
     CK(cudaMallocHost(&c->h_keys, (uint64_t)k * 8));
     c->h_keys_cap = k;
@@ -697,7 +696,6 @@ void gim_destroy(gim_ctx* c) {
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
   if (c->h_u64) cudaFreeHost(c->h_u64);
   if (c->h_keys) cudaFreeHost(c->h_keys);
-  if (c->h_desc) cudaFreeHost(c->h_desc);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   cudaGetLastError();
   delete c;

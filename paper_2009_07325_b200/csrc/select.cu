@@ -339,6 +339,25 @@ cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, ui
   return cudaGetLastError();
 }
 
+// Writes the segment descriptor table from a by-value parameter (no host staging buffer).
+struct SegTable {
+  InvSegDev seg[kMaxInvSeg];
+  uint32_t nseg;
+};
+__global__ void k_set_segs(SegTable t, InvSegDev* out, uint32_t* nseg_out) {
+  if (threadIdx.x < kMaxInvSeg) out[threadIdx.x] = t.seg[threadIdx.x];
+  if (threadIdx.x == 0) *nseg_out = t.nseg;
+}
+
+cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, InvSegDev* out, uint32_t* nseg_out,
+                            cudaStream_t s) {
+  SegTable t;
+  for (int q = 0; q < kMaxInvSeg; ++q) t.seg[q] = (q < (int)nseg) ? segs[q] : InvSegDev{nullptr, nullptr};
+  t.nseg = nseg;
+  k_set_segs<<<1, 32, 0, s>>>(t, out, nseg_out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* delta, uint32_t n, int grid,
                                cudaStream_t s) {
   k_count_delta<<<grid, 256, 0, s>>>(cnt, snap, delta, n);

@@ -149,7 +149,8 @@ class Gim:
                 return None
 
         def _free(ptr, stream, user):
-            torch.cuda.caching_allocator_delete(ptr)
+            if torch is not None and getattr(torch, "cuda", None) is not None:   # interpreter teardown
+                torch.cuda.caching_allocator_delete(ptr)
 
         a, f = ALLOC_FN(_alloc), FREE_FN(_free)
         self._keep += [a, f]
@@ -260,7 +261,12 @@ def torch_allreduce(group=None, device: str = "cuda"):
         t = torch.as_tensor(_View(), device="cuda")
         s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
         with torch.cuda.stream(s):
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+            if dist.get_backend(group) == "gloo":     # functional testing: stage through host
+                h = t.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
         return 0
 
     return fn

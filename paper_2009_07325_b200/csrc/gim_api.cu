@@ -358,7 +358,8 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     c->stage_cap = c->staging_init;
   } else {
     const double mean = c->nsets ? (double)c->pool_len / (double)c->nsets : 32.0;
-    const uint64_t want = (uint64_t)(mean * (double)cnt * 1.25) + (1u << 20);
+    const uint64_t want = (uint64_t)(mean * (double)cnt * 1.25) + (1u << 20) +
+                          (uint64_t)c->num_sms * 64 * kStageChunk;   // per-warp chunk slack
     if (c->stage_cap < want && !c->staging_init) {
       TRY(dalloc(c, c->staging, want * 4));
       c->stage_cap = c->staging.bytes / 4;

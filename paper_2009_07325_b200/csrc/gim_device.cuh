@@ -152,6 +152,15 @@ constexpr int kRRIlp = GIM_RR_ILP;    // Philox chains per lane per iteration (1
 constexpr int kHubIlp = GIM_HUB_ILP;  // Philox chains per lane per step on a hub node
 constexpr uint32_t kHubGroups = 32u * GIM_HUB_ILP;   // nodes with >= this many slot groups are hubs
 constexpr int kGiantThreads = 512;
+#ifndef GIM_CLAIM_BATCH
+#define GIM_CLAIM_BATCH 1
+#endif
+#ifndef GIM_CLAIM_TAIL_DIV
+#define GIM_CLAIM_TAIL_DIV 4
+#endif
+constexpr uint32_t kClaimBatch = GIM_CLAIM_BATCH;       // RR ids claimed per warp per atomic
+constexpr uint32_t kClaimTailDiv = GIM_CLAIM_TAIL_DIV;  // last count/div ids claimed one by one
+constexpr uint32_t kStageChunk = 1024;    // staging elements reserved per warp per atomic
 constexpr int kLtWarps = 8;          // K-LT: warps per CTA
 constexpr int kLtCap = 64;           // K-LT: path entries per lane in shared memory
 constexpr int kLtCap2 = 512;         // K-LT: max path per lane (shared + global spill)

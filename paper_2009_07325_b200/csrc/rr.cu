@@ -201,10 +201,20 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
   const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
   uint32_t coins = 0, lives = 0;    // 32-bit per-warp counters, flushed before they can wrap
 
+  uint32_t claim_next = 0, claim_end = 0;            // ids claimed kClaimBatch at a time
+  unsigned long long chunk_off = 0;                  // this warp's staging chunk
+  uint32_t chunk_left = 0;
   while (true) {
-    uint32_t i = 0;
-    if (lane == 0) i = atomicAdd(&p.ctr->claim, 1u);
-    i = __shfl_sync(kFull, i, 0);
+    if (claim_next == claim_end) {
+      // batches amortise the shared counter (tiny sets); single ids near the end keep the
+      // heavy-tailed last sets from piling up on one warp
+      const uint32_t batch = (claim_end < p.count - p.count / kClaimTailDiv) ? kClaimBatch : 1u;
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&p.ctr->claim, batch);
+      claim_next = __shfl_sync(kFull, base, 0);
+      claim_end = claim_next + batch;
+    }
+    const uint32_t i = claim_next++;
     if (i >= p.count) break;
     const uint32_t item = p.item_list ? p.item_list[i] : i;
     if (p.force_giant) {
@@ -324,9 +334,16 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
         p.giant_recs[atomicAdd(&p.ctr->giant_count, 1u)] =
             fits ? GiantRec{item, tail, resume, 0u, off} : GiantRec{item, 0u, 0u, 0u, 0ull};
     } else {
-      unsigned long long off = 0;
-      if (lane == 0) off = atomicAdd(&p.ctr->stage_tail, (unsigned long long)tail);
-      off = __shfl_sync(kFull, off, 0);
+      if (tail > chunk_left) {                       // reserve a new staging chunk
+        const uint32_t want = max(tail, kStageChunk);
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&p.ctr->stage_tail, (unsigned long long)want);
+        chunk_off = __shfl_sync(kFull, base, 0);
+        chunk_left = want;
+      }
+      const unsigned long long off = chunk_off;
+      chunk_off += tail;
+      chunk_left -= tail;
       if (off + tail > p.stage_cap) {
         if (lane == 0) p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = item;
       } else {
@@ -392,6 +409,8 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
   bool active = false, want = true;       // want: lane needs a new walk
   uint32_t coins = 0, lives = 0;
   const uint32_t cap = min((uint32_t)kLtCap2, p.qcap);
+  unsigned long long chunk_off = 0;                  // this warp's staging chunk
+  uint32_t chunk_left = 0;
   while (true) {
     // refill lanes that finished (one claim per warp)
     const uint32_t need = __ballot_sync(kFull, want);
@@ -455,9 +474,16 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
         if (lane >= off) incl += y;
       }
       const uint32_t tot = __shfl_sync(kFull, incl, 31);
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(&p.ctr->stage_tail, (unsigned long long)tot);
-      base = __shfl_sync(kFull, base, 0);
+      if (tot > chunk_left) {                        // reserve a new staging chunk
+        const uint32_t want = max(tot, kStageChunk);
+        unsigned long long b0 = 0;
+        if (lane == 0) b0 = atomicAdd(&p.ctr->stage_tail, (unsigned long long)want);
+        chunk_off = __shfl_sync(kFull, b0, 0);
+        chunk_left = want;
+      }
+      const unsigned long long base = chunk_off;
+      chunk_off += tot;
+      chunk_left -= tot;
       if (finish) {
         const unsigned long long off = base + incl - len;
         if (off + len > p.stage_cap) {

@@ -147,14 +147,18 @@ gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
  *                          NodeSelection from a captured CUDA graph; 0: launch them one by one.
  *  GIM_OPT_INV_SEGMENTS = 1 (default): index each generation chunk's sets as it is stored (one
  *                          inverted-index segment per chunk); 0: rebuild one index over the
- *                          whole pool at every selection (ablation). */
+ *                          whole pool at every selection (ablation).
+ *  GIM_OPT_ARGMAX_CAND  = 1 (default): for P = 1 and n >= 2^23 the per-step argmax scans a candidate list of
+ *                          <= 65536 nodes (count >= a power-of-two threshold) and falls back to
+ *                          the full scan once no candidate reaches the threshold; 0: always full. */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
   GIM_OPT_PROFILE = 3,
   GIM_OPT_STAGING_CAP = 4,
   GIM_OPT_SELECT_GRAPH = 6,
-  GIM_OPT_INV_SEGMENTS = 7
+  GIM_OPT_INV_SEGMENTS = 7,
+  GIM_OPT_ARGMAX_CAND = 8
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

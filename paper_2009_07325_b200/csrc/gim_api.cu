@@ -81,6 +81,8 @@ struct gim_ctx {
   int inv_segmented = 1;        // GIM_OPT_INV_SEGMENTS
   DevBuf cnt_snap;              // count_total at the last indexed chunk
   DevBuf seg_desc;              // device InvSegDev[kMaxInvSeg] + uint32 nseg
+  DevBuf cand;                  // argmax candidates + hist[33] + tau_p1 + ncand
+  int use_cand = 1;             // GIM_OPT_ARGMAX_CAND
   // options
   int force_giant = 0, profile = 0;
   uint32_t qcap = kQMax;
@@ -546,10 +548,25 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
     if (c->arfn(c->cnt.p, n, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(count) failed");
   }
   auto* keys = reinterpret_cast<unsigned long long*>(c->keys.p);
+  // P = 1: candidate list for the argmax (at most kMaxCand nodes whose initial count reaches
+  // tau_p1); the full-scan argmax runs only once no candidate reaches tau_p1
+  const uint32_t kMaxCand = 1u << 16;
+  uint32_t* cand = nullptr;
+  unsigned int *hist = nullptr, *ncand = nullptr;
+  uint32_t* tau_p1 = nullptr;
+  if (!dec && c->use_cand && n >= (1u << 23)) {   // small n: the full scan is cheaper than a launch
+    TRY(ensure(c, c->cand, (uint64_t)kMaxCand * 4 + 64 * 4));
+    cand = c->cand.as<uint32_t>();
+    hist = reinterpret_cast<unsigned int*>(cand + kMaxCand);
+    tau_p1 = reinterpret_cast<uint32_t*>(hist + 40);
+    ncand = reinterpret_cast<unsigned int*>(hist + 41);
+    TRY(launched(c, launch_cand_setup(c->cnt.as<uint32_t>(), c->n, kMaxCand, hist, tau_p1, cand, ncand,
+                                      c->num_sms * 4, c->stream), "candidate setup", 3));
+  }
   if (!dec && c->use_graph) {
     // P = 1: the 2k argmax/cover launches replayed from a CUDA graph (captured once per set of
     // buffer pointers; steady-state IMM runs reuse it), so the GPU runs them back to back.
-    const std::vector<uintptr_t> key = {(uintptr_t)c->cnt.p, (uintptr_t)segd,
+    const std::vector<uintptr_t> key = {(uintptr_t)c->cnt.p, (uintptr_t)segd, (uintptr_t)cand,
                                         (uintptr_t)c->offsets.p, (uintptr_t)c->pool.p, (uintptr_t)c->covered.p,
                                         (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n};
     if (!c->sel_exec || key != c->sel_key) {
@@ -558,7 +575,8 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
       cudaGraph_t graph = nullptr;
       CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       for (uint32_t j = 0; j < k; ++j) {
-        launch_argmax(c->cnt.as<uint32_t>(), nullptr, c->n, keys, (int)j, c->num_sms * 4, c->stream);
+        if (cand) launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream);
+        launch_argmax(c->cnt.as<uint32_t>(), nullptr, c->n, keys, (int)j, tau_p1, c->num_sms * 4, c->stream);
         launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                      c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * 8, c->stream);
       }
@@ -569,13 +587,15 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
       c->sel_key = key;
     }
     Prof pf(c, CLS_SELECT);
-    TRY(launched(c, cudaGraphLaunch(c->sel_exec, c->stream), "selection graph", 2 * (int)k));
+    TRY(launched(c, cudaGraphLaunch(c->sel_exec, c->stream), "selection graph", (cand ? 3 : 2) * (int)k));
   } else {
     for (uint32_t j = 0; j < k; ++j) {
       {
         Prof pf(c, CLS_SELECT);
-        TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, c->n, keys, (int)j, c->num_sms * 4, c->stream),
-                     "k_argmax"));
+        if (cand) TRY(launched(c, launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream),
+                               "k_argmax_cand"));
+        TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, c->n, keys, (int)j, tau_p1, c->num_sms * 4,
+                                      c->stream), "k_argmax"));
         TRY(launched(c, launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                                      c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * 8,
                                      c->stream), "k_cover"));
@@ -680,7 +700,7 @@ void gim_destroy(gim_ctx* c) {
   DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
                     &c->sizes, &c->soff, &c->giant_list, &c->retry_list, &c->item_list, &c->scan_out,
                     &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->bitmaps, &c->gqueues, &c->cnt,
-                    &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc};
+                    &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand};
   for (auto& sg : c->iseg) {
     dfree(c, sg.off);
     dfree(c, sg.inv);
@@ -950,6 +970,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_PROFILE: c->profile = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_SELECT_GRAPH: c->use_graph = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_INV_SEGMENTS: c->inv_segmented = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_ARGMAX_CAND: c->use_cand = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_STAGING_CAP:
       if (value < 0) return fail(c, GIM_EINVAL, "staging cap must be >= 0");
       c->staging_init = (uint64_t)value;

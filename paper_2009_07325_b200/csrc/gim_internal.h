@@ -30,7 +30,11 @@ cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, InvSegDev* out
 cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* delta, uint32_t n, int grid,
                                cudaStream_t s);
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
-                          int grid, cudaStream_t s);
+                          const uint32_t* tau_p1, int grid, cudaStream_t s);
+cudaError_t launch_cand_setup(const uint32_t* cnt, uint32_t n, uint32_t kmax, unsigned int* hist,
+                              uint32_t* tau_p1, uint32_t* cand, unsigned int* ncand, int grid, cudaStream_t s);
+cudaError_t launch_argmax_cand(const uint32_t* cnt, const uint32_t* cand, const unsigned int* ncand,
+                               unsigned long long* keys, int j, int grid, cudaStream_t s);
 struct InvSegDev;
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,
                          const uint64_t* offsets, const uint32_t* pool,

@@ -178,8 +178,11 @@ __device__ __forceinline__ void argmax_one(uint32_t c, uint32_t v, unsigned long
 }
 
 __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int32_t* __restrict__ dec,
-                                                uint32_t n, unsigned long long* __restrict__ keys, int j) {
-  (void)j;
+                                                uint32_t n, unsigned long long* __restrict__ keys, int j,
+                                                const uint32_t* __restrict__ tau_p1) {
+  // candidate mode: the candidate argmax already found a count >= tau_p1, which no node outside
+  // the candidate list can reach (their counts started below it and only decrease)
+  if (tau_p1 != nullptr && (uint32_t)(keys[j] >> 32) >= *tau_p1 && keys[j] != 0ull) return;
   __shared__ unsigned long long s_best[8];
   unsigned long long best = 0;
   const uint32_t n4 = n >> 2;
@@ -224,6 +227,82 @@ __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int3
     uint32_t c = cnt[v];
     if (dec != nullptr && c != kSent && dec[v]) { c -= (uint32_t)dec[v]; dec[v] = 0; cnt[v] = c; }
     argmax_one(c, v, best);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+    best = o > best ? o : best;
+  }
+  if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    best = (threadIdx.x < (blockDim.x >> 5)) ? s_best[threadIdx.x] : 0ull;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+      best = o > best ? o : best;
+    }
+    if (threadIdx.x == 0 && best) atomicMax(keys + j, best);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Candidate list for the argmax (P = 1): tau_p1 = 2^B - 1 for the smallest B such that at most
+// kMaxCand nodes have count >= 2^B - 1 (log2-bucket histogram), and cand = those nodes.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_cnt_hist(const uint32_t* __restrict__ cnt, uint32_t n,
+                                                  unsigned int* __restrict__ hist) {
+  __shared__ unsigned int h[33];
+  if (threadIdx.x < 33) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t c = cnt[v];
+    atomicAdd(&h[31 - __clz(c + 1u)], 1u);           // bucket floor(log2(c + 1)), 0..32
+  }
+  __syncthreads();
+  if (threadIdx.x < 33 && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void k_pick_tau(const unsigned int* __restrict__ hist, uint32_t kmax, uint32_t* tau_p1,
+                           unsigned int* ncand) {
+  unsigned long long cum = 0;
+  uint32_t B = 33;
+  for (int b = 32; b >= 0; --b) {
+    cum += hist[b];
+    if (cum > kmax) break;
+    B = (uint32_t)b;
+  }
+  // nodes in buckets >= B are candidates: count >= 2^B - 1 (B = 0: every node)
+  *tau_p1 = (B >= 32) ? 0xFFFFFFFFu : ((1u << B) - 1u);
+  *ncand = 0;
+}
+
+__global__ void __launch_bounds__(256) k_cand_compact(const uint32_t* __restrict__ cnt, uint32_t n,
+                                                      const uint32_t* __restrict__ tau_p1,
+                                                      uint32_t* __restrict__ cand, unsigned int* ncand) {
+  const uint32_t t = *tau_p1;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < n; v0 += gridDim.x * blockDim.x) {
+    const uint32_t v = v0 + threadIdx.x;
+    const bool take = v < n && cnt[v] >= t && t != 0xFFFFFFFFu;
+    const uint32_t m = __ballot_sync(kFull, take);
+    uint32_t base = 0;
+    if (lane == 0 && m) base = atomicAdd(ncand, (unsigned int)__popc(m));
+    base = __shfl_sync(kFull, base, 0);
+    if (take) cand[base + __popc(m & ((1u << lane) - 1u))] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_argmax_cand(const uint32_t* __restrict__ cnt,
+                                                     const uint32_t* __restrict__ cand,
+                                                     const unsigned int* __restrict__ ncand,
+                                                     unsigned long long* __restrict__ keys, int j) {
+  __shared__ unsigned long long s_best[8];
+  const uint32_t nc = *ncand;
+  unsigned long long best = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+    const uint32_t v = cand[i];
+    argmax_one(cnt[v], v, best);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -365,8 +444,24 @@ cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* de
 }
 
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
-                          int grid, cudaStream_t s) {
-  k_argmax<<<grid, 256, 0, s>>>(cnt, dec, n, keys, j);
+                          const uint32_t* tau_p1, int grid, cudaStream_t s) {
+  k_argmax<<<grid, 256, 0, s>>>(cnt, dec, n, keys, j, tau_p1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cand_setup(const uint32_t* cnt, uint32_t n, uint32_t kmax, unsigned int* hist,
+                              uint32_t* tau_p1, uint32_t* cand, unsigned int* ncand, int grid, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(hist, 0, 33 * sizeof(unsigned int), s);
+  if (e != cudaSuccess) return e;
+  k_cnt_hist<<<grid, 256, 0, s>>>(cnt, n, hist);
+  k_pick_tau<<<1, 1, 0, s>>>(hist, kmax, tau_p1, ncand);
+  k_cand_compact<<<grid, 256, 0, s>>>(cnt, n, tau_p1, cand, ncand);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_argmax_cand(const uint32_t* cnt, const uint32_t* cand, const unsigned int* ncand,
+                               unsigned long long* keys, int j, int grid, cudaStream_t s) {
+  k_argmax_cand<<<grid, 256, 0, s>>>(cnt, cand, ncand, keys, j);
   return cudaGetLastError();
 }
 

@@ -98,14 +98,15 @@ def test_pool_parity_C1_invariance(opts):
         assert c.stats()["giant_sets"] == T
 
 
-@pytest.mark.parametrize("graph,segs", [(1, 1), (0, 1), (1, 0)])
-def test_pool_parity_C2_and_select(graph, segs):
+@pytest.mark.parametrize("graph,segs,cand", [(1, 1, 1), (0, 1, 1), (1, 0, 1), (1, 1, 0)])
+def test_pool_parity_C2_and_select(graph, segs, cand):
     """k = 50 selection through the argmax/cover launches replayed from a CUDA graph (default)
     and launched one by one; pool generated in several calls (several index segments)."""
     w = gi.WORKLOADS["C2"]
     g = gi.workload_graph("C2")
     T = 30011
-    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_GRAPH: graph, P.OPT_INV_SEGMENTS: segs})
+    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_GRAPH: graph, P.OPT_INV_SEGMENTS: segs,
+                                         P.OPT_ARGMAX_CAND: cand})
     for t in (1000, 7000, 7001, 20000):
         c.generate_rr(t, w.rr_seed)
     c.generate_rr(T, w.rr_seed)
@@ -253,6 +254,7 @@ def test_full_size_sampled(key):
     # non-increasing (greedy on a coverage function), covered = #sets hit by the seeds.
     seeds, gains, cov = c.select(w.k)
     c.set_option(P.OPT_SELECT_GRAPH, 0)
+    c.set_option(P.OPT_ARGMAX_CAND, 0)
     s2, g2, c2 = c.select(w.k)
     assert np.array_equal(seeds, s2) and np.array_equal(gains, g2) and cov == c2
     assert seeds[0] == int(np.argmax(cnt)) and gains[0] == int(cnt.max())

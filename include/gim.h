@@ -150,7 +150,8 @@ gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
  *                          whole pool at every selection (ablation).
  *  GIM_OPT_ARGMAX_CAND  = 1 (default): for P = 1 and n >= 2^23 the per-step argmax scans a candidate list of
  *                          <= 65536 nodes (count >= a power-of-two threshold) and falls back to
- *                          the full scan once no candidate reaches the threshold; 0: always full. */
+ *                          the full scan once no candidate reaches the threshold; 0: always full;
+ *                          2: candidates whatever n (tests). */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,

@@ -554,7 +554,7 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
   uint32_t* cand = nullptr;
   unsigned int *hist = nullptr, *ncand = nullptr;
   uint32_t* tau_p1 = nullptr;
-  if (!dec && c->use_cand && n >= (1u << 23)) {   // small n: the full scan is cheaper than a launch
+  if (!dec && (c->use_cand == 2 || (c->use_cand == 1 && n >= (1u << 23)))) {   // small n: full scan is cheaper
     TRY(ensure(c, c->cand, (uint64_t)kMaxCand * 4 + 64 * 4));
     cand = c->cand.as<uint32_t>();
     hist = reinterpret_cast<unsigned int*>(cand + kMaxCand);
@@ -970,7 +970,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_PROFILE: c->profile = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_SELECT_GRAPH: c->use_graph = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_INV_SEGMENTS: c->inv_segmented = value ? 1 : 0; return GIM_OK;
-    case GIM_OPT_ARGMAX_CAND: c->use_cand = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_ARGMAX_CAND: c->use_cand = (value < 0 || value > 2) ? 1 : (int)value; return GIM_OK;
     case GIM_OPT_STAGING_CAP:
       if (value < 0) return fail(c, GIM_EINVAL, "staging cap must be >= 0");
       c->staging_init = (uint64_t)value;

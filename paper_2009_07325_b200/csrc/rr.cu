@@ -528,10 +528,16 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
 // sweep of the hub path, and append new nodes with an atomic tail; the set is complete when no
 // node is pending and no warp is busy (the order of expansion cannot change the set).
 // ------------------------------------------------------------------------------------------
+constexpr uint32_t kSplitGroups = 2048;   // hub nodes above this are split across warps
+constexpr uint32_t kChunkRing = 128;      // shared ring of published hub chunks
+constexpr uint32_t kBusySlot = 0xFFFFFFFEu; // ring slot being written (node ids are < 2^32 - 2)
+
 template <int MODEL, int SCHEME>
 __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint32_t* bitmaps,
-                                                            uint32_t* gqueues, uint64_t bm_words) {
+                                                               uint32_t* gqueues, uint64_t bm_words) {
   __shared__ uint32_t s_head, s_tail, s_busy, s_r;
+  __shared__ uint32_t s_chead, s_cres;           // hub-chunk ring: claimed / reserved counters
+  __shared__ uint4 s_ring[kChunkRing];           // {node, a, b, thr}; .x == kEmpty: not yet written
   __shared__ unsigned long long s_off;
   const int lane = threadIdx.x & 31;
   uint32_t* bm = bitmaps + (uint64_t)blockIdx.x * bm_words;
@@ -539,6 +545,7 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
   const uint32_t giant_count = *(volatile unsigned int*)&p.ctr->giant_count;
   const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
   uint32_t coins = 0, lives = 0;
+  for (uint32_t i = threadIdx.x; i < kChunkRing; i += kGiantThreads) s_ring[i].x = kEmpty;
   auto visit = [bm](uint32_t u) {
     const uint32_t bit = 1u << (u & 31);
     return !(atomicOr(&bm[u >> 5], bit) & bit);
@@ -583,14 +590,25 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
         s_head = rec.head;
       }
     }
-    if (threadIdx.x == 0) s_busy = 0;
+    if (threadIdx.x == 0) {
+      s_busy = 0;
+      s_chead = 0;
+      s_cres = 0;
+    }
     __syncthreads();
-    // asynchronous expansion: warps claim queued nodes until none is pending and none is busy
+    // asynchronous expansion: warps claim published hub chunks first, then queued nodes, until
+    // nothing is pending and no warp is busy
     while (true) {
-      uint32_t f = 0, state = 0;                 // state: 1 = got a node, 2 = done
+      uint32_t f = 0, state = 0;                 // 1 = node f, 3 = ring entry f, 2 = done
       if (lane == 0) {
         atomicAdd(&s_busy, 1u);
         while (true) {
+          const uint32_t ch = *(volatile uint32_t*)&s_chead;
+          const uint32_t cr = *(volatile uint32_t*)&s_cres;
+          if (ch < cr) {
+            if (atomicCAS(&s_chead, ch, ch + 1) == ch) { f = ch; state = 3; break; }
+            continue;
+          }
           const uint32_t h = *(volatile uint32_t*)&s_head;
           const uint32_t t = *(volatile uint32_t*)&s_tail;
           if (h < t) {
@@ -603,7 +621,9 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
             __threadfence_block();
             const uint32_t h2 = *(volatile uint32_t*)&s_head;
             const uint32_t t2 = *(volatile uint32_t*)&s_tail;
-            if (h2 < t2) { atomicAdd(&s_busy, 1u); break; }
+            const uint32_t ch2 = *(volatile uint32_t*)&s_chead;
+            const uint32_t cr2 = *(volatile uint32_t*)&s_cres;
+            if (h2 < t2 || ch2 < cr2) { atomicAdd(&s_busy, 1u); break; }
             if (b0 == 0) { state = 2; break; }
             __nanosleep(64);
           }
@@ -613,23 +633,97 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
       state = __shfl_sync(kFull, state, 0);
       if (state == 2) break;
       f = __shfl_sync(kFull, f, 0);
-      // the appender may still be writing the entry: read it at L2 (atomic), sleep while empty
-      uint32_t v = atomicOr(Q + f, 0u);
-      while (v == kEmpty) {
-        __nanosleep(32);
+      uint32_t v, a, b, thr = 0;
+      bool node_start = false;
+      if (state == 3) {                          // a published chunk of a hub node
+        uint4 e;
+        if (lane == 0) {
+          volatile uint4* slot = &s_ring[f % kChunkRing];
+          while ((e.x = slot->x) == kEmpty || e.x == kBusySlot) __nanosleep(32);
+          __threadfence_block();
+          e.y = slot->y; e.z = slot->z; e.w = slot->w;
+          __threadfence_block();
+          slot->x = kEmpty;                      // consumed
+        }
+        v = __shfl_sync(kFull, e.x, 0);
+        a = __shfl_sync(kFull, e.y, 0);
+        b = __shfl_sync(kFull, e.z, 0);
+        thr = __shfl_sync(kFull, e.w, 0);
+      } else {
+        // the appender may still be writing the entry: read it at L2 (atomic), sleep while empty
         v = atomicOr(Q + f, 0u);
+        while (v == kEmpty) {
+          __nanosleep(32);
+          v = atomicOr(Q + f, 0u);
+        }
+        a = __ldg(p.row_ptr + v);
+        b = __ldg(p.row_ptr + v + 1);
+        node_start = true;
       }
-      const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
       if (b > a) {
         if (MODEL == MODEL_IC) {
-          const uint32_t thr = node_thr<SCHEME>(p, b - a);
-          if (lane == 0) coins += b - a;
-          hub_sweep<SCHEME>(p, id_lo, id_hi, a, b, thr, never, lane, lives, [&](uint32_t g, uint32_t m) {
-            uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
-            if (m) ic_take_live(p, g, m, uu, visit);
-            append(uu);
-            return true;
-          });
+          if (node_start) {
+            thr = node_thr<SCHEME>(p, b - a);
+            if (lane == 0) coins += b - a;
+            const uint32_t g_lo = a >> 2, g_hi = (b - 1) >> 2;
+            if (g_hi - g_lo + 1 > kSplitGroups) {  // hub: publish chunks 1.. for idle warps
+              const uint32_t nch = (g_hi - g_lo) / kSplitGroups;   // chunks after the first
+              uint32_t pushed = 0, base = 0;
+              if (lane == 0) {                   // reserve ring room: outstanding <= kChunkRing
+                while (true) {
+                  const uint32_t cr = *(volatile uint32_t*)&s_cres;
+                  const uint32_t ch = *(volatile uint32_t*)&s_chead;
+                  const uint32_t m = min(nch, kChunkRing - (cr - ch));
+                  if (m == 0) break;
+                  if (atomicCAS(&s_cres, cr, cr + m) == cr) { pushed = m; base = cr; break; }
+                }
+              }
+              pushed = __shfl_sync(kFull, pushed, 0);
+              base = __shfl_sync(kFull, base, 0);
+              if (pushed) {
+                for (uint32_t c = lane; c < pushed; c += 32) {
+                  const uint32_t gs = g_lo + (c + 1) * kSplitGroups;
+                  const uint32_t ge = min(g_hi, gs + kSplitGroups - 1);
+                  uint4* slot = &s_ring[(base + c) % kChunkRing];
+                  while (atomicCAS(&slot->x, kEmpty, kBusySlot) != kEmpty) __nanosleep(32);
+                  volatile uint4* vs = slot;
+                  vs->y = max(a, gs << 2);
+                  vs->z = min(b, (ge + 1) << 2);
+                  vs->w = thr;
+                  __threadfence_block();
+                  vs->x = v;                     // publish
+                }
+                // this warp keeps chunk 0 and any chunks that did not fit in the ring
+                const uint32_t kept_end = min(b, (g_lo + kSplitGroups) << 2);   // chunk 0
+                hub_sweep<SCHEME>(p, id_lo, id_hi, a, kept_end, thr, never, lane, lives,
+                                  [&](uint32_t g, uint32_t m) {
+                                    uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
+                                    if (m) ic_take_live(p, g, m, uu, visit);
+                                    append(uu);
+                                    return true;
+                                  });
+                if (pushed < nch) {              // sweep the chunks beyond the pushed ones
+                  const uint32_t rs = (g_lo + (pushed + 1) * kSplitGroups) << 2;
+                  if (rs < b)
+                    hub_sweep<SCHEME>(p, id_lo, id_hi, rs, b, thr, never, lane, lives,
+                                      [&](uint32_t g, uint32_t m) {
+                                        uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
+                                        if (m) ic_take_live(p, g, m, uu, visit);
+                                        append(uu);
+                                        return true;
+                                      });
+                }
+                b = a;                           // done with this node
+              }
+            }
+          }
+          if (b > a)
+            hub_sweep<SCHEME>(p, id_lo, id_hi, a, b, thr, never, lane, lives, [&](uint32_t g, uint32_t m) {
+              uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
+              if (m) ic_take_live(p, g, m, uu, visit);
+              append(uu);
+              return true;
+            });
         } else {
           const uint32_t d = b - a;
           const uint32_t j = lt_choose<SCHEME>(p, id, v, a, d, lane);

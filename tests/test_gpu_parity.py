@@ -98,7 +98,7 @@ def test_pool_parity_C1_invariance(opts):
         assert c.stats()["giant_sets"] == T
 
 
-@pytest.mark.parametrize("graph,segs,cand", [(1, 1, 1), (0, 1, 1), (1, 0, 1), (1, 1, 0)])
+@pytest.mark.parametrize("graph,segs,cand", [(1, 1, 1), (0, 1, 2), (1, 0, 1), (1, 1, 0), (1, 1, 2)])
 def test_pool_parity_C2_and_select(graph, segs, cand):
     """k = 50 selection through the argmax/cover launches replayed from a CUDA graph (default)
     and launched one by one; pool generated in several calls (several index segments)."""
@@ -133,10 +133,10 @@ def test_extend_truncate_reseed():
         _same_pool(c, o, T)
 
 
-@pytest.mark.parametrize("graph", [1, 0])
-def test_select_zero_gain_and_k_eq_n(graph):
+@pytest.mark.parametrize("graph,cand", [(1, 1), (0, 0), (1, 2)])
+def test_select_zero_gain_and_k_eq_n(graph, cand):
     g = gi.diamond()
-    c = _ctx(g, gi.LT, gi.W_WC, opts={P.OPT_SELECT_GRAPH: graph})
+    c = _ctx(g, gi.LT, gi.W_WC, opts={P.OPT_SELECT_GRAPH: graph, P.OPT_ARGMAX_CAND: cand})
     c.generate_rr(16, 200907325)
     s, gns, cov = c.select(4)
     o = oracle.Oracle(g, gi.LT, gi.W_WC)
@@ -254,7 +254,7 @@ def test_full_size_sampled(key):
     # non-increasing (greedy on a coverage function), covered = #sets hit by the seeds.
     seeds, gains, cov = c.select(w.k)
     c.set_option(P.OPT_SELECT_GRAPH, 0)
-    c.set_option(P.OPT_ARGMAX_CAND, 0)
+    c.set_option(P.OPT_ARGMAX_CAND, 2)
     s2, g2, c2 = c.select(w.k)
     assert np.array_equal(seeds, s2) and np.array_equal(gains, g2) and cov == c2
     assert seeds[0] == int(np.argmax(cnt)) and gains[0] == int(cnt.max())

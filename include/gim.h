@@ -151,7 +151,11 @@ gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
  *  GIM_OPT_ARGMAX_CAND  = 1 (default): for P = 1 and n >= 2^23 the per-step argmax scans a candidate list of
  *                          <= 65536 nodes (count >= a power-of-two threshold) and falls back to
  *                          the full scan once no candidate reaches the threshold; 0: always full;
- *                          2: candidates whatever n (tests). */
+ *                          2: candidates whatever n (tests).
+ *  GIM_OPT_IC_LANE      = -1 (default): IC sampling starts with the lane-per-set kernel when the
+ *                          running mean of coins per set is below 160 (tiny sets) and the chunk
+ *                          has >= 131072 sets, else the warp kernel; 1: always lane-first;
+ *                          0: never. Results are identical. */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -159,7 +163,8 @@ typedef enum {
   GIM_OPT_STAGING_CAP = 4,
   GIM_OPT_SELECT_GRAPH = 6,
   GIM_OPT_INV_SEGMENTS = 7,
-  GIM_OPT_ARGMAX_CAND = 8
+  GIM_OPT_ARGMAX_CAND = 8,
+  GIM_OPT_IC_LANE = 9
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

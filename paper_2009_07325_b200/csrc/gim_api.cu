@@ -61,7 +61,7 @@ struct gim_ctx {
   std::vector<Seg> segs;
   DevBuf pool, offsets, count_total;
   // generation scratch
-  DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr, dump, lt_spill;
+  DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr, dump, lt_spill, esc_list;
   DevBuf bitmaps, gqueues;
   uint32_t giant_slots = 0;
   bool giant_cap_reached = false;
@@ -85,6 +85,8 @@ struct gim_ctx {
   int use_cand = 1;             // GIM_OPT_ARGMAX_CAND
   // options
   int force_giant = 0, profile = 0;
+  int ic_lane = -1;             // GIM_OPT_IC_LANE: -1 auto (mean coins per set), 0 off, 1 on
+  double coins_per_set = 0.0;   // running estimate from previous chunks
   uint32_t qcap = kQMax;
   uint64_t staging_init = 0;
   gim_stats st{};
@@ -352,6 +354,7 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   TRY(ensure(c, c->dump, std::max<uint64_t>((uint64_t)cnt * 8, 1u << 20) * 4));
   TRY(ensure(c, c->retry_list, (uint64_t)cnt * 4));
   TRY(ensure(c, c->item_list, (uint64_t)cnt * 4));
+  TRY(ensure(c, c->esc_list, (uint64_t)cnt * 4));
   TRY(ensure(c, c->scan_out, ((uint64_t)cnt + 1) * 8));
   TRY(ensure(c, c->scan_tmp, (scan_tiles(cnt) + 2) * 8));
   TRY(ensure(c, c->ctr, sizeof(GenCounters)));
@@ -384,8 +387,28 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   const uint64_t bm_words = ((uint64_t)c->n + 31) / 32;
   // warp kernel, then the giant kernel unconditionally (it reads the giant count on the device
   // and exits at once when there is none), then the size scan: one host sync per chunk.
+  // IC with tiny sets: the lane kernel runs first and escalates big sets to the warp kernel
+  // (small chunks stay on the warp path: with few sets in flight, one lane per set exposes each
+  // set's whole chain of dependent loads)
+  const bool lane_first = c->model == MODEL_IC &&
+                          (c->ic_lane == 1 || (c->ic_lane == -1 && c->coins_per_set > 0.0 &&
+                                               c->coins_per_set < 160.0 && cnt >= (1u << 17)));
   auto run_pass = [&](const RRParams& pp) -> gim_status {
-    {
+    if (lane_first) {
+      RRParams pl = pp;
+      pl.esc_list = c->esc_list.as<uint32_t>();
+      {
+        Prof pf(c, CLS_RR);
+        TRY(launched(c, launch_rr_ic_lane(c->scheme, pl, c->num_sms * 4, c->stream), "k_rr_ic_lane"));
+        c->st.n_rr_launches++;
+      }
+      RRParams pw = pp;                        // the warp kernel replays the escalated items
+      pw.item_list = c->esc_list.as<uint32_t>();
+      pw.count_ptr = &c->ctr.as<GenCounters>()->esc_count;
+      Prof pf(c, CLS_RR);
+      TRY(launched(c, launch_rr_warp(c->model, c->scheme, pw, rr_grid, c->stream), "k_rr_warp(escalated)"));
+      c->st.n_rr_launches++;
+    } else {
       Prof pf(c, CLS_RR);
       TRY(launched(c, launch_rr_warp(c->model, c->scheme, pp, rr_grid, c->stream), "k_rr_warp"));
       c->st.n_rr_launches++;
@@ -421,6 +444,7 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     GenCounters h = *c->h_ctr;
     h.stage_tail = old_cap;
     h.claim = h.claim_giant = h.giant_count = h.retry_count = 0;
+    h.claim_lane = h.esc_count = 0;
     h.dump_tail = 0;
     *c->h_ctr = h;
     CK(cudaMemcpyAsync(c->ctr.p, c->h_ctr, sizeof(GenCounters), cudaMemcpyHostToDevice, c->stream));
@@ -445,6 +469,8 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   }
   c->st.coins += c->h_ctr->coins;
   c->st.live_edges += c->h_ctr->live;
+  if (cnt >= 4096)   // running mean coins per set drives the lane/warp choice of later chunks
+    c->coins_per_set = (double)(c->h_ctr->coins + c->h_ctr->coins_giant) / (double)cnt;
   c->st.coins_giant += c->h_ctr->coins_giant;
   c->st.live_giant += c->h_ctr->live_giant;
   // two-pass storage: sizes were scanned above; compacting copy + count_total
@@ -699,7 +725,7 @@ void gim_destroy(gim_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
                     &c->sizes, &c->soff, &c->giant_list, &c->retry_list, &c->item_list, &c->scan_out,
-                    &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->bitmaps, &c->gqueues, &c->cnt,
+                    &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand};
   for (auto& sg : c->iseg) {
     dfree(c, sg.off);
@@ -970,6 +996,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_PROFILE: c->profile = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_SELECT_GRAPH: c->use_graph = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_INV_SEGMENTS: c->inv_segmented = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_IC_LANE: c->ic_lane = (value < -1 || value > 1) ? -1 : (int)value; return GIM_OK;
     case GIM_OPT_ARGMAX_CAND: c->use_cand = (value < 0 || value > 2) ? 1 : (int)value; return GIM_OK;
     case GIM_OPT_STAGING_CAP:
       if (value < 0) return fail(c, GIM_EINVAL, "staging cap must be >= 0");

@@ -80,6 +80,8 @@ struct GenCounters {
   unsigned long long live_giant;
   unsigned long long dump_tail;    // partial-BFS dump allocator (elements)
   unsigned int claim;              // warp-kernel work claim
+  unsigned int claim_lane;         // lane-kernel work claim
+  unsigned int esc_count;          // sets escalated by the lane kernel to the warp kernel
   unsigned int claim_giant;        // giant-kernel work claim
   unsigned int giant_count;        // ids pushed to the giant list
   unsigned int retry_count;        // ids whose staging write did not fit
@@ -112,6 +114,8 @@ struct RRParams {
   uint32_t rk[20];             // Philox round keys of `seed` (host-computed)
   uint64_t id_base;            // global RR id = id_base + item
   uint32_t count;              // items to process
+  const unsigned int* count_ptr;   // if set, the item count is read here (device-produced lists)
+  uint32_t* esc_list;          // IC lane kernel: items escalated to the warp kernel
   const uint32_t* item_list;   // nullptr: items are 0..count-1; else item = item_list[i]
   uint32_t* sizes;             // [chunk] RR size per item
   uint64_t* soff;              // [chunk] staging offset per item
@@ -164,6 +168,9 @@ constexpr uint32_t kStageChunk = 1024;    // staging elements reserved per warp 
 constexpr int kLtWarps = 8;          // K-LT: warps per CTA
 constexpr int kLtCap = 64;           // K-LT: path entries per lane in shared memory
 constexpr int kLtCap2 = 512;         // K-LT: max path per lane (shared + global spill)
+constexpr int kIcLaneWarps = 8;      // K-IC lane kernel: warps per CTA
+constexpr int kIcLaneCap = 32;       // K-IC lane kernel: set size limit (then escalate)
+constexpr uint32_t kIcLaneMaxDeg = 256;   // K-IC lane kernel: in-degree limit (then escalate)
 constexpr int kGiantWin = 2048;      // frontier window of the giant kernel (smem)
 
 }  // namespace gim

@@ -7,6 +7,7 @@ namespace gim {
 struct RRParams;
 
 int lt_blocks_per_sm();
+cudaError_t launch_rr_ic_lane(int scheme, const RRParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rr_warp(int model, int scheme, const RRParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
                             uint32_t* gqueues, uint64_t bm_words, cudaStream_t s);

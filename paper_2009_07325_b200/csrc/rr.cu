@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
   const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
   uint32_t coins = 0, lives = 0;    // 32-bit per-warp counters, flushed before they can wrap
 
+  const uint32_t count = p.count_ptr ? *p.count_ptr : p.count;
   uint32_t claim_next = 0, claim_end = 0;            // ids claimed kClaimBatch at a time
   unsigned long long chunk_off = 0;                  // this warp's staging chunk
   uint32_t chunk_left = 0;
@@ -208,14 +209,14 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
     if (claim_next == claim_end) {
       // batches amortise the shared counter (tiny sets); single ids near the end keep the
       // heavy-tailed last sets from piling up on one warp
-      const uint32_t batch = (claim_end < p.count - p.count / kClaimTailDiv) ? kClaimBatch : 1u;
+      const uint32_t batch = (claim_end < count - count / kClaimTailDiv) ? kClaimBatch : 1u;
       uint32_t base = 0;
       if (lane == 0) base = atomicAdd(&p.ctr->claim, batch);
       claim_next = __shfl_sync(kFull, base, 0);
       claim_end = claim_next + batch;
     }
     const uint32_t i = claim_next++;
-    if (i >= p.count) break;
+    if (i >= count) break;
     const uint32_t item = p.item_list ? p.item_list[i] : i;
     if (p.force_giant) {
       if (lane == 0) p.giant_recs[atomicAdd(&p.ctr->giant_count, 1u)] = GiantRec{item, 0u, 0u, 0u, 0ull};
@@ -367,6 +368,153 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
     atomicAdd(&p.ctr->coins, c64);
     atomicAdd(&p.ctr->live, l64);
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// K-IC lane kernel (tiny RR sets, e.g. uniform p = 0.01 on C5: ~1.5 nodes and ~56 coins per
+// set): each lane owns one RR set with a 32-node queue in shared memory (lane-interleaved) that is
+// also its visited set; every iteration each lane evaluates ONE slot group (one Philox = 4 coins)
+// of its current node, so the warp's Philox work stays lane-parallel across 32 independent sets.
+// A set that reaches a node with > kIcLaneMaxDeg in-edges or more than kIcLaneCap nodes is
+// escalated: its id goes to esc_list and the warp kernel replays it exactly (same coins).
+// ------------------------------------------------------------------------------------------
+template <int SCHEME>
+__global__ void __launch_bounds__(kIcLaneWarps * 32) k_rr_ic_lane(RRParams p) {
+  extern __shared__ uint32_t smem[];
+  const int lane = threadIdx.x & 31;
+  uint32_t* qv = smem + (threadIdx.x >> 5) * (kIcLaneCap * 32);     // qv[i * 32 + lane]
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
+  uint32_t item = 0, head = 0, tail = 0, a = 0, b = 0, g = 0, g_hi = 0, thr = 0;
+  uint64_t id = 0;
+  bool active = false, want = true, on_node = false;
+  uint32_t coins = 0, lives = 0;
+  unsigned long long chunk_off = 0;
+  uint32_t chunk_left = 0;
+  while (true) {
+    const uint32_t need = __ballot_sync(kFull, want);
+    if (need) {                              // refill finished lanes with one claim
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&p.ctr->claim_lane, (uint32_t)__popc(need));
+      base = __shfl_sync(kFull, base, 0);
+      if (want) {
+        const uint32_t i = base + __popc(need & lt_mask);
+        want = false;
+        active = i < p.count;
+        if (active) {
+          item = p.item_list ? p.item_list[i] : i;
+          id = p.id_base + item;
+          qv[lane] = rr_root(p.seed, id, p.n);
+          head = 0;
+          tail = 1;
+          on_node = false;
+          if (p.force_giant) {                 // forced fallback: everything via the warp kernel
+            p.esc_list[atomicAdd(&p.ctr->esc_count, 1u)] = item;
+            active = false;
+            want = true;
+          }
+        }
+      }
+    }
+    if (!__any_sync(kFull, active)) {
+      if (!__any_sync(kFull, want)) break;
+      continue;
+    }
+    bool finish = false, escalate = false;
+    if (active && !on_node) {                // next node of this lane's BFS
+      if (head == tail) {
+        finish = true;
+      } else {
+        const uint32_t v = qv[head * 32 + lane];
+        ++head;
+        a = __ldg(p.row_ptr + v);
+        b = __ldg(p.row_ptr + v + 1);
+        if (b - a > kIcLaneMaxDeg) {
+          escalate = true;
+        } else if (b > a) {
+          on_node = true;
+          g = a >> 2;
+          g_hi = (b - 1) >> 2;
+          thr = node_thr<SCHEME>(p, b - a);
+          coins += b - a;
+        }
+      }
+    }
+    if (active && on_node) {                 // one slot group of the current node
+      const uint4 w = philox4x32_10_rk(make_uint4((uint32_t)id, (uint32_t)(id >> 32), g, 0u), p.rk);
+      uint32_t m = never ? 0u : live_mask_words<SCHEME>(p, w, g, a, b, thr);
+      lives += __popc(m);
+      while (m) {
+        const uint32_t j = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t u = __ldg(p.src + (g << 2) + j);
+        bool seen = false;
+        for (uint32_t t = 0; t < tail; ++t) seen |= (qv[t * 32 + lane] == u);
+        if (!seen) {
+          if (tail == (uint32_t)kIcLaneCap) { escalate = true; break; }
+          qv[tail * 32 + lane] = u;
+          ++tail;
+        }
+      }
+      if (++g > g_hi) on_node = false;
+    }
+    if (escalate) {
+      p.esc_list[atomicAdd(&p.ctr->esc_count, 1u)] = item;
+      active = false;
+      want = true;
+    }
+    // finished sets: warp-aggregated staging (per-warp chunk), then per-lane copy
+    const uint32_t fin = __ballot_sync(kFull, finish);
+    if (fin) {
+      uint32_t incl = finish ? tail : 0u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += y;
+      }
+      const uint32_t tot = __shfl_sync(kFull, incl, 31);
+      if (tot > chunk_left) {
+        const uint32_t want_el = max(tot, kStageChunk);
+        unsigned long long b0 = 0;
+        if (lane == 0) b0 = atomicAdd(&p.ctr->stage_tail, (unsigned long long)want_el);
+        chunk_off = __shfl_sync(kFull, b0, 0);
+        chunk_left = want_el;
+      }
+      const unsigned long long base = chunk_off;
+      chunk_off += tot;
+      chunk_left -= tot;
+      if (finish) {
+        const unsigned long long off = base + incl - tail;
+        if (off + tail > p.stage_cap) {
+          p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = item;
+        } else {
+          for (uint32_t t = 0; t < tail; ++t) p.staging[off + t] = qv[t * 32 + lane];
+          p.sizes[item] = tail;
+          p.soff[item] = off;
+        }
+        active = false;
+        want = true;
+      }
+    }
+  }
+  unsigned long long c64 = coins, l64 = lives;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    c64 += __shfl_xor_sync(kFull, c64, off);
+    l64 += __shfl_xor_sync(kFull, l64, off);
+  }
+  if (lane == 0) {
+    atomicAdd(&p.ctr->coins, c64);
+    atomicAdd(&p.ctr->live, l64);
+  }
+}
+
+cudaError_t launch_rr_ic_lane(int scheme, const RRParams& p, int grid, cudaStream_t s) {
+  const int smem = kIcLaneWarps * kIcLaneCap * 32 * 4;
+  if (scheme == W_WC) k_rr_ic_lane<W_WC><<<grid, kIcLaneWarps * 32, smem, s>>>(p);
+  else if (scheme == W_UNIFORM) k_rr_ic_lane<W_UNIFORM><<<grid, kIcLaneWarps * 32, smem, s>>>(p);
+  else k_rr_ic_lane<W_EXPLICIT><<<grid, kIcLaneWarps * 32, smem, s>>>(p);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------------

@@ -70,9 +70,9 @@ def test_pool_parity_tiny(gname):
     g = {"diamond": gi.diamond(), "chain": gi.chain(6), "star": gi.star_in(40),
          "cycle": gi.cycle_plus(), "rand0": gi.random_small(9, 30, 0),
          "rand1": gi.random_small(12, 60, 1), "rand2": gi.random_small(30, 200, 2)}[gname]
-    for name, gg, model, scheme, pu in _variants(g):
+    for (name, gg, model, scheme, pu), lane in [(v, l) for v in _variants(g) for l in (0, 1)]:
         T = 3001                       # many warps + a ragged tail
-        c = _ctx(gg, model, scheme, pu)
+        c = _ctx(gg, model, scheme, pu, opts={P.OPT_IC_LANE: lane})
         c.generate_rr(T, 4242)
         o = oracle.Oracle(gg, model, scheme, pu)
         o.generate(T, 4242)
@@ -83,7 +83,9 @@ def test_pool_parity_tiny(gname):
 
 
 @pytest.mark.parametrize("opts", [{}, {P.OPT_FORCE_GIANT: 1}, {P.OPT_QUEUE_CAP: 4},
-                                  {P.OPT_STAGING_CAP: 64}, {P.OPT_QUEUE_CAP: 32, P.OPT_STAGING_CAP: 1000}])
+                                  {P.OPT_STAGING_CAP: 64}, {P.OPT_QUEUE_CAP: 32, P.OPT_STAGING_CAP: 1000},
+                                  {P.OPT_IC_LANE: 1}, {P.OPT_IC_LANE: 1, P.OPT_STAGING_CAP: 64},
+                                  {P.OPT_IC_LANE: 1, P.OPT_FORCE_GIANT: 1}, {P.OPT_IC_LANE: 1, P.OPT_QUEUE_CAP: 8}])
 def test_pool_parity_C1_invariance(opts):
     """Same pool whatever the queue capacity, forced fallback or staging retries."""
     w = gi.WORKLOADS["C1"]

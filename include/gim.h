@@ -155,7 +155,11 @@ gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
  *  GIM_OPT_IC_LANE      = -1 (default): IC sampling starts with the lane-per-set kernel when the
  *                          running mean of coins per set is below 160 (tiny sets) and the chunk
  *                          has >= 131072 sets, else the warp kernel; 1: always lane-first;
- *                          0: never. Results are identical. */
+ *                          0: never. Results are identical.
+ *  GIM_OPT_SPECULATE    = 0 (default) / 1: inside gim_imm, sample the next round's RR ids on a
+ *                          second stream while a round's NodeSelection runs (capped at the
+ *                          largest theta the LB test can yield; excess is truncated). Results
+ *                          are identical; measured slower on C4 and neutral on C3. */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -164,7 +168,8 @@ typedef enum {
   GIM_OPT_SELECT_GRAPH = 6,
   GIM_OPT_INV_SEGMENTS = 7,
   GIM_OPT_ARGMAX_CAND = 8,
-  GIM_OPT_IC_LANE = 9
+  GIM_OPT_IC_LANE = 9,
+  GIM_OPT_SPECULATE = 10
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

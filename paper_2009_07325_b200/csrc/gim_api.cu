@@ -37,7 +37,13 @@ constexpr uint32_t kChunk = 1u << 22;   // RR ids per generation chunk (bounds s
 struct gim_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;   // speculative sampling overlapping a NodeSelection (gim_imm)
   bool own_stream = false;
+  int speculate = 0;                // GIM_OPT_SPECULATE (measured: no gain)
+  cudaEvent_t ev_cnt_copied = nullptr, ev_sel_done = nullptr;
+  bool sel_pending = false;         // a selection is in flight on `stream`
+  uint64_t set_limit = ~0ull;       // cover skips local sets >= this (after a tail truncation)
+  bool truncated = false;
   int num_sms = 148;
   std::string err;
   gim_alloc_fn afn = nullptr;
@@ -286,6 +292,8 @@ gim_status reset_pool(gim_ctx* c, uint64_t seed) {
   CK(cudaMemsetAsync(c->offsets.p, 0, 8, c->stream));
   drop_inv(c);
   c->inv_valid = true;
+  c->set_limit = ~0ull;
+  c->truncated = false;
   TRY(ensure(c, c->cnt_snap, (uint64_t)c->n * 4));
   CK(cudaMemsetAsync(c->cnt_snap.p, 0, (uint64_t)c->n * 4, c->stream));
   return GIM_OK;
@@ -475,6 +483,8 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   c->st.live_giant += c->h_ctr->live_giant;
   // two-pass storage: sizes were scanned above; compacting copy + count_total
   const uint64_t total = c->h_u64[0];
+  if (c->sel_pending && (c->pool.bytes < (c->pool_len + total) * 4 || c->offsets.bytes < (c->nsets + cnt + 1) * 8))
+    CK(cudaEventSynchronize(c->ev_sel_done));   // the running selection reads pool/offsets
   TRY(grow_keep(c, c->pool, (c->pool_len + total) * 4, c->pool_len * 4));
   TRY(grow_keep(c, c->offsets, (c->nsets + cnt + 1) * 8, (c->nsets + 1) * 8));
   {
@@ -516,7 +526,8 @@ gim_status truncate_pool(gim_ctx* c, uint64_t theta) {
   c->nsets = keep_sets;
   c->pool_len = e0;
   c->T_global = theta;
-  c->inv_valid = false;
+  c->set_limit = keep_sets;          // the index segments stay valid: cover skips cut sets
+  c->truncated = true;
   return GIM_OK;
 }
 
@@ -527,6 +538,11 @@ gim_status generate(gim_ctx* c, uint64_t theta, uint64_t seed) {
   if (theta < c->T_global) {
     TRY(truncate_pool(c, theta));
   } else if (theta > c->T_global) {
+    if (c->truncated) {                // segment deltas no longer match: rebuild at the next select
+      c->inv_valid = false;
+      c->truncated = false;
+      c->set_limit = ~0ull;
+    }
     const uint64_t a = c->T_global, len = theta - a;
     const uint64_t lo = a + (uint64_t)((unsigned __int128)len * c->rank / c->world);
     const uint64_t hi = a + (uint64_t)((unsigned __int128)len * (c->rank + 1) / c->world);
@@ -537,7 +553,7 @@ gim_status generate(gim_ctx* c, uint64_t theta, uint64_t seed) {
 }
 
 // ---- NodeSelection (O7) ---------------------------------------------------------------------
-gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains, uint64_t* covered) {
+gim_status select_launch(gim_ctx* c, uint32_t k) {
   if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
   if (k < 1 || k > c->n) return fail(c, GIM_EINVAL, "k must satisfy 1 <= k <= n");
   if (!c->have_seed || c->T_global == 0) return fail(c, GIM_ESTATE, "RR pool is empty");
@@ -553,19 +569,24 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
     CK(cudaMemsetAsync(c->cnt_snap.p, 0, n * 4, c->stream));
     TRY(build_inv_segment(c, 0, c->nsets, 0, c->pool_len));
     c->inv_valid = true;
+    c->set_limit = ~0ull;
+    c->truncated = false;
   }
   TRY(ensure(c, c->seg_desc, sizeof(InvSegDev) * kMaxInvSeg + 16));
   {
     InvSegDev tab[kMaxInvSeg];
     for (size_t q = 0; q < c->iseg.size(); ++q)
       tab[q] = InvSegDev{c->iseg[q].off.as<uint64_t>(), c->iseg[q].inv.as<uint32_t>()};
-    TRY(launched(c, launch_set_segs(tab, (uint32_t)c->iseg.size(), c->seg_desc.as<InvSegDev>(),
+    TRY(launched(c, launch_set_segs(tab, (uint32_t)c->iseg.size(),
+                                    (uint32_t)std::min<uint64_t>(c->set_limit, 0xFFFFFFFFull),
+                                    c->seg_desc.as<InvSegDev>(),
                                     reinterpret_cast<uint32_t*>(c->seg_desc.as<InvSegDev>() + kMaxInvSeg),
                                     c->stream), "k_set_segs"));
   }
   const InvSegDev* segd = c->seg_desc.as<InvSegDev>();
   const uint32_t* nsegd = reinterpret_cast<const uint32_t*>(segd + kMaxInvSeg);
   CK(cudaMemcpyAsync(c->cnt.p, c->count_total.p, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaEventRecord(c->ev_cnt_copied, c->stream));
   CK(cudaMemsetAsync(c->covered.p, 0, std::max<uint64_t>(c->nsets, 1), c->stream));
   CK(cudaMemsetAsync(c->keys.p, 0, (uint64_t)k * 8, c->stream));
   if (dec) {
@@ -638,19 +659,41 @@ gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains,
     CK(cudaMallocHost(&c->h_keys, (uint64_t)k * 8));
     c->h_keys_cap = k;
   }
-  unsigned long long* hk = c->h_keys;
-  CK(cudaMemcpyAsync(hk, keys, (uint64_t)k * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->h_keys, keys, (uint64_t)k * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaEventRecord(c->ev_sel_done, c->stream));
+  c->sel_pending = true;
+  return GIM_OK;
+}
+
+gim_status select_finish(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains, uint64_t* covered) {
   TRY(sync(c));
+  c->sel_pending = false;
   uint64_t cov = 0;
   for (uint32_t j = 0; j < k; ++j) {
-    seeds[j] = ~(uint32_t)(hk[j] & 0xFFFFFFFFull);
-    const uint64_t g = hk[j] >> 32;
+    seeds[j] = ~(uint32_t)(c->h_keys[j] & 0xFFFFFFFFull);
+    const uint64_t g = c->h_keys[j] >> 32;
     if (gains) gains[j] = g;
     cov += g;
   }
   if (covered) *covered = cov;
   c->st.selects++;
   return GIM_OK;
+}
+
+gim_status select_impl(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains, uint64_t* covered) {
+  TRY(select_launch(c, k));
+  return select_finish(c, k, seeds, gains, covered);
+}
+
+// Speculative sampling on stream2 while the selection launched on `stream` runs: the library's
+// generation code runs unchanged with the two streams swapped. stream2 first waits until the
+// selection has copied count_total (which k_store updates).
+gim_status generate_speculative(gim_ctx* c, uint64_t theta, uint64_t seed) {
+  CK(cudaStreamWaitEvent(c->stream2, c->ev_cnt_copied, 0));
+  std::swap(c->stream, c->stream2);
+  const gim_status st = generate(c, theta, seed);
+  std::swap(c->stream, c->stream2);
+  return st;
 }
 
 // ---- IMM constants (O8; readings R1-R3, R21) -----------------------------------------------
@@ -704,6 +747,13 @@ gim_status gim_create(int device, void* cuda_stream, gim_ctx** out) {
     }
     c->own_stream = true;
   }
+  if (cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_cnt_copied, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_sel_done, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return GIM_ECUDA;
+  }
   cudaMemPool_t mp;
   if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) {
     uint64_t thr = ~0ull;
@@ -744,6 +794,10 @@ void gim_destroy(gim_ctx* c) {
   if (c->h_u64) cudaFreeHost(c->h_u64);
   if (c->h_keys) cudaFreeHost(c->h_keys);
   if (c->own_stream) cudaStreamDestroy(c->stream);
+  cudaStreamSynchronize(c->stream2);
+  cudaStreamDestroy(c->stream2);
+  cudaEventDestroy(c->ev_cnt_copied);
+  cudaEventDestroy(c->ev_sel_done);
   cudaGetLastError();
   delete c;
 }
@@ -917,24 +971,38 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
   uint64_t cov = 0;
   std::vector<uint32_t> tmp(k);
   const int i_max = (int)std::floor(std::log2(n)) - 1;       // reading R5
+  bool passed = false;
   for (int i = 1; i <= i_max && i <= 64; ++i) {              // Alg. 2 l.2
     const double x = n / std::ldexp(1.0, i);                 // l.3
     const double theta_i = K.lambda_p / x;                   // l.4 (f = lambda', reading R1)
     const uint64_t T = (uint64_t)std::ceil(theta_i);
-    TRY(generate(c, std::max<uint64_t>(c->T_global, T), seed));   // l.5 (reading R4)
-    TRY(select_impl(c, k, tmp.data(), nullptr, &cov));       // l.6 (reading R9)
+    const uint64_t R = std::max<uint64_t>(c->T_global, T);   // l.5 (reading R4)
+    TRY(generate(c, R, seed));
+    if (c->T_global > R) TRY(truncate_pool(c, R));            // drop excess speculation
+    // speculative target while this round's selection runs: the next round's T if the test
+    // fails, capped by ceil(lambda*/x), the largest theta a passing test can produce
+    const uint64_t spec = std::min<uint64_t>(
+        (i < i_max) ? (uint64_t)std::ceil(K.lambda_p / (x / 2.0)) : 0ull, (uint64_t)std::ceil(K.lambda_s / x));
+    TRY(select_launch(c, k));                                 // l.6 (reading R9)
+    if (c->speculate && spec > R) TRY(generate_speculative(c, spec, seed));
+    TRY(select_finish(c, k, tmp.data(), nullptr, &cov));
     r.theta_i[i - 1] = T;
     r.theta_i_real[i - 1] = theta_i;
     r.cov_i[i - 1] = cov;
     r.rounds = (uint32_t)i;
-    if ((n * (double)cov) / (double)c->T_global >= (1.0 + K.eps_p) * x) {   // l.7 (reading R7)
-      LB = (n * (double)cov) / (double)c->T_global / (1.0 + K.eps_p);       // l.8
+    if ((n * (double)cov) / (double)R >= (1.0 + K.eps_p) * x) {   // l.7 (reading R7)
+      LB = (n * (double)cov) / (double)R / (1.0 + K.eps_p);       // l.8
+      passed = true;
       break;
     }
   }
+  (void)passed;
   const double theta = K.lambda_s / LB;                      // reading R2
   const uint64_t T = (uint64_t)std::ceil(theta);
-  TRY(generate(c, std::max<uint64_t>(c->T_global, T), seed));    // reading R8
+  uint64_t R_last = 0;
+  for (uint32_t q = 0; q < r.rounds; ++q) R_last = std::max<uint64_t>(R_last, r.theta_i[q]);
+  const uint64_t R_final = std::max<uint64_t>(R_last, T);   // reading R8
+  TRY(generate(c, R_final, seed));                           // extends or truncates speculation
   std::vector<uint64_t> gains(k);
   TRY(select_impl(c, k, seeds, gains.data(), &cov));
   r.LB = LB;
@@ -996,6 +1064,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_PROFILE: c->profile = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_SELECT_GRAPH: c->use_graph = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_INV_SEGMENTS: c->inv_segmented = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_SPECULATE: c->speculate = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_IC_LANE: c->ic_lane = (value < -1 || value > 1) ? -1 : (int)value; return GIM_OK;
     case GIM_OPT_ARGMAX_CAND: c->use_cand = (value < 0 || value > 2) ? 1 : (int)value; return GIM_OK;
     case GIM_OPT_STAGING_CAP:

@@ -26,8 +26,8 @@ cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, ui
                                const uint64_t* inv_off, uint32_t* cursor, uint32_t* inv, int grid,
                                cudaStream_t s);
 struct InvSegDev;
-cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, InvSegDev* out, uint32_t* nseg_out,
-                            cudaStream_t s);
+cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, uint32_t limit, InvSegDev* out,
+                            uint32_t* nseg_out, cudaStream_t s);
 cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* delta, uint32_t n, int grid,
                                cudaStream_t s);
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,

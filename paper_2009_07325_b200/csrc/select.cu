@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
                                                int32_t* __restrict__ dec) {
   __shared__ uint64_t s_lo[kMaxInvSeg], s_end[kMaxInvSeg];   // list start, inclusive prefix end
   __shared__ const uint32_t* s_inv[kMaxInvSeg];
-  __shared__ uint32_t s_nseg;
+  __shared__ uint32_t s_nseg, s_limit;
   const uint32_t sub = threadIdx.x & 7;
   const uint32_t u = ~(uint32_t)keys[j];
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[u] = kSent;   // retire the pick (never decremented)
@@ -363,10 +363,13 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
       s_inv[l] = sg.inv;
     }
     const uint32_t used = __ballot_sync(kFull, sg.off != nullptr);   // warp-wide vote
-    if (l == 0) s_nseg = __popc(used);
+    if (l == 0) {
+      s_nseg = __popc(used);
+      s_limit = reinterpret_cast<const uint32_t*>(segs + kMaxInvSeg)[1];
+    }
   }
   __syncthreads();
-  const uint32_t ns = s_nseg;
+  const uint32_t ns = s_nseg, limit = s_limit;
   const uint64_t total = ns ? s_end[kMaxInvSeg - 1] : 0;
   const uint64_t ngroups = (uint64_t)gridDim.x * (blockDim.x >> 3);
   uint32_t q = 0;
@@ -374,6 +377,7 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
     while (t >= s_end[q]) ++q;                 // t increases monotonically per group
     const uint64_t pos = s_lo[q] + (t - (q ? s_end[q - 1] : 0));
     const uint32_t r = s_inv[q][pos];
+    if (r >= limit) continue;                  // truncated away (tail of the last segment)
     const uint8_t cov = covered[r];            // flag and offsets loaded together
     const uint64_t a = offsets[r], b = offsets[r + 1];
     if (cov) continue;
@@ -421,18 +425,22 @@ cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, ui
 // Writes the segment descriptor table from a by-value parameter (no host staging buffer).
 struct SegTable {
   InvSegDev seg[kMaxInvSeg];
-  uint32_t nseg;
+  uint32_t nseg, limit;
 };
 __global__ void k_set_segs(SegTable t, InvSegDev* out, uint32_t* nseg_out) {
   if (threadIdx.x < kMaxInvSeg) out[threadIdx.x] = t.seg[threadIdx.x];
-  if (threadIdx.x == 0) *nseg_out = t.nseg;
+  if (threadIdx.x == 0) {
+    nseg_out[0] = t.nseg;
+    nseg_out[1] = t.limit;            // local sets >= limit were truncated away
+  }
 }
 
-cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, InvSegDev* out, uint32_t* nseg_out,
-                            cudaStream_t s) {
+cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, uint32_t limit, InvSegDev* out,
+                            uint32_t* nseg_out, cudaStream_t s) {
   SegTable t;
   for (int q = 0; q < kMaxInvSeg; ++q) t.seg[q] = (q < (int)nseg) ? segs[q] : InvSegDev{nullptr, nullptr};
   t.nseg = nseg;
+  t.limit = limit;
   k_set_segs<<<1, 32, 0, s>>>(t, out, nseg_out);
   return cudaGetLastError();
 }

@@ -322,3 +322,22 @@ def test_sharded_emulation_equals_single():
             lo, hi = r * T // Pn, (r + 1) * T // Pn
             assert np.array_equal(ids, np.arange(lo, hi, dtype=np.uint64))
             assert np.array_equal(nodes, rnodes[roff[lo]:roff[hi]])
+
+
+@pytest.mark.parametrize("key", ["C3", "C4"])
+def test_imm_speculation_invariance(key):
+    """gim_imm with the next round's RR ids sampled on a second stream while each round's
+    NodeSelection runs (default) returns exactly what the sequential schedule returns."""
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    out = []
+    for spec in (1, 0):
+        c = _ctx(g, w.model, w.scheme, opts={P.OPT_SPECULATE: spec})
+        out.append(c.imm(w.k, w.eps, w.ell, w.rr_seed))
+        ids, off, nodes = c.rr_export(sort_each_set=False)
+        assert len(ids) == out[-1].R_final
+        c.close()
+    a, b = out
+    assert np.array_equal(a.seeds, b.seeds) and a.R_final == b.R_final and a.covered == b.covered
+    assert a.LB == b.LB and a.theta == b.theta and a.rounds == b.rounds
+    assert np.array_equal(a.theta_i, b.theta_i) and np.array_equal(a.cov_i, b.cov_i)

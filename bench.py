@@ -166,10 +166,12 @@ def run_reference(args, w):
 # GPU arm
 # ------------------------------------------------------------------------------------------
 def alu_peak_gcoins(sm_mhz, sms=148):
-    """ALU roof of IC sampling: one Philox4x32-10 = 20 IMAD.WIDE.U32 on
-    the FMA pipe (reciprocal throughput 2 cycles per warp instruction per SM sub-partition,
-    B300_MICROARCH.md "Pipe rates"), 4 SMSPs per SM -> 3.2 Philox = 12.8 coins per cycle per SM."""
-    return 12.8 * sms * sm_mhz * 1e6 / 1e9
+    """ALU roof of IC sampling: one Philox4x32-10 = 20 IMAD.WIDE.U32, which issue
+    only to the FMA-heavy pipe at 4 cycles per warp instruction (16 lanes x a 64-bit result; the
+    32-bit IMAD rate of B300_MICROARCH.md "Pipe rates" is rt_SMSP = 2). 80 cycles per warp-Philox
+    per SM sub-partition, 4 SMSPs -> 1.6 Philox = 6.4 coins per cycle per SM. ncu evidence:
+    profiles/r01_ncu_k_philox_bench.txt (fmaheavy 82% busy, ALU 49%, issue 56%)."""
+    return 6.4 * sms * sm_mhz * 1e6 / 1e9
 
 
 def load_profile_traffic():
@@ -276,7 +278,7 @@ def run_gim(args, w):
         "traffic": traffic,
         "per_launch_ms": rr_ms / n_rr, "launches": n_rr,
         "coins_per_launch": coins / n_rr,
-        "peak_basis": f"derived: 12.8 coins/cycle/SM x 148 SMs x {sm_max:.0f} MHz (Philox4x32-10 = 20 IMAD.WIDE on the FMA pipe)",
+        "peak_basis": f"derived: 6.4 coins/cycle/SM x 148 SMs x {sm_max:.0f} MHz (Philox4x32-10 = 20 IMAD.WIDE.U32, 4 cycles each on the FMA-heavy pipe)",
         "philox_microbench_gcoins": measured_philox,
         "frac_of_microbench": (achieved / measured_philox) if measured_philox else None,
         "traffic_note": "DRAM bytes of one captured launch (profiles/ncu_traffic.json), not averaged",

@@ -159,7 +159,9 @@ gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
  *  GIM_OPT_SPECULATE    = 0 (default) / 1: inside gim_imm, sample the next round's RR ids on a
  *                          second stream while a round's NodeSelection runs (capped at the
  *                          largest theta the LB test can yield; excess is truncated). Results
- *                          are identical; measured slower on C4 and neutral on C3. */
+ *                          are identical; measured slower on C4 and neutral on C3.
+ *  GIM_OPT_MB_CHAINS    = 1 / 4 / 8 (default 8): interleaved Philox chains per thread in
+ *                          gim_microbench_philox. */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -169,7 +171,8 @@ typedef enum {
   GIM_OPT_INV_SEGMENTS = 7,
   GIM_OPT_ARGMAX_CAND = 8,
   GIM_OPT_IC_LANE = 9,
-  GIM_OPT_SPECULATE = 10
+  GIM_OPT_SPECULATE = 10,
+  GIM_OPT_MB_CHAINS = 11
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

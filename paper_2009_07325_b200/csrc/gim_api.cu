@@ -91,6 +91,7 @@ struct gim_ctx {
   int use_cand = 1;             // GIM_OPT_ARGMAX_CAND
   // options
   int force_giant = 0, profile = 0;
+  int mb_chains = 8;            // GIM_OPT_MB_CHAINS: Philox chains per thread in the microbenchmark
   int ic_lane = -1;             // GIM_OPT_IC_LANE: -1 auto (mean coins per set), 0 off, 1 on
   double coins_per_set = 0.0;   // running estimate from previous chunks
   uint32_t qcap = kQMax;
@@ -1064,6 +1065,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_PROFILE: c->profile = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_SELECT_GRAPH: c->use_graph = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_INV_SEGMENTS: c->inv_segmented = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_MB_CHAINS: c->mb_chains = (int)value; return GIM_OK;
     case GIM_OPT_SPECULATE: c->speculate = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_IC_LANE: c->ic_lane = (value < -1 || value > 1) ? -1 : (int)value; return GIM_OK;
     case GIM_OPT_ARGMAX_CAND: c->use_cand = (value < 0 || value > 2) ? 1 : (int)value; return GIM_OK;
@@ -1090,6 +1092,7 @@ gim_status gim_reset_stats(gim_ctx* c) {
 
 gim_status gim_microbench_philox(gim_ctx* c, uint64_t groups, double* ms) {
   if (!c || !ms || groups == 0) return GIM_EINVAL;
+  const int chains = c->mb_chains;
   c->err.clear();
   DeviceGuard g(c->device);
   const int grid = c->num_sms * 8;
@@ -1100,9 +1103,9 @@ gim_status gim_microbench_philox(gim_ctx* c, uint64_t groups, double* ms) {
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
-  CK(launch_philox_bench(1, per, sink.as<uint32_t>(), grid, c->stream));   // warm-up
+  CK(launch_philox_bench(1, per, sink.as<uint32_t>(), grid, c->stream, chains));   // warm-up
   CK(cudaEventRecord(a, c->stream));
-  CK(launch_philox_bench(2, per, sink.as<uint32_t>(), grid, c->stream));
+  CK(launch_philox_bench(2, per, sink.as<uint32_t>(), grid, c->stream, chains));
   CK(cudaEventRecord(b, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   float t = 0.f;

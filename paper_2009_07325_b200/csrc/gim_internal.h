@@ -17,7 +17,8 @@ cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const u
 cudaError_t launch_count_sub(const uint32_t* pool, uint64_t e0, uint64_t e1, uint32_t* count_total,
                              int grid, cudaStream_t s);
 
-cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* sink, int grid, cudaStream_t s);
+cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* sink, int grid, cudaStream_t s,
+                                int chains);
 
 uint64_t scan_tiles(uint64_t count);
 cudaError_t launch_scan_u32(const uint32_t* in, uint64_t count, uint64_t* out, uint64_t* tile_tmp,

@@ -1030,21 +1030,23 @@ cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const u
 
 // Philox microbenchmark (diagnostic, gim_microbench_philox): each thread evaluates `per_thread`
 // slot groups of one RR id, exactly the per-group work of the IC kernel without memory traffic.
+template <int NCH>
 __global__ void __launch_bounds__(256) k_philox_bench(RRParams p, uint32_t per_thread, uint32_t* sink) {
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t acc = 0;
-  for (uint32_t i = 0; i < per_thread; i += 4) {
-    uint4 w[4];
+  for (uint32_t i = 0; i < per_thread; i += NCH) {
+    uint4 w[NCH];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) w[r] = make_uint4(tid, 0u, i + r, 0u);
-    philox4x32_10_rk_xn<4>(w, p.rk);             // the hub sweep's 4 interleaved chains
+    for (int r = 0; r < NCH; ++r) w[r] = make_uint4(tid, 0u, i + r, 0u);
+    philox4x32_10_rk_xn<NCH>(w, p.rk);           // NCH interleaved chains (the hub sweep uses 4)
 #pragma unroll
-    for (int r = 0; r < 4; ++r) acc += (min(min(w[r].x, w[r].y), min(w[r].z, w[r].w)) <= 0x1000u);
+    for (int r = 0; r < NCH; ++r) acc += (min(min(w[r].x, w[r].y), min(w[r].z, w[r].w)) <= 0x1000u);
   }
   if (acc == 0xFFFFFFFFu) sink[0] = acc;
 }
 
-cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* sink, int grid, cudaStream_t s) {
+cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* sink, int grid, cudaStream_t s,
+                                int chains) {
   RRParams p{};
   uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   for (int r = 0; r < 10; ++r) {
@@ -1053,7 +1055,9 @@ cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* si
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
   }
-  k_philox_bench<<<grid, 256, 0, s>>>(p, (per_thread + 3) & ~3u, sink);
+  if (chains >= 8) k_philox_bench<8><<<grid, 256, 0, s>>>(p, (per_thread + 7) & ~7u, sink);
+  else if (chains >= 4) k_philox_bench<4><<<grid, 256, 0, s>>>(p, (per_thread + 3) & ~3u, sink);
+  else k_philox_bench<1><<<grid, 256, 0, s>>>(p, per_thread, sink);
   return cudaGetLastError();
 }
 

@@ -155,6 +155,7 @@ constexpr int kRRIlp = GIM_RR_ILP;    // Philox chains per lane per iteration (1
 #endif
 constexpr int kHubIlp = GIM_HUB_ILP;  // Philox chains per lane per step on a hub node
 constexpr uint32_t kHubGroups = 32u * GIM_HUB_ILP;   // nodes with >= this many slot groups are hubs
+static_assert((kHubGroups & (kHubGroups - 1u)) == 0u, "hub steps are split off with a mask");
 constexpr int kGiantThreads = 512;
 #ifndef GIM_CLAIM_BATCH
 #define GIM_CLAIM_BATCH 1

@@ -139,15 +139,71 @@ __device__ __forceinline__ bool append_live(const RRParams& p, uint32_t g, uint3
   if (m) ic_take_live(p, g, m, uu, vis);
   const uint32_t cnt = (uu[0] != kEmpty) + (uu[1] != kEmpty) + (uu[2] != kEmpty) + (uu[3] != kEmpty);
   uint32_t total;
-  uint32_t pos = tail + warp_excl_scan(cnt, lane, total);
-  if (tail + total > p.qcap) return false;
+  if (!__any_sync(kFull, cnt > 1u)) {
+    // common case (WC: ~one live in-edge per node): at most one new node per lane, so the
+    // append offsets are a ballot prefix instead of a warp scan
+    const uint32_t has = __ballot_sync(kFull, cnt != 0u);
+    total = __popc(has);
+    if (tail + total > p.qcap) return false;
+    if (cnt) q[tail + __popc(has & ((1u << lane) - 1u))] = min(min(uu[0], uu[1]), min(uu[2], uu[3]));
+  } else {
+    uint32_t pos = tail + warp_excl_scan(cnt, lane, total);
+    if (tail + total > p.qcap) return false;
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
-    if (uu[j] != kEmpty) q[pos++] = uu[j];
+    for (int j = 0; j < 4; ++j)
+      if (uu[j] != kEmpty) q[pos++] = uu[j];
+  }
   tail += total;
   return true;
 }
 
+
+// Sweep of whole hub steps: groups [g0, g0 + steps * kHubGroups) of a node with in-edge range
+// [a, b), all inside [a>>2, (b-1)>>2] (the node's remaining groups, fewer than one step, are
+// swept by the flattened batch). kHubIlp independent Philox chains per lane, interleaved round
+// by round. Fast path: only "could any coin be live?" — the minimum of a lane's 4*kHubIlp coins
+// against the node threshold — then one warp vote; exact masks (packed 4 bits per chain) are
+// built from the same registers only when some lane may hold a live slot.
+template <int SCHEME, class OnLive>
+__device__ __forceinline__ bool hub_sweep_whole(const RRParams& p, uint32_t id_lo, uint32_t id_hi,
+                                                uint32_t a, uint32_t b, uint32_t g0, uint32_t steps,
+                                                uint32_t thr, bool never, int lane, uint32_t& lives,
+                                                OnLive on_live) {
+  if (never) return true;
+  for (uint32_t gb = g0, s = 0; s < steps; ++s, gb += kHubGroups) {
+    uint4 w[kHubIlp];
+#pragma unroll
+    for (int r = 0; r < kHubIlp; ++r) w[r] = make_uint4(id_lo, id_hi, gb + 32u * r + lane, 0u);
+    philox4x32_10_rk_xn<kHubIlp>(w, p.rk);
+    uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+    for (int r = 0; r < kHubIlp; ++r) mn = min(mn, min(min(w[r].x, w[r].y), min(w[r].z, w[r].w)));
+    if (!__any_sync(kFull, SCHEME == W_EXPLICIT || mn <= thr)) continue;
+    uint32_t packed = 0;
+    if (SCHEME != W_EXPLICIT) {
+#pragma unroll
+      for (int r = 0; r < kHubIlp; ++r)
+        packed |= live_mask_words<SCHEME>(p, w[r], gb + 32u * r + lane, a, b, thr) << (4 * r);
+      if (!__any_sync(kFull, packed)) continue;
+    }
+#pragma unroll 1
+    for (int r = 0; r < kHubIlp; ++r) {
+      uint32_t m;
+      if (SCHEME != W_EXPLICIT) {
+        m = (packed >> (4 * r)) & 0xFu;
+      } else {   // per-edge thresholds: one chain's mask at a time (register pressure)
+        uint4 wr = w[0];
+#pragma unroll
+        for (int t = 1; t < kHubIlp; ++t) wr = (t == r) ? w[t] : wr;
+        m = live_mask_words<SCHEME>(p, wr, gb + 32u * r + lane, a, b, thr);
+      }
+      if (!__any_sync(kFull, m)) continue;
+      lives += __popc(m);
+      if (!on_live(gb + 32u * r + lane, m)) return false;
+    }
+  }
+  return true;
+}
 
 // Sweep of one node's slot groups [a>>2, (b-1)>>2] with kHubIlp independent Philox chains per
 // lane (128 x kHubIlp slots per warp step). Fast path: only "could any coin be live?" — the
@@ -255,25 +311,29 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
         coins += b - a;
         resume = head;                                  // batch start: re-expanded on overflow
         head += nb;
-        // hubs (>= kHubGroups slot groups) are swept alone below; the rest are flattened here
-        const uint32_t hubs = __ballot_sync(kFull, ng >= kHubGroups);
-        const uint32_t ngf = (ng >= kHubGroups) ? 0u : ng;
+        // a hub (>= kHubGroups slot groups) sweeps its whole kHubGroups-steps alone below; the
+        // remaining < kHubGroups groups of every node are flattened here
+        const uint32_t hub_full = ng & ~(kHubGroups - 1u);
+        const uint32_t hubs = __ballot_sync(kFull, hub_full != 0u);
+        const uint32_t ngf = ng - hub_full;
+        const uint32_t gs = (a >> 2) + hub_full;        // first flattened group of this node
         uint32_t total_g;
         const uint32_t E = warp_excl_scan(ngf, lane, total_g);   // exclusive group prefix
         const uint32_t P = E + ngf;
+        const uint32_t top = nb > 1 ? 1u << (31 - __clz(nb - 1)) : 0u;   // search depth ~ log2(nb)
         for (uint32_t base = 0; base < total_g; base += 32) {
           const uint32_t gi = base + lane;
           uint32_t k = 0;                               // node of flattened group gi
-          if (nb > 1) {
 #pragma unroll
-            for (uint32_t step = 16; step >= 1; step >>= 1) {
+          for (uint32_t step = 16; step >= 1; step >>= 1) {
+            if (step <= top) {
               const uint32_t pv = __shfl_sync(kFull, P, k + step - 1);
               if (pv <= gi) k += step;
             }
           }
           const uint32_t ak = __shfl_sync(kFull, a, k), bk = __shfl_sync(kFull, b, k);
-          const uint32_t tk = __shfl_sync(kFull, thr, k), ek = __shfl_sync(kFull, E, k);
-          const uint32_t g = (ak >> 2) + (gi - ek);
+          const uint32_t tk = __shfl_sync(kFull, thr, k), gk = __shfl_sync(kFull, gs - E, k);
+          const uint32_t g = gk + gi;
           uint32_t m = 0;
           if (gi < total_g && !never) m = ic_live_mask<SCHEME>(p, id_lo, id_hi, k0, k1, g, ak, bk, tk);
           if (!__any_sync(kFull, m)) continue;          // no live in-edge in these 128 slots
@@ -284,9 +344,10 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
         for (uint32_t hm = overflow ? 0u : hubs; hm; hm &= hm - 1) {
           const uint32_t k = __ffs(hm) - 1;
           const uint32_t ak = __shfl_sync(kFull, a, k), bk = __shfl_sync(kFull, b, k);
-          const uint32_t tk = __shfl_sync(kFull, thr, k);
-          if (!hub_sweep<SCHEME>(p, id_lo, id_hi, ak, bk, tk, never, lane, lives,
-                                 [&](uint32_t g, uint32_t m) { return append_live(p, g, m, q, tail, lane, vis); }))
+          const uint32_t tk = __shfl_sync(kFull, thr, k), hk = __shfl_sync(kFull, hub_full, k);
+          if (!hub_sweep_whole<SCHEME>(p, id_lo, id_hi, ak, bk, ak >> 2, hk / kHubGroups, tk, never, lane,
+                                       lives,
+                                       [&](uint32_t g, uint32_t m) { return append_live(p, g, m, q, tail, lane, vis); }))
             overflow = true;
         }
         __syncwarp();

@@ -584,6 +584,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
                                     reinterpret_cast<uint32_t*>(c->seg_desc.as<InvSegDev>() + kMaxInvSeg),
                                     c->stream), "k_set_segs"));
   }
+  const bool limited = c->set_limit != ~0ull;     // cover must skip truncated sets
   const InvSegDev* segd = c->seg_desc.as<InvSegDev>();
   const uint32_t* nsegd = reinterpret_cast<const uint32_t*>(segd + kMaxInvSeg);
   CK(cudaMemcpyAsync(c->cnt.p, c->count_total.p, n * 4, cudaMemcpyDeviceToDevice, c->stream));
@@ -616,7 +617,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
     // buffer pointers; steady-state IMM runs reuse it), so the GPU runs them back to back.
     const std::vector<uintptr_t> key = {(uintptr_t)c->cnt.p, (uintptr_t)segd, (uintptr_t)cand,
                                         (uintptr_t)c->offsets.p, (uintptr_t)c->pool.p, (uintptr_t)c->covered.p,
-                                        (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n};
+                                        (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n, (uintptr_t)limited};
     if (!c->sel_exec || key != c->sel_key) {
       if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
       c->sel_exec = nullptr;
@@ -626,7 +627,8 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
         if (cand) launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream);
         launch_argmax(c->cnt.as<uint32_t>(), nullptr, c->n, keys, (int)j, tau_p1, c->num_sms * 4, c->stream);
         launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
-                     c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * 8, c->stream);
+                     c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * 8, c->stream,
+                     limited);
       }
       CK(cudaStreamEndCapture(c->stream, &graph));
       const cudaError_t ie = cudaGraphInstantiate(&c->sel_exec, graph, 0);
@@ -646,7 +648,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
                                       c->stream), "k_argmax"));
         TRY(launched(c, launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                                      c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * 8,
-                                     c->stream), "k_cover"));
+                                     c->stream, limited), "k_cover"));
       }
       if (dec && j + 1 < k) {
         c->st.allreduces++;
@@ -972,7 +974,6 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
   uint64_t cov = 0;
   std::vector<uint32_t> tmp(k);
   const int i_max = (int)std::floor(std::log2(n)) - 1;       // reading R5
-  bool passed = false;
   for (int i = 1; i <= i_max && i <= 64; ++i) {              // Alg. 2 l.2
     const double x = n / std::ldexp(1.0, i);                 // l.3
     const double theta_i = K.lambda_p / x;                   // l.4 (f = lambda', reading R1)
@@ -993,11 +994,9 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
     r.rounds = (uint32_t)i;
     if ((n * (double)cov) / (double)R >= (1.0 + K.eps_p) * x) {   // l.7 (reading R7)
       LB = (n * (double)cov) / (double)R / (1.0 + K.eps_p);       // l.8
-      passed = true;
       break;
     }
   }
-  (void)passed;
   const double theta = K.lambda_s / LB;                      // reading R2
   const uint64_t T = (uint64_t)std::ceil(theta);
   uint64_t R_last = 0;

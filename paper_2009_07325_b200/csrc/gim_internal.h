@@ -40,7 +40,8 @@ cudaError_t launch_argmax_cand(const uint32_t* cnt, const uint32_t* cand, const 
 struct InvSegDev;
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,
                          const uint64_t* offsets, const uint32_t* pool,
-                         uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s);
+                         uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s,
+                         bool limit);
 cudaError_t launch_validate_csr(const uint64_t* rp64, uint32_t n, uint64_t m, const uint32_t* src,
                                 uint32_t* rp32, uint32_t* err, uint32_t* bad_row, int grid, cudaStream_t s);
 }  // namespace gim

@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(256) k_argmax_cand(const uint32_t* __restrict_
 // short and mostly covered, so spreading entries over many groups (latency hiding) beats
 // flattening members within a warp (measured 19 vs 94 us per step on C3).
 // ------------------------------------------------------------------------------------------
+template <bool LIMIT>
 __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restrict__ keys, int j,
                                                const InvSegDev* __restrict__ segs,
                                                const uint32_t* __restrict__ nseg_ptr_unused,
@@ -346,6 +347,8 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
     const uint32_t l = threadIdx.x;
     InvSegDev sg{nullptr, nullptr};
     if (l < (uint32_t)kMaxInvSeg) sg = segs[l];  // unused slots are null: no dependency on nseg
+    // set-id limit (only after a tail truncation), loaded alongside the descriptors
+    const uint32_t lim = (LIMIT && l == 0) ? reinterpret_cast<const uint32_t*>(segs + kMaxInvSeg)[1] : 0u;
     uint64_t lo = 0, len = 0;
     if (sg.off) {
       lo = sg.off[u];
@@ -365,22 +368,22 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
     const uint32_t used = __ballot_sync(kFull, sg.off != nullptr);   // warp-wide vote
     if (l == 0) {
       s_nseg = __popc(used);
-      s_limit = reinterpret_cast<const uint32_t*>(segs + kMaxInvSeg)[1];
+      s_limit = lim;
     }
   }
   __syncthreads();
-  const uint32_t ns = s_nseg, limit = s_limit;
-  const uint64_t total = ns ? s_end[kMaxInvSeg - 1] : 0;
+  const uint32_t ns = s_nseg, limit = LIMIT ? s_limit : 0xFFFFFFFFu;
+  const uint64_t total = (ns && limit) ? s_end[kMaxInvSeg - 1] : 0;   // limit 0: every set cut
   const uint64_t ngroups = (uint64_t)gridDim.x * (blockDim.x >> 3);
   uint32_t q = 0;
   for (uint64_t t = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); t < total; t += ngroups) {
     while (t >= s_end[q]) ++q;                 // t increases monotonically per group
     const uint64_t pos = s_lo[q] + (t - (q ? s_end[q - 1] : 0));
-    const uint32_t r = s_inv[q][pos];
-    if (r >= limit) continue;                  // truncated away (tail of the last segment)
+    const uint32_t r0 = s_inv[q][pos];
+    const uint32_t r = LIMIT ? min(r0, limit - 1u) : r0;   // sets >= limit were truncated away
     const uint8_t cov = covered[r];            // flag and offsets loaded together
     const uint64_t a = offsets[r], b = offsets[r + 1];
-    if (cov) continue;
+    if (cov || (LIMIT && r0 != r)) continue;
     if (sub == 0) covered[r] = 1;      // each r appears once across the lists of u: no race
     if (dec == nullptr) {
       for (uint64_t e = a + sub; e < b; e += 8) {
@@ -475,8 +478,9 @@ cudaError_t launch_argmax_cand(const uint32_t* cnt, const uint32_t* cand, const 
 
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,
                          const uint64_t* offsets, const uint32_t* pool,
-                         uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s) {
-  k_cover<<<grid, 256, 0, s>>>(keys, j, segs, nseg, offsets, pool, covered, cnt, dec);
+                         uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s, bool limit) {
+  if (limit) k_cover<true><<<grid, 256, 0, s>>>(keys, j, segs, nseg, offsets, pool, covered, cnt, dec);
+  else k_cover<false><<<grid, 256, 0, s>>>(keys, j, segs, nseg, offsets, pool, covered, cnt, dec);
   return cudaGetLastError();
 }
 

@@ -141,7 +141,14 @@ constexpr int kRRWarps = 8;          // warps per CTA
 #endif
 constexpr int kQMax = GIM_QMAX;      // queue capacity (the queue doubles as the RR buffer)
 constexpr int kHSize = GIM_HSIZE;    // visited hash slots (load <= (Q + 128) / H)
-constexpr int kRRSmemPerWarp = (kQMax + kHSize) * 4;   // 6 KB -> 4 CTAs x 8 warps per SM
+#ifndef GIM_PEND
+#define GIM_PEND 128
+#endif
+// pending live in-edges of the batch being expanded (their src copies in flight, cp.async);
+// >= 128 = the most one warp step can find (32 lanes x 4 slots)
+constexpr int kPend = GIM_PEND;
+static_assert(kPend >= 128, "one warp step can find 128 live slots");
+constexpr int kRRSmemPerWarp = (kQMax + kHSize + kPend) * 4;   // 6.5 KB -> 4 CTAs x 8 warps per SM
 #ifndef GIM_RR_BLOCKS
 #define GIM_RR_BLOCKS 4
 #endif

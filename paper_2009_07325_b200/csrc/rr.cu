@@ -34,6 +34,13 @@ __device__ __forceinline__ bool hash_insert(uint32_t* h, uint32_t u) {
   }
 }
 
+// Asynchronous 4-byte global -> shared copy (completion: cp_async_wait_all, then __syncwarp).
+__device__ __forceinline__ void cp_async4(uint32_t* dst_smem, const uint32_t* src) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // LT: index of the chosen in-edge of v (0..d-1) or d if none (reading R18). Warp-collective.
 template <int SCHEME>
 __device__ __forceinline__ uint32_t lt_choose(const RRParams& p, uint64_t id, uint32_t v,
@@ -250,8 +257,9 @@ template <int MODEL, int SCHEME>
 __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRParams p) {
   extern __shared__ uint32_t smem[];
   const int lane = threadIdx.x & 31;
-  uint32_t* q = smem + (threadIdx.x >> 5) * (kQMax + kHSize);
+  uint32_t* q = smem + (threadIdx.x >> 5) * (kQMax + kHSize + kPend);
   uint32_t* h = q + kQMax;
+  uint32_t* pend = h + kHSize;
   for (int i = lane; i < kHSize; i += 32) h[i] = kEmpty;
   __syncwarp();
   const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
@@ -290,7 +298,52 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
     bool overflow = false;
     if (MODEL == MODEL_IC) {
       const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
-      auto vis = [h](uint32_t u) { return hash_insert(h, u); };
+      // Live in-edges found during a batch are not resolved on the spot: each lane starts an
+      // asynchronous copy of src[e] into pend[] and the sweep goes on, so the batch's source
+      // loads overlap its remaining coin work and each other. flush() waits once, then
+      // test-and-sets the sources in the visited hash and appends the new ones to the queue.
+      uint32_t npend = 0;                                // warp-uniform
+      auto flush = [&]() -> bool {
+        cp_async_wait_all();
+        __syncwarp();
+        bool ok = true;
+        for (uint32_t base = 0; base < npend; base += 32) {
+          const uint32_t i = base + lane;
+          uint32_t u = 0;
+          bool isnew = false;
+          if (i < npend) {
+            u = pend[i];
+            isnew = hash_insert(h, u);
+          }
+          const uint32_t has = __ballot_sync(kFull, isnew);
+          const uint32_t total = __popc(has);
+          if (tail + total > p.qcap) { ok = false; break; }
+          if (isnew) q[tail + __popc(has & ((1u << lane) - 1u))] = u;
+          tail += total;
+        }
+        npend = 0;
+        __syncwarp();
+        return ok;
+      };
+      auto pend_add = [&](uint32_t g, uint32_t m) -> bool {
+        const uint32_t cnt = __popc(m);
+        uint32_t total, off;
+        if (!__any_sync(kFull, cnt > 1u)) {            // usual case: <= 1 live slot per lane
+          const uint32_t has = __ballot_sync(kFull, cnt != 0u);
+          total = __popc(has);
+          off = __popc(has & ((1u << lane) - 1u));
+        } else {
+          off = warp_excl_scan(cnt, lane, total);
+        }
+        if (npend + total > (uint32_t)kPend && !flush()) return false;
+        uint32_t pos = npend + off;
+        const uint32_t e0 = g << 2;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (m & (1u << j)) cp_async4(pend + pos++, p.src + e0 + j);
+        npend += total;
+        return true;
+      };
       // Expand every pending frontier node of this RR set together: lane i holds node
       // q[head + i] of the batch (row range, live threshold, group count), the warp sweeps the
       // concatenation of their slot-group ranges 32 groups at a time, and live in-edges found
@@ -338,7 +391,7 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
           if (gi < total_g && !never) m = ic_live_mask<SCHEME>(p, id_lo, id_hi, k0, k1, g, ak, bk, tk);
           if (!__any_sync(kFull, m)) continue;          // no live in-edge in these 128 slots
           lives += __popc(m);
-          if (!append_live(p, g, m, q, tail, lane, vis)) { overflow = true; break; }
+          if (!pend_add(g, m)) { overflow = true; break; }
         }
         // hub sweep: kHubIlp independent Philox chains per lane, 128 x kHubIlp slots per step
         for (uint32_t hm = overflow ? 0u : hubs; hm; hm &= hm - 1) {
@@ -346,10 +399,10 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
           const uint32_t ak = __shfl_sync(kFull, a, k), bk = __shfl_sync(kFull, b, k);
           const uint32_t tk = __shfl_sync(kFull, thr, k), hk = __shfl_sync(kFull, hub_full, k);
           if (!hub_sweep_whole<SCHEME>(p, id_lo, id_hi, ak, bk, ak >> 2, hk / kHubGroups, tk, never, lane,
-                                       lives,
-                                       [&](uint32_t g, uint32_t m) { return append_live(p, g, m, q, tail, lane, vis); }))
+                                       lives, pend_add))
             overflow = true;
         }
+        if (!overflow && !flush()) overflow = true;
         __syncwarp();
         if (overflow) break;
       }

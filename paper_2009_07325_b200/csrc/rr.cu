@@ -793,6 +793,15 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
 constexpr uint32_t kSplitGroups = 2048;   // hub nodes above this are split across warps
 constexpr uint32_t kChunkRing = 128;      // shared ring of published hub chunks
 constexpr uint32_t kBusySlot = 0xFFFFFFFEu; // ring slot being written (node ids are < 2^32 - 2)
+constexpr uint32_t kGiantWarps = kGiantThreads / 32;
+static_assert(kSplitGroups % kHubGroups == 0, "hub chunks are whole hub steps");
+
+// Relaxed load at gpu scope (not hoisted out of spin loops, not served from a stale L1 line).
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* ptr) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
 
 template <int MODEL, int SCHEME>
 __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint32_t* bitmaps,
@@ -823,6 +832,51 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if (uu[j] != kEmpty) Q[pos++] = uu[j];
+  };
+  // IC: live in-edges of a claimed batch, resolved together (as in K-RR): cp.async of src[e]
+  // into pend[], then one wait, bitmap test-and-set and append per 32 entries
+  __shared__ uint32_t s_pend[kGiantWarps][kPend];
+  uint32_t* pend = s_pend[threadIdx.x >> 5];
+  uint32_t npend = 0;                                  // warp-uniform
+  auto flush = [&]() {
+    cp_async_wait_all();
+    __syncwarp();
+    for (uint32_t base = 0; base < npend; base += 32) {
+      const uint32_t i = base + lane;
+      uint32_t u = 0;
+      bool isnew = false;
+      if (i < npend) {
+        u = pend[i];
+        isnew = visit(u);
+      }
+      const uint32_t has = __ballot_sync(kFull, isnew);
+      const uint32_t total = __popc(has);
+      uint32_t b0 = 0;
+      if (lane == 0 && total) b0 = atomicAdd(&s_tail, total);
+      b0 = __shfl_sync(kFull, b0, 0);
+      if (isnew) Q[b0 + __popc(has & ((1u << lane) - 1u))] = u;
+    }
+    npend = 0;
+    __syncwarp();
+  };
+  auto pend_add = [&](uint32_t g, uint32_t m) -> bool {
+    const uint32_t cnt = __popc(m);
+    uint32_t total, off;
+    if (!__any_sync(kFull, cnt > 1u)) {
+      const uint32_t has = __ballot_sync(kFull, cnt != 0u);
+      total = __popc(has);
+      off = __popc(has & ((1u << lane) - 1u));
+    } else {
+      off = warp_excl_scan(cnt, lane, total);
+    }
+    if (npend + total > (uint32_t)kPend) flush();
+    uint32_t pos = npend + off;
+    const uint32_t e0 = g << 2;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (m & (1u << j)) cp_async4(pend + pos++, p.src + e0 + j);
+    npend += total;
+    return true;
   };
 
   while (true) {
@@ -858,10 +912,10 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
       s_cres = 0;
     }
     __syncthreads();
-    // asynchronous expansion: warps claim published hub chunks first, then queued nodes, until
-    // nothing is pending and no warp is busy
+    // asynchronous expansion: warps claim published hub chunks first, then batches of queued
+    // nodes, until nothing is pending and no warp is busy
     while (true) {
-      uint32_t f = 0, state = 0;                 // 1 = node f, 3 = ring entry f, 2 = done
+      uint32_t f = 0, state = 0, c = 1;          // 1 = nodes Q[f, f+c), 3 = ring entry f, 2 = done
       if (lane == 0) {
         atomicAdd(&s_busy, 1u);
         while (true) {
@@ -874,7 +928,10 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
           const uint32_t h = *(volatile uint32_t*)&s_head;
           const uint32_t t = *(volatile uint32_t*)&s_tail;
           if (h < t) {
-            if (atomicCAS(&s_head, h, h + 1) == h) { f = h; state = 1; break; }
+            // IC: a batch of up to 32 nodes, smaller while the frontier is narrow so that
+            // every warp of the block gets work; LT: one node (its walk is a single path)
+            const uint32_t want = (MODEL == MODEL_IC) ? min(32u, max(1u, (t - h) / kGiantWarps)) : 1u;
+            if (atomicCAS(&s_head, h, h + want) == h) { f = h; c = want; state = 1; break; }
             continue;
           }
           atomicSub(&s_busy, 1u);
@@ -895,98 +952,120 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
       state = __shfl_sync(kFull, state, 0);
       if (state == 2) break;
       f = __shfl_sync(kFull, f, 0);
-      uint32_t v, a, b, thr = 0;
-      bool node_start = false;
-      if (state == 3) {                          // a published chunk of a hub node
-        uint4 e;
-        if (lane == 0) {
-          volatile uint4* slot = &s_ring[f % kChunkRing];
-          while ((e.x = slot->x) == kEmpty || e.x == kBusySlot) __nanosleep(32);
-          __threadfence_block();
-          e.y = slot->y; e.z = slot->z; e.w = slot->w;
-          __threadfence_block();
-          slot->x = kEmpty;                      // consumed
-        }
-        v = __shfl_sync(kFull, e.x, 0);
-        a = __shfl_sync(kFull, e.y, 0);
-        b = __shfl_sync(kFull, e.z, 0);
-        thr = __shfl_sync(kFull, e.w, 0);
-      } else {
-        // the appender may still be writing the entry: read it at L2 (atomic), sleep while empty
-        v = atomicOr(Q + f, 0u);
-        while (v == kEmpty) {
-          __nanosleep(32);
-          v = atomicOr(Q + f, 0u);
-        }
-        a = __ldg(p.row_ptr + v);
-        b = __ldg(p.row_ptr + v + 1);
-        node_start = true;
-      }
-      if (b > a) {
-        if (MODEL == MODEL_IC) {
-          if (node_start) {
-            thr = node_thr<SCHEME>(p, b - a);
-            if (lane == 0) coins += b - a;
-            const uint32_t g_lo = a >> 2, g_hi = (b - 1) >> 2;
-            if (g_hi - g_lo + 1 > kSplitGroups) {  // hub: publish chunks 1.. for idle warps
-              const uint32_t nch = (g_hi - g_lo) / kSplitGroups;   // chunks after the first
-              uint32_t pushed = 0, base = 0;
+      c = __shfl_sync(kFull, c, 0);
+      if (MODEL == MODEL_IC) {
+        if (state == 3) {                        // a published chunk [a, b) of a hub node
+          uint4 e;
+          if (lane == 0) {
+            volatile uint4* slot = &s_ring[f % kChunkRing];
+            while ((e.x = slot->x) == kEmpty || e.x == kBusySlot) __nanosleep(32);
+            __threadfence_block();
+            e.y = slot->y; e.z = slot->z; e.w = slot->w;
+            __threadfence_block();
+            slot->x = kEmpty;                    // consumed
+          }
+          const uint32_t a = __shfl_sync(kFull, e.y, 0), b = __shfl_sync(kFull, e.z, 0);
+          const uint32_t thr = __shfl_sync(kFull, e.w, 0);
+          hub_sweep<SCHEME>(p, id_lo, id_hi, a, b, thr, never, lane, lives, pend_add);
+        } else {
+          // a batch of c queued nodes, expanded like a K-RR batch: lane i holds node Q[f+i]
+          uint32_t a = 0, b = 0, thr = 0, ng = 0;
+          if ((uint32_t)lane < c) {
+            // the appender may still be writing the entry: read it at L2, sleep while empty
+            uint32_t v = ld_relaxed_gpu(Q + f + lane);
+            while (v == kEmpty) {
+              __nanosleep(32);
+              v = ld_relaxed_gpu(Q + f + lane);
+            }
+            a = __ldg(p.row_ptr + v);
+            b = __ldg(p.row_ptr + v + 1);
+            if (b > a) {
+              ng = ((b - 1) >> 2) - (a >> 2) + 1;
+              thr = node_thr<SCHEME>(p, b - a);
+              coins += b - a;
+            }
+          }
+          const uint32_t hub_full = ng & ~(kHubGroups - 1u);
+          const uint32_t hubs = __ballot_sync(kFull, hub_full != 0u);
+          const uint32_t ngf = ng - hub_full;
+          const uint32_t gs = (a >> 2) + hub_full;
+          uint32_t total_g;
+          const uint32_t E = warp_excl_scan(ngf, lane, total_g);
+          const uint32_t P = E + ngf;
+          const uint32_t top = c > 1 ? 1u << (31 - __clz(c - 1)) : 0u;
+          for (uint32_t base = 0; base < total_g; base += 32) {
+            const uint32_t gi = base + lane;
+            uint32_t k = 0;
+#pragma unroll
+            for (uint32_t step = 16; step >= 1; step >>= 1) {
+              if (step <= top) {
+                const uint32_t pv = __shfl_sync(kFull, P, k + step - 1);
+                if (pv <= gi) k += step;
+              }
+            }
+            const uint32_t ak = __shfl_sync(kFull, a, k), bk = __shfl_sync(kFull, b, k);
+            const uint32_t tk = __shfl_sync(kFull, thr, k), gk = __shfl_sync(kFull, gs - E, k);
+            const uint32_t g = gk + gi;
+            uint32_t m = 0;
+            if (gi < total_g && !never) m = ic_live_mask<SCHEME>(p, id_lo, id_hi, 0u, 0u, g, ak, bk, tk);
+            if (!__any_sync(kFull, m)) continue;
+            lives += __popc(m);
+            pend_add(g, m);
+          }
+          for (uint32_t hm = hubs; hm; hm &= hm - 1) {
+            const uint32_t k = __ffs(hm) - 1;
+            const uint32_t ak = __shfl_sync(kFull, a, k), bk = __shfl_sync(kFull, b, k);
+            const uint32_t tk = __shfl_sync(kFull, thr, k), hk = __shfl_sync(kFull, hub_full, k);
+            const uint32_t g_lo = ak >> 2;
+            uint32_t kept = hk;                  // whole-step groups this warp sweeps itself
+            if (hk > kSplitGroups) {
+              // big hub: publish its groups [g_lo + kSplitGroups, g_lo + hk) as chunks of
+              // kSplitGroups for idle warps (ring room permitting); sweep the rest here
+              const uint32_t nch = (hk - 1) / kSplitGroups;   // chunks after the first
+              uint32_t pushed = 0, rbase = 0;
               if (lane == 0) {                   // reserve ring room: outstanding <= kChunkRing
                 while (true) {
                   const uint32_t cr = *(volatile uint32_t*)&s_cres;
                   const uint32_t ch = *(volatile uint32_t*)&s_chead;
-                  const uint32_t m = min(nch, kChunkRing - (cr - ch));
-                  if (m == 0) break;
-                  if (atomicCAS(&s_cres, cr, cr + m) == cr) { pushed = m; base = cr; break; }
+                  const uint32_t mm = min(nch, kChunkRing - (cr - ch));
+                  if (mm == 0) break;
+                  if (atomicCAS(&s_cres, cr, cr + mm) == cr) { pushed = mm; rbase = cr; break; }
                 }
               }
               pushed = __shfl_sync(kFull, pushed, 0);
-              base = __shfl_sync(kFull, base, 0);
-              if (pushed) {
-                for (uint32_t c = lane; c < pushed; c += 32) {
-                  const uint32_t gs = g_lo + (c + 1) * kSplitGroups;
-                  const uint32_t ge = min(g_hi, gs + kSplitGroups - 1);
-                  uint4* slot = &s_ring[(base + c) % kChunkRing];
-                  while (atomicCAS(&slot->x, kEmpty, kBusySlot) != kEmpty) __nanosleep(32);
-                  volatile uint4* vs = slot;
-                  vs->y = max(a, gs << 2);
-                  vs->z = min(b, (ge + 1) << 2);
-                  vs->w = thr;
-                  __threadfence_block();
-                  vs->x = v;                     // publish
-                }
-                // this warp keeps chunk 0 and any chunks that did not fit in the ring
-                const uint32_t kept_end = min(b, (g_lo + kSplitGroups) << 2);   // chunk 0
-                hub_sweep<SCHEME>(p, id_lo, id_hi, a, kept_end, thr, never, lane, lives,
-                                  [&](uint32_t g, uint32_t m) {
-                                    uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
-                                    if (m) ic_take_live(p, g, m, uu, visit);
-                                    append(uu);
-                                    return true;
-                                  });
-                if (pushed < nch) {              // sweep the chunks beyond the pushed ones
-                  const uint32_t rs = (g_lo + (pushed + 1) * kSplitGroups) << 2;
-                  if (rs < b)
-                    hub_sweep<SCHEME>(p, id_lo, id_hi, rs, b, thr, never, lane, lives,
-                                      [&](uint32_t g, uint32_t m) {
-                                        uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
-                                        if (m) ic_take_live(p, g, m, uu, visit);
-                                        append(uu);
-                                        return true;
-                                      });
-                }
-                b = a;                           // done with this node
+              rbase = __shfl_sync(kFull, rbase, 0);
+              const uint32_t g_end = g_lo + hk;
+              for (uint32_t cc = lane; cc < pushed; cc += 32) {
+                const uint32_t cs = g_lo + (cc + 1) * kSplitGroups;
+                const uint32_t ce = min(g_end, cs + kSplitGroups);
+                uint4* slot = &s_ring[(rbase + cc) % kChunkRing];
+                while (atomicCAS(&slot->x, kEmpty, kBusySlot) != kEmpty) __nanosleep(32);
+                volatile uint4* vs = slot;
+                vs->y = cs << 2;                 // cs > g_lo: past a
+                vs->z = min(bk, ce << 2);
+                vs->w = tk;
+                __threadfence_block();
+                vs->x = 0u;                      // publish (any value but kEmpty / kBusySlot)
               }
+              kept = kSplitGroups;
+              const uint32_t rs = g_lo + (pushed + 1) * kSplitGroups;   // unpushed chunks
+              if (rs < g_end)
+                hub_sweep<SCHEME>(p, id_lo, id_hi, rs << 2, min(bk, g_end << 2), tk, never, lane, lives,
+                                  pend_add);
             }
+            hub_sweep_whole<SCHEME>(p, id_lo, id_hi, ak, bk, g_lo, kept / kHubGroups, tk, never, lane, lives,
+                                    pend_add);
           }
-          if (b > a)
-            hub_sweep<SCHEME>(p, id_lo, id_hi, a, b, thr, never, lane, lives, [&](uint32_t g, uint32_t m) {
-              uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};
-              if (m) ic_take_live(p, g, m, uu, visit);
-              append(uu);
-              return true;
-            });
-        } else {
+        }
+        flush();
+      } else {                                   // LT: one node, one draw
+        uint32_t v = ld_relaxed_gpu(Q + f);
+        while (v == kEmpty) {
+          __nanosleep(32);
+          v = ld_relaxed_gpu(Q + f);
+        }
+        const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
+        if (b > a) {
           const uint32_t d = b - a;
           const uint32_t j = lt_choose<SCHEME>(p, id, v, a, d, lane);
           uint32_t uu[4] = {kEmpty, kEmpty, kEmpty, kEmpty};

@@ -35,9 +35,9 @@ __device__ __forceinline__ bool hash_insert(uint32_t* h, uint32_t u) {
 }
 
 // Asynchronous 4-byte global -> shared copy (completion: cp_async_wait_all, then __syncwarp).
-__device__ __forceinline__ void cp_async4(uint32_t* dst_smem, const uint32_t* src) {
-  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src) : "memory");
+// dst: shared-space byte address (__cvta_generic_to_shared of the buffer, computed once)
+__device__ __forceinline__ void cp_async4(uint32_t dst, const uint32_t* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -260,6 +260,7 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
   uint32_t* q = smem + (threadIdx.x >> 5) * (kQMax + kHSize + kPend);
   uint32_t* h = q + kQMax;
   uint32_t* pend = h + kHSize;
+  const uint32_t pend_s = (uint32_t)__cvta_generic_to_shared(pend);
   for (int i = lane; i < kHSize; i += 32) h[i] = kEmpty;
   __syncwarp();
   const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
@@ -336,11 +337,11 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
           off = warp_excl_scan(cnt, lane, total);
         }
         if (npend + total > (uint32_t)kPend && !flush()) return false;
-        uint32_t pos = npend + off;
-        const uint32_t e0 = g << 2;
+        uint32_t pos = pend_s + 4u * (npend + off);
+        const uint32_t* sp = p.src + (g << 2);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (m & (1u << j)) cp_async4(pend + pos++, p.src + e0 + j);
+          if (m & (1u << j)) { cp_async4(pos, sp + j); pos += 4u; }
         npend += total;
         return true;
       };
@@ -837,6 +838,7 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
   // into pend[], then one wait, bitmap test-and-set and append per 32 entries
   __shared__ uint32_t s_pend[kGiantWarps][kPend];
   uint32_t* pend = s_pend[threadIdx.x >> 5];
+  const uint32_t pend_s = (uint32_t)__cvta_generic_to_shared(pend);
   uint32_t npend = 0;                                  // warp-uniform
   auto flush = [&]() {
     cp_async_wait_all();
@@ -870,11 +872,11 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
       off = warp_excl_scan(cnt, lane, total);
     }
     if (npend + total > (uint32_t)kPend) flush();
-    uint32_t pos = npend + off;
-    const uint32_t e0 = g << 2;
+    uint32_t pos = pend_s + 4u * (npend + off);
+    const uint32_t* sp = p.src + (g << 2);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      if (m & (1u << j)) cp_async4(pend + pos++, p.src + e0 + j);
+      if (m & (1u << j)) { cp_async4(pos, sp + j); pos += 4u; }
     npend += total;
     return true;
   };

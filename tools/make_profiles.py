@@ -29,6 +29,7 @@ KEYS = [
     "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
     "smsp__thread_inst_executed_per_inst_executed.ratio",
     "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
@@ -66,9 +67,9 @@ def launch_shares(wl, rnd):
              f"{'kernel':44s} {'launches':>8s} {'total_ms':>10s} {'avg_us':>10s} {'share':>6s}"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"{k:44s} {v[0]:8d} {v[1] / 1e3:10.3f} {v[1] / v[0]:10.1f} {v[1] / tot:6.3f}")
-    no_bench = tot - agg.get("k_philox_bench", [0, 0.0])[1]
-    lines.append(f"# share of the hot path without the microbenchmark: k_rr_warp "
-                 f"{agg.get("k_rr_warp<0, 1>", [0, 0])[1] / no_bench:.3f}")
+    no_bench = tot - sum(v[1] for k, v in agg.items() if k.startswith("k_philox_bench"))
+    rr = sum(v[1] for k, v in agg.items() if k.startswith("k_rr_warp"))
+    lines.append(f"# share of the hot path without the microbenchmark: k_rr_warp {rr / no_bench:.3f}")
     open(os.path.join(OUT, f"{rnd}_launch_shares_{wl}.txt"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 

@@ -795,6 +795,10 @@ constexpr uint32_t kSplitGroups = 2048;   // hub nodes above this are split acro
 constexpr uint32_t kChunkRing = 128;      // shared ring of published hub chunks
 constexpr uint32_t kBusySlot = 0xFFFFFFFEu; // ring slot being written (node ids are < 2^32 - 2)
 constexpr uint32_t kGiantWarps = kGiantThreads / 32;
+#ifndef GIM_GIANT_DIV
+#define GIM_GIANT_DIV 4
+#endif
+constexpr uint32_t kGiantClaimDiv = GIM_GIANT_DIV;   // batch = pending / this, clamped to [1, 32]
 static_assert(kSplitGroups % kHubGroups == 0, "hub chunks are whole hub steps");
 
 // Relaxed load at gpu scope (not hoisted out of spin loops, not served from a stale L1 line).
@@ -932,7 +936,7 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
           if (h < t) {
             // IC: a batch of up to 32 nodes, smaller while the frontier is narrow so that
             // every warp of the block gets work; LT: one node (its walk is a single path)
-            const uint32_t want = (MODEL == MODEL_IC) ? min(32u, max(1u, (t - h) / kGiantWarps)) : 1u;
+            const uint32_t want = (MODEL == MODEL_IC) ? min(32u, max(1u, (t - h) / kGiantClaimDiv)) : 1u;
             if (atomicCAS(&s_head, h, h + want) == h) { f = h; c = want; state = 1; break; }
             continue;
           }

@@ -496,10 +496,6 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
                                  c->num_sms * 8, c->stream), "k_store"));
   }
   c->segs.push_back(Seg{gstart, c->nsets, cnt});
-  if (c->inv_segmented && c->inv_valid && c->iseg.size() < (size_t)kMaxInvSeg)
-    TRY(build_inv_segment(c, c->nsets, c->nsets + cnt, c->pool_len, c->pool_len + total));
-  else
-    c->inv_valid = false;                      // rebuilt as one segment at the next selection
   c->nsets += cnt;
   c->pool_len += total;
   c->st.rr_sets += cnt;
@@ -547,7 +543,16 @@ gim_status generate(gim_ctx* c, uint64_t theta, uint64_t seed) {
     const uint64_t a = c->T_global, len = theta - a;
     const uint64_t lo = a + (uint64_t)((unsigned __int128)len * c->rank / c->world);
     const uint64_t hi = a + (uint64_t)((unsigned __int128)len * (c->rank + 1) / c->world);
+    const uint64_t set0 = c->nsets, e0 = c->pool_len;
     for (uint64_t s = lo; s < hi; s += kChunk) TRY(gen_chunk(c, s, (uint32_t)std::min<uint64_t>(kChunk, hi - s)));
+    // one inverted-index segment per generate call (= per IMM round): its O(n) count scan is
+    // paid once per round, not once per 2^22-id chunk
+    if (c->nsets > set0) {
+      if (c->inv_segmented && c->inv_valid && c->iseg.size() < (size_t)kMaxInvSeg)
+        TRY(build_inv_segment(c, set0, c->nsets, e0, c->pool_len));
+      else
+        c->inv_valid = false;                  // rebuilt as one segment at the next selection
+    }
     c->T_global = theta;
   }
   return sync(c);

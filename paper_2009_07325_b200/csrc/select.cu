@@ -252,12 +252,43 @@ __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int3
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_cnt_hist(const uint32_t* __restrict__ cnt, uint32_t n,
                                                   unsigned int* __restrict__ hist) {
+  // bucket floor(log2(c + 1)), 0..32. Streams cnt as uint4 (4 loads in flight per thread); the
+  // common small buckets 0..7 are counted in registers (a shared atomic per count serialises
+  // when nearly every node falls in the same bucket), the rest with shared atomics.
   __shared__ unsigned int h[33];
   if (threadIdx.x < 33) h[threadIdx.x] = 0;
   __syncthreads();
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const uint32_t c = cnt[v];
-    atomicAdd(&h[31 - __clz(c + 1u)], 1u);           // bucket floor(log2(c + 1)), 0..32
+  uint32_t r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  auto add = [&](uint32_t c) {
+    const uint32_t b = 31 - __clz(c + 1u);
+    if (b < 8) {
+#pragma unroll
+      for (uint32_t j = 0; j < 8; ++j) r[j] += (b == j);
+    } else {
+      atomicAdd(&h[b], 1u);
+    }
+  };
+  const uint32_t n4 = n >> 2;
+  const uint4* c4 = reinterpret_cast<const uint4*>(cnt);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += 4 * stride) {
+    uint4 w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * stride;
+      w[u] = (i < n4) ? __ldcs(c4 + i) : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i0 + u * stride >= n4) continue;             // past the end
+      add(w[u].x); add(w[u].y); add(w[u].z); add(w[u].w);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3u)) add(cnt[(n4 << 2) + threadIdx.x]);
+#pragma unroll
+  for (uint32_t j = 0; j < 8; ++j) {
+    const uint32_t t = __reduce_add_sync(kFull, r[j]);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(&h[j], t);
   }
   __syncthreads();
   if (threadIdx.x < 33 && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
@@ -281,15 +312,41 @@ __global__ void __launch_bounds__(256) k_cand_compact(const uint32_t* __restrict
                                                       const uint32_t* __restrict__ tau_p1,
                                                       uint32_t* __restrict__ cand, unsigned int* ncand) {
   const uint32_t t = *tau_p1;
+  if (t == 0xFFFFFFFFu) return;
   const int lane = threadIdx.x & 31;
-  for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < n; v0 += gridDim.x * blockDim.x) {
-    const uint32_t v = v0 + threadIdx.x;
-    const bool take = v < n && cnt[v] >= t && t != 0xFFFFFFFFu;
-    const uint32_t m = __ballot_sync(kFull, take);
-    uint32_t base = 0;
-    if (lane == 0 && m) base = atomicAdd(ncand, (unsigned int)__popc(m));
-    base = __shfl_sync(kFull, base, 0);
-    if (take) cand[base + __popc(m & ((1u << lane) - 1u))] = v;
+  const uint32_t n4 = (n + 3) >> 2;                    // uint4 groups; the ragged tail is masked
+  const uint4* c4 = reinterpret_cast<const uint4*>(cnt);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  // warp-uniform trip count: every lane of a warp runs the same iterations (ballots below)
+  for (uint32_t b0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); b0 < n4; b0 += 4 * stride) {
+    uint4 w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = b0 + u * stride + lane;
+      if (i + 1 < n4 || (i + 1 == n4 && (n & 3u) == 0)) w[u] = __ldcs(c4 + i);
+      else if (i + 1 == n4) {                          // last group, partly past n
+        const uint32_t v = i << 2;
+        w[u] = make_uint4(cnt[v], v + 1 < n ? cnt[v + 1] : 0u, v + 2 < n ? cnt[v + 2] : 0u, 0u);
+      } else {
+        w[u] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = b0 + u * stride + lane;
+      const uint32_t v = i << 2;
+      const uint32_t m = (uint32_t)(w[u].x >= t && v < n) | ((uint32_t)(w[u].y >= t && v + 1 < n) << 1) |
+                         ((uint32_t)(w[u].z >= t && v + 2 < n) << 2) | ((uint32_t)(w[u].w >= t && v + 3 < n) << 3);
+      if (!__any_sync(kFull, m)) continue;             // usual: no candidate in these 128 nodes
+      uint32_t total;
+      const uint32_t off = warp_excl_scan_u32(__popc(m), lane, total);
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(ncand, total);
+      uint32_t pos = __shfl_sync(kFull, base, 0) + off;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (m & (1u << j)) cand[pos++] = v + j;
+    }
   }
 }
 

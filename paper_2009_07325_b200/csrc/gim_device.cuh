@@ -62,6 +62,18 @@ __device__ __forceinline__ void philox4x32_10_rk_xn(uint4 (&c)[N], const uint32_
   }
 }
 
+// Lane k (0..31) whose half-open range [P_{k-1}, P_k) contains i, given inclusive prefixes
+// P_k held per lane (non-decreasing; i < P_31). Warp-collective.
+__device__ __forceinline__ uint32_t warp_owner(uint32_t P, uint32_t i) {
+  uint32_t k = 0;
+#pragma unroll
+  for (uint32_t step = 16; step >= 1; step >>= 1) {
+    const uint32_t pv = __shfl_sync(kFull, P, k + step - 1);
+    if (pv <= i) k += step;
+  }
+  return k;
+}
+
 // Root of RR set `id`: floor(u64 * n / 2^64), u64 = out0 | out1 << 32 of slot 2^63
 // ("u = randSelect(V)", Alg. 3 l.5; reading R17).
 __device__ __forceinline__ uint32_t rr_root(uint64_t seed, uint64_t id, uint32_t n) {

@@ -1130,17 +1130,37 @@ __global__ void __launch_bounds__(256) k_store(const uint32_t* __restrict__ stag
                                                uint64_t pool_base, uint32_t* __restrict__ pool,
                                                uint64_t* __restrict__ offsets_out,
                                                uint32_t* __restrict__ count_total) {
+  // A warp takes 32 consecutive sets (contiguous in the pool) and copies their concatenated
+  // members 32 at a time: lane k holds set r0+k (size, staging offset, inclusive end), each
+  // element finds its set by a warp binary search. Pool writes are coalesced; tiny sets (C5:
+  // 1.5 members on average) no longer leave most lanes idle.
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < count; i += nwarps) {
-    const uint32_t sz = sizes[i];
-    const uint64_t from = soff[i], to = pool_base + scan[i];
-    for (uint32_t t = lane; t < sz; t += 32) {
-      const uint32_t v = staging[from + t];
-      pool[to + t] = v;
-      atomicAdd(count_total + v, 1u);
+  for (uint32_t r0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32u; r0 < count;
+       r0 += nwarps * 32u) {
+    const uint32_t nr = min(32u, count - r0);
+    const uint64_t base = scan[r0];
+    uint32_t sz = 0;
+    uint64_t from = 0;
+    if ((uint32_t)lane < nr) {
+      sz = sizes[r0 + lane];
+      from = soff[r0 + lane];
+      offsets_out[r0 + lane] = pool_base + scan[r0 + lane];
     }
-    if (lane == 0) offsets_out[i] = to;
+    uint32_t total;
+    const uint32_t E = warp_excl_scan(sz, lane, total);
+    const uint32_t P = E + sz;
+    for (uint32_t i0 = 0; i0 < total; i0 += 32) {       // warp-uniform trip count
+      const uint32_t i = i0 + lane;
+      const uint32_t k = warp_owner(P, i);
+      const uint64_t fk = __shfl_sync(kFull, from, k);
+      const uint32_t ek = __shfl_sync(kFull, E, k);
+      if (i < total) {
+        const uint32_t v = staging[fk + (i - ek)];
+        pool[pool_base + base + i] = v;
+        atomicAdd(count_total + v, 1u);
+      }
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) offsets_out[count] = pool_base + scan[count];
 }

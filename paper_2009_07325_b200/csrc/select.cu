@@ -114,15 +114,6 @@ __device__ __forceinline__ uint32_t warp_excl_scan_u32(uint32_t x, int lane, uin
   total = __shfl_sync(kFull, incl, 31);
   return incl - x;
 }
-__device__ __forceinline__ uint32_t warp_owner(uint32_t P, uint32_t i) {
-  uint32_t k = 0;
-#pragma unroll
-  for (uint32_t step = 16; step >= 1; step >>= 1) {
-    const uint32_t pv = __shfl_sync(kFull, P, k + step - 1);
-    if (pv <= i) k += step;
-  }
-  return k;
-}
 
 // ------------------------------------------------------------------------------------------
 // K-INV scatter: inv[inv_off[v] + cursor[v]++] = local set index r, for every member v of r.

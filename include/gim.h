@@ -105,7 +105,8 @@ gim_status gim_generate_rr(gim_ctx* ctx, uint64_t theta, uint64_t seed);
  * every uncovered RR set containing u_j is covered and count[w] -= 1 for each member (Alg. 7,
  * P:541-561; R11). seeds_out[k] required; gains_out[k] (marginal coverage) and covered_out
  * (sum of gains = |{i : S cap RR_i != {}}|) may be NULL. Errors: GIM_EINVAL (k < 1 or k > n),
- * GIM_ESTATE (empty pool / missing all-reduce), GIM_ECOLL, GIM_ECUDA. */
+ * GIM_ESTATE (empty pool / missing all-reduce), GIM_ENOMEM (also: the node -> RR index holds
+ * 32-bit positions, so a rank's pool must stay below 2^32 - 1 elements), GIM_ECOLL, GIM_ECUDA. */
 gim_status gim_select(gim_ctx* ctx, uint32_t k, uint32_t* seeds_out, uint64_t* gains_out,
                       uint64_t* covered_out);
 

@@ -258,8 +258,9 @@ void drop_inv(gim_ctx* c) {
 // histogram is count_total - cnt_snap (no extra atomics), then scan + cursor scatter.
 gim_status build_inv_segment(gim_ctx* c, uint64_t set0, uint64_t set1, uint64_t e0, uint64_t e1) {
   const uint64_t n = c->n;
+  if (e1 - e0 >= 0xFFFFFFFFull) return fail(c, GIM_ENOMEM, "an index segment must hold < 2^32 RR elements");
   gim_ctx::InvSeg sg;
-  TRY(dalloc(c, sg.off, (n + 1) * 8));
+  TRY(dalloc(c, sg.off, (n + 1) * 4));
   TRY(dalloc(c, sg.inv, std::max<uint64_t>(e1 - e0, 1) * 4));
   TRY(ensure(c, c->cursor, n * 4));
   TRY(ensure(c, c->scan_tmp, (scan_tiles(n) + 2) * 8));
@@ -267,14 +268,14 @@ gim_status build_inv_segment(gim_ctx* c, uint64_t set0, uint64_t set1, uint64_t 
   TRY(launched(c, launch_count_delta(c->count_total.as<uint32_t>(), c->cnt_snap.as<uint32_t>(),
                                      c->cursor.as<uint32_t>(), c->n, c->num_sms * 8, c->stream), "k_count_delta"));
   int nl = 0;
-  cudaError_t e = launch_scan_u32(c->cursor.as<uint32_t>(), n, sg.off.as<uint64_t>(), c->scan_tmp.as<uint64_t>(),
-                                  c->scan_tmp.as<uint64_t>() + scan_tiles(n) + 1, c->stream, &nl);
+  // exclusive prefix = start of each node's list; the scatter advances it to the list's end
+  cudaError_t e = launch_scan_u32_to32(c->cursor.as<uint32_t>(), n, sg.off.as<uint32_t>(), c->scan_tmp.as<uint64_t>(),
+                                       c->scan_tmp.as<uint64_t>() + scan_tiles(n) + 1, c->stream, &nl);
   TRY(launched(c, e, "scan(segment counts)", nl));
-  CK(cudaMemsetAsync(c->cursor.p, 0, n * 4, c->stream));
   if (set1 > set0)
     TRY(launched(c, launch_inv_scatter(c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), (uint32_t)set0,
-                                       (uint32_t)set1, sg.off.as<uint64_t>(), c->cursor.as<uint32_t>(),
-                                       sg.inv.as<uint32_t>(), c->num_sms * 8, c->stream), "k_inv_scatter"));
+                                       (uint32_t)set1, sg.off.as<uint32_t>(), sg.inv.as<uint32_t>(),
+                                       c->num_sms * 8, c->stream), "k_inv_scatter"));
   c->iseg.push_back(std::move(sg));
   return GIM_OK;
 }
@@ -548,7 +549,8 @@ gim_status generate(gim_ctx* c, uint64_t theta, uint64_t seed) {
     // one inverted-index segment per generate call (= per IMM round): its O(n) count scan is
     // paid once per round, not once per 2^22-id chunk
     if (c->nsets > set0) {
-      if (c->inv_segmented && c->inv_valid && c->iseg.size() < (size_t)kMaxInvSeg)
+      if (c->inv_segmented && c->inv_valid && c->iseg.size() < (size_t)kMaxInvSeg &&
+          c->pool_len - e0 < 0xFFFFFFFFull)
         TRY(build_inv_segment(c, set0, c->nsets, e0, c->pool_len));
       else
         c->inv_valid = false;                  // rebuilt as one segment at the next selection
@@ -582,7 +584,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   {
     InvSegDev tab[kMaxInvSeg];
     for (size_t q = 0; q < c->iseg.size(); ++q)
-      tab[q] = InvSegDev{c->iseg[q].off.as<uint64_t>(), c->iseg[q].inv.as<uint32_t>()};
+      tab[q] = InvSegDev{c->iseg[q].off.as<uint32_t>(), c->iseg[q].inv.as<uint32_t>()};
     TRY(launched(c, launch_set_segs(tab, (uint32_t)c->iseg.size(),
                                     (uint32_t)std::min<uint64_t>(c->set_limit, 0xFFFFFFFFull),
                                     c->seg_desc.as<InvSegDev>(),

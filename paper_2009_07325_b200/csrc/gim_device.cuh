@@ -107,10 +107,10 @@ struct GiantRec {
   unsigned long long dump_off;
 };
 
-// One segment of the inverted node -> RR index (built per generation chunk): the local set ids
-// containing v are inv[off[v] .. off[v+1]).
+// One segment of the inverted node -> RR index (built per generate call): the local set ids
+// containing v are inv[end[v-1] .. end[v]) (end[-1] = 0). 32-bit: a segment holds < 2^32 elements.
 struct InvSegDev {
-  const uint64_t* off;
+  const uint32_t* end;
   const uint32_t* inv;
 };
 constexpr int kMaxInvSeg = 16;

@@ -23,9 +23,11 @@ cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* si
 uint64_t scan_tiles(uint64_t count);
 cudaError_t launch_scan_u32(const uint32_t* in, uint64_t count, uint64_t* out, uint64_t* tile_tmp,
                             uint64_t* total_tmp, cudaStream_t s, int* launches);
+// same, 32-bit output (the caller guarantees the total is < 2^32)
+cudaError_t launch_scan_u32_to32(const uint32_t* in, uint64_t count, uint32_t* out, uint64_t* tile_tmp,
+                                 uint64_t* total_tmp, cudaStream_t s, int* launches);
 cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, uint32_t set0, uint32_t set1,
-                               const uint64_t* inv_off, uint32_t* cursor, uint32_t* inv, int grid,
-                               cudaStream_t s);
+                               uint32_t* end, uint32_t* inv, int grid, cudaStream_t s);
 struct InvSegDev;
 cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, uint32_t limit, InvSegDev* out,
                             uint32_t* nseg_out, cudaStream_t s);

@@ -80,10 +80,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(uint64_t* __restric
 }
 
 // Phase 3: out[i] = exclusive prefix (uint64); out[count] = total.
+template <class OutT>
 __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __restrict__ in, uint64_t count,
                                                              const uint64_t* __restrict__ tile_sums,
                                                              const uint64_t* __restrict__ grand_total,
-                                                             uint64_t* __restrict__ out) {
+                                                             OutT* __restrict__ out) {
   __shared__ uint64_t s_total;
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanPerThread;
   uint32_t v[kScanPerThread];
@@ -96,10 +97,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const uint32_t* __r
   uint64_t ex = block_excl_scan(s, &s_total) + tile_sums[blockIdx.x];
 #pragma unroll
   for (int j = 0; j < kScanPerThread; ++j) {
-    if (base + j < count) out[base + j] = ex;
+    if (base + j < count) out[base + j] = (OutT)ex;
     ex += v[j];
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) out[count] = *grand_total;
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[count] = (OutT)*grand_total;
 }
 
 // Warp-level helpers: exclusive scan of one value per lane, and the lane (0..31) whose
@@ -123,8 +124,7 @@ __device__ __forceinline__ uint32_t warp_excl_scan_u32(uint32_t x, int lane, uin
 __global__ void __launch_bounds__(256) k_inv_scatter(const uint64_t* __restrict__ offsets,
                                                      const uint32_t* __restrict__ pool, uint32_t set0,
                                                      uint32_t nsets_end,
-                                                     const uint64_t* __restrict__ inv_off,
-                                                     uint32_t* __restrict__ cursor,
+                                                     uint32_t* __restrict__ end,
                                                      uint32_t* __restrict__ inv) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
@@ -141,8 +141,7 @@ __global__ void __launch_bounds__(256) k_inv_scatter(const uint64_t* __restrict_
       const uint32_t k = warp_owner(P, i);
       if (i < hi_rel) {
         const uint32_t v = pool[base + i];
-        const uint32_t pos = atomicAdd(cursor + v, 1u);
-        inv[inv_off[v] + pos] = r0 + k;
+        inv[atomicAdd(end + v, 1u)] = r0 + k;     // end[v]: start of v's list, advanced to its end
       }
     }
   }
@@ -398,9 +397,9 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
     // set-id limit (only after a tail truncation), loaded alongside the descriptors
     const uint32_t lim = (LIMIT && l == 0) ? reinterpret_cast<const uint32_t*>(segs + kMaxInvSeg)[1] : 0u;
     uint64_t lo = 0, len = 0;
-    if (sg.off) {
-      lo = sg.off[u];
-      len = sg.off[u + 1] - lo;
+    if (sg.end) {
+      lo = u ? sg.end[u - 1] : 0u;
+      len = sg.end[u] - lo;
     }
     uint64_t incl = len;
 #pragma unroll
@@ -413,7 +412,7 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
       s_end[l] = incl;
       s_inv[l] = sg.inv;
     }
-    const uint32_t used = __ballot_sync(kFull, sg.off != nullptr);   // warp-wide vote
+    const uint32_t used = __ballot_sync(kFull, sg.end != nullptr);   // warp-wide vote
     if (l == 0) {
       s_nseg = __popc(used);
       s_limit = lim;
@@ -452,8 +451,9 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
 // ------------------------------------------------------------------------------------------
 uint64_t scan_tiles(uint64_t count) { return (count + kScanTile - 1) / kScanTile; }
 
-cudaError_t launch_scan_u32(const uint32_t* in, uint64_t count, uint64_t* out, uint64_t* tile_tmp,
-                            uint64_t* total_tmp, cudaStream_t s, int* launches) {
+template <class OutT>
+cudaError_t launch_scan_impl(const uint32_t* in, uint64_t count, OutT* out, uint64_t* tile_tmp,
+                             uint64_t* total_tmp, cudaStream_t s, int* launches) {
   const uint64_t nt = scan_tiles(count);
   if (nt > 0) {
     k_scan_sums<<<(unsigned)nt, kScanThreads, 0, s>>>(in, count, tile_tmp);
@@ -461,15 +461,22 @@ cudaError_t launch_scan_u32(const uint32_t* in, uint64_t count, uint64_t* out, u
   }
   k_scan_tiles<<<1, kScanThreads, 0, s>>>(tile_tmp, nt, total_tmp);
   ++*launches;
-  k_scan_apply<<<(unsigned)(nt > 0 ? nt : 1), kScanThreads, 0, s>>>(in, count, tile_tmp, total_tmp, out);
+  k_scan_apply<OutT><<<(unsigned)(nt > 0 ? nt : 1), kScanThreads, 0, s>>>(in, count, tile_tmp, total_tmp, out);
   ++*launches;
   return cudaGetLastError();
 }
+cudaError_t launch_scan_u32(const uint32_t* in, uint64_t count, uint64_t* out, uint64_t* tile_tmp,
+                            uint64_t* total_tmp, cudaStream_t s, int* launches) {
+  return launch_scan_impl<uint64_t>(in, count, out, tile_tmp, total_tmp, s, launches);
+}
+cudaError_t launch_scan_u32_to32(const uint32_t* in, uint64_t count, uint32_t* out, uint64_t* tile_tmp,
+                                 uint64_t* total_tmp, cudaStream_t s, int* launches) {
+  return launch_scan_impl<uint32_t>(in, count, out, tile_tmp, total_tmp, s, launches);
+}
 
 cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, uint32_t set0, uint32_t set1,
-                               const uint64_t* inv_off, uint32_t* cursor, uint32_t* inv, int grid,
-                               cudaStream_t s) {
-  k_inv_scatter<<<grid, 256, 0, s>>>(offsets, pool, set0, set1, inv_off, cursor, inv);
+                               uint32_t* end, uint32_t* inv, int grid, cudaStream_t s) {
+  k_inv_scatter<<<grid, 256, 0, s>>>(offsets, pool, set0, set1, end, inv);
   return cudaGetLastError();
 }
 

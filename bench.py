@@ -16,6 +16,7 @@ over NCCL.
 sample of the same workload on the host cores.
 """
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -42,6 +43,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gim", choices=["gim", "reference"])
     ap.add_argument("--workload", default="C3", choices=sorted(gi.WORKLOADS))
+    ap.add_argument("--k", type=int, default=0, help="override the workload's k (parameter sweeps)")
+    ap.add_argument("--eps", type=float, default=0.0, help="override the workload's eps (parameter sweeps)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -64,9 +67,10 @@ def config_of(w, world):
             "ell": w.ell, "model": "IC" if w.model == gi.IC else "LT",
             "weights": {gi.W_WC: "weighted cascade 1/d_in", gi.W_UNIFORM: f"uniform p={w.p_uniform}",
                         gi.W_EXPLICIT: "explicit"}[w.scheme],
-            "generator": f"plg gamma={w.gamma} rho={w.rho} d_cap={w.d_cap} graph_seed={w.graph_seed}",
+            "generator": (f"barabasi-albert r={w.ba_r} r0={w.ba_r + 1} graph_seed={w.graph_seed}" if w.gen == "ba"
+                          else f"plg gamma={w.gamma} rho={w.rho} d_cap={w.d_cap} graph_seed={w.graph_seed}"),
             "rr_seed": w.rr_seed, "parallelism": f"dp{world} (RR-id slices, replicated graph)",
-            "l2": "inputs larger than L2 (C3/C4/C5 graphs exceed the 126 MB L2)" if w.m > 30_000_000
+            "l2": "inputs larger than L2 (the graph's CSR exceeds the 126 MB L2)" if w.m > 30_000_000
             else "graph is L2-resident (no flush between steps)"}
 
 
@@ -366,6 +370,9 @@ def run_gim(args, w):
 def main():
     args = parse()
     w = gi.WORKLOADS[args.workload]
+    if args.k or args.eps:      # sweep point: same graph, other (k, eps); named in config
+        w = dataclasses.replace(w, k=args.k or w.k, eps=args.eps or w.eps,
+                                desc=f"{w.desc} [sweep: k={args.k or w.k}, eps={args.eps or w.eps}]")
     if args.impl == "reference":
         run_reference(args, w)
     else:

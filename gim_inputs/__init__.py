@@ -138,6 +138,9 @@ def build_lib(force: bool = False) -> str:
 @functools.lru_cache(maxsize=1)
 def _lib():
     lib = ctypes.CDLL(build_lib())
+    lib.ba_generate.restype = ctypes.c_int
+    lib.ba_generate.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
+                                ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
     lib.plg_generate.restype = ctypes.c_int
     lib.plg_generate.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
@@ -159,6 +162,26 @@ def plg(n: int, m: int, gamma: float, rho: float, d_cap: float, graph_seed: int,
     return Graph(n=n, row_ptr=row_ptr, src=src, name=name,
                  meta=dict(generator="plg", n=n, m=m, gamma=gamma, rho=rho, d_cap=d_cap,
                            graph_seed=graph_seed, i0=i0.value))
+
+
+def ba_edges(n: int, r: int, r0: int) -> int:
+    """Directed edge count of the BA graph: both directions of r0(r0-1)/2 + r(n - r0) edges."""
+    return 2 * (r0 * (r0 - 1) // 2 + r * (n - r0))
+
+
+def ba(n: int, r: int, graph_seed: int, r0: int = 0, name: str = "") -> Graph:
+    """Barabasi-Albert scale-free graph of the paper's density experiment: clique of
+    r0 (default r + 1) nodes, each later node attaches to r distinct degree-proportional
+    targets; undirected, stored as both directed edges (canonical in-CSR)."""
+    r0 = r0 or r + 1
+    m = ba_edges(n, r, r0)
+    row_ptr = np.empty(n + 1, dtype=np.uint64)
+    src = np.empty(m, dtype=np.uint32)
+    rc = _lib().ba_generate(n, r, r0, graph_seed, m, row_ptr.ctypes.data, src.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(f"ba_generate failed rc={rc}")
+    return Graph(n=n, row_ptr=row_ptr, src=src, name=name,
+                 meta=dict(generator="ba", n=n, m=m, r=r, r0=r0, graph_seed=graph_seed))
 
 
 def stats(g: Graph) -> dict:
@@ -191,6 +214,8 @@ class Workload:
     eps: float
     ell: float = 1.0
     rr_seed: int = 200907325
+    gen: str = "plg"       # "plg" (Chung-Lu, configs C1-C5) or "ba" (Barabasi-Albert, r = ba_r)
+    ba_r: int = 0
 
 
 WORKLOADS = {
@@ -207,9 +232,20 @@ WORKLOADS = {
 }
 
 
+# The paper's density sweep (§4.6): BA graphs, n = 10^6, r = 2..32, IC-WC, k = 50,
+# eps = 0.05. Not a BASELINE.json config: bench lines only.
+for _r in (2, 4, 8, 16, 32):
+    WORKLOADS[f"B{_r}"] = Workload(
+        f"B{_r}", f"Barabasi-Albert n=10^6, r={_r} (undirected, both directions), IC-WC, k=50, eps=0.05",
+        1000000, ba_edges(1000000, _r, _r + 1), 0.0, 1.0, 0.0, 100 + _r, IC, W_WC, 0.0, 50, 0.05,
+        gen="ba", ba_r=_r)
+
+
 @functools.lru_cache(maxsize=4)
 def workload_graph(key: str) -> Graph:
     w = WORKLOADS[key]
+    if w.gen == "ba":
+        return ba(w.n, w.ba_r, w.graph_seed, name=f"{key}-graph")
     return plg(w.n, w.m, w.gamma, w.rho, w.d_cap, w.graph_seed, name=f"{key}-graph")
 
 

@@ -216,4 +216,56 @@ int plg_generate(uint32_t n, uint64_t m, double gamma, double rho, double d_cap,
   return -4;
 }
 
+
+// Barabasi-Albert scale-free graph (the paper's density experiment): a clique of r0
+// nodes, then nodes v = r0..n-1 arrive one by one and attach to r distinct existing nodes, each
+// drawn with probability d_i / sum_j d_j (uniform pick from the endpoint list, redrawn on a
+// repeat). Undirected: every edge {a, b} becomes a->b and b->a. Output: canonical in-CSR
+// (sources ascending). m = 2 * (r0 (r0 - 1) / 2 + r (n - r0)). Draw t uses rnd(base, t, 0).
+// Returns 0, or -1 on invalid arguments (need 1 <= r <= r0, 2 <= r0 <= n), -2 if m != m_expect.
+int ba_generate(uint32_t n, uint32_t r, uint32_t r0, uint64_t graph_seed, uint64_t m_expect,
+                uint64_t* row_ptr, uint32_t* src) {
+  if (r < 1 || r0 < r || r0 < 2 || n < r0) return -1;
+  const uint64_t m_und = (uint64_t)r0 * (r0 - 1) / 2 + (uint64_t)r * (n - r0);
+  if (2 * m_und != m_expect) return -2;
+  std::vector<uint32_t> ea(m_und), eb(m_und);
+  std::vector<uint32_t> ends;
+  ends.reserve(2 * m_und);
+  uint64_t k = 0;
+  for (uint32_t i = 0; i < r0; ++i)
+    for (uint32_t j = 0; j < i; ++j) {
+      ea[k] = j; eb[k] = i; ++k;
+      ends.push_back(i); ends.push_back(j);
+    }
+  const uint64_t base = fmix64(graph_seed ^ 0x452821E638D01377ULL);
+  std::vector<uint32_t> tg(r);
+  uint64_t t = 0;
+  for (uint32_t v = r0; v < n; ++v) {
+    uint32_t got = 0;
+    while (got < r) {
+      const uint32_t u = ends[(size_t)mulhi64(rnd(base, t++, 0), ends.size())];
+      bool dup = false;
+      for (uint32_t q = 0; q < got; ++q) dup |= (tg[q] == u);
+      if (!dup) tg[got++] = u;
+    }
+    for (uint32_t q = 0; q < r; ++q) {
+      ea[k] = tg[q]; eb[k] = v; ++k;
+      ends.push_back(tg[q]); ends.push_back(v);
+    }
+  }
+  // in-CSR of both directions: counting sort by destination, then sort each row
+  std::vector<uint64_t> deg(n + 1, 0);
+  for (uint64_t e = 0; e < m_und; ++e) { ++deg[ea[e]]; ++deg[eb[e]]; }
+  row_ptr[0] = 0;
+  for (uint32_t v = 0; v < n; ++v) row_ptr[v + 1] = row_ptr[v] + deg[v];
+  std::vector<uint64_t> cur(row_ptr, row_ptr + n);
+  for (uint64_t e = 0; e < m_und; ++e) {
+    src[cur[eb[e]]++] = ea[e];          // ea -> eb
+    src[cur[ea[e]]++] = eb[e];          // eb -> ea
+  }
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t v = 0; v < (int64_t)n; ++v) std::sort(src + row_ptr[v], src + row_ptr[v + 1]);
+  return 0;
+}
+
 }  // extern "C"

@@ -223,7 +223,20 @@ def test_imm_parity_C1_LT():
     assert np.array_equal(r.seeds, ro.seeds) and r.R_final == ro.R_final and r.covered == ro.cov
 
 
-@pytest.mark.parametrize("key", ["C3", "C4", pytest.param("C5", marks=pytest.mark.skipif(
+def test_imm_parity_BA_small():
+    """The paper's density workload family (Barabasi-Albert) at a size the oracle runs
+    in a second: full IMM trace and seeds bit-exact (WC on an undirected graph is critical, so
+    sets reach the giant path)."""
+    g = gi.ba(20000, 8, 11)
+    c = _ctx(g, gi.IC, gi.W_WC)
+    r = c.imm(20, 0.3, 1.0, 5)
+    ro = oracle.Oracle(g, gi.IC, gi.W_WC).imm(20, 0.3, 1.0, 5)
+    assert r.rounds == ro.rounds and np.array_equal(r.theta_i, ro.T_i) and np.array_equal(r.cov_i, ro.cov_i)
+    assert r.R_final == ro.R_final and r.covered == ro.cov
+    assert np.array_equal(r.seeds, ro.seeds), (r.seeds, ro.seeds)
+
+
+@pytest.mark.parametrize("key", ["C3", "C4", "B8", pytest.param("C5", marks=pytest.mark.skipif(
     os.environ.get("GIM_TEST_C5") != "1", reason="C5 graph generation takes minutes: set GIM_TEST_C5=1"))])
 def test_full_size_sampled(key):
     """BASELINE.json full size: 2^21 RR sets in the launch configuration bench.py times; sampled

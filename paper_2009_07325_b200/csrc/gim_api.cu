@@ -393,7 +393,7 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     TRY(ensure(c, c->lt_spill, (uint64_t)rr_grid * kLtWarps * (kLtCap2 - kLtCap) * 32 * 4));
     p.lt_spill = c->lt_spill.as<uint32_t>();
   }
-  TRY(ensure_giant_slots(c, 2u * (uint32_t)c->num_sms));
+  TRY(ensure_giant_slots(c, (uint32_t)kGiantBlocksPerSM * (uint32_t)c->num_sms));
   const uint64_t bm_words = ((uint64_t)c->n + 31) / 32;
   // warp kernel, then the giant kernel unconditionally (it reads the giant count on the device
   // and exits at once when there is none), then the size scan: one host sync per chunk.

@@ -170,12 +170,16 @@ constexpr int kRRSmemPerWarp = (kQMax + kHSize + kPend) * 4;   // 6.5 KB -> 4 CT
 constexpr int kRRBlocksPerSM = GIM_RR_BLOCKS;
 constexpr int kRRIlp = GIM_RR_ILP;    // Philox chains per lane per iteration (1 or 2)
 #ifndef GIM_HUB_ILP
-#define GIM_HUB_ILP 4
+#define GIM_HUB_ILP 2
 #endif
 constexpr int kHubIlp = GIM_HUB_ILP;  // Philox chains per lane per step on a hub node
 constexpr uint32_t kHubGroups = 32u * GIM_HUB_ILP;   // nodes with >= this many slot groups are hubs
 static_assert((kHubGroups & (kHubGroups - 1u)) == 0u, "hub steps are split off with a mask");
-constexpr int kGiantThreads = 512;
+#ifndef GIM_GIANT_THREADS
+#define GIM_GIANT_THREADS 256
+#endif
+constexpr int kGiantThreads = GIM_GIANT_THREADS;              // warps of one giant set = this / 32
+constexpr int kGiantBlocksPerSM = 1024 / GIM_GIANT_THREADS;   // giant sets in flight per SM
 #ifndef GIM_CLAIM_BATCH
 #define GIM_CLAIM_BATCH 1
 #endif

@@ -135,6 +135,54 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t cnt, int lane, uint3
   return incl - cnt;
 }
 
+// Flattened sweep of a batch's short slot-group ranges. Lane i of the batch
+// brings node i's remaining groups [gs, gs + ngf) with its row range [a, b) and live threshold.
+// The non-empty ranges are compacted into lanes 0..nne-1 once per batch; the owner of flattened
+// group gi of a 32-group window is then one ballot + one redux away (the starts of non-empty
+// ranges are distinct), instead of a 5-step dependent shuffle search per window.
+struct Flat {
+  uint32_t a, b, thr, gofs, start;   // compacted lane r: the r-th non-empty range; gofs = gs - start
+  uint32_t nne, total;               // non-empty ranges, total flattened groups
+};
+
+__device__ __forceinline__ Flat flat_setup(uint32_t a, uint32_t b, uint32_t thr, uint32_t gs, uint32_t ngf,
+                                           int lane) {
+  Flat f;
+  const uint32_t ne = __ballot_sync(kFull, ngf != 0u);
+  f.nne = __popc(ne);
+  const uint32_t E = warp_excl_scan(ngf, lane, f.total);
+  // src = position of the (lane+1)-th set bit of ne (lanes >= nne get junk); usually every
+  // node of the batch has a range (ne is a prefix mask) and src = lane
+  uint32_t src = (uint32_t)lane;
+  if (ne & (ne + 1u)) {                        // warp-uniform: some range is empty
+    uint32_t r = (uint32_t)lane;
+    src = 0;
+#pragma unroll
+    for (uint32_t w = 16; w >= 1; w >>= 1) {
+      const uint32_t c = __popc((ne >> src) & ((1u << w) - 1u));
+      if (c <= r) { r -= c; src += w; }
+    }
+    src &= 31u;
+  }
+  f.a = __shfl_sync(kFull, a, src);
+  f.b = __shfl_sync(kFull, b, src);
+  f.thr = __shfl_sync(kFull, thr, src);
+  f.start = __shfl_sync(kFull, E, src);
+  f.gofs = __shfl_sync(kFull, gs - E, src);
+  return f;
+}
+
+// Compacted lane owning flattened group base + lane (any lane in [0, nne) if past the total).
+__device__ __forceinline__ uint32_t flat_owner(const Flat& f, uint32_t base, int lane) {
+  if (f.nne <= 1u) return 0u;                  // warp-uniform: a single range
+  const bool ok = (uint32_t)lane < f.nne;
+  const uint32_t before = __popc(__ballot_sync(kFull, ok && f.start < base));
+  const uint32_t d = f.start - base;
+  const uint32_t starts = __reduce_or_sync(kFull, (ok && f.start >= base && d < 32u) ? (1u << d) : 0u);
+  const uint32_t cnt = before + __popc(starts & (0xFFFFFFFFu >> (31 - lane)));
+  return cnt ? cnt - 1u : 0u;
+}
+
 
 // Slow path of the warp kernel: load src[e] for this lane's live slots of group g, test-and-set
 // them in the smem visited hash and append the new nodes to the queue (warp-collective).
@@ -371,22 +419,13 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
         const uint32_t hubs = __ballot_sync(kFull, hub_full != 0u);
         const uint32_t ngf = ng - hub_full;
         const uint32_t gs = (a >> 2) + hub_full;        // first flattened group of this node
-        uint32_t total_g;
-        const uint32_t E = warp_excl_scan(ngf, lane, total_g);   // exclusive group prefix
-        const uint32_t P = E + ngf;
-        const uint32_t top = nb > 1 ? 1u << (31 - __clz(nb - 1)) : 0u;   // search depth ~ log2(nb)
+        const Flat f = flat_setup(a, b, thr, gs, ngf, lane);
+        const uint32_t total_g = f.total;
         for (uint32_t base = 0; base < total_g; base += 32) {
           const uint32_t gi = base + lane;
-          uint32_t k = 0;                               // node of flattened group gi
-#pragma unroll
-          for (uint32_t step = 16; step >= 1; step >>= 1) {
-            if (step <= top) {
-              const uint32_t pv = __shfl_sync(kFull, P, k + step - 1);
-              if (pv <= gi) k += step;
-            }
-          }
-          const uint32_t ak = __shfl_sync(kFull, a, k), bk = __shfl_sync(kFull, b, k);
-          const uint32_t tk = __shfl_sync(kFull, thr, k), gk = __shfl_sync(kFull, gs - E, k);
+          const uint32_t k = flat_owner(f, base, lane);   // compacted range of flattened group gi
+          const uint32_t ak = __shfl_sync(kFull, f.a, k), bk = __shfl_sync(kFull, f.b, k);
+          const uint32_t tk = __shfl_sync(kFull, f.thr, k), gk = __shfl_sync(kFull, f.gofs, k);
           const uint32_t g = gk + gi;
           uint32_t m = 0;
           if (gi < total_g && !never) m = ic_live_mask<SCHEME>(p, id_lo, id_hi, k0, k1, g, ak, bk, tk);
@@ -809,7 +848,7 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* ptr) {
 }
 
 template <int MODEL, int SCHEME>
-__global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint32_t* bitmaps,
+__global__ void __launch_bounds__(kGiantThreads, kGiantBlocksPerSM) k_rr_giant(RRParams p, uint32_t* bitmaps,
                                                                uint32_t* gqueues, uint64_t bm_words) {
   __shared__ uint32_t s_head, s_tail, s_busy, s_r;
   __shared__ uint32_t s_chead, s_cres;           // hub-chunk ring: claimed / reserved counters
@@ -998,6 +1037,8 @@ __global__ void __launch_bounds__(kGiantThreads, 2) k_rr_giant(RRParams p, uint3
           uint32_t total_g;
           const uint32_t E = warp_excl_scan(ngf, lane, total_g);
           const uint32_t P = E + ngf;
+          // node of flattened group gi: shuffle search (measured faster than flat_setup/flat_owner
+          // here: giant batches are often a few nodes, where the search is 0-2 steps deep)
           const uint32_t top = c > 1 ? 1u << (31 - __clz(c - 1)) : 0u;
           for (uint32_t base = 0; base < total_g; base += 32) {
             const uint32_t gi = base + lane;

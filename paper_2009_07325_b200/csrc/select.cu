@@ -376,6 +376,11 @@ __global__ void __launch_bounds__(256) k_argmax_cand(const uint32_t* __restrict_
 // short and mostly covered, so spreading entries over many groups (latency hiding) beats
 // flattening members within a warp (measured 19 vs 94 us per step on C3).
 // ------------------------------------------------------------------------------------------
+#ifndef GIM_COVER_ILP
+#define GIM_COVER_ILP 16
+#endif
+constexpr int kCoverIlp = GIM_COVER_ILP;
+
 template <bool LIMIT>
 __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restrict__ keys, int j,
                                                const InvSegDev* __restrict__ segs,
@@ -432,15 +437,17 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
     const uint64_t a = offsets[r], b = offsets[r + 1];
     if (cov || (LIMIT && r0 != r)) continue;
     if (sub == 0) covered[r] = 1;      // each r appears once across the lists of u: no race
-    if (dec == nullptr) {
-      for (uint64_t e = a + sub; e < b; e += 8) {
-        const uint32_t w = pool[e];
-        if (w != u) atomicSub(cnt + w, 1u);
-      }
-    } else {
-      for (uint64_t e = a + sub; e < b; e += 8) {
-        const uint32_t w = pool[e];
-        if (w != u) atomicAdd(dec + w, 1);
+    // members: kCoverIlp loads in flight per lane (big sets would otherwise serialise one L2
+    // round trip per 8 members), then fire-and-forget decrements; u itself is skipped
+    for (uint64_t e = a + sub; e < b; e += 8 * kCoverIlp) {
+      uint32_t w[kCoverIlp];
+#pragma unroll
+      for (int t = 0; t < kCoverIlp; ++t) w[t] = (e + 8 * t < b) ? pool[e + 8 * t] : u;
+#pragma unroll
+      for (int t = 0; t < kCoverIlp; ++t) {
+        if (w[t] == u) continue;
+        if (dec == nullptr) atomicSub(cnt + w[t], 1u);
+        else atomicAdd(dec + w[t], 1);
       }
     }
   }

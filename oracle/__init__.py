@@ -51,6 +51,14 @@ def _lib():
         "og_imm_constants": (_int, [_u32, _u32, _dbl, _dbl, _p]),
         "og_imm": (_int, [_p, _u32, _dbl, _dbl, _u64, _p, _p, _p, _p, _p, _p, _p]),
         "og_mc_spread": (_int, [_p, _p, _u32, _u64, _u64, _p, _p]),
+        "og_mrim_generate": (_int, [_p, _u64, _u32, _u64]),
+        "og_mrim_num_sets": (_u64, [_p]),
+        "og_mrim_pool_len": (_u64, [_p]),
+        "og_mrim_export": (None, [_p, _p, _p, _p]),
+        "og_mrim_select_pool": (_int, [_u32, _u32, _u64, _p, _p, _p, _u32, _p, _p, _p]),
+        "og_mrim_select": (_int, [_p, _u32, _p, _p, _p]),
+        "og_mrim_constants": (_int, [_u32, _u32, _u32, _dbl, _dbl, _p]),
+        "og_mrim": (_int, [_p, _u32, _u32, _dbl, _dbl, _u64, _p, _p, _p, _p, _p, _p, _p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -90,6 +98,35 @@ def imm_constants(n: int, k: int, eps: float, ell: float = 1.0) -> dict:
         raise ValueError("invalid IMM parameters")
     return dict(zip(["ell_eff", "eps_prime", "lnC", "lambda_prime", "alpha", "beta",
                      "lambda_star"], out.tolist()))
+
+
+def mrim_constants(n: int, k: int, T: int, eps: float, ell: float = 1.0) -> dict:
+    """R28: IMM's constants with ln C(n*T, k*T) for ln C(n, k)."""
+    out = np.zeros(7, dtype=np.float64)
+    rc = _lib().og_mrim_constants(n, k, T, eps, ell, _ptr(out))
+    if rc:
+        raise ValueError("invalid MRIM parameters")
+    return dict(zip(["ell_eff", "eps_prime", "lnC", "lambda_prime", "alpha", "beta",
+                     "lambda_star"], out.tolist()))
+
+
+def mrim_select_pool(n: int, T: int, offsets: np.ndarray, pairs: np.ndarray, k: int,
+                     count: Optional[np.ndarray] = None):
+    """R27 on an explicit system of ascending pair sets (pair id = t*n + u). Returns
+    (picks, gains, cov) with k*T picks (pair ids) in pick order."""
+    offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+    pairs = np.ascontiguousarray(pairs, dtype=np.uint32)
+    if count is None:
+        count = np.bincount(pairs.astype(np.int64), minlength=n * T).astype(np.uint32)
+    count = np.ascontiguousarray(count, dtype=np.uint32)
+    seeds = np.zeros(k * T, dtype=np.uint32)
+    gains = np.zeros(k * T, dtype=np.uint64)
+    cov = np.zeros(1, dtype=np.uint64)
+    rc = _lib().og_mrim_select_pool(n, T, len(offsets) - 1, _ptr(offsets), _ptr(pairs) if len(pairs) else None,
+                                    _ptr(count), k, _ptr(seeds), _ptr(gains), _ptr(cov))
+    if rc:
+        raise ValueError(f"og_mrim_select_pool rc={rc}")
+    return seeds, gains, int(cov[0])
 
 
 def select_pool(n: int, offsets: np.ndarray, nodes: np.ndarray, k: int,
@@ -213,3 +250,52 @@ class Oracle:
         _lib().og_mc_spread(self._h, _ptr(s), len(s), trials, mc_seed, ctypes.byref(mean),
                             ctypes.byref(se))
         return mean.value, se.value
+
+    # ---- MRIM (R26-R28; oracle/gim_oracle.c "MRIM") ----------------------------------------
+    def mrim_generate(self, N: int, T: int, seed: int) -> None:
+        if _lib().og_mrim_generate(self._h, N, T, seed):
+            raise ValueError("og_mrim_generate: invalid T")
+        self._T_mr = T
+
+    def mrim_export(self):
+        ns = int(_lib().og_mrim_num_sets(self._h))
+        pl = int(_lib().og_mrim_pool_len(self._h))
+        T = self._mrim_T
+        off = np.zeros(ns + 1, dtype=np.uint64)
+        pairs = np.zeros(max(pl, 1), dtype=np.uint32)
+        cnt = np.zeros(self.n * T, dtype=np.uint32)
+        _lib().og_mrim_export(self._h, _ptr(off), _ptr(pairs), _ptr(cnt))
+        return off, pairs[:pl], cnt
+
+    def mrim_select(self, k: int):
+        T = self._mrim_T
+        seeds = np.zeros(k * T, dtype=np.uint32)
+        gains = np.zeros(k * T, dtype=np.uint64)
+        cov = np.zeros(1, dtype=np.uint64)
+        rc = _lib().og_mrim_select(self._h, k, _ptr(seeds), _ptr(gains), _ptr(cov))
+        if rc:
+            raise ValueError(f"og_mrim_select rc={rc}")
+        return seeds, gains, int(cov[0])
+
+    def mrim(self, k: int, T: int, eps: float, ell: float, seed: int) -> ImmResult:
+        seeds = np.zeros(k * T, dtype=np.uint32)
+        gains = np.zeros(k * T, dtype=np.uint64)
+        dres = np.zeros(7, dtype=np.float64)
+        th = np.zeros(64, dtype=np.float64)
+        TT = np.zeros(64, dtype=np.uint64)
+        cv = np.zeros(64, dtype=np.uint64)
+        u = np.zeros(3, dtype=np.uint64)
+        self._T_mr = T
+        rc = _lib().og_mrim(self._h, k, T, eps, ell, seed, _ptr(seeds), _ptr(gains), _ptr(dres),
+                            _ptr(th), _ptr(TT), _ptr(cv), _ptr(u))
+        if rc:
+            raise ValueError("og_mrim: invalid parameters")
+        r = int(u[0])
+        return ImmResult(seeds=seeds, gains=gains, LB=dres[0], theta=dres[1], spread_est=dres[2],
+                         ell_eff=dres[3], eps_prime=dres[4], lambda_prime=dres[5],
+                         lambda_star=dres[6], rounds=r, R_final=int(u[1]), cov=int(u[2]),
+                         theta_i=th[:r].copy(), T_i=TT[:r].copy(), cov_i=cv[:r].copy())
+
+    @property
+    def _mrim_T(self) -> int:
+        return int(self._T_mr) if hasattr(self, "_T_mr") else 1

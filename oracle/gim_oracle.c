@@ -111,6 +111,15 @@ typedef struct og_ctx {
   uint32_t* count;        /* n */
   /* workload statistics */
   uint64_t stat_coins, stat_live;
+  /* MRIM pool (R26): mr_nsets sets of (node, round) pair ids, count over n*T pairs */
+  uint32_t mr_T;
+  uint64_t mr_seed;
+  int mr_have;
+  uint64_t mr_nsets, mr_len, mr_cap_sets, mr_cap_pool;
+  uint64_t* mr_offsets;
+  uint32_t* mr_nodes;
+  uint32_t* mr_count;
+  uint32_t* mr_tmp;
 } og_ctx;
 
 static int cmp_u32(const void* a, const void* b) {
@@ -124,6 +133,7 @@ void og_destroy(og_ctx* c) {
   free(c->out_ptr); free(c->out_dst); free(c->out_in_slot);
   free(c->visited); free(c->queue);
   free(c->offsets); free(c->nodes); free(c->count);
+  free(c->mr_offsets); free(c->mr_nodes); free(c->mr_count); free(c->mr_tmp);
   free(c);
 }
 
@@ -179,9 +189,8 @@ static int ic_live(og_ctx* c, uint64_t seed, uint64_t id, uint64_t e, uint32_t v
  * P:166-168 realised as the randomized BFS of P:260 / Alg. 3 l.8-22, with the root
  * marked visited (R12) and exact set semantics (R13). Writes the set, ascending, to out[];
  * returns its size. */
-static uint32_t rr_ic(og_ctx* c, uint64_t seed, uint64_t id, uint32_t* out) {
+static uint32_t rr_ic(og_ctx* c, uint64_t seed, uint64_t id, uint32_t root, uint32_t* out) {
   uint32_t head = 0, tail = 0, i;
-  uint32_t root = og_root(seed, id, c->n);
   c->visited[root] = 1;
   c->queue[tail++] = root;
   while (head < tail) {
@@ -206,9 +215,9 @@ static uint32_t rr_ic(og_ctx* c, uint64_t seed, uint64_t id, uint32_t* out) {
 /* O5. LT RR set: reverse random walk choosing at most one in-edge per node according to the
  * edge weights, frontier <= 1, stopping at a node with no chosen edge or at an
  * already-visited node (R19). Half-open fixed-point intervals (R18). */
-static uint32_t rr_lt(og_ctx* c, uint64_t seed, uint64_t id, uint32_t* out) {
+static uint32_t rr_lt(og_ctx* c, uint64_t seed, uint64_t id, uint32_t root, uint32_t* out) {
   uint32_t len = 0, i;
-  uint32_t v = og_root(seed, id, c->n);
+  uint32_t v = root;
   c->visited[v] = 1;
   c->queue[len++] = v;
   for (;;) {
@@ -241,8 +250,13 @@ static uint32_t rr_lt(og_ctx* c, uint64_t seed, uint64_t id, uint32_t* out) {
   return len;
 }
 
+/* the RR set of id `id` grown from `root` (og_rr_set: root = og_root(seed, id), O3) */
+static uint32_t rr_from(og_ctx* c, uint64_t seed, uint64_t id, uint32_t root, uint32_t* out) {
+  return (c->model == OG_LT) ? rr_lt(c, seed, id, root, out) : rr_ic(c, seed, id, root, out);
+}
+
 uint32_t og_rr_set(og_ctx* c, uint64_t seed, uint64_t id, uint32_t* out) {
-  return (c->model == OG_LT) ? rr_lt(c, seed, id, out) : rr_ic(c, seed, id, out);
+  return rr_from(c, seed, id, og_root(seed, id, c->n), out);
 }
 
 /* O6. Extend (or truncate) the pool to exactly { RR(seed, i) : 0 <= i < T } in id order, with
@@ -350,15 +364,17 @@ int og_select(og_ctx* c, uint32_t k, uint32_t* seeds_out, uint64_t* gains_out, u
  * expression order fixed.
  * out = { ell_eff, eps_prime, lnC, lambda_prime, alpha, beta, lambda_star }
  * ------------------------------------------------------------------------------------------ */
-int og_imm_constants(uint32_t n, uint32_t k, double eps, double ell, double out[7]) {
+/* lnC = ln C(N, K) (the union bound over candidate seed sets); N = n, K = k for IMM; MRIM
+ * (R28) takes N = n*T pairs and K = k*T picks. */
+static int imm_constants_g(uint32_t n, uint64_t N, uint64_t K, double eps, double ell, double out[7]) {
   double ln_n, log2n, ell_eff, eps_p, lnC = 0.0, lambda_p, alpha, beta, lambda_s, e = M_E;
-  uint32_t t;
-  if (n < 2 || k < 1 || k > n || !(eps > 0.0 && eps < 1.0) || !(ell > 0.0)) return 1;
+  uint64_t t;
+  if (n < 2 || K < 1 || K > N || !(eps > 0.0 && eps < 1.0) || !(ell > 0.0)) return 1;
   ln_n = log((double)n);
   log2n = log2((double)n);
   ell_eff = ell * (1.0 + log(2.0) / ln_n);
   eps_p = sqrt(2.0) * eps;
-  for (t = 1; t <= k; ++t) lnC += log((double)(n - k + t)) - log((double)t);
+  for (t = 1; t <= K; ++t) lnC += log((double)(N - K + t)) - log((double)t);
   lambda_p = (2.0 + 2.0 / 3.0 * eps_p) * (lnC + ell_eff * ln_n + log(log2n)) * (double)n / (eps_p * eps_p);
   alpha = sqrt(ell_eff * ln_n + log(2.0));
   beta = sqrt((1.0 - 1.0 / e) * (lnC + ell_eff * ln_n + log(2.0)));
@@ -369,6 +385,11 @@ int og_imm_constants(uint32_t n, uint32_t k, double eps, double ell, double out[
   out[0] = ell_eff; out[1] = eps_p; out[2] = lnC; out[3] = lambda_p;
   out[4] = alpha; out[5] = beta; out[6] = lambda_s;
   return 0;
+}
+
+int og_imm_constants(uint32_t n, uint32_t k, double eps, double ell, double out[7]) {
+  if (k > n) return 1;
+  return imm_constants_g(n, n, k, eps, ell, out);
 }
 
 /* O8 driver: Alg. 2 rounds, then theta = lambda_star / LB and the final selection
@@ -495,5 +516,169 @@ int og_mc_spread(og_ctx* c, const uint32_t* S, uint32_t k, uint64_t trials, uint
     *stderr_out = sqrt((var > 0 ? var : 0) / (double)trials);
   }
   free(q); free(act); free(acc); free(touched);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * MRIM: multi-round influence maximization, the CR-NAIMM algorithm of Sun et al. (KDD'18) as
+ * gIM adapts it (§4.8): "after selecting a random node, we initiate a random BFS
+ * originating from the selected node as many times as the number of rounds. Also, each element
+ * in a random RR set is a tuple of node-id and round number. The rest of our algorithm remains
+ * almost intact." The goal: a seed set per round maximizing the number of nodes
+ * influenced at least once. Readings R26-R28:
+ * R26  MRR_i = {(u, t) : 0 <= t < T, u in RR^t_i}: root_i = og_root(seed, i) is shared by the T
+ *      rounds; round t's BFS (IC coins / LT draws, O4/O5) is keyed by the standard RR id
+ *      i*T + t, so the rounds are independent and T = 1 is exactly the standard RR set i.
+ *      The pair (u, t) is the id t*n + u; a set is stored ascending (rounds, then nodes).
+ * R27  selection: greedy max coverage over pairs (Alg. 1 l.6-10, Alg. 7 with pair counters)
+ *      where a round accepts at most k seeds: each of the k*T picks is the unselected pair of a
+ *      not-yet-full round with the largest count, ties -> lowest pair id.
+ * R28  theta: IMM's lambda', lambda* (R1, R2) with ln C(n*T, k*T) for ln C(n, k) (the pairs are
+ *      the ground set, k*T picks); n, ell_eff and the rounds x = n / 2^i unchanged (the
+ *      objective counts nodes, at most n).
+ * ------------------------------------------------------------------------------------------ */
+int og_mrim_generate(og_ctx* c, uint64_t N, uint32_t T, uint64_t seed) {
+  uint64_t i, j;
+  uint32_t t;
+  const uint64_t nT = (uint64_t)c->n * T;
+  if (T < 1 || nT >= 0xFFFFFFFFull) return 1;
+  if (!c->mr_have || c->mr_seed != seed || c->mr_T != T) {
+    free(c->mr_offsets); free(c->mr_nodes); free(c->mr_count);
+    c->mr_T = T; c->mr_seed = seed; c->mr_have = 1;
+    c->mr_nsets = 0; c->mr_len = 0;
+    c->mr_cap_sets = 1024;
+    c->mr_offsets = (uint64_t*)calloc(c->mr_cap_sets + 1, sizeof(uint64_t));
+    c->mr_cap_pool = 4096;
+    c->mr_nodes = (uint32_t*)malloc(sizeof(uint32_t) * c->mr_cap_pool);
+    c->mr_count = (uint32_t*)calloc(nT, sizeof(uint32_t));
+    if (!c->mr_tmp) c->mr_tmp = (uint32_t*)malloc(sizeof(uint32_t) * c->n);
+  }
+  while (c->mr_nsets > N) {                   /* truncate */
+    uint64_t a = c->mr_offsets[c->mr_nsets - 1], b = c->mr_offsets[c->mr_nsets];
+    for (j = a; j < b; ++j) c->mr_count[c->mr_nodes[j]]--;
+    c->mr_nsets--; c->mr_len = a;
+  }
+  for (i = c->mr_nsets; i < N; ++i) {
+    uint32_t root = og_root(seed, i, c->n);   /* "selecting a random node" */
+    if (c->mr_nsets + 1 > c->mr_cap_sets) {
+      c->mr_cap_sets *= 2;
+      c->mr_offsets = (uint64_t*)realloc(c->mr_offsets, sizeof(uint64_t) * (c->mr_cap_sets + 1));
+    }
+    if (c->mr_len + nT > c->mr_cap_pool) {
+      while (c->mr_len + nT > c->mr_cap_pool) c->mr_cap_pool *= 2;
+      c->mr_nodes = (uint32_t*)realloc(c->mr_nodes, sizeof(uint32_t) * c->mr_cap_pool);
+    }
+    for (t = 0; t < T; ++t) {                 /* "as many times as the number of rounds" */
+      uint32_t len = rr_from(c, seed, i * (uint64_t)T + t, root, c->mr_tmp), q;
+      for (q = 0; q < len; ++q) {
+        uint32_t pr = t * c->n + c->mr_tmp[q];   /* (node-id, round) tuple */
+        c->mr_nodes[c->mr_len++] = pr;
+        c->mr_count[pr]++;
+      }
+    }
+    c->mr_nsets++;
+    c->mr_offsets[c->mr_nsets] = c->mr_len;
+  }
+  return 0;
+}
+
+uint64_t og_mrim_num_sets(const og_ctx* c) { return c->mr_have ? c->mr_nsets : 0; }
+uint64_t og_mrim_pool_len(const og_ctx* c) { return c->mr_have ? c->mr_len : 0; }
+void og_mrim_export(const og_ctx* c, uint64_t* offsets_out, uint32_t* pairs_out, uint32_t* count_out) {
+  if (!c->mr_have) return;
+  if (offsets_out) memcpy(offsets_out, c->mr_offsets, sizeof(uint64_t) * (c->mr_nsets + 1));
+  if (pairs_out && c->mr_len) memcpy(pairs_out, c->mr_nodes, sizeof(uint32_t) * c->mr_len);
+  if (count_out) memcpy(count_out, c->mr_count, sizeof(uint32_t) * (uint64_t)c->n * c->mr_T);
+}
+
+/* R27 over a pool of ascending pair sets: n nodes, T rounds, k seeds per round; seeds_out and
+ * gains_out hold the k*T picks (pair ids) in pick order. */
+int og_mrim_select_pool(uint32_t n, uint32_t T, uint64_t nsets, const uint64_t* offsets,
+                        const uint32_t* pairs, const uint32_t* count, uint32_t k, uint32_t* seeds_out,
+                        uint64_t* gains_out, uint64_t* cov_out) {
+  const uint64_t nT = (uint64_t)n * T;
+  int64_t* cnt;
+  uint8_t *covered, *selected;
+  uint32_t* picks;
+  uint64_t i, w, v, cov = 0;
+  uint32_t j;
+  if (T < 1 || k < 1 || k > n) return 1;
+  cnt = (int64_t*)malloc(sizeof(int64_t) * nT);
+  covered = (uint8_t*)calloc(nsets ? nsets : 1, 1);
+  selected = (uint8_t*)calloc(nT, 1);
+  picks = (uint32_t*)calloc(T, sizeof(uint32_t));
+  for (v = 0; v < nT; ++v) cnt[v] = count[v];
+  for (j = 0; j < k * T; ++j) {
+    int64_t best = -1;
+    uint32_t u = 0;
+    for (v = 0; v < nT; ++v)
+      if (!selected[v] && picks[v / n] < k && cnt[v] > best) { best = cnt[v]; u = (uint32_t)v; }
+    selected[u] = 1;
+    picks[u / n]++;
+    seeds_out[j] = u;
+    if (gains_out) gains_out[j] = (uint64_t)best;
+    cov += (uint64_t)best;
+    for (i = 0; i < nsets; ++i) {                        /* Alg. 7 with pair counters */
+      uint64_t off = offsets[i], len = offsets[i + 1] - offsets[i];
+      if (covered[i]) continue;
+      if (!contains_sorted(pairs + off, len, u)) continue;
+      covered[i] = 1;
+      for (w = 0; w < len; ++w) cnt[pairs[off + w]]--;
+    }
+  }
+  if (cov_out) *cov_out = cov;
+  free(cnt); free(covered); free(selected); free(picks);
+  return 0;
+}
+
+int og_mrim_select(og_ctx* c, uint32_t k, uint32_t* seeds_out, uint64_t* gains_out, uint64_t* cov_out) {
+  if (!c->mr_have || c->mr_nsets == 0) return 2;
+  return og_mrim_select_pool(c->n, c->mr_T, c->mr_nsets, c->mr_offsets, c->mr_nodes, c->mr_count, k,
+                             seeds_out, gains_out, cov_out);
+}
+
+int og_mrim_constants(uint32_t n, uint32_t k, uint32_t T, double eps, double ell, double out[7]) {
+  if (T < 1 || k > n) return 1;
+  return imm_constants_g(n, (uint64_t)n * T, (uint64_t)k * T, eps, ell, out);
+}
+
+/* Alg. 2 over MRIM sets (R26-R28), exactly as og_imm: LB rounds on x = n / 2^i,
+ * theta = lambda* / LB, cumulative pool, final selection of k*T pairs. Outputs as og_imm. */
+int og_mrim(og_ctx* c, uint32_t k, uint32_t T, double eps, double ell, uint64_t seed,
+            uint32_t* seeds_out, uint64_t* gains_out, double dres[7], double tr_theta[64],
+            uint64_t tr_T[64], uint64_t tr_cov[64], uint64_t ures[3]) {
+  double K[7], n = (double)c->n, LB = 1.0, theta, log2n;
+  uint64_t cov = 0, Tn, R;
+  int i, i_max, rounds = 0;
+  uint32_t* tmp_seeds;
+  if (og_mrim_constants(c->n, k, T, eps, ell, K)) return 1;
+  tmp_seeds = (uint32_t*)malloc(sizeof(uint32_t) * k * T);
+  c->mr_have = 0;                                        /* R = {} */
+  if (og_mrim_generate(c, 0, T, seed)) { free(tmp_seeds); return 1; }
+  log2n = log2(n);
+  i_max = (int)floor(log2n) - 1;
+  for (i = 1; i <= i_max && i <= 64; ++i) {
+    double x = n / ldexp(1.0, i);
+    double theta_i = K[3] / x;
+    Tn = (uint64_t)ceil(theta_i);
+    R = c->mr_nsets > Tn ? c->mr_nsets : Tn;
+    og_mrim_generate(c, R, T, seed);
+    og_mrim_select(c, k, tmp_seeds, NULL, &cov);
+    tr_theta[i - 1] = theta_i; tr_T[i - 1] = Tn; tr_cov[i - 1] = cov;
+    rounds = i;
+    if ((n * (double)cov) / (double)c->mr_nsets >= (1.0 + K[1]) * x) {
+      LB = (n * (double)cov) / (double)c->mr_nsets / (1.0 + K[1]);
+      break;
+    }
+  }
+  theta = K[6] / LB;
+  Tn = (uint64_t)ceil(theta);
+  R = c->mr_nsets > Tn ? c->mr_nsets : Tn;
+  og_mrim_generate(c, R, T, seed);
+  og_mrim_select(c, k, seeds_out, gains_out, &cov);
+  dres[0] = LB; dres[1] = theta; dres[2] = n * (double)cov / (double)c->mr_nsets;
+  dres[3] = K[0]; dres[4] = K[1]; dres[5] = K[3]; dres[6] = K[6];
+  ures[0] = (uint64_t)rounds; ures[1] = c->mr_nsets; ures[2] = cov;
+  free(tmp_seeds);
   return 0;
 }

@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--workload", default="C3", choices=sorted(gi.WORKLOADS))
     ap.add_argument("--k", type=int, default=0, help="override the workload's k (parameter sweeps)")
     ap.add_argument("--eps", type=float, default=0.0, help="override the workload's eps (parameter sweeps)")
+    ap.add_argument("--rounds", type=int, default=1,
+                    help="MRIM rounds T (CR-NAIMM, §4.8; readings R26-R28): value counts MRIM sets/s")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -62,8 +64,14 @@ def dist_env():
     return world, rank, local
 
 
-def config_of(w, world):
-    return {"workload": f"{w.key}: {w.desc}", "n": w.n, "m": w.m, "k": w.k, "eps": w.eps,
+def unit_of(args):
+    return UNIT if args.rounds == 1 else "MRIM sets/s"
+
+
+def config_of(w, world, rounds=1):
+    mr = {} if rounds == 1 else {"mrim_rounds": rounds,
+                                 "mrim": f"CR-NAIMM (§4.8): k={w.k} seeds per round, T={rounds} rounds"}
+    return {"workload": f"{w.key}: {w.desc}", **mr, "n": w.n, "m": w.m, "k": w.k, "eps": w.eps,
             "ell": w.ell, "model": "IC" if w.model == gi.IC else "LT",
             "weights": {gi.W_WC: "weighted cascade 1/d_in", gi.W_UNIFORM: f"uniform p={w.p_uniform}",
                         gi.W_EXPLICIT: "explicit"}[w.scheme],
@@ -127,17 +135,23 @@ class Clocks:
 # ------------------------------------------------------------------------------------------
 # reference arm: the oracle on the host cores
 # ------------------------------------------------------------------------------------------
-def oracle_sample(w, g, seconds, k):
+def oracle_sample(w, g, seconds, k, rounds=1):
     """Oracle RR generation (ids 0..T-1, grown in chunks until `seconds` elapse) followed by one
-    NodeSelection (k) over that sample; returns (sets, wall seconds)."""
+    NodeSelection (k) over that sample; returns (sets, wall seconds). rounds > 1: MRIM sets."""
     import oracle
     o = oracle.Oracle(g, w.model, w.scheme, w.p_uniform)
     t0 = time.perf_counter()
-    T, chunk = 0, 2000
+    T, chunk = 0, max(2000 // rounds, 200)
     while time.perf_counter() - t0 < seconds:
         T += chunk
-        o.generate(T, w.rr_seed)
-    o.select(k)
+        if rounds > 1:
+            o.mrim_generate(T, rounds, w.rr_seed)
+        else:
+            o.generate(T, w.rr_seed)
+    if rounds > 1:
+        o.mrim_select(k)
+    else:
+        o.select(k)
     return T, time.perf_counter() - t0
 
 
@@ -148,21 +162,22 @@ def run_reference(args, w):
     g = gi.workload_graph(w.key)
     per_step = max(1.0, min(10.0, 60.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        oracle_sample(w, g, per_step / 4, w.k)
+        oracle_sample(w, g, per_step / 4, w.k, args.rounds)
     tot_sets, tot_s = 0, 0.0
     for _ in range(args.steps):
-        T, s = oracle_sample(w, g, per_step, w.k)
+        T, s = oracle_sample(w, g, per_step, w.k, args.rounds)
         tot_sets += T
         tot_s += s
     v = tot_sets / tot_s
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+    unit = unit_of(args)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": unit, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_s / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic", "config": config_of(w, 1),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "data": "synthetic", "config": config_of(w, 1, args.rounds),
+            "cpu_baseline": {"value": v, "unit": unit, "cores": 1, "kind": "oracle",
                              "sample": f"per step: oracle RR sets of ids 0..T-1 for ~{per_step:.1f}s, "
                                        f"then one k={w.k} NodeSelection over them"},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -206,6 +221,8 @@ def run_gim(args, w):
     stream = torch.cuda.Stream(local)
     ctx = P.Gim(local, stream=stream.cuda_stream)
     ctx.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme, weights=g.weights, p_uniform=w.p_uniform)
+    if args.rounds > 1:
+        ctx.set_rounds(args.rounds)
     if world > 1:
         ctx.set_shard(rank, world)
         ctx.set_allreduce(P.torch_allreduce())
@@ -302,6 +319,8 @@ def run_gim(args, w):
         rp_h = torch.from_numpy(g.row_ptr).pin_memory()
         src_h = torch.from_numpy(g.src).pin_memory()
         ctx2 = P.Gim(local, stream=stream.cuda_stream)
+        if args.rounds > 1:
+            ctx2.set_rounds(args.rounds)
         if world > 1:
             ctx2.set_shard(rank, world)
             ctx2.set_allreduce(P.torch_allreduce())
@@ -325,9 +344,9 @@ def run_gim(args, w):
         torch.cuda.synchronize()
         barrier()
         ms2 = max_over_ranks(f0.elapsed_time(f1))
-        e2e = {"value": e2e_sets / (ms2 / 1000.0), "unit": UNIT,
+        e2e = {"value": e2e_sets / (ms2 / 1000.0), "unit": unit_of(args),
                "h2d_bytes_per_step": int(g.row_ptr.nbytes + g.src.nbytes),
-               "d2h_bytes_per_step": int(4 * w.k + 8 * w.k * (r.rounds + 1)),
+               "d2h_bytes_per_step": int((4 * w.k + 8 * w.k * (r.rounds + 1)) * args.rounds),
                "ms_per_step": ms2 / args.steps,
                "note": "per step: gim_load_graph (H2D of the in-CSR from pinned host buffers + on-device validation) + gim_imm + seeds D2H"}
         ctx2.close()
@@ -335,16 +354,16 @@ def run_gim(args, w):
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) --------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        T, s = oracle_sample(w, g, args.cpu_seconds, w.k)
-        cpu = {"value": T / s, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"oracle RR sets of ids 0..{T - 1} ({s:.1f}s) + one k={w.k} NodeSelection over them, "
-                         "single-threaded C"}
+        T, s = oracle_sample(w, g, args.cpu_seconds, w.k, args.rounds)
+        cpu = {"value": T / s, "unit": unit_of(args), "cores": 1, "kind": "oracle",
+               "sample": f"oracle {'MRIM' if args.rounds > 1 else 'RR'} sets of ids 0..{T - 1} ({s:.1f}s) + one "
+                         f"k={w.k} NodeSelection over them, single-threaded C"}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        line = {"metric": METRIC, "value": value, "unit": unit_of(args), "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-                "config": config_of(w, world),
+                "config": config_of(w, world, args.rounds),
                 "imm_time_s": ms / args.steps / 1000.0,
                 "rr_sets_per_step": r0.R_final, "theta": r0.theta, "LB": r0.LB, "rounds": r0.rounds,
                 "spread_est": r0.spread_est,

@@ -135,8 +135,26 @@ gim_status gim_imm(gim_ctx* ctx, uint32_t k, double eps, double ell, uint64_t se
 gim_status gim_rr_export(gim_ctx* ctx, uint64_t* n_sets, uint64_t* pool_len, uint64_t* ids_out,
                          uint64_t* offsets_out, uint32_t* nodes_out, int sort_each_set);
 
-/* count_out[n]: this rank's local occurrence counts (Occur). */
+/* count_out[n] (n*T in MRIM mode, indexed by pair id): this rank's local occurrence counts
+ * (Occur). */
 gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
+
+/* Multi-round IM (MRIM), the CR-NAIMM algorithm as gIM adapts it (§4.8: "after
+ * selecting a random node, we initiate a random BFS originating from the selected node as many
+ * times as the number of rounds. Also, each element in a random RR set is a tuple of node-id and
+ * round number"). rounds = T >= 1 (T = 1, the default, is standard IM); discards the pool.
+ * Readings:
+ *  R26 MRIM set i = {(u, t) : 0 <= t < T, u in RR^t_i}: the T rounds share root(seed, i) and
+ *      round t draws the coins of standard RR id i*T + t; the pair (u, t) is the element id
+ *      t*n + u. In MRIM mode theta (gim_generate_rr) counts MRIM sets; gim_rr_export returns the
+ *      T*theta per-round sets (ids i*T + t) whose members are pair ids.
+ *  R27 gim_select(k): k seeds PER ROUND, k*T picks in greedy order: the unselected pair of a
+ *      round with fewer than k seeds with the largest count, ties -> lowest pair id;
+ *      seeds_out[k*T] / gains_out[k*T] hold pair ids (round = id / n, node = id % n).
+ *  R28 gim_imm(k): IMM with ln C(n*T, k*T) in lambda' and lambda*; seeds_out[k*T] pair ids;
+ *      R_final / theta count MRIM sets.
+ * GIM_EINVAL if T == 0 or n*T >= 2^32 - 1 (pair ids are uint32, 2^32 - 1 is a sentinel). */
+gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
 
 /* Tunables (test / ablation hooks; the defaults are the tuned configuration):
  *  GIM_OPT_FORCE_GIANT  = 1: every RR set goes through the block-per-RR giant kernel.

@@ -53,6 +53,7 @@ def _lib():
         "og_mc_spread": (_int, [_p, _p, _u32, _u64, _u64, _p, _p]),
         "og_mrim_generate": (_int, [_p, _u64, _u32, _u64]),
         "og_mrim_num_sets": (_u64, [_p]),
+        "og_mrim_set": (_u32, [_p, _u64, _u64, _u32, _p]),
         "og_mrim_pool_len": (_u64, [_p]),
         "og_mrim_export": (None, [_p, _p, _p, _p]),
         "og_mrim_select_pool": (_int, [_u32, _u32, _u64, _p, _p, _p, _u32, _p, _p, _p]),
@@ -256,6 +257,11 @@ class Oracle:
         if _lib().og_mrim_generate(self._h, N, T, seed):
             raise ValueError("og_mrim_generate: invalid T")
         self._T_mr = T
+
+    def mrim_set(self, seed: int, i: int, T: int) -> np.ndarray:
+        buf = np.zeros(self.n * T, dtype=np.uint32)
+        ln = _lib().og_mrim_set(self._h, seed, i, T, _ptr(buf))
+        return buf[:ln].copy()
 
     def mrim_export(self):
         ns = int(_lib().og_mrim_num_sets(self._h))

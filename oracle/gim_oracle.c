@@ -582,6 +582,17 @@ int og_mrim_generate(og_ctx* c, uint64_t N, uint32_t T, uint64_t seed) {
   return 0;
 }
 
+/* One MRIM set (R26) by itself, ascending pair ids; returns its size (out: n*T entries). */
+uint32_t og_mrim_set(og_ctx* c, uint64_t seed, uint64_t i, uint32_t T, uint32_t* out) {
+  uint32_t root = og_root(seed, i, c->n), len = 0, t, q;
+  if (!c->mr_tmp) c->mr_tmp = (uint32_t*)malloc(sizeof(uint32_t) * c->n);
+  for (t = 0; t < T; ++t) {
+    uint32_t l = rr_from(c, seed, i * (uint64_t)T + t, root, c->mr_tmp);
+    for (q = 0; q < l; ++q) out[len++] = t * c->n + c->mr_tmp[q];
+  }
+  return len;
+}
+
 uint64_t og_mrim_num_sets(const og_ctx* c) { return c->mr_have ? c->mr_nsets : 0; }
 uint64_t og_mrim_pool_len(const og_ctx* c) { return c->mr_have ? c->mr_len : 0; }
 void og_mrim_export(const og_ctx* c, uint64_t* offsets_out, uint32_t* pairs_out, uint32_t* count_out) {

@@ -57,6 +57,9 @@ struct gim_ctx {
   float p_uniform = 0.f;
   uint64_t thr_uniform = 0;
   DevBuf row_ptr, src, thr_edge;
+  // MRIM (readings R26-R28): rounds T; pair ids t*n + u index the count / index / selection
+  // arrays (n*T of them); the T rounds of MRIM set i are the consecutive standard ids i*T + t
+  uint32_t rounds = 1;
   // sharding
   int rank = 0, world = 1;
   gim_allreduce_fn arfn = nullptr;
@@ -106,6 +109,8 @@ struct gim_ctx {
 };
 
 namespace {
+
+uint64_t nsp(const gim_ctx* c) { return (uint64_t)c->n * c->rounds; }   // counted elements
 
 struct DeviceGuard {
   int prev = -1;
@@ -257,7 +262,7 @@ void drop_inv(gim_ctx* c) {
 // Index local sets [set0, set1) (pool elements [e0, e1)) as a new segment; the per-node
 // histogram is count_total - cnt_snap (no extra atomics), then scan + cursor scatter.
 gim_status build_inv_segment(gim_ctx* c, uint64_t set0, uint64_t set1, uint64_t e0, uint64_t e1) {
-  const uint64_t n = c->n;
+  const uint64_t n = nsp(c);
   if (e1 - e0 >= 0xFFFFFFFFull) return fail(c, GIM_ENOMEM, "an index segment must hold < 2^32 RR elements");
   gim_ctx::InvSeg sg;
   TRY(dalloc(c, sg.off, (n + 1) * 4));
@@ -266,7 +271,7 @@ gim_status build_inv_segment(gim_ctx* c, uint64_t set0, uint64_t set1, uint64_t 
   TRY(ensure(c, c->scan_tmp, (scan_tiles(n) + 2) * 8));
   Prof pf(c, CLS_INV);
   TRY(launched(c, launch_count_delta(c->count_total.as<uint32_t>(), c->cnt_snap.as<uint32_t>(),
-                                     c->cursor.as<uint32_t>(), c->n, c->num_sms * 8, c->stream), "k_count_delta"));
+                                     c->cursor.as<uint32_t>(), (uint32_t)n, c->num_sms * 8, c->stream), "k_count_delta"));
   int nl = 0;
   // exclusive prefix = start of each node's list; the scatter advances it to the list's end
   cudaError_t e = launch_scan_u32_to32(c->cursor.as<uint32_t>(), n, sg.off.as<uint32_t>(), c->scan_tmp.as<uint64_t>(),
@@ -288,16 +293,16 @@ gim_status reset_pool(gim_ctx* c, uint64_t seed) {
   c->nsets = 0;
   c->pool_len = 0;
   c->segs.clear();
-  TRY(ensure(c, c->count_total, (uint64_t)c->n * 4));
-  CK(cudaMemsetAsync(c->count_total.p, 0, (uint64_t)c->n * 4, c->stream));
+  TRY(ensure(c, c->count_total, nsp(c) * 4));
+  CK(cudaMemsetAsync(c->count_total.p, 0, nsp(c) * 4, c->stream));
   TRY(ensure(c, c->offsets, 8 * 1024));
   CK(cudaMemsetAsync(c->offsets.p, 0, 8, c->stream));
   drop_inv(c);
   c->inv_valid = true;
   c->set_limit = ~0ull;
   c->truncated = false;
-  TRY(ensure(c, c->cnt_snap, (uint64_t)c->n * 4));
-  CK(cudaMemsetAsync(c->cnt_snap.p, 0, (uint64_t)c->n * 4, c->stream));
+  TRY(ensure(c, c->cnt_snap, nsp(c) * 4));
+  CK(cudaMemsetAsync(c->cnt_snap.p, 0, nsp(c) * 4, c->stream));
   return GIM_OK;
 }
 
@@ -348,6 +353,7 @@ RRParams base_params(gim_ctx* c) {
   p.qcap = c->qcap;
   p.lt_spill = c->lt_spill.as<uint32_t>();
   p.force_giant = c->force_giant;
+  p.rounds = c->rounds;
   return p;
 }
 
@@ -494,7 +500,8 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     TRY(launched(c, launch_store(c->staging.as<uint32_t>(), c->sizes.as<uint32_t>(), c->soff.as<uint64_t>(),
                                  c->scan_out.as<uint64_t>(), cnt, c->pool_len, c->pool.as<uint32_t>(),
                                  c->offsets.as<uint64_t>() + c->nsets, c->count_total.as<uint32_t>(),
-                                 c->num_sms * 8, c->stream), "k_store"));
+                                 c->rounds, (uint32_t)(gstart % c->rounds), c->n, c->num_sms * 8, c->stream),
+                    "k_store"));
   }
   c->segs.push_back(Seg{gstart, c->nsets, cnt});
   c->nsets += cnt;
@@ -529,9 +536,11 @@ gim_status truncate_pool(gim_ctx* c, uint64_t theta) {
   return GIM_OK;
 }
 
-gim_status generate(gim_ctx* c, uint64_t theta, uint64_t seed) {
+// theta counts sets in API units: RR sets, or MRIM sets of `rounds` standard ids each (R26)
+gim_status generate(gim_ctx* c, uint64_t theta_sets, uint64_t seed) {
   if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
-  if (theta >= (1ull << 32)) return fail(c, GIM_EINVAL, "theta must be < 2^32");
+  if (theta_sets >= (1ull << 32) / c->rounds) return fail(c, GIM_EINVAL, "theta * rounds must be < 2^32");
+  const uint64_t theta = theta_sets * c->rounds;
   if (!c->have_seed || c->seed != seed) TRY(reset_pool(c, seed));
   if (theta < c->T_global) {
     TRY(truncate_pool(c, theta));
@@ -541,9 +550,10 @@ gim_status generate(gim_ctx* c, uint64_t theta, uint64_t seed) {
       c->truncated = false;
       c->set_limit = ~0ull;
     }
-    const uint64_t a = c->T_global, len = theta - a;
-    const uint64_t lo = a + (uint64_t)((unsigned __int128)len * c->rank / c->world);
-    const uint64_t hi = a + (uint64_t)((unsigned __int128)len * (c->rank + 1) / c->world);
+    // the rank's slice of the new sets (whole MRIM sets: the T rounds of a set stay together)
+    const uint64_t a = c->T_global, len = (theta - a) / c->rounds, Tr = c->rounds;
+    const uint64_t lo = a + Tr * (uint64_t)((unsigned __int128)len * c->rank / c->world);
+    const uint64_t hi = a + Tr * (uint64_t)((unsigned __int128)len * (c->rank + 1) / c->world);
     const uint64_t set0 = c->nsets, e0 = c->pool_len;
     for (uint64_t s = lo; s < hi; s += kChunk) TRY(gen_chunk(c, s, (uint32_t)std::min<uint64_t>(kChunk, hi - s)));
     // one inverted-index segment per generate call (= per IMM round): its O(n) count scan is
@@ -566,10 +576,13 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   if (k < 1 || k > c->n) return fail(c, GIM_EINVAL, "k must satisfy 1 <= k <= n");
   if (!c->have_seed || c->T_global == 0) return fail(c, GIM_ESTATE, "RR pool is empty");
   if (c->world > 1 && !c->arfn) return fail(c, GIM_ESTATE, "world > 1 requires gim_set_allreduce");
-  const uint64_t n = c->n;
+  const uint64_t n = nsp(c);                        // counted elements (nodes, or MRIM pairs)
+  const uint32_t kk = k * c->rounds;                // picks: k per round (R27)
+  const MrimSel mrs{c->rounds, c->n, k};
+  const MrimSel* mr = c->rounds > 1 ? &mrs : nullptr;
   TRY(ensure(c, c->cnt, n * 4));
-  TRY(ensure(c, c->covered, std::max<uint64_t>(c->nsets, 1)));
-  TRY(ensure(c, c->keys, (uint64_t)k * 8));
+  TRY(ensure(c, c->covered, std::max<uint64_t>(c->nsets / c->rounds, 1)));
+  TRY(ensure(c, c->keys, (uint64_t)kk * 8));
   if (c->world > 1) TRY(ensure(c, c->dec, n * 4));
   int32_t* dec = c->world > 1 ? c->dec.as<int32_t>() : nullptr;
   if (!c->inv_valid) {                          // one segment over the whole local pool
@@ -596,8 +609,8 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   const uint32_t* nsegd = reinterpret_cast<const uint32_t*>(segd + kMaxInvSeg);
   CK(cudaMemcpyAsync(c->cnt.p, c->count_total.p, n * 4, cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaEventRecord(c->ev_cnt_copied, c->stream));
-  CK(cudaMemsetAsync(c->covered.p, 0, std::max<uint64_t>(c->nsets, 1), c->stream));
-  CK(cudaMemsetAsync(c->keys.p, 0, (uint64_t)k * 8, c->stream));
+  CK(cudaMemsetAsync(c->covered.p, 0, std::max<uint64_t>(c->nsets / c->rounds, 1), c->stream));
+  CK(cudaMemsetAsync(c->keys.p, 0, (uint64_t)kk * 8, c->stream));
   if (dec) {
     CK(cudaMemsetAsync(dec, 0, n * 4, c->stream));
     c->st.allreduces++;
@@ -610,13 +623,13 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   uint32_t* cand = nullptr;
   unsigned int *hist = nullptr, *ncand = nullptr;
   uint32_t* tau_p1 = nullptr;
-  if (!dec && (c->use_cand == 2 || (c->use_cand == 1 && n >= (1u << 23)))) {   // small n: full scan is cheaper
+  if (!dec && c->rounds == 1 && (c->use_cand == 2 || (c->use_cand == 1 && n >= (1u << 23)))) {   // small n: full scan is cheaper
     TRY(ensure(c, c->cand, (uint64_t)kMaxCand * 4 + 64 * 4));
     cand = c->cand.as<uint32_t>();
     hist = reinterpret_cast<unsigned int*>(cand + kMaxCand);
     tau_p1 = reinterpret_cast<uint32_t*>(hist + 40);
     ncand = reinterpret_cast<unsigned int*>(hist + 41);
-    TRY(launched(c, launch_cand_setup(c->cnt.as<uint32_t>(), c->n, kMaxCand, hist, tau_p1, cand, ncand,
+    TRY(launched(c, launch_cand_setup(c->cnt.as<uint32_t>(), (uint32_t)n, kMaxCand, hist, tau_p1, cand, ncand,
                                       c->num_sms * 4, c->stream), "candidate setup", 3));
   }
   if (!dec && c->use_graph) {
@@ -624,18 +637,20 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
     // buffer pointers; steady-state IMM runs reuse it), so the GPU runs them back to back.
     const std::vector<uintptr_t> key = {(uintptr_t)c->cnt.p, (uintptr_t)segd, (uintptr_t)cand,
                                         (uintptr_t)c->offsets.p, (uintptr_t)c->pool.p, (uintptr_t)c->covered.p,
-                                        (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n, (uintptr_t)limited};
+                                        (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n, (uintptr_t)limited,
+                                        (uintptr_t)c->rounds};
     if (!c->sel_exec || key != c->sel_key) {
       if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
       c->sel_exec = nullptr;
       cudaGraph_t graph = nullptr;
       CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      for (uint32_t j = 0; j < k; ++j) {
+      for (uint32_t j = 0; j < kk; ++j) {
         if (cand) launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream);
-        launch_argmax(c->cnt.as<uint32_t>(), nullptr, c->n, keys, (int)j, tau_p1, c->num_sms * 4, c->stream);
+        launch_argmax(c->cnt.as<uint32_t>(), nullptr, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * 4, c->stream,
+                      mr != nullptr);
         launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                      c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * 8, c->stream,
-                     limited);
+                     limited, mr);
       }
       CK(cudaStreamEndCapture(c->stream, &graph));
       const cudaError_t ie = cudaGraphInstantiate(&c->sel_exec, graph, 0);
@@ -644,32 +659,32 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
       c->sel_key = key;
     }
     Prof pf(c, CLS_SELECT);
-    TRY(launched(c, cudaGraphLaunch(c->sel_exec, c->stream), "selection graph", (cand ? 3 : 2) * (int)k));
+    TRY(launched(c, cudaGraphLaunch(c->sel_exec, c->stream), "selection graph", (cand ? 3 : 2) * (int)kk));
   } else {
-    for (uint32_t j = 0; j < k; ++j) {
+    for (uint32_t j = 0; j < kk; ++j) {
       {
         Prof pf(c, CLS_SELECT);
         if (cand) TRY(launched(c, launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream),
                                "k_argmax_cand"));
-        TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, c->n, keys, (int)j, tau_p1, c->num_sms * 4,
-                                      c->stream), "k_argmax"));
+        TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * 4,
+                                      c->stream, mr != nullptr), "k_argmax"));
         TRY(launched(c, launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                                      c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * 8,
-                                     c->stream, limited), "k_cover"));
+                                     c->stream, limited, mr), "k_cover"));
       }
-      if (dec && j + 1 < k) {
+      if (dec && j + 1 < kk) {
         c->st.allreduces++;
         if (c->arfn(dec, n, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(dec) failed");
       }
     }
   }
-  if (c->h_keys_cap < k) {
+  if (c->h_keys_cap < kk) {
     if (c->h_keys) cudaFreeHost(c->h_keys);
     c->h_keys = nullptr;
-    CK(cudaMallocHost(&c->h_keys, (uint64_t)k * 8));
-    c->h_keys_cap = k;
+    CK(cudaMallocHost(&c->h_keys, (uint64_t)kk * 8));
+    c->h_keys_cap = kk;
   }
-  CK(cudaMemcpyAsync(c->h_keys, keys, (uint64_t)k * 8, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->h_keys, keys, (uint64_t)kk * 8, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaEventRecord(c->ev_sel_done, c->stream));
   c->sel_pending = true;
   return GIM_OK;
@@ -679,7 +694,7 @@ gim_status select_finish(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gain
   TRY(sync(c));
   c->sel_pending = false;
   uint64_t cov = 0;
-  for (uint32_t j = 0; j < k; ++j) {
+  for (uint32_t j = 0; j < k * c->rounds; ++j) {
     seeds[j] = ~(uint32_t)(c->h_keys[j] & 0xFFFFFFFFull);
     const uint64_t g = c->h_keys[j] >> 32;
     if (gains) gains[j] = g;
@@ -711,7 +726,8 @@ struct ImmConst {
   double ell_eff, eps_p, lnC, lambda_p, alpha, beta, lambda_s;
 };
 
-ImmConst imm_constants(uint32_t n_, uint32_t k, double eps, double ell) {
+// ln C(N, K) in lambda', lambda*: N = n, K = k for IMM; MRIM (R28) N = n*T pairs, K = k*T picks
+ImmConst imm_constants(uint32_t n_, uint32_t k, double eps, double ell, uint32_t T = 1) {
   ImmConst K;
   const double n = (double)n_;
   const double ln_n = std::log(n);
@@ -719,7 +735,8 @@ ImmConst imm_constants(uint32_t n_, uint32_t k, double eps, double ell) {
   K.ell_eff = ell * (1.0 + std::log(2.0) / ln_n);
   K.eps_p = std::sqrt(2.0) * eps;
   K.lnC = 0.0;
-  for (uint32_t t = 1; t <= k; ++t) K.lnC += std::log((double)(n_ - k + t)) - std::log((double)t);
+  const uint64_t NN = (uint64_t)n_ * T, KK = (uint64_t)k * T;
+  for (uint64_t t = 1; t <= KK; ++t) K.lnC += std::log((double)(NN - KK + t)) - std::log((double)t);
   K.lambda_p = (2.0 + 2.0 / 3.0 * K.eps_p) * (K.lnC + K.ell_eff * ln_n + std::log(log2n)) * n / (K.eps_p * K.eps_p);
   K.alpha = std::sqrt(K.ell_eff * ln_n + std::log(2.0));
   K.beta = std::sqrt((1.0 - 1.0 / M_E) * (K.lnC + K.ell_eff * ln_n + std::log(2.0)));
@@ -840,6 +857,7 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
   if (scheme == GIM_W_UNIFORM && !(p_uniform >= 0.f && p_uniform <= 1.f)) return fail(c, GIM_EINVAL, "p_uniform must be in [0,1]");
   // canonical in-CSR (reading R15): the end points here, everything else on the device below
   if (rp[0] != 0 || rp[n] != m) return fail(c, GIM_EINVAL, "row_ptr[0] must be 0 and row_ptr[n] must be m");
+  if ((uint64_t)n * c->rounds >= 0xFFFFFFFFull) return fail(c, GIM_EINVAL, "n * rounds must be < 2^32 - 1");
   // release the previous graph and pool
   dfree(c, c->row_ptr);
   dfree(c, c->src);
@@ -967,7 +985,7 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
   if (!(ell > 0.0)) return fail(c, GIM_EINVAL, "ell must be > 0");
   DeviceGuard g(c->device);
   const double t_api = now_ms();
-  const ImmConst K = imm_constants(c->n, k, eps, ell);
+  const ImmConst K = imm_constants(c->n, k, eps, ell, c->rounds);
   gim_imm_result r;
   std::memset(&r, 0, sizeof(r));
   r.ell_eff = K.ell_eff;
@@ -979,15 +997,16 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
   TRY(generate(c, 0, seed));
   double LB = 1.0;                                           // reading R6
   uint64_t cov = 0;
-  std::vector<uint32_t> tmp(k);
+  std::vector<uint32_t> tmp((size_t)k * c->rounds);
+  auto R_sets = [c]() { return c->T_global / c->rounds; };     // sets in API units
   const int i_max = (int)std::floor(std::log2(n)) - 1;       // reading R5
   for (int i = 1; i <= i_max && i <= 64; ++i) {              // Alg. 2 l.2
     const double x = n / std::ldexp(1.0, i);                 // l.3
     const double theta_i = K.lambda_p / x;                   // l.4 (f = lambda', reading R1)
     const uint64_t T = (uint64_t)std::ceil(theta_i);
-    const uint64_t R = std::max<uint64_t>(c->T_global, T);   // l.5 (reading R4)
+    const uint64_t R = std::max<uint64_t>(R_sets(), T);      // l.5 (reading R4)
     TRY(generate(c, R, seed));
-    if (c->T_global > R) TRY(truncate_pool(c, R));            // drop excess speculation
+    if (R_sets() > R) TRY(truncate_pool(c, R * c->rounds));  // drop excess speculation
     // speculative target while this round's selection runs: the next round's T if the test
     // fails, capped by ceil(lambda*/x), the largest theta a passing test can produce
     const uint64_t spec = std::min<uint64_t>(
@@ -1010,13 +1029,13 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
   for (uint32_t q = 0; q < r.rounds; ++q) R_last = std::max<uint64_t>(R_last, r.theta_i[q]);
   const uint64_t R_final = std::max<uint64_t>(R_last, T);   // reading R8
   TRY(generate(c, R_final, seed));                           // extends or truncates speculation
-  std::vector<uint64_t> gains(k);
+  std::vector<uint64_t> gains((size_t)k * c->rounds);
   TRY(select_impl(c, k, seeds, gains.data(), &cov));
   r.LB = LB;
   r.theta = theta;
-  r.R_final = c->T_global;
+  r.R_final = R_sets();
   r.covered = cov;
-  r.spread_est = n * (double)cov / (double)c->T_global;     // Eq. 3
+  r.spread_est = n * (double)cov / (double)R_sets();        // Eq. 3
   if (res) *res = r;
   c->st.host_ms_api += now_ms() - t_api;
   return GIM_OK;
@@ -1049,13 +1068,26 @@ gim_status gim_rr_export(gim_ctx* c, uint64_t* n_sets, uint64_t* pool_len, uint6
   return GIM_OK;
 }
 
+gim_status gim_set_rounds(gim_ctx* c, uint32_t rounds) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  if (rounds == 0) return fail(c, GIM_EINVAL, "rounds must be >= 1");
+  if (c->graph && (uint64_t)c->n * rounds >= 0xFFFFFFFFull)
+    return fail(c, GIM_EINVAL, "n * rounds must be < 2^32 - 1 (uint32 pair ids)");
+  if (rounds != c->rounds) {
+    c->rounds = rounds;
+    c->have_seed = false;                      // the pool (and its index) is regenerated
+  }
+  return GIM_OK;
+}
+
 gim_status gim_counts_export(gim_ctx* c, uint32_t* count_out) {
   if (!c) return GIM_EINVAL;
   c->err.clear();
   if (!count_out) return fail(c, GIM_EINVAL, "count_out required");
   if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
   DeviceGuard g(c->device);
-  CK(cudaMemcpyAsync(count_out, c->count_total.p, (uint64_t)c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(count_out, c->count_total.p, nsp(c) * 4, cudaMemcpyDeviceToHost, c->stream));
   return sync(c);
 }
 

@@ -83,6 +83,13 @@ __device__ __forceinline__ uint32_t rr_root(uint64_t seed, uint64_t id, uint32_t
   return (uint32_t)__umul64hi(u64, (uint64_t)n);
 }
 
+// MRIM (reading R26, §4.8): the T rounds of MRIM set i are standard RR ids i*T + t that
+// share the root of id i ("after selecting a random node, we initiate a random BFS originating
+// from the selected node as many times as the number of rounds"). rounds = 1: standard IM.
+__device__ __forceinline__ uint32_t rr_root_of(uint64_t seed, uint64_t id, uint32_t n, uint32_t rounds) {
+  return rr_root(seed, rounds > 1u ? id / rounds : id, n);
+}
+
 // Device counters of one generation launch sequence (zeroed by the host per chunk).
 struct GenCounters {
   unsigned long long stage_tail;   // staging bump allocator (elements)
@@ -141,6 +148,7 @@ struct RRParams {
   uint32_t qcap;               // shared-memory queue capacity (<= kQMax)
   uint32_t* lt_spill;          // LT: per-warp spill of walks longer than kLtCap (lane-interleaved)
   int force_giant;
+  uint32_t rounds;             // MRIM rounds T (1 = standard IM): root of id = root(id / T)
 };
 
 // Shared-memory layout of the warp-per-RR kernel.

@@ -13,7 +13,8 @@ cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, 
                             uint32_t* gqueues, uint64_t bm_words, cudaStream_t s);
 cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const uint64_t* soff,
                          const uint64_t* scan, uint32_t count, uint64_t pool_base, uint32_t* pool,
-                         uint64_t* offsets_out, uint32_t* count_total, int grid, cudaStream_t s);
+                         uint64_t* offsets_out, uint32_t* count_total, uint32_t rounds, uint32_t round0,
+                         uint32_t n, int grid, cudaStream_t s);
 cudaError_t launch_count_sub(const uint32_t* pool, uint64_t e0, uint64_t e1, uint32_t* count_total,
                              int grid, cudaStream_t s);
 
@@ -34,16 +35,20 @@ cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, uint32_t limit
 cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* delta, uint32_t n, int grid,
                                cudaStream_t s);
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
-                          const uint32_t* tau_p1, int grid, cudaStream_t s);
+                          const uint32_t* tau_p1, int grid, cudaStream_t s, bool excl = false);
 cudaError_t launch_cand_setup(const uint32_t* cnt, uint32_t n, uint32_t kmax, unsigned int* hist,
                               uint32_t* tau_p1, uint32_t* cand, unsigned int* ncand, int grid, cudaStream_t s);
 cudaError_t launch_argmax_cand(const uint32_t* cnt, const uint32_t* cand, const unsigned int* ncand,
                                unsigned long long* keys, int j, int grid, cudaStream_t s);
 struct InvSegDev;
+// MRIM selection (R27): pair ids t*n + u over `rounds` rounds, at most k picks per round
+struct MrimSel {
+  uint32_t rounds, n, k;
+};
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,
                          const uint64_t* offsets, const uint32_t* pool,
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s,
-                         bool limit);
+                         bool limit, const MrimSel* mr = nullptr);
 cudaError_t launch_validate_csr(const uint64_t* rp64, uint32_t n, uint64_t m, const uint32_t* src,
                                 uint32_t* rp32, uint32_t* err, uint32_t* bad_row, int grid, cudaStream_t s);
 }  // namespace gim

@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
     }
     const uint64_t id = p.id_base + item;
     const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
-    const uint32_t root = rr_root(p.seed, id, p.n);
+    const uint32_t root = rr_root_of(p.seed, id, p.n, p.rounds);
     if (lane == 0) {
       q[0] = root;
       h[hash_slot(root)] = root;     // table is empty here
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(kIcLaneWarps * 32) k_rr_ic_lane(RRParams p) {
         if (active) {
           item = p.item_list ? p.item_list[i] : i;
           id = p.id_base + item;
-          qv[lane] = rr_root(p.seed, id, p.n);
+          qv[lane] = rr_root_of(p.seed, id, p.n, p.rounds);
           head = 0;
           tail = 1;
           on_node = false;
@@ -727,7 +727,7 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
         if (active) {
           item = p.item_list ? p.item_list[i] : i;
           id = p.id_base + item;
-          v = rr_root(p.seed, id, p.n);
+          v = rr_root_of(p.seed, id, p.n, p.rounds);
           path[lane] = v;
           len = 1;
           if (p.force_giant) {
@@ -934,7 +934,7 @@ __global__ void __launch_bounds__(kGiantThreads, kGiantBlocksPerSM) k_rr_giant(R
     const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
     if (rec.qlen == 0) {
       if (threadIdx.x == 0) {
-        const uint32_t root = rr_root(p.seed, id, p.n);
+        const uint32_t root = rr_root_of(p.seed, id, p.n, p.rounds);
         Q[0] = root;
         atomicOr(&bm[root >> 5], 1u << (root & 31));
         s_tail = 1;
@@ -1170,7 +1170,8 @@ __global__ void __launch_bounds__(256) k_store(const uint32_t* __restrict__ stag
                                                const uint64_t* __restrict__ scan, uint32_t count,
                                                uint64_t pool_base, uint32_t* __restrict__ pool,
                                                uint64_t* __restrict__ offsets_out,
-                                               uint32_t* __restrict__ count_total) {
+                                               uint32_t* __restrict__ count_total, uint32_t rounds,
+                                               uint32_t round0, uint32_t n) {
   // A warp takes 32 consecutive sets (contiguous in the pool) and copies their concatenated
   // members 32 at a time: lane k holds set r0+k (size, staging offset, inclusive end), each
   // element finds its set by a warp binary search. Pool writes are coalesced; tiny sets (C5:
@@ -1181,12 +1182,14 @@ __global__ void __launch_bounds__(256) k_store(const uint32_t* __restrict__ stag
        r0 += nwarps * 32u) {
     const uint32_t nr = min(32u, count - r0);
     const uint64_t base = scan[r0];
-    uint32_t sz = 0;
+    uint32_t sz = 0, roff = 0;
     uint64_t from = 0;
     if ((uint32_t)lane < nr) {
       sz = sizes[r0 + lane];
       from = soff[r0 + lane];
       offsets_out[r0 + lane] = pool_base + scan[r0 + lane];
+      // MRIM (R26): element (u, t) of round t = id mod T is stored as the pair id t*n + u
+      if (rounds > 1u) roff = ((round0 + r0 + lane) % rounds) * n;
     }
     uint32_t total;
     const uint32_t E = warp_excl_scan(sz, lane, total);
@@ -1196,8 +1199,9 @@ __global__ void __launch_bounds__(256) k_store(const uint32_t* __restrict__ stag
       const uint32_t k = warp_owner(P, i);
       const uint64_t fk = __shfl_sync(kFull, from, k);
       const uint32_t ek = __shfl_sync(kFull, E, k);
+      const uint32_t ok = rounds > 1u ? __shfl_sync(kFull, roff, k) : 0u;
       if (i < total) {
-        const uint32_t v = staging[fk + (i - ek)];
+        const uint32_t v = staging[fk + (i - ek)] + ok;
         pool[pool_base + base + i] = v;
         atomicAdd(count_total + v, 1u);
       }
@@ -1282,9 +1286,9 @@ cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, 
 
 cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const uint64_t* soff,
                          const uint64_t* scan, uint32_t count, uint64_t pool_base, uint32_t* pool,
-                         uint64_t* offsets_out, uint32_t* count_total, int grid, cudaStream_t s) {
+                         uint64_t* offsets_out, uint32_t* count_total, uint32_t rounds, uint32_t round0, uint32_t n, int grid, cudaStream_t s) {
   k_store<<<grid, 256, 0, s>>>(staging, sizes, soff, scan, count, pool_base, pool, offsets_out,
-                               count_total);
+                               count_total, rounds, round0, n);
   return cudaGetLastError();
 }
 

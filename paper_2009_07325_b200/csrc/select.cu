@@ -162,14 +162,16 @@ __global__ void __launch_bounds__(256) k_count_delta(const uint32_t* __restrict_
 // all-reduced decrements of the previous step first (P > 1) and retires the previous pick.
 // Streams count as uint4 (4 nodes per load) with 4 independent loads in flight per thread.
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ void argmax_one(uint32_t c, uint32_t v, unsigned long long& best) {
-  const unsigned long long key = (c == kSent) ? 0ull : (((unsigned long long)c << 32) | (unsigned long long)(~v));
+// excl = 0x80000000 in MRIM mode: pairs of a round that already has its k seeds carry the high
+// bit (set by k_cover) and are skipped like selected ones; 0 otherwise.
+__device__ __forceinline__ void argmax_one(uint32_t c, uint32_t v, unsigned long long& best, uint32_t excl) {
+  const unsigned long long key = (c == kSent || (c & excl)) ? 0ull : (((unsigned long long)c << 32) | (unsigned long long)(~v));
   best = key > best ? key : best;
 }
 
 __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int32_t* __restrict__ dec,
                                                 uint32_t n, unsigned long long* __restrict__ keys, int j,
-                                                const uint32_t* __restrict__ tau_p1) {
+                                                const uint32_t* __restrict__ tau_p1, uint32_t excl) {
   // candidate mode: the candidate argmax already found a count >= tau_p1, which no node outside
   // the candidate list can reach (their counts started below it and only decrease)
   if (tau_p1 != nullptr && (uint32_t)(keys[j] >> 32) >= *tau_p1 && keys[j] != 0ull) return;
@@ -206,17 +208,17 @@ __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int3
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const uint32_t v = (i0 + u * stride) << 2;
-      argmax_one(x[u].x, v, best);
-      argmax_one(x[u].y, v + 1, best);
-      argmax_one(x[u].z, v + 2, best);
-      argmax_one(x[u].w, v + 3, best);
+      argmax_one(x[u].x, v, best, excl);
+      argmax_one(x[u].y, v + 1, best, excl);
+      argmax_one(x[u].z, v + 2, best, excl);
+      argmax_one(x[u].w, v + 3, best, excl);
     }
   }
   // tail (n % 4 nodes)
   for (uint32_t v = (n4 << 2) + blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
     uint32_t c = cnt[v];
     if (dec != nullptr && c != kSent && dec[v]) { c -= (uint32_t)dec[v]; dec[v] = 0; cnt[v] = c; }
-    argmax_one(c, v, best);
+    argmax_one(c, v, best, excl);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(256) k_argmax_cand(const uint32_t* __restrict_
   unsigned long long best = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
     const uint32_t v = cand[i];
-    argmax_one(cnt[v], v, best);
+    argmax_one(cnt[v], v, best, 0u);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
                                                const uint64_t* __restrict__ offsets,
                                                const uint32_t* __restrict__ pool,
                                                uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
-                                               int32_t* __restrict__ dec) {
+                                               int32_t* __restrict__ dec, MrimSel mr) {
   __shared__ uint64_t s_lo[kMaxInvSeg], s_end[kMaxInvSeg];   // list start, inclusive prefix end
   __shared__ const uint32_t* s_inv[kMaxInvSeg];
   __shared__ uint32_t s_nseg, s_limit;
@@ -423,7 +425,24 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
       s_limit = lim;
     }
   }
+  // MRIM (R27): the pick that gives round t = u / n its k-th seed closes the round: every pair of
+  // the round gets the high bit (atomicOr commutes with this kernel's decrements; counts stay
+  // < 2^31), so the argmax skips it from now on
+  __shared__ uint32_t s_close;
+  if (mr.rounds > 1u && threadIdx.x < 32) {
+    const uint32_t t = u / mr.n;
+    uint32_t picks = 0;
+    for (int q = (int)threadIdx.x; q <= j; q += 32) picks += (~(uint32_t)keys[q]) / mr.n == t;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) picks += __shfl_xor_sync(kFull, picks, off);
+    if (threadIdx.x == 0) s_close = picks == mr.k ? 1u : 0u;
+  }
   __syncthreads();
+  if (mr.rounds > 1u && s_close) {
+    const uint32_t t = u / mr.n;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < mr.n; v += gridDim.x * blockDim.x)
+      atomicOr(cnt + (uint64_t)t * mr.n + v, 0x80000000u);
+  }
   const uint32_t ns = s_nseg, limit = LIMIT ? s_limit : 0xFFFFFFFFu;
   const uint64_t total = (ns && limit) ? s_end[kMaxInvSeg - 1] : 0;   // limit 0: every set cut
   const uint64_t ngroups = (uint64_t)gridDim.x * (blockDim.x >> 3);
@@ -433,10 +452,13 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
     const uint64_t pos = s_lo[q] + (t - (q ? s_end[q - 1] : 0));
     const uint32_t r0 = s_inv[q][pos];
     const uint32_t r = LIMIT ? min(r0, limit - 1u) : r0;   // sets >= limit were truncated away
-    const uint8_t cov = covered[r];            // flag and offsets loaded together
-    const uint64_t a = offsets[r], b = offsets[r + 1];
+    // MRIM: entry r is round r mod T of MRIM set r / T, whose T rounds are consecutive sets
+    const uint32_t ci = mr.rounds > 1u ? r / mr.rounds : r;
+    const uint8_t cov = covered[ci];           // flag and offsets loaded together
+    const uint64_t a = offsets[mr.rounds > 1u ? ci * mr.rounds : r];
+    const uint64_t b = offsets[mr.rounds > 1u ? ci * mr.rounds + mr.rounds : r + 1];
     if (cov || (LIMIT && r0 != r)) continue;
-    if (sub == 0) covered[r] = 1;      // each r appears once across the lists of u: no race
+    if (sub == 0) covered[ci] = 1;     // each set appears once across the lists of u: no race
     // members: kCoverIlp loads in flight per lane (big sets would otherwise serialise one L2
     // round trip per 8 members), then fire-and-forget decrements; u itself is skipped
     for (uint64_t e = a + sub; e < b; e += 8 * kCoverIlp) {
@@ -517,8 +539,8 @@ cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* de
 }
 
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
-                          const uint32_t* tau_p1, int grid, cudaStream_t s) {
-  k_argmax<<<grid, 256, 0, s>>>(cnt, dec, n, keys, j, tau_p1);
+                          const uint32_t* tau_p1, int grid, cudaStream_t s, bool excl) {
+  k_argmax<<<grid, 256, 0, s>>>(cnt, dec, n, keys, j, tau_p1, excl ? 0x80000000u : 0u);
   return cudaGetLastError();
 }
 
@@ -540,9 +562,11 @@ cudaError_t launch_argmax_cand(const uint32_t* cnt, const uint32_t* cand, const 
 
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,
                          const uint64_t* offsets, const uint32_t* pool,
-                         uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s, bool limit) {
-  if (limit) k_cover<true><<<grid, 256, 0, s>>>(keys, j, segs, nseg, offsets, pool, covered, cnt, dec);
-  else k_cover<false><<<grid, 256, 0, s>>>(keys, j, segs, nseg, offsets, pool, covered, cnt, dec);
+                         uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s, bool limit,
+                         const MrimSel* mr) {
+  const MrimSel m = mr ? *mr : MrimSel{1u, 0u, 0u};
+  if (limit) k_cover<true><<<grid, 256, 0, s>>>(keys, j, segs, nseg, offsets, pool, covered, cnt, dec, m);
+  else k_cover<false><<<grid, 256, 0, s>>>(keys, j, segs, nseg, offsets, pool, covered, cnt, dec, m);
   return cudaGetLastError();
 }
 

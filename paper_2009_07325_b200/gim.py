@@ -72,6 +72,7 @@ SIGNATURES = {
     "gim_get_stats": (_i32, [_p, ctypes.POINTER(StatsC)]),
     "gim_reset_stats": (_i32, [_p]),
     "gim_microbench_philox": (_i32, [_p, _u64, ctypes.POINTER(_dbl)]),
+    "gim_set_rounds": (_i32, [_p, _u32]),
 }
 
 _lib_handle = None
@@ -131,6 +132,7 @@ class Gim:
             raise GimError(st, "gim_create failed (no usable CUDA device?)")
         self._h = h
         self.device = device
+        self.rounds = 1                      # MRIM rounds T (gim_set_rounds)
         if torch_allocator:
             self._use_torch_allocator(device)
 
@@ -188,15 +190,20 @@ class Gim:
     def generate_rr(self, theta: int, seed: int):
         self._check(self._lib.gim_generate_rr(self._h, theta, seed))
 
+    def set_rounds(self, rounds: int):
+        """MRIM mode (readings R26-R28): T rounds; select/imm then return k*T pair ids t*n + u."""
+        self._check(self._lib.gim_set_rounds(self._h, rounds))
+        self.rounds = rounds
+
     def select(self, k: int):
-        seeds = np.zeros(k, dtype=np.uint32)
-        gains = np.zeros(k, dtype=np.uint64)
+        seeds = np.zeros(k * self.rounds, dtype=np.uint32)
+        gains = np.zeros(k * self.rounds, dtype=np.uint64)
         cov = np.zeros(1, dtype=np.uint64)
         self._check(self._lib.gim_select(self._h, k, _ptr(seeds), _ptr(gains), _ptr(cov)))
         return seeds, gains, int(cov[0])
 
     def imm(self, k: int, eps: float, ell: float, seed: int) -> ImmResult:
-        seeds = np.zeros(k, dtype=np.uint32)
+        seeds = np.zeros(k * self.rounds, dtype=np.uint32)
         r = ImmResultC()
         self._check(self._lib.gim_imm(self._h, k, eps, ell, seed, _ptr(seeds), ctypes.byref(r)))
         nr = int(r.rounds)

@@ -98,6 +98,15 @@ def test_mrim_sets_equal_bruteforce(model, T):
         assert np.array_equal(cnt, np.bincount(pairs.astype(np.int64), minlength=g.n * T))
 
 
+def test_mrim_set_alone_equals_pool():
+    g = gi.random_small(9, 30, 0)
+    o = oracle.Oracle(g, gi.IC, gi.W_WC)
+    o.mrim_generate(50, 4, SEED)
+    off, pairs, _ = o.mrim_export()
+    for i in range(50):
+        assert o.mrim_set(SEED, i, 4).tolist() == pairs[off[i]:off[i + 1]].tolist()
+
+
 def test_mrim_extend_truncate_reseed():
     g = gi.random_small(7, 14, 3)
     o = oracle.Oracle(g, gi.IC, gi.W_WC)

@@ -5,6 +5,7 @@ gpurun_out/sweep_<name>.jsonl.
   python tools/sweep.py density      # BA n=10^6, r = 2..32, k=50, eps=0.05
   python tools/sweep.py k            # C3 (IC) and C4 (LT), k = 1..200, eps=0.1
   python tools/sweep.py eps          # C3, eps = 0.05..0.5, k=50
+  python tools/sweep.py mrim         # MRIM k=10, T=5, eps=0.1 on C2/C3/C4 (Table 3)
 """
 import json
 import os
@@ -17,6 +18,10 @@ POINTS = {
     "k": [["--workload", wl, "--k", str(k), "--no-cpu-baseline"]
           for wl in ("C3", "C4") for k in (1, 10, 25, 50, 100, 200)],
     "eps": [["--workload", "C3", "--eps", str(e), "--no-cpu-baseline"] for e in (0.05, 0.1, 0.2, 0.3, 0.5)],
+    # MRIM (CR-NAIMM, §4.8 Table 3 settings: k = 10, T = 5, eps = 0.1)
+    "mrim": [["--workload", "C2", "--k", "10", "--rounds", "5", "--cpu-seconds", "8"],
+             ["--workload", "C3", "--k", "10", "--rounds", "5", "--cpu-seconds", "8"],
+             ["--workload", "C4", "--k", "10", "--rounds", "5", "--no-cpu-baseline"]],
 }
 
 

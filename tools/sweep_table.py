@@ -18,7 +18,9 @@ def main():
            "after 3 warm-ups, graph resident; `cpu` = the oracle's RR sets/s on one host core, bounded",
            "sample). Reproduces the *shape* of the paper's Figs. 4-7 (P:716-779) on synthetic inputs.", ""]
     for name, title in (("density", "Density sweep: Barabasi-Albert n = 10^6, IC-WC, k = 50, eps = 0.05 (P:754-779)"),
-                        ("k", "k sweep, eps = 0.1 (P:744-748)"), ("eps", "eps sweep, C3, k = 50 (P:750)")):
+                        ("k", "k sweep, eps = 0.1 (P:744-748)"), ("eps", "eps sweep, C3, k = 50 (P:750)"),
+                        ("mrim", "MRIM (CR-NAIMM, Table 3 settings k = 10 per round, T = 5, eps = 0.1; "
+                                 "sets = MRIM sets of T reverse BFS each; P:790-822)")):
         rs = rows(name)
         if not rs:
             continue

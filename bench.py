@@ -371,7 +371,8 @@ def run_gim(args, w):
                 "phase_ms_per_step": phases,
                 "rr_stats": {"mean_len": st["rr_elements"] / max(st["rr_sets"], 1),
                              "coins_per_set": (st["coins"] + st["coins_giant"]) / max(st["rr_sets"], 1),
-                             "giant_frac": st["giant_sets"] / max(st["rr_sets"], 1)},
+                             "giant_frac": st["giant_sets"] / max(st["rr_sets"], 1),
+                             "coins_per_giant_set": st["coins_giant"] / max(st["giant_sets"], 1)},
                 "gpu_launches": st["launches"],
                 "step_wall_ms": [round(x, 3) for x in step_wall],
                 "host": {"api_ms_per_step": st["host_ms_api"] / args.steps,

@@ -139,6 +139,17 @@ gim_status gim_rr_export(gim_ctx* ctx, uint64_t* n_sets, uint64_t* pool_len, uin
  * (Occur). */
 gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
 
+/* Forward Monte-Carlo spread (verification at scale; IC only): `trials` independent instance
+ * graphs of the IC process, each newly active node trying each out-edge once; the
+ * coin of out-slot e (out-CSR rows sorted by (source, in-slot)) in trial t is word (e & 3) of
+ * Philox(mc_seed; t, tag 11 | e >> 2) — independent of every RR stream. mean_out = mean number
+ * of activated nodes (seeds included, duplicates once), stderr_out (nullable) its standard error,
+ * sizes_out[trials] (nullable) the per-trial counts. Builds the out-CSR on first use. Compared
+ * with n * F_R'(S) on an independent RR pool it checks Eq. 3 at full size.
+ * Errors: GIM_ESTATE (no graph), GIM_EINVAL (LT model, k == 0, trials == 0, seed >= n). */
+gim_status gim_mc_spread(gim_ctx* ctx, const uint32_t* seeds, uint32_t k, uint64_t trials, uint64_t mc_seed,
+                         double* mean_out, double* stderr_out, uint32_t* sizes_out);
+
 /* Multi-round IM (MRIM), the CR-NAIMM algorithm as gIM adapts it (§4.8: "after
  * selecting a random node, we initiate a random BFS originating from the selected node as many
  * times as the number of rounds. Also, each element in a random RR set is a tuple of node-id and
@@ -179,6 +190,12 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                          second stream while a round's NodeSelection runs (capped at the
  *                          largest theta the LB test can yield; excess is truncated). Results
  *                          are identical; measured slower on C4 and neutral on C3.
+ *  GIM_OPT_PDL          = 0 (default) / 1: launch the argmax / cover kernels of the greedy steps
+ *                         with programmatic dependent launch (each kernel's CTAs become resident
+ *                         while its predecessor runs and wait for its results). Process-wide.
+ *  GIM_OPT_GIANT_NT     = 0 (default, auto) / 256 / 128: threads per giant-set CTA of the
+ *                         block-per-RR fallback (auto: 128 when the previous chunk produced >= 12
+ *                         giant sets per 256-thread slot, else 256).
  *  GIM_OPT_MB_CHAINS    = 1 / 4 / 8 (default 8): interleaved Philox chains per thread in
  *                          gim_microbench_philox. */
 typedef enum {
@@ -191,7 +208,9 @@ typedef enum {
   GIM_OPT_ARGMAX_CAND = 8,
   GIM_OPT_IC_LANE = 9,
   GIM_OPT_SPECULATE = 10,
-  GIM_OPT_MB_CHAINS = 11
+  GIM_OPT_MB_CHAINS = 11,
+  GIM_OPT_PDL = 12,
+  GIM_OPT_GIANT_NT = 13
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

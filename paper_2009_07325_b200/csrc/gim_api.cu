@@ -30,6 +30,10 @@ struct Seg {
 enum { CLS_RR = 0, CLS_GIANT, CLS_STORE, CLS_INV, CLS_SELECT, CLS_N };
 
 constexpr uint32_t kChunk = 1u << 22;   // RR ids per generation chunk (bounds staging)
+#ifndef GIM_ARGMAX_CTAS
+#define GIM_ARGMAX_CTAS 4
+#endif
+constexpr int kArgmaxCtasPerSM = GIM_ARGMAX_CTAS;   // k_argmax grid = this x #SMs (256 threads each)
 
 
 }  // namespace
@@ -57,6 +61,8 @@ struct gim_ctx {
   float p_uniform = 0.f;
   uint64_t thr_uniform = 0;
   DevBuf row_ptr, src, thr_edge;
+  DevBuf out_ptr, out_dst, out_in, thr_wc;   // out-CSR for gim_mc_spread (built on first use)
+  bool out_valid = false;
   // MRIM (readings R26-R28): rounds T; pair ids t*n + u index the count / index / selection
   // arrays (n*T of them); the T rounds of MRIM set i are the consecutive standard ids i*T + t
   uint32_t rounds = 1;
@@ -73,6 +79,9 @@ struct gim_ctx {
   DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr, dump, lt_spill, esc_list;
   DevBuf bitmaps, gqueues;
   uint32_t giant_slots = 0;
+  uint32_t giant_n = 0;             // n the giant slots were sized for (reused while n <= giant_n)
+  int giant_nt_opt = 0;             // GIM_OPT_GIANT_NT: 0 auto, else threads per giant CTA
+  double giant_per_slot = 0.0;      // giant sets per default slot in the previous chunk
   bool giant_cap_reached = false;
   uint64_t stage_cap = 0;
   GenCounters* h_ctr = nullptr;   // pinned
@@ -321,6 +330,7 @@ gim_status ensure_giant_slots(gim_ctx* c, uint32_t want) {
   TRY(dalloc(c, c->gqueues, (uint64_t)c->n * 4 * slots));
   CK(cudaMemsetAsync(c->gqueues.p, 0xFF, (uint64_t)c->n * 4 * slots, c->stream));   // kEmpty
   c->giant_slots = slots;
+  c->giant_n = c->n;
   return GIM_OK;
 }
 
@@ -399,7 +409,12 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     TRY(ensure(c, c->lt_spill, (uint64_t)rr_grid * kLtWarps * (kLtCap2 - kLtCap) * 32 * 4));
     p.lt_spill = c->lt_spill.as<uint32_t>();
   }
-  TRY(ensure_giant_slots(c, (uint32_t)kGiantBlocksPerSM * (uint32_t)c->num_sms));
+  // giant CTA width: narrow (more sets in flight) when the previous chunk had many giant sets
+  // per default slot — dense graphs, where K-GIANT otherwise dominates
+  const int giant_nt = c->giant_nt_opt ? c->giant_nt_opt
+                                       : (c->giant_per_slot >= 12.0 ? kGiantThreadsNarrow : kGiantThreads);
+  const uint32_t giant_grid = (uint32_t)(1024 / giant_nt) * (uint32_t)c->num_sms;
+  TRY(ensure_giant_slots(c, giant_grid));
   const uint64_t bm_words = ((uint64_t)c->n + 31) / 32;
   // warp kernel, then the giant kernel unconditionally (it reads the giant count on the device
   // and exits at once when there is none), then the size scan: one host sync per chunk.
@@ -431,8 +446,9 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     }
     {
       Prof pf(c, CLS_GIANT);
-      TRY(launched(c, launch_rr_giant(c->model, c->scheme, pp, (int)c->giant_slots, c->bitmaps.as<uint32_t>(),
-                                      c->gqueues.as<uint32_t>(), bm_words, c->stream), "k_rr_giant"));
+      TRY(launched(c, launch_rr_giant(c->model, c->scheme, pp, (int)std::min(c->giant_slots, giant_grid),
+                                      c->bitmaps.as<uint32_t>(), c->gqueues.as<uint32_t>(), bm_words,
+                                      c->stream, giant_nt), "k_rr_giant"));
       c->st.n_giant_launches++;
     }
     return GIM_OK;
@@ -449,6 +465,8 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   CK(cudaMemcpyAsync(c->h_u64, c->scan_out.as<uint64_t>() + cnt, 8, cudaMemcpyDeviceToHost, c->stream));
   TRY(read_ctr(c));
   c->st.giant_sets += c->h_ctr->giant_count;
+  if (cnt >= 4096)
+    c->giant_per_slot = (double)c->h_ctr->giant_count / ((double)kGiantBlocksPerSM * (double)c->num_sms);
   for (int iter = 0; c->h_ctr->retry_count; ++iter) {
     if (iter > 40) return fail(c, GIM_ENOMEM, "staging retry loop did not converge");
     // staging overflow: grow (keep the part already written) and redo the failed items
@@ -646,7 +664,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
       CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
       for (uint32_t j = 0; j < kk; ++j) {
         if (cand) launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream);
-        launch_argmax(c->cnt.as<uint32_t>(), nullptr, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * 4, c->stream,
+        launch_argmax(c->cnt.as<uint32_t>(), nullptr, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * kArgmaxCtasPerSM, c->stream,
                       mr != nullptr);
         launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                      c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * 8, c->stream,
@@ -666,7 +684,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
         Prof pf(c, CLS_SELECT);
         if (cand) TRY(launched(c, launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream),
                                "k_argmax_cand"));
-        TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * 4,
+        TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * kArgmaxCtasPerSM,
                                       c->stream, mr != nullptr), "k_argmax"));
         TRY(launched(c, launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                                      c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * 8,
@@ -803,7 +821,8 @@ void gim_destroy(gim_ctx* c) {
   DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
                     &c->sizes, &c->soff, &c->giant_list, &c->retry_list, &c->item_list, &c->scan_out,
                     &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
-                    &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand};
+                    &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
+                    &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc};
   for (auto& sg : c->iseg) {
     dfree(c, sg.off);
     dfree(c, sg.inv);
@@ -862,11 +881,21 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
   dfree(c, c->row_ptr);
   dfree(c, c->src);
   dfree(c, c->thr_edge);
-  dfree(c, c->bitmaps);
-  dfree(c, c->gqueues);
-  c->giant_slots = 0;
-  c->giant_cap_reached = false;
+  // giant slots (bitmaps all zero, queues all kEmpty: K-GIANT restores both after every set) are
+  // kept for a graph that is not larger, so reloading a graph does not re-clear gigabytes
+  if (n > c->giant_n) {
+    dfree(c, c->bitmaps);
+    dfree(c, c->gqueues);
+    c->giant_slots = 0;
+    c->giant_n = 0;
+    c->giant_cap_reached = false;
+  }
   c->graph = false;
+  c->out_valid = false;
+  dfree(c, c->out_ptr);
+  dfree(c, c->out_dst);
+  dfree(c, c->out_in);
+  dfree(c, c->thr_wc);
   c->n = n;
   c->m = m;
   c->model = model;
@@ -1081,6 +1110,71 @@ gim_status gim_set_rounds(gim_ctx* c, uint32_t rounds) {
   return GIM_OK;
 }
 
+gim_status gim_mc_spread(gim_ctx* c, const uint32_t* seeds, uint32_t k, uint64_t trials, uint64_t mc_seed,
+                         double* mean_out, double* stderr_out, uint32_t* sizes_out) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
+  if (c->model != GIM_IC) return fail(c, GIM_EINVAL, "forward Monte-Carlo is implemented for IC only");
+  if (!seeds || k < 1 || trials < 1 || !mean_out) return fail(c, GIM_EINVAL, "seeds, k >= 1, trials >= 1, mean_out required");
+  for (uint32_t i = 0; i < k; ++i)
+    if (seeds[i] >= c->n) return fail(c, GIM_EINVAL, "seed id out of range");
+  DeviceGuard g(c->device);
+  const uint64_t n = c->n, m = c->m;
+  const int grid = c->num_sms * 8;
+  if (!c->out_valid) {                          // out-CSR: once per graph
+    TRY(dalloc(c, c->out_ptr, (n + 1) * 4));
+    TRY(dalloc(c, c->out_dst, (m + 4) * 4));
+    TRY(dalloc(c, c->out_in, (m + 4) * 4));
+    TRY(dalloc(c, c->thr_wc, (m + 4) * 4));    // groups of 4 are read as one uint4
+    TRY(ensure(c, c->scan_tmp, (scan_tiles(n) + 2) * 8));
+    size_t tb = 0;
+    CK(build_out_csr(nullptr, nullptr, c->n, m, c->scheme, nullptr, nullptr, nullptr, nullptr, nullptr, &tb,
+                     nullptr, grid, c->stream));
+    DevBuf tmp;
+    TRY(dalloc(c, tmp, tb));
+    const cudaError_t e = build_out_csr(c->row_ptr.as<uint32_t>(), c->src.as<uint32_t>(), c->n, m, c->scheme,
+                                        c->out_ptr.as<uint32_t>(), c->out_dst.as<uint32_t>(), c->out_in.as<uint32_t>(),
+                                        c->thr_wc.as<uint32_t>(), tmp.p, &tb, c->scan_tmp.as<uint64_t>(), grid,
+                                        c->stream);
+    dfree(c, tmp);
+    if (e != cudaSuccess) return fail_cuda(c, "build_out_csr", e);
+    c->out_valid = true;
+  }
+  TRY(ensure_giant_slots(c, 2u * (uint32_t)c->num_sms));   // one MC trial per slot at a time
+  const uint32_t mc_grid = std::min<uint32_t>(c->giant_slots, 2u * (uint32_t)c->num_sms);
+  DevBuf dseeds, dsizes, dclaim;
+  TRY(dalloc(c, dseeds, (uint64_t)k * 4));
+  TRY(dalloc(c, dsizes, trials * 4));
+  TRY(dalloc(c, dclaim, 8));
+  CK(cudaMemcpyAsync(dseeds.p, seeds, (uint64_t)k * 4, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(dclaim.p, 0, 8, c->stream));
+  const uint64_t bm_words = (n + 31) / 32;
+  TRY(launched(c, launch_mc_ic(c->scheme, c->n, c->out_ptr.as<uint32_t>(), c->out_dst.as<uint32_t>(),
+                               c->out_in.as<uint32_t>(), c->thr_wc.as<uint32_t>(), c->thr_edge.as<uint64_t>(),
+                               c->thr_uniform, dseeds.as<uint32_t>(), k, trials, mc_seed,
+                               dclaim.as<unsigned long long>(), dsizes.as<uint32_t>(), c->bitmaps.as<uint32_t>(),
+                               c->gqueues.as<uint32_t>(), bm_words, (int)mc_grid, c->stream), "k_mc_ic"));
+  std::vector<uint32_t> sz(trials);
+  CK(cudaMemcpyAsync(sz.data(), dsizes.p, trials * 4, cudaMemcpyDeviceToHost, c->stream));
+  TRY(sync(c));
+  dfree(c, dseeds);
+  dfree(c, dsizes);
+  dfree(c, dclaim);
+  // mean and standard error in trial order, the oracle's expressions (og_mc_spread)
+  double sum = 0.0, sum2 = 0.0;
+  for (uint64_t t = 0; t < trials; ++t) {
+    sum += (double)sz[t];
+    sum2 += (double)sz[t] * (double)sz[t];
+  }
+  const double mean = sum / (double)trials;
+  const double var = sum2 / (double)trials - mean * mean;
+  *mean_out = mean;
+  if (stderr_out) *stderr_out = std::sqrt((var > 0 ? var : 0) / (double)trials);
+  if (sizes_out) std::memcpy(sizes_out, sz.data(), trials * 4);
+  return GIM_OK;
+}
+
 gim_status gim_counts_export(gim_ctx* c, uint32_t* count_out) {
   if (!c) return GIM_EINVAL;
   c->err.clear();
@@ -1105,6 +1199,16 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_INV_SEGMENTS: c->inv_segmented = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_MB_CHAINS: c->mb_chains = (int)value; return GIM_OK;
     case GIM_OPT_SPECULATE: c->speculate = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_GIANT_NT:
+      if (value != 0 && value != kGiantThreads && value != kGiantThreadsNarrow)
+        return fail(c, GIM_EINVAL, "giant CTA width must be 0 (auto), 256 or 128");
+      c->giant_nt_opt = (int)value;
+      return GIM_OK;
+    case GIM_OPT_PDL:
+      set_pdl((int)value);
+      if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);   // recapture with the new launch mode
+      c->sel_exec = nullptr;
+      return GIM_OK;
     case GIM_OPT_IC_LANE: c->ic_lane = (value < -1 || value > 1) ? -1 : (int)value; return GIM_OK;
     case GIM_OPT_ARGMAX_CAND: c->use_cand = (value < 0 || value > 2) ? 1 : (int)value; return GIM_OK;
     case GIM_OPT_STAGING_CAP:

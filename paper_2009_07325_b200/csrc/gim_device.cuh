@@ -188,6 +188,9 @@ static_assert((kHubGroups & (kHubGroups - 1u)) == 0u, "hub steps are split off w
 #endif
 constexpr int kGiantThreads = GIM_GIANT_THREADS;              // warps of one giant set = this / 32
 constexpr int kGiantBlocksPerSM = 1024 / GIM_GIANT_THREADS;   // giant sets in flight per SM
+// Narrow giant CTAs (8 giant sets in flight per SM, 4 warps each) for chunks with many giant sets
+// per slot (dense graphs: BA r >= 16); chosen per chunk from the previous chunk's giant count.
+constexpr int kGiantThreadsNarrow = 128;
 #ifndef GIM_CLAIM_BATCH
 #define GIM_CLAIM_BATCH 1
 #endif

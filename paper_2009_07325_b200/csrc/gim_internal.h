@@ -10,7 +10,7 @@ int lt_blocks_per_sm();
 cudaError_t launch_rr_ic_lane(int scheme, const RRParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rr_warp(int model, int scheme, const RRParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
-                            uint32_t* gqueues, uint64_t bm_words, cudaStream_t s);
+                            uint32_t* gqueues, uint64_t bm_words, cudaStream_t s, int nt);
 cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const uint64_t* soff,
                          const uint64_t* scan, uint32_t count, uint64_t pool_base, uint32_t* pool,
                          uint64_t* offsets_out, uint32_t* count_total, uint32_t rounds, uint32_t round0,
@@ -22,6 +22,7 @@ cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* si
                                 int chains);
 
 uint64_t scan_tiles(uint64_t count);
+void set_pdl(int on);   // programmatic dependent launch of the selection kernels (GIM_OPT_PDL)
 cudaError_t launch_scan_u32(const uint32_t* in, uint64_t count, uint64_t* out, uint64_t* tile_tmp,
                             uint64_t* total_tmp, cudaStream_t s, int* launches);
 // same, 32-bit output (the caller guarantees the total is < 2^32)
@@ -51,4 +52,13 @@ cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev*
                          bool limit, const MrimSel* mr = nullptr);
 cudaError_t launch_validate_csr(const uint64_t* rp64, uint32_t n, uint64_t m, const uint32_t* src,
                                 uint32_t* rp32, uint32_t* err, uint32_t* bad_row, int grid, cudaStream_t s);
+// forward Monte-Carlo (mc.cu)
+cudaError_t build_out_csr(const uint32_t* row_ptr, const uint32_t* src, uint32_t n, uint64_t m, int scheme,
+                          uint32_t* out_ptr, uint32_t* out_dst, uint32_t* out_in, uint32_t* thr_wc,
+                          void* tmp, size_t* tmp_bytes, uint64_t* scan_tmp, int grid, cudaStream_t s);
+cudaError_t launch_mc_ic(int scheme, uint32_t n, const uint32_t* out_ptr, const uint32_t* out_dst,
+                         const uint32_t* out_in, const uint32_t* thr_wc, const uint64_t* thr_edge,
+                         uint64_t thr_uniform, const uint32_t* seeds, uint32_t k, uint64_t trials, uint64_t mc_seed,
+                         unsigned long long* claim, uint32_t* sizes, uint32_t* bitmaps, uint32_t* queues,
+                         uint64_t bm_words, int grid, cudaStream_t s);
 }  // namespace gim

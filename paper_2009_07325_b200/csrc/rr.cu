@@ -833,7 +833,6 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
 constexpr uint32_t kSplitGroups = 2048;   // hub nodes above this are split across warps
 constexpr uint32_t kChunkRing = 128;      // shared ring of published hub chunks
 constexpr uint32_t kBusySlot = 0xFFFFFFFEu; // ring slot being written (node ids are < 2^32 - 2)
-constexpr uint32_t kGiantWarps = kGiantThreads / 32;
 #ifndef GIM_GIANT_DIV
 #define GIM_GIANT_DIV 4
 #endif
@@ -847,8 +846,8 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* ptr) {
   return v;
 }
 
-template <int MODEL, int SCHEME>
-__global__ void __launch_bounds__(kGiantThreads, kGiantBlocksPerSM) k_rr_giant(RRParams p, uint32_t* bitmaps,
+template <int MODEL, int SCHEME, int kGiantThreads>
+__global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_giant(RRParams p, uint32_t* bitmaps,
                                                                uint32_t* gqueues, uint64_t bm_words) {
   __shared__ uint32_t s_head, s_tail, s_busy, s_r;
   __shared__ uint32_t s_chead, s_cres;           // hub-chunk ring: claimed / reserved counters
@@ -879,6 +878,7 @@ __global__ void __launch_bounds__(kGiantThreads, kGiantBlocksPerSM) k_rr_giant(R
   };
   // IC: live in-edges of a claimed batch, resolved together (as in K-RR): cp.async of src[e]
   // into pend[], then one wait, bitmap test-and-set and append per 32 entries
+  constexpr uint32_t kGiantWarps = kGiantThreads / 32;
   __shared__ uint32_t s_pend[kGiantWarps][kPend];
   uint32_t* pend = s_pend[threadIdx.x >> 5];
   const uint32_t pend_s = (uint32_t)__cvta_generic_to_shared(pend);
@@ -1271,17 +1271,26 @@ cudaError_t launch_rr_warp(int model, int scheme, const RRParams& p, int grid, c
   return launch_rr_lt(scheme, p, grid, s);
 }
 
-cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
-                            uint32_t* gqueues, uint64_t bm_words, cudaStream_t s) {
+template <int NT>
+cudaError_t launch_rr_giant_nt(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
+                               uint32_t* gqueues, uint64_t bm_words, cudaStream_t s) {
   if (model == MODEL_IC) {
-    if (scheme == W_WC) k_rr_giant<MODEL_IC, W_WC><<<grid, kGiantThreads, 0, s>>>(p, bitmaps, gqueues, bm_words);
-    else if (scheme == W_UNIFORM) k_rr_giant<MODEL_IC, W_UNIFORM><<<grid, kGiantThreads, 0, s>>>(p, bitmaps, gqueues, bm_words);
-    else k_rr_giant<MODEL_IC, W_EXPLICIT><<<grid, kGiantThreads, 0, s>>>(p, bitmaps, gqueues, bm_words);
+    if (scheme == W_WC) k_rr_giant<MODEL_IC, W_WC, NT><<<grid, NT, 0, s>>>(p, bitmaps, gqueues, bm_words);
+    else if (scheme == W_UNIFORM) k_rr_giant<MODEL_IC, W_UNIFORM, NT><<<grid, NT, 0, s>>>(p, bitmaps, gqueues, bm_words);
+    else k_rr_giant<MODEL_IC, W_EXPLICIT, NT><<<grid, NT, 0, s>>>(p, bitmaps, gqueues, bm_words);
   } else {
-    if (scheme == W_WC) k_rr_giant<MODEL_LT, W_WC><<<grid, kGiantThreads, 0, s>>>(p, bitmaps, gqueues, bm_words);
-    else k_rr_giant<MODEL_LT, W_EXPLICIT><<<grid, kGiantThreads, 0, s>>>(p, bitmaps, gqueues, bm_words);
+    if (scheme == W_WC) k_rr_giant<MODEL_LT, W_WC, NT><<<grid, NT, 0, s>>>(p, bitmaps, gqueues, bm_words);
+    else k_rr_giant<MODEL_LT, W_EXPLICIT, NT><<<grid, NT, 0, s>>>(p, bitmaps, gqueues, bm_words);
   }
   return cudaGetLastError();
+}
+
+// nt = threads per giant set: kGiantThreads (default) or kGiantThreadsNarrow (many giant sets)
+cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
+                            uint32_t* gqueues, uint64_t bm_words, cudaStream_t s, int nt) {
+  if (nt == kGiantThreadsNarrow)
+    return launch_rr_giant_nt<kGiantThreadsNarrow>(model, scheme, p, grid, bitmaps, gqueues, bm_words, s);
+  return launch_rr_giant_nt<kGiantThreads>(model, scheme, p, grid, bitmaps, gqueues, bm_words, s);
 }
 
 cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const uint64_t* soff,

@@ -162,6 +162,13 @@ __global__ void __launch_bounds__(256) k_count_delta(const uint32_t* __restrict_
 // all-reduced decrements of the previous step first (P > 1) and retires the previous pick.
 // Streams count as uint4 (4 nodes per load) with 4 independent loads in flight per thread.
 // ------------------------------------------------------------------------------------------
+// Programmatic dependent launch (the greedy steps' argmax/cover chain): a kernel lets the next
+// one in the stream launch at once (its CTAs become resident and wait) and itself waits for the
+// previous kernel's results before touching them, so the 2k dependent launches of a selection
+// do not pay a launch gap each. Both are no-ops without a programmatic predecessor/successor.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // excl = 0x80000000 in MRIM mode: pairs of a round that already has its k seeds carry the high
 // bit (set by k_cover) and are skipped like selected ones; 0 otherwise.
 __device__ __forceinline__ void argmax_one(uint32_t c, uint32_t v, unsigned long long& best, uint32_t excl) {
@@ -172,6 +179,8 @@ __device__ __forceinline__ void argmax_one(uint32_t c, uint32_t v, unsigned long
 __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int32_t* __restrict__ dec,
                                                 uint32_t n, unsigned long long* __restrict__ keys, int j,
                                                 const uint32_t* __restrict__ tau_p1, uint32_t excl) {
+  pdl_wait();
+  pdl_trigger();
   // candidate mode: the candidate argmax already found a count >= tau_p1, which no node outside
   // the candidate list can reach (their counts started below it and only decrease)
   if (tau_p1 != nullptr && (uint32_t)(keys[j] >> 32) >= *tau_p1 && keys[j] != 0ull) return;
@@ -347,6 +356,8 @@ __global__ void __launch_bounds__(256) k_argmax_cand(const uint32_t* __restrict_
                                                      const unsigned int* __restrict__ ncand,
                                                      unsigned long long* __restrict__ keys, int j) {
   __shared__ unsigned long long s_best[8];
+  pdl_wait();
+  pdl_trigger();
   const uint32_t nc = *ncand;
   unsigned long long best = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
@@ -395,6 +406,8 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
   __shared__ const uint32_t* s_inv[kMaxInvSeg];
   __shared__ uint32_t s_nseg, s_limit;
   const uint32_t sub = threadIdx.x & 7;
+  pdl_wait();
+  pdl_trigger();
   const uint32_t u = ~(uint32_t)keys[j];
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[u] = kSent;   // retire the pick (never decremented)
   if (threadIdx.x < 32) {                     // lanes load the segments' list bounds in parallel
@@ -478,6 +491,9 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
 // ------------------------------------------------------------------------------------------
 // Host launch wrappers
 // ------------------------------------------------------------------------------------------
+int g_pdl = 0;   // GIM_OPT_PDL (process-wide: the launch wrappers carry no ctx)
+void set_pdl(int on) { g_pdl = on ? 1 : 0; }
+
 uint64_t scan_tiles(uint64_t count) { return (count + kScanTile - 1) / kScanTile; }
 
 template <class OutT>
@@ -538,10 +554,25 @@ cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* de
   return cudaGetLastError();
 }
 
+// Launch with programmatic stream serialization (see pdl_wait / pdl_trigger).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
                           const uint32_t* tau_p1, int grid, cudaStream_t s, bool excl) {
-  k_argmax<<<grid, 256, 0, s>>>(cnt, dec, n, keys, j, tau_p1, excl ? 0x80000000u : 0u);
-  return cudaGetLastError();
+  return launch_pdl(k_argmax, grid, 256, s, cnt, dec, n, keys, j, tau_p1, excl ? 0x80000000u : 0u);
 }
 
 cudaError_t launch_cand_setup(const uint32_t* cnt, uint32_t n, uint32_t kmax, unsigned int* hist,
@@ -556,8 +587,7 @@ cudaError_t launch_cand_setup(const uint32_t* cnt, uint32_t n, uint32_t kmax, un
 
 cudaError_t launch_argmax_cand(const uint32_t* cnt, const uint32_t* cand, const unsigned int* ncand,
                                unsigned long long* keys, int j, int grid, cudaStream_t s) {
-  k_argmax_cand<<<grid, 256, 0, s>>>(cnt, cand, ncand, keys, j);
-  return cudaGetLastError();
+  return launch_pdl(k_argmax_cand, grid, 256, s, cnt, cand, ncand, keys, j);
 }
 
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,
@@ -565,9 +595,8 @@ cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev*
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s, bool limit,
                          const MrimSel* mr) {
   const MrimSel m = mr ? *mr : MrimSel{1u, 0u, 0u};
-  if (limit) k_cover<true><<<grid, 256, 0, s>>>(keys, j, segs, nseg, offsets, pool, covered, cnt, dec, m);
-  else k_cover<false><<<grid, 256, 0, s>>>(keys, j, segs, nseg, offsets, pool, covered, cnt, dec, m);
-  return cudaGetLastError();
+  if (limit) return launch_pdl(k_cover<true>, grid, 256, s, keys, j, segs, nseg, offsets, pool, covered, cnt, dec, m);
+  return launch_pdl(k_cover<false>, grid, 256, s, keys, j, segs, nseg, offsets, pool, covered, cnt, dec, m);
 }
 
 }  // namespace gim

@@ -24,7 +24,7 @@ LIB_PATH = os.environ.get("GIM_LIB_PATH") or os.path.join(_HERE, "libgim.so")
 GIM_OK, GIM_EINVAL, GIM_ESTATE, GIM_ENOMEM, GIM_ECUDA, GIM_ECOLL, GIM_ELTWEIGHT = range(7)
 IC, LT = 0, 1
 W_EXPLICIT, W_WC, W_UNIFORM = 0, 1, 2
-OPT_FORCE_GIANT, OPT_QUEUE_CAP, OPT_PROFILE, OPT_STAGING_CAP, OPT_SELECT_GRAPH, OPT_INV_SEGMENTS, OPT_ARGMAX_CAND, OPT_IC_LANE, OPT_SPECULATE, OPT_MB_CHAINS = 1, 2, 3, 4, 6, 7, 8, 9, 10, 11
+OPT_FORCE_GIANT, OPT_QUEUE_CAP, OPT_PROFILE, OPT_STAGING_CAP, OPT_SELECT_GRAPH, OPT_INV_SEGMENTS, OPT_ARGMAX_CAND, OPT_IC_LANE, OPT_SPECULATE, OPT_MB_CHAINS, OPT_PDL, OPT_GIANT_NT = 1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12, 13
 
 _STATUS = {0: "GIM_OK", 1: "GIM_EINVAL", 2: "GIM_ESTATE", 3: "GIM_ENOMEM", 4: "GIM_ECUDA",
            5: "GIM_ECOLL", 6: "GIM_ELTWEIGHT"}
@@ -73,6 +73,7 @@ SIGNATURES = {
     "gim_reset_stats": (_i32, [_p]),
     "gim_microbench_philox": (_i32, [_p, _u64, ctypes.POINTER(_dbl)]),
     "gim_set_rounds": (_i32, [_p, _u32]),
+    "gim_mc_spread": (_i32, [_p, _p, _u32, _u64, _u64, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl), _p]),
 }
 
 _lib_handle = None
@@ -194,6 +195,15 @@ class Gim:
         """MRIM mode (readings R26-R28): T rounds; select/imm then return k*T pair ids t*n + u."""
         self._check(self._lib.gim_set_rounds(self._h, rounds))
         self.rounds = rounds
+
+    def mc_spread(self, seeds, trials: int, mc_seed: int, return_sizes: bool = False):
+        """Forward Monte-Carlo spread of `seeds` under IC (gim_mc_spread): (mean, stderr[, sizes])."""
+        s = np.ascontiguousarray(seeds, dtype=np.uint32)
+        mean, se = _dbl(), _dbl()
+        sizes = np.zeros(trials, dtype=np.uint32) if return_sizes else None
+        self._check(self._lib.gim_mc_spread(self._h, _ptr(s), len(s), trials, mc_seed, ctypes.byref(mean),
+                                            ctypes.byref(se), _ptr(sizes)))
+        return (mean.value, se.value, sizes) if return_sizes else (mean.value, se.value)
 
     def select(self, k: int):
         seeds = np.zeros(k * self.rounds, dtype=np.uint32)

@@ -125,6 +125,24 @@ def test_pool_parity_C2_and_select(graph, segs, cand):
     assert st["rr_elements"] == len(o.export()[1])
 
 
+@pytest.mark.parametrize("pdl", [0, 1])
+def test_select_pdl_invariance(pdl):
+    """Programmatic dependent launch of the argmax/cover chain (GIM_OPT_PDL) changes no result,
+    with the CUDA-graph replay and with one-by-one launches."""
+    w = gi.WORKLOADS["C2"]
+    g = gi.workload_graph("C2")
+    o = oracle.Oracle(g, w.model, w.scheme)
+    o.generate(20011, w.rr_seed)
+    ref = o.select(50)
+    for graph in (1, 0):
+        c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_GRAPH: graph})
+        c.set_option(P.OPT_PDL, pdl)
+        c.generate_rr(20011, w.rr_seed)
+        s, gn, cov = c.select(50)
+        assert np.array_equal(s, ref[0]) and np.array_equal(gn, ref[1]) and cov == ref[2]
+    c.set_option(P.OPT_PDL, 1)
+
+
 def test_extend_truncate_reseed():
     g = gi.random_small(40, 300, 5)
     c = _ctx(g, gi.IC, gi.W_WC)

@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo + --same-device: functional multi-rank test on 1 GPU)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (functional testing)")
+    ap.add_argument("--dense-exchange", action="store_true",
+                    help="N > 1: per-step count/decrement all-reduce instead of the replicated pool")
     return ap.parse_args()
 
 
@@ -77,7 +79,9 @@ def config_of(w, world, rounds=1):
                         gi.W_EXPLICIT: "explicit"}[w.scheme],
             "generator": (f"barabasi-albert r={w.ba_r} r0={w.ba_r + 1} graph_seed={w.graph_seed}" if w.gen == "ba"
                           else f"plg gamma={w.gamma} rho={w.rho} d_cap={w.d_cap} graph_seed={w.graph_seed}"),
-            "rr_seed": w.rr_seed, "parallelism": f"dp{world} (RR-id slices, replicated graph)",
+            "rr_seed": w.rr_seed,
+            "parallelism": f"dp{world} (RR-id slices sampled per rank, replicated graph"
+                           + (", each round's sets all-gathered, NodeSelection replicated)" if world > 1 else ")"),
             "l2": "inputs larger than L2 (the graph's CSR exceeds the 126 MB L2)" if w.m > 30_000_000
             else "graph is L2-resident (no flush between steps)"}
 
@@ -226,6 +230,8 @@ def run_gim(args, w):
     if world > 1:
         ctx.set_shard(rank, world)
         ctx.set_allreduce(P.torch_allreduce())
+        if not args.dense_exchange:            # replicated pool: no per-step collectives
+            ctx.set_allgather(P.torch_allgather())
     ctx.set_option(P.OPT_PROFILE, 1)
     for o in args.opt:
         name, val = o.split("=")
@@ -324,6 +330,8 @@ def run_gim(args, w):
         if world > 1:
             ctx2.set_shard(rank, world)
             ctx2.set_allreduce(P.torch_allreduce())
+            if not args.dense_exchange:
+                ctx2.set_allgather(P.torch_allgather())
         def e2e_step():
             ctx2.load_graph(g.n, rp_h.numpy(), src_h.numpy(), w.model, w.scheme, weights=g.weights,
                             p_uniform=w.p_uniform)

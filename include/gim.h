@@ -83,6 +83,19 @@ gim_status gim_set_shard(gim_ctx* ctx, int rank, int world);
 typedef int (*gim_allreduce_fn)(void* dev_buf, uint64_t count, void* cuda_stream, void* user);
 gim_status gim_set_allreduce(gim_ctx* ctx, gim_allreduce_fn fn, void* user);
 
+/* All-gather over the world: every rank contributes `bytes` bytes of device memory at dev_send;
+ * dev_recv (world * bytes, device) receives them in rank order; enqueued on / ordered with
+ * cuda_stream; returns 0 on success. With world > 1 and an all-gather set, the library runs the
+ * REPLICATED-POOL protocol (SURVEY.md §8(e) mitigation): each rank samples its slice of every
+ * round's new RR ids, then the round's sets are all-gathered (one size exchange + two padded
+ * all-gathers per generate call) so every rank holds the global pool in global id order, and
+ * NodeSelection runs locally and identically on every rank with no per-step collective
+ * (gim_set_allreduce is then unused). Without it, the per-step count/decrement all-reduce
+ * protocol is used. gim_rr_export / gim_counts_export then return the global pool. */
+typedef int (*gim_allgather_fn)(const void* dev_send, uint64_t bytes, void* dev_recv, void* cuda_stream,
+                                void* user);
+gim_status gim_set_allgather(gim_ctx* ctx, gim_allgather_fn fn, void* user);
+
 /* Route every device allocation of ctx through the caller (e.g. torch's caching allocator).
  * Must be called before gim_load_graph. alloc_fn returns NULL on failure. */
 typedef void* (*gim_alloc_fn)(uint64_t bytes, void* cuda_stream, void* user);
@@ -196,6 +209,9 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *  GIM_OPT_GIANT_NT     = 0 (default, auto) / 256 / 128: threads per giant-set CTA of the
  *                         block-per-RR fallback (auto: 128 when the previous chunk produced >= 12
  *                         giant sets per 256-thread slot, else 256).
+ *  GIM_OPT_FRESH_FINAL  = 0 (default: IMM's published reuse of the estimation sets, R8) / 1:
+ *                         gim_imm's final phase samples a fresh pool of ceil(theta) sets with the
+ *                         key seed ^ 0x9E3779B97F4A7C15 (reading R29; the Chen 2018 fix [EXT]).
  *  GIM_OPT_MB_CHAINS    = 1 / 4 / 8 (default 8): interleaved Philox chains per thread in
  *                          gim_microbench_philox. */
 typedef enum {
@@ -210,7 +226,8 @@ typedef enum {
   GIM_OPT_SPECULATE = 10,
   GIM_OPT_MB_CHAINS = 11,
   GIM_OPT_PDL = 12,
-  GIM_OPT_GIANT_NT = 13
+  GIM_OPT_GIANT_NT = 13,
+  GIM_OPT_FRESH_FINAL = 14
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

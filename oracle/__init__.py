@@ -52,6 +52,7 @@ def _lib():
         "og_imm": (_int, [_p, _u32, _dbl, _dbl, _u64, _p, _p, _p, _p, _p, _p, _p]),
         "og_mc_spread": (_int, [_p, _p, _u32, _u64, _u64, _p, _p]),
         "og_mrim_generate": (_int, [_p, _u64, _u32, _u64]),
+        "og_set_fresh_final": (None, [_p, _int]),
         "og_mrim_num_sets": (_u64, [_p]),
         "og_mrim_set": (_u32, [_p, _u64, _u64, _u32, _p]),
         "og_mrim_pool_len": (_u64, [_p]),
@@ -251,6 +252,10 @@ class Oracle:
         _lib().og_mc_spread(self._h, _ptr(s), len(s), trials, mc_seed, ctypes.byref(mean),
                             ctypes.byref(se))
         return mean.value, se.value
+
+    def set_fresh_final(self, on: bool) -> None:
+        """R29: IMM's final phase on a fresh pool (key seed ^ 0x9E3779B97F4A7C15)."""
+        _lib().og_set_fresh_final(self._h, int(bool(on)))
 
     # ---- MRIM (R26-R28; oracle/gim_oracle.c "MRIM") ----------------------------------------
     def mrim_generate(self, N: int, T: int, seed: int) -> None:

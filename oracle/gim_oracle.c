@@ -120,6 +120,7 @@ typedef struct og_ctx {
   uint32_t* mr_nodes;
   uint32_t* mr_count;
   uint32_t* mr_tmp;
+  int fresh_final;          /* R29: final phase on a fresh pool (og_set_fresh_final) */
 } og_ctx;
 
 static int cmp_u32(const void* a, const void* b) {
@@ -392,6 +393,13 @@ int og_imm_constants(uint32_t n, uint32_t k, double eps, double ell, double out[
   return imm_constants_g(n, n, k, eps, ell, out);
 }
 
+/* R29 (SURVEY R8's NEXT variant; Chen 2018 [EXT] on IMM's martingale analysis): the final phase
+ * draws a fresh pool, independent of the sets that produced LB — the sets of a second key,
+ * seed ^ 0x9E3779B97F4A7C15: R_final = ceil(theta) sets RR(seed_f, i). Off by default (IMM's
+ * published reuse, R8). */
+#define OG_FRESH_KEY 0x9E3779B97F4A7C15ull
+void og_set_fresh_final(og_ctx* c, int on) { c->fresh_final = on ? 1 : 0; }
+
 /* O8 driver: Alg. 2 rounds, then theta = lambda_star / LB and the final selection
  * (Alg. 1). Readings R4-R8. Cumulative pool (IMM reuses the estimation sets).
  * dres = { LB, theta, spread_est, ell_eff, eps_prime, lambda_prime, lambda_star }
@@ -426,8 +434,12 @@ int og_imm(og_ctx* c, uint32_t k, double eps, double ell, uint64_t seed, uint32_
   }
   theta = K[6] / LB;                                     /* R2 */
   T = (uint64_t)ceil(theta);
-  R = c->nsets > T ? c->nsets : T;                       /* R8: reuse, no truncation */
-  og_generate(c, R, seed);
+  if (c->fresh_final) {
+    og_generate(c, T, seed ^ OG_FRESH_KEY);              /* R29: a different key discards R */
+  } else {
+    R = c->nsets > T ? c->nsets : T;                     /* R8: reuse, no truncation */
+    og_generate(c, R, seed);
+  }
   og_select(c, k, seeds_out, gains_out, &cov);
   dres[0] = LB; dres[1] = theta; dres[2] = n * (double)cov / (double)c->nsets;   /* Eq. 3 */
   dres[3] = K[0]; dres[4] = K[1]; dres[5] = K[3]; dres[6] = K[6];
@@ -684,8 +696,12 @@ int og_mrim(og_ctx* c, uint32_t k, uint32_t T, double eps, double ell, uint64_t 
   }
   theta = K[6] / LB;
   Tn = (uint64_t)ceil(theta);
-  R = c->mr_nsets > Tn ? c->mr_nsets : Tn;
-  og_mrim_generate(c, R, T, seed);
+  if (c->fresh_final) {
+    og_mrim_generate(c, Tn, T, seed ^ OG_FRESH_KEY);     /* R29 */
+  } else {
+    R = c->mr_nsets > Tn ? c->mr_nsets : Tn;
+    og_mrim_generate(c, R, T, seed);
+  }
   og_mrim_select(c, k, seeds_out, gains_out, &cov);
   dres[0] = LB; dres[1] = theta; dres[2] = n * (double)cov / (double)c->mr_nsets;
   dres[3] = K[0]; dres[4] = K[1]; dres[5] = K[3]; dres[6] = K[6];

@@ -10,7 +10,7 @@ namespace gim {
 __global__ void __launch_bounds__(256) k_validate_csr(const uint64_t* __restrict__ rp64, uint32_t n,
                                                       uint64_t m, const uint32_t* __restrict__ src,
                                                       uint32_t* __restrict__ rp32, uint32_t* err,
-                                                      uint32_t* bad_row) {
+                                                      uint32_t* bad_row, uint32_t* __restrict__ thr_node) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   for (uint32_t v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); v < n; v += nwarps) {
@@ -29,6 +29,9 @@ __global__ void __launch_bounds__(256) k_validate_csr(const uint64_t* __restrict
     e_bits = __reduce_or_sync(kFull, e_bits);
     if (lane == 0) {
       rp32[v] = (uint32_t)a;
+      // WC live threshold of row v (p = 1/d_in(v): coin <= thr <=> coin * d < 2^32), read by the
+      // RR kernels in parallel with the row pointers instead of a division per expanded node
+      if (thr_node) thr_node[v] = (b > a) ? (uint32_t)(0xFFFFFFFFull / (b - a)) : 0u;
       if (e_bits) {
         atomicOr(err, e_bits);
         atomicMin(bad_row, v);
@@ -39,8 +42,9 @@ __global__ void __launch_bounds__(256) k_validate_csr(const uint64_t* __restrict
 }
 
 cudaError_t launch_validate_csr(const uint64_t* rp64, uint32_t n, uint64_t m, const uint32_t* src,
-                                uint32_t* rp32, uint32_t* err, uint32_t* bad_row, int grid, cudaStream_t s) {
-  k_validate_csr<<<grid, 256, 0, s>>>(rp64, n, m, src, rp32, err, bad_row);
+                                uint32_t* rp32, uint32_t* err, uint32_t* bad_row, uint32_t* thr_node, int grid,
+                                cudaStream_t s) {
+  k_validate_csr<<<grid, 256, 0, s>>>(rp64, n, m, src, rp32, err, bad_row, thr_node);
   return cudaGetLastError();
 }
 

@@ -60,7 +60,7 @@ struct gim_ctx {
   int model = 0, scheme = 0;
   float p_uniform = 0.f;
   uint64_t thr_uniform = 0;
-  DevBuf row_ptr, src, thr_edge;
+  DevBuf row_ptr, src, thr_edge, thr_node;
   DevBuf out_ptr, out_dst, out_in, thr_wc;   // out-CSR for gim_mc_spread (built on first use)
   bool out_valid = false;
   // MRIM (readings R26-R28): rounds T; pair ids t*n + u index the count / index / selection
@@ -70,6 +70,9 @@ struct gim_ctx {
   int rank = 0, world = 1;
   gim_allreduce_fn arfn = nullptr;
   void* aruser = nullptr;
+  gim_allgather_fn agfn = nullptr;   // set: replicated-pool protocol (no per-step collectives)
+  void* aguser = nullptr;
+  DevBuf ag_small, ag_send, ag_recv;
   // pool (O6)
   bool have_seed = false;
   uint64_t seed = 0, T_global = 0, nsets = 0, pool_len = 0;
@@ -81,6 +84,7 @@ struct gim_ctx {
   uint32_t giant_slots = 0;
   uint32_t giant_n = 0;             // n the giant slots were sized for (reused while n <= giant_n)
   int giant_nt_opt = 0;             // GIM_OPT_GIANT_NT: 0 auto, else threads per giant CTA
+  int fresh_final = 0;              // GIM_OPT_FRESH_FINAL (reading R29)
   double giant_per_slot = 0.0;      // giant sets per default slot in the previous chunk
   bool giant_cap_reached = false;
   uint64_t stage_cap = 0;
@@ -339,6 +343,7 @@ RRParams base_params(gim_ctx* c) {
   p.n = c->n;
   p.row_ptr = c->row_ptr.as<uint32_t>();
   p.src = c->src.as<uint32_t>();
+  p.thr_node = c->thr_node.as<uint32_t>();
   p.thr_edge = c->thr_edge.as<uint64_t>();
   p.thr_uniform = c->thr_uniform;
   p.seed = c->seed;
@@ -554,6 +559,85 @@ gim_status truncate_pool(gim_ctx* c, uint64_t theta) {
   return GIM_OK;
 }
 
+// Replicated-pool protocol (world > 1 with an all-gather hook, include/gim.h gim_set_allgather):
+// this rank generated its slice of the new global ids [a, theta) as local sets [set0, nsets) /
+// elements [e0, pool_len); exchange element counts, all-gather the slices' sizes and elements
+// (padded to the largest slice), and rebuild [set0, ...) as ALL new sets in global id order
+// (rank slices are contiguous and rank-ordered), with count_total updated to the global counts.
+gim_status replicate_round(gim_ctx* c, uint64_t a, uint64_t theta, uint64_t set0, uint64_t e0, size_t seg0) {
+  const int W = c->world;
+  const uint64_t Tr = c->rounds, len = (theta - a) / Tr;
+  const uint64_t Ls = c->pool_len - e0, Ss = c->nsets - set0;
+  std::vector<uint64_t> S(W), L(W);
+  uint64_t maxS = 1, totS = 0;
+  for (int r = 0; r < W; ++r) {
+    S[r] = Tr * ((uint64_t)((unsigned __int128)len * (r + 1) / W) - (uint64_t)((unsigned __int128)len * r / W));
+    maxS = std::max(maxS, S[r]);
+    totS += S[r];
+  }
+  if (S[c->rank] != Ss) return fail(c, GIM_ESTATE, "replicated pool: local slice size mismatch");
+  // 1. element counts of every rank
+  TRY(ensure(c, c->ag_small, 8 * (uint64_t)(W + 1)));
+  c->h_u64[0] = Ls;
+  CK(cudaMemcpyAsync(c->ag_small.p, c->h_u64, 8, cudaMemcpyHostToDevice, c->stream));
+  c->st.allreduces++;
+  if (c->agfn(c->ag_small.p, 8, c->ag_small.as<uint64_t>() + 1, c->stream, c->aguser))
+    return fail(c, GIM_ECOLL, "all-gather(element counts) failed");
+  std::vector<uint64_t> hL(W);
+  CK(cudaMemcpyAsync(hL.data(), c->ag_small.as<uint64_t>() + 1, 8 * (uint64_t)W, cudaMemcpyDeviceToHost, c->stream));
+  TRY(sync(c));
+  uint64_t maxL = 1, totL = 0;
+  for (int r = 0; r < W; ++r) {
+    L[r] = hL[r];
+    maxL = std::max(maxL, L[r]);
+    totL += L[r];
+  }
+  if (hL[c->rank] != Ls) return fail(c, GIM_ECOLL, "all-gather returned a wrong own element count");
+  // 2. sizes of the local sets, padded to maxS; elements padded to maxL (pool capacity)
+  TRY(ensure(c, c->ag_send, std::max(maxS * 4, maxL * 4)));
+  TRY(ensure(c, c->ag_recv, (uint64_t)W * std::max(maxS * 4, maxL * 4)));
+  TRY(launched(c, launch_sizes_of(c->offsets.as<uint64_t>() + set0, Ss, maxS, c->ag_send.as<uint32_t>(),
+                                  c->num_sms * 4, c->stream), "k_sizes_of"));
+  c->st.allreduces++;
+  if (c->agfn(c->ag_send.p, maxS * 4, c->ag_recv.p, c->stream, c->aguser))
+    return fail(c, GIM_ECOLL, "all-gather(set sizes) failed");
+  // compact the gathered sizes in rank order into the scan input
+  TRY(ensure(c, c->sizes, (totS + 1) * 4));
+  TRY(ensure(c, c->scan_out, (totS + 1) * 8));
+  TRY(ensure(c, c->scan_tmp, (scan_tiles(totS) + 2) * 8));
+  for (int r = 0, o = 0; r < W; o += (int)S[r], ++r)
+    if (S[r]) CK(cudaMemcpyAsync(c->sizes.as<uint32_t>() + o, c->ag_recv.as<uint32_t>() + (uint64_t)r * maxS, S[r] * 4,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+  // elements: undo the local counts, gather, write back in rank order, count globally
+  if (Ls) TRY(launched(c, launch_count_sub(c->pool.as<uint32_t>(), e0, e0 + Ls, c->count_total.as<uint32_t>(),
+                                           c->num_sms * 8, c->stream), "k_count_sub"));
+  CK(cudaMemcpyAsync(c->ag_send.p, c->pool.as<uint32_t>() + e0, Ls * 4, cudaMemcpyDeviceToDevice, c->stream));
+  c->st.allreduces++;
+  if (c->agfn(c->ag_send.p, maxL * 4, c->ag_recv.p, c->stream, c->aguser))
+    return fail(c, GIM_ECOLL, "all-gather(set elements) failed");
+  TRY(grow_keep(c, c->pool, (e0 + totL) * 4, e0 * 4));
+  TRY(grow_keep(c, c->offsets, (set0 + totS + 1) * 8, (set0 + 1) * 8));
+  for (uint64_t r = 0, o = 0; r < (uint64_t)W; o += L[r], ++r)
+    if (L[r]) CK(cudaMemcpyAsync(c->pool.as<uint32_t>() + e0 + o, c->ag_recv.as<uint32_t>() + r * maxL, L[r] * 4,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+  if (totL) TRY(launched(c, launch_count_add(c->pool.as<uint32_t>(), e0, e0 + totL, c->count_total.as<uint32_t>(),
+                                             c->num_sms * 8, c->stream), "k_count_add"));
+  {
+    int nl = 0;
+    cudaError_t e = launch_scan_u32(c->sizes.as<uint32_t>(), totS, c->scan_out.as<uint64_t>(),
+                                    c->scan_tmp.as<uint64_t>(), c->scan_tmp.as<uint64_t>() + scan_tiles(totS) + 1,
+                                    c->stream, &nl);
+    TRY(launched(c, e, "scan(gathered sizes)", nl));
+  }
+  TRY(launched(c, launch_offsets_of(c->scan_out.as<uint64_t>(), totS, e0, c->offsets.as<uint64_t>() + set0,
+                                    c->num_sms * 4, c->stream), "k_offsets_of"));
+  c->nsets = set0 + totS;
+  c->pool_len = e0 + totL;
+  c->segs.resize(seg0);
+  c->segs.push_back(Seg{a, set0, totS});
+  return GIM_OK;
+}
+
 // theta counts sets in API units: RR sets, or MRIM sets of `rounds` standard ids each (R26)
 gim_status generate(gim_ctx* c, uint64_t theta_sets, uint64_t seed) {
   if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
@@ -573,7 +657,9 @@ gim_status generate(gim_ctx* c, uint64_t theta_sets, uint64_t seed) {
     const uint64_t lo = a + Tr * (uint64_t)((unsigned __int128)len * c->rank / c->world);
     const uint64_t hi = a + Tr * (uint64_t)((unsigned __int128)len * (c->rank + 1) / c->world);
     const uint64_t set0 = c->nsets, e0 = c->pool_len;
+    const size_t seg0 = c->segs.size();
     for (uint64_t s = lo; s < hi; s += kChunk) TRY(gen_chunk(c, s, (uint32_t)std::min<uint64_t>(kChunk, hi - s)));
+    if (c->world > 1 && c->agfn) TRY(replicate_round(c, a, theta, set0, e0, seg0));
     // one inverted-index segment per generate call (= per IMM round): its O(n) count scan is
     // paid once per round, not once per 2^22-id chunk
     if (c->nsets > set0) {
@@ -593,7 +679,8 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
   if (k < 1 || k > c->n) return fail(c, GIM_EINVAL, "k must satisfy 1 <= k <= n");
   if (!c->have_seed || c->T_global == 0) return fail(c, GIM_ESTATE, "RR pool is empty");
-  if (c->world > 1 && !c->arfn) return fail(c, GIM_ESTATE, "world > 1 requires gim_set_allreduce");
+  const bool sharded = c->world > 1 && !c->agfn;   // replicated pool: select as P = 1
+  if (sharded && !c->arfn) return fail(c, GIM_ESTATE, "world > 1 requires gim_set_allreduce or gim_set_allgather");
   const uint64_t n = nsp(c);                        // counted elements (nodes, or MRIM pairs)
   const uint32_t kk = k * c->rounds;                // picks: k per round (R27)
   const MrimSel mrs{c->rounds, c->n, k};
@@ -601,8 +688,8 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   TRY(ensure(c, c->cnt, n * 4));
   TRY(ensure(c, c->covered, std::max<uint64_t>(c->nsets / c->rounds, 1)));
   TRY(ensure(c, c->keys, (uint64_t)kk * 8));
-  if (c->world > 1) TRY(ensure(c, c->dec, n * 4));
-  int32_t* dec = c->world > 1 ? c->dec.as<int32_t>() : nullptr;
+  if (sharded) TRY(ensure(c, c->dec, n * 4));
+  int32_t* dec = sharded ? c->dec.as<int32_t>() : nullptr;
   if (!c->inv_valid) {                          // one segment over the whole local pool
     drop_inv(c);
     CK(cudaMemsetAsync(c->cnt_snap.p, 0, n * 4, c->stream));
@@ -822,7 +909,8 @@ void gim_destroy(gim_ctx* c) {
                     &c->sizes, &c->soff, &c->giant_list, &c->retry_list, &c->item_list, &c->scan_out,
                     &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
-                    &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc};
+                    &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->thr_node, &c->ag_small,
+                    &c->ag_send, &c->ag_recv};
   for (auto& sg : c->iseg) {
     dfree(c, sg.off);
     dfree(c, sg.inv);
@@ -904,6 +992,8 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
   c->thr_uniform = (uint64_t)std::ceil((double)p_uniform * 4294967296.0);
   TRY(dalloc(c, c->row_ptr, ((uint64_t)n + 1) * 4));
   TRY(dalloc(c, c->src, std::max<uint64_t>(m, 1) * 4));
+  if (scheme == GIM_W_WC) TRY(dalloc(c, c->thr_node, ((uint64_t)n + 1) * 4));
+  else dfree(c, c->thr_node);
   {
     // upload (pinned host buffers DMA directly), validate + convert row pointers on the device
     DevBuf rp64;
@@ -914,7 +1004,8 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
     CK(cudaMemsetAsync(flags, 0, 4, c->stream));
     CK(cudaMemsetAsync(flags + 1, 0xFF, 4, c->stream));
     TRY(launched(c, launch_validate_csr(rp64.as<uint64_t>(), n, m, c->src.as<uint32_t>(), c->row_ptr.as<uint32_t>(),
-                                        flags, flags + 1, c->num_sms * 8, c->stream), "k_validate_csr"));
+                                        flags, flags + 1, scheme == GIM_W_WC ? c->thr_node.as<uint32_t>() : nullptr,
+                                        c->num_sms * 8, c->stream), "k_validate_csr"));
     CK(cudaMemcpyAsync(c->h_u64, flags, 8, cudaMemcpyDeviceToHost, c->stream));
     TRY(sync(c));
     dfree(c, rp64);
@@ -970,6 +1061,15 @@ gim_status gim_set_shard(gim_ctx* c, int rank, int world) {
   c->have_seed = false;
   c->T_global = c->nsets = c->pool_len = 0;
   c->segs.clear();
+  return GIM_OK;
+}
+
+gim_status gim_set_allgather(gim_ctx* c, gim_allgather_fn fn, void* user) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  c->agfn = fn;
+  c->aguser = user;
+  c->have_seed = false;                        // the pool layout changes: regenerate
   return GIM_OK;
 }
 
@@ -1056,8 +1156,14 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
   const uint64_t T = (uint64_t)std::ceil(theta);
   uint64_t R_last = 0;
   for (uint32_t q = 0; q < r.rounds; ++q) R_last = std::max<uint64_t>(R_last, r.theta_i[q]);
-  const uint64_t R_final = std::max<uint64_t>(R_last, T);   // reading R8
-  TRY(generate(c, R_final, seed));                           // extends or truncates speculation
+  if (c->fresh_final) {
+    // reading R29: the final phase on a fresh pool of ceil(theta) sets of a second key (the
+    // different seed makes generate discard the estimation pool)
+    TRY(generate(c, T, seed ^ 0x9E3779B97F4A7C15ull));
+  } else {
+    const uint64_t R_final = std::max<uint64_t>(R_last, T);   // reading R8
+    TRY(generate(c, R_final, seed));                         // extends or truncates speculation
+  }
   std::vector<uint64_t> gains((size_t)k * c->rounds);
   TRY(select_impl(c, k, seeds, gains.data(), &cov));
   r.LB = LB;
@@ -1199,6 +1305,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_INV_SEGMENTS: c->inv_segmented = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_MB_CHAINS: c->mb_chains = (int)value; return GIM_OK;
     case GIM_OPT_SPECULATE: c->speculate = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_FRESH_FINAL: c->fresh_final = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_GIANT_NT:
       if (value != 0 && value != kGiantThreads && value != kGiantThreadsNarrow)
         return fail(c, GIM_EINVAL, "giant CTA width must be 0 (auto), 256 or 128");

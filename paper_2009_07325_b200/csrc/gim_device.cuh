@@ -127,6 +127,7 @@ struct RRParams {
   uint32_t n;
   const uint32_t* row_ptr;     // in-CSR row pointers (uint32, m < 2^32)
   const uint32_t* src;         // in-CSR sources
+  const uint32_t* thr_node;    // WC: per-node live threshold floor((2^32-1)/d_in(v))
   const uint64_t* thr_edge;    // explicit weights: IC ceil(w*2^32), LT floor(w*2^32)
   uint64_t thr_uniform;        // uniform p: ceil(p*2^32)
   uint64_t seed;

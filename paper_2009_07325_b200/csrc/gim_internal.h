@@ -15,6 +15,12 @@ cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const u
                          const uint64_t* scan, uint32_t count, uint64_t pool_base, uint32_t* pool,
                          uint64_t* offsets_out, uint32_t* count_total, uint32_t rounds, uint32_t round0,
                          uint32_t n, int grid, cudaStream_t s);
+cudaError_t launch_count_add(const uint32_t* pool, uint64_t e0, uint64_t e1, uint32_t* count_total, int grid,
+                             cudaStream_t s);
+cudaError_t launch_sizes_of(const uint64_t* offsets, uint64_t cnt, uint64_t padded, uint32_t* sizes, int grid,
+                            cudaStream_t s);
+cudaError_t launch_offsets_of(const uint64_t* scan, uint64_t cnt, uint64_t base, uint64_t* offsets_out, int grid,
+                              cudaStream_t s);
 cudaError_t launch_count_sub(const uint32_t* pool, uint64_t e0, uint64_t e1, uint32_t* count_total,
                              int grid, cudaStream_t s);
 
@@ -51,7 +57,8 @@ cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev*
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s,
                          bool limit, const MrimSel* mr = nullptr);
 cudaError_t launch_validate_csr(const uint64_t* rp64, uint32_t n, uint64_t m, const uint32_t* src,
-                                uint32_t* rp32, uint32_t* err, uint32_t* bad_row, int grid, cudaStream_t s);
+                                uint32_t* rp32, uint32_t* err, uint32_t* bad_row, uint32_t* thr_node, int grid,
+                                cudaStream_t s);
 // forward Monte-Carlo (mc.cu)
 cudaError_t build_out_csr(const uint32_t* row_ptr, const uint32_t* src, uint32_t n, uint64_t m, int scheme,
                           uint32_t* out_ptr, uint32_t* out_dst, uint32_t* out_in, uint32_t* thr_wc,

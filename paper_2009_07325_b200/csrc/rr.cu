@@ -402,11 +402,12 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
         uint32_t a = 0, b = 0, thr = 0, ng = 0;
         if (lane < nb) {
           const uint32_t v = q[head + lane];
+          const uint32_t tv = (SCHEME == W_WC) ? __ldg(p.thr_node + v) : 0u;   // loads in parallel
           a = __ldg(p.row_ptr + v);
           b = __ldg(p.row_ptr + v + 1);
           if (b > a) {
             ng = ((b - 1) >> 2) - (a >> 2) + 1;
-            thr = node_thr<SCHEME>(p, b - a);
+            thr = (SCHEME == W_WC) ? tv : node_thr<SCHEME>(p, b - a);
           }
         }
         if (coins >= 0x80000000u) { atomicAdd(&p.ctr->coins, (unsigned long long)coins); coins = 0; }
@@ -1022,11 +1023,12 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
               __nanosleep(32);
               v = ld_relaxed_gpu(Q + f + lane);
             }
+            const uint32_t tv = (SCHEME == W_WC) ? __ldg(p.thr_node + v) : 0u;
             a = __ldg(p.row_ptr + v);
             b = __ldg(p.row_ptr + v + 1);
             if (b > a) {
               ng = ((b - 1) >> 2) - (a >> 2) + 1;
-              thr = node_thr<SCHEME>(p, b - a);
+              thr = (SCHEME == W_WC) ? tv : node_thr<SCHEME>(p, b - a);
               coins += b - a;
             }
           }
@@ -1210,6 +1212,28 @@ __global__ void __launch_bounds__(256) k_store(const uint32_t* __restrict__ stag
   if (blockIdx.x == 0 && threadIdx.x == 0) offsets_out[count] = pool_base + scan[count];
 }
 
+// count_total[v] += 1 for every element of pool[e0, e1) (replicated pool: the gathered round).
+__global__ void k_count_add(const uint32_t* __restrict__ pool, uint64_t e0, uint64_t e1,
+                            uint32_t* __restrict__ count_total) {
+  for (uint64_t t = e0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < e1;
+       t += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(count_total + pool[t], 1u);
+}
+
+// sizes[j] = offsets[j+1] - offsets[j] (j < cnt), zero-padded to `padded` entries.
+__global__ void k_sizes_of(const uint64_t* __restrict__ offsets, uint64_t cnt, uint64_t padded,
+                           uint32_t* __restrict__ sizes) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < padded; j += (uint64_t)gridDim.x * blockDim.x)
+    sizes[j] = j < cnt ? (uint32_t)(offsets[j + 1] - offsets[j]) : 0u;
+}
+
+// offsets_out[j] = base + scan[j] for j <= cnt (scan = exclusive prefix of sizes, scan[cnt] = total).
+__global__ void k_offsets_of(const uint64_t* __restrict__ scan, uint64_t cnt, uint64_t base,
+                             uint64_t* __restrict__ offsets_out) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j <= cnt; j += (uint64_t)gridDim.x * blockDim.x)
+    offsets_out[j] = base + scan[j];
+}
+
 // count_total[v] -= 1 for every member of local sets [s0, s1) (pool truncation).
 __global__ void k_count_sub(const uint32_t* __restrict__ pool, uint64_t e0, uint64_t e1,
                             uint32_t* __restrict__ count_total) {
@@ -1334,6 +1358,21 @@ cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* si
   return cudaGetLastError();
 }
 
+cudaError_t launch_count_add(const uint32_t* pool, uint64_t e0, uint64_t e1, uint32_t* count_total, int grid,
+                             cudaStream_t s) {
+  k_count_add<<<grid, 256, 0, s>>>(pool, e0, e1, count_total);
+  return cudaGetLastError();
+}
+cudaError_t launch_sizes_of(const uint64_t* offsets, uint64_t cnt, uint64_t padded, uint32_t* sizes, int grid,
+                            cudaStream_t s) {
+  k_sizes_of<<<grid, 256, 0, s>>>(offsets, cnt, padded, sizes);
+  return cudaGetLastError();
+}
+cudaError_t launch_offsets_of(const uint64_t* scan, uint64_t cnt, uint64_t base, uint64_t* offsets_out, int grid,
+                              cudaStream_t s) {
+  k_offsets_of<<<grid, 256, 0, s>>>(scan, cnt, base, offsets_out);
+  return cudaGetLastError();
+}
 cudaError_t launch_count_sub(const uint32_t* pool, uint64_t e0, uint64_t e1, uint32_t* count_total,
                              int grid, cudaStream_t s) {
   k_count_sub<<<grid, 256, 0, s>>>(pool, e0, e1, count_total);

@@ -24,7 +24,7 @@ LIB_PATH = os.environ.get("GIM_LIB_PATH") or os.path.join(_HERE, "libgim.so")
 GIM_OK, GIM_EINVAL, GIM_ESTATE, GIM_ENOMEM, GIM_ECUDA, GIM_ECOLL, GIM_ELTWEIGHT = range(7)
 IC, LT = 0, 1
 W_EXPLICIT, W_WC, W_UNIFORM = 0, 1, 2
-OPT_FORCE_GIANT, OPT_QUEUE_CAP, OPT_PROFILE, OPT_STAGING_CAP, OPT_SELECT_GRAPH, OPT_INV_SEGMENTS, OPT_ARGMAX_CAND, OPT_IC_LANE, OPT_SPECULATE, OPT_MB_CHAINS, OPT_PDL, OPT_GIANT_NT = 1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12, 13
+OPT_FORCE_GIANT, OPT_QUEUE_CAP, OPT_PROFILE, OPT_STAGING_CAP, OPT_SELECT_GRAPH, OPT_INV_SEGMENTS, OPT_ARGMAX_CAND, OPT_IC_LANE, OPT_SPECULATE, OPT_MB_CHAINS, OPT_PDL, OPT_GIANT_NT, OPT_FRESH_FINAL = 1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12, 13, 14
 
 _STATUS = {0: "GIM_OK", 1: "GIM_EINVAL", 2: "GIM_ESTATE", 3: "GIM_ENOMEM", 4: "GIM_ECUDA",
            5: "GIM_ECOLL", 6: "GIM_ELTWEIGHT"}
@@ -33,6 +33,7 @@ _p, _u32, _u64, _i32, _i64, _dbl = (ctypes.c_void_p, ctypes.c_uint32, ctypes.c_u
                                     ctypes.c_int, ctypes.c_int64, ctypes.c_double)
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, _p, _u64, _p, _p)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, _p, _u64, _p, _p, _p)
 ALLOC_FN = ctypes.CFUNCTYPE(_p, _u64, _p, _p)
 FREE_FN = ctypes.CFUNCTYPE(None, _p, _p, _p)
 
@@ -62,6 +63,7 @@ SIGNATURES = {
     "gim_load_graph": (_i32, [_p, _u32, _u64, _p, _p, _p, _i32, _i32, ctypes.c_float]),
     "gim_set_shard": (_i32, [_p, _i32, _i32]),
     "gim_set_allreduce": (_i32, [_p, ALLREDUCE_FN, _p]),
+    "gim_set_allgather": (_i32, [_p, ALLGATHER_FN, _p]),
     "gim_set_allocator": (_i32, [_p, ALLOC_FN, FREE_FN, _p]),
     "gim_generate_rr": (_i32, [_p, _u64, _u64]),
     "gim_select": (_i32, [_p, _u32, _p, _p, _p]),
@@ -188,6 +190,13 @@ class Gim:
         self._keep.append(cb)
         self._check(self._lib.gim_set_allreduce(self._h, cb, None))
 
+    def set_allgather(self, fn: Callable[[int, int, int, int], int]):
+        """fn(send_ptr, nbytes, recv_ptr, cuda_stream) -> 0: all-gather of nbytes per rank into
+        recv (world * nbytes, rank order). Switches world > 1 to the replicated-pool protocol."""
+        cb = ALLGATHER_FN(lambda snd, nb, rcv, stream, user: int(fn(snd, nb, rcv, stream or 0)))
+        self._keep.append(cb)
+        self._check(self._lib.gim_set_allgather(self._h, cb, None))
+
     def generate_rr(self, theta: int, seed: int):
         self._check(self._lib.gim_generate_rr(self._h, theta, seed))
 
@@ -284,6 +293,37 @@ def torch_allreduce(group=None, device: str = "cuda"):
                 t.copy_(h)
             else:
                 dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return 0
+
+    return fn
+
+
+def torch_allgather(group=None):
+    """all-gather callback for Gim.set_allgather: torch.distributed.all_gather_into_tensor of the
+    library's device bytes, ordered on the library's stream (NCCL over NVLink for an nccl group;
+    a gloo group stages through host memory, for functional tests)."""
+    import torch
+    import torch.distributed as dist
+
+    def view(ptr, nbytes):
+        class _View:
+            __cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1",
+                                        "data": (int(ptr), False), "version": 3, "strides": None,
+                                        "stream": None}
+        return torch.as_tensor(_View(), device="cuda")
+
+    def fn(send: int, nbytes: int, recv: int, stream: int) -> int:
+        world = dist.get_world_size(group)
+        src = view(send, nbytes)
+        dst = view(recv, nbytes * world)
+        s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            if dist.get_backend(group) == "gloo":
+                parts = [torch.empty(int(nbytes), dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(parts, src.cpu(), group=group)
+                dst.copy_(torch.cat(parts).to(dst.device))
+            else:
+                dist.all_gather_into_tensor(dst, src, group=group)
         return 0
 
     return fn

@@ -21,7 +21,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, q, key, T, k):
+def _worker(rank, world, port, q, key, T, k, replicated=False):
     import torch.distributed as dist
     import paper_2009_07325_b200 as P
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -33,6 +33,8 @@ def _worker(rank, world, port, q, key, T, k):
     c.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme)
     c.set_shard(rank, world)
     c.set_allreduce(P.torch_allreduce())
+    if replicated:
+        c.set_allgather(P.torch_allgather())
     c.generate_rr(T, w.rr_seed)
     seeds, gains, cov = c.select(k)
     ids, off, nodes = c.rr_export()
@@ -67,4 +69,33 @@ def test_multiprocess_shards_equal_single(world):
         lo, hi = P.shard_slice(0, T, rank, world)
         assert id0 == lo and nids == hi - lo
         assert nsum == int(np.sum(rnodes[roff[lo]:roff[hi]].astype(np.uint64)))
+        assert iseeds == rimm.seeds.tolist() and R == rimm.R_final and LB == rimm.LB
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multiprocess_replicated_pool_equals_single(world):
+    """The replicated-pool protocol through torch.distributed (gloo, all ranks on cuda:0): each
+    rank ends with the whole P = 1 pool and returns the P = 1 selection and IMM."""
+    import torch.multiprocessing as mp
+    import paper_2009_07325_b200 as P
+    key, T, k = "C2", 40009, 30
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    ref = P.Gim(0)
+    ref.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme)
+    ref.generate_rr(T, w.rr_seed)
+    rs, rg, rc = ref.select(k)
+    _, roff, rnodes = ref.rr_export()
+    rimm = ref.imm(k, w.eps, w.ell, w.rr_seed)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, key, T, k, True)) for r in range(world)]
+    [p.start() for p in procs]
+    out = sorted([q.get(timeout=600) for _ in range(world)])
+    [p.join(120) for p in procs]
+    for rank, seeds, gains, cov, id0, nids, nsum, iseeds, R, LB in out:
+        assert seeds == rs.tolist() and gains == rg.tolist() and cov == rc
+        assert id0 == 0 and nids == T
+        assert nsum == int(np.sum(rnodes.astype(np.uint64)))
         assert iseeds == rimm.seeds.tolist() and R == rimm.R_final and LB == rimm.LB

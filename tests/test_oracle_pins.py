@@ -556,3 +556,28 @@ def test_mc_spread_vs_ris_estimate_C1():
     mean, se = o.mc_spread(r.seeds, 20000, 17)
     assert se / mean < 0.003
     assert abs(mean - ris) / mean < 0.01, (mean, ris)
+
+
+def test_imm_fresh_final_pool_C1():
+    """R29 (SURVEY R8's NEXT variant, Chen 2018 [EXT]): with a fresh final pool the estimation
+    trace is IMM's unchanged, and the final seeds are exactly NodeSelection over the
+    ceil(lambda*/LB) sets of the second key — recomputed here by composing the pinned og_generate
+    and og_select, not by the driver."""
+    g = gi.workload_graph("C1")
+    w = gi.WORKLOADS["C1"]
+    o = oracle.Oracle(g, w.model, w.scheme)
+    r = o.imm(w.k, w.eps, w.ell, w.rr_seed)
+    o.set_fresh_final(True)
+    f = o.imm(w.k, w.eps, w.ell, w.rr_seed)
+    assert (f.rounds, f.LB, f.theta) == (r.rounds, r.LB, r.theta)
+    assert np.array_equal(f.T_i, r.T_i) and np.array_equal(f.cov_i, r.cov_i)
+    T = math.ceil(f.theta)
+    assert f.R_final == T
+    o2 = oracle.Oracle(g, w.model, w.scheme)
+    o2.generate(T, w.rr_seed ^ 0x9E3779B97F4A7C15)
+    s, gn, cov = o2.select(w.k)
+    assert np.array_equal(f.seeds, s) and np.array_equal(f.gains, gn) and f.cov == cov
+    assert abs(f.spread_est - g.n * cov / T) < 1e-9 * g.n
+    # the fresh pool shares no set with the estimation pool's key: its estimate is not biased by
+    # the selection (R24) — both estimates agree within a few percent on C1
+    assert abs(f.spread_est - r.spread_est) / r.spread_est < 0.05

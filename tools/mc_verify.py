@@ -35,12 +35,17 @@ def main():
         ris = g.n * hit.mean()
         ris_se = g.n * np.sqrt(hit.mean() * (1 - hit.mean()) / T)
         t0 = time.perf_counter()
-        trials = 2000
-        mean, se = c.mc_spread(r.seeds, trials, 17)
+        if w.model == gi.IC:
+            trials, mc_impl = 2000, "gpu gim_mc_spread"
+            mean, se = c.mc_spread(r.seeds, trials, 17)
+        else:   # LT: forward MC only in the oracle (host, single-threaded, bounded trials)
+            import oracle
+            trials, mc_impl = 400, "oracle og_mc_spread (host)"
+            mean, se = oracle.Oracle(g, w.model, w.scheme, w.p_uniform).mc_spread(r.seeds, trials, 17)
         mc_s = time.perf_counter() - t0
         line = {"workload": key, "k": w.k, "eps": w.eps, "R_final": r.R_final,
                 "spread_est_imm_pool": r.spread_est, "ris_independent_pool": ris, "ris_stderr": ris_se,
-                "mc_trials": trials, "mc_mean": mean, "mc_stderr": se, "mc_seconds_incl_out_csr": mc_s,
+                "mc_impl": mc_impl, "mc_trials": trials, "mc_mean": mean, "mc_stderr": se, "mc_seconds_incl_out_csr": mc_s,
                 "rel_diff_mc_vs_ris": abs(mean - ris) / mean}
         print(json.dumps(line), flush=True)
         out.write(json.dumps(line) + "\n")

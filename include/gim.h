@@ -152,14 +152,17 @@ gim_status gim_rr_export(gim_ctx* ctx, uint64_t* n_sets, uint64_t* pool_len, uin
  * (Occur). */
 gim_status gim_counts_export(gim_ctx* ctx, uint32_t* count_out);
 
-/* Forward Monte-Carlo spread (verification at scale; IC only): `trials` independent instance
- * graphs of the IC process, each newly active node trying each out-edge once; the
- * coin of out-slot e (out-CSR rows sorted by (source, in-slot)) in trial t is word (e & 3) of
- * Philox(mc_seed; t, tag 11 | e >> 2) — independent of every RR stream. mean_out = mean number
+/* Forward Monte-Carlo spread (verification at scale): `trials` independent runs of the
+ * diffusion. IC: each newly active node tries each out-edge once; the coin of
+ * out-slot e (out-CSR rows sorted by (source, in-slot)) in trial t is word (e & 3) of
+ * Philox(mc_seed; t, tag 11 | e >> 2). LT (Eq. 1; reading R30): tau_v = (o + 1/2)/2^32
+ * with o = word 0 of Philox(mc_seed; t, tag 11 | 2^40 | v), compared exactly (WC: active
+ * in-neighbours * 2^33 >= (2o + 1) d_in(v); explicit: sum of floor(w 2^32) >= o + 1); trials <
+ * 2^24 - 1. Both are independent of every RR stream. mean_out = mean number
  * of activated nodes (seeds included, duplicates once), stderr_out (nullable) its standard error,
  * sizes_out[trials] (nullable) the per-trial counts. Builds the out-CSR on first use. Compared
  * with n * F_R'(S) on an independent RR pool it checks Eq. 3 at full size.
- * Errors: GIM_ESTATE (no graph), GIM_EINVAL (LT model, k == 0, trials == 0, seed >= n). */
+ * Errors: GIM_ESTATE (no graph), GIM_EINVAL (k == 0, trials == 0, seed >= n). */
 gim_status gim_mc_spread(gim_ctx* ctx, const uint32_t* seeds, uint32_t k, uint64_t trials, uint64_t mc_seed,
                          double* mean_out, double* stderr_out, uint32_t* sizes_out);
 

@@ -453,6 +453,9 @@ int og_imm(og_ctx* c, uint32_t k, double eps, double ell, uint64_t seed, uint32_
  * IC per P:120: each newly active u tries each out-edge once with probability p_uv.
  * LT per Eq. 1: thresholds tau_v ~ U(0,1); v activates when the summed weight of
  * its active in-neighbours reaches tau_v (iterated to the fixpoint, which is order-free).
+ * Reading R30: tau_v = (o + 1/2) / 2^32 (o = the tag-11 draw of v) is compared EXACTLY — WC
+ * (w = 1/d_in(v)): cnt * 2^33 >= (2o + 1) * d_in(v); explicit weights in the fixed point of R18
+ * (W = floor(w 2^32)): sum W >= o + 1 — so the activated set has no rounding-order dependence.
  * Randomness: Philox keyed (mc_seed; trial, tag-11 slot), independent of any RR stream.
  * ------------------------------------------------------------------------------------------ */
 static void build_out_csr(og_ctx* c) {
@@ -485,7 +488,7 @@ int og_mc_spread(og_ctx* c, const uint32_t* S, uint32_t k, uint64_t trials, uint
                  double* mean_out, double* stderr_out) {
   uint32_t* q = (uint32_t*)malloc(sizeof(uint32_t) * c->n);
   uint8_t* act = (uint8_t*)calloc(c->n, 1);
-  double* acc = (double*)calloc(c->n, sizeof(double));
+  uint64_t* acc = (uint64_t*)calloc(c->n, sizeof(uint64_t));
   uint32_t* touched = (uint32_t*)malloc(sizeof(uint32_t) * (c->m + c->n + 1));
   double sum = 0.0, sum2 = 0.0;
   uint64_t t;
@@ -499,28 +502,32 @@ int og_mc_spread(og_ctx* c, const uint32_t* S, uint32_t k, uint64_t trials, uint
       uint64_t e;
       for (e = c->out_ptr[u]; e < c->out_ptr[u + 1]; ++e) {
         uint32_t v = c->out_dst[e];
-        double p;
         if (act[v]) continue;
-        p = edge_p(c, c->out_in_slot[e], v);
         if (c->model == OG_IC) {
+          double p = edge_p(c, c->out_in_slot[e], v);
           uint32_t o[4];
           keyed(mc_seed, t, SLOT_MC | (e >> 2), o);
           if ((double)o[e & 3] < p * 4294967296.0) { act[v] = 1; q[tail++] = v; }
         } else {
           uint32_t o[4];
-          double tau;
-          keyed(mc_seed, t, SLOT_MC | (((uint64_t)1) << 40) | (uint64_t)v, o);
-          tau = ((double)o[0] + 0.5) / 4294967296.0;      /* tau_v ~ U(0,1) */
-          if (acc[v] == 0.0) touched[ntouch++] = v;
-          acc[v] += p;
-          if (acc[v] >= tau) { act[v] = 1; q[tail++] = v; }
+          int met;
+          keyed(mc_seed, t, SLOT_MC | (((uint64_t)1) << 40) | (uint64_t)v, o);   /* tau_v */
+          if (acc[v] == 0) touched[ntouch++] = v;
+          if (c->scheme == OG_W_WC) {
+            acc[v] += 1;                                   /* active in-neighbours */
+            met = ((unsigned __int128)acc[v] << 33) >= (unsigned __int128)(2 * (uint64_t)o[0] + 1) * deg_in(c, v);
+          } else {
+            acc[v] += c->thr_edge[c->out_in_slot[e]];     /* LT: floor(w 2^32) */
+            met = acc[v] >= (uint64_t)o[0] + 1;
+          }
+          if (met) { act[v] = 1; q[tail++] = v; }
         }
       }
     }
     sum += (double)tail;
     sum2 += (double)tail * (double)tail;
     for (i = 0; i < tail; ++i) act[q[i]] = 0;
-    for (i = 0; i < ntouch; ++i) acc[touched[i]] = 0.0;
+    for (i = 0; i < ntouch; ++i) acc[touched[i]] = 0;
   }
   *mean_out = sum / (double)trials;
   {

@@ -1221,7 +1221,7 @@ gim_status gim_mc_spread(gim_ctx* c, const uint32_t* seeds, uint32_t k, uint64_t
   if (!c) return GIM_EINVAL;
   c->err.clear();
   if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
-  if (c->model != GIM_IC) return fail(c, GIM_EINVAL, "forward Monte-Carlo is implemented for IC only");
+  if (c->model == GIM_LT && trials >= 0xFFFFFFull) return fail(c, GIM_EINVAL, "LT forward MC: trials < 2^24 - 1");
   if (!seeds || k < 1 || trials < 1 || !mean_out) return fail(c, GIM_EINVAL, "seeds, k >= 1, trials >= 1, mean_out required");
   for (uint32_t i = 0; i < k; ++i)
     if (seeds[i] >= c->n) return fail(c, GIM_EINVAL, "seed id out of range");
@@ -1248,7 +1248,15 @@ gim_status gim_mc_spread(gim_ctx* c, const uint32_t* seeds, uint32_t k, uint64_t
     c->out_valid = true;
   }
   TRY(ensure_giant_slots(c, 2u * (uint32_t)c->num_sms));   // one MC trial per slot at a time
-  const uint32_t mc_grid = std::min<uint32_t>(c->giant_slots, 2u * (uint32_t)c->num_sms);
+  uint32_t mc_grid = std::min<uint32_t>(c->giant_slots, 2u * (uint32_t)c->num_sms);
+  DevBuf lt_acc;                                   // LT: per-slot 64-bit (trial tag | accumulator)
+  if (c->model == GIM_LT) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    mc_grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(mc_grid, (free_b / 4) / (n * 8 + 1)));
+    TRY(dalloc(c, lt_acc, (uint64_t)mc_grid * n * 8));
+    CK(cudaMemsetAsync(lt_acc.p, 0, (uint64_t)mc_grid * n * 8, c->stream));
+  }
   DevBuf dseeds, dsizes, dclaim;
   TRY(dalloc(c, dseeds, (uint64_t)k * 4));
   TRY(dalloc(c, dsizes, trials * 4));
@@ -1260,10 +1268,14 @@ gim_status gim_mc_spread(gim_ctx* c, const uint32_t* seeds, uint32_t k, uint64_t
                                c->out_in.as<uint32_t>(), c->thr_wc.as<uint32_t>(), c->thr_edge.as<uint64_t>(),
                                c->thr_uniform, dseeds.as<uint32_t>(), k, trials, mc_seed,
                                dclaim.as<unsigned long long>(), dsizes.as<uint32_t>(), c->bitmaps.as<uint32_t>(),
-                               c->gqueues.as<uint32_t>(), bm_words, (int)mc_grid, c->stream), "k_mc_ic"));
+                               c->gqueues.as<uint32_t>(), bm_words, (int)mc_grid, c->stream,
+                               c->row_ptr.as<uint32_t>(),
+                               c->model == GIM_LT ? lt_acc.as<unsigned long long>() : nullptr),
+               c->model == GIM_LT ? "k_mc_lt" : "k_mc_ic"));
   std::vector<uint32_t> sz(trials);
   CK(cudaMemcpyAsync(sz.data(), dsizes.p, trials * 4, cudaMemcpyDeviceToHost, c->stream));
   TRY(sync(c));
+  dfree(c, lt_acc);
   dfree(c, dseeds);
   dfree(c, dsizes);
   dfree(c, dclaim);

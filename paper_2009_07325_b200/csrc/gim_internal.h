@@ -67,5 +67,6 @@ cudaError_t launch_mc_ic(int scheme, uint32_t n, const uint32_t* out_ptr, const 
                          const uint32_t* out_in, const uint32_t* thr_wc, const uint64_t* thr_edge,
                          uint64_t thr_uniform, const uint32_t* seeds, uint32_t k, uint64_t trials, uint64_t mc_seed,
                          unsigned long long* claim, uint32_t* sizes, uint32_t* bitmaps, uint32_t* queues,
-                         uint64_t bm_words, int grid, cudaStream_t s);
+                         uint64_t bm_words, int grid, cudaStream_t s, const uint32_t* row_ptr = nullptr,
+                         unsigned long long* lt_accs = nullptr);   // lt_accs set: LT forward process
 }  // namespace gim

@@ -192,6 +192,110 @@ __global__ void __launch_bounds__(kMcThreads, 2) k_mc_ic(McParams p, uint32_t* b
   }
 }
 
+// LT forward process (Eq. 1) with the exact threshold comparison of reading R30:
+// tau_v = (o + 1/2) / 2^32, o = word 0 of Philox(mc_seed; t, tag 11 | 2^40 | v); v activates when
+// its active in-neighbours reach it — WC: cnt * 2^33 >= (2o + 1) * d_in(v); explicit: sum of
+// W = floor(w 2^32) >= o + 1. Per slot and node a 64-bit accumulator (trial tag << 40 | acc),
+// updated by CAS: the update that crosses the threshold activates v (exactly once), so the
+// activated set is the order-free fixpoint, trial by trial equal to the oracle's.
+template <int SCHEME>
+__device__ __forceinline__ bool lt_met(uint64_t acc, uint32_t o, uint32_t d) {
+  if (SCHEME == W_WC) return ((unsigned __int128)acc << 33) >= (unsigned __int128)(2ull * o + 1ull) * d;
+  return acc >= (uint64_t)o + 1ull;
+}
+
+template <int SCHEME>
+__global__ void __launch_bounds__(kMcThreads, 2) k_mc_lt(McParams p, const uint32_t* __restrict__ row_ptr,
+                                                        uint32_t* bitmaps, uint32_t* queues, uint64_t bm_words,
+                                                        unsigned long long* accs) {
+  __shared__ unsigned long long s_t;
+  __shared__ uint32_t s_head, s_tail;
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t* bm = bitmaps + (uint64_t)blockIdx.x * bm_words;
+  uint32_t* Q = queues + (uint64_t)blockIdx.x * p.n;
+  unsigned long long* acc = accs + (uint64_t)blockIdx.x * p.n;
+  while (true) {
+    if (threadIdx.x == 0) {
+      s_t = atomicAdd(p.claim, 1ull);
+      s_tail = 0;
+    }
+    __syncthreads();
+    const unsigned long long t = s_t;
+    if (t >= p.trials) break;
+    const unsigned long long tag = (t % 0xFFFFFFull) + 1ull;   // 24-bit, never 0 (= untouched)
+    for (uint32_t i = threadIdx.x; i < p.k; i += blockDim.x) {
+      const uint32_t u = p.seeds[i];
+      const uint32_t bit = 1u << (u & 31);
+      if (!(atomicOr(bm + (u >> 5), bit) & bit)) Q[atomicAdd(&s_tail, 1u)] = u;
+    }
+    __syncthreads();
+    uint32_t lo = 0, hi = s_tail;
+    while (lo < hi) {
+      if (threadIdx.x == 0) s_head = lo;
+      __syncthreads();
+      while (true) {
+        uint32_t f = 0;
+        if (lane == 0) f = atomicAdd(&s_head, 32u);
+        f = __shfl_sync(kFull, f, 0);
+        if (f >= hi) break;
+        const uint32_t c = min(32u, hi - f);
+        uint32_t a = 0, b = 0, nv = 0;
+        if (lane < c) {
+          const uint32_t u = Q[f + lane];
+          a = p.out_ptr[u];
+          b = p.out_ptr[u + 1];
+          nv = b - a;
+        }
+        // flattened sweep over the batch's out-slots, one slot per lane
+        uint32_t P = nv;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, P, off);
+          if ((int)lane >= off) P += y;
+        }
+        const uint32_t total = __shfl_sync(kFull, P, 31);
+        const uint32_t E = P - nv;
+        for (uint32_t base = 0; base < total; base += 32) {
+          const uint32_t gi = base + lane;
+          const uint32_t kk = warp_owner(P, gi < total ? gi : total - 1);
+          const uint32_t ek = __shfl_sync(kFull, a - E, kk);
+          if (gi >= total) continue;
+          const uint32_t e = ek + gi;
+          const uint32_t v = p.out_dst[e];
+          const uint32_t bit = 1u << (v & 31);
+          if (bm[v >> 5] & bit) continue;                   // already active
+          const uint64_t inc = (SCHEME == W_WC) ? 1ull : p.thr_edge[p.out_in[e]];
+          unsigned long long old = acc[v], prev, nw;
+          uint64_t cur;
+          while (true) {
+            cur = ((old >> 40) == tag) ? (old & ((1ull << 40) - 1ull)) : 0ull;
+            nw = (tag << 40) | (cur + inc);
+            prev = atomicCAS(acc + v, old, nw);
+            if (prev == old) break;
+            old = prev;
+          }
+          const uint32_t o = philox4x32_10_rk(make_uint4((uint32_t)t, (uint32_t)(t >> 32), v, kSlotMcHi | 0x100u), p.rk).x;
+          const uint32_t d = (SCHEME == W_WC) ? row_ptr[v + 1] - row_ptr[v] : 0u;
+          if (lt_met<SCHEME>(cur + inc, o, d) && !lt_met<SCHEME>(cur, o, d) &&
+              !(atomicOr(bm + (v >> 5), bit) & bit))
+            Q[atomicAdd(&s_tail, 1u)] = v;
+        }
+      }
+      __syncthreads();
+      lo = hi;
+      hi = s_tail;
+      __syncthreads();
+    }
+    const uint32_t size = hi;
+    if (threadIdx.x == 0) p.sizes[t] = size;
+    for (uint32_t i = threadIdx.x; i < size; i += blockDim.x) {
+      bm[Q[i] >> 5] = 0u;
+      Q[i] = kEmpty;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 // Out-CSR of the in-CSR: out_ptr[n+1], out_dst[m], out_in[m] (in-slot of each out-slot, rows
@@ -245,7 +349,8 @@ cudaError_t launch_mc_ic(int scheme, uint32_t n, const uint32_t* out_ptr, const 
                          const uint32_t* out_in, const uint32_t* thr_wc, const uint64_t* thr_edge,
                          uint64_t thr_uniform, const uint32_t* seeds, uint32_t k, uint64_t trials, uint64_t mc_seed,
                          unsigned long long* claim, uint32_t* sizes, uint32_t* bitmaps, uint32_t* queues,
-                         uint64_t bm_words, int grid, cudaStream_t s) {
+                         uint64_t bm_words, int grid, cudaStream_t s, const uint32_t* row_ptr,
+                         unsigned long long* lt_accs) {
   McParams p{};
   p.n = n;
   p.out_ptr = out_ptr;
@@ -266,6 +371,11 @@ cudaError_t launch_mc_ic(int scheme, uint32_t n, const uint32_t* out_ptr, const 
   }
   p.claim = claim;
   p.sizes = sizes;
+  if (lt_accs) {
+    if (scheme == W_WC) k_mc_lt<W_WC><<<grid, kMcThreads, 0, s>>>(p, row_ptr, bitmaps, queues, bm_words, lt_accs);
+    else k_mc_lt<W_EXPLICIT><<<grid, kMcThreads, 0, s>>>(p, row_ptr, bitmaps, queues, bm_words, lt_accs);
+    return cudaGetLastError();
+  }
   if (scheme == W_WC) k_mc_ic<W_WC><<<grid, kMcThreads, 0, s>>>(p, bitmaps, queues, bm_words);
   else if (scheme == W_UNIFORM) k_mc_ic<W_UNIFORM><<<grid, kMcThreads, 0, s>>>(p, bitmaps, queues, bm_words);
   else k_mc_ic<W_EXPLICIT><<<grid, kMcThreads, 0, s>>>(p, bitmaps, queues, bm_words);

@@ -74,11 +74,49 @@ def test_mc_verified_spread_full_size(key):
     assert abs(mean - ris) / mean < 0.01, (mean, ris, r.spread_est)
 
 
+@pytest.mark.parametrize("scheme", [gi.W_WC, gi.W_EXPLICIT])
+def test_mc_lt_equals_oracle_tiny(scheme):
+    """LT forward process (reading R30: exact threshold comparison) bit-exact with the oracle."""
+    for g0 in (gi.diamond(), gi.cycle_plus(), gi.random_small(30, 200, 2), gi.random_small(12, 60, 1)):
+        g = g0
+        if scheme == gi.W_EXPLICIT:
+            rng = np.random.default_rng(g.n)
+            din = g0.in_degree()
+            dst = np.repeat(np.arange(g0.n), din)
+            g = gi.with_weights(g0, (rng.uniform(0.0, 1.0, size=g0.m) / np.maximum(din[dst], 1)).astype(np.float32))
+        c = _ctx(g, gi.LT, scheme)
+        o = oracle.Oracle(g, gi.LT, scheme)
+        for S in ([0], [1, 2], [0, 0, 3]):
+            S = [s % g.n for s in S]
+            assert c.mc_spread(S, 4001, 99) == o.mc_spread(S, 4001, 99), S
+
+
+def test_mc_lt_equals_oracle_C1():
+    w = gi.WORKLOADS["C1"]
+    g = gi.workload_graph("C1")
+    c = _ctx(g, gi.LT, gi.W_WC)
+    c.generate_rr(20000, w.rr_seed)
+    seeds, _, _ = c.select(50)
+    assert c.mc_spread(seeds, 2001, 5) == oracle.Oracle(g, gi.LT, gi.W_WC).mc_spread(seeds, 2001, 5)
+
+
+def test_mc_lt_verified_spread_C4():
+    """C4 (LT): forward MC of IMM's seeds within 1% of n * F_R'(S) on an independent pool."""
+    w = gi.WORKLOADS["C4"]
+    g = gi.workload_graph("C4")
+    c = _ctx(g, w.model, w.scheme)
+    r = c.imm(w.k, w.eps, w.ell, w.rr_seed)
+    T = 1 << 21
+    c2 = _ctx(g, w.model, w.scheme)
+    c2.generate_rr(T, w.rr_seed + 1)
+    ris = _ris_estimate(c2, g.n, r.seeds, T)
+    mean, se = c.mc_spread(r.seeds, 2000, 17)
+    assert se / mean < 0.004, (mean, se)
+    assert abs(mean - ris) / mean < 0.01, (mean, ris, r.spread_est)
+
+
 def test_mc_errors():
     g = gi.diamond()
-    c = _ctx(g, gi.LT, gi.W_WC)
-    with pytest.raises(P.GimError):
-        c.mc_spread([0], 10, 1)                                  # LT: not implemented
     c = _ctx(g, gi.IC, gi.W_WC)
     with pytest.raises(P.GimError):
         c.mc_spread([7], 10, 1)                                  # seed out of range

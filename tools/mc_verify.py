@@ -18,7 +18,7 @@ import paper_2009_07325_b200 as P  # noqa: E402
 
 def main():
     out = open(os.path.join(ROOT, "gpurun_out", "mc_verify.jsonl"), "a")
-    for key in sys.argv[1:]:
+    for key in [a for a in sys.argv[1:] if not a.startswith("--")]:
         w = gi.WORKLOADS[key]
         g = gi.workload_graph(key)
         c = P.Gim(0)
@@ -35,10 +35,10 @@ def main():
         ris = g.n * hit.mean()
         ris_se = g.n * np.sqrt(hit.mean() * (1 - hit.mean()) / T)
         t0 = time.perf_counter()
-        if w.model == gi.IC:
+        if "--host-lt" not in sys.argv or w.model == gi.IC:
             trials, mc_impl = 2000, "gpu gim_mc_spread"
             mean, se = c.mc_spread(r.seeds, trials, 17)
-        else:   # LT: forward MC only in the oracle (host, single-threaded, bounded trials)
+        else:   # LT with the oracle's forward MC on the host (single-threaded, bounded trials)
             import oracle
             trials, mc_impl = 400, "oracle og_mc_spread (host)"
             mean, se = oracle.Oracle(g, w.model, w.scheme, w.p_uniform).mc_spread(r.seeds, trials, 17)

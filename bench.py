@@ -271,6 +271,11 @@ def run_gim(args, w):
     value = total_sets / (ms / 1000.0)
     r0 = results[-1]
 
+    # RR-set size distribution of the last IMM run's pool, outside the timing
+    sizes = np.diff(ctx.rr_offsets().astype(np.int64))
+    size_q = ({"p50": int(np.percentile(sizes, 50)), "p99": int(np.percentile(sizes, 99)),
+               "max": int(sizes.max())} if len(sizes) else None)
+
     # ---- dominant kernel roofline: K-RR (warp-per-RR sampling), ALU-bound by Philox ----------
     rr_ms = st["ms_rr"]
     n_rr = max(st["n_rr_launches"], 1)
@@ -380,7 +385,8 @@ def run_gim(args, w):
                 "rr_stats": {"mean_len": st["rr_elements"] / max(st["rr_sets"], 1),
                              "coins_per_set": (st["coins"] + st["coins_giant"]) / max(st["rr_sets"], 1),
                              "giant_frac": st["giant_sets"] / max(st["rr_sets"], 1),
-                             "coins_per_giant_set": st["coins_giant"] / max(st["giant_sets"], 1)},
+                             "coins_per_giant_set": st["coins_giant"] / max(st["giant_sets"], 1),
+                             "size_quantiles": size_q},
                 "gpu_launches": st["launches"],
                 "step_wall_ms": [round(x, 3) for x in step_wall],
                 "host": {"api_ms_per_step": st["host_ms_api"] / args.steps,

@@ -244,6 +244,16 @@ class Gim:
                                             _ptr(off), _ptr(nodes), int(sort_each_set)))
         return ids[:ns.value], off, nodes[:pl.value]
 
+    def rr_offsets(self) -> np.ndarray:
+        """offsets[n_sets + 1] of this rank's pool only (gim_rr_export without the members)."""
+        ns, pl = _u64(), _u64()
+        self._check(self._lib.gim_rr_export(self._h, ctypes.byref(ns), ctypes.byref(pl), None, None,
+                                            None, 0))
+        off = np.zeros(ns.value + 1, dtype=np.uint64)
+        self._check(self._lib.gim_rr_export(self._h, ctypes.byref(ns), ctypes.byref(pl), None,
+                                            _ptr(off), None, 0))
+        return off
+
     def counts_export(self, n: int) -> np.ndarray:
         out = np.zeros(n, dtype=np.uint32)
         self._check(self._lib.gim_counts_export(self._h, _ptr(out)))

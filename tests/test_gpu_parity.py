@@ -85,7 +85,9 @@ def test_pool_parity_tiny(gname):
 @pytest.mark.parametrize("opts", [{}, {P.OPT_FORCE_GIANT: 1}, {P.OPT_QUEUE_CAP: 4},
                                   {P.OPT_STAGING_CAP: 64}, {P.OPT_QUEUE_CAP: 32, P.OPT_STAGING_CAP: 1000},
                                   {P.OPT_IC_LANE: 1}, {P.OPT_IC_LANE: 1, P.OPT_STAGING_CAP: 64},
-                                  {P.OPT_IC_LANE: 1, P.OPT_FORCE_GIANT: 1}, {P.OPT_IC_LANE: 1, P.OPT_QUEUE_CAP: 8}])
+                                  {P.OPT_IC_LANE: 1, P.OPT_FORCE_GIANT: 1}, {P.OPT_IC_LANE: 1, P.OPT_QUEUE_CAP: 8},
+                                  {P.OPT_FORCE_GIANT: 1, P.OPT_GIANT_NT: 128}, {P.OPT_QUEUE_CAP: 16, P.OPT_GIANT_NT: 128},
+                                  {P.OPT_FORCE_GIANT: 1, P.OPT_GIANT_NT: 256}])
 def test_pool_parity_C1_invariance(opts):
     """Same pool whatever the queue capacity, forced fallback or staging retries."""
     w = gi.WORKLOADS["C1"]
@@ -254,7 +256,7 @@ def test_imm_parity_BA_small():
     assert np.array_equal(r.seeds, ro.seeds), (r.seeds, ro.seeds)
 
 
-@pytest.mark.parametrize("key", ["C3", "C4", "B8", pytest.param("C5", marks=pytest.mark.skipif(
+@pytest.mark.parametrize("key", ["C3", "C4", "B8", "B32", pytest.param("C5", marks=pytest.mark.skipif(
     os.environ.get("GIM_TEST_C5") != "1", reason="C5 graph generation takes minutes: set GIM_TEST_C5=1"))])
 def test_full_size_sampled(key):
     """BASELINE.json full size: 2^21 RR sets in the launch configuration bench.py times; sampled

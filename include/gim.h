@@ -215,6 +215,9 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *  GIM_OPT_FRESH_FINAL  = 0 (default: IMM's published reuse of the estimation sets, R8) / 1:
  *                         gim_imm's final phase samples a fresh pool of ceil(theta) sets with the
  *                         key seed ^ 0x9E3779B97F4A7C15 (reading R29; the Chen 2018 fix [EXT]).
+ *  GIM_OPT_SELECT_PERSISTENT = 0 (default) / 1: for P = 1 (or a replicated pool) run the k
+ *                         greedy steps of a selection in one cooperative launch with grid
+ *                         barriers between the argmax and cover phases (no candidate list).
  *  GIM_OPT_MB_CHAINS    = 1 / 4 / 8 (default 8): interleaved Philox chains per thread in
  *                          gim_microbench_philox. */
 typedef enum {
@@ -230,7 +233,8 @@ typedef enum {
   GIM_OPT_MB_CHAINS = 11,
   GIM_OPT_PDL = 12,
   GIM_OPT_GIANT_NT = 13,
-  GIM_OPT_FRESH_FINAL = 14
+  GIM_OPT_FRESH_FINAL = 14,
+  GIM_OPT_SELECT_PERSISTENT = 15
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

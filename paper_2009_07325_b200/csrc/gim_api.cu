@@ -85,6 +85,8 @@ struct gim_ctx {
   uint32_t giant_n = 0;             // n the giant slots were sized for (reused while n <= giant_n)
   int giant_nt_opt = 0;             // GIM_OPT_GIANT_NT: 0 auto, else threads per giant CTA
   int fresh_final = 0;              // GIM_OPT_FRESH_FINAL (reading R29)
+  int sel_persistent = 0;           // GIM_OPT_SELECT_PERSISTENT: k steps in one cooperative launch
+  DevBuf sel_bar;
   double giant_per_slot = 0.0;      // giant sets per default slot in the previous chunk
   bool giant_cap_reached = false;
   uint64_t stage_cap = 0;
@@ -737,7 +739,16 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
     TRY(launched(c, launch_cand_setup(c->cnt.as<uint32_t>(), (uint32_t)n, kMaxCand, hist, tau_p1, cand, ncand,
                                       c->num_sms * 4, c->stream), "candidate setup", 3));
   }
-  if (!dec && c->use_graph) {
+  if (!dec && !cand && c->sel_persistent) {
+    // P = 1: the k greedy steps in one cooperative launch, grid barriers between the phases
+    TRY(ensure(c, c->sel_bar, 64));
+    CK(cudaMemsetAsync(c->sel_bar.p, 0, 8, c->stream));
+    Prof pf(c, CLS_SELECT);
+    TRY(launched(c, launch_select_persistent(c->cnt.as<uint32_t>(), (uint32_t)n, keys, (int)kk, segd,
+                                             c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
+                                             c->covered.as<uint8_t>(), mr, limited, c->sel_bar.as<unsigned int>(),
+                                             c->num_sms, c->stream), "k_select_persistent"));
+  } else if (!dec && c->use_graph) {
     // P = 1: the 2k argmax/cover launches replayed from a CUDA graph (captured once per set of
     // buffer pointers; steady-state IMM runs reuse it), so the GPU runs them back to back.
     const std::vector<uintptr_t> key = {(uintptr_t)c->cnt.p, (uintptr_t)segd, (uintptr_t)cand,
@@ -910,7 +921,7 @@ void gim_destroy(gim_ctx* c) {
                     &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
                     &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->thr_node, &c->ag_small,
-                    &c->ag_send, &c->ag_recv};
+                    &c->ag_send, &c->ag_recv, &c->sel_bar};
   for (auto& sg : c->iseg) {
     dfree(c, sg.off);
     dfree(c, sg.inv);
@@ -1318,6 +1329,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_MB_CHAINS: c->mb_chains = (int)value; return GIM_OK;
     case GIM_OPT_SPECULATE: c->speculate = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_FRESH_FINAL: c->fresh_final = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_SELECT_PERSISTENT: c->sel_persistent = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_GIANT_NT:
       if (value != 0 && value != kGiantThreads && value != kGiantThreadsNarrow)
         return fail(c, GIM_EINVAL, "giant CTA width must be 0 (auto), 256 or 128");

@@ -52,6 +52,10 @@ struct InvSegDev;
 struct MrimSel {
   uint32_t rounds, n, k;
 };
+cudaError_t launch_select_persistent(uint32_t* cnt, uint32_t n, unsigned long long* keys, int kk,
+                                     const InvSegDev* segs, const uint64_t* offsets, const uint32_t* pool,
+                                     uint8_t* covered, const MrimSel* mr, bool limit, unsigned int* bar,
+                                     int num_sms, cudaStream_t s);
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,
                          const uint64_t* offsets, const uint32_t* pool,
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s,

@@ -10,6 +10,8 @@
 // so a selection touches each pool element at most once for decrements. The argmax is one
 // streaming pass with a packed 64-bit key (count << 32 | ~v) reduced by warp shuffles and one
 // atomicMax per CTA; the previous pick is retired inside the same pass (count = sentinel).
+#include <algorithm>
+
 #include "gim_device.cuh"
 #include "gim_internal.h"
 
@@ -176,15 +178,13 @@ __device__ __forceinline__ void argmax_one(uint32_t c, uint32_t v, unsigned long
   best = key > best ? key : best;
 }
 
-__global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int32_t* __restrict__ dec,
-                                                uint32_t n, unsigned long long* __restrict__ keys, int j,
-                                                const uint32_t* __restrict__ tau_p1, uint32_t excl) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ void argmax_step(uint32_t* __restrict__ cnt, int32_t* __restrict__ dec,
+                                            uint32_t n, unsigned long long* __restrict__ keys, int j,
+                                            const uint32_t* __restrict__ tau_p1, uint32_t excl) {
   // candidate mode: the candidate argmax already found a count >= tau_p1, which no node outside
   // the candidate list can reach (their counts started below it and only decrease)
   if (tau_p1 != nullptr && (uint32_t)(keys[j] >> 32) >= *tau_p1 && keys[j] != 0ull) return;
-  __shared__ unsigned long long s_best[8];
+  __shared__ unsigned long long s_best[32];   // up to 1024 threads per CTA
   unsigned long long best = 0;
   const uint32_t n4 = n >> 2;
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -245,6 +245,14 @@ __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int3
     }
     if (threadIdx.x == 0 && best) atomicMax(keys + j, best);
   }
+}
+
+__global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int32_t* __restrict__ dec,
+                                                uint32_t n, unsigned long long* __restrict__ keys, int j,
+                                                const uint32_t* __restrict__ tau_p1, uint32_t excl) {
+  pdl_wait();
+  pdl_trigger();
+  argmax_step(cnt, dec, n, keys, j, tau_p1, excl);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -395,19 +403,16 @@ __global__ void __launch_bounds__(256) k_argmax_cand(const uint32_t* __restrict_
 constexpr int kCoverIlp = GIM_COVER_ILP;
 
 template <bool LIMIT>
-__global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restrict__ keys, int j,
-                                               const InvSegDev* __restrict__ segs,
-                                               const uint32_t* __restrict__ nseg_ptr_unused,
-                                               const uint64_t* __restrict__ offsets,
-                                               const uint32_t* __restrict__ pool,
-                                               uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
-                                               int32_t* __restrict__ dec, MrimSel mr) {
+__device__ __forceinline__ void cover_step(const unsigned long long* __restrict__ keys, int j,
+                                           const InvSegDev* __restrict__ segs,
+                                           const uint64_t* __restrict__ offsets,
+                                           const uint32_t* __restrict__ pool,
+                                           uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
+                                           int32_t* __restrict__ dec, MrimSel mr) {
   __shared__ uint64_t s_lo[kMaxInvSeg], s_end[kMaxInvSeg];   // list start, inclusive prefix end
   __shared__ const uint32_t* s_inv[kMaxInvSeg];
   __shared__ uint32_t s_nseg, s_limit;
   const uint32_t sub = threadIdx.x & 7;
-  pdl_wait();
-  pdl_trigger();
   const uint32_t u = ~(uint32_t)keys[j];
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[u] = kSent;   // retire the pick (never decremented)
   if (threadIdx.x < 32) {                     // lanes load the segments' list bounds in parallel
@@ -485,6 +490,59 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
         else atomicAdd(dec + w[t], 1);
       }
     }
+  }
+}
+
+template <bool LIMIT>
+__global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restrict__ keys, int j,
+                                               const InvSegDev* __restrict__ segs,
+                                               const uint32_t* __restrict__ nseg_ptr_unused,
+                                               const uint64_t* __restrict__ offsets,
+                                               const uint32_t* __restrict__ pool,
+                                               uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
+                                               int32_t* __restrict__ dec, MrimSel mr) {
+  pdl_wait();
+  pdl_trigger();
+  cover_step<LIMIT>(keys, j, segs, offsets, pool, covered, cnt, dec, mr);
+}
+
+// Grid-wide barrier of a co-resident (cooperatively launched) grid: generation counter; the
+// arriving CTA reads the generation before arriving, the last arrival resets the count and bumps
+// the generation; fences order every CTA's writes of the phase before the next phase's reads.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// The k greedy steps of one NodeSelection in ONE cooperative launch (P = 1): per step the argmax
+// phase and the cover phase of the kernels above, separated by grid barriers instead of kernel
+// boundaries (GIM_OPT_SELECT_PERSISTENT).
+template <bool LIMIT>
+__global__ void __launch_bounds__(1024, 1) k_select_persistent(uint32_t* __restrict__ cnt, uint32_t n,
+                                                           unsigned long long* __restrict__ keys, int kk,
+                                                           const InvSegDev* __restrict__ segs,
+                                                           const uint64_t* __restrict__ offsets,
+                                                           const uint32_t* __restrict__ pool,
+                                                           uint8_t* __restrict__ covered, MrimSel mr,
+                                                           uint32_t excl, unsigned int* bar) {
+  for (int j = 0; j < kk; ++j) {
+    argmax_step(cnt, nullptr, n, keys, j, nullptr, excl);
+    grid_barrier(bar);
+    cover_step<LIMIT>(keys, j, segs, offsets, pool, covered, cnt, nullptr, mr);
+    grid_barrier(bar);
   }
 }
 
@@ -588,6 +646,19 @@ cudaError_t launch_cand_setup(const uint32_t* cnt, uint32_t n, uint32_t kmax, un
 cudaError_t launch_argmax_cand(const uint32_t* cnt, const uint32_t* cand, const unsigned int* ncand,
                                unsigned long long* keys, int j, int grid, cudaStream_t s) {
   return launch_pdl(k_argmax_cand, grid, 256, s, cnt, cand, ncand, keys, j);
+}
+
+cudaError_t launch_select_persistent(uint32_t* cnt, uint32_t n, unsigned long long* keys, int kk,
+                                     const InvSegDev* segs, const uint64_t* offsets, const uint32_t* pool,
+                                     uint8_t* covered, const MrimSel* mr, bool limit, unsigned int* bar,
+                                     int num_sms, cudaStream_t s) {
+  const MrimSel m = mr ? *mr : MrimSel{1u, 0u, 0u};
+  const uint32_t excl = mr ? 0x80000000u : 0u;
+  void* kern = limit ? (void*)k_select_persistent<true> : (void*)k_select_persistent<false>;
+  // one 1024-thread CTA per SM: the grid barrier's arrival counter sees #SM atomics, not 4-8x more
+  const int grid = num_sms;
+  void* args[] = {&cnt, &n, &keys, &kk, &segs, &offsets, &pool, &covered, (void*)&m, (void*)&excl, &bar};
+  return cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(1024), args, 0, s);
 }
 
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,

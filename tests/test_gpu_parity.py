@@ -474,3 +474,29 @@ def test_replicated_pool_emulation_equals_single(Pn, rounds):
             assert np.array_equal(np.sort(nodes[off[i]:off[i + 1]]), np.sort(rnodes[roff[i]:roff[i + 1]]))
         assert np.array_equal(cnt, rcnt)
         assert np.array_equal(imm.seeds, rimm.seeds) and imm.R_final == rimm.R_final and imm.LB == rimm.LB
+
+
+@pytest.mark.parametrize("rounds", [1, 3])
+def test_select_persistent_equals_oracle(rounds):
+    """GIM_OPT_SELECT_PERSISTENT: the k greedy steps in one cooperative launch (grid barriers
+    between argmax and cover) — seeds, gains and coverage bit-exact, standard and MRIM."""
+    w = gi.WORKLOADS["C2"]
+    g = gi.workload_graph("C2")
+    N = 20011 if rounds == 1 else 5003
+    k = 50 if rounds == 1 else 10
+    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_PERSISTENT: 1})
+    c.set_rounds(rounds)
+    c.generate_rr(N, w.rr_seed)
+    o = oracle.Oracle(g, w.model, w.scheme)
+    if rounds == 1:
+        o.generate(N, w.rr_seed)
+        ref = o.select(k)
+    else:
+        o.mrim_generate(N, rounds, w.rr_seed)
+        ref = o.mrim_select(k)
+    for _ in range(2):                                     # non-destructive, repeatable
+        s, gn, cov = c.select(k)
+        assert np.array_equal(s, ref[0]) and np.array_equal(gn, ref[1]) and cov == ref[2]
+    r = c.imm(k, w.eps, w.ell, w.rr_seed)
+    ro = o.imm(k, w.eps, w.ell, w.rr_seed) if rounds == 1 else o.mrim(k, rounds, w.eps, w.ell, w.rr_seed)
+    assert np.array_equal(r.seeds, ro.seeds) and r.R_final == ro.R_final

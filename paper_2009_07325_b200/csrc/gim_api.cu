@@ -34,6 +34,10 @@ constexpr uint32_t kChunk = 1u << 22;   // RR ids per generation chunk (bounds s
 #define GIM_ARGMAX_CTAS 4
 #endif
 constexpr int kArgmaxCtasPerSM = GIM_ARGMAX_CTAS;   // k_argmax grid = this x #SMs (256 threads each)
+#ifndef GIM_COVER_CTAS
+#define GIM_COVER_CTAS 8
+#endif
+constexpr int kCoverCtasPerSM = GIM_COVER_CTAS;     // k_cover grid = this x #SMs (256 threads each)
 
 
 }  // namespace
@@ -640,8 +644,10 @@ gim_status replicate_round(gim_ctx* c, uint64_t a, uint64_t theta, uint64_t set0
   return GIM_OK;
 }
 
-// theta counts sets in API units: RR sets, or MRIM sets of `rounds` standard ids each (R26)
-gim_status generate(gim_ctx* c, uint64_t theta_sets, uint64_t seed) {
+// theta counts sets in API units: RR sets, or MRIM sets of `rounds` standard ids each (R26).
+// host_sync = false (inside gim_imm): the selection that follows is enqueued behind the index
+// build without a host round trip; errors surface at its completion sync.
+gim_status generate(gim_ctx* c, uint64_t theta_sets, uint64_t seed, bool host_sync = true) {
   if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
   if (theta_sets >= (1ull << 32) / c->rounds) return fail(c, GIM_EINVAL, "theta * rounds must be < 2^32");
   const uint64_t theta = theta_sets * c->rounds;
@@ -673,7 +679,7 @@ gim_status generate(gim_ctx* c, uint64_t theta_sets, uint64_t seed) {
     }
     c->T_global = theta;
   }
-  return sync(c);
+  return host_sync ? sync(c) : GIM_OK;
 }
 
 // ---- NodeSelection (O7) ---------------------------------------------------------------------
@@ -765,7 +771,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
         launch_argmax(c->cnt.as<uint32_t>(), nullptr, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * kArgmaxCtasPerSM, c->stream,
                       mr != nullptr);
         launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
-                     c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * 8, c->stream,
+                     c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * kCoverCtasPerSM, c->stream,
                      limited, mr);
       }
       CK(cudaStreamEndCapture(c->stream, &graph));
@@ -785,7 +791,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
         TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * kArgmaxCtasPerSM,
                                       c->stream, mr != nullptr), "k_argmax"));
         TRY(launched(c, launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
-                                     c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * 8,
+                                     c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * kCoverCtasPerSM,
                                      c->stream, limited, mr), "k_cover"));
       }
       if (dec && j + 1 < kk) {
@@ -1145,7 +1151,7 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
     const double theta_i = K.lambda_p / x;                   // l.4 (f = lambda', reading R1)
     const uint64_t T = (uint64_t)std::ceil(theta_i);
     const uint64_t R = std::max<uint64_t>(R_sets(), T);      // l.5 (reading R4)
-    TRY(generate(c, R, seed));
+    TRY(generate(c, R, seed, false));
     if (R_sets() > R) TRY(truncate_pool(c, R * c->rounds));  // drop excess speculation
     // speculative target while this round's selection runs: the next round's T if the test
     // fails, capped by ceil(lambda*/x), the largest theta a passing test can produce
@@ -1170,10 +1176,10 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
   if (c->fresh_final) {
     // reading R29: the final phase on a fresh pool of ceil(theta) sets of a second key (the
     // different seed makes generate discard the estimation pool)
-    TRY(generate(c, T, seed ^ 0x9E3779B97F4A7C15ull));
+    TRY(generate(c, T, seed ^ 0x9E3779B97F4A7C15ull, false));
   } else {
     const uint64_t R_final = std::max<uint64_t>(R_last, T);   // reading R8
-    TRY(generate(c, R_final, seed));                         // extends or truncates speculation
+    TRY(generate(c, R_final, seed, false));                  // extends or truncates speculation
   }
   std::vector<uint64_t> gains((size_t)k * c->rounds);
   TRY(select_impl(c, k, seeds, gains.data(), &cov));

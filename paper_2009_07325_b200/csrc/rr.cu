@@ -831,7 +831,10 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
 // sweep of the hub path, and append new nodes with an atomic tail; the set is complete when no
 // node is pending and no warp is busy (the order of expansion cannot change the set).
 // ------------------------------------------------------------------------------------------
-constexpr uint32_t kSplitGroups = 2048;   // hub nodes above this are split across warps
+#ifndef GIM_SPLIT_GROUPS
+#define GIM_SPLIT_GROUPS 2048
+#endif
+constexpr uint32_t kSplitGroups = GIM_SPLIT_GROUPS;   // hub nodes above this are split across warps
 constexpr uint32_t kChunkRing = 128;      // shared ring of published hub chunks
 constexpr uint32_t kBusySlot = 0xFFFFFFFEu; // ring slot being written (node ids are < 2^32 - 2)
 #ifndef GIM_GIANT_DIV

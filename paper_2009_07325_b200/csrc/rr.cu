@@ -838,7 +838,7 @@ constexpr uint32_t kSplitGroups = GIM_SPLIT_GROUPS;   // hub nodes above this ar
 constexpr uint32_t kChunkRing = 128;      // shared ring of published hub chunks
 constexpr uint32_t kBusySlot = 0xFFFFFFFEu; // ring slot being written (node ids are < 2^32 - 2)
 #ifndef GIM_GIANT_DIV
-#define GIM_GIANT_DIV 4
+#define GIM_GIANT_DIV 2
 #endif
 constexpr uint32_t kGiantClaimDiv = GIM_GIANT_DIV;   // batch = pending / this, clamped to [1, 32]
 static_assert(kSplitGroups % kHubGroups == 0, "hub chunks are whole hub steps");

@@ -202,7 +202,10 @@ constexpr uint32_t kClaimBatch = GIM_CLAIM_BATCH;       // RR ids claimed per wa
 constexpr uint32_t kClaimTailDiv = GIM_CLAIM_TAIL_DIV;  // last count/div ids claimed one by one
 constexpr uint32_t kStageChunk = 1024;    // staging elements reserved per warp per atomic
 constexpr int kLtWarps = 8;          // K-LT: warps per CTA
-constexpr int kLtCap = 64;           // K-LT: path entries per lane in shared memory
+#ifndef GIM_LT_CAP
+#define GIM_LT_CAP 64
+#endif
+constexpr int kLtCap = GIM_LT_CAP;   // K-LT: path entries per lane in shared memory
 constexpr int kLtCap2 = 512;         // K-LT: max path per lane (shared + global spill)
 constexpr int kIcLaneWarps = 8;      // K-IC lane kernel: warps per CTA
 constexpr int kIcLaneCap = 32;       // K-IC lane kernel: set size limit (then escalate)

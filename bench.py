@@ -221,6 +221,8 @@ def run_gim(args, w):
         else:
             dist.init_process_group("gloo")
     torch.cuda.set_device(local)
+    if world > 1:   # torchrun pins OMP_NUM_THREADS=1: give each rank its share of the host cores
+        gi.set_threads(max(1, (os.cpu_count() or 1) // int(os.environ.get("LOCAL_WORLD_SIZE", world))))
     g = gi.workload_graph(w.key)
     stream = torch.cuda.Stream(local)
     ctx = P.Gim(local, stream=stream.cuda_stream)

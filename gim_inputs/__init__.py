@@ -141,12 +141,19 @@ def _lib():
     lib.ba_generate.restype = ctypes.c_int
     lib.ba_generate.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
                                 ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
+    lib.plg_set_threads.restype = None
+    lib.plg_set_threads.argtypes = [ctypes.c_int]
     lib.plg_generate.restype = ctypes.c_int
     lib.plg_generate.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_double, ctypes.c_uint64,
                                  ctypes.c_void_p, ctypes.c_void_p,
                                  ctypes.POINTER(ctypes.c_double)]
     return lib
+
+
+def set_threads(k: int) -> None:
+    """OpenMP threads used by the generator (its output is independent of the thread count)."""
+    _lib().plg_set_threads(int(k))
 
 
 def plg(n: int, m: int, gamma: float, rho: float, d_cap: float, graph_seed: int,

@@ -80,10 +80,20 @@ Alias build_alias(uint32_t n, double i0, double a) {
   return t;
 }
 
+// Sum of w(i) over i < n in a fixed order (256 fixed chunks summed in order), so the result —
+// and through solve_i0 the alias tables and the graph — does not depend on the thread count.
 double sum_weights(uint32_t n, double i0, double a) {
+  constexpr int64_t C = 256;
+  double part[C];
+#pragma omp parallel for schedule(static)
+  for (int64_t c = 0; c < C; ++c) {
+    const int64_t lo = (int64_t)n * c / C, hi = (int64_t)n * (c + 1) / C;
+    double s = 0.0;
+    for (int64_t i = lo; i < hi; ++i) s += std::pow((double)i + i0, -a);
+    part[c] = s;
+  }
   double s = 0.0;
-#pragma omp parallel for reduction(+ : s) schedule(static)
-  for (int64_t i = 0; i < (int64_t)n; ++i) s += std::pow((double)i + i0, -a);
+  for (int64_t c = 0; c < C; ++c) s += part[c];
   return s;
 }
 
@@ -112,6 +122,12 @@ void permutation(uint32_t n, uint64_t base, std::vector<uint32_t>& perm) {
 }  // namespace
 
 extern "C" {
+
+// OpenMP threads of the generator (torchrun sets OMP_NUM_THREADS=1 per rank; the output does
+// not depend on the thread count).
+void plg_set_threads(int k) {
+  if (k > 0) omp_set_num_threads(k);
+}
 
 // Generates the canonical in-CSR. Caller provides row_ptr[n+1] and src[m].
 // Returns 0 on success, <0 on invalid arguments, -4 if the edge budget cannot be met

@@ -312,7 +312,8 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
   for (int i = lane; i < kHSize; i += 32) h[i] = kEmpty;
   __syncwarp();
   const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
-  uint32_t coins = 0, lives = 0;    // 32-bit per-warp counters, flushed before they can wrap
+  unsigned long long coins = 0;     // per-lane counters (statistics only)
+  uint32_t lives = 0;
 
   const uint32_t count = p.count_ptr ? *p.count_ptr : p.count;
   uint32_t claim_next = 0, claim_end = 0;            // ids claimed kClaimBatch at a time
@@ -410,7 +411,6 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
             thr = (SCHEME == W_WC) ? tv : node_thr<SCHEME>(p, b - a);
           }
         }
-        if (coins >= 0x80000000u) { atomicAdd(&p.ctr->coins, (unsigned long long)coins); coins = 0; }
         coins += b - a;
         resume = head;                                  // batch start: re-expanded on overflow
         head += nb;

@@ -111,7 +111,8 @@ def main():
     launch_shares(wl, rnd)
     tj = os.path.join(OUT, "ncu_traffic.json")
     traffic = json.load(open(tj)) if os.path.exists(tj) else {}
-    for name, rep in [("k_rr_warp", f"prof_rr_{wl}.ncu-rep"), ("k_rr_giant", f"prof_giant_{wl}.ncu-rep")]:
+    for name, rep in [("k_rr_warp", f"prof_rr_{wl}.ncu-rep"), ("k_rr_giant", f"prof_giant_{wl}.ncu-rep"),
+                      ("k_cover", f"prof_cover_{wl}.ncu-rep"), ("k_argmax", f"prof_argmax_{wl}.ncu-rep")]:
         p = os.path.join(GO, rep)
         if os.path.exists(p):
             traffic[f"{wl}:{name}"] = full_capture(p, name, wl, rnd)

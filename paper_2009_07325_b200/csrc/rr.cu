@@ -525,6 +525,38 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
   }
 }
 
+// Lane-per-set kernels: refill the lanes that want a new set (mask `need`) from the warp's pool of
+// claimed ids [pool_next, pool_end) (warp-uniform); one global atomic per kLaneClaim sets instead
+// of one per refill — with 1.5-node sets a refill happens almost every iteration, and the
+// returning atomic on the shared counter was the top stall of K-IC-lane on C5 (35% of ncu
+// samples). Returns this lane's id (meaningful for the lanes in `need`). Warp-collective.
+#ifndef GIM_LANE_PIPE
+#define GIM_LANE_PIPE 0
+#endif
+#ifndef GIM_LANE_CLAIM
+#define GIM_LANE_CLAIM 64
+#endif
+constexpr uint32_t kLaneClaim = GIM_LANE_CLAIM;
+static_assert(kLaneClaim >= 32, "one claim must cover a full warp refill");
+__device__ __forceinline__ uint32_t lane_claim(unsigned int* ctr, uint32_t need, uint32_t& pool_next,
+                                               uint32_t& pool_end, int lane) {
+  const uint32_t nneed = __popc(need), avail = pool_end - pool_next;
+  uint32_t base = 0;
+  if (avail < nneed) {
+    if (lane == 0) base = atomicAdd(ctr, kLaneClaim);
+    base = __shfl_sync(kFull, base, 0);
+  }
+  const uint32_t r = __popc(need & ((1u << lane) - 1u));
+  const uint32_t i = r < avail ? pool_next + r : base + (r - avail);
+  if (avail < nneed) {
+    pool_next = base + (nneed - avail);
+    pool_end = base + kLaneClaim;
+  } else {
+    pool_next += nneed;
+  }
+  return i;
+}
+
 // ------------------------------------------------------------------------------------------
 // K-IC lane kernel (tiny RR sets, e.g. uniform p = 0.01 on C5: ~1.5 nodes and ~56 coins per
 // set): each lane owns one RR set with a 32-node queue in shared memory (lane-interleaved) that is
@@ -538,22 +570,19 @@ __global__ void __launch_bounds__(kIcLaneWarps * 32) k_rr_ic_lane(RRParams p) {
   extern __shared__ uint32_t smem[];
   const int lane = threadIdx.x & 31;
   uint32_t* qv = smem + (threadIdx.x >> 5) * (kIcLaneCap * 32);     // qv[i * 32 + lane]
-  const uint32_t lt_mask = (1u << lane) - 1u;
   const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
-  uint32_t item = 0, head = 0, tail = 0, a = 0, b = 0, g = 0, g_hi = 0, thr = 0;
+  uint32_t item = 0, head = 0, tail = 0, a = 0, b = 0, g = 0, g_hi = 0, thr = 0, pa = 0, pb = 0;
   uint64_t id = 0;
-  bool active = false, want = true, on_node = false;
+  bool active = false, want = true, on_node = false, pend = false;
   uint32_t coins = 0, lives = 0;
   unsigned long long chunk_off = 0;
   uint32_t chunk_left = 0;
+  uint32_t pool_next = 0, pool_end = 0;      // warp-uniform pool of claimed ids
   while (true) {
     const uint32_t need = __ballot_sync(kFull, want);
-    if (need) {                              // refill finished lanes with one claim
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&p.ctr->claim_lane, (uint32_t)__popc(need));
-      base = __shfl_sync(kFull, base, 0);
+    if (need) {                              // refill finished lanes from the warp's id pool
+      const uint32_t i = lane_claim(&p.ctr->claim_lane, need, pool_next, pool_end, lane);
       if (want) {
-        const uint32_t i = base + __popc(need & lt_mask);
         want = false;
         active = i < p.count;
         if (active) {
@@ -563,6 +592,7 @@ __global__ void __launch_bounds__(kIcLaneWarps * 32) k_rr_ic_lane(RRParams p) {
           head = 0;
           tail = 1;
           on_node = false;
+          pend = false;
           if (p.force_giant) {                 // forced fallback: everything via the warp kernel
             p.esc_list[atomicAdd(&p.ctr->esc_count, 1u)] = item;
             active = false;
@@ -577,6 +607,33 @@ __global__ void __launch_bounds__(kIcLaneWarps * 32) k_rr_ic_lane(RRParams p) {
     }
     bool finish = false, escalate = false;
     if (active && !on_node) {                // next node of this lane's BFS
+#if GIM_LANE_PIPE
+      // software-pipelined: the row pointers of the next node are loaded in one iteration and
+      // used in the next, so their latency overlaps the other lanes' Philox work instead of
+      // stalling the whole warp at the load
+      if (pend) {
+        pend = false;
+        a = pa;
+        b = pb;
+        if (b - a > kIcLaneMaxDeg) {
+          escalate = true;
+        } else if (b > a) {
+          on_node = true;
+          g = a >> 2;
+          g_hi = (b - 1) >> 2;
+          thr = node_thr<SCHEME>(p, b - a);
+          coins += b - a;
+        }
+      } else if (head == tail) {
+        finish = true;
+      } else {
+        const uint32_t v = qv[head * 32 + lane];
+        ++head;
+        pa = __ldg(p.row_ptr + v);
+        pb = __ldg(p.row_ptr + v + 1);
+        pend = true;
+      }
+#else
       if (head == tail) {
         finish = true;
       } else {
@@ -594,6 +651,7 @@ __global__ void __launch_bounds__(kIcLaneWarps * 32) k_rr_ic_lane(RRParams p) {
           coins += b - a;
         }
       }
+#endif
     }
     if (active && on_node) {                 // one slot group of the current node
       const uint4 w = philox4x32_10_rk(make_uint4((uint32_t)id, (uint32_t)(id >> 32), g, 0u), p.rk);
@@ -706,7 +764,6 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
   auto at = [&](uint32_t t) -> uint32_t& {
     return t < (uint32_t)kLtCap ? path[t * 32 + lane] : spill[(t - kLtCap) * 32 + lane];
   };
-  const uint32_t lt_mask = (1u << lane) - 1u;
   uint32_t item = 0, v = 0, len = 0;
   uint64_t id = 0;
   bool active = false, want = true;       // want: lane needs a new walk
@@ -717,12 +774,14 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
   while (true) {
     // refill lanes that finished (one claim per warp)
     const uint32_t need = __ballot_sync(kFull, want);
-    if (need) {
+    if (need) {                              // refill finished lanes from the warp's id pool
+      // LT walks are long (≈ 18 nodes on C4): refills are rare and a warp-local id pool only
+      // delays the tail (measured 2.61 vs 2.48 ms) — one claim per refill
       uint32_t base = 0;
       if (lane == 0) base = atomicAdd(&p.ctr->claim, (uint32_t)__popc(need));
       base = __shfl_sync(kFull, base, 0);
+      const uint32_t i = base + __popc(need & ((1u << lane) - 1u));
       if (want) {
-        const uint32_t i = base + __popc(need & lt_mask);
         want = false;
         active = i < p.count;
         if (active) {

@@ -308,12 +308,25 @@ def torch_allreduce(group=None, device: str = "cuda"):
     return fn
 
 
-def torch_allgather(group=None):
+def torch_allgather(group=None, device: str = "cuda"):
     """all-gather callback for Gim.set_allgather: torch.distributed.all_gather_into_tensor of the
     library's device bytes, ordered on the library's stream (NCCL over NVLink for an nccl group;
-    a gloo group stages through host memory, for functional tests)."""
+    a gloo group stages through host memory, for functional tests). device="cpu" wraps host
+    pointers instead (the multi-process gloo tests of this plumbing)."""
     import torch
     import torch.distributed as dist
+
+    if device == "cpu":
+        def fn_cpu(send: int, nbytes: int, recv: int, stream: int) -> int:
+            world = dist.get_world_size(group)
+            u8 = ctypes.POINTER(ctypes.c_uint8)
+            src = np.ctypeslib.as_array(ctypes.cast(send, u8), shape=(int(nbytes),))
+            dst = np.ctypeslib.as_array(ctypes.cast(recv, u8), shape=(int(nbytes) * world,))
+            parts = [torch.empty(int(nbytes), dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, torch.from_numpy(src.copy()), group=group)
+            dst[:] = torch.cat(parts).numpy()
+            return 0
+        return fn_cpu
 
     def view(ptr, nbytes):
         class _View:

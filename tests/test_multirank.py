@@ -121,3 +121,77 @@ def test_sharded_selection_protocol_equals_single(world):
     [p.join(60) for p in procs]
     for rank, seeds, gains in out:
         assert seeds == rs.tolist() and gains == rg.tolist()
+
+
+def _worker_allgather(rank, world, port, q):
+    _init(rank, world, port)
+    import paper_2009_07325_b200 as P
+    fn = P.torch_allgather(device="cpu")
+    send = (np.arange(6, dtype=np.uint8) + 10 * rank)
+    recv = np.zeros(6 * world, dtype=np.uint8)
+    rc = fn(send.ctypes.data, send.nbytes, recv.ctypes.data, 0)
+    q.put((rank, rc, recv.tolist()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_allgather_callback_gloo(world):
+    """The replicated-pool protocol's all-gather callback (binding plumbing): every rank receives
+    all ranks' bytes in rank order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker_allgather, args=(r, world, port, q)) for r in range(world)]
+    [p.start() for p in procs]
+    out = sorted(q.get(timeout=120) for _ in range(world))
+    [p.join(60) for p in procs]
+    want = [int(x) for r in range(world) for x in (np.arange(6) + 10 * r)]
+    for rank, rc, recv in out:
+        assert rc == 0 and recv == want
+
+
+def _replicated_round_protocol(rank, world, port, q, T, key):
+    """Host emulation of replicate_round (gim_api.cu) on oracle pools: each rank holds its slice of
+    RR ids, exchanges element counts, all-gathers sizes and elements padded to the largest slice,
+    and rebuilds the global pool in rank order."""
+    _init(rank, world, port)
+    import oracle
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    o = oracle.Oracle(g, w.model, w.scheme)
+    o.generate(T, w.rr_seed)
+    off, nodes, _ = o.export()
+    lo, hi = rank * T // world, (rank + 1) * T // world
+    sizes = np.diff(off[lo:hi + 1]).astype(np.uint32)
+    elems = nodes[off[lo]:off[hi]].astype(np.uint32)
+    L = torch.tensor([len(elems)], dtype=torch.int64)
+    Ls = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(Ls, L)
+    Ls = [int(x) for x in Ls]
+    S = [(r + 1) * T // world - r * T // world for r in range(world)]
+    maxL, maxS = max(Ls), max(S)
+    ps = np.zeros(maxS, dtype=np.uint32); ps[:len(sizes)] = sizes
+    pe = np.zeros(maxL, dtype=np.uint32); pe[:len(elems)] = elems
+    gs = [torch.zeros(maxS, dtype=torch.int64) for _ in range(world)]
+    ge = [torch.zeros(maxL, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(gs, torch.from_numpy(ps.astype(np.int64)))
+    dist.all_gather(ge, torch.from_numpy(pe.astype(np.int64)))
+    all_sizes = np.concatenate([gs[r].numpy()[:S[r]] for r in range(world)])
+    all_elems = np.concatenate([ge[r].numpy()[:Ls[r]] for r in range(world)])
+    q.put((rank, np.array_equal(np.concatenate([[0], np.cumsum(all_sizes)]), off.astype(np.int64)),
+           np.array_equal(all_elems, nodes.astype(np.int64))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_replicated_pool_protocol_equals_single(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_replicated_round_protocol, args=(r, world, port, q, 5003, "C1"))
+             for r in range(world)]
+    [p.start() for p in procs]
+    out = sorted(q.get(timeout=300) for _ in range(world))
+    [p.join(60) for p in procs]
+    for rank, off_ok, elems_ok in out:
+        assert off_ok and elems_ok, rank

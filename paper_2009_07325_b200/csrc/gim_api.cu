@@ -94,6 +94,7 @@ struct gim_ctx {
   double giant_per_slot = 0.0;      // giant sets per default slot in the previous chunk
   bool giant_cap_reached = false;
   uint64_t stage_cap = 0;
+  int lt_bps = 0;                  // resident K-LT CTAs per SM on this context's device
   GenCounters* h_ctr = nullptr;   // pinned
   uint64_t* h_u64 = nullptr;      // pinned scratch
   unsigned long long* h_keys = nullptr;   // pinned selection keys
@@ -414,9 +415,8 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   p.item_list = nullptr;
   int rr_grid = c->num_sms * kRRBlocksPerSM;   // persistent CTAs, 8 warps each
   if (c->model == MODEL_LT) {
-    static int lt_bps = 0;
-    if (!lt_bps) lt_bps = lt_blocks_per_sm();
-    rr_grid = c->num_sms * lt_bps;
+    if (!c->lt_bps) c->lt_bps = lt_blocks_per_sm();   // per context (= per device)
+    rr_grid = c->num_sms * c->lt_bps;
     TRY(ensure(c, c->lt_spill, (uint64_t)rr_grid * kLtWarps * (kLtCap2 - kLtCap) * 32 * 4));
     p.lt_spill = c->lt_spill.as<uint32_t>();
   }
@@ -520,6 +520,8 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   c->st.live_giant += c->h_ctr->live_giant;
   // two-pass storage: sizes were scanned above; compacting copy + count_total
   const uint64_t total = c->h_u64[0];
+  // k_store totals the members of 32 consecutive sets in uint32 (a window lies inside the chunk)
+  if (total >= 0xFFFFFFFFull) return fail(c, GIM_ENOMEM, "a generate chunk must hold < 2^32 RR elements");
   if (c->sel_pending && (c->pool.bytes < (c->pool_len + total) * 4 || c->offsets.bytes < (c->nsets + cnt + 1) * 8))
     CK(cudaEventSynchronize(c->ev_sel_done));   // the running selection reads pool/offsets
   TRY(grow_keep(c, c->pool, (c->pool_len + total) * 4, c->pool_len * 4));
@@ -611,7 +613,7 @@ gim_status replicate_round(gim_ctx* c, uint64_t a, uint64_t theta, uint64_t set0
   TRY(ensure(c, c->sizes, (totS + 1) * 4));
   TRY(ensure(c, c->scan_out, (totS + 1) * 8));
   TRY(ensure(c, c->scan_tmp, (scan_tiles(totS) + 2) * 8));
-  for (int r = 0, o = 0; r < W; o += (int)S[r], ++r)
+  for (uint64_t r = 0, o = 0; r < (uint64_t)W; o += S[r], ++r)
     if (S[r]) CK(cudaMemcpyAsync(c->sizes.as<uint32_t>() + o, c->ag_recv.as<uint32_t>() + (uint64_t)r * maxS, S[r] * 4,
                                  cudaMemcpyDeviceToDevice, c->stream));
   // elements: undo the local counts, gather, write back in rank order, count globally
@@ -1228,6 +1230,10 @@ gim_status gim_set_rounds(gim_ctx* c, uint32_t rounds) {
     return fail(c, GIM_EINVAL, "n * rounds must be < 2^32 - 1 (uint32 pair ids)");
   if (rounds != c->rounds) {
     c->rounds = rounds;
+    if (c->graph) {                            // empty pool; count vectors sized n * rounds
+      DeviceGuard g(c->device);
+      TRY(reset_pool(c, c->seed));
+    }
     c->have_seed = false;                      // the pool (and its index) is regenerated
   }
   return GIM_OK;
@@ -1316,6 +1322,10 @@ gim_status gim_counts_export(gim_ctx* c, uint32_t* count_out) {
   if (!count_out) return fail(c, GIM_EINVAL, "count_out required");
   if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
   DeviceGuard g(c->device);
+  // rounds may have been raised since the last generate (gim_set_rounds): the device vector
+  // then has fewer than n * rounds entries
+  if (c->count_total.bytes < nsp(c) * 4)
+    return fail(c, GIM_ESTATE, "count vector does not match the MRIM rounds: generate first");
   CK(cudaMemcpyAsync(count_out, c->count_total.p, nsp(c) * 4, cudaMemcpyDeviceToHost, c->stream));
   return sync(c);
 }

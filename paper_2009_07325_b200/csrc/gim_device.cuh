@@ -173,11 +173,7 @@ constexpr int kRRSmemPerWarp = (kQMax + kHSize + kPend) * 4;   // 6.5 KB -> 4 CT
 #ifndef GIM_RR_BLOCKS
 #define GIM_RR_BLOCKS 4
 #endif
-#ifndef GIM_RR_ILP
-#define GIM_RR_ILP 2
-#endif
 constexpr int kRRBlocksPerSM = GIM_RR_BLOCKS;
-constexpr int kRRIlp = GIM_RR_ILP;    // Philox chains per lane per iteration (1 or 2)
 #ifndef GIM_HUB_ILP
 #define GIM_HUB_ILP 2
 #endif

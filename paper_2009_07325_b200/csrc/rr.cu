@@ -16,6 +16,7 @@
 //    keyed RNG makes the replay draw the same coins);
 //  * two-pass storage: bump-allocated staging + sizes, then exclusive scan and a compacting
 //    copy that also builds count_total (Occur; Alg. 6 l.4-11).
+#include <atomic>
 #include "gim_device.cuh"
 #include "gim_internal.h"
 
@@ -1307,16 +1308,23 @@ __global__ void k_count_sub(const uint32_t* __restrict__ pool, uint64_t e0, uint
 // ------------------------------------------------------------------------------------------
 // Host launch wrappers
 // ------------------------------------------------------------------------------------------
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): `done` holds one
+// bit per device ordinal (contexts on several devices in one process each need their own).
+static cudaError_t set_smem_once(std::atomic<uint64_t>& done, const void* fn, int smem) {
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  if (cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) return e;
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return cudaSuccess;
+}
+
 template <int MODEL, int SCHEME>
 static cudaError_t launch_rr_t(const RRParams& p, int grid, cudaStream_t s) {
   const int smem = kRRWarps * kRRSmemPerWarp;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_rr_warp<MODEL, SCHEME>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};        // the attribute is per device: one bit each
+  if (cudaError_t e = set_smem_once(attr, (const void*)k_rr_warp<MODEL, SCHEME>, smem)) return e;
   k_rr_warp<MODEL, SCHEME><<<grid, kRRWarps * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
@@ -1324,12 +1332,8 @@ static cudaError_t launch_rr_t(const RRParams& p, int grid, cudaStream_t s) {
 template <int SCHEME>
 static cudaError_t launch_lt_t(const RRParams& p, int grid, cudaStream_t s) {
   const int smem = kLtWarps * kLtCap * 32 * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_rr_lt_lane<SCHEME>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = set_smem_once(attr, (const void*)k_rr_lt_lane<SCHEME>, smem)) return e;
   k_rr_lt_lane<SCHEME><<<grid, kLtWarps * 32, smem, s>>>(p);
   return cudaGetLastError();
 }

@@ -136,6 +136,7 @@ class Gim:
         self._h = h
         self.device = device
         self.rounds = 1                      # MRIM rounds T (gim_set_rounds)
+        self.n = 0                           # nodes of the loaded graph
         if torch_allocator:
             self._use_torch_allocator(device)
 
@@ -180,6 +181,7 @@ class Gim:
         w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float32)
         self._check(self._lib.gim_load_graph(self._h, n, len(s), _ptr(rp), _ptr(s) if len(s) else None,
                                              _ptr(w), model, scheme, p_uniform))
+        self.n = n
 
     def set_shard(self, rank: int, world: int):
         self._check(self._lib.gim_set_shard(self._h, rank, world))
@@ -244,6 +246,13 @@ class Gim:
                                             _ptr(off), _ptr(nodes), int(sort_each_set)))
         return ids[:ns.value], off, nodes[:pl.value]
 
+    def pool_size(self):
+        """(n_sets, pool_len) of this rank's pool (gim_rr_export size query)."""
+        ns, pl = _u64(), _u64()
+        self._check(self._lib.gim_rr_export(self._h, ctypes.byref(ns), ctypes.byref(pl), None, None,
+                                            None, 0))
+        return int(ns.value), int(pl.value)
+
     def rr_offsets(self) -> np.ndarray:
         """offsets[n_sets + 1] of this rank's pool only (gim_rr_export without the members)."""
         ns, pl = _u64(), _u64()
@@ -254,10 +263,15 @@ class Gim:
                                             _ptr(off), None, 0))
         return off
 
-    def counts_export(self, n: int) -> np.ndarray:
-        out = np.zeros(n, dtype=np.uint32)
+    def counts_export(self, n: int = 0) -> np.ndarray:
+        """count_total: n * rounds entries (MRIM pair counts when rounds > 1). The buffer is
+        sized by the binding from the loaded graph and the rounds; ``n`` is only checked."""
+        want = self.n * self.rounds
+        if n and n not in (self.n, want):
+            raise ValueError(f"counts_export: n={n} does not match the loaded graph ({self.n} x {self.rounds})")
+        out = np.zeros(max(want, 1), dtype=np.uint32)
         self._check(self._lib.gim_counts_export(self._h, _ptr(out)))
-        return out
+        return out[:want]
 
     def set_option(self, opt: int, value: int):
         self._check(self._lib.gim_set_option(self._h, opt, value))

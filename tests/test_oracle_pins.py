@@ -402,6 +402,38 @@ def test_forward_mc_vs_exact():
             assert abs(mean - float(exact_spread(d, worlds, S))) < 4.5 * se + 1e-9
 
 
+def _mc_cases():
+    """og_mc_spread's non-WC branches (IC uniform, IC explicit, LT explicit) on the diamond and the
+    cycle-plus-tail graph. Weights differ per in-slot so that a wrong slot index, a swapped
+    source/destination or a dropped weight moves the exact spread by far more than 4.5 standard
+    errors at 40,000 trials."""
+    d, cy = gi.diamond(), gi.cycle_plus()
+    # diamond in-slots: e0 0->1, e1 0->2, e2 1->3, e3 2->3; cycle_plus: e0 2->0, e1 3->0, e2 0->1, e3 1->2
+    return [
+        ("ic_uni_diamond", d, gi.IC, gi.W_UNIFORM, 0.3),
+        ("ic_uni_cycle", cy, gi.IC, gi.W_UNIFORM, 0.55),
+        ("ic_exp_diamond", gi.with_weights(d, [0.9, 0.2, 0.6, 0.1]), gi.IC, gi.W_EXPLICIT, 0.0),
+        ("ic_exp_cycle", gi.with_weights(cy, [0.7, 0.25, 0.5, 0.95]), gi.IC, gi.W_EXPLICIT, 0.0),
+        ("lt_exp_diamond", gi.with_weights(d, [0.9, 0.2, 0.6, 0.3]), gi.LT, gi.W_EXPLICIT, 0.0),
+        ("lt_exp_cycle", gi.with_weights(cy, [0.45, 0.35, 0.8, 0.6]), gi.LT, gi.W_EXPLICIT, 0.0),
+    ]
+
+
+@pytest.mark.parametrize("case", _mc_cases(), ids=lambda c: c[0])
+def test_forward_mc_vs_exact_weight_schemes(case):
+    """Forward MC (IC P:118-122; LT Eq. 1 P:127-131 with the exact thresholds of reading R30)
+    against the exact spread over all live-edge worlds (IC: each edge live w.p. p_e; LT: each node
+    keeps at most one in-edge, edge t w.p. w_t — the live-edge view of LT)."""
+    _, g, model, scheme, pu = case
+    p = _p_exact(g, scheme, pu)
+    worlds = list(_ic_worlds(g, p)) if model == gi.IC else list(_lt_worlds(g, p))
+    o = oracle.Oracle(g, model, scheme, pu)
+    for S in ([0], [1], [2], [3], [1, 2]):
+        exact = float(exact_spread(g, worlds, S))
+        mean, se = o.mc_spread(S, 40000, 17)
+        assert abs(mean - exact) < 4.5 * se + 1e-9, (S, mean, exact, se)
+
+
 # --------------------------------------------------------------------------------------
 # O7: NodeSelection vs brute force
 # --------------------------------------------------------------------------------------

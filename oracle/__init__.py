@@ -53,6 +53,11 @@ def _lib():
         "og_mc_spread": (_int, [_p, _p, _u32, _u64, _u64, _p, _p]),
         "og_mrim_generate": (_int, [_p, _u64, _u32, _u64]),
         "og_set_fresh_final": (None, [_p, _int]),
+        "og_set_skip": (_int, [_p, _int]),
+        "og_skip_ln": (_dbl, [_dbl]),
+        "og_skip_inv": (_dbl, [_int, _u64, ctypes.c_float]),
+        "og_skip_gap": (_dbl, [_dbl, _u32]),
+        "og_skip_word": (_u32, [_u64, _u64, _u32, _u32, _u32]),
         "og_mrim_num_sets": (_u64, [_p]),
         "og_mrim_set": (_u32, [_p, _u64, _u64, _u32, _p]),
         "og_mrim_pool_len": (_u64, [_p]),
@@ -91,6 +96,23 @@ def coin(seed: int, rr_id: int, e: int) -> int:
 
 def lt_draw(seed: int, rr_id: int, v: int) -> int:
     return int(_lib().og_lt_draw(seed, rr_id, v))
+
+
+# --- R31 geometric-skip contract (oracle/gim_oracle.c "R31") -----------------------------
+def skip_ln(x: float) -> float:
+    return float(_lib().og_skip_ln(x))
+
+
+def skip_inv(scheme: int, d: int, p_uniform: float = 0.0) -> float:
+    return float(_lib().og_skip_inv(scheme, d, p_uniform))
+
+
+def skip_gap(inv: float, r: int) -> float:
+    return float(_lib().og_skip_gap(inv, r))
+
+
+def skip_word(seed: int, rr_id: int, v: int, block: int, j: int) -> int:
+    return int(_lib().og_skip_word(seed, rr_id, v, block, j))
 
 
 def imm_constants(n: int, k: int, eps: float, ell: float = 1.0) -> dict:
@@ -252,6 +274,11 @@ class Oracle:
         _lib().og_mc_spread(self._h, _ptr(s), len(s), trials, mc_seed, ctypes.byref(mean),
                             ctypes.byref(se))
         return mean.value, se.value
+
+    def set_skip(self, on: bool) -> None:
+        """R31: live in-edges by geometric gaps (IC with WC or uniform weights); pool restarts."""
+        if _lib().og_set_skip(self._h, int(bool(on))):
+            raise ValueError("the skip contract needs IC with WC or uniform weights")
 
     def set_fresh_final(self, on: bool) -> None:
         """R29: IMM's final phase on a fresh pool (key seed ^ 0x9E3779B97F4A7C15)."""

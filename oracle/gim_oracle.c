@@ -121,6 +121,7 @@ typedef struct og_ctx {
   uint32_t* mr_count;
   uint32_t* mr_tmp;
   int fresh_final;          /* R29: final phase on a fresh pool (og_set_fresh_final) */
+  int skip;                 /* R31: geometric-skip RNG contract (og_set_skip) */
 } og_ctx;
 
 static int cmp_u32(const void* a, const void* b) {
@@ -186,6 +187,92 @@ static int ic_live(og_ctx* c, uint64_t seed, uint64_t id, uint64_t e, uint32_t v
   return coin < c->thr_edge[e];
 }
 
+/* ------------------------------------------------------------------------------------------
+ * R31 (option, off by default; SURVEY.md §8(f) NEXT "geometric skip sampling"). Alg. 3 l.18
+ * draws one U(0,1) per in-edge. Where every in-edge of v has the same probability p —
+ * weighted cascade p = 1/d_in(v) and uniform p — the live in-edges of v are i.i.d.
+ * Bernoulli(p) slots, so the gaps between consecutive live slots are geometric:
+ * Pr[gap >= g] = (1-p)^g. This contract draws the gaps instead of the coins:
+ *  * the in-edge offsets of v are cut into blocks of SKIP_BLOCK: block b = offsets
+ *    [b*1024, min((b+1)*1024, d));
+ *  * draw j (j = 0, 1, ...) of block b is word (j & 3) of Philox(seed; id_lo, 2^31 | b, v,
+ *    j >> 2) — counter word 1 carries the tag bit (RR ids are < 2^32, so that word is 0 in every
+ *    other draw of the key scheme);
+ *  * gap = floor(ln(U) * inv_v), U = (r + 1/2) 2^-32, inv_v = 1 / ln(1 - p) — inversion of the
+ *    geometric CDF; starting at pos = b*1024: while pos + gap < end of block, offset pos + gap
+ *    is live and pos += gap + 1;
+ *  * p = 1 (WC with d = 1, uniform p >= 1): every in-edge is live, no draw; p = 0: none is.
+ * ln is skip_ln below: a fixed sequence of correctly rounded IEEE-754 double operations, so
+ * every machine evaluates it (and the gap) identically. Pins: skip_ln against mpmath; the exact
+ * gap distribution (counted over all 2^32 words) against (1-p)^g; per-slot live rates and the
+ * Eq. 3 estimator against exact enumeration (tests/test_oracle_skip.py).
+ * ------------------------------------------------------------------------------------------ */
+#define SKIP_BLOCK 1024u
+#define SKIP_LN2_HI 6.93147180369123816490e-01   /* ln 2 = HI + LO, HI with 21 trailing zero bits */
+#define SKIP_LN2_LO 1.90821492927058770002e-10
+
+/* ln x for a positive normal double: x = m 2^e with m in [sqrt(1/2), sqrt(2)),
+ * ln x = e ln2 + 2 atanh(y), y = (m-1)/(m+1) (|y| <= 0.1716), atanh(y)/y = sum_k y^2k/(2k+1)
+ * up to k = 9 (remainder < 1e-17 relative), Horner with fma. */
+double og_skip_ln(double x) {
+  uint64_t bits;
+  double m, y, y2, s;
+  int e;
+  memcpy(&bits, &x, 8);
+  e = (int)((bits >> 52) & 0x7FF) - 1023;
+  bits = (bits & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull;
+  memcpy(&m, &bits, 8);                          /* m in [1, 2) */
+  if (m > 1.4142135623730951) { m = m * 0.5; e += 1; }
+  y = (m - 1.0) / (m + 1.0);
+  y2 = y * y;
+  s = 1.0 / 19.0;
+  s = fma(s, y2, 1.0 / 17.0);
+  s = fma(s, y2, 1.0 / 15.0);
+  s = fma(s, y2, 1.0 / 13.0);
+  s = fma(s, y2, 1.0 / 11.0);
+  s = fma(s, y2, 1.0 / 9.0);
+  s = fma(s, y2, 1.0 / 7.0);
+  s = fma(s, y2, 1.0 / 5.0);
+  s = fma(s, y2, 1.0 / 3.0);
+  s = fma(s, y2, 1.0);
+  return (double)e * SKIP_LN2_HI + ((double)e * SKIP_LN2_LO + (2.0 * y) * s);
+}
+
+/* inv_v = 1 / ln(1 - p) < 0; 0 when p = 1 (every in-edge live, no draws). WC: 1 - 1/d as
+ * (d-1)/d (one rounding). Uniform: 1 - p exact for a float32 p. */
+double og_skip_inv(int scheme, uint64_t d, float p_uniform) {
+  double q;
+  if (scheme == OG_W_WC) {
+    if (d <= 1) return 0.0;
+    q = (double)(d - 1) / (double)d;
+  } else {
+    q = 1.0 - (double)p_uniform;
+    if (!(q > 0.0)) return 0.0;
+  }
+  return 1.0 / og_skip_ln(q);
+}
+
+/* gap of word r: floor(ln((r + 1/2) 2^-32) * inv), returned as a double (>= 0; compare before
+ * converting: it may exceed any block) */
+double og_skip_gap(double inv, uint32_t r) {
+  return floor(og_skip_ln(((double)r + 0.5) * 0x1p-32) * inv);
+}
+
+uint32_t og_skip_word(uint64_t seed, uint64_t id, uint32_t v, uint32_t b, uint32_t j) {
+  uint32_t o[4], ctr[4], key[2];
+  ctr[0] = (uint32_t)id; ctr[1] = 0x80000000u | b; ctr[2] = v; ctr[3] = j >> 2;
+  key[0] = (uint32_t)seed; key[1] = (uint32_t)(seed >> 32);
+  og_philox(ctr, key, o);
+  return o[j & 3];
+}
+
+/* R31 selects the skip contract (IC with WC or uniform weights only); the pool restarts. */
+int og_set_skip(og_ctx* c, int on) {
+  if (on && (c->model != OG_IC || c->scheme == OG_W_EXPLICIT)) return 1;
+  if ((on ? 1 : 0) != c->skip) { c->skip = on ? 1 : 0; c->have_seed = 0; c->mr_have = 0; }
+  return 0;
+}
+
 /* O4. IC RR set: reverse BFS over live in-edges from a uniform root — the RR set definition of
  * P:166-168 realised as the randomized BFS of P:260 / Alg. 3 l.8-22, with the root
  * marked visited (R12) and exact set semantics (R13). Writes the set, ascending, to out[];
@@ -197,6 +284,34 @@ static uint32_t rr_ic(og_ctx* c, uint64_t seed, uint64_t id, uint32_t root, uint
   while (head < tail) {
     uint32_t v = c->queue[head++];
     uint64_t e;
+    if (c->skip) {                                    /* R31: the same BFS, live slots by gaps */
+      uint64_t a = c->row_ptr[v], d = c->row_ptr[v + 1] - a, b;
+      double inv;
+      if (d == 0 || (c->scheme == OG_W_UNIFORM && c->thr_uniform == 0)) continue;
+      inv = og_skip_inv(c->scheme, d, c->p_uniform);
+      for (b = 0; b * SKIP_BLOCK < d; ++b) {
+        uint64_t pos = b * SKIP_BLOCK, end = pos + SKIP_BLOCK < d ? pos + SKIP_BLOCK : d;
+        uint32_t j;
+        for (j = 0; pos < end; ++j) {
+          if (inv != 0.0) {
+            double g = og_skip_gap(inv, og_skip_word(seed, id, v, (uint32_t)b, j));
+            c->stat_coins++;
+            if (g >= (double)(end - pos)) break;
+            pos += (uint64_t)g;
+          }
+          c->stat_live++;
+          {
+            uint32_t u = c->src[a + pos];
+            if (!c->visited[u]) {
+              c->visited[u] = 1;
+              c->queue[tail++] = u;
+            }
+          }
+          pos += 1;
+        }
+      }
+      continue;
+    }
     for (e = c->row_ptr[v]; e < c->row_ptr[v + 1]; ++e) {
       if (ic_live(c, seed, id, e, v)) {
         uint32_t u = c->src[e];

@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo + --same-device: functional multi-rank test on 1 GPU)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (functional testing)")
+    ap.add_argument("--skip", action="store_true",
+                    help="geometric-skip RNG contract (reading R31, GIM_OPT_SKIP) instead of one coin per in-edge")
     ap.add_argument("--dense-exchange", action="store_true",
                     help="N > 1: per-step count/decrement all-reduce instead of the replicated pool")
     return ap.parse_args()
@@ -235,6 +237,8 @@ def run_gim(args, w):
         if not args.dense_exchange:            # replicated pool: no per-step collectives
             ctx.set_allgather(P.torch_allgather())
     ctx.set_option(P.OPT_PROFILE, 1)
+    if args.skip:
+        ctx.set_option(P.OPT_SKIP, 1)
     for o in args.opt:
         name, val = o.split("=")
         ctx.set_option(getattr(P, name), int(val))
@@ -332,6 +336,8 @@ def run_gim(args, w):
         rp_h = torch.from_numpy(g.row_ptr).pin_memory()
         src_h = torch.from_numpy(g.src).pin_memory()
         ctx2 = P.Gim(local, stream=stream.cuda_stream)
+        if args.skip:
+            ctx2.set_option(P.OPT_SKIP, 1)
         if args.rounds > 1:
             ctx2.set_rounds(args.rounds)
         if world > 1:

@@ -219,7 +219,19 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                         greedy steps of a selection in one cooperative launch with grid
  *                         barriers between the argmax and cover phases (no candidate list).
  *  GIM_OPT_MB_CHAINS    = 1 / 4 / 8 (default 8): interleaved Philox chains per thread in
- *                          gim_microbench_philox. */
+ *                          gim_microbench_philox.
+ *  GIM_OPT_SKIP         = 0 (default: one Philox coin per in-edge, reading R16) / 1: the
+ *                         geometric-skip RNG contract (reading R31): the live in-edges
+ *                         of a visited node v are drawn as geometric gaps, blocks of 1024 in-edge
+ *                         offsets, draw j of block b = word (j & 3) of Philox(seed; id_lo, 2^31|b,
+ *                         v, j >> 2), gap = floor(ln((r + 1/2) 2^-32) / ln(1 - p)). Same
+ *                         distribution of RR sets (Bernoulli(p) per in-edge), different sets: the
+ *                         pool restarts. IC with WC or uniform weights only (GIM_EINVAL otherwise;
+ *                         a later gim_load_graph of another model/scheme turns it off).
+ *  GIM_OPT_SKIP_SPILL   = S (0 = auto: 16384 for WC, 2048 for uniform; else 1..16384): under
+ *                         GIM_OPT_SKIP, a set that outgrows the warp kernel's shared queue
+ *                         continues in the warp's global spill tier up to S nodes, beyond that
+ *                         in the CTA-per-set giant kernel. Results are identical. */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -234,7 +246,9 @@ typedef enum {
   GIM_OPT_PDL = 12,
   GIM_OPT_GIANT_NT = 13,
   GIM_OPT_FRESH_FINAL = 14,
-  GIM_OPT_SELECT_PERSISTENT = 15
+  GIM_OPT_SELECT_PERSISTENT = 15,
+  GIM_OPT_SKIP = 16,
+  GIM_OPT_SKIP_SPILL = 17
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

@@ -55,6 +55,7 @@ def _lib():
         "og_set_fresh_final": (None, [_p, _int]),
         "og_set_skip": (_int, [_p, _int]),
         "og_skip_ln": (_dbl, [_dbl]),
+        "og_skip_ln_series": (_dbl, [_dbl]),
         "og_skip_inv": (_dbl, [_int, _u64, ctypes.c_float]),
         "og_skip_gap": (_dbl, [_dbl, _u32]),
         "og_skip_word": (_u32, [_u64, _u64, _u32, _u32, _u32]),
@@ -101,6 +102,10 @@ def lt_draw(seed: int, rr_id: int, v: int) -> int:
 # --- R31 geometric-skip contract (oracle/gim_oracle.c "R31") -----------------------------
 def skip_ln(x: float) -> float:
     return float(_lib().og_skip_ln(x))
+
+
+def skip_ln_series(x: float) -> float:
+    return float(_lib().og_skip_ln_series(x))
 
 
 def skip_inv(scheme: int, d: int, p_uniform: float = 0.0) -> float:

@@ -202,8 +202,9 @@ static int ic_live(og_ctx* c, uint64_t seed, uint64_t id, uint64_t e, uint32_t v
  *    geometric CDF; starting at pos = b*1024: while pos + gap < end of block, offset pos + gap
  *    is live and pos += gap + 1;
  *  * p = 1 (WC with d = 1, uniform p >= 1): every in-edge is live, no draw; p = 0: none is.
- * ln is skip_ln below: a fixed sequence of correctly rounded IEEE-754 double operations, so
- * every machine evaluates it (and the gap) identically. Pins: skip_ln against mpmath; the exact
+ * ln is og_skip_ln below: a fixed sequence of correctly rounded IEEE-754 double operations
+ * (a 182-entry table of centers, itself built by the same kind of sequence), so every machine
+ * evaluates it (and the gap) identically. Pins: skip_ln against mpmath; the exact
  * gap distribution (counted over all 2^32 words) against (1-p)^g; per-slot live rates and the
  * Eq. 3 estimator against exact enumeration (tests/test_oracle_skip.py).
  * ------------------------------------------------------------------------------------------ */
@@ -211,10 +212,10 @@ static int ic_live(og_ctx* c, uint64_t seed, uint64_t id, uint64_t e, uint32_t v
 #define SKIP_LN2_HI 6.93147180369123816490e-01   /* ln 2 = HI + LO, HI with 21 trailing zero bits */
 #define SKIP_LN2_LO 1.90821492927058770002e-10
 
-/* ln x for a positive normal double: x = m 2^e with m in [sqrt(1/2), sqrt(2)),
+/* The series form: ln x for a positive normal double, x = m 2^e with m in [sqrt(1/2), sqrt(2)),
  * ln x = e ln2 + 2 atanh(y), y = (m-1)/(m+1) (|y| <= 0.1716), atanh(y)/y = sum_k y^2k/(2k+1)
- * up to k = 9 (remainder < 1e-17 relative), Horner with fma. */
-double og_skip_ln(double x) {
+ * up to k = 9 (remainder < 1e-17 relative), Horner with fma. Used to tabulate ln(c_k) below. */
+double og_skip_ln_series(double x) {
   uint64_t bits;
   double m, y, y2, s;
   int e;
@@ -236,6 +237,47 @@ double og_skip_ln(double x) {
   s = fma(s, y2, 1.0 / 3.0);
   s = fma(s, y2, 1.0);
   return (double)e * SKIP_LN2_HI + ((double)e * SKIP_LN2_LO + (2.0 * y) * s);
+}
+
+/* The ln of the contract (division-free per call): m in [sqrt(1/2), sqrt(2)) as above, nearest
+ * center c_k = 1 + k/256 (k = floor((m - 1) 256 + 1/2), -75 <= k <= 106), t = (m - c_k) R_k with
+ * R_k = 1/c_k, ln m = L_k + ln(1 + t), L_k = ln c_k (the series form), ln(1 + t) by its Taylor
+ * polynomial of degree 7 (|t| <= 1/512: remainder < 1e-19 relative). Center 0 is exactly 1
+ * (L = 0, R = 1), so x near 1 keeps its relative accuracy. */
+#define SKIP_K0 75
+static double skip_L[SKIP_K0 + 107], skip_R[SKIP_K0 + 107];
+static int skip_tab_ready;
+static void skip_tables(void) {
+  int k;
+  for (k = -SKIP_K0; k <= 106; ++k) {
+    double c = 1.0 + (double)k / 256.0;
+    skip_R[k + SKIP_K0] = 1.0 / c;
+    skip_L[k + SKIP_K0] = og_skip_ln_series(c);
+  }
+  skip_tab_ready = 1;
+}
+
+double og_skip_ln(double x) {
+  uint64_t bits;
+  double m, c, t, s;
+  int e, k;
+  if (!skip_tab_ready) skip_tables();
+  memcpy(&bits, &x, 8);
+  e = (int)((bits >> 52) & 0x7FF) - 1023;
+  bits = (bits & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull;
+  memcpy(&m, &bits, 8);                          /* m in [1, 2) */
+  if (m > 1.4142135623730951) { m = m * 0.5; e += 1; }
+  k = (int)floor((m - 1.0) * 256.0 + 0.5);
+  c = 1.0 + (double)k / 256.0;
+  t = (m - c) * skip_R[k + SKIP_K0];
+  s = 1.0 / 7.0;
+  s = fma(s, t, -1.0 / 6.0);
+  s = fma(s, t, 1.0 / 5.0);
+  s = fma(s, t, -1.0 / 4.0);
+  s = fma(s, t, 1.0 / 3.0);
+  s = fma(s, t, -1.0 / 2.0);
+  s = fma(s, t, 1.0);
+  return (double)e * SKIP_LN2_HI + ((double)e * SKIP_LN2_LO + (skip_L[k + SKIP_K0] + t * s));
 }
 
 /* inv_v = 1 / ln(1 - p) < 0; 0 when p = 1 (every in-edge live, no draws). WC: 1 - 1/d as

@@ -1,7 +1,8 @@
 // csr.cu — on-device validation of the canonical in-CSR (reading R15) and conversion of the
 // uint64 row pointers of the C ABI to the uint32 row pointers the kernels read (§8(a) row a1).
 // One warp per row: monotone row pointers within [0, m], sources < n, no self-loop, sources
-// strictly ascending. Violations set bits in *err and the lowest offending row in *bad_row.
+// strictly ascending. Violations set bits in *err and the lowest offending row in *bad_row;
+// err[2] receives the largest in-degree (the geometric-skip contract tabulates 1/ln(1 - 1/d)).
 #include "gim_device.cuh"
 #include "gim_internal.h"
 
@@ -27,6 +28,7 @@ __global__ void __launch_bounds__(256) k_validate_csr(const uint64_t* __restrict
       }
     }
     e_bits = __reduce_or_sync(kFull, e_bits);
+    if (lane == 0 && b > a && b - a > *(volatile uint32_t*)(err + 2)) atomicMax(err + 2, (uint32_t)(b - a));
     if (lane == 0) {
       rp32[v] = (uint32_t)a;
       // WC live threshold of row v (p = 1/d_in(v): coin <= thr <=> coin * d < 2^32), read by the

@@ -85,6 +85,7 @@ struct gim_ctx {
   // generation scratch
   DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr, dump, lt_spill, esc_list;
   DevBuf bitmaps, gqueues;
+  DevBuf skip_spill;              // R31: per-warp global queue + hash of k_skip_warp (kEmpty when unused)
   uint32_t giant_slots = 0;
   uint32_t giant_n = 0;             // n the giant slots were sized for (reused while n <= giant_n)
   int giant_nt_opt = 0;             // GIM_OPT_GIANT_NT: 0 auto, else threads per giant CTA
@@ -95,6 +96,13 @@ struct gim_ctx {
   bool giant_cap_reached = false;
   uint64_t stage_cap = 0;
   int lt_bps = 0;                  // resident K-LT CTAs per SM on this context's device
+  int skip = 0;                    // geometric-skip RNG contract (GIM_OPT_SKIP, reading R31)
+  int skip_bps = 0;                // resident k_skip_lane CTAs per SM
+  int skip_lane = -1;              // skip: -1 auto (lane kernel first for big chunks), 0 / 1
+  uint32_t skip_spill_cap = 0;     // skip: spill-tier set size limit (GIM_OPT_SKIP_SPILL; 0 = auto)
+  uint32_t max_deg = 0;            // largest in-degree of the loaded graph
+  DevBuf skip_tab;                 // skip: log centers L_k, R_k (2 x 184 doubles) + inv per in-degree
+  bool skip_tab_valid = false;
   GenCounters* h_ctr = nullptr;   // pinned
   uint64_t* h_u64 = nullptr;      // pinned scratch
   unsigned long long* h_keys = nullptr;   // pinned selection keys
@@ -353,6 +361,8 @@ RRParams base_params(gim_ctx* c) {
   p.thr_node = c->thr_node.as<uint32_t>();
   p.thr_edge = c->thr_edge.as<uint64_t>();
   p.thr_uniform = c->thr_uniform;
+  p.p_uniform = c->p_uniform;
+  p.skip_tab = c->skip_tab.as<double>();
   p.seed = c->seed;
   {
     uint32_t k0 = (uint32_t)c->seed, k1 = (uint32_t)(c->seed >> 32);
@@ -409,6 +419,13 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     }
   }
   CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(GenCounters), c->stream));
+  if (c->skip && !c->skip_tab_valid) {         // R31: log-center tables + 1/ln(1-p) per in-degree
+    const uint64_t nd = (c->scheme == W_WC ? (uint64_t)c->max_deg : 0) + 2;
+    TRY(ensure(c, c->skip_tab, (2 * kSkipTabK + nd) * 8));
+    TRY(launched(c, launch_skip_tables(c->scheme, c->p_uniform, c->max_deg, c->skip_tab.as<double>(),
+                                       c->stream), "k_skip_tables"));
+    c->skip_tab_valid = true;
+  }
   RRParams p = base_params(c);
   p.id_base = gstart;
   p.count = cnt;
@@ -436,6 +453,45 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
                           (c->ic_lane == 1 || (c->ic_lane == -1 && c->coins_per_set > 0.0 &&
                                                c->coins_per_set < 160.0 && cnt >= (1u << 17)));
   auto run_pass = [&](const RRParams& pp) -> gim_status {
+    if (c->skip) {                             // R31: lane kernel -> warp kernel -> giant kernel
+      const bool sl = c->skip_lane == 1 || (c->skip_lane == -1 && cnt >= (1u << 15));
+      RRParams pw = pp;
+      if (sl) {
+        if (!c->skip_bps) c->skip_bps = skip_lane_blocks_per_sm();
+        RRParams pl = pp;
+        pl.esc_list = c->esc_list.as<uint32_t>();
+        {
+          Prof pf(c, CLS_RR);
+          TRY(launched(c, launch_skip_lane(c->scheme, pl, c->num_sms * c->skip_bps, c->stream), "k_skip_lane"));
+          c->st.n_rr_launches++;
+        }
+        pw.item_list = c->esc_list.as<uint32_t>();
+        pw.count_ptr = &c->ctr.as<GenCounters>()->esc_count;
+      }
+      {
+        const uint64_t spill_b = (uint64_t)c->num_sms * kRRBlocksPerSM * kRRWarps * skip_spill_words_per_warp() * 4;
+        if (c->skip_spill.bytes < spill_b) {           // hash halves must start (and stay) empty
+          TRY(dalloc(c, c->skip_spill, spill_b));
+          CK(cudaMemsetAsync(c->skip_spill.p, 0xFF, spill_b, c->stream));
+        }
+        pw.skip_spill = c->skip_spill.as<uint32_t>();
+        // auto: WC sets grow by ~1 live in-edge per node (deep, narrow: the warp's spill tier
+        // keeps them in flight beside the small ones); uniform-p sets become big through hubs of
+        // thousands of live in-edges (wide: better spread over a CTA by the giant kernel)
+        const uint32_t cap = c->skip_spill_cap ? c->skip_spill_cap : (c->scheme == W_WC ? 16384u : 2048u);
+        pw.skip_spill_cap = std::min<uint32_t>(cap, (uint32_t)skip_spill_words_per_warp() / 3);
+        Prof pf(c, CLS_RR);
+        TRY(launched(c, launch_skip_warp(c->scheme, pw, c->num_sms * kRRBlocksPerSM, c->stream), "k_skip_warp"));
+        c->st.n_rr_launches++;
+      }
+      {
+        Prof pf(c, CLS_GIANT);
+        TRY(launched(c, launch_skip_giant(c->scheme, pp, (int)c->giant_slots, c->bitmaps.as<uint32_t>(),
+                                          c->gqueues.as<uint32_t>(), bm_words, c->stream), "k_skip_giant"));
+        c->st.n_giant_launches++;
+      }
+      return GIM_OK;
+    }
     if (lane_first) {
       RRParams pl = pp;
       pl.esc_list = c->esc_list.as<uint32_t>();
@@ -926,7 +982,7 @@ void gim_destroy(gim_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
                     &c->sizes, &c->soff, &c->giant_list, &c->retry_list, &c->item_list, &c->scan_out,
-                    &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
+                    &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->skip_spill, &c->skip_tab, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
                     &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->thr_node, &c->ag_small,
                     &c->ag_send, &c->ag_recv, &c->sel_bar};
@@ -1007,6 +1063,7 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
   c->m = m;
   c->model = model;
   c->scheme = scheme;
+  if (c->skip && ((int)model != MODEL_IC || (int)scheme == W_EXPLICIT)) c->skip = 0;   // R31 needs IC + WC/uniform
   c->p_uniform = p_uniform;
   c->thr_uniform = (uint64_t)std::ceil((double)p_uniform * 4294967296.0);
   TRY(dalloc(c, c->row_ptr, ((uint64_t)n + 1) * 4));
@@ -1022,12 +1079,15 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
     if (m) CK(cudaMemcpyAsync(c->src.p, src, m * 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(flags, 0, 4, c->stream));
     CK(cudaMemsetAsync(flags + 1, 0xFF, 4, c->stream));
+    CK(cudaMemsetAsync(flags + 2, 0, 8, c->stream));                 // max in-degree
     TRY(launched(c, launch_validate_csr(rp64.as<uint64_t>(), n, m, c->src.as<uint32_t>(), c->row_ptr.as<uint32_t>(),
                                         flags, flags + 1, scheme == GIM_W_WC ? c->thr_node.as<uint32_t>() : nullptr,
                                         c->num_sms * 8, c->stream), "k_validate_csr"));
-    CK(cudaMemcpyAsync(c->h_u64, flags, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->h_u64, flags, 16, cudaMemcpyDeviceToHost, c->stream));
     TRY(sync(c));
     dfree(c, rp64);
+    c->max_deg = (uint32_t)c->h_u64[1];
+    c->skip_tab_valid = false;
     const uint32_t err = (uint32_t)c->h_u64[0], row = (uint32_t)(c->h_u64[0] >> 32);
     if (err) {
       dfree(c, c->row_ptr);
@@ -1345,6 +1405,21 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_MB_CHAINS: c->mb_chains = (int)value; return GIM_OK;
     case GIM_OPT_SPECULATE: c->speculate = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_FRESH_FINAL: c->fresh_final = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_SKIP_SPILL:
+      if (value < 0 || value > 16384) return fail(c, GIM_EINVAL, "spill cap must be in [0 (auto), 16384]");
+      c->skip_spill_cap = (uint32_t)value;
+      return GIM_OK;
+    case GIM_OPT_SKIP: {
+      const int on = value ? 1 : 0;
+      if (on && c->graph && (c->model != MODEL_IC || c->scheme == W_EXPLICIT))
+        return fail(c, GIM_EINVAL, "the geometric-skip contract needs IC with WC or uniform weights");
+      if (on != c->skip) {
+        c->skip = on;
+        c->have_seed = false;                  // different RR sets: the pool restarts
+      }
+      if (value == 2 || value == 3) c->skip_lane = value - 2;   // test hook: 2 = warp only, 3 = lane first
+      return GIM_OK;
+    }
     case GIM_OPT_SELECT_PERSISTENT: c->sel_persistent = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_GIANT_NT:
       if (value != 0 && value != kGiantThreads && value != kGiantThreadsNarrow)

@@ -130,6 +130,8 @@ struct RRParams {
   const uint32_t* thr_node;    // WC: per-node live threshold floor((2^32-1)/d_in(v))
   const uint64_t* thr_edge;    // explicit weights: IC ceil(w*2^32), LT floor(w*2^32)
   uint64_t thr_uniform;        // uniform p: ceil(p*2^32)
+  float p_uniform;             // uniform p itself (geometric-skip contract, R31)
+  const double* skip_tab;      // R31: L_k[184], R_k[184], then inv[d] (WC: d = 0..max_deg; uniform: inv[0])
   uint64_t seed;
   uint32_t rk[20];             // Philox round keys of `seed` (host-computed)
   uint64_t id_base;            // global RR id = id_base + item
@@ -148,6 +150,8 @@ struct RRParams {
   uint32_t* retry_list;        // items whose staging write failed
   uint32_t qcap;               // shared-memory queue capacity (<= kQMax)
   uint32_t* lt_spill;          // LT: per-warp spill of walks longer than kLtCap (lane-interleaved)
+  uint32_t* skip_spill;        // R31 warp kernel: per-warp global queue + hash for sets > qcap
+  uint32_t skip_spill_cap;     // R31: sets beyond this many nodes go to the CTA giant kernel
   int force_giant;
   uint32_t rounds;             // MRIM rounds T (1 = standard IM): root of id = root(id / T)
 };

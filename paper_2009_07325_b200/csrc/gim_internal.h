@@ -11,6 +11,15 @@ cudaError_t launch_rr_ic_lane(int scheme, const RRParams& p, int grid, cudaStrea
 cudaError_t launch_rr_warp(int model, int scheme, const RRParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
                             uint32_t* gqueues, uint64_t bm_words, cudaStream_t s, int nt);
+// geometric-skip contract (skip.cu, reading R31)
+cudaError_t launch_skip_lane(int scheme, const RRParams& p, int grid, cudaStream_t s);
+cudaError_t launch_skip_warp(int scheme, const RRParams& p, int grid, cudaStream_t s);
+cudaError_t launch_skip_giant(int scheme, const RRParams& p, int grid, uint32_t* bitmaps, uint32_t* gqueues,
+                              uint64_t bm_words, cudaStream_t s);
+int skip_lane_blocks_per_sm();
+uint64_t skip_spill_words_per_warp();
+constexpr int kSkipTabK = 184;   // log centers k = -75..106 (+ padding) of the R31 ln
+cudaError_t launch_skip_tables(int scheme, float p_uniform, uint32_t max_deg, double* tab, cudaStream_t s);
 cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const uint64_t* soff,
                          const uint64_t* scan, uint32_t count, uint64_t pool_base, uint32_t* pool,
                          uint64_t* offsets_out, uint32_t* count_total, uint32_t rounds, uint32_t round0,

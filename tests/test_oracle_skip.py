@@ -29,6 +29,19 @@ mpmath = pytest.importorskip("mpmath")
 mpmath.mp.dps = 40
 
 
+def test_skip_ln_series_vs_mpmath():
+    """The table entries' own log (the series form) against mpmath."""
+    worst = 0.0
+    for k in range(-75, 107):
+        c = 1.0 + k / 256.0
+        if k == 0:
+            assert oracle.skip_ln_series(c) == 0.0
+            continue
+        ex = mpmath.log(mpmath.mpf(c))
+        worst = max(worst, float(abs((mpmath.mpf(oracle.skip_ln_series(c)) - ex) / ex)))
+    assert worst < 4e-16, worst
+
+
 def test_skip_ln_vs_mpmath():
     rng = np.random.default_rng(7)
     xs = list(rng.uniform(0.0, 1.0, 3000)) + list(np.exp(rng.uniform(-24, 0.7, 3000)))
@@ -171,7 +184,7 @@ def _fma(a, b, c):
     return float(Fraction(a) * Fraction(b) + Fraction(c))      # one correctly rounded result
 
 
-def _ln_ref(x):
+def _ln_series_ref(x):
     m, e = math.frexp(x)                                        # x = m 2^e, m in [0.5, 1)
     m, e = m * 2.0, e - 1                                       # m in [1, 2)
     if m > 1.4142135623730951:
@@ -183,6 +196,23 @@ def _ln_ref(x):
         s = _fma(s, y2, 1.0 / k)
     s = _fma(s, y2, 1.0)
     return e * 6.93147180369123816490e-01 + (e * 1.90821492927058770002e-10 + (2.0 * y) * s)
+
+
+_TAB = {k: (_ln_series_ref(1.0 + k / 256.0), 1.0 / (1.0 + k / 256.0)) for k in range(-75, 107)}
+
+
+def _ln_ref(x):
+    m, e = math.frexp(x)
+    m, e = m * 2.0, e - 1
+    if m > 1.4142135623730951:
+        m, e = m * 0.5, e + 1
+    k = math.floor((m - 1.0) * 256.0 + 0.5)
+    L, R = _TAB[k]
+    t = (m - (1.0 + k / 256.0)) * R
+    s = 1.0 / 7.0
+    for c in (-1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -1.0 / 2.0, 1.0):
+        s = _fma(s, t, c)
+    return e * 6.93147180369123816490e-01 + (e * 1.90821492927058770002e-10 + (L + t * s))
 
 
 def _skip_live_ref(g, scheme, pu, seed, rr_id):
@@ -219,6 +249,7 @@ def test_skip_words_and_gaps_match_reference():
         assert oracle.skip_word(seed, rid, v, blk, j) == w
         x = float(rng.uniform(1e-12, 1.5))
         assert oracle.skip_ln(x) == _ln_ref(x)
+        assert oracle.skip_ln_series(x) == _ln_series_ref(x)
 
 
 @pytest.mark.parametrize("scheme", [gi.W_WC, gi.W_UNIFORM])

@@ -11,7 +11,7 @@ P:211-236 for the trace).
 The oracle run is also the full single-core IMM time of the paper's baseline protocol
 (single-core IMM), recorded with the CPU model and the pinned core.
 
-    python tools/oracle_golden.py C3 [C4 C5 ...] [--core 0] [--fresh-final]
+    python tools/oracle_golden.py C3 [C4 C5 ...] [--core 0] [--fresh-final] [--skip]
 """
 from __future__ import annotations
 
@@ -51,7 +51,7 @@ def cpu_model() -> str:
     return platform.processor() or "unknown"
 
 
-def run(key: str, core: int, fresh_final: bool) -> dict:
+def run(key: str, core: int, fresh_final: bool, skip: bool = False) -> dict:
     w = gi.WORKLOADS[key]
     t0 = time.time()
     g = gi.workload_graph(key)
@@ -60,6 +60,8 @@ def run(key: str, core: int, fresh_final: bool) -> dict:
     os.sched_setaffinity(0, {core})
     o = oracle.Oracle(g, w.model, w.scheme, w.p_uniform)
     o.set_fresh_final(fresh_final)
+    if skip:
+        o.set_skip(True)
     t0 = time.perf_counter()
     r = o.imm(w.k, w.eps, w.ell, w.rr_seed)
     t_imm = time.perf_counter() - t0
@@ -69,7 +71,7 @@ def run(key: str, core: int, fresh_final: bool) -> dict:
     out = dict(
         config=key, desc=w.desc, n=g.n, m=g.m, model=w.model, scheme=w.scheme,
         p_uniform=w.p_uniform, k=w.k, eps=w.eps, ell=w.ell, rr_seed=w.rr_seed,
-        fresh_final=fresh_final, graph_sha256=graph_hash,
+        fresh_final=fresh_final, skip=skip, graph_sha256=graph_hash,
         seeds=r.seeds.tolist(), gains=[int(x) for x in r.gains], cov=r.cov, R_final=r.R_final,
         rounds=r.rounds, T_i=[int(x) for x in r.T_i], cov_i=[int(x) for x in r.cov_i],
         theta_i=r.theta_i.tolist(), LB=r.LB, theta=r.theta, spread_est=r.spread_est,
@@ -89,11 +91,12 @@ def main() -> None:
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--core", type=int, default=0)
     ap.add_argument("--fresh-final", action="store_true")
+    ap.add_argument("--skip", action="store_true", help="geometric-skip RNG contract (reading R31)")
     ap.add_argument("--out-dir", default=os.path.join(ROOT, "tests", "golden"))
     a = ap.parse_args()
     for key in a.configs:
-        res = run(key, a.core, a.fresh_final)
-        name = f"imm_{key}{'_fresh' if a.fresh_final else ''}.json"
+        res = run(key, a.core, a.fresh_final, a.skip)
+        name = f"imm_{key}{'_fresh' if a.fresh_final else ''}{'_skip' if a.skip else ''}.json"
         with open(os.path.join(a.out_dir, name), "w") as f:
             json.dump(res, f, indent=1)
         print(f"{key}: R={res['R_final']} seeds[:5]={res['seeds'][:5]} "

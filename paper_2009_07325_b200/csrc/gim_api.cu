@@ -85,7 +85,7 @@ struct gim_ctx {
   // generation scratch
   DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr, dump, lt_spill, esc_list;
   DevBuf bitmaps, gqueues;
-  DevBuf skip_spill;              // R31: per-warp global queue + hash of k_skip_warp (kEmpty when unused)
+  DevBuf spill;                   // per-warp global queue + hash of the warp kernels' spill tier (kEmpty when unused)
   uint32_t giant_slots = 0;
   uint32_t giant_n = 0;             // n the giant slots were sized for (reused while n <= giant_n)
   int giant_nt_opt = 0;             // GIM_OPT_GIANT_NT: 0 auto, else threads per giant CTA
@@ -99,7 +99,8 @@ struct gim_ctx {
   int skip = 0;                    // geometric-skip RNG contract (GIM_OPT_SKIP, reading R31)
   int skip_bps = 0;                // resident k_skip_lane CTAs per SM
   int skip_lane = -1;              // skip: -1 auto (lane kernel first for big chunks), 0 / 1
-  uint32_t skip_spill_cap = 0;     // skip: spill-tier set size limit (GIM_OPT_SKIP_SPILL; 0 = auto)
+  int64_t spill_cap = -1;          // spill-tier set size limit (GIM_OPT_SPILL; -1 = auto)
+  uint32_t spill_cap_eff = 0;      // the cap of the current generate call (<= qcap: no spill)
   uint32_t max_deg = 0;            // largest in-degree of the loaded graph
   DevBuf skip_tab;                 // skip: log centers L_k, R_k (2 x 184 doubles) + inv per in-degree
   bool skip_tab_valid = false;
@@ -120,6 +121,11 @@ struct gim_ctx {
   DevBuf seg_desc;              // device InvSegDev[kMaxInvSeg] + uint32 nseg
   DevBuf cand;                  // argmax candidates + hist[33] + tau_p1 + ncand
   int use_cand = 1;             // GIM_OPT_ARGMAX_CAND
+  uint32_t sel_fused = 0;       // GIM_OPT_SELECT_FUSED: candidate cap of the fused steps (0 = off)
+  bool force_unfused = false;   // the fused selection failed its certificate: redo unfused
+  bool sel_fused_used = false;  // the pending selection ran fused
+  DevBuf sel_done;              // fused steps: per-step completion tickets + the fail flag
+  int fused_ctas = 2;           // fused cover grid = this x #SMs (fewer tickets per step)
   // options
   int force_giant = 0, profile = 0;
   int mb_chains = 8;            // GIM_OPT_MB_CHAINS: Philox chains per thread in the microbenchmark
@@ -363,6 +369,8 @@ RRParams base_params(gim_ctx* c) {
   p.thr_uniform = c->thr_uniform;
   p.p_uniform = c->p_uniform;
   p.skip_tab = c->skip_tab.as<double>();
+  p.spill = c->spill.as<uint32_t>();
+  p.spill_cap = c->spill_cap_eff;
   p.seed = c->seed;
   {
     uint32_t k0 = (uint32_t)c->seed, k1 = (uint32_t)(c->seed >> 32);
@@ -419,6 +427,26 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     }
   }
   CK(cudaMemsetAsync(c->ctr.p, 0, sizeof(GenCounters), c->stream));
+  if (c->model == MODEL_IC) {
+    // spill tier of the warp kernels. Auto: WC sets grow by ~1 live in-edge per node (deep,
+    // narrow: kept in flight beside the small ones in the warp's spill tier); uniform-p sets
+    // become big through hubs of thousands of live in-edges (wide: better spread over a CTA)
+    // (per-edge coins: no spill by default — a giant set's ~10^5 coins on one warp finish
+    // after the rest of the launch; measured C3 sampling 16.5 vs 14.4 ms with K-GIANT)
+    uint32_t cap = c->spill_cap >= 0 ? (uint32_t)c->spill_cap
+                                     : (!c->skip ? 0u : (c->scheme == W_WC ? kSpillQ : 2048u));
+    cap = std::min<uint32_t>(cap, kSpillQ);
+    c->spill_cap_eff = cap;
+    if (cap > c->qcap) {
+      const uint64_t need = (uint64_t)c->num_sms * kRRBlocksPerSM * kRRWarps * spill_words_per_warp() * 4;
+      if (c->spill.bytes < need) {             // hash halves must start (and stay) empty
+        TRY(dalloc(c, c->spill, need));
+        CK(cudaMemsetAsync(c->spill.p, 0xFF, need, c->stream));
+      }
+    }
+  } else {
+    c->spill_cap_eff = 0;
+  }
   if (c->skip && !c->skip_tab_valid) {         // R31: log-center tables + 1/ln(1-p) per in-degree
     const uint64_t nd = (c->scheme == W_WC ? (uint64_t)c->max_deg : 0) + 2;
     TRY(ensure(c, c->skip_tab, (2 * kSkipTabK + nd) * 8));
@@ -469,17 +497,6 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
         pw.count_ptr = &c->ctr.as<GenCounters>()->esc_count;
       }
       {
-        const uint64_t spill_b = (uint64_t)c->num_sms * kRRBlocksPerSM * kRRWarps * skip_spill_words_per_warp() * 4;
-        if (c->skip_spill.bytes < spill_b) {           // hash halves must start (and stay) empty
-          TRY(dalloc(c, c->skip_spill, spill_b));
-          CK(cudaMemsetAsync(c->skip_spill.p, 0xFF, spill_b, c->stream));
-        }
-        pw.skip_spill = c->skip_spill.as<uint32_t>();
-        // auto: WC sets grow by ~1 live in-edge per node (deep, narrow: the warp's spill tier
-        // keeps them in flight beside the small ones); uniform-p sets become big through hubs of
-        // thousands of live in-edges (wide: better spread over a CTA by the giant kernel)
-        const uint32_t cap = c->skip_spill_cap ? c->skip_spill_cap : (c->scheme == W_WC ? 16384u : 2048u);
-        pw.skip_spill_cap = std::min<uint32_t>(cap, (uint32_t)skip_spill_words_per_warp() / 3);
         Prof pf(c, CLS_RR);
         TRY(launched(c, launch_skip_warp(c->scheme, pw, c->num_sms * kRRBlocksPerSM, c->stream), "k_skip_warp"));
         c->st.n_rr_launches++;
@@ -794,7 +811,10 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   uint32_t* cand = nullptr;
   unsigned int *hist = nullptr, *ncand = nullptr;
   uint32_t* tau_p1 = nullptr;
-  if (!dec && c->rounds == 1 && (c->use_cand == 2 || (c->use_cand == 1 && n >= (1u << 23)))) {   // small n: full scan is cheaper
+  const bool fused_mode = !dec && c->rounds == 1 && c->sel_fused && !c->force_unfused && !c->speculate &&
+                          !c->sel_persistent;
+  if (!fused_mode && !dec && c->rounds == 1 &&
+      (c->use_cand == 2 || (c->use_cand == 1 && n >= (1u << 23)))) {   // small n: full scan is cheaper
     TRY(ensure(c, c->cand, (uint64_t)kMaxCand * 4 + 64 * 4));
     cand = c->cand.as<uint32_t>();
     hist = reinterpret_cast<unsigned int*>(cand + kMaxCand);
@@ -803,7 +823,58 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
     TRY(launched(c, launch_cand_setup(c->cnt.as<uint32_t>(), (uint32_t)n, kMaxCand, hist, tau_p1, cand, ncand,
                                       c->num_sms * 4, c->stream), "candidate setup", 3));
   }
-  if (!dec && !cand && c->sel_persistent) {
+  // fused greedy steps (P = 1, standard IM): one launch per step, candidate argmax in the last
+  // CTA of each cover; certificate failures are redone unfused by select_finish
+  const bool fused = !dec && c->rounds == 1 && c->sel_fused && !c->force_unfused && !c->speculate &&
+                     !c->sel_persistent;
+  c->sel_fused_used = fused;
+  uint32_t* fflag = nullptr;
+  unsigned int* done = nullptr;
+  if (fused) {
+    const uint32_t cap = c->sel_fused;
+    TRY(ensure(c, c->cand, (uint64_t)cap * 4 + 64 * 4));
+    cand = c->cand.as<uint32_t>();
+    hist = reinterpret_cast<unsigned int*>(cand + cap);
+    tau_p1 = reinterpret_cast<uint32_t*>(hist + 40);
+    ncand = reinterpret_cast<unsigned int*>(hist + 41);
+    TRY(launched(c, launch_cand_setup(c->cnt.as<uint32_t>(), (uint32_t)n, cap, hist, tau_p1, cand, ncand,
+                                      c->num_sms * 4, c->stream), "candidate setup", 3));
+    TRY(ensure(c, c->sel_done, ((uint64_t)kk + 2) * 4));
+    done = c->sel_done.as<unsigned int>();
+    fflag = reinterpret_cast<uint32_t*>(done + kk);
+    CK(cudaMemsetAsync(done, 0, ((uint64_t)kk + 2) * 4, c->stream));
+  }
+  if (fused) {
+    const std::vector<uintptr_t> key = {(uintptr_t)c->cnt.p, (uintptr_t)segd, (uintptr_t)cand,
+                                        (uintptr_t)c->offsets.p, (uintptr_t)c->pool.p, (uintptr_t)c->covered.p,
+                                        (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n, (uintptr_t)limited,
+                                        (uintptr_t)c->rounds, (uintptr_t)done, (uintptr_t)c->fused_ctas};
+    int nl = 0;
+    if (c->use_graph) {
+      if (!c->sel_exec || key != c->sel_key) {
+        if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
+        c->sel_exec = nullptr;
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        launch_select_fused(keys, (int)kk, segd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
+                            c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), cand, ncand, tau_p1, done, fflag,
+                            c->num_sms * c->fused_ctas, c->stream, limited, &nl);
+        CK(cudaStreamEndCapture(c->stream, &graph));
+        const cudaError_t ie = cudaGraphInstantiate(&c->sel_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) return fail_cuda(c, "cudaGraphInstantiate", ie);
+        c->sel_key = key;
+      }
+      Prof pf(c, CLS_SELECT);
+      TRY(launched(c, cudaGraphLaunch(c->sel_exec, c->stream), "selection graph (fused)", (int)kk + 1));
+    } else {
+      Prof pf(c, CLS_SELECT);
+      TRY(launched(c, launch_select_fused(keys, (int)kk, segd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
+                                          c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), cand, ncand, tau_p1, done,
+                                          fflag, c->num_sms * c->fused_ctas, c->stream, limited, &nl),
+                   "fused selection", (int)kk + 1));
+    }
+  } else if (!dec && !cand && c->sel_persistent) {
     // P = 1: the k greedy steps in one cooperative launch, grid barriers between the phases
     TRY(ensure(c, c->sel_bar, 64));
     CK(cudaMemsetAsync(c->sel_bar.p, 0, 8, c->stream));
@@ -858,13 +929,15 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
       }
     }
   }
-  if (c->h_keys_cap < kk) {
+  if (c->h_keys_cap < kk + 1) {
     if (c->h_keys) cudaFreeHost(c->h_keys);
     c->h_keys = nullptr;
-    CK(cudaMallocHost(&c->h_keys, (uint64_t)kk * 8));
-    c->h_keys_cap = kk;
+    CK(cudaMallocHost(&c->h_keys, ((uint64_t)kk + 1) * 8));
+    c->h_keys_cap = kk + 1;
   }
   CK(cudaMemcpyAsync(c->h_keys, keys, (uint64_t)kk * 8, cudaMemcpyDeviceToHost, c->stream));
+  c->h_keys[kk] = 0;
+  if (fused) CK(cudaMemcpyAsync(c->h_keys + kk, fflag, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaEventRecord(c->ev_sel_done, c->stream));
   c->sel_pending = true;
   return GIM_OK;
@@ -873,6 +946,16 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
 gim_status select_finish(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains, uint64_t* covered) {
   TRY(sync(c));
   c->sel_pending = false;
+  if (c->sel_fused_used && c->h_keys[(uint64_t)k * c->rounds]) {
+    // a candidate argmax could not be certified (best candidate below tau): redo unfused
+    c->st.fused_fallbacks++;
+    c->force_unfused = true;
+    const gim_status st = select_launch(c, k);
+    c->force_unfused = false;
+    TRY(st);
+    TRY(sync(c));
+    c->sel_pending = false;
+  }
   uint64_t cov = 0;
   for (uint32_t j = 0; j < k * c->rounds; ++j) {
     seeds[j] = ~(uint32_t)(c->h_keys[j] & 0xFFFFFFFFull);
@@ -982,7 +1065,7 @@ void gim_destroy(gim_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
                     &c->sizes, &c->soff, &c->giant_list, &c->retry_list, &c->item_list, &c->scan_out,
-                    &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->skip_spill, &c->skip_tab, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
+                    &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->spill, &c->skip_tab, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
                     &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->thr_node, &c->ag_small,
                     &c->ag_send, &c->ag_recv, &c->sel_bar};
@@ -1405,9 +1488,9 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_MB_CHAINS: c->mb_chains = (int)value; return GIM_OK;
     case GIM_OPT_SPECULATE: c->speculate = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_FRESH_FINAL: c->fresh_final = value ? 1 : 0; return GIM_OK;
-    case GIM_OPT_SKIP_SPILL:
-      if (value < 0 || value > 16384) return fail(c, GIM_EINVAL, "spill cap must be in [0 (auto), 16384]");
-      c->skip_spill_cap = (uint32_t)value;
+    case GIM_OPT_SPILL:
+      if (value < -1 || value > (int64_t)kSpillQ) return fail(c, GIM_EINVAL, "spill cap must be in [-1 (auto), 16384]");
+      c->spill_cap = value;
       return GIM_OK;
     case GIM_OPT_SKIP: {
       const int on = value ? 1 : 0;
@@ -1432,6 +1515,16 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
       c->sel_exec = nullptr;
       return GIM_OK;
     case GIM_OPT_IC_LANE: c->ic_lane = (value < -1 || value > 1) ? -1 : (int)value; return GIM_OK;
+    case GIM_OPT_FUSED_CTAS:
+      if (value < 1 || value > 16) return fail(c, GIM_EINVAL, "fused CTAs per SM must be in [1, 16]");
+      c->fused_ctas = (int)value;
+      if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
+      c->sel_exec = nullptr;
+      return GIM_OK;
+    case GIM_OPT_SELECT_FUSED:
+      if (value < 0 || value > (1 << 16)) return fail(c, GIM_EINVAL, "fused candidate cap must be in [0, 65536]");
+      c->sel_fused = (uint32_t)value;
+      return GIM_OK;
     case GIM_OPT_ARGMAX_CAND: c->use_cand = (value < 0 || value > 2) ? 1 : (int)value; return GIM_OK;
     case GIM_OPT_STAGING_CAP:
       if (value < 0) return fail(c, GIM_EINVAL, "staging cap must be >= 0");

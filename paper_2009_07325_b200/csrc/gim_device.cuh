@@ -150,8 +150,8 @@ struct RRParams {
   uint32_t* retry_list;        // items whose staging write failed
   uint32_t qcap;               // shared-memory queue capacity (<= kQMax)
   uint32_t* lt_spill;          // LT: per-warp spill of walks longer than kLtCap (lane-interleaved)
-  uint32_t* skip_spill;        // R31 warp kernel: per-warp global queue + hash for sets > qcap
-  uint32_t skip_spill_cap;     // R31: sets beyond this many nodes go to the CTA giant kernel
+  uint32_t* spill;             // warp kernels: per-warp global queue + hash for sets > qcap
+  uint32_t spill_cap;          // sets beyond this many nodes go to the CTA giant kernel (<= qcap: no spill)
   int force_giant;
   uint32_t rounds;             // MRIM rounds T (1 = standard IM): root of id = root(id / T)
 };
@@ -211,5 +211,28 @@ constexpr int kIcLaneWarps = 8;      // K-IC lane kernel: warps per CTA
 constexpr int kIcLaneCap = 32;       // K-IC lane kernel: set size limit (then escalate)
 constexpr uint32_t kIcLaneMaxDeg = 256;   // K-IC lane kernel: in-degree limit (then escalate)
 constexpr int kGiantWin = 2048;      // frontier window of the giant kernel (smem)
+
+// Spill tier of the warp-per-set kernels (K-RR and the R31 warp kernel): a set that outgrows the
+// shared-memory queue continues in its warp's global queue gq (kSpillQ entries) and open-
+// addressing hash gh (kSpillH slots, kEmpty when unused, L2-resident) instead of being handed to
+// the CTA-per-set giant kernel: giant sets then run beside the small ones.
+constexpr uint32_t kSpillQ = 16384;
+constexpr uint32_t kSpillH = 32768;          // power of two
+__device__ __forceinline__ bool spill_hash_insert(uint32_t* gh, uint32_t u) {
+  uint32_t s = (u * 0x9E3779B1u) >> 17;       // top 15 bits: kSpillH = 2^15 slots
+  while (true) {
+    const uint32_t old = atomicCAS(&gh[s], kEmpty, u);
+    if (old == kEmpty) return true;
+    if (old == u) return false;
+    s = (s + 1) & (kSpillH - 1u);
+  }
+}
+// walk from u's home slot to the slot holding it (holes left by members erased before cannot
+// stop the walk: it compares against u, not against empty)
+__device__ __forceinline__ void spill_hash_erase(uint32_t* gh, uint32_t u) {
+  uint32_t s = (u * 0x9E3779B1u) >> 17;
+  while (gh[s] != u) s = (s + 1) & (kSpillH - 1u);
+  gh[s] = kEmpty;
+}
 
 }  // namespace gim

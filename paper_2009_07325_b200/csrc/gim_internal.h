@@ -17,7 +17,7 @@ cudaError_t launch_skip_warp(int scheme, const RRParams& p, int grid, cudaStream
 cudaError_t launch_skip_giant(int scheme, const RRParams& p, int grid, uint32_t* bitmaps, uint32_t* gqueues,
                               uint64_t bm_words, cudaStream_t s);
 int skip_lane_blocks_per_sm();
-uint64_t skip_spill_words_per_warp();
+uint64_t spill_words_per_warp();   // spill tier of the warp kernels: words per warp
 constexpr int kSkipTabK = 184;   // log centers k = -75..106 (+ padding) of the R31 ln
 cudaError_t launch_skip_tables(int scheme, float p_uniform, uint32_t max_deg, double* tab, cudaStream_t s);
 cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const uint64_t* soff,
@@ -69,6 +69,11 @@ cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev*
                          const uint64_t* offsets, const uint32_t* pool,
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s,
                          bool limit, const MrimSel* mr = nullptr);
+// fused greedy steps (P = 1): candidate argmax of step 0, then per step cover + next argmax
+cudaError_t launch_select_fused(unsigned long long* keys, int kk, const InvSegDev* segs, const uint64_t* offsets,
+                                const uint32_t* pool, uint8_t* covered, uint32_t* cnt, const uint32_t* cand,
+                                const unsigned int* ncand, const uint32_t* tau_p1, unsigned int* done,
+                                uint32_t* fail, int grid, cudaStream_t s, bool limit, int* launches);
 cudaError_t launch_validate_csr(const uint64_t* rp64, uint32_t n, uint64_t m, const uint32_t* src,
                                 uint32_t* rp32, uint32_t* err, uint32_t* bad_row, uint32_t* thr_node, int grid,
                                 cudaStream_t s);

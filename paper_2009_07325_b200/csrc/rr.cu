@@ -312,6 +312,11 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
   const uint32_t pend_s = (uint32_t)__cvta_generic_to_shared(pend);
   for (int i = lane; i < kHSize; i += 32) h[i] = kEmpty;
   __syncwarp();
+  // spill tier (p.spill_cap > p.qcap): this warp's global queue + hash for sets > qcap
+  const uint64_t gwarp = (uint64_t)blockIdx.x * kRRWarps + (threadIdx.x >> 5);
+  uint32_t* gq = p.spill + gwarp * (uint64_t)(kSpillQ + kSpillH);
+  uint32_t* gh = gq + kSpillQ;
+  const bool can_spill = p.spill_cap > p.qcap;
   const uint32_t k0 = (uint32_t)p.seed, k1 = (uint32_t)(p.seed >> 32);
   unsigned long long coins = 0;     // per-lane counters (statistics only)
   uint32_t lives = 0;
@@ -347,6 +352,7 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
     __syncwarp();
     uint32_t head = 0, tail = 1, resume = 0;
     bool overflow = false;
+    bool spilled = false;                              // warp-uniform: members in gq / gh
     if (MODEL == MODEL_IC) {
       const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
       // Live in-edges found during a batch are not resolved on the spot: each lane starts an
@@ -364,12 +370,23 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
           bool isnew = false;
           if (i < npend) {
             u = pend[i];
-            isnew = hash_insert(h, u);
+            isnew = spilled ? spill_hash_insert(gh, u) : hash_insert(h, u);
           }
           const uint32_t has = __ballot_sync(kFull, isnew);
           const uint32_t total = __popc(has);
-          if (tail + total > p.qcap) { ok = false; break; }
-          if (isnew) q[tail + __popc(has & ((1u << lane) - 1u))] = u;
+          if (!spilled && can_spill && tail + total > p.qcap) {
+            // move the set to the spill tier: queue copied, members re-inserted in gh
+            for (uint32_t t = lane; t < tail; t += 32) {
+              const uint32_t x = q[t];
+              gq[t] = x;
+              spill_hash_insert(gh, x);
+            }
+            if (isnew) spill_hash_insert(gh, u);
+            spilled = true;
+            __syncwarp();
+          }
+          if (tail + total > (spilled ? p.spill_cap : p.qcap)) { ok = false; break; }
+          if (isnew) (spilled ? gq : q)[tail + __popc(has & ((1u << lane) - 1u))] = u;
           tail += total;
         }
         npend = 0;
@@ -403,7 +420,7 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
         const uint32_t nb = min(tail - head, 32u);
         uint32_t a = 0, b = 0, thr = 0, ng = 0;
         if (lane < nb) {
-          const uint32_t v = q[head + lane];
+          const uint32_t v = spilled ? gq[head + lane] : q[head + lane];
           const uint32_t tv = (SCHEME == W_WC) ? __ldg(p.thr_node + v) : 0u;   // loads in parallel
           a = __ldg(p.row_ptr + v);
           b = __ldg(p.row_ptr + v + 1);
@@ -486,7 +503,7 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
       off = __shfl_sync(kFull, off, 0);
       const bool fits = off + tail <= p.dump_cap;
       if (fits)
-        for (uint32_t t = lane; t < tail; t += 32) p.dump[off + t] = q[t];
+        for (uint32_t t = lane; t < tail; t += 32) p.dump[off + t] = spilled ? gq[t] : q[t];
       if (lane == 0)
         p.giant_recs[atomicAdd(&p.ctr->giant_count, 1u)] =
             fits ? GiantRec{item, tail, resume, 0u, off} : GiantRec{item, 0u, 0u, 0u, 0ull};
@@ -504,13 +521,22 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
       if (off + tail > p.stage_cap) {
         if (lane == 0) p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = item;
       } else {
-        for (uint32_t t = lane; t < tail; t += 32) p.staging[off + t] = q[t];
+        for (uint32_t t = lane; t < tail; t += 32) p.staging[off + t] = spilled ? gq[t] : q[t];
         if (lane == 0) { p.sizes[item] = tail; p.soff[item] = off; }
       }
     }
-    // clear the visited hash (vectorised; 4 KB)
+    // clear the visited structures: the shared hash as a whole (vectorised, 4 KB: measured
+    // faster than erasing by member list, 11.41 vs 11.71 ms C3 sampling); the spill hash by
+    // member list, or wholly after an overflow (nodes hashed but never queued)
+    if (overflow) cp_async_wait_all();
     uint4* h4 = reinterpret_cast<uint4*>(h);
     for (int t = lane; t < kHSize / 4; t += 32) h4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    if (spilled && overflow) {
+      uint4* gh4 = reinterpret_cast<uint4*>(gh);
+      for (uint32_t t = lane; t < kSpillH / 4; t += 32) gh4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    } else if (spilled) {
+      for (uint32_t t = lane; t < tail; t += 32) spill_hash_erase(gh, gq[t]);
+    }
     __syncwarp();
   }
   // per-warp statistics

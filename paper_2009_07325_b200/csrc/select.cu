@@ -506,6 +506,84 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
   cover_step<LIMIT>(keys, j, segs, offsets, pool, covered, cnt, dec, mr);
 }
 
+// ------------------------------------------------------------------------------------------
+// Fused greedy step (P = 1): k_cover_next(j) retires pick j and decrements (cover_step), then the
+// last CTA to finish — a completion ticket per step — computes pick j + 1 over the candidate
+// list: the nodes whose initial count reaches tau (at most a few thousand). Counts only
+// decrease, so a best candidate count >= tau certifies the argmax over all nodes (every other
+// node started below tau); otherwise *fail is set and the host redoes the selection with the
+// full-scan argmax. One launch and one dependency chain per greedy step instead of two.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cand_argmax_cta(const uint32_t* cnt, const uint32_t* __restrict__ cand,
+                                                uint32_t nc, uint32_t tau_p1, unsigned long long* keys, int j,
+                                                uint32_t* fail) {
+  __shared__ unsigned long long s_cbest[32];
+  unsigned long long best = 0;
+  for (uint32_t i0 = threadIdx.x; i0 < nc; i0 += 4 * blockDim.x) {
+    uint32_t v[4], c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t i = i0 + u * blockDim.x;
+      v[u] = i < nc ? cand[i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = (i0 + u * blockDim.x < nc) ? __ldcg(cnt + v[u]) : kSent;   // L2: atomics land there
+#pragma unroll
+    for (int u = 0; u < 4; ++u) argmax_one(c[u], v[u], best, 0u);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+    best = o > best ? o : best;
+  }
+  if ((threadIdx.x & 31) == 0) s_cbest[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    best = (threadIdx.x < (blockDim.x >> 5)) ? s_cbest[threadIdx.x] : 0ull;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+      best = o > best ? o : best;
+    }
+    if (threadIdx.x == 0) {
+      keys[j] = best;
+      if (best == 0ull || (uint32_t)(best >> 32) < tau_p1) atomicExch(fail, 1u);   // not certified
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_cand_argmax0(const uint32_t* cnt, const uint32_t* __restrict__ cand,
+                                                      const unsigned int* __restrict__ ncand,
+                                                      const uint32_t* __restrict__ tau_p1,
+                                                      unsigned long long* keys, uint32_t* fail) {
+  cand_argmax_cta(cnt, cand, *ncand, *tau_p1, keys, 0, fail);
+}
+
+template <bool LIMIT>
+__global__ void __launch_bounds__(256) k_cover_next(unsigned long long* __restrict__ keys, int j, int kk,
+                                                    const InvSegDev* __restrict__ segs,
+                                                    const uint64_t* __restrict__ offsets,
+                                                    const uint32_t* __restrict__ pool,
+                                                    uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
+                                                    const uint32_t* __restrict__ cand,
+                                                    const unsigned int* __restrict__ ncand,
+                                                    const uint32_t* __restrict__ tau_p1,
+                                                    unsigned int* __restrict__ done, uint32_t* fail) {
+  if (keys[j] == 0ull) return;                 // no candidate left (already failed): the rest no-ops
+  cover_step<LIMIT>(keys, j, segs, offsets, pool, covered, cnt, nullptr, MrimSel{1u, 0u, 0u});
+  if (j + 1 >= kk) return;
+  __shared__ uint32_t s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();                            // this CTA's decrements before its ticket
+    s_last = atomicAdd(done + j, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  cand_argmax_cta(cnt, cand, *ncand, *tau_p1, keys, j + 1, fail);
+}
+
 // Grid-wide barrier of a co-resident (cooperatively launched) grid: generation counter; the
 // arriving CTA reads the generation before arriving, the last arrival resets the count and bumps
 // the generation; fences order every CTA's writes of the phase before the next phase's reads.
@@ -659,6 +737,23 @@ cudaError_t launch_select_persistent(uint32_t* cnt, uint32_t n, unsigned long lo
   const int grid = num_sms;
   void* args[] = {&cnt, &n, &keys, &kk, &segs, &offsets, &pool, &covered, (void*)&m, (void*)&excl, &bar};
   return cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(1024), args, 0, s);
+}
+
+cudaError_t launch_select_fused(unsigned long long* keys, int kk, const InvSegDev* segs, const uint64_t* offsets,
+                                const uint32_t* pool, uint8_t* covered, uint32_t* cnt, const uint32_t* cand,
+                                const unsigned int* ncand, const uint32_t* tau_p1, unsigned int* done,
+                                uint32_t* fail, int grid, cudaStream_t s, bool limit, int* launches) {
+  k_cand_argmax0<<<1, 256, 0, s>>>(cnt, cand, ncand, tau_p1, keys, fail);
+  for (int j = 0; j < kk; ++j) {
+    if (limit)
+      k_cover_next<true><<<grid, 256, 0, s>>>(keys, j, kk, segs, offsets, pool, covered, cnt, cand, ncand, tau_p1,
+                                              done, fail);
+    else
+      k_cover_next<false><<<grid, 256, 0, s>>>(keys, j, kk, segs, offsets, pool, covered, cnt, cand, ncand, tau_p1,
+                                               done, fail);
+  }
+  *launches = kk + 1;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,

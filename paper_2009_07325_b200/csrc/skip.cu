@@ -437,24 +437,7 @@ __device__ __forceinline__ bool skip_expand_batch(const RRParams& p, const doubl
 // global spill tier; one that outgrows that too becomes a giant record (restarted from its
 // root by k_skip_giant: the draws are keyed, so the replay is exact).
 // ------------------------------------------------------------------------------------------
-constexpr uint32_t kSpillQ = 16384;          // k_skip_warp spill tier: queue entries per warp
-constexpr uint32_t kSpillH = 32768;          //   and open-addressing hash slots (power of two)
-uint64_t skip_spill_words_per_warp() { return kSpillQ + kSpillH; }
-
-__device__ __forceinline__ bool spill_hash_insert(uint32_t* gh, uint32_t u) {
-  uint32_t s = (u * 0x9E3779B1u) >> 17;       // top 15 bits: kSpillH = 2^15 slots
-  while (true) {
-    const uint32_t old = atomicCAS(&gh[s], kEmpty, u);
-    if (old == kEmpty) return true;
-    if (old == u) return false;
-    s = (s + 1) & (kSpillH - 1u);
-  }
-}
-__device__ __forceinline__ void spill_hash_erase(uint32_t* gh, uint32_t u) {
-  uint32_t s = (u * 0x9E3779B1u) >> 17;
-  while (gh[s] != u) s = (s + 1) & (kSpillH - 1u);
-  gh[s] = kEmpty;
-}
+uint64_t spill_words_per_warp() { return kSpillQ + kSpillH; }
 
 template <int SCHEME>
 __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_skip_warp(RRParams p) {
@@ -470,7 +453,7 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_skip_warp(RRP
   // queue gq (kSpillQ) + hash gh (kSpillH, L2-resident) instead of being restarted elsewhere —
   // giant sets then run concurrently with (and hidden behind) the small ones
   const uint64_t gwarp = (uint64_t)blockIdx.x * kRRWarps + (threadIdx.x >> 5);
-  uint32_t* gq = p.skip_spill + gwarp * (uint64_t)(kSpillQ + kSpillH);
+  uint32_t* gq = p.spill + gwarp * (uint64_t)(kSpillQ + kSpillH);
   uint32_t* gh = gq + kSpillQ;
   for (int i = lane; i < kHSize; i += 32) h[i] = kEmpty;
   __syncwarp();
@@ -524,7 +507,7 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_skip_warp(RRP
           spilled = true;
           __syncwarp();
         }
-        if (spilled && tail + total > p.skip_spill_cap) { ok = false; break; }
+        if (spilled && tail + total > p.spill_cap) { ok = false; break; }
         if (isnew) (spilled ? gq : q)[tail + __popc(has & ((1u << lane) - 1u))] = u;
         tail += total;
       }

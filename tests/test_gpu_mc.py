@@ -55,8 +55,7 @@ def _ris_estimate(c_pool, n, S, T):
     return n * hit.mean()
 
 
-@pytest.mark.parametrize("key", ["C3", pytest.param("C5", marks=pytest.mark.skipif(
-    os.environ.get("GIM_TEST_C5") != "1", reason="C5 graph generation takes minutes: set GIM_TEST_C5=1"))])
+@pytest.mark.parametrize("key", ["C3", "C5"])
 def test_mc_verified_spread_full_size(key):
     """north_star: Monte-Carlo-verified spread within 1% — IMM's seeds at BASELINE size, forward
     MC (2,000 instance graphs) vs n * F_R'(S) on an independent pool R' (2^21 sets, another seed;

@@ -87,9 +87,14 @@ def test_pool_parity_tiny(gname):
                                   {P.OPT_IC_LANE: 1}, {P.OPT_IC_LANE: 1, P.OPT_STAGING_CAP: 64},
                                   {P.OPT_IC_LANE: 1, P.OPT_FORCE_GIANT: 1}, {P.OPT_IC_LANE: 1, P.OPT_QUEUE_CAP: 8},
                                   {P.OPT_FORCE_GIANT: 1, P.OPT_GIANT_NT: 128}, {P.OPT_QUEUE_CAP: 16, P.OPT_GIANT_NT: 128},
-                                  {P.OPT_FORCE_GIANT: 1, P.OPT_GIANT_NT: 256}])
+                                  {P.OPT_FORCE_GIANT: 1, P.OPT_GIANT_NT: 256},
+                                  {P.OPT_SPILL: 0}, {P.OPT_QUEUE_CAP: 8, P.OPT_SPILL: 64},
+                                  {P.OPT_QUEUE_CAP: 32, P.OPT_SPILL: 40, P.OPT_STAGING_CAP: 1000},
+                                  {P.OPT_IC_LANE: 1, P.OPT_QUEUE_CAP: 4, P.OPT_SPILL: 16384}])
 def test_pool_parity_C1_invariance(opts):
-    """Same pool whatever the queue capacity, forced fallback or staging retries."""
+    """Same pool whatever the queue capacity, spill-tier capacity (sets beyond the shared queue
+    continue in the warp's global queue + hash, beyond the spill cap in K-GIANT), forced
+    fallback or staging retries."""
     w = gi.WORKLOADS["C1"]
     g = gi.workload_graph("C1")
     T = 40013
@@ -256,8 +261,7 @@ def test_imm_parity_BA_small():
     assert np.array_equal(r.seeds, ro.seeds), (r.seeds, ro.seeds)
 
 
-@pytest.mark.parametrize("key", ["C3", "C4", "B8", "B32", pytest.param("C5", marks=pytest.mark.skipif(
-    os.environ.get("GIM_TEST_C5") != "1", reason="C5 graph generation takes minutes: set GIM_TEST_C5=1"))])
+@pytest.mark.parametrize("key", ["C3", "C4", "B8", "B32", "C5"])
 def test_full_size_sampled(key):
     """BASELINE.json full size: 2^21 RR sets in the launch configuration bench.py times; sampled
     ids recomputed one by one by the oracle; counts checked by the size-free identities."""
@@ -500,3 +504,27 @@ def test_select_persistent_equals_oracle(rounds):
     r = c.imm(k, w.eps, w.ell, w.rr_seed)
     ro = o.imm(k, w.eps, w.ell, w.rr_seed) if rounds == 1 else o.mrim(k, rounds, w.eps, w.ell, w.rr_seed)
     assert np.array_equal(r.seeds, ro.seeds) and r.R_final == ro.R_final
+
+
+@pytest.mark.parametrize("key", ["C1", "C2"])
+def test_fused_selection_modes(key):
+    """GIM_OPT_SELECT_FUSED (one launch per greedy step, candidate argmax certified by tau in the
+    last CTA): every candidate cap — including caps so small that the certificate fails and the
+    selection is redone unfused — gives the oracle's seeds and gains (O7, Alg. 7)."""
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    T = 50021
+    o = oracle.Oracle(g, w.model, w.scheme, w.p_uniform)
+    o.generate(T, w.rr_seed)
+    os_, og, oc = o.select(w.k)
+    for cap, graph in ((2048, 1), (2048, 0), (64, 1), (1, 1), (0, 1)):
+        c = _ctx(g, w.model, w.scheme, w.p_uniform, {P.OPT_SELECT_FUSED: cap, P.OPT_SELECT_GRAPH: graph})
+        c.generate_rr(T, w.rr_seed)
+        c.reset_stats()
+        s, gn, cv = c.select(w.k)
+        assert np.array_equal(s, os_) and np.array_equal(gn, og) and cv == oc, cap
+        if cap == 1:
+            assert c.stats()["fused_fallbacks"] >= 1
+        s2, g2, c2 = c.select(w.k)                  # non-destructive, graph replay
+        assert np.array_equal(s2, os_) and np.array_equal(g2, og)
+        c.close()

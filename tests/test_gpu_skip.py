@@ -88,7 +88,7 @@ def test_skip_tiers_big_sets():
     g = gi.from_edges(leaves + 302, edges)
     T = 4000
     for m, cap in ((1, 2048), (2, 16384), (3, 600), (3, 16384)):
-        c = _ctx(g, gi.W_UNIFORM, 0.9, m, {P.OPT_SKIP_SPILL: cap})
+        c = _ctx(g, gi.W_UNIFORM, 0.9, m, {P.OPT_SPILL: cap})
         c.generate_rr(T, 3)
         o = _oracle(g, gi.W_UNIFORM, 0.9)
         o.generate(T, 3)

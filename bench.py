@@ -56,8 +56,13 @@ def parse():
     ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (functional testing)")
     ap.add_argument("--skip", action="store_true",
                     help="geometric-skip RNG contract (reading R31, GIM_OPT_SKIP) instead of one coin per in-edge")
-    ap.add_argument("--dense-exchange", action="store_true",
-                    help="N > 1: per-step count/decrement all-reduce instead of the replicated pool")
+    ap.add_argument("--protocol", default="replicated", choices=["replicated", "allreduce", "reducescatter"],
+                    help="N > 1 exchange: replicated pool (all-gather per round), dense per-step "
+                         "all-reduce (north_star), or node-sharded reduce-scatter selection")
+    ap.add_argument("--dense-exchange", action="store_true", help="alias of --protocol allreduce")
+    ap.add_argument("--force-collectives", action="store_true",
+                    help="run the --protocol exchange even at N = 1 (drives the NCCL callbacks on one GPU)")
+    ap.add_argument("--no-variants", action="store_true", help="skip the geometric-skip variant measurement")
     return ap.parse_args()
 
 
@@ -72,7 +77,12 @@ def unit_of(args):
     return UNIT if args.rounds == 1 else "MRIM sets/s"
 
 
-def config_of(w, world, rounds=1):
+PROTO_DESC = {"replicated": "each round's sets all-gathered, NodeSelection replicated",
+              "allreduce": "count all-reduce + per-step decrement all-reduce",
+              "reducescatter": "node-sharded selection: counts/decrements reduce-scattered, per-step key exchange"}
+
+
+def config_of(w, world, rounds=1, protocol="replicated", force=False):
     mr = {} if rounds == 1 else {"mrim_rounds": rounds,
                                  "mrim": f"CR-NAIMM (§4.8): k={w.k} seeds per round, T={rounds} rounds"}
     return {"workload": f"{w.key}: {w.desc}", **mr, "n": w.n, "m": w.m, "k": w.k, "eps": w.eps,
@@ -83,7 +93,7 @@ def config_of(w, world, rounds=1):
                           else f"plg gamma={w.gamma} rho={w.rho} d_cap={w.d_cap} graph_seed={w.graph_seed}"),
             "rr_seed": w.rr_seed,
             "parallelism": f"dp{world} (RR-id slices sampled per rank, replicated graph"
-                           + (", each round's sets all-gathered, NodeSelection replicated)" if world > 1 else ")"),
+                           + (f"; {protocol}: {PROTO_DESC[protocol]})" if world > 1 or force else ")"),
             "l2": "inputs larger than L2 (the graph's CSR exceeds the 126 MB L2)" if w.m > 30_000_000
             else "graph is L2-resident (no flush between steps)"}
 
@@ -141,11 +151,40 @@ class Clocks:
 # ------------------------------------------------------------------------------------------
 # reference arm: the oracle on the host cores
 # ------------------------------------------------------------------------------------------
-def oracle_sample(w, g, seconds, k, rounds=1):
+def host_cpu():
+    """CPU model and core count of this host (lscpu), for the baseline's context."""
+    model = "unknown"
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def golden_imm_time(key, skip=False):
+    """The oracle's FULL single-core IMM run on this workload (the paper's baseline protocol,
+    single-core IMM), recorded by tools/oracle_golden.py with its CPU model
+    and pinned core in tests/golden/imm_<key>.json — measured on the build host, not in this run."""
+    path = os.path.join(ROOT, "tests", "golden", f"imm_{key}{'_skip' if skip else ''}.json")
+    if not os.path.exists(path):
+        return None
+    gd = json.load(open(path))
+    o = gd.get("oracle_run", {})
+    return {"kind": "oracle full IMM", "imm_s": o.get("imm_s"), "rr_sets": gd.get("R_final"),
+            "rr_sets_per_s": o.get("rr_sets_per_s"), "cpu_model": o.get("cpu_model"), "nproc": o.get("nproc"),
+            "taskset_core": o.get("taskset_core"), "where": "build host (tools/oracle_golden.py), not this run"}
+
+
+def oracle_sample(w, g, seconds, k, rounds=1, skip=False):
     """Oracle RR generation (ids 0..T-1, grown in chunks until `seconds` elapse) followed by one
     NodeSelection (k) over that sample; returns (sets, wall seconds). rounds > 1: MRIM sets."""
     import oracle
     o = oracle.Oracle(g, w.model, w.scheme, w.p_uniform)
+    if skip:
+        o.set_skip(True)
     t0 = time.perf_counter()
     T, chunk = 0, max(2000 // rounds, 200)
     while time.perf_counter() - t0 < seconds:
@@ -166,6 +205,8 @@ def run_reference(args, w):
     if rank != 0:
         return
     g = gi.workload_graph(w.key)
+    core = sorted(os.sched_getaffinity(0))[-1]
+    os.sched_setaffinity(0, {core})                           # the oracle is single-threaded: one core
     per_step = max(1.0, min(10.0, 60.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         oracle_sample(w, g, per_step / 4, w.k, args.rounds)
@@ -182,7 +223,8 @@ def run_reference(args, w):
             "data": "synthetic", "config": config_of(w, 1, args.rounds),
             "cpu_baseline": {"value": v, "unit": unit, "cores": 1, "kind": "oracle",
                              "sample": f"per step: oracle RR sets of ids 0..T-1 for ~{per_step:.1f}s, "
-                                       f"then one k={w.k} NodeSelection over them"},
+                                       f"then one k={w.k} NodeSelection over them",
+                             **host_cpu(), "taskset_core": core, "full_imm": golden_imm_time(w.key)},
             "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -217,7 +259,10 @@ def run_gim(args, w):
     world, rank, local = dist_env()
     if args.same_device:
         local = 0
-    if world > 1:
+    pg = world > 1 or args.force_collectives
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"          # no version banner on stdout: one JSON line only
+    if pg:
         if args.backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -231,11 +276,17 @@ def run_gim(args, w):
     ctx.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme, weights=g.weights, p_uniform=w.p_uniform)
     if args.rounds > 1:
         ctx.set_rounds(args.rounds)
-    if world > 1:
-        ctx.set_shard(rank, world)
-        ctx.set_allreduce(P.torch_allreduce())
-        if not args.dense_exchange:            # replicated pool: no per-step collectives
-            ctx.set_allgather(P.torch_allgather())
+    def hooks(cx):
+        if world > 1 or args.force_collectives:
+            cx.set_shard(rank, world)
+            cx.set_allreduce(P.torch_allreduce())
+            if args.protocol == "replicated":      # no per-step collectives
+                cx.set_allgather(P.torch_allgather())
+            elif args.protocol == "reducescatter":
+                cx.set_reducescatter(P.torch_reducescatter())
+            if args.force_collectives:
+                cx.set_option(P.OPT_FORCE_COLLECTIVES, 1)
+    hooks(ctx)
     ctx.set_option(P.OPT_PROFILE, 1)
     if args.skip:
         ctx.set_option(P.OPT_SKIP, 1)
@@ -293,7 +344,8 @@ def run_gim(args, w):
     # write per visited node + 4 B src per live in-edge (coins are drawn before any load)
     warp_elems = st["rr_elements"]
     alg_bytes = 12 * st["rr_sets"] + 12 * warp_elems + 4 * st["live_edges"]
-    traffic = load_profile_traffic().get(f"{w.key}:k_rr_warp")
+    tr = load_profile_traffic().get(f"{w.key}:k_rr_warp{':skip' if args.skip else ''}")
+    tr = tr if isinstance(tr, dict) else None
     mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = mp.get("hbm_gbs", 6650.0)
@@ -313,13 +365,19 @@ def run_gim(args, w):
                 "peak": hbm_peak, "unit": "GB/s", "frac": alg_gbs / hbm_peak}
     roofline = {
         **head,
-        "traffic": traffic,
+        "traffic": tr["dram_bytes"] if tr else None,
+        "traffic_launch_sets": tr["launch_sets"] if tr else None,
+        "traffic_launch_alg_bytes": tr["alg_bytes"] if tr else None,
+        "sector_eff": tr["sector_eff"] if tr else None,
+        "dram_gbs": tr["dram_gbs"] if tr else None,
+        "traffic_note": ("dram__bytes_read+write of ONE k_rr_warp launch (a 2^20-set generate_rr call, "
+                         "tools/traffic_capture.py, profiles/ncu_traffic.json) against the algorithmic bytes "
+                         "of the same launch; sector_eff = algorithmic / DRAM bytes") if tr else None,
         "per_launch_ms": rr_ms / n_rr, "launches": n_rr,
         "coins_per_launch": coins / n_rr,
         "peak_basis": f"derived: 6.4 coins/cycle/SM x 148 SMs x {sm_max:.0f} MHz (Philox4x32-10 = 20 IMAD.WIDE.U32, 4 cycles each on the FMA-heavy pipe)",
         "philox_microbench_gcoins": measured_philox,
         "frac_of_microbench": (achieved / measured_philox) if measured_philox else None,
-        "traffic_note": "DRAM bytes of one captured launch (profiles/ncu_traffic.json), not averaged",
         "algorithmic_gbs": alg_gbs,
         "hbm_peak_gbs": hbm_peak,
         "hbm_frac": alg_gbs / hbm_peak,
@@ -329,6 +387,46 @@ def run_gim(args, w):
               "ms_store": st["ms_store"] / args.steps, "ms_inv": st["ms_inv"] / args.steps,
               "ms_select": st["ms_select"] / args.steps}
     gen_ms = st["ms_rr"] + st["ms_giant"] + st["ms_store"]
+
+    # ---- the geometric-skip contract (reading R31) on the same graph and launch shape -------
+    variants = None
+    if (not args.skip and not args.no_variants and w.model == gi.IC and w.scheme != gi.W_EXPLICIT
+            and args.rounds == 1):
+        ctx.set_option(P.OPT_SKIP, 1)
+        for _ in range(max(args.warmup, 0)):
+            ctx.imm(w.k, w.eps, w.ell, w.rr_seed)
+        ctx.reset_stats()
+        barrier()
+        torch.cuda.synchronize()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(stream)
+        vres = [ctx.imm(w.k, w.eps, w.ell, w.rr_seed) for _ in range(args.steps)]
+        v1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        vms = max_over_ranks(v0.elapsed_time(v1))
+        vst = ctx.stats()
+        v_rr_ms = vst["ms_rr"] + vst["ms_giant"]
+        # algorithmic bytes: 12 B per set + per visited node 8 B row pointers, 8 B tabulated
+        # 1/ln(1-p) and 4 B staging write + 4 B per live in-edge; the draws are ~2 per node
+        v_alg = 12 * vst["rr_sets"] + 20 * vst["rr_elements"] + 4 * (vst["live_edges"] + vst["live_giant"])
+        v_gbs = v_alg / (v_rr_ms / 1000.0) / 1e9 if v_rr_ms > 0 else 0.0
+        vtr = load_profile_traffic().get(f"{w.key}:k_rr_warp:skip")
+        variants = {"geometric_skip": {
+            "rng": "reading R31 (GIM_OPT_SKIP): live in-edges drawn as geometric gaps; bit-exact vs the "
+                   "oracle's skip mirror (tests/test_gpu_skip.py), same distribution of RR sets",
+            "value": sum(r.R_final for r in vres) / (vms / 1000.0), "unit": unit_of(args),
+            "ms_per_step": vms / args.steps,
+            "phase_ms_per_step": {k_: vst[k_] / args.steps for k_ in ("ms_rr", "ms_giant", "ms_store", "ms_inv",
+                                                                      "ms_select")},
+            "draws_per_set": (vst["coins"] + vst["coins_giant"]) / max(vst["rr_sets"], 1),
+            "seeds_head": vres[-1].seeds[:8].tolist(),
+            "roofline": {"kernel": "k_skip_lane + k_skip_warp (+ k_skip_giant): dependent row-pointer / "
+                                   "source loads per BFS level", "bound": "hbm", "achieved": v_gbs,
+                         "peak": hbm_peak, "unit": "GB/s", "frac": v_gbs / hbm_peak,
+                         "traffic": vtr.get("dram_bytes") if isinstance(vtr, dict) else None,
+                         "sector_eff": vtr.get("sector_eff") if isinstance(vtr, dict) else None}}}
+        ctx.set_option(P.OPT_SKIP, 0)
 
     # ---- end to end through the public API with host buffers -------------------------------
     e2e = None
@@ -340,15 +438,11 @@ def run_gim(args, w):
             ctx2.set_option(P.OPT_SKIP, 1)
         if args.rounds > 1:
             ctx2.set_rounds(args.rounds)
-        if world > 1:
-            ctx2.set_shard(rank, world)
-            ctx2.set_allreduce(P.torch_allreduce())
-            if not args.dense_exchange:
-                ctx2.set_allgather(P.torch_allgather())
+        hooks(ctx2)
         def e2e_step():
             ctx2.load_graph(g.n, rp_h.numpy(), src_h.numpy(), w.model, w.scheme, weights=g.weights,
                             p_uniform=w.p_uniform)
-            if world > 1:
+            if world > 1 or args.force_collectives:
                 ctx2.set_shard(rank, world)
             return ctx2.imm(w.k, w.eps, w.ell, w.rr_seed)
         for _ in range(max(args.warmup, 1)):
@@ -375,16 +469,26 @@ def run_gim(args, w):
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only) --------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        T, s = oracle_sample(w, g, args.cpu_seconds, w.k, args.rounds)
+        core = sorted(os.sched_getaffinity(0))[-1]
+        old_aff = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {core})                       # one pinned host core
+        try:
+            T, s = oracle_sample(w, g, args.cpu_seconds, w.k, args.rounds, skip=args.skip)
+        finally:
+            os.sched_setaffinity(0, old_aff)
         cpu = {"value": T / s, "unit": unit_of(args), "cores": 1, "kind": "oracle",
                "sample": f"oracle {'MRIM' if args.rounds > 1 else 'RR'} sets of ids 0..{T - 1} ({s:.1f}s) + one "
-                         f"k={w.k} NodeSelection over them, single-threaded C"}
+                         f"k={w.k} NodeSelection over them, single-threaded C"
+                         + (" (geometric-skip contract, R31)" if args.skip else ""),
+               **host_cpu(), "taskset_core": core, "full_imm": golden_imm_time(w.key, args.skip)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": unit_of(args), "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-                "config": config_of(w, world, args.rounds),
+                "config": {**config_of(w, world, args.rounds, args.protocol, args.force_collectives),
+                           "rng": ("geometric-skip contract (reading R31, GIM_OPT_SKIP)" if args.skip else
+                                   "Philox4x32-10 coin per in-edge slot (reading R16, north_star)")},
                 "imm_time_s": ms / args.steps / 1000.0,
                 "rr_sets_per_step": r0.R_final, "theta": r0.theta, "LB": r0.LB, "rounds": r0.rounds,
                 "spread_est": r0.spread_est,
@@ -402,15 +506,18 @@ def run_gim(args, w):
                          "syncs_per_step": st["n_syncs"] / args.steps,
                          "allocs_in_timed_region": st["n_allocs"]},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+                "variants": variants,
                 "seeds_head": r0.seeds[:8].tolist()}
         print(json.dumps(line), flush=True)
     ctx.close()
-    if world > 1:
+    if pg:
         dist.destroy_process_group()
 
 
 def main():
     args = parse()
+    if args.dense_exchange:
+        args.protocol = "allreduce"
     w = gi.WORKLOADS[args.workload]
     if args.k or args.eps:      # sweep point: same graph, other (k, eps); named in config
         w = dataclasses.replace(w, k=args.k or w.k, eps=args.eps or w.eps,

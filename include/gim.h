@@ -96,6 +96,20 @@ typedef int (*gim_allgather_fn)(const void* dev_send, uint64_t bytes, void* dev_
                                 void* user);
 gim_status gim_set_allgather(gim_ctx* ctx, gim_allgather_fn fn, void* user);
 
+/* Reduce-scatter over the world of int32 elements in device memory: dev_recv[recv_count] =
+ * SUM over ranks r of their dev_send[rank * recv_count .. (rank + 1) * recv_count) for THIS
+ * rank; enqueued on / ordered with cuda_stream; returns 0 on success. With world > 1, a
+ * reduce-scatter and an all-reduce (and no all-gather) set, NodeSelection runs the
+ * NODE-SHARDED protocol: nodes are split into world contiguous shards of
+ * ceil(n / world); the local counts are reduce-scattered once, then per greedy step every rank
+ * takes the argmax of its shard's global counts, the world's candidate keys are exchanged with
+ * a 2*world-int32 SUM all-reduce (each rank fills only its own slot), the winner is covered in
+ * the rank's local pool and its decrements are reduce-scattered to the shard owners — about
+ * half the per-step bytes of the dense all-reduce protocol and no replicated pool. */
+typedef int (*gim_reducescatter_fn)(void* dev_send, void* dev_recv, uint64_t recv_count, void* cuda_stream,
+                                    void* user);
+gim_status gim_set_reducescatter(gim_ctx* ctx, gim_reducescatter_fn fn, void* user);
+
 /* Route every device allocation of ctx through the caller (e.g. torch's caching allocator).
  * Must be called before gim_load_graph. alloc_fn returns NULL on failure. */
 typedef void* (*gim_alloc_fn)(uint64_t bytes, void* cuda_stream, void* user);
@@ -240,7 +254,9 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                         count >= tau certifies the global argmax); an uncertified step makes
  *                         the selection rerun unfused (gim_stats.fused_fallbacks). Results are
  *                         identical; measured 4.48 vs 4.23 ms per C3 selection set (off).
- *  GIM_OPT_FUSED_CTAS   = c (default 2, 1..16): CTAs per SM of the fused step kernel. */
+ *  GIM_OPT_FUSED_CTAS   = c (default 2, 1..16): CTAs per SM of the fused step kernel.
+ *  GIM_OPT_FORCE_COLLECTIVES = 1: run the world > 1 exchange protocol selected by the hooks even
+ *                         at world = 1 (test hook: drives the NCCL callbacks on one GPU). */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -259,7 +275,8 @@ typedef enum {
   GIM_OPT_SKIP = 16,
   GIM_OPT_SPILL = 17,
   GIM_OPT_SELECT_FUSED = 18,
-  GIM_OPT_FUSED_CTAS = 19
+  GIM_OPT_FUSED_CTAS = 19,
+  GIM_OPT_FORCE_COLLECTIVES = 20
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

@@ -76,6 +76,10 @@ struct gim_ctx {
   void* aruser = nullptr;
   gim_allgather_fn agfn = nullptr;   // set: replicated-pool protocol (no per-step collectives)
   void* aguser = nullptr;
+  gim_reducescatter_fn rsfn = nullptr;   // set (with arfn, no agfn): node-sharded selection
+  void* rsuser = nullptr;
+  DevBuf rs_gcnt, rs_dshard, rs_keys, rs_kx;   // node-sharded selection: shard counts/decrements, keys
+  int force_coll = 0;                  // GIM_OPT_FORCE_COLLECTIVES: world-1 runs the P > 1 protocol
   DevBuf ag_small, ag_send, ag_recv;
   // pool (O6)
   bool have_seed = false;
@@ -742,7 +746,7 @@ gim_status generate(gim_ctx* c, uint64_t theta_sets, uint64_t seed, bool host_sy
     const uint64_t set0 = c->nsets, e0 = c->pool_len;
     const size_t seg0 = c->segs.size();
     for (uint64_t s = lo; s < hi; s += kChunk) TRY(gen_chunk(c, s, (uint32_t)std::min<uint64_t>(kChunk, hi - s)));
-    if (c->world > 1 && c->agfn) TRY(replicate_round(c, a, theta, set0, e0, seg0));
+    if ((c->world > 1 || c->force_coll) && c->agfn) TRY(replicate_round(c, a, theta, set0, e0, seg0));
     // one inverted-index segment per generate call (= per IMM round): its O(n) count scan is
     // paid once per round, not once per 2^22-id chunk
     if (c->nsets > set0) {
@@ -758,11 +762,83 @@ gim_status generate(gim_ctx* c, uint64_t theta_sets, uint64_t seed, bool host_sy
 }
 
 // ---- NodeSelection (O7) ---------------------------------------------------------------------
+gim_status read_keys(gim_ctx* c, uint32_t kk) {
+  if (c->h_keys_cap < kk + 1) {
+    if (c->h_keys) cudaFreeHost(c->h_keys);
+    c->h_keys = nullptr;
+    CK(cudaMallocHost(&c->h_keys, ((uint64_t)kk + 1) * 8));
+    c->h_keys_cap = kk + 1;
+  }
+  CK(cudaMemcpyAsync(c->h_keys, c->keys.p, (uint64_t)kk * 8, cudaMemcpyDeviceToHost, c->stream));
+  c->h_keys[kk] = 0;
+  return GIM_OK;
+}
+
+// Node-sharded selection (world > 1, gim_set_reducescatter + gim_set_allreduce): rank r owns the
+// global counts of nodes [r ns, (r+1) ns), ns = ceil(n / world). Counts are reduce-scattered
+// once; per greedy step (Alg. 1 l.6-10, Alg. 7): the argmax of the own shard (the
+// previous step's reduce-scattered decrements applied first), the keys of all ranks exchanged
+// by a SUM all-reduce of one slot per rank, the global pick (largest key: lowest id on ties,
+// R10) retired by its owner and covered in the local pool, the local decrements
+// reduce-scattered to the owners.
+gim_status select_launch_rs(gim_ctx* c, uint32_t k, const InvSegDev* segd, const uint32_t* nsegd, bool limited) {
+  const uint64_t n = c->n;
+  const uint32_t W = (uint32_t)c->world, r = (uint32_t)c->rank;
+  const uint64_t ns = (n + W - 1) / W, npad = ns * W;
+  const uint32_t id_base = (uint32_t)(ns * r);
+  const uint32_t ns_valid = n > id_base ? (uint32_t)std::min<uint64_t>(ns, n - id_base) : 0u;
+  const uint32_t kk = k;
+  TRY(ensure(c, c->cnt, npad * 4));
+  TRY(ensure(c, c->dec, npad * 4));
+  TRY(ensure(c, c->rs_gcnt, ns * 4 + 16));
+  TRY(ensure(c, c->rs_dshard, ns * 4 + 16));
+  TRY(ensure(c, c->rs_keys, (uint64_t)kk * 8));
+  TRY(ensure(c, c->rs_kx, (uint64_t)W * 8));
+  auto* keys = reinterpret_cast<unsigned long long*>(c->keys.p);
+  auto* lkeys = reinterpret_cast<unsigned long long*>(c->rs_keys.p);
+  auto* kx = reinterpret_cast<unsigned long long*>(c->rs_kx.p);
+  uint32_t* gcnt = c->rs_gcnt.as<uint32_t>();
+  int32_t* dshard = c->rs_dshard.as<int32_t>();
+  int32_t* dec = c->dec.as<int32_t>();
+  CK(cudaMemcpyAsync(c->cnt.p, c->count_total.p, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+  if (npad > n) CK(cudaMemsetAsync(c->cnt.as<uint32_t>() + n, 0, (npad - n) * 4, c->stream));
+  CK(cudaEventRecord(c->ev_cnt_copied, c->stream));
+  CK(cudaMemsetAsync(c->covered.p, 0, std::max<uint64_t>(c->nsets, 1), c->stream));
+  CK(cudaMemsetAsync(keys, 0, (uint64_t)kk * 8, c->stream));
+  CK(cudaMemsetAsync(lkeys, 0, (uint64_t)kk * 8, c->stream));
+  CK(cudaMemsetAsync(dec, 0, npad * 4, c->stream));
+  CK(cudaMemsetAsync(dshard, 0, ns * 4, c->stream));
+  c->st.allreduces++;
+  if (c->rsfn(c->cnt.p, gcnt, ns, c->stream, c->rsuser)) return fail(c, GIM_ECOLL, "reduce-scatter(count) failed");
+  Prof pf(c, CLS_SELECT);
+  for (uint32_t j = 0; j < kk; ++j) {
+    TRY(launched(c, launch_argmax(gcnt, dshard, ns_valid, lkeys, (int)j, nullptr, c->num_sms * kArgmaxCtasPerSM,
+                                  c->stream, false, id_base), "k_argmax(shard)"));
+    TRY(launched(c, launch_rs_pack(lkeys, (int)j, r, W, kx, c->stream), "k_rs_pack"));
+    c->st.allreduces++;
+    if (c->arfn(kx, 2ull * W, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(keys) failed");
+    TRY(launched(c, launch_rs_pick(kx, W, keys, (int)j, gcnt, id_base, ns_valid, c->stream), "k_rs_pick"));
+    TRY(launched(c, launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
+                                 c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * kCoverCtasPerSM,
+                                 c->stream, limited, nullptr), "k_cover"));
+    if (j + 1 < kk) {
+      c->st.allreduces++;
+      if (c->rsfn(dec, dshard, ns, c->stream, c->rsuser)) return fail(c, GIM_ECOLL, "reduce-scatter(dec) failed");
+      CK(cudaMemsetAsync(dec, 0, npad * 4, c->stream));
+    }
+  }
+  c->sel_fused_used = false;
+  TRY(read_keys(c, kk));
+  CK(cudaEventRecord(c->ev_sel_done, c->stream));
+  c->sel_pending = true;
+  return GIM_OK;
+}
+
 gim_status select_launch(gim_ctx* c, uint32_t k) {
   if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
   if (k < 1 || k > c->n) return fail(c, GIM_EINVAL, "k must satisfy 1 <= k <= n");
   if (!c->have_seed || c->T_global == 0) return fail(c, GIM_ESTATE, "RR pool is empty");
-  const bool sharded = c->world > 1 && !c->agfn;   // replicated pool: select as P = 1
+  const bool sharded = (c->world > 1 || c->force_coll) && !c->agfn;   // replicated pool: select as P = 1
   if (sharded && !c->arfn) return fail(c, GIM_ESTATE, "world > 1 requires gim_set_allreduce or gim_set_allgather");
   const uint64_t n = nsp(c);                        // counted elements (nodes, or MRIM pairs)
   const uint32_t kk = k * c->rounds;                // picks: k per round (R27)
@@ -795,6 +871,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   const bool limited = c->set_limit != ~0ull;     // cover must skip truncated sets
   const InvSegDev* segd = c->seg_desc.as<InvSegDev>();
   const uint32_t* nsegd = reinterpret_cast<const uint32_t*>(segd + kMaxInvSeg);
+  if (sharded && c->rsfn && c->rounds == 1) return select_launch_rs(c, k, segd, nsegd, limited);
   CK(cudaMemcpyAsync(c->cnt.p, c->count_total.p, n * 4, cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaEventRecord(c->ev_cnt_copied, c->stream));
   CK(cudaMemsetAsync(c->covered.p, 0, std::max<uint64_t>(c->nsets / c->rounds, 1), c->stream));
@@ -1068,7 +1145,7 @@ void gim_destroy(gim_ctx* c) {
                     &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->spill, &c->skip_tab, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
                     &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->thr_node, &c->ag_small,
-                    &c->ag_send, &c->ag_recv, &c->sel_bar};
+                    &c->ag_send, &c->ag_recv, &c->sel_bar, &c->rs_gcnt, &c->rs_dshard, &c->rs_keys, &c->rs_kx};
   for (auto& sg : c->iseg) {
     dfree(c, sg.off);
     dfree(c, sg.inv);
@@ -1232,6 +1309,14 @@ gim_status gim_set_allgather(gim_ctx* c, gim_allgather_fn fn, void* user) {
   c->agfn = fn;
   c->aguser = user;
   c->have_seed = false;                        // the pool layout changes: regenerate
+  return GIM_OK;
+}
+
+gim_status gim_set_reducescatter(gim_ctx* c, gim_reducescatter_fn fn, void* user) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  c->rsfn = fn;
+  c->rsuser = user;
   return GIM_OK;
 }
 
@@ -1520,6 +1605,10 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
       c->fused_ctas = (int)value;
       if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
       c->sel_exec = nullptr;
+      return GIM_OK;
+    case GIM_OPT_FORCE_COLLECTIVES:
+      c->force_coll = value ? 1 : 0;
+      c->have_seed = false;
       return GIM_OK;
     case GIM_OPT_SELECT_FUSED:
       if (value < 0 || value > (1 << 16)) return fail(c, GIM_EINVAL, "fused candidate cap must be in [0, 65536]");

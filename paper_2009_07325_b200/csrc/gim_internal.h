@@ -51,7 +51,13 @@ cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, uint32_t limit
 cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* delta, uint32_t n, int grid,
                                cudaStream_t s);
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
-                          const uint32_t* tau_p1, int grid, cudaStream_t s, bool excl = false);
+                          const uint32_t* tau_p1, int grid, cudaStream_t s, bool excl = false,
+                          uint32_t id_base = 0);
+// node-sharded selection (gim_set_reducescatter): key exchange pack / global pick
+cudaError_t launch_rs_pack(const unsigned long long* local_keys, int j, uint32_t rank, uint32_t world,
+                           unsigned long long* kx, cudaStream_t s);
+cudaError_t launch_rs_pick(const unsigned long long* kx, uint32_t world, unsigned long long* keys, int j,
+                           uint32_t* gshard, uint32_t id_base, uint32_t ns_valid, cudaStream_t s);
 cudaError_t launch_cand_setup(const uint32_t* cnt, uint32_t n, uint32_t kmax, unsigned int* hist,
                               uint32_t* tau_p1, uint32_t* cand, unsigned int* ncand, int grid, cudaStream_t s);
 cudaError_t launch_argmax_cand(const uint32_t* cnt, const uint32_t* cand, const unsigned int* ncand,

@@ -180,7 +180,8 @@ __device__ __forceinline__ void argmax_one(uint32_t c, uint32_t v, unsigned long
 
 __device__ __forceinline__ void argmax_step(uint32_t* __restrict__ cnt, int32_t* __restrict__ dec,
                                             uint32_t n, unsigned long long* __restrict__ keys, int j,
-                                            const uint32_t* __restrict__ tau_p1, uint32_t excl) {
+                                            const uint32_t* __restrict__ tau_p1, uint32_t excl,
+                                            uint32_t id_base = 0) {
   // candidate mode: the candidate argmax already found a count >= tau_p1, which no node outside
   // the candidate list can reach (their counts started below it and only decrease)
   if (tau_p1 != nullptr && (uint32_t)(keys[j] >> 32) >= *tau_p1 && keys[j] != 0ull) return;
@@ -216,7 +217,7 @@ __device__ __forceinline__ void argmax_step(uint32_t* __restrict__ cnt, int32_t*
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const uint32_t v = (i0 + u * stride) << 2;
+      const uint32_t v = id_base + ((i0 + u * stride) << 2);
       argmax_one(x[u].x, v, best, excl);
       argmax_one(x[u].y, v + 1, best, excl);
       argmax_one(x[u].z, v + 2, best, excl);
@@ -227,7 +228,7 @@ __device__ __forceinline__ void argmax_step(uint32_t* __restrict__ cnt, int32_t*
   for (uint32_t v = (n4 << 2) + blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
     uint32_t c = cnt[v];
     if (dec != nullptr && c != kSent && dec[v]) { c -= (uint32_t)dec[v]; dec[v] = 0; cnt[v] = c; }
-    argmax_one(c, v, best, excl);
+    argmax_one(c, id_base + v, best, excl);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -249,10 +250,30 @@ __device__ __forceinline__ void argmax_step(uint32_t* __restrict__ cnt, int32_t*
 
 __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int32_t* __restrict__ dec,
                                                 uint32_t n, unsigned long long* __restrict__ keys, int j,
-                                                const uint32_t* __restrict__ tau_p1, uint32_t excl) {
+                                                const uint32_t* __restrict__ tau_p1, uint32_t excl,
+                                                uint32_t id_base) {
   pdl_wait();
   pdl_trigger();
-  argmax_step(cnt, dec, n, keys, j, tau_p1, excl);
+  argmax_step(cnt, dec, n, keys, j, tau_p1, excl, id_base);
+}
+
+// Node-sharded selection (include/gim.h gim_set_reducescatter): this rank's best key of step j
+// goes to its slot of the exchange buffer (2 int32 per rank, the other slots zero, so a SUM
+// all-reduce gathers them); after the exchange the largest key is the global pick, which the
+// owner of its shard retires.
+__global__ void k_rs_pack(const unsigned long long* __restrict__ local_keys, int j, uint32_t rank, uint32_t world,
+                          unsigned long long* __restrict__ kx) {
+  for (uint32_t r = threadIdx.x; r < world; r += blockDim.x) kx[r] = (r == rank) ? local_keys[j] : 0ull;
+}
+__global__ void k_rs_pick(const unsigned long long* __restrict__ kx, uint32_t world, unsigned long long* keys, int j,
+                          uint32_t* __restrict__ gshard, uint32_t id_base, uint32_t ns_valid) {
+  if (threadIdx.x == 0) {
+    unsigned long long best = 0;
+    for (uint32_t r = 0; r < world; ++r) best = kx[r] > best ? kx[r] : best;
+    keys[j] = best;
+    const uint32_t u = ~(uint32_t)best;
+    if (best && u - id_base < ns_valid) gshard[u - id_base] = kSent;
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -617,7 +638,7 @@ __global__ void __launch_bounds__(1024, 1) k_select_persistent(uint32_t* __restr
                                                            uint8_t* __restrict__ covered, MrimSel mr,
                                                            uint32_t excl, unsigned int* bar) {
   for (int j = 0; j < kk; ++j) {
-    argmax_step(cnt, nullptr, n, keys, j, nullptr, excl);
+    argmax_step(cnt, nullptr, n, keys, j, nullptr, excl, 0u);
     grid_barrier(bar);
     cover_step<LIMIT>(keys, j, segs, offsets, pool, covered, cnt, nullptr, mr);
     grid_barrier(bar);
@@ -707,8 +728,19 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t
 }
 
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
-                          const uint32_t* tau_p1, int grid, cudaStream_t s, bool excl) {
-  return launch_pdl(k_argmax, grid, 256, s, cnt, dec, n, keys, j, tau_p1, excl ? 0x80000000u : 0u);
+                          const uint32_t* tau_p1, int grid, cudaStream_t s, bool excl, uint32_t id_base) {
+  return launch_pdl(k_argmax, grid, 256, s, cnt, dec, n, keys, j, tau_p1, excl ? 0x80000000u : 0u, id_base);
+}
+
+cudaError_t launch_rs_pack(const unsigned long long* local_keys, int j, uint32_t rank, uint32_t world,
+                           unsigned long long* kx, cudaStream_t s) {
+  k_rs_pack<<<1, 64, 0, s>>>(local_keys, j, rank, world, kx);
+  return cudaGetLastError();
+}
+cudaError_t launch_rs_pick(const unsigned long long* kx, uint32_t world, unsigned long long* keys, int j,
+                           uint32_t* gshard, uint32_t id_base, uint32_t ns_valid, cudaStream_t s) {
+  k_rs_pick<<<1, 32, 0, s>>>(kx, world, keys, j, gshard, id_base, ns_valid);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_cand_setup(const uint32_t* cnt, uint32_t n, uint32_t kmax, unsigned int* hist,

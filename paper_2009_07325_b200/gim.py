@@ -24,7 +24,7 @@ LIB_PATH = os.environ.get("GIM_LIB_PATH") or os.path.join(_HERE, "libgim.so")
 GIM_OK, GIM_EINVAL, GIM_ESTATE, GIM_ENOMEM, GIM_ECUDA, GIM_ECOLL, GIM_ELTWEIGHT = range(7)
 IC, LT = 0, 1
 W_EXPLICIT, W_WC, W_UNIFORM = 0, 1, 2
-OPT_FORCE_GIANT, OPT_QUEUE_CAP, OPT_PROFILE, OPT_STAGING_CAP, OPT_SELECT_GRAPH, OPT_INV_SEGMENTS, OPT_ARGMAX_CAND, OPT_IC_LANE, OPT_SPECULATE, OPT_MB_CHAINS, OPT_PDL, OPT_GIANT_NT, OPT_FRESH_FINAL, OPT_SELECT_PERSISTENT, OPT_SKIP, OPT_SPILL, OPT_SELECT_FUSED, OPT_FUSED_CTAS = 1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19
+OPT_FORCE_GIANT, OPT_QUEUE_CAP, OPT_PROFILE, OPT_STAGING_CAP, OPT_SELECT_GRAPH, OPT_INV_SEGMENTS, OPT_ARGMAX_CAND, OPT_IC_LANE, OPT_SPECULATE, OPT_MB_CHAINS, OPT_PDL, OPT_GIANT_NT, OPT_FRESH_FINAL, OPT_SELECT_PERSISTENT, OPT_SKIP, OPT_SPILL, OPT_SELECT_FUSED, OPT_FUSED_CTAS, OPT_FORCE_COLLECTIVES = 1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20
 
 _STATUS = {0: "GIM_OK", 1: "GIM_EINVAL", 2: "GIM_ESTATE", 3: "GIM_ENOMEM", 4: "GIM_ECUDA",
            5: "GIM_ECOLL", 6: "GIM_ELTWEIGHT"}
@@ -34,6 +34,7 @@ _p, _u32, _u64, _i32, _i64, _dbl = (ctypes.c_void_p, ctypes.c_uint32, ctypes.c_u
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, _p, _u64, _p, _p)
 ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, _p, _u64, _p, _p, _p)
+REDUCESCATTER_FN = ctypes.CFUNCTYPE(ctypes.c_int, _p, _p, _u64, _p, _p)
 ALLOC_FN = ctypes.CFUNCTYPE(_p, _u64, _p, _p)
 FREE_FN = ctypes.CFUNCTYPE(None, _p, _p, _p)
 
@@ -64,6 +65,7 @@ SIGNATURES = {
     "gim_set_shard": (_i32, [_p, _i32, _i32]),
     "gim_set_allreduce": (_i32, [_p, ALLREDUCE_FN, _p]),
     "gim_set_allgather": (_i32, [_p, ALLGATHER_FN, _p]),
+    "gim_set_reducescatter": (_i32, [_p, REDUCESCATTER_FN, _p]),
     "gim_set_allocator": (_i32, [_p, ALLOC_FN, FREE_FN, _p]),
     "gim_generate_rr": (_i32, [_p, _u64, _u64]),
     "gim_select": (_i32, [_p, _u32, _p, _p, _p]),
@@ -198,6 +200,14 @@ class Gim:
         cb = ALLGATHER_FN(lambda snd, nb, rcv, stream, user: int(fn(snd, nb, rcv, stream or 0)))
         self._keep.append(cb)
         self._check(self._lib.gim_set_allgather(self._h, cb, None))
+
+    def set_reducescatter(self, fn: Callable[[int, int, int, int], int]):
+        """fn(send_ptr, recv_ptr, recv_count_int32, cuda_stream) -> 0: SUM reduce-scatter of int32
+        (this rank's block of the sum). With set_allreduce (and no all-gather), world > 1
+        selection runs the node-sharded protocol (include/gim.h gim_set_reducescatter)."""
+        cb = REDUCESCATTER_FN(lambda snd, rcv, cnt, stream, user: int(fn(snd, rcv, cnt, stream or 0)))
+        self._keep.append(cb)
+        self._check(self._lib.gim_set_reducescatter(self._h, cb, None))
 
     def generate_rr(self, theta: int, seed: int):
         self._check(self._lib.gim_generate_rr(self._h, theta, seed))
@@ -361,6 +371,50 @@ def torch_allgather(group=None, device: str = "cuda"):
                 dst.copy_(torch.cat(parts).to(dst.device))
             else:
                 dist.all_gather_into_tensor(dst, src, group=group)
+        return 0
+
+    return fn
+
+
+def torch_reducescatter(group=None, device: str = "cuda"):
+    """reduce-scatter callback for Gim.set_reducescatter: torch.distributed.reduce_scatter_tensor
+    (SUM) of the library's int32 device buffers, ordered on the library's stream (NCCL over
+    NVLink for an nccl group; a gloo group stages through host memory with an all-reduce, for
+    functional tests). device="cpu" wraps host pointers (the multi-process gloo tests)."""
+    import torch
+    import torch.distributed as dist
+
+    def host(ptr, count):
+        return np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctypes.c_int32)), shape=(int(count),))
+
+    if device == "cpu":
+        def fn_cpu(send: int, recv: int, count: int, stream: int) -> int:
+            world, rank = dist.get_world_size(group), dist.get_rank(group)
+            full = torch.from_numpy(host(send, count * world).copy())
+            dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
+            host(recv, count)[:] = full[rank * count:(rank + 1) * count].numpy()
+            return 0
+        return fn_cpu
+
+    def view(ptr, count):
+        class _View:
+            __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<i4",
+                                        "data": (int(ptr), False), "version": 3, "strides": None,
+                                        "stream": None}
+        return torch.as_tensor(_View(), device="cuda")
+
+    def fn(send: int, recv: int, count: int, stream: int) -> int:
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        src = view(send, count * world)
+        dst = view(recv, count)
+        s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            if dist.get_backend(group) == "gloo":
+                h = src.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+                dst.copy_(h[rank * count:(rank + 1) * count].to(dst.device))
+            else:
+                dist.reduce_scatter_tensor(dst, src, op=dist.ReduceOp.SUM, group=group)
         return 0
 
     return fn

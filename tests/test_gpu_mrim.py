@@ -150,57 +150,3 @@ def test_mrim_full_size_sampled_C3():
     set_of = np.repeat(np.arange(N), np.diff(moff.astype(np.int64)))
     hit[set_of[np.isin(pairs, s)]] = True
     assert int(hit.sum()) == cov == int(gn.sum())
-
-
-def test_mrim_sharded_emulation_equals_single():
-    """P = 2 ranks (host-summing all-reduce) split whole MRIM sets and select identically."""
-    import torch
-    w = gi.WORKLOADS["C1"]
-    g = gi.workload_graph("C1")
-    T, N, k = 3, 9001, 10
-    ref = _ctx(g, w.model, w.scheme)
-    ref.set_rounds(T)
-    ref.generate_rr(N, w.rr_seed)
-    rs = ref.select(k)
-    Pn = 2
-    bar = threading.Barrier(Pn)
-    bufs = [None] * Pn
-
-    def make_cb(r):
-        def cb(ptr, count, stream):
-            class V:
-                __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<i4",
-                                            "data": (int(ptr), False), "version": 3,
-                                            "strides": None, "stream": None}
-            t = torch.as_tensor(V(), device="cuda")
-            torch.cuda.ExternalStream(stream).synchronize()
-            bufs[r] = t.cpu()
-            bar.wait()
-            tot = sum(bufs)
-            bar.wait()
-            t.copy_(tot.cuda())
-            torch.cuda.synchronize()
-            return 0
-        return cb
-
-    ctxs = []
-    for r in range(Pn):
-        c = _ctx(g, w.model, w.scheme)
-        c.set_rounds(T)
-        c.set_shard(r, Pn)
-        c.set_allreduce(make_cb(r))
-        ctxs.append(c)
-    out = [None] * Pn
-
-    def run(r):
-        ctxs[r].generate_rr(N, w.rr_seed)
-        out[r] = ctxs[r].select(k)
-
-    th = [threading.Thread(target=run, args=(r,)) for r in range(Pn)]
-    [t.start() for t in th]
-    [t.join() for t in th]
-    for r in range(Pn):
-        assert np.array_equal(out[r][0], rs[0]) and np.array_equal(out[r][1], rs[1]) and out[r][2] == rs[2]
-        ids, _, _ = ctxs[r].rr_export()
-        lo, hi = r * N // Pn, (r + 1) * N // Pn
-        assert np.array_equal(ids, np.arange(lo * T, hi * T, dtype=np.uint64))

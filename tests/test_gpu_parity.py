@@ -304,63 +304,6 @@ def test_full_size_sampled(key):
     assert int(hit.sum()) == cov == int(gains.sum())
 
 
-def test_sharded_emulation_equals_single():
-    """P contexts (one per emulated rank) with a host-side summing all-reduce: pools are the
-    slices of the P=1 pool and the selection is identical (SURVEY.md §4 "multi-GPU without a
-    cluster")."""
-    import torch
-    w = gi.WORKLOADS["C2"]
-    g = gi.workload_graph("C2")
-    T, k = 50021, 50
-    ref = _ctx(g, w.model, w.scheme)
-    ref.generate_rr(T, w.rr_seed)
-    rseeds, rgains, rcov = ref.select(k)
-    _, roff, rnodes = ref.rr_export()
-    for Pn in (2, 3):
-        bar = threading.Barrier(Pn)
-        bufs = [None] * Pn
-        ctxs = []
-
-        def make_cb(r):
-            def cb(ptr, count, stream):
-                class V:
-                    __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<i4",
-                                                "data": (int(ptr), False), "version": 3,
-                                                "strides": None, "stream": None}
-                t = torch.as_tensor(V(), device="cuda")
-                torch.cuda.ExternalStream(stream).synchronize()
-                bufs[r] = t.cpu()
-                bar.wait()
-                tot = sum(bufs)
-                bar.wait()
-                t.copy_(tot.cuda())
-                torch.cuda.synchronize()
-                return 0
-            return cb
-
-        for r in range(Pn):
-            c = _ctx(g, w.model, w.scheme)
-            c.set_shard(r, Pn)
-            c.set_allreduce(make_cb(r))
-            ctxs.append(c)
-        out = [None] * Pn
-
-        def run(r):
-            ctxs[r].generate_rr(T, w.rr_seed)
-            out[r] = ctxs[r].select(k)
-
-        th = [threading.Thread(target=run, args=(r,)) for r in range(Pn)]
-        [t.start() for t in th]
-        [t.join() for t in th]
-        for r in range(Pn):
-            assert np.array_equal(out[r][0], rseeds) and np.array_equal(out[r][1], rgains)
-            assert out[r][2] == rcov
-            ids, off, nodes = ctxs[r].rr_export()
-            lo, hi = r * T // Pn, (r + 1) * T // Pn
-            assert np.array_equal(ids, np.arange(lo, hi, dtype=np.uint64))
-            assert np.array_equal(nodes, rnodes[roff[lo]:roff[hi]])
-
-
 @pytest.mark.parametrize("key", ["C3", "C4"])
 def test_imm_speculation_invariance(key):
     """gim_imm with the next round's RR ids sampled on a second stream while each round's
@@ -401,83 +344,6 @@ def test_imm_fresh_final_parity(key, rounds):
     assert rel(r.LB, ro.LB) and rel(r.theta, ro.theta)
     assert r.R_final == ro.R_final == math.ceil(ro.theta) and r.covered == ro.cov
     assert np.array_equal(r.seeds, ro.seeds)
-
-
-def _emulated_allgather(Pn):
-    """Host-side all-gather among Pn threads (one per emulated rank) for Gim.set_allgather."""
-    import torch
-    bar = threading.Barrier(Pn)
-    parts = [None] * Pn
-
-    def view(ptr, nbytes):
-        class V:
-            __cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1",
-                                        "data": (int(ptr), False), "version": 3,
-                                        "strides": None, "stream": None}
-        return torch.as_tensor(V(), device="cuda")
-
-    def make(r):
-        def cb(send, nbytes, recv, stream):
-            torch.cuda.ExternalStream(stream).synchronize()
-            parts[r] = view(send, nbytes).cpu()
-            bar.wait()
-            allp = torch.cat(parts)
-            bar.wait()
-            view(recv, nbytes * Pn).copy_(allp.cuda())
-            torch.cuda.synchronize()
-            return 0
-        return cb
-    return make
-
-
-@pytest.mark.parametrize("Pn,rounds", [(2, 1), (3, 1), (2, 3)])
-def test_replicated_pool_emulation_equals_single(Pn, rounds):
-    """Replicated-pool protocol (gim_set_allgather): every emulated rank samples its slice of each
-    round and ends up with the P = 1 pool (global id order, counts), the same selection and the
-    same IMM — with no per-step collective."""
-    w = gi.WORKLOADS["C2"]
-    g = gi.workload_graph("C2")
-    T, k = 30011 if rounds == 1 else 6007, 30 if rounds == 1 else 10
-    ref = _ctx(g, w.model, w.scheme)
-    ref.set_rounds(rounds)
-    for t in (1000, T):
-        ref.generate_rr(t, w.rr_seed)
-    rsel = ref.select(k)
-    rids, roff, rnodes = ref.rr_export(sort_each_set=False)
-    rcnt = ref.counts_export(g.n * rounds)
-    rimm = ref.imm(k, w.eps, w.ell, w.rr_seed)
-    make = _emulated_allgather(Pn)
-    ctxs = []
-    for r in range(Pn):
-        c = _ctx(g, w.model, w.scheme)
-        c.set_rounds(rounds)
-        c.set_shard(r, Pn)
-        c.set_allgather(make(r))
-        ctxs.append(c)
-    out = [None] * Pn
-
-    def run(r):
-        c = ctxs[r]
-        for t in (1000, T):
-            c.generate_rr(t, w.rr_seed)
-        sel = c.select(k)
-        exp = c.rr_export(sort_each_set=False)
-        cnt = c.counts_export(g.n * rounds)
-        imm = c.imm(k, w.eps, w.ell, w.rr_seed)
-        out[r] = (sel, exp, cnt, imm)
-
-    th = [threading.Thread(target=run, args=(r,)) for r in range(Pn)]
-    [t.start() for t in th]
-    [t.join() for t in th]
-    for r in range(Pn):
-        sel, (ids, off, nodes), cnt, imm = out[r]
-        assert np.array_equal(sel[0], rsel[0]) and np.array_equal(sel[1], rsel[1]) and sel[2] == rsel[2]
-        assert np.array_equal(ids, rids) and np.array_equal(off, roff)
-        # members of a set may be stored in another order (discovery order): compare sorted sets
-        for i in range(0, len(ids), 97):
-            assert np.array_equal(np.sort(nodes[off[i]:off[i + 1]]), np.sort(rnodes[roff[i]:roff[i + 1]]))
-        assert np.array_equal(cnt, rcnt)
-        assert np.array_equal(imm.seeds, rimm.seeds) and imm.R_final == rimm.R_final and imm.LB == rimm.LB
 
 
 @pytest.mark.parametrize("rounds", [1, 3])

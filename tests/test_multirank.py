@@ -1,7 +1,10 @@
-"""Multi-process (world_size 2 and 3, gloo on CPU) tests of the N > 1 host logic: the all-reduce
-callback plumbing of the binding, the RR-id slicing, and the sharded NodeSelection protocol the
-library runs per greedy step (count all-reduce once, then decrement all-reduce per step) —
-executed here on oracle pools split by rank, which must reproduce the single-process selection."""
+"""Multi-process (world_size 2 and 3, gloo on CPU) tests of the N > 1 host logic: the collective
+callback plumbing of the binding (all-reduce, all-gather, reduce-scatter), the RR-id slicing, and
+HOST EMULATIONS of the library's exchange protocols — dense count/decrement all-reduce per greedy
+step, node-sharded reduce-scatter selection, replicated-pool round all-gather — executed here on
+oracle pools split by rank, which must reproduce the oracle's single-process selection / pool.
+(The library's own implementation of the protocols is checked on the GPU against the oracle by
+tests/test_gpu_multirank.py and tests/test_gpu_multiproc.py.)"""
 import os
 import socket
 
@@ -184,7 +187,7 @@ def _replicated_round_protocol(rank, world, port, q, T, key):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_replicated_pool_protocol_equals_single(world):
+def test_replicated_round_host_emulation(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
@@ -195,3 +198,107 @@ def test_replicated_pool_protocol_equals_single(world):
     [p.join(60) for p in procs]
     for rank, off_ok, elems_ok in out:
         assert off_ok and elems_ok, rank
+
+
+def _worker_reducescatter(rank, world, port, q):
+    _init(rank, world, port)
+    import paper_2009_07325_b200 as P
+    fn = P.torch_reducescatter(device="cpu")
+    send = (np.arange(4 * world, dtype=np.int32) + 100 * rank)
+    recv = np.zeros(4, dtype=np.int32)
+    rc = fn(send.ctypes.data, recv.ctypes.data, 4, 0)
+    q.put((rank, rc, recv.tolist()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_reducescatter_callback_gloo(world):
+    """The node-sharded protocol's reduce-scatter callback: rank r receives the SUM over ranks of
+    block r."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker_reducescatter, args=(r, world, port, q)) for r in range(world)]
+    [p.start() for p in procs]
+    out = sorted(q.get(timeout=120) for _ in range(world))
+    [p.join(60) for p in procs]
+    for rank, rc, recv in out:
+        want = [sum(4 * rank + i + 100 * r for r in range(world)) for i in range(4)]
+        assert rc == 0 and recv == want
+
+
+def _node_sharded_select(rank, world, port, q, key, T, k):
+    """Host emulation of select_launch_rs (gim_api.cu): node shards of ceil(n / world); counts
+    reduce-scattered once; per step the shard argmax, the key exchange (one slot per rank, SUM),
+    the local cover and the decrements reduce-scattered to the owners."""
+    _init(rank, world, port)
+    import oracle
+    from paper_2009_07325_b200 import shard_slice
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    o = oracle.Oracle(g, w.model, w.scheme)
+    o.generate(T, w.rr_seed)
+    off, nodes, _ = o.export()
+    lo, hi = shard_slice(0, T, rank, world)
+    sets = [nodes[off[i]:off[i + 1]] for i in range(lo, hi)]
+    n = g.n
+    ns = -(-n // world)
+    local = np.zeros(ns * world, dtype=np.int64)
+    for s_ in sets:
+        local[s_] += 1
+    full = torch.from_numpy(local)
+    dist.all_reduce(full)                                  # reduce-scatter = all-reduce + own block
+    gshard = full.numpy()[rank * ns:(rank + 1) * ns].copy()
+    valid = max(0, min(ns, n - rank * ns))
+    inv = {}
+    for r, s_ in enumerate(sets):
+        for v in s_:
+            inv.setdefault(int(v), []).append(r)
+    covered = np.zeros(len(sets), dtype=bool)
+    selected = np.zeros(ns, dtype=bool)
+    seeds, gains = [], []
+    for _ in range(k):
+        key_ = 0
+        if valid:
+            c = np.where(selected[:valid], -1, gshard[:valid])
+            i = int(np.argmax(c))                            # lowest id among maxima
+            if c[i] >= 0:
+                key_ = (int(c[i]) << 32) | (0xFFFFFFFF - (rank * ns + i))
+        kx = torch.zeros(world, dtype=torch.int64)
+        kx[rank] = key_
+        dist.all_reduce(kx)                                  # key exchange: one slot per rank
+        best = int(kx.max())
+        u = 0xFFFFFFFF - (best & 0xFFFFFFFF)
+        seeds.append(u)
+        gains.append(best >> 32)
+        if rank * ns <= u < rank * ns + valid:
+            selected[u - rank * ns] = True
+        dec = np.zeros(ns * world, dtype=np.int64)
+        for r in inv.get(u, []):
+            if not covered[r]:
+                covered[r] = True
+                dec[sets[r]] += 1
+        d = torch.from_numpy(dec)
+        dist.all_reduce(d)
+        gshard -= d.numpy()[rank * ns:(rank + 1) * ns]
+    q.put((rank, seeds, gains))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_node_sharded_protocol_host_emulation(world):
+    import oracle
+    key, T, k = "C1", 20000, 20
+    w = gi.WORKLOADS[key]
+    o = oracle.Oracle(gi.workload_graph(key), w.model, w.scheme)
+    o.generate(T, w.rr_seed)
+    rs, rg, _ = o.select(k)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_node_sharded_select, args=(r, world, port, q, key, T, k)) for r in range(world)]
+    [p.start() for p in procs]
+    out = [q.get(timeout=300) for _ in range(world)]
+    [p.join(60) for p in procs]
+    for rank, seeds, gains in out:
+        assert seeds == rs.tolist() and gains == rg.tolist()

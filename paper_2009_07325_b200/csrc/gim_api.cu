@@ -87,6 +87,7 @@ struct gim_ctx {
   std::vector<Seg> segs;
   DevBuf pool, offsets, count_total;
   // generation scratch
+  DevBuf giant2_list;             // sets the shared-memory giant pass hands to the global pass
   DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr, dump, lt_spill, esc_list;
   DevBuf bitmaps, gqueues;
   DevBuf spill;                   // per-warp global queue + hash of the warp kernels' spill tier (kEmpty when unused)
@@ -100,6 +101,7 @@ struct gim_ctx {
   bool giant_cap_reached = false;
   uint64_t stage_cap = 0;
   int lt_bps = 0;                  // resident K-LT CTAs per SM on this context's device
+  int giant_sq = 0;                // GIM_OPT_GIANT_SHARED: shared-memory first giant pass (measured neutral: off)
   int skip = 0;                    // geometric-skip RNG contract (GIM_OPT_SKIP, reading R31)
   int skip_bps = 0;                // resident k_skip_lane CTAs per SM
   int skip_lane = -1;              // skip: -1 auto (lane kernel first for big chunks), 0 / 1
@@ -391,6 +393,7 @@ RRParams base_params(gim_ctx* c) {
   p.stage_cap = c->stage_cap;
   p.ctr = c->ctr.as<GenCounters>();
   p.giant_recs = c->giant_list.as<GiantRec>();
+  p.giant2_recs = c->giant2_list.as<GiantRec>();
   p.dump = c->dump.as<uint32_t>();
   p.dump_cap = c->dump.bytes / 4;
   p.retry_list = c->retry_list.as<uint32_t>();
@@ -411,6 +414,7 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   TRY(ensure(c, c->sizes, (uint64_t)cnt * 4));
   TRY(ensure(c, c->soff, (uint64_t)cnt * 8));
   TRY(ensure(c, c->giant_list, (uint64_t)cnt * sizeof(GiantRec)));
+  TRY(ensure(c, c->giant2_list, (uint64_t)cnt * sizeof(GiantRec)));
   TRY(ensure(c, c->dump, std::max<uint64_t>((uint64_t)cnt * 8, 1u << 20) * 4));
   TRY(ensure(c, c->retry_list, (uint64_t)cnt * 4));
   TRY(ensure(c, c->item_list, (uint64_t)cnt * 4));
@@ -534,9 +538,19 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     }
     {
       Prof pf(c, CLS_GIANT);
-      TRY(launched(c, launch_rr_giant(c->model, c->scheme, pp, (int)std::min(c->giant_slots, giant_grid),
+      // wide CTAs: a shared-memory pass first (sets up to kGQS nodes), the global-bitmap pass
+      // for the sets it hands over; narrow CTAs (many giant sets): the global pass directly
+      const bool sq = c->giant_sq && giant_nt == kGiantThreads;
+      if (sq) {
+        TRY(launched(c, launch_rr_giant(c->model, c->scheme, pp, c->num_sms * kGiantBlocksPerSM, nullptr, nullptr, 0,
+                                        c->stream, giant_nt, true), "k_rr_giant(shared)"));
+        c->st.n_giant_launches++;
+      }
+      RRParams pg = pp;
+      pg.giant_pass2 = sq ? 1 : 0;               // else the global pass reads the first list
+      TRY(launched(c, launch_rr_giant(c->model, c->scheme, pg, (int)std::min(c->giant_slots, giant_grid),
                                       c->bitmaps.as<uint32_t>(), c->gqueues.as<uint32_t>(), bm_words,
-                                      c->stream, giant_nt), "k_rr_giant"));
+                                      c->stream, giant_nt, false), "k_rr_giant"));
       c->st.n_giant_launches++;
     }
     return GIM_OK;
@@ -566,6 +580,7 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     GenCounters h = *c->h_ctr;
     h.stage_tail = old_cap;
     h.claim = h.claim_giant = h.giant_count = h.retry_count = 0;
+    h.giant2_count = h.claim_giant2 = 0;
     h.claim_lane = h.esc_count = 0;
     h.dump_tail = 0;
     *c->h_ctr = h;
@@ -589,6 +604,10 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
       TRY(sync(c));
     }
   }
+#ifdef GIM_WINSTAT
+  fprintf(stderr, "WINSTAT sets=%u windows=%llu valid_groups=%llu hub_steps=%llu coins=%llu\n", cnt,
+          c->h_ctr->dbg[0], c->h_ctr->dbg[1], c->h_ctr->dbg[2], c->h_ctr->coins);
+#endif
   c->st.coins += c->h_ctr->coins;
   c->st.live_edges += c->h_ctr->live;
   if (cnt >= 4096)   // running mean coins per set drives the lane/warp choice of later chunks
@@ -1141,7 +1160,7 @@ void gim_destroy(gim_ctx* c) {
   DeviceGuard g(c->device);
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
-                    &c->sizes, &c->soff, &c->giant_list, &c->retry_list, &c->item_list, &c->scan_out,
+                    &c->sizes, &c->soff, &c->giant_list, &c->giant2_list, &c->retry_list, &c->item_list, &c->scan_out,
                     &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->spill, &c->skip_tab, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
                     &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->thr_node, &c->ag_small,
@@ -1606,6 +1625,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
       if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
       c->sel_exec = nullptr;
       return GIM_OK;
+    case GIM_OPT_GIANT_SHARED: c->giant_sq = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_FORCE_COLLECTIVES:
       c->force_coll = value ? 1 : 0;
       c->have_seed = false;

@@ -104,6 +104,9 @@ struct GenCounters {
   unsigned int claim_giant;        // giant-kernel work claim
   unsigned int giant_count;        // ids pushed to the giant list
   unsigned int retry_count;        // ids whose staging write did not fit
+  unsigned int giant2_count;       // sets the shared-memory giant pass handed to the global pass
+  unsigned int claim_giant2;       // global giant pass work claim
+  unsigned long long dbg[4];       // GIM_WINSTAT builds: K-RR flattened windows / valid groups / hub steps
 };
 
 // A set handed from the warp kernel to the giant kernel: the warp's partial BFS (queue
@@ -145,6 +148,8 @@ struct RRParams {
   uint64_t stage_cap;
   GenCounters* ctr;
   GiantRec* giant_recs;        // sets handed to the giant kernel
+  GiantRec* giant2_recs;       // sets the shared-memory giant pass hands to the global pass
+  int giant_pass2;             // the global giant pass reads giant2_recs (after the shared pass)
   uint32_t* dump;              // partial-BFS dumps
   uint64_t dump_cap;
   uint32_t* retry_list;        // items whose staging write failed

@@ -10,7 +10,7 @@ int lt_blocks_per_sm();
 cudaError_t launch_rr_ic_lane(int scheme, const RRParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rr_warp(int model, int scheme, const RRParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
-                            uint32_t* gqueues, uint64_t bm_words, cudaStream_t s, int nt);
+                            uint32_t* gqueues, uint64_t bm_words, cudaStream_t s, int nt, bool sq);
 // geometric-skip contract (skip.cu, reading R31)
 cudaError_t launch_skip_lane(int scheme, const RRParams& p, int grid, cudaStream_t s);
 cudaError_t launch_skip_warp(int scheme, const RRParams& p, int grid, cudaStream_t s);

@@ -448,6 +448,12 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
           const uint32_t g = gk + gi;
           uint32_t m = 0;
           if (gi < total_g && !never) m = ic_live_mask<SCHEME>(p, id_lo, id_hi, k0, k1, g, ak, bk, tk);
+#ifdef GIM_WINSTAT
+          if (lane == 0) {
+            atomicAdd(&p.ctr->dbg[0], 1ull);
+            atomicAdd(&p.ctr->dbg[1], (unsigned long long)min(32u, total_g - base));
+          }
+#endif
           if (!__any_sync(kFull, m)) continue;          // no live in-edge in these 128 slots
           lives += __popc(m);
           if (!pend_add(g, m)) { overflow = true; break; }
@@ -457,6 +463,9 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
           const uint32_t k = __ffs(hm) - 1;
           const uint32_t ak = __shfl_sync(kFull, a, k), bk = __shfl_sync(kFull, b, k);
           const uint32_t tk = __shfl_sync(kFull, thr, k), hk = __shfl_sync(kFull, hub_full, k);
+#ifdef GIM_WINSTAT
+          if (lane == 0) atomicAdd(&p.ctr->dbg[2], (unsigned long long)(hk / kHubGroups));
+#endif
           if (!hub_sweep_whole<SCHEME>(p, id_lo, id_hi, ak, bk, ak >> 2, hk / kHubGroups, tk, never, lane,
                                        lives, pend_add))
             overflow = true;
@@ -936,23 +945,70 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* ptr) {
   return v;
 }
 
-template <int MODEL, int SCHEME, int kGiantThreads>
+// SQ = true (the first pass): queue and visited hash in shared memory (kGQS entries, kGHS slots)
+// — every claim, visit and queue read is a shared-memory access, not an L2 round trip; a set
+// that outgrows kGQS is aborted and handed to the second pass (SQ = false: per-CTA global
+// bitmap Visited[n], and global queue), which resumes it from its original record.
+constexpr uint32_t kGQS = 4096;
+constexpr uint32_t kGHS = 8192;              // power of two, load <= 1/2
+template <int MODEL, int SCHEME, int kGiantThreads, bool SQ>
 __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_giant(RRParams p, uint32_t* bitmaps,
                                                                uint32_t* gqueues, uint64_t bm_words) {
-  __shared__ uint32_t s_head, s_tail, s_busy, s_r;
+  __shared__ uint32_t s_head, s_tail, s_busy, s_r, s_abort;
   __shared__ uint32_t s_chead, s_cres;           // hub-chunk ring: claimed / reserved counters
   __shared__ uint4 s_ring[kChunkRing];           // {node, a, b, thr}; .x == kEmpty: not yet written
   __shared__ unsigned long long s_off;
+  extern __shared__ uint32_t dsm[];              // SQ: queue [kGQS] + hash [kGHS]
   const int lane = threadIdx.x & 31;
-  uint32_t* bm = bitmaps + (uint64_t)blockIdx.x * bm_words;
-  uint32_t* Q = gqueues + (uint64_t)blockIdx.x * p.n;     // entries are kEmpty when unused
-  const uint32_t giant_count = *(volatile unsigned int*)&p.ctr->giant_count;
+  uint32_t* bm = SQ ? nullptr : bitmaps + (uint64_t)blockIdx.x * bm_words;
+  uint32_t* Q = SQ ? dsm : gqueues + (uint64_t)blockIdx.x * p.n;     // entries are kEmpty when unused
+  uint32_t* Hs = dsm + kGQS;
+  const uint32_t cap = SQ ? kGQS : p.n;
+  const bool second = !SQ && p.giant_pass2;     // the global pass after the shared one
+  const GiantRec* recs = second ? p.giant2_recs : p.giant_recs;
+  unsigned int* claim_ctr = second ? &p.ctr->claim_giant2 : &p.ctr->claim_giant;
+  const uint32_t giant_count = second ? *(volatile unsigned int*)&p.ctr->giant2_count
+                                      : *(volatile unsigned int*)&p.ctr->giant_count;
   const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
   uint32_t coins = 0, lives = 0;
   for (uint32_t i = threadIdx.x; i < kChunkRing; i += kGiantThreads) s_ring[i].x = kEmpty;
-  auto visit = [bm](uint32_t u) {
+  if (SQ) {
+    for (uint32_t i = threadIdx.x; i < kGQS + kGHS; i += kGiantThreads) dsm[i] = kEmpty;
+    if (threadIdx.x == 0) s_abort = 0;
+  }
+  auto visit = [&](uint32_t u) -> bool {
+    if (SQ) {
+      uint32_t sl = (u * 0x9E3779B1u) >> 19;     // top 13 bits: kGHS = 2^13 slots
+      while (true) {
+        const uint32_t old = atomicCAS(&Hs[sl], kEmpty, u);
+        if (old == kEmpty) return true;
+        if (old == u) return false;
+        sl = (sl + 1) & (kGHS - 1u);
+      }
+    }
     const uint32_t bit = 1u << (u & 31);
     return !(atomicOr(&bm[u >> 5], bit) & bit);
+  };
+  // read queue entry i, written by another warp possibly still in flight (kEmpty until then)
+  auto qread = [&](uint32_t i) -> uint32_t {
+    if (SQ) {
+      uint32_t v = *(volatile uint32_t*)&Q[i];
+      while (v == kEmpty && !*(volatile uint32_t*)&s_abort) {
+        __nanosleep(32);
+        v = *(volatile uint32_t*)&Q[i];
+      }
+      return v == kEmpty ? 0u : v;             // aborted: any node (the set is discarded)
+    }
+    uint32_t v = ld_relaxed_gpu(Q + i);
+    while (v == kEmpty) {
+      __nanosleep(32);
+      v = ld_relaxed_gpu(Q + i);
+    }
+    return v;
+  };
+  auto qwrite = [&](uint32_t pos, uint32_t u) {
+    if (pos < cap) Q[pos] = u;
+    else if (SQ) s_abort = 1u;                 // the set outgrows the shared queue
   };
   // append this lane's new nodes uu[] to the block queue (warp-collective)
   auto append = [&](const uint32_t (&uu)[4]) {
@@ -964,7 +1020,7 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
     uint32_t pos = __shfl_sync(kFull, base, 0) + excl;
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      if (uu[j] != kEmpty) Q[pos++] = uu[j];
+      if (uu[j] != kEmpty) qwrite(pos++, uu[j]);
   };
   // IC: live in-edges of a claimed batch, resolved together (as in K-RR): cp.async of src[e]
   // into pend[], then one wait, bitmap test-and-set and append per 32 entries
@@ -989,7 +1045,7 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
       uint32_t b0 = 0;
       if (lane == 0 && total) b0 = atomicAdd(&s_tail, total);
       b0 = __shfl_sync(kFull, b0, 0);
-      if (isnew) Q[b0 + __popc(has & ((1u << lane) - 1u))] = u;
+      if (isnew) qwrite(b0 + __popc(has & ((1u << lane) - 1u)), u);
     }
     npend = 0;
     __syncwarp();
@@ -1015,26 +1071,32 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
   };
 
   while (true) {
-    if (threadIdx.x == 0) s_r = atomicAdd(&p.ctr->claim_giant, 1u);
+    if (threadIdx.x == 0) s_r = atomicAdd(claim_ctr, 1u);
     __syncthreads();
     const uint32_t r = s_r;
     if (r >= giant_count) break;
-    const GiantRec rec = p.giant_recs[r];
+    const GiantRec rec = recs[r];
     const uint64_t id = p.id_base + rec.item;
     const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
     if (rec.qlen == 0) {
       if (threadIdx.x == 0) {
         const uint32_t root = rr_root_of(p.seed, id, p.n, p.rounds);
         Q[0] = root;
-        atomicOr(&bm[root >> 5], 1u << (root & 31));
+        visit(root);
         s_tail = 1;
+        s_head = 0;
+      }
+    } else if (SQ && rec.qlen > kGQS) {        // the dump alone outgrows the shared queue
+      if (threadIdx.x == 0) {
+        s_abort = 1u;
+        s_tail = 0;
         s_head = 0;
       }
     } else {                                   // resume the warp kernel's partial BFS
       for (uint32_t t = threadIdx.x; t < rec.qlen; t += kGiantThreads) {
         const uint32_t u = p.dump[rec.dump_off + t];
         Q[t] = u;
-        atomicOr(&bm[u >> 5], 1u << (u & 31));
+        visit(u);
       }
       if (threadIdx.x == 0) {
         s_tail = rec.qlen;
@@ -1054,6 +1116,11 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
       if (lane == 0) {
         atomicAdd(&s_busy, 1u);
         while (true) {
+          if (SQ && *(volatile uint32_t*)&s_abort) {   // the set moves to the global pass
+            atomicSub(&s_busy, 1u);
+            state = 2;
+            break;
+          }
           const uint32_t ch = *(volatile uint32_t*)&s_chead;
           const uint32_t cr = *(volatile uint32_t*)&s_cres;
           if (ch < cr) {
@@ -1061,7 +1128,7 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
             continue;
           }
           const uint32_t h = *(volatile uint32_t*)&s_head;
-          const uint32_t t = *(volatile uint32_t*)&s_tail;
+          const uint32_t t = min(*(volatile uint32_t*)&s_tail, cap);
           if (h < t) {
             // IC: a batch of up to 32 nodes, smaller while the frontier is narrow so that
             // every warp of the block gets work; LT: one node (its walk is a single path)
@@ -1074,9 +1141,10 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
             const uint32_t b0 = *(volatile uint32_t*)&s_busy;
             __threadfence_block();
             const uint32_t h2 = *(volatile uint32_t*)&s_head;
-            const uint32_t t2 = *(volatile uint32_t*)&s_tail;
+            const uint32_t t2 = min(*(volatile uint32_t*)&s_tail, cap);
             const uint32_t ch2 = *(volatile uint32_t*)&s_chead;
             const uint32_t cr2 = *(volatile uint32_t*)&s_cres;
+            if (SQ && *(volatile uint32_t*)&s_abort) { state = 2; break; }
             if (h2 < t2 || ch2 < cr2) { atomicAdd(&s_busy, 1u); break; }
             if (b0 == 0) { state = 2; break; }
             __nanosleep(64);
@@ -1106,12 +1174,8 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
           // a batch of c queued nodes, expanded like a K-RR batch: lane i holds node Q[f+i]
           uint32_t a = 0, b = 0, thr = 0, ng = 0;
           if ((uint32_t)lane < c) {
-            // the appender may still be writing the entry: read it at L2, sleep while empty
-            uint32_t v = ld_relaxed_gpu(Q + f + lane);
-            while (v == kEmpty) {
-              __nanosleep(32);
-              v = ld_relaxed_gpu(Q + f + lane);
-            }
+            // the appender may still be writing the entry: sleep while empty
+            const uint32_t v = qread(f + lane);
             const uint32_t tv = (SCHEME == W_WC) ? __ldg(p.thr_node + v) : 0u;
             a = __ldg(p.row_ptr + v);
             b = __ldg(p.row_ptr + v + 1);
@@ -1197,11 +1261,7 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
         }
         flush();
       } else {                                   // LT: one node, one draw
-        uint32_t v = ld_relaxed_gpu(Q + f);
-        while (v == kEmpty) {
-          __nanosleep(32);
-          v = ld_relaxed_gpu(Q + f);
-        }
+        const uint32_t v = qread(f);
         const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
         if (b > a) {
           const uint32_t d = b - a;
@@ -1225,6 +1285,17 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
       }
     }
     __syncthreads();
+    if (SQ && s_abort) {                       // hand the set to the global pass, restore state
+      const uint32_t used = min(s_tail, cap);
+      if (threadIdx.x == 0) p.giant2_recs[atomicAdd(&p.ctr->giant2_count, 1u)] = rec;
+      for (uint32_t t = threadIdx.x; t < used; t += kGiantThreads) Q[t] = kEmpty;
+      uint4* h4 = reinterpret_cast<uint4*>(Hs);
+      for (uint32_t t = threadIdx.x; t < kGHS / 4; t += kGiantThreads) h4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+      for (uint32_t i = threadIdx.x; i < kChunkRing; i += kGiantThreads) s_ring[i].x = kEmpty;
+      __syncthreads();
+      if (threadIdx.x == 0) s_abort = 0;
+      continue;
+    }
     const uint32_t size = s_tail;
     if (threadIdx.x == 0) s_off = atomicAdd(&p.ctr->stage_tail, (unsigned long long)size);
     __syncthreads();
@@ -1235,8 +1306,12 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
     for (uint32_t t = threadIdx.x; t < size; t += kGiantThreads) {
       const uint32_t u = Q[t];
       if (fits) p.staging[off + t] = u;
-      bm[u >> 5] = 0u;
+      if (!SQ) bm[u >> 5] = 0u;
       Q[t] = kEmpty;
+    }
+    if (SQ) {
+      uint4* h4 = reinterpret_cast<uint4*>(Hs);
+      for (uint32_t t = threadIdx.x; t < kGHS / 4; t += kGiantThreads) h4[t] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     }
     __syncthreads();
   }
@@ -1387,26 +1462,45 @@ cudaError_t launch_rr_warp(int model, int scheme, const RRParams& p, int grid, c
   return launch_rr_lt(scheme, p, grid, s);
 }
 
-template <int NT>
+template <int MODEL, int SCHEME, int NT, bool SQ>
+static cudaError_t giant_attr() {
+  if (!SQ) return cudaSuccess;
+  static std::atomic<uint64_t> done{0};
+  return set_smem_once(done, (const void*)k_rr_giant<MODEL, SCHEME, NT, SQ>, (int)((kGQS + kGHS) * 4));
+}
+
+template <int NT, bool SQ>
 cudaError_t launch_rr_giant_nt(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
                                uint32_t* gqueues, uint64_t bm_words, cudaStream_t s) {
+  const int smem = SQ ? (int)((kGQS + kGHS) * 4) : 0;
+  cudaError_t e = cudaSuccess;
   if (model == MODEL_IC) {
-    if (scheme == W_WC) k_rr_giant<MODEL_IC, W_WC, NT><<<grid, NT, 0, s>>>(p, bitmaps, gqueues, bm_words);
-    else if (scheme == W_UNIFORM) k_rr_giant<MODEL_IC, W_UNIFORM, NT><<<grid, NT, 0, s>>>(p, bitmaps, gqueues, bm_words);
-    else k_rr_giant<MODEL_IC, W_EXPLICIT, NT><<<grid, NT, 0, s>>>(p, bitmaps, gqueues, bm_words);
+    e = scheme == W_WC ? giant_attr<MODEL_IC, W_WC, NT, SQ>()
+        : scheme == W_UNIFORM ? giant_attr<MODEL_IC, W_UNIFORM, NT, SQ>() : giant_attr<MODEL_IC, W_EXPLICIT, NT, SQ>();
   } else {
-    if (scheme == W_WC) k_rr_giant<MODEL_LT, W_WC, NT><<<grid, NT, 0, s>>>(p, bitmaps, gqueues, bm_words);
-    else k_rr_giant<MODEL_LT, W_EXPLICIT, NT><<<grid, NT, 0, s>>>(p, bitmaps, gqueues, bm_words);
+    e = scheme == W_WC ? giant_attr<MODEL_LT, W_WC, NT, SQ>() : giant_attr<MODEL_LT, W_EXPLICIT, NT, SQ>();
+  }
+  if (e != cudaSuccess) return e;
+  if (model == MODEL_IC) {
+    if (scheme == W_WC) k_rr_giant<MODEL_IC, W_WC, NT, SQ><<<grid, NT, smem, s>>>(p, bitmaps, gqueues, bm_words);
+    else if (scheme == W_UNIFORM) k_rr_giant<MODEL_IC, W_UNIFORM, NT, SQ><<<grid, NT, smem, s>>>(p, bitmaps, gqueues, bm_words);
+    else k_rr_giant<MODEL_IC, W_EXPLICIT, NT, SQ><<<grid, NT, smem, s>>>(p, bitmaps, gqueues, bm_words);
+  } else {
+    if (scheme == W_WC) k_rr_giant<MODEL_LT, W_WC, NT, SQ><<<grid, NT, smem, s>>>(p, bitmaps, gqueues, bm_words);
+    else k_rr_giant<MODEL_LT, W_EXPLICIT, NT, SQ><<<grid, NT, smem, s>>>(p, bitmaps, gqueues, bm_words);
   }
   return cudaGetLastError();
 }
 
-// nt = threads per giant set: kGiantThreads (default) or kGiantThreadsNarrow (many giant sets)
+// nt = threads per giant set: kGiantThreads (default) or kGiantThreadsNarrow (many giant sets).
+// sq: the shared-memory first pass over giant_recs (then call again with sq = false for the
+// sets it hands over in giant2_recs); !sq alone: the global pass over giant_recs directly.
 cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,
-                            uint32_t* gqueues, uint64_t bm_words, cudaStream_t s, int nt) {
+                            uint32_t* gqueues, uint64_t bm_words, cudaStream_t s, int nt, bool sq) {
+  if (sq) return launch_rr_giant_nt<kGiantThreads, true>(model, scheme, p, grid, bitmaps, gqueues, bm_words, s);
   if (nt == kGiantThreadsNarrow)
-    return launch_rr_giant_nt<kGiantThreadsNarrow>(model, scheme, p, grid, bitmaps, gqueues, bm_words, s);
-  return launch_rr_giant_nt<kGiantThreads>(model, scheme, p, grid, bitmaps, gqueues, bm_words, s);
+    return launch_rr_giant_nt<kGiantThreadsNarrow, false>(model, scheme, p, grid, bitmaps, gqueues, bm_words, s);
+  return launch_rr_giant_nt<kGiantThreads, false>(model, scheme, p, grid, bitmaps, gqueues, bm_words, s);
 }
 
 cudaError_t launch_store(const uint32_t* staging, const uint32_t* sizes, const uint64_t* soff,

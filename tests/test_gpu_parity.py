@@ -90,7 +90,9 @@ def test_pool_parity_tiny(gname):
                                   {P.OPT_FORCE_GIANT: 1, P.OPT_GIANT_NT: 256},
                                   {P.OPT_SPILL: 0}, {P.OPT_QUEUE_CAP: 8, P.OPT_SPILL: 64},
                                   {P.OPT_QUEUE_CAP: 32, P.OPT_SPILL: 40, P.OPT_STAGING_CAP: 1000},
-                                  {P.OPT_IC_LANE: 1, P.OPT_QUEUE_CAP: 4, P.OPT_SPILL: 16384}])
+                                  {P.OPT_IC_LANE: 1, P.OPT_QUEUE_CAP: 4, P.OPT_SPILL: 16384},
+                                  {P.OPT_GIANT_SHARED: 0}, {P.OPT_GIANT_SHARED: 0, P.OPT_FORCE_GIANT: 1},
+                                  {P.OPT_GIANT_SHARED: 1, P.OPT_QUEUE_CAP: 16}])
 def test_pool_parity_C1_invariance(opts):
     """Same pool whatever the queue capacity, spill-tier capacity (sets beyond the shared queue
     continue in the warp's global queue + hash, beyond the spill cap in K-GIANT), forced
@@ -393,4 +395,24 @@ def test_fused_selection_modes(key):
             assert c.stats()["fused_fallbacks"] >= 1
         s2, g2, c2 = c.select(w.k)                  # non-destructive, graph replay
         assert np.array_equal(s2, os_) and np.array_equal(g2, og)
+        c.close()
+
+
+@pytest.mark.parametrize("model,scheme,pu", [(gi.IC, gi.W_UNIFORM, 0.9), (gi.IC, gi.W_WC, 0.0), (gi.LT, gi.W_WC, 0.0)])
+def test_giant_shared_pass_handover(model, scheme, pu):
+    """Giant sets beyond the shared-memory giant pass (4096 nodes) are handed to the global-bitmap
+    pass and resumed there: an in-star of 20,000 leaves fed by a chain (IC uniform p = 0.9 gives
+    ~18,000-node sets), plus long chains for WC/LT; pools bit-exact with the oracle under both
+    giant modes and forced giant."""
+    leaves = 20000
+    edges = [(i, 0) for i in range(1, leaves + 1)] + [(leaves + 1 + i, leaves + 2 + i) for i in range(6000)]
+    edges += [(leaves + 6001, 0)]
+    g = gi.from_edges(leaves + 6002, edges)
+    T = 3000
+    o = oracle.Oracle(g, model, scheme, pu)
+    o.generate(T, 9)
+    for opts in ({}, {P.OPT_FORCE_GIANT: 1}, {P.OPT_GIANT_SHARED: 0}):
+        c = _ctx(g, model, scheme, pu, opts)
+        c.generate_rr(T, 9)
+        _same_pool(c, o, T)
         c.close()

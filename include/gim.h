@@ -260,7 +260,12 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *  GIM_OPT_GIANT_SHARED = 0 (default) / 1: giant sets (outgrowing the warp queue) first go through
  *                         a block-per-set pass with the queue and visited hash in shared memory
  *                         (sets up to 4096 nodes); larger ones continue in the global-bitmap pass.
- *                         Results are identical; measured neutral on C3 (giant 3.07 vs 3.03 ms). */
+ *                         Results are identical; measured neutral on C3 (giant 3.07 vs 3.03 ms).
+ *  GIM_OPT_SKIP_LANE_CAP = L (default 32, 1..512): under GIM_OPT_SKIP, the lane-per-set kernel keeps
+ *                         sets of up to L nodes (32 in shared memory, the rest in a per-lane
+ *                         global spill); larger sets escalate to the warp kernel. Results are
+ *                         identical; measured C3 sampling 7.5 / 11.7 / 18.4 / 29.6 / 61.9 ms at
+ *                         L = 32 / 96 / 160 / 256 / 512 (a long set holds its whole warp). */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -281,7 +286,8 @@ typedef enum {
   GIM_OPT_SELECT_FUSED = 18,
   GIM_OPT_FUSED_CTAS = 19,
   GIM_OPT_FORCE_COLLECTIVES = 20,
-  GIM_OPT_GIANT_SHARED = 21
+  GIM_OPT_GIANT_SHARED = 21,
+  GIM_OPT_SKIP_LANE_CAP = 22
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

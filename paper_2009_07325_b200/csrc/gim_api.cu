@@ -91,6 +91,8 @@ struct gim_ctx {
   DevBuf sizes, soff, giant_list, retry_list, item_list, scan_out, scan_tmp, staging, ctr, dump, lt_spill, esc_list;
   DevBuf bitmaps, gqueues;
   DevBuf spill;                   // per-warp global queue + hash of the warp kernels' spill tier (kEmpty when unused)
+  DevBuf lane_spill;              // R31 lane kernel: per-lane members beyond the shared 32
+  uint32_t skip_lane_cap = 32;    // R31 lane kernel: set size limit (GIM_OPT_SKIP_LANE_CAP)
   uint32_t giant_slots = 0;
   uint32_t giant_n = 0;             // n the giant slots were sized for (reused while n <= giant_n)
   int giant_nt_opt = 0;             // GIM_OPT_GIANT_NT: 0 auto, else threads per giant CTA
@@ -496,6 +498,11 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
         if (!c->skip_bps) c->skip_bps = skip_lane_blocks_per_sm();
         RRParams pl = pp;
         pl.esc_list = c->esc_list.as<uint32_t>();
+        pl.lane_cap = c->skip_lane_cap;
+        if (c->skip_lane_cap > 32) {
+          TRY(ensure(c, c->lane_spill, skip_lane_spill_words(c->num_sms * c->skip_bps) * 4));
+          pl.lane_spill = c->lane_spill.as<uint32_t>();
+        }
         {
           Prof pf(c, CLS_RR);
           TRY(launched(c, launch_skip_lane(c->scheme, pl, c->num_sms * c->skip_bps, c->stream), "k_skip_lane"));
@@ -1161,7 +1168,7 @@ void gim_destroy(gim_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
                     &c->sizes, &c->soff, &c->giant_list, &c->giant2_list, &c->retry_list, &c->item_list, &c->scan_out,
-                    &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->spill, &c->skip_tab, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
+                    &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->spill, &c->lane_spill, &c->skip_tab, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
                     &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->thr_node, &c->ag_small,
                     &c->ag_send, &c->ag_recv, &c->sel_bar, &c->rs_gcnt, &c->rs_dshard, &c->rs_keys, &c->rs_kx};
@@ -1624,6 +1631,10 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
       c->fused_ctas = (int)value;
       if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
       c->sel_exec = nullptr;
+      return GIM_OK;
+    case GIM_OPT_SKIP_LANE_CAP:
+      if (value < 1 || value > 512) return fail(c, GIM_EINVAL, "lane cap must be in [1, 512]");
+      c->skip_lane_cap = (uint32_t)value;
       return GIM_OK;
     case GIM_OPT_GIANT_SHARED: c->giant_sq = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_FORCE_COLLECTIVES:

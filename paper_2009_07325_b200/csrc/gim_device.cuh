@@ -157,6 +157,8 @@ struct RRParams {
   uint32_t* lt_spill;          // LT: per-warp spill of walks longer than kLtCap (lane-interleaved)
   uint32_t* spill;             // warp kernels: per-warp global queue + hash for sets > qcap
   uint32_t spill_cap;          // sets beyond this many nodes go to the CTA giant kernel (<= qcap: no spill)
+  uint32_t* lane_spill;        // R31 lane kernel: per-lane global members beyond the shared 32
+  uint32_t lane_cap;           // R31 lane kernel: set size limit (then escalate to the warp kernel)
   int force_giant;
   uint32_t rounds;             // MRIM rounds T (1 = standard IM): root of id = root(id / T)
 };

@@ -17,6 +17,7 @@ cudaError_t launch_skip_warp(int scheme, const RRParams& p, int grid, cudaStream
 cudaError_t launch_skip_giant(int scheme, const RRParams& p, int grid, uint32_t* bitmaps, uint32_t* gqueues,
                               uint64_t bm_words, cudaStream_t s);
 int skip_lane_blocks_per_sm();
+uint64_t skip_lane_spill_words(int grid);   // lane kernel's global member spill, words
 uint64_t spill_words_per_warp();   // spill tier of the warp kernels: words per warp
 constexpr int kSkipTabK = 184;   // log centers k = -75..106 (+ padding) of the R31 ln
 cudaError_t launch_skip_tables(int scheme, float p_uniform, uint32_t max_deg, double* tab, cudaStream_t s);

@@ -35,7 +35,8 @@ namespace gim {
 
 constexpr uint32_t kSkipBlock = 1024;
 constexpr int kSkipLaneWarps = 8;
-constexpr int kSkipLaneCap = 32;             // lane kernel: set size limit (then escalate)
+constexpr int kSkipLaneCap = 32;             // lane kernel: members per lane in shared memory
+constexpr uint32_t kSkipLaneCap2 = 512;      // lane kernel: most members per lane (shared + global spill)
 constexpr uint32_t kSkipLaneMaxBlk = 8;      // lane kernel: blocks per node limit (then escalate)
 constexpr uint32_t kSkipTag = 0x80000000u;   // counter word 1 of a skip draw: 2^31 | block
 
@@ -198,6 +199,14 @@ __global__ void __launch_bounds__(kSkipLaneWarps * 32) k_skip_lane(RRParams p) {
   __syncthreads();
   const int lane = threadIdx.x & 31;
   uint32_t* qv = smem + (threadIdx.x >> 5) * (kSkipLaneCap * 32);     // qv[i * 32 + lane]
+  // members beyond kSkipLaneCap continue in this warp's global spill region (lane-interleaved,
+  // L1-resident while the warp works on it), up to p.lane_cap; beyond that the set escalates
+  const uint64_t gwarp = (uint64_t)blockIdx.x * kSkipLaneWarps + (threadIdx.x >> 5);
+  uint32_t* lsp = p.lane_spill + gwarp * (uint64_t)((kSkipLaneCap2 - kSkipLaneCap) * 32);
+  const uint32_t lcap = min(p.lane_cap, kSkipLaneCap2);
+  auto at = [&](uint32_t t) -> uint32_t& {
+    return t < (uint32_t)kSkipLaneCap ? qv[t * 32 + lane] : lsp[(t - kSkipLaneCap) * 32 + lane];
+  };
   const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
   uint32_t item = 0, head = 0, tail = 0, draws = 0, lives = 0;
   uint32_t id_lo = 0;
@@ -254,7 +263,7 @@ __global__ void __launch_bounds__(kSkipLaneWarps * 32) k_skip_lane(RRParams p) {
       if (head == tail) {
         finish = true;
       } else {
-        const uint32_t v = qv[head * 32 + lane];
+        const uint32_t v = at(head);
         ++head;
         const uint32_t a = __ldg(p.row_ptr + v), b = __ldg(p.row_ptr + v + 1);
         const uint32_t d = b - a;
@@ -280,10 +289,12 @@ __global__ void __launch_bounds__(kSkipLaneWarps * 32) k_skip_lane(RRParams p) {
         ++lives;
         const uint32_t u = __ldg(p.src + e);
         bool seen = false;
-        for (uint32_t t = 0; t < tail; ++t) seen |= (qv[t * 32 + lane] == u);
+        const uint32_t ts = min(tail, (uint32_t)kSkipLaneCap);
+        for (uint32_t t = 0; t < ts; ++t) seen |= (qv[t * 32 + lane] == u);
+        for (uint32_t t = kSkipLaneCap; t < tail; ++t) seen |= (lsp[(t - kSkipLaneCap) * 32 + lane] == u);
         if (!seen) {
-          if (tail == (uint32_t)kSkipLaneCap) escalate = true;
-          else { qv[tail * 32 + lane] = u; ++tail; }
+          if (tail >= lcap) escalate = true;
+          else { at(tail) = u; ++tail; }
         }
       } else if ((cur.blk + 1u) * kSkipBlock < cur.d) {
         skip_block(cur, cur.blk + 1u);
@@ -320,7 +331,7 @@ __global__ void __launch_bounds__(kSkipLaneWarps * 32) k_skip_lane(RRParams p) {
         if (off + tail > p.stage_cap) {
           p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = item;
         } else {
-          for (uint32_t t = 0; t < tail; ++t) p.staging[off + t] = qv[t * 32 + lane];
+          for (uint32_t t = 0; t < tail; ++t) p.staging[off + t] = at(t);
           p.sizes[item] = tail;
           p.soff[item] = off;
         }
@@ -748,6 +759,8 @@ cudaError_t launch_skip_giant(int scheme, const RRParams& p, int grid, uint32_t*
   else k_skip_giant<W_UNIFORM><<<grid, kSkipGiantWarps * 32, 0, s>>>(p, bitmaps, gqueues, bm_words);
   return cudaGetLastError();
 }
+
+uint64_t skip_lane_spill_words(int grid) { return (uint64_t)grid * kSkipLaneWarps * 32 * (kSkipLaneCap2 - kSkipLaneCap); }
 
 int skip_lane_blocks_per_sm() {
   int bps = 1;

@@ -55,7 +55,8 @@ def _bipartite(d, hubs):
 
 MODES = {"auto": (1, {}), "warp": (2, {}), "lane": (3, {}), "giant": (1, {P.OPT_FORCE_GIANT: 1}),
          "q4": (2, {P.OPT_QUEUE_CAP: 4}), "q32_lane": (3, {P.OPT_QUEUE_CAP: 32}),
-         "staging": (3, {P.OPT_STAGING_CAP: 64})}
+         "staging": (3, {P.OPT_STAGING_CAP: 64}), "lane512": (3, {P.OPT_SKIP_LANE_CAP: 512}),
+         "lane8": (3, {P.OPT_SKIP_LANE_CAP: 8}), "lane40_q4": (3, {P.OPT_SKIP_LANE_CAP: 40, P.OPT_QUEUE_CAP: 4})}
 
 
 @pytest.mark.parametrize("mode", list(MODES))
@@ -97,7 +98,7 @@ def test_skip_tiers_big_sets():
 
 
 @pytest.mark.parametrize("key", ["C1", "C2"])
-@pytest.mark.parametrize("mode", ["auto", "warp", "lane", "giant", "q32_lane"])
+@pytest.mark.parametrize("mode", ["auto", "warp", "lane", "giant", "q32_lane", "lane512", "lane8"])
 def test_skip_pool_configs(key, mode):
     m, opts = MODES[mode]
     w = gi.WORKLOADS[key]

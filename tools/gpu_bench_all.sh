@@ -1,6 +1,9 @@
+# Bench lines of every BASELINE.json config (+ the geometric-skip variant measured in the same
+# run for IC configs) and the BA density extremes, one B200.
 mkdir -p gpurun_out
-timeout -s KILL 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "default rc=$?"
-timeout -s KILL 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; echo "reference rc=$?"
-timeout -s KILL 600 python bench.py --workload C4 --no-cpu-baseline > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err; echo "C4 rc=$?"
-timeout -s KILL 600 python bench.py --workload C2 --no-cpu-baseline > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err; echo "C2 rc=$?"
-timeout -s KILL 600 python bench.py --workload C1 --no-cpu-baseline > gpurun_out/bench_C1.json 2> gpurun_out/bench_C1.err; echo "C1 rc=$?"
+for w in C1 C2 C3 C4 C5; do
+  python bench.py --workload $w --steps 10 --warmup 3 > gpurun_out/r02_bench_$w.json 2> gpurun_out/r02_bench_$w.err
+done
+for w in B2 B32; do
+  python bench.py --workload $w --steps 3 --warmup 2 --no-e2e --no-cpu-baseline > gpurun_out/r02_bench_$w.json 2> gpurun_out/r02_bench_$w.err
+done

@@ -8,7 +8,7 @@ Reads gpurun_out/launches_<WL>.csv (ncu --metrics gpu__time_duration.sum launch 
   profiles/<round>_launches_<WL>.csv      the raw launch list
   profiles/<round>_launch_shares_<WL>.txt per-kernel totals and shares (cold, serialised)
   profiles/<round>_ncu_<kernel>_<WL>.txt  key metrics of the full capture
-  profiles/ncu_traffic.json               DRAM bytes per launch of the captured kernels (bench.py)
+  profiles/ncu_traffic.json               bench-launch:* DRAM bytes per captured launch
 """
 import collections
 import csv
@@ -115,10 +115,11 @@ def main():
                       ("k_cover", f"prof_cover_{wl}.ncu-rep"), ("k_argmax", f"prof_argmax_{wl}.ncu-rep")]:
         p = os.path.join(GO, rep)
         if os.path.exists(p):
-            traffic[f"{wl}:{name}"] = full_capture(p, name, wl, rnd)
-    traffic["_note"] = ("DRAM read+write bytes of ONE captured launch (ncu --set full; the 9th launch "
-                        "of the kernel in bench.py --steps 1 --warmup 1 = round-4 chunk of the timed "
-                        "IMM run), per launch")
+            traffic[f"bench-launch:{wl}:{name}"] = full_capture(p, name, wl, rnd)
+    traffic["_note"] = ("bench-launch:* = DRAM read+write bytes of ONE captured launch (ncu --set full) "
+                        "of the kernel inside bench.py --steps 1 --warmup 1; <WL>:k_rr_warp[:skip] = "
+                        "tools/traffic_capture.py (one 2^20-set generate_rr call, paired with the same "
+                        "call's algorithmic bytes; what bench.py reports)")
     json.dump(traffic, open(tj, "w"), indent=1)
     print(json.dumps(traffic, indent=1))
 

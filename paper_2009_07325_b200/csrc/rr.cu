@@ -936,6 +936,10 @@ constexpr uint32_t kBusySlot = 0xFFFFFFFEu; // ring slot being written (node ids
 #define GIM_GIANT_DIV 2
 #endif
 constexpr uint32_t kGiantClaimDiv = GIM_GIANT_DIV;   // batch = pending / this, clamped to [1, 32]
+#ifndef GIM_GIANT_FLAT_MIN
+#define GIM_GIANT_FLAT_MIN 8
+#endif
+constexpr uint32_t kGiantFlatMin = GIM_GIANT_FLAT_MIN;   // batches of >= this many nodes: ballot/redux owner lookup
 static_assert(kSplitGroups % kHubGroups == 0, "hub chunks are whole hub steps");
 
 // Relaxed load at gpu scope (not hoisted out of spin loops, not served from a stale L1 line).
@@ -1189,24 +1193,39 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
           const uint32_t hubs = __ballot_sync(kFull, hub_full != 0u);
           const uint32_t ngf = ng - hub_full;
           const uint32_t gs = (a >> 2) + hub_full;
+          // node of flattened group gi: for small batches (often a few nodes while the frontier
+          // is narrow) a shuffle search 0-2 steps deep; for wide ones (dense graphs) the
+          // ballot/redux lookup of K-RR over the compacted ranges (one step per window)
+          const bool wide = c >= kGiantFlatMin;
           uint32_t total_g;
           const uint32_t E = warp_excl_scan(ngf, lane, total_g);
           const uint32_t P = E + ngf;
-          // node of flattened group gi: shuffle search (measured faster than flat_setup/flat_owner
-          // here: giant batches are often a few nodes, where the search is 0-2 steps deep)
+          Flat f{};
+          if (wide) f = flat_setup(a, b, thr, gs, ngf, lane);
           const uint32_t top = c > 1 ? 1u << (31 - __clz(c - 1)) : 0u;
           for (uint32_t base = 0; base < total_g; base += 32) {
             const uint32_t gi = base + lane;
-            uint32_t k = 0;
+            uint32_t ak, bk, tk, gk;
+            if (wide) {
+              const uint32_t k = flat_owner(f, base, lane);
+              ak = __shfl_sync(kFull, f.a, k);
+              bk = __shfl_sync(kFull, f.b, k);
+              tk = __shfl_sync(kFull, f.thr, k);
+              gk = __shfl_sync(kFull, f.gofs, k);
+            } else {
+              uint32_t k = 0;
 #pragma unroll
-            for (uint32_t step = 16; step >= 1; step >>= 1) {
-              if (step <= top) {
-                const uint32_t pv = __shfl_sync(kFull, P, k + step - 1);
-                if (pv <= gi) k += step;
+              for (uint32_t step = 16; step >= 1; step >>= 1) {
+                if (step <= top) {
+                  const uint32_t pv = __shfl_sync(kFull, P, k + step - 1);
+                  if (pv <= gi) k += step;
+                }
               }
+              ak = __shfl_sync(kFull, a, k);
+              bk = __shfl_sync(kFull, b, k);
+              tk = __shfl_sync(kFull, thr, k);
+              gk = __shfl_sync(kFull, gs - E, k);
             }
-            const uint32_t ak = __shfl_sync(kFull, a, k), bk = __shfl_sync(kFull, b, k);
-            const uint32_t tk = __shfl_sync(kFull, thr, k), gk = __shfl_sync(kFull, gs - E, k);
             const uint32_t g = gk + gi;
             uint32_t m = 0;
             if (gi < total_g && !never) m = ic_live_mask<SCHEME>(p, id_lo, id_hi, 0u, 0u, g, ak, bk, tk);

@@ -805,6 +805,18 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
   bool active = false, want = true;       // want: lane needs a new walk
   uint32_t coins = 0, lives = 0;
   const uint32_t cap = min((uint32_t)kLtCap2, p.qcap);
+  // 128-bit Bloom filter of the lane's path (one hashed bit per member): a next node whose bit is
+  // clear is certainly new, so the O(len) membership scan runs only on a possible revisit
+  uint32_t bl0 = 0, bl1 = 0, bl2 = 0, bl3 = 0;
+  auto bloom_bit = [](uint32_t u) { return (u * 0x9E3779B1u) >> 25; };   // 0..127
+  auto bloom_test = [&](uint32_t h) {
+    const uint32_t w = (h & 64u) ? ((h & 32u) ? bl3 : bl2) : ((h & 32u) ? bl1 : bl0);
+    return (w >> (h & 31u)) & 1u;
+  };
+  auto bloom_set = [&](uint32_t h) {
+    const uint32_t b = 1u << (h & 31u);
+    if (h < 32u) bl0 |= b; else if (h < 64u) bl1 |= b; else if (h < 96u) bl2 |= b; else bl3 |= b;
+  };
   unsigned long long chunk_off = 0;                  // this warp's staging chunk
   uint32_t chunk_left = 0;
   while (true) {
@@ -826,6 +838,8 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
           v = rr_root_of(p.seed, id, p.n, p.rounds);
           path[lane] = v;
           len = 1;
+          bl0 = bl1 = bl2 = bl3 = 0;
+          bloom_set(bloom_bit(v));
           if (p.force_giant) {
             p.giant_recs[atomicAdd(&p.ctr->giant_count, 1u)] = GiantRec{item, 0u, 0u, 0u, 0ull};
             active = false;
@@ -853,12 +867,15 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
           ++lives;
           const uint32_t u = __ldg(p.src + a + j);
           bool seen = false;
-          const uint32_t ls = min(len, (uint32_t)kLtCap);
-          for (uint32_t t = 0; t < ls; ++t) seen |= (path[t * 32 + lane] == u);
-          for (uint32_t t = kLtCap; t < len; ++t) seen |= (spill[(t - kLtCap) * 32 + lane] == u);
+          const uint32_t hb = bloom_bit(u);
+          if (bloom_test(hb)) {                 // possible revisit: scan the path
+            const uint32_t ls = min(len, (uint32_t)kLtCap);
+            for (uint32_t t = 0; t < ls; ++t) seen |= (path[t * 32 + lane] == u);
+            for (uint32_t t = kLtCap; t < len; ++t) seen |= (spill[(t - kLtCap) * 32 + lane] == u);
+          }
           if (seen) finish = true;
           else if (len == cap) overflow = true;
-          else { at(len) = u; ++len; v = u; }
+          else { at(len) = u; ++len; v = u; bloom_set(hb); }
         }
       }
     }
@@ -882,15 +899,29 @@ __global__ void __launch_bounds__(kLtWarps * 32) k_rr_lt_lane(RRParams p) {
       const unsigned long long base = chunk_off;
       chunk_off += tot;
       chunk_left -= tot;
+      unsigned long long off = 0;
+      bool ok = false;
       if (finish) {
-        const unsigned long long off = base + incl - len;
-        if (off + len > p.stage_cap) {
+        off = base + incl - len;
+        ok = off + len <= p.stage_cap;
+        if (!ok) {
           p.retry_list[atomicAdd(&p.ctr->retry_count, 1u)] = item;
         } else {
-          for (uint32_t t = 0; t < len; ++t) p.staging[off + t] = at(t);
           p.sizes[item] = len;
           p.soff[item] = off;
         }
+      }
+      // the whole warp copies each finished walk in turn: 32 coalesced elements per step
+      // instead of one lane writing its path element by element
+      __syncwarp();
+      for (uint32_t cm = __ballot_sync(kFull, finish && ok); cm; cm &= cm - 1) {
+        const int k = __ffs(cm) - 1;
+        const uint32_t lk = __shfl_sync(kFull, len, k);
+        const unsigned long long ok_off = __shfl_sync(kFull, off, k);
+        for (uint32_t t = lane; t < lk; t += 32)
+          p.staging[ok_off + t] = t < (uint32_t)kLtCap ? path[t * 32 + k] : spill[(t - kLtCap) * 32 + k];
+      }
+      if (finish) {
         active = false;
         want = true;
       }

@@ -265,7 +265,16 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                         sets of up to L nodes (32 in shared memory, the rest in a per-lane
  *                         global spill); larger sets escalate to the warp kernel. Results are
  *                         identical; measured C3 sampling 7.5 / 11.7 / 18.4 / 29.6 / 61.9 ms at
- *                         L = 32 / 96 / 160 / 256 / 512 (a long set holds its whole warp). */
+ *                         L = 32 / 96 / 160 / 256 / 512 (a long set holds its whole warp).
+ *  GIM_OPT_SELECT_COOP  = C (0 = off; 1..8192): for P = 1 (standard IM, no speculation) run the k
+ *                         greedy steps of a selection in ONE cooperative launch with one grid
+ *                         barrier per step: every CTA takes the argmax redundantly over the <= C
+ *                         candidates whose initial count reaches tau (certified: counts only
+ *                         decrease), and the cover accumulates only the candidates' decrements;
+ *                         an uncertified step makes the selection rerun with the default
+ *                         kernels (gim_stats.fused_fallbacks). Results are identical; measured
+ *                         slower (C3 selection 5.85 / 6.87 ms at C = 2048 / 8192 vs 4.28 ms, no
+ *                         fallbacks): the grid barrier costs more than the launch it replaces. */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -287,7 +296,8 @@ typedef enum {
   GIM_OPT_FUSED_CTAS = 19,
   GIM_OPT_FORCE_COLLECTIVES = 20,
   GIM_OPT_GIANT_SHARED = 21,
-  GIM_OPT_SKIP_LANE_CAP = 22
+  GIM_OPT_SKIP_LANE_CAP = 22,
+  GIM_OPT_SELECT_COOP = 23
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

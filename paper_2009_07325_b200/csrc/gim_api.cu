@@ -134,6 +134,9 @@ struct gim_ctx {
   bool sel_fused_used = false;  // the pending selection ran fused
   DevBuf sel_done;              // fused steps: per-step completion tickets + the fail flag
   int fused_ctas = 2;           // fused cover grid = this x #SMs (fewer tickets per step)
+  uint32_t sel_coop = 0;        // GIM_OPT_SELECT_COOP: candidate cap of the cooperative selection (0 = off)
+  DevBuf cmap, cdec;            // cooperative selection: node -> candidate index (kEmpty), decrement rings
+  uint64_t cmap_n = 0;          // nodes covered by cmap (kEmpty-initialised)
   // options
   int force_giant = 0, profile = 0;
   int mb_chains = 8;            // GIM_OPT_MB_CHAINS: Philox chains per thread in the microbenchmark
@@ -914,8 +917,8 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   uint32_t* cand = nullptr;
   unsigned int *hist = nullptr, *ncand = nullptr;
   uint32_t* tau_p1 = nullptr;
-  const bool fused_mode = !dec && c->rounds == 1 && c->sel_fused && !c->force_unfused && !c->speculate &&
-                          !c->sel_persistent;
+  const bool fused_mode = !dec && c->rounds == 1 && (c->sel_fused || c->sel_coop) && !c->force_unfused &&
+                          !c->speculate && !c->sel_persistent;
   if (!fused_mode && !dec && c->rounds == 1 &&
       (c->use_cand == 2 || (c->use_cand == 1 && n >= (1u << 23)))) {   // small n: full scan is cheaper
     TRY(ensure(c, c->cand, (uint64_t)kMaxCand * 4 + 64 * 4));
@@ -925,6 +928,46 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
     ncand = reinterpret_cast<unsigned int*>(hist + 41);
     TRY(launched(c, launch_cand_setup(c->cnt.as<uint32_t>(), (uint32_t)n, kMaxCand, hist, tau_p1, cand, ncand,
                                       c->num_sms * 4, c->stream), "candidate setup", 3));
+  }
+  // cooperative selection (P = 1, standard IM): one cooperative launch, one grid barrier per
+  // step, redundant per-CTA candidate argmax; certificate failures are redone by select_finish
+  const bool coop = !dec && c->rounds == 1 && c->sel_coop && !c->force_unfused && !c->speculate &&
+                    !c->sel_persistent;
+  if (coop) {
+    const uint32_t cap = std::min<uint32_t>(c->sel_coop, kCoopCands);
+    TRY(ensure(c, c->cand, (uint64_t)kCoopCands * 4 + 64 * 4));
+    uint32_t* cnd = c->cand.as<uint32_t>();
+    unsigned int* hst = reinterpret_cast<unsigned int*>(cnd + kCoopCands);
+    uint32_t* tau = reinterpret_cast<uint32_t*>(hst + 40);
+    unsigned int* ncd = reinterpret_cast<unsigned int*>(hst + 41);
+    TRY(launched(c, launch_cand_setup(c->cnt.as<uint32_t>(), (uint32_t)n, cap, hst, tau, cnd, ncd,
+                                      c->num_sms * 4, c->stream), "candidate setup", 3));
+    if (c->cmap_n < n || !c->cmap.p) {
+      TRY(dalloc(c, c->cmap, n * 4));
+      CK(cudaMemsetAsync(c->cmap.p, 0xFF, n * 4, c->stream));
+      c->cmap_n = n;
+    }
+    TRY(ensure(c, c->cdec, 3ull * kCoopCands * 4));
+    CK(cudaMemsetAsync(c->cdec.p, 0, 3ull * kCoopCands * 4, c->stream));
+    TRY(ensure(c, c->sel_bar, 64));
+    CK(cudaMemsetAsync(c->sel_bar.p, 0, 8, c->stream));
+    TRY(ensure(c, c->sel_done, ((uint64_t)kk + 2) * 4));
+    uint32_t* ff = c->sel_done.as<uint32_t>() + kk;
+    CK(cudaMemsetAsync(ff, 0, 4, c->stream));
+    {
+      Prof pf(c, CLS_SELECT);
+      TRY(launched(c, launch_select_coop(c->cnt.as<uint32_t>(), cnd, ncd, tau, c->cmap.as<uint32_t>(),
+                                         c->cdec.as<int32_t>(), keys, (int)kk, segd, c->offsets.as<uint64_t>(),
+                                         c->pool.as<uint32_t>(), c->covered.as<uint8_t>(),
+                                         c->sel_bar.as<unsigned int>(), ff, c->num_sms, limited, c->stream),
+                   "k_select_coop", 3));
+    }
+    c->sel_fused_used = true;
+    TRY(read_keys(c, kk));
+    CK(cudaMemcpyAsync(c->h_keys + kk, ff, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaEventRecord(c->ev_sel_done, c->stream));
+    c->sel_pending = true;
+    return GIM_OK;
   }
   // fused greedy steps (P = 1, standard IM): one launch per step, candidate argmax in the last
   // CTA of each cover; certificate failures are redone unfused by select_finish
@@ -1637,6 +1680,10 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
       c->skip_lane_cap = (uint32_t)value;
       return GIM_OK;
     case GIM_OPT_GIANT_SHARED: c->giant_sq = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_SELECT_COOP:
+      if (value < 0 || value > (int64_t)kCoopCands) return fail(c, GIM_EINVAL, "coop candidate cap must be in [0, 8192]");
+      c->sel_coop = (uint32_t)value;
+      return GIM_OK;
     case GIM_OPT_FORCE_COLLECTIVES:
       c->force_coll = value ? 1 : 0;
       c->have_seed = false;

@@ -81,6 +81,13 @@ cudaError_t launch_select_fused(unsigned long long* keys, int kk, const InvSegDe
                                 const uint32_t* pool, uint8_t* covered, uint32_t* cnt, const uint32_t* cand,
                                 const unsigned int* ncand, const uint32_t* tau_p1, unsigned int* done,
                                 uint32_t* fail, int grid, cudaStream_t s, bool limit, int* launches);
+// cooperative selection: one launch, one grid barrier per greedy step, redundant candidate argmax
+constexpr uint32_t kCoopCands = 8192;   // most candidates of the cooperative selection
+cudaError_t launch_select_coop(const uint32_t* cnt, const uint32_t* cand, const unsigned int* ncand,
+                               const uint32_t* tau_p1, uint32_t* cmap, int32_t* cdec, unsigned long long* keys,
+                               int kk, const InvSegDev* segs, const uint64_t* offsets, const uint32_t* pool,
+                               uint8_t* covered, unsigned int* bar, uint32_t* fail, int num_sms, bool limit,
+                               cudaStream_t s);
 cudaError_t launch_validate_csr(const uint64_t* rp64, uint32_t n, uint64_t m, const uint32_t* src,
                                 uint32_t* rp32, uint32_t* err, uint32_t* bad_row, uint32_t* thr_node, int grid,
                                 cudaStream_t s);

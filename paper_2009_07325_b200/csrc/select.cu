@@ -10,6 +10,7 @@
 // so a selection touches each pool element at most once for decrements. The argmax is one
 // streaming pass with a packed 64-bit key (count << 32 | ~v) reduced by warp shuffles and one
 // atomicMax per CTA; the previous pick is retired inside the same pass (count = sentinel).
+#include <atomic>
 #include <algorithm>
 
 #include "gim_device.cuh"
@@ -429,13 +430,17 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
                                            const uint64_t* __restrict__ offsets,
                                            const uint32_t* __restrict__ pool,
                                            uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
-                                           int32_t* __restrict__ dec, MrimSel mr) {
+                                           int32_t* __restrict__ dec, MrimSel mr,
+                                           uint32_t u_known = kEmpty, const uint32_t* __restrict__ cmap = nullptr,
+                                           int32_t* __restrict__ cdec = nullptr) {
   __shared__ uint64_t s_lo[kMaxInvSeg], s_end[kMaxInvSeg];   // list start, inclusive prefix end
   __shared__ const uint32_t* s_inv[kMaxInvSeg];
   __shared__ uint32_t s_nseg, s_limit;
   const uint32_t sub = threadIdx.x & 7;
-  const uint32_t u = ~(uint32_t)keys[j];
-  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[u] = kSent;   // retire the pick (never decremented)
+  // u_known: the pick computed by this CTA itself (cooperative selection; the pick is excluded
+  // from later argmaxes there, not retired in cnt, which other CTAs may still be reading)
+  const uint32_t u = u_known != kEmpty ? u_known : ~(uint32_t)keys[j];
+  if (u_known == kEmpty && blockIdx.x == 0 && threadIdx.x == 0) cnt[u] = kSent;   // retire the pick
   if (threadIdx.x < 32) {                     // lanes load the segments' list bounds in parallel
     const uint32_t l = threadIdx.x;
     InvSegDev sg{nullptr, nullptr};
@@ -504,6 +509,16 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
       uint32_t w[kCoverIlp];
 #pragma unroll
       for (int t = 0; t < kCoverIlp; ++t) w[t] = (e + 8 * t < b) ? pool[e + 8 * t] : u;
+#pragma unroll
+      if (cmap != nullptr) {                   // cooperative selection: candidates only
+        uint32_t ci[kCoverIlp];
+#pragma unroll
+        for (int t = 0; t < kCoverIlp; ++t) ci[t] = (w[t] == u) ? kEmpty : __ldg(cmap + w[t]);
+#pragma unroll
+        for (int t = 0; t < kCoverIlp; ++t)
+          if (ci[t] != kEmpty) atomicAdd(cdec + ci[t], 1);
+        continue;
+      }
 #pragma unroll
       for (int t = 0; t < kCoverIlp; ++t) {
         if (w[t] == u) continue;
@@ -624,6 +639,102 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar) {
     __threadfence();
   }
   __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------
+// Cooperative selection (P = 1, GIM_OPT_SELECT_COOP): the k greedy steps in ONE cooperative
+// launch with ONE grid barrier per step. The argmax only ever looks at the candidate list (the
+// <= C nodes whose initial count reaches tau; counts only decrease, so a best candidate count
+// >= tau certifies the global argmax), and every CTA computes it redundantly from a private
+// copy of the candidates' counts in shared memory — no cross-CTA reduction, hence no barrier
+// between the argmax and the cover of a step. The cover of step j adds the decrements of
+// CANDIDATE members to buffer B[j % 3] (indexed through cmap: node -> candidate index);
+// after the step's barrier every CTA subtracts B[j % 3] from its copy. Three rotating buffers
+// make a buffer's reuse safe with one barrier per step: B[(j+1) % 3] (read in step j-1's
+// argmax, by every CTA before barrier j-1) is zeroed by block 0 during step j, and its next
+// writer is step j+1's cover, after barrier j. Non-candidate counts are never read again. An
+// uncertified step makes every CTA (all compute the same best) stop and sets *fail: the host
+// redoes the selection with the full-scan kernels.
+// ------------------------------------------------------------------------------------------
+constexpr uint32_t kCoopCandMax = 8192;
+template <bool LIMIT>
+__global__ void __launch_bounds__(1024, 1) k_select_coop(const uint32_t* __restrict__ cnt,
+                                                         const uint32_t* __restrict__ cand,
+                                                         const unsigned int* __restrict__ ncand,
+                                                         const uint32_t* __restrict__ tau_p1,
+                                                         const uint32_t* __restrict__ cmap, int32_t* cdec,
+                                                         unsigned long long* __restrict__ keys, int kk,
+                                                         const InvSegDev* __restrict__ segs,
+                                                         const uint64_t* __restrict__ offsets,
+                                                         const uint32_t* __restrict__ pool,
+                                                         uint8_t* __restrict__ covered, unsigned int* bar,
+                                                         uint32_t* fail) {
+  extern __shared__ uint32_t s_coop[];               // [kCoopCandMax] counts + [kCoopCandMax] node ids
+  uint32_t* s_cnt = s_coop;                          // this CTA's copy of the candidates' counts
+  uint32_t* s_v = s_coop + kCoopCandMax;
+  __shared__ unsigned long long s_red[32];
+  __shared__ uint32_t s_idx[32];
+  const uint32_t nc = min(*ncand, kCoopCandMax), tau = *tau_p1;
+  for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+    const uint32_t v = cand[i];
+    s_v[i] = v;
+    s_cnt[i] = cnt[v];
+  }
+  __syncthreads();
+  for (int j = 0; j < kk; ++j) {
+    if (j > 0) {                                          // the previous step's decrements
+      const int32_t* bj = cdec + (uint64_t)((j - 1) % 3) * kCoopCandMax;
+      for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x)
+        if (s_cnt[i] != kSent) s_cnt[i] -= (uint32_t)__ldcg(bj + i);
+    }
+    if (blockIdx.x == 0) {                                // zero the buffer step j+1 will fill
+      int32_t* bz = cdec + (uint64_t)((j + 1) % 3) * kCoopCandMax;
+      for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) bz[i] = 0;
+    }
+    __syncthreads();
+    unsigned long long best = 0;                          // key = count << 32 | ~v (R10)
+    uint32_t bidx = 0;
+    for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+      const uint32_t c = s_cnt[i];
+      if (c == kSent) continue;
+      const unsigned long long key = ((unsigned long long)c << 32) | (unsigned long long)(~s_v[i]);
+      if (key > best) { best = key; bidx = i; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+      const uint32_t oi = __shfl_xor_sync(kFull, bidx, off);
+      if (o > best) { best = o; bidx = oi; }
+    }
+    if ((threadIdx.x & 31) == 0) { s_red[threadIdx.x >> 5] = best; s_idx[threadIdx.x >> 5] = bidx; }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      best = (threadIdx.x < (blockDim.x >> 5)) ? s_red[threadIdx.x] : 0ull;
+      bidx = (threadIdx.x < (blockDim.x >> 5)) ? s_idx[threadIdx.x] : 0u;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+        const uint32_t oi = __shfl_xor_sync(kFull, bidx, off);
+        if (o > best) { best = o; bidx = oi; }
+      }
+      if (threadIdx.x == 0) {
+        s_red[0] = best;
+        s_idx[0] = bidx;
+        if (best != 0ull) s_cnt[bidx] = kSent;            // excluded from later steps
+      }
+    }
+    __syncthreads();
+    best = s_red[0];
+    __syncthreads();                                      // s_red is rewritten next step
+    if (best == 0ull || (uint32_t)(best >> 32) < tau) {   // not certified: every CTA stops
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(fail, 1u);
+      return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) keys[j] = best;
+    cover_step<LIMIT>(keys, j, segs, offsets, pool, covered, nullptr, nullptr, MrimSel{1u, 0u, 0u},
+                      ~(uint32_t)best, cmap, cdec + (uint64_t)(j % 3) * kCoopCandMax);
+    grid_barrier(bar);
+  }
 }
 
 // The k greedy steps of one NodeSelection in ONE cooperative launch (P = 1): per step the argmax
@@ -785,6 +896,37 @@ cudaError_t launch_select_fused(unsigned long long* keys, int kk, const InvSegDe
                                                done, fail);
   }
   *launches = kk + 1;
+  return cudaGetLastError();
+}
+
+// cmap[v] = candidate index of node v, kEmpty otherwise (filled by k_cand_map after a kEmpty memset)
+__global__ void k_cand_map(const uint32_t* __restrict__ cand, const unsigned int* __restrict__ ncand,
+                           uint32_t* __restrict__ cmap, int unmap) {
+  const uint32_t nc = min(*ncand, kCoopCandMax);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x)
+    cmap[cand[i]] = unmap ? kEmpty : i;
+}
+
+cudaError_t launch_select_coop(const uint32_t* cnt, const uint32_t* cand, const unsigned int* ncand,
+                               const uint32_t* tau_p1, uint32_t* cmap, int32_t* cdec, unsigned long long* keys,
+                               int kk, const InvSegDev* segs, const uint64_t* offsets, const uint32_t* pool,
+                               uint8_t* covered, unsigned int* bar, uint32_t* fail, int num_sms, bool limit,
+                               cudaStream_t s) {
+  const int smem = (int)(2 * kCoopCandMax * 4);
+  void* kern = limit ? (void*)k_select_coop<true> : (void*)k_select_coop<false>;
+  static std::atomic<uint64_t> attr{0};
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  if (!(attr.load() & (1ull << (dev & 63)))) {
+    if (cudaError_t e = cudaFuncSetAttribute((const void*)k_select_coop<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) return e;
+    if (cudaError_t e = cudaFuncSetAttribute((const void*)k_select_coop<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) return e;
+    attr.fetch_or(1ull << (dev & 63));
+  }
+  k_cand_map<<<64, 256, 0, s>>>(cand, ncand, cmap, 0);
+  void* args[] = {&cnt, &cand, &ncand, &tau_p1, &cmap, &cdec, &keys, &kk, &segs, &offsets, &pool, &covered, &bar, &fail};
+  cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3((unsigned)num_sms), dim3(1024), args, (size_t)smem, s);
+  if (e != cudaSuccess) return e;
+  k_cand_map<<<64, 256, 0, s>>>(cand, ncand, cmap, 1);   // restore cmap to all-kEmpty
   return cudaGetLastError();
 }
 

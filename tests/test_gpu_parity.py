@@ -416,3 +416,40 @@ def test_giant_shared_pass_handover(model, scheme, pu):
         c.generate_rr(T, 9)
         _same_pool(c, o, T)
         c.close()
+
+
+@pytest.mark.parametrize("key", ["C1", "C2"])
+def test_coop_selection_modes(key):
+    """GIM_OPT_SELECT_COOP (one cooperative launch, one grid barrier per greedy step, redundant
+    candidate argmax per CTA, candidate-only decrement rings): the oracle's seeds and gains at
+    every candidate cap, including caps that fail the certificate and rerun (O7, Alg. 7)."""
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    T = 50021
+    o = oracle.Oracle(g, w.model, w.scheme, w.p_uniform)
+    o.generate(T, w.rr_seed)
+    os_, og, oc = o.select(w.k)
+    for cap in (8192, 2048, 64, 1):
+        c = _ctx(g, w.model, w.scheme, w.p_uniform, {P.OPT_SELECT_COOP: cap})
+        c.generate_rr(T // 2, w.rr_seed)
+        c.generate_rr(T, w.rr_seed)                       # two index segments
+        c.reset_stats()
+        for _ in range(2):                                # non-destructive, repeatable
+            s, gn, cv = c.select(w.k)
+            assert np.array_equal(s, os_) and np.array_equal(gn, og) and cv == oc, cap
+        if cap == 1:
+            assert c.stats()["fused_fallbacks"] >= 1
+        c.close()
+
+
+@pytest.mark.parametrize("key", ["C1", "C3", "C4"])
+def test_coop_selection_imm_golden(key):
+    """Full IMM with the cooperative selection equals the oracle's committed run."""
+    import json
+    gd = json.load(open(os.path.join(os.path.dirname(__file__), "golden", f"imm_{key}.json")))
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    c = _ctx(g, w.model, w.scheme, w.p_uniform, {P.OPT_SELECT_COOP: 4096})
+    r = c.imm(w.k, w.eps, w.ell, w.rr_seed)
+    assert r.seeds.tolist() == gd["seeds"] and r.cov_i.tolist() == gd["cov_i"] and r.R_final == gd["R_final"]
+    c.close()

@@ -238,8 +238,7 @@ __device__ __forceinline__ bool spill_hash_insert(uint32_t* gh, uint32_t u) {
 // stop the walk: it compares against u, not against empty)
 __device__ __forceinline__ void spill_hash_erase(uint32_t* gh, uint32_t u) {
   uint32_t s = (u * 0x9E3779B1u) >> 17;
-  while (gh[s] != u) s = (s + 1) & (kSpillH - 1u);
-  gh[s] = kEmpty;
+  while (atomicCAS(&gh[s], u, kEmpty) != u) s = (s + 1) & (kSpillH - 1u);
 }
 
 }  // namespace gim

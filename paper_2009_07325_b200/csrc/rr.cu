@@ -1026,11 +1026,11 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
   };
   // read queue entry i, written by another warp possibly still in flight (kEmpty until then)
   auto qread = [&](uint32_t i) -> uint32_t {
-    if (SQ) {
-      uint32_t v = *(volatile uint32_t*)&Q[i];
-      while (v == kEmpty && !*(volatile uint32_t*)&s_abort) {
+    if (SQ) {                                  // atomic reads: the writer is another warp
+      uint32_t v = atomicOr(&Q[i], 0u);
+      while (v == kEmpty && !atomicOr(&s_abort, 0u)) {
         __nanosleep(32);
-        v = *(volatile uint32_t*)&Q[i];
+        v = atomicOr(&Q[i], 0u);
       }
       return v == kEmpty ? 0u : v;             // aborted: any node (the set is discarded)
     }
@@ -1042,8 +1042,12 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
     return v;
   };
   auto qwrite = [&](uint32_t pos, uint32_t u) {
-    if (pos < cap) Q[pos] = u;
-    else if (SQ) s_abort = 1u;                 // the set outgrows the shared queue
+    if (SQ) {
+      if (pos < cap) atomicExch(&Q[pos], u);
+      else atomicExch(&s_abort, 1u);           // the set outgrows the shared queue
+    } else {
+      Q[pos] = u;
+    }
   };
   // append this lane's new nodes uu[] to the block queue (warp-collective)
   auto append = [&](const uint32_t (&uu)[4]) {
@@ -1151,7 +1155,7 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
       if (lane == 0) {
         atomicAdd(&s_busy, 1u);
         while (true) {
-          if (SQ && *(volatile uint32_t*)&s_abort) {   // the set moves to the global pass
+          if (SQ && atomicOr(&s_abort, 0u)) {          // the set moves to the global pass
             atomicSub(&s_busy, 1u);
             state = 2;
             break;
@@ -1179,7 +1183,7 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
             const uint32_t t2 = min(*(volatile uint32_t*)&s_tail, cap);
             const uint32_t ch2 = *(volatile uint32_t*)&s_chead;
             const uint32_t cr2 = *(volatile uint32_t*)&s_cres;
-            if (SQ && *(volatile uint32_t*)&s_abort) { state = 2; break; }
+            if (SQ && atomicOr(&s_abort, 0u)) { state = 2; break; }
             if (h2 < t2 || ch2 < cr2) { atomicAdd(&s_busy, 1u); break; }
             if (b0 == 0) { state = 2; break; }
             __nanosleep(64);

@@ -363,11 +363,11 @@ __device__ __forceinline__ bool skip_hash_insert(uint32_t* h, uint32_t u) {
 }
 
 // clear member u from the hash: walk from its home slot to the slot holding it (holes left by
-// members cleared before cannot stop the walk: it compares against u, not against empty)
+// members cleared before cannot stop the walk: it compares against u, not against empty). The
+// lanes of a warp erase concurrently, so every probe is one atomic compare-and-swap.
 __device__ __forceinline__ void skip_hash_erase(uint32_t* h, uint32_t u) {
   uint32_t s = __umulhi(u * 0x9E3779B1u, (uint32_t)kHSize);
-  while (h[s] != u) s = (s + 1 == (uint32_t)kHSize) ? 0u : s + 1;
-  h[s] = kEmpty;
+  while (atomicCAS(&h[s], u, kEmpty) != u) s = (s + 1 == (uint32_t)kHSize) ? 0u : s + 1;
 }
 
 __device__ __forceinline__ void cp_async4_skip(uint32_t dst, const uint32_t* src) {

@@ -138,7 +138,12 @@ gim_status gim_select(gim_ctx* ctx, uint32_t k, uint32_t* seeds_out, uint64_t* g
                       uint64_t* covered_out);
 
 /* IMM result / trace (reading R1-R8, R21). theta_i[r] are the round targets ceil(theta_i)
- * actually sampled, cov_i[r] the covered count of round r's selection. */
+ * actually sampled, cov_i[r] the covered count of round r's selection over its sel_steps_i[r]
+ * greedy steps. With GIM_OPT_IMM_EARLY_EXIT (default on) an estimation round's selection stops
+ * at the first step j whose bound cov_j + (k - j) * gain_j (gains never increase) falls below
+ * the smallest count that passes the round's test (Alg. 2 l.7): the round fails either way, so
+ * LB, theta, R_final and the seeds are unchanged; then sel_steps_i[r] < k (k * T in MRIM mode)
+ * and cov_i[r] is the covered count of those steps. */
 typedef struct {
   double ell_eff, eps_prime, lambda_prime, lambda_star, LB, theta;
   uint32_t rounds;
@@ -147,6 +152,7 @@ typedef struct {
   uint64_t R_final;
   uint64_t covered;
   double spread_est;   /* n * covered / R_final (Eq. 3) */
+  uint32_t sel_steps_i[64];
 } gim_imm_result;
 
 /* Full IMM (Alg. 2 bootstrap of LB, then theta = lambda_star / LB and the final NodeSelection):
@@ -274,7 +280,16 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                         an uncertified step makes the selection rerun with the default
  *                         kernels (gim_stats.fused_fallbacks). Results are identical; measured
  *                         slower (C3 selection 5.85 / 6.87 ms at C = 2048 / 8192 vs 4.28 ms, no
- *                         fallbacks): the grid barrier costs more than the launch it replaces. */
+ *                         fallbacks): the grid barrier costs more than the launch it replaces.
+ *  GIM_OPT_IMM_EARLY_EXIT = 1 (default) / 0: bounded greedy in gim_imm's estimation rounds (see
+ *                         gim_imm_result.sel_steps_i); 0 runs every round's k steps.
+ *  GIM_OPT_COND_GRAPH   = 1 (default) / 0: the replayed selection graph is one conditional (IF)
+ *                         node per greedy step, so the steps after a bounded-greedy stop are
+ *                         skipped by the graph instead of launching kernels that return at once
+ *                         (falls back to the plain graph where conditional nodes are refused).
+ *  GIM_OPT_INV_PASSES   = P (0 = auto: one pass per 32 MB of per-node cursors, 1..64): the
+ *                         inverted-index scatter runs P node-range passes over the new sets so
+ *                         each pass's cursor atomics stay in the L2 (results identical). */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -297,7 +312,10 @@ typedef enum {
   GIM_OPT_FORCE_COLLECTIVES = 20,
   GIM_OPT_GIANT_SHARED = 21,
   GIM_OPT_SKIP_LANE_CAP = 22,
-  GIM_OPT_SELECT_COOP = 23
+  GIM_OPT_SELECT_COOP = 23,
+  GIM_OPT_IMM_EARLY_EXIT = 24,
+  GIM_OPT_COND_GRAPH = 25,
+  GIM_OPT_INV_PASSES = 26
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 
@@ -321,6 +339,7 @@ typedef struct {
   double host_ms_sync;          /* host wall time blocked in stream synchronisation       */
   double host_ms_api;           /* host wall time inside gim_generate_rr/select/imm       */
   uint64_t fused_fallbacks;     /* fused selections redone unfused (uncertified argmax)   */
+  uint64_t probe_stops;         /* gim_imm rounds settled by the first-step probe alone   */
 } gim_stats;
 gim_status gim_get_stats(gim_ctx* ctx, gim_stats* out);
 gim_status gim_reset_stats(gim_ctx* ctx);

@@ -124,6 +124,11 @@ struct gim_ctx {
   };
   std::vector<InvSeg> iseg;
   bool inv_valid = true;
+  // lazy segments: sets [pend_set0, nsets) (elements [pend_e0, pool_len)) are not indexed yet;
+  // the next selection indexes them as ONE segment (several IMM rounds whose selections stopped
+  // at their first step share one O(n) histogram/scan pass)
+  bool inv_pending = false;
+  uint64_t pend_set0 = 0, pend_e0 = 0;
   int inv_segmented = 1;        // GIM_OPT_INV_SEGMENTS
   DevBuf cnt_snap;              // count_total at the last indexed chunk
   DevBuf seg_desc;              // device InvSegDev[kMaxInvSeg] + uint32 nseg
@@ -136,6 +141,15 @@ struct gim_ctx {
   int fused_ctas = 2;           // fused cover grid = this x #SMs (fewer tickets per step)
   uint32_t sel_coop = 0;        // GIM_OPT_SELECT_COOP: candidate cap of the cooperative selection (0 = off)
   DevBuf cmap, cdec;            // cooperative selection: node -> candidate index (kEmpty), decrement rings
+  DevBuf sel_ctl;               // SelCtl of the bounded greedy (IMM estimation rounds)
+  DevBuf probe;                 // first-step argmax key of gim_imm's probe
+  uint64_t sel_cstar = 0;       // smallest passing covered count of the running round (0 = off)
+  uint32_t last_sel_steps = 0;  // greedy steps the last selection ran
+  int cond_graph = 1;           // selection graph as IF nodes per step (0: unsupported / off)
+  int inv_passes = 0;           // GIM_OPT_INV_PASSES: node-range passes of the index scatter (0 = auto)
+  bool sel_cond_used = false;   // the pending selection replays a conditional graph
+  int sel_per_step = 2;         // kernels per greedy step of the pending graph replay
+  int imm_early_exit = 1;       // GIM_OPT_IMM_EARLY_EXIT
   uint64_t cmap_n = 0;          // nodes covered by cmap (kEmpty-initialised)
   // options
   int force_giant = 0, profile = 0;
@@ -150,6 +164,7 @@ struct gim_ctx {
   // CUDA graph of the k-step selection loop (P = 1), valid while its key is unchanged
   cudaGraphExec_t sel_exec = nullptr;
   std::vector<uintptr_t> sel_key;
+  bool sel_cond = false;        // sel_exec is the conditional (IF node per step) graph
   int use_graph = 1;
 };
 
@@ -322,11 +337,38 @@ gim_status build_inv_segment(gim_ctx* c, uint64_t set0, uint64_t set1, uint64_t 
   cudaError_t e = launch_scan_u32_to32(c->cursor.as<uint32_t>(), n, sg.off.as<uint32_t>(), c->scan_tmp.as<uint64_t>(),
                                        c->scan_tmp.as<uint64_t>() + scan_tiles(n) + 1, c->stream, &nl);
   TRY(launched(c, e, "scan(segment counts)", nl));
-  if (set1 > set0)
-    TRY(launched(c, launch_inv_scatter(c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), (uint32_t)set0,
-                                       (uint32_t)set1, sg.off.as<uint32_t>(), sg.inv.as<uint32_t>(),
-                                       c->num_sms * 8, c->stream), "k_inv_scatter"));
+  if (set1 > set0) {
+    // node-range passes: each keeps <= kInvPassBytes of cursors (+ its inv range) in the L2
+    const uint64_t kInvPassBytes = 32ull << 20;
+    const int passes = c->inv_passes > 0 ? c->inv_passes
+                                         : (int)std::max<uint64_t>(1, (n * 4 + kInvPassBytes - 1) / kInvPassBytes);
+    e = launch_inv_scatter(c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), (uint32_t)set0, (uint32_t)set1,
+                           sg.off.as<uint32_t>(), sg.inv.as<uint32_t>(), c->num_sms * 8, c->stream, (uint32_t)n,
+                           passes, &nl);
+    TRY(launched(c, e, "k_inv_scatter", nl));
+  }
   c->iseg.push_back(std::move(sg));
+  return GIM_OK;
+}
+
+// Index the pending (unindexed) sets as one new segment, or rebuild the whole index as one
+// segment when it is invalid or a new segment would not fit (kMaxInvSeg, 2^32 elements).
+gim_status flush_inv(gim_ctx* c) {
+  if (c->inv_valid && c->inv_pending) {
+    if (c->iseg.size() < (size_t)kMaxInvSeg && c->pool_len - c->pend_e0 < 0xFFFFFFFFull)
+      TRY(build_inv_segment(c, c->pend_set0, c->nsets, c->pend_e0, c->pool_len));
+    else
+      c->inv_valid = false;
+  }
+  c->inv_pending = false;
+  if (!c->inv_valid) {                          // one segment over the whole local pool
+    drop_inv(c);
+    CK(cudaMemsetAsync(c->cnt_snap.p, 0, nsp(c) * 4, c->stream));
+    TRY(build_inv_segment(c, 0, c->nsets, 0, c->pool_len));
+    c->inv_valid = true;
+    c->set_limit = ~0ull;
+    c->truncated = false;
+  }
   return GIM_OK;
 }
 
@@ -344,6 +386,7 @@ gim_status reset_pool(gim_ctx* c, uint64_t seed) {
   CK(cudaMemsetAsync(c->offsets.p, 0, 8, c->stream));
   drop_inv(c);
   c->inv_valid = true;
+  c->inv_pending = false;
   c->set_limit = ~0ull;
   c->truncated = false;
   TRY(ensure(c, c->cnt_snap, nsp(c) * 4));
@@ -665,6 +708,7 @@ gim_status truncate_pool(gim_ctx* c, uint64_t theta) {
     TRY(launched(c, launch_count_sub(c->pool.as<uint32_t>(), e0, c->pool_len, c->count_total.as<uint32_t>(),
                                      c->num_sms * 8, c->stream), "k_count_sub"));
   c->segs = kept;
+  if (c->inv_pending && keep_sets <= c->pend_set0) c->inv_pending = false;   // the unindexed sets are gone
   c->nsets = keep_sets;
   c->pool_len = e0;
   c->T_global = theta;
@@ -776,14 +820,18 @@ gim_status generate(gim_ctx* c, uint64_t theta_sets, uint64_t seed, bool host_sy
     const size_t seg0 = c->segs.size();
     for (uint64_t s = lo; s < hi; s += kChunk) TRY(gen_chunk(c, s, (uint32_t)std::min<uint64_t>(kChunk, hi - s)));
     if ((c->world > 1 || c->force_coll) && c->agfn) TRY(replicate_round(c, a, theta, set0, e0, seg0));
-    // one inverted-index segment per generate call (= per IMM round): its O(n) count scan is
-    // paid once per round, not once per 2^22-id chunk
+    // the new sets join the unindexed range; the next selection indexes it as one segment (its
+    // O(n) count scan is paid once per selection that needs it, not per 2^22-id chunk or round)
     if (c->nsets > set0) {
-      if (c->inv_segmented && c->inv_valid && c->iseg.size() < (size_t)kMaxInvSeg &&
-          c->pool_len - e0 < 0xFFFFFFFFull)
-        TRY(build_inv_segment(c, set0, c->nsets, e0, c->pool_len));
-      else
+      if (c->inv_segmented && c->inv_valid) {
+        if (!c->inv_pending) {
+          c->inv_pending = true;
+          c->pend_set0 = set0;
+          c->pend_e0 = e0;
+        }
+      } else {
         c->inv_valid = false;                  // rebuilt as one segment at the next selection
+      }
     }
     c->T_global = theta;
   }
@@ -810,7 +858,7 @@ gim_status read_keys(gim_ctx* c, uint32_t kk) {
 // by a SUM all-reduce of one slot per rank, the global pick (largest key: lowest id on ties,
 // R10) retired by its owner and covered in the local pool, the local decrements
 // reduce-scattered to the owners.
-gim_status select_launch_rs(gim_ctx* c, uint32_t k, const InvSegDev* segd, const uint32_t* nsegd, bool limited) {
+gim_status select_launch_rs(gim_ctx* c, uint32_t k, const InvSegDev* segd, SelCtl* ctl, bool limited) {
   const uint64_t n = c->n;
   const uint32_t W = (uint32_t)c->world, r = (uint32_t)c->rank;
   const uint64_t ns = (n + W - 1) / W, npad = ns * W;
@@ -835,6 +883,7 @@ gim_status select_launch_rs(gim_ctx* c, uint32_t k, const InvSegDev* segd, const
   CK(cudaMemsetAsync(c->covered.p, 0, std::max<uint64_t>(c->nsets, 1), c->stream));
   CK(cudaMemsetAsync(keys, 0, (uint64_t)kk * 8, c->stream));
   CK(cudaMemsetAsync(lkeys, 0, (uint64_t)kk * 8, c->stream));
+  TRY(launched(c, launch_sel_ctl(ctl, c->sel_cstar, kk, c->stream), "k_sel_ctl"));
   CK(cudaMemsetAsync(dec, 0, npad * 4, c->stream));
   CK(cudaMemsetAsync(dshard, 0, ns * 4, c->stream));
   c->st.allreduces++;
@@ -842,12 +891,12 @@ gim_status select_launch_rs(gim_ctx* c, uint32_t k, const InvSegDev* segd, const
   Prof pf(c, CLS_SELECT);
   for (uint32_t j = 0; j < kk; ++j) {
     TRY(launched(c, launch_argmax(gcnt, dshard, ns_valid, lkeys, (int)j, nullptr, c->num_sms * kArgmaxCtasPerSM,
-                                  c->stream, false, id_base), "k_argmax(shard)"));
+                                  c->stream, false, id_base, ctl), "k_argmax(shard)"));
     TRY(launched(c, launch_rs_pack(lkeys, (int)j, r, W, kx, c->stream), "k_rs_pack"));
     c->st.allreduces++;
     if (c->arfn(kx, 2ull * W, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(keys) failed");
     TRY(launched(c, launch_rs_pick(kx, W, keys, (int)j, gcnt, id_base, ns_valid, c->stream), "k_rs_pick"));
-    TRY(launched(c, launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
+    TRY(launched(c, launch_cover(keys, (int)j, segd, ctl, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                                  c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * kCoverCtasPerSM,
                                  c->stream, limited, nullptr), "k_cover"));
     if (j + 1 < kk) {
@@ -878,14 +927,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   TRY(ensure(c, c->keys, (uint64_t)kk * 8));
   if (sharded) TRY(ensure(c, c->dec, n * 4));
   int32_t* dec = sharded ? c->dec.as<int32_t>() : nullptr;
-  if (!c->inv_valid) {                          // one segment over the whole local pool
-    drop_inv(c);
-    CK(cudaMemsetAsync(c->cnt_snap.p, 0, n * 4, c->stream));
-    TRY(build_inv_segment(c, 0, c->nsets, 0, c->pool_len));
-    c->inv_valid = true;
-    c->set_limit = ~0ull;
-    c->truncated = false;
-  }
+  TRY(flush_inv(c));
   TRY(ensure(c, c->seg_desc, sizeof(InvSegDev) * kMaxInvSeg + 16));
   {
     InvSegDev tab[kMaxInvSeg];
@@ -899,12 +941,14 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   }
   const bool limited = c->set_limit != ~0ull;     // cover must skip truncated sets
   const InvSegDev* segd = c->seg_desc.as<InvSegDev>();
-  const uint32_t* nsegd = reinterpret_cast<const uint32_t*>(segd + kMaxInvSeg);
-  if (sharded && c->rsfn && c->rounds == 1) return select_launch_rs(c, k, segd, nsegd, limited);
+  TRY(ensure(c, c->sel_ctl, sizeof(SelCtl)));
+  SelCtl* ctl = c->sel_ctl.as<SelCtl>();
+  if (sharded && c->rsfn && c->rounds == 1) return select_launch_rs(c, k, segd, ctl, limited);
   CK(cudaMemcpyAsync(c->cnt.p, c->count_total.p, n * 4, cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaEventRecord(c->ev_cnt_copied, c->stream));
   CK(cudaMemsetAsync(c->covered.p, 0, std::max<uint64_t>(c->nsets / c->rounds, 1), c->stream));
   CK(cudaMemsetAsync(c->keys.p, 0, (uint64_t)kk * 8, c->stream));
+  TRY(launched(c, launch_sel_ctl(ctl, c->sel_cstar, kk, c->stream), "k_sel_ctl"));
   if (dec) {
     CK(cudaMemsetAsync(dec, 0, n * 4, c->stream));
     c->st.allreduces++;
@@ -1035,37 +1079,78 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
     const std::vector<uintptr_t> key = {(uintptr_t)c->cnt.p, (uintptr_t)segd, (uintptr_t)cand,
                                         (uintptr_t)c->offsets.p, (uintptr_t)c->pool.p, (uintptr_t)c->covered.p,
                                         (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n, (uintptr_t)limited,
-                                        (uintptr_t)c->rounds};
+                                        (uintptr_t)c->rounds, (uintptr_t)ctl};
+    auto step = [&](uint32_t j, unsigned long long h) {
+      if (cand) launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream, ctl);
+      launch_argmax(c->cnt.as<uint32_t>(), nullptr, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * kArgmaxCtasPerSM, c->stream,
+                    mr != nullptr, 0u, ctl);
+      launch_cover(keys, (int)j, segd, ctl, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
+                   c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * kCoverCtasPerSM, c->stream,
+                   limited, mr, h);
+    };
     if (!c->sel_exec || key != c->sel_key) {
       if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
       c->sel_exec = nullptr;
+      c->sel_key.clear();
       cudaGraph_t graph = nullptr;
-      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      for (uint32_t j = 0; j < kk; ++j) {
-        if (cand) launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream);
-        launch_argmax(c->cnt.as<uint32_t>(), nullptr, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * kArgmaxCtasPerSM, c->stream,
-                      mr != nullptr);
-        launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
-                     c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * kCoverCtasPerSM, c->stream,
-                     limited, mr);
+      if (c->cond_graph) {
+        // one IF node per greedy step on one handle (reset to 1 at every replay): the cover that
+        // stops a bounded greedy clears it and the graph skips the remaining steps itself
+        cudaError_t e = cudaGraphCreate(&graph, 0);
+        cudaGraphConditionalHandle h = 0;
+        if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, graph, 1u, cudaGraphCondAssignDefault);
+        cudaGraphNode_t prev = nullptr;
+        for (uint32_t j = 0; j < kk && e == cudaSuccess; ++j) {
+          cudaGraphNodeParams cp = {};
+          cp.type = cudaGraphNodeTypeConditional;
+          cp.conditional.handle = h;
+          cp.conditional.type = cudaGraphCondTypeIf;
+          cp.conditional.size = 1;
+          cudaGraphNode_t node = nullptr;
+          e = cudaGraphAddNode(&node, graph, prev ? &prev : nullptr, prev ? 1 : 0, &cp);
+          if (e != cudaSuccess) break;
+          cudaGraph_t body = cp.conditional.phGraph_out[0];
+          e = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+          if (e != cudaSuccess) break;
+          step(j, (unsigned long long)h);
+          const cudaError_t le = cudaGetLastError();
+          e = cudaStreamEndCapture(c->stream, &body);
+          if (e == cudaSuccess) e = le;
+          prev = node;
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&c->sel_exec, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        graph = nullptr;
+        if (e != cudaSuccess) {                  // no conditional nodes here: plain graph below
+          cudaGetLastError();
+          c->sel_exec = nullptr;
+          c->cond_graph = 0;
+        }
       }
-      CK(cudaStreamEndCapture(c->stream, &graph));
-      const cudaError_t ie = cudaGraphInstantiate(&c->sel_exec, graph, 0);
-      cudaGraphDestroy(graph);
-      if (ie != cudaSuccess) return fail_cuda(c, "cudaGraphInstantiate", ie);
+      if (!c->sel_exec) {
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        for (uint32_t j = 0; j < kk; ++j) step(j, 0ull);
+        CK(cudaStreamEndCapture(c->stream, &graph));
+        const cudaError_t ie = cudaGraphInstantiate(&c->sel_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) return fail_cuda(c, "cudaGraphInstantiate", ie);
+      }
+      c->sel_cond = c->cond_graph != 0;
       c->sel_key = key;
     }
     Prof pf(c, CLS_SELECT);
+    c->sel_cond_used = c->sel_cond;
+    c->sel_per_step = cand ? 3 : 2;
     TRY(launched(c, cudaGraphLaunch(c->sel_exec, c->stream), "selection graph", (cand ? 3 : 2) * (int)kk));
   } else {
     for (uint32_t j = 0; j < kk; ++j) {
       {
         Prof pf(c, CLS_SELECT);
-        if (cand) TRY(launched(c, launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream),
+        if (cand) TRY(launched(c, launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream, ctl),
                                "k_argmax_cand"));
         TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * kArgmaxCtasPerSM,
-                                      c->stream, mr != nullptr), "k_argmax"));
-        TRY(launched(c, launch_cover(keys, (int)j, segd, nsegd, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
+                                      c->stream, mr != nullptr, 0u, ctl), "k_argmax"));
+        TRY(launched(c, launch_cover(keys, (int)j, segd, ctl, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                                      c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * kCoverCtasPerSM,
                                      c->stream, limited, mr), "k_cover"));
       }
@@ -1103,13 +1188,19 @@ gim_status select_finish(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gain
     c->sel_pending = false;
   }
   uint64_t cov = 0;
+  uint32_t steps = 0;                   // a step that ran has a nonzero key (k <= n: a pick exists)
+  const bool cond_used = c->sel_cond_used;
+  c->sel_cond_used = false;
   for (uint32_t j = 0; j < k * c->rounds; ++j) {
+    steps += c->h_keys[j] != 0ull;
     seeds[j] = ~(uint32_t)(c->h_keys[j] & 0xFFFFFFFFull);
     const uint64_t g = c->h_keys[j] >> 32;
     if (gains) gains[j] = g;
     cov += g;
   }
   if (covered) *covered = cov;
+  c->last_sel_steps = steps;
+  if (cond_used) c->st.launches -= (uint64_t)c->sel_per_step * (k * c->rounds - steps);   // skipped IF bodies
   c->st.selects++;
   return GIM_OK;
 }
@@ -1214,7 +1305,8 @@ void gim_destroy(gim_ctx* c) {
                     &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->spill, &c->lane_spill, &c->skip_tab, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
                     &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->thr_node, &c->ag_small,
-                    &c->ag_send, &c->ag_recv, &c->sel_bar, &c->rs_gcnt, &c->rs_dshard, &c->rs_keys, &c->rs_kx};
+                    &c->ag_send, &c->ag_recv, &c->sel_bar, &c->rs_gcnt, &c->rs_dshard, &c->rs_keys, &c->rs_kx,
+                    &c->sel_ctl, &c->cmap, &c->cdec, &c->sel_done, &c->probe};
   for (auto& sg : c->iseg) {
     dfree(c, sg.off);
     dfree(c, sg.inv);
@@ -1236,6 +1328,10 @@ void gim_destroy(gim_ctx* c) {
   cudaStreamDestroy(c->stream2);
   cudaEventDestroy(c->ev_cnt_copied);
   cudaEventDestroy(c->ev_sel_done);
+  // the default pool keeps freed memory (release threshold = max, set in gim_create): hand the
+  // unused part back so other processes on this GPU can use it
+  cudaMemPool_t mp;
+  if (cudaDeviceGetDefaultMemPool(&mp, c->device) == cudaSuccess) cudaMemPoolTrimTo(mp, 0);
   cudaGetLastError();
   delete c;
 }
@@ -1456,12 +1552,56 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
     // fails, capped by ceil(lambda*/x), the largest theta a passing test can produce
     const uint64_t spec = std::min<uint64_t>(
         (i < i_max) ? (uint64_t)std::ceil(K.lambda_p / (x / 2.0)) : 0ull, (uint64_t)std::ceil(K.lambda_s / x));
-    TRY(select_launch(c, k));                                 // l.6 (reading R9)
-    if (c->speculate && spec > R) TRY(generate_speculative(c, spec, seed));
-    TRY(select_finish(c, k, tmp.data(), nullptr, &cov));
+    // bounded greedy: the smallest covered count c* that passes l.7 in the same double
+    // arithmetic (the test is monotone in cov); a selection whose bound cov_j + (k - j) gain_j
+    // drops below c* stops there, and the test below then fails as it would after k steps
+    c->sel_cstar = 0;
+    if (c->imm_early_exit) {
+      auto passes = [&](uint64_t cv) { return (n * (double)cv) / (double)R >= (1.0 + K.eps_p) * x; };
+      uint64_t lo = 0, hi = R + 1;             // passes(hi) assumed; c* = R + 1 if nothing passes
+      while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (passes(mid)) hi = mid; else lo = mid + 1;
+      }
+      c->sel_cstar = lo;                       // >= 1 since R >= 1 (0 would disable the bound)
+    }
+    // probe: the first greedy pick is the argmax of count_total itself; when already
+    // k * gain_0 < c* the bounded greedy would stop at its first cover, so the round's result
+    // (one pick, cov = gain_0) is known without indexing the new sets or launching the
+    // selection — their index segment is built later, merged with the next rounds' sets
+    bool probed = false;
+    const bool global_counts = !(c->world > 1 || c->force_coll) || c->agfn;
+    if (c->sel_cstar && c->inv_pending && global_counts && !c->speculate) {
+      TRY(ensure(c, c->probe, 8));
+      CK(cudaMemsetAsync(c->probe.p, 0, 8, c->stream));
+      {
+        Prof pf(c, CLS_SELECT);
+        TRY(launched(c, launch_argmax(c->count_total.as<uint32_t>(), nullptr, (uint32_t)nsp(c),
+                                      c->probe.as<unsigned long long>(), 0, nullptr, c->num_sms * kArgmaxCtasPerSM,
+                                      c->stream, c->rounds > 1), "k_argmax(probe)"));
+      }
+      CK(cudaMemcpyAsync(c->h_u64, c->probe.p, 8, cudaMemcpyDeviceToHost, c->stream));
+      TRY(sync(c));
+      const uint64_t g0 = c->h_u64[0] >> 32;
+      if ((uint64_t)k * c->rounds * g0 < c->sel_cstar) {
+        probed = true;
+        cov = g0;
+        c->last_sel_steps = 1;
+        c->st.probe_stops++;
+      }
+    }
+    if (!probed) {
+      const gim_status sst = select_launch(c, k);             // l.6 (reading R9)
+      c->sel_cstar = 0;
+      TRY(sst);
+      if (c->speculate && spec > R) TRY(generate_speculative(c, spec, seed));
+      TRY(select_finish(c, k, tmp.data(), nullptr, &cov));
+    }
+    c->sel_cstar = 0;
     r.theta_i[i - 1] = T;
     r.theta_i_real[i - 1] = theta_i;
     r.cov_i[i - 1] = cov;
+    r.sel_steps_i[i - 1] = c->last_sel_steps;
     r.rounds = (uint32_t)i;
     if ((n * (double)cov) / (double)R >= (1.0 + K.eps_p) * x) {   // l.7 (reading R7)
       LB = (n * (double)cov) / (double)R / (1.0 + K.eps_p);       // l.8
@@ -1658,6 +1798,13 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
       return GIM_OK;
     }
     case GIM_OPT_SELECT_PERSISTENT: c->sel_persistent = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_IMM_EARLY_EXIT: c->imm_early_exit = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_INV_PASSES: c->inv_passes = (value < 0 || value > 64) ? 0 : (int)value; return GIM_OK;
+    case GIM_OPT_COND_GRAPH:
+      c->cond_graph = value ? 1 : 0;
+      if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);   // recapture in the new form
+      c->sel_exec = nullptr;
+      return GIM_OK;
     case GIM_OPT_GIANT_NT:
       if (value != 0 && value != kGiantThreads && value != kGiantThreadsNarrow)
         return fail(c, GIM_EINVAL, "giant CTA width must be 0 (auto), 256 or 128");

@@ -45,15 +45,17 @@ cudaError_t launch_scan_u32(const uint32_t* in, uint64_t count, uint64_t* out, u
 cudaError_t launch_scan_u32_to32(const uint32_t* in, uint64_t count, uint32_t* out, uint64_t* tile_tmp,
                                  uint64_t* total_tmp, cudaStream_t s, int* launches);
 cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, uint32_t set0, uint32_t set1,
-                               uint32_t* end, uint32_t* inv, int grid, cudaStream_t s);
+                               uint32_t* end, uint32_t* inv, int grid, cudaStream_t s, uint32_t n, int passes,
+                               int* launches);
 struct InvSegDev;
 cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, uint32_t limit, InvSegDev* out,
                             uint32_t* nseg_out, cudaStream_t s);
 cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* delta, uint32_t n, int grid,
                                cudaStream_t s);
+struct SelCtl;
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
                           const uint32_t* tau_p1, int grid, cudaStream_t s, bool excl = false,
-                          uint32_t id_base = 0);
+                          uint32_t id_base = 0, const SelCtl* ctl = nullptr);
 // node-sharded selection (gim_set_reducescatter): key exchange pack / global pick
 cudaError_t launch_rs_pack(const unsigned long long* local_keys, int j, uint32_t rank, uint32_t world,
                            unsigned long long* kx, cudaStream_t s);
@@ -62,8 +64,18 @@ cudaError_t launch_rs_pick(const unsigned long long* kx, uint32_t world, unsigne
 cudaError_t launch_cand_setup(const uint32_t* cnt, uint32_t n, uint32_t kmax, unsigned int* hist,
                               uint32_t* tau_p1, uint32_t* cand, unsigned int* ncand, int grid, cudaStream_t s);
 cudaError_t launch_argmax_cand(const uint32_t* cnt, const uint32_t* cand, const unsigned int* ncand,
-                               unsigned long long* keys, int j, int grid, cudaStream_t s);
+                               unsigned long long* keys, int j, int grid, cudaStream_t s,
+                               const SelCtl* ctl = nullptr);
 struct InvSegDev;
+// Bounded greedy of an IMM estimation round (gim_imm): cstar = the
+// smallest covered count that passes the round's test (Alg. 2 l.7); 0 disables. stop is set by
+// the cover of the first step whose bound cov_j + (kk - j) * gain_j falls below cstar, and every
+// later argmax / cover of the selection returns at once.
+struct SelCtl {
+  unsigned long long cstar;
+  uint32_t stop, kk;
+};
+cudaError_t launch_sel_ctl(SelCtl* ctl, unsigned long long cstar, uint32_t kk, cudaStream_t s);
 // MRIM selection (R27): pair ids t*n + u over `rounds` rounds, at most k picks per round
 struct MrimSel {
   uint32_t rounds, n, k;
@@ -72,10 +84,10 @@ cudaError_t launch_select_persistent(uint32_t* cnt, uint32_t n, unsigned long lo
                                      const InvSegDev* segs, const uint64_t* offsets, const uint32_t* pool,
                                      uint8_t* covered, const MrimSel* mr, bool limit, unsigned int* bar,
                                      int num_sms, cudaStream_t s);
-cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,
+cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, SelCtl* ctl,
                          const uint64_t* offsets, const uint32_t* pool,
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s,
-                         bool limit, const MrimSel* mr = nullptr);
+                         bool limit, const MrimSel* mr = nullptr, unsigned long long cond = 0ull);
 // fused greedy steps (P = 1): candidate argmax of step 0, then per step cover + next argmax
 cudaError_t launch_select_fused(unsigned long long* keys, int kk, const InvSegDev* segs, const uint64_t* offsets,
                                 const uint32_t* pool, uint8_t* covered, uint32_t* cnt, const uint32_t* cand,

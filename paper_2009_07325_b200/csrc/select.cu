@@ -122,13 +122,16 @@ __device__ __forceinline__ uint32_t warp_excl_scan_u32(uint32_t x, int lane, uin
 // ------------------------------------------------------------------------------------------
 // K-INV scatter: inv[inv_off[v] + cursor[v]++] = local set index r, for every member v of r.
 // A warp takes 32 consecutive sets (contiguous in the pool) and sweeps their members 32 at a
-// time; the owning set of a member is found with a 5-step shuffle search.
+// time; the owning set of a member is found with a 5-step shuffle search. Only members in the
+// node range [vlo, vlo + vspan) are scattered: when the cursor array is larger than the L2
+// (C5: 166 MB), the host runs one pass per node range so the cursor atomics and the inv writes
+// of a pass stay L2-resident instead of each being a random DRAM read-modify-write.
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_inv_scatter(const uint64_t* __restrict__ offsets,
                                                      const uint32_t* __restrict__ pool, uint32_t set0,
                                                      uint32_t nsets_end,
                                                      uint32_t* __restrict__ end,
-                                                     uint32_t* __restrict__ inv) {
+                                                     uint32_t* __restrict__ inv, uint32_t vlo, uint32_t vspan) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
   const uint32_t nsets = nsets_end;
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__(256) k_inv_scatter(const uint64_t* __restrict_
       const uint32_t k = warp_owner(P, i);
       if (i < hi_rel) {
         const uint32_t v = pool[base + i];
-        inv[atomicAdd(end + v, 1u)] = r0 + k;     // end[v]: start of v's list, advanced to its end
+        if (v - vlo < vspan) inv[atomicAdd(end + v, 1u)] = r0 + k;   // end[v]: list start, advanced to its end
       }
     }
   }
@@ -182,7 +185,8 @@ __device__ __forceinline__ void argmax_one(uint32_t c, uint32_t v, unsigned long
 __device__ __forceinline__ void argmax_step(uint32_t* __restrict__ cnt, int32_t* __restrict__ dec,
                                             uint32_t n, unsigned long long* __restrict__ keys, int j,
                                             const uint32_t* __restrict__ tau_p1, uint32_t excl,
-                                            uint32_t id_base = 0) {
+                                            uint32_t id_base = 0, const SelCtl* ctl = nullptr) {
+  if (ctl != nullptr && *(volatile const uint32_t*)&ctl->stop) return;   // bounded greedy stopped
   // candidate mode: the candidate argmax already found a count >= tau_p1, which no node outside
   // the candidate list can reach (their counts started below it and only decrease)
   if (tau_p1 != nullptr && (uint32_t)(keys[j] >> 32) >= *tau_p1 && keys[j] != 0ull) return;
@@ -252,10 +256,10 @@ __device__ __forceinline__ void argmax_step(uint32_t* __restrict__ cnt, int32_t*
 __global__ void __launch_bounds__(256) k_argmax(uint32_t* __restrict__ cnt, int32_t* __restrict__ dec,
                                                 uint32_t n, unsigned long long* __restrict__ keys, int j,
                                                 const uint32_t* __restrict__ tau_p1, uint32_t excl,
-                                                uint32_t id_base) {
+                                                uint32_t id_base, const SelCtl* ctl) {
   pdl_wait();
   pdl_trigger();
-  argmax_step(cnt, dec, n, keys, j, tau_p1, excl, id_base);
+  argmax_step(cnt, dec, n, keys, j, tau_p1, excl, id_base, ctl);
 }
 
 // Node-sharded selection (include/gim.h gim_set_reducescatter): this rank's best key of step j
@@ -384,10 +388,12 @@ __global__ void __launch_bounds__(256) k_cand_compact(const uint32_t* __restrict
 __global__ void __launch_bounds__(256) k_argmax_cand(const uint32_t* __restrict__ cnt,
                                                      const uint32_t* __restrict__ cand,
                                                      const unsigned int* __restrict__ ncand,
-                                                     unsigned long long* __restrict__ keys, int j) {
+                                                     unsigned long long* __restrict__ keys, int j,
+                                                     const SelCtl* ctl) {
   __shared__ unsigned long long s_best[8];
   pdl_wait();
   pdl_trigger();
+  if (ctl != nullptr && *(volatile const uint32_t*)&ctl->stop) return;
   const uint32_t nc = *ncand;
   unsigned long long best = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
@@ -432,11 +438,29 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
                                            uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
                                            int32_t* __restrict__ dec, MrimSel mr,
                                            uint32_t u_known = kEmpty, const uint32_t* __restrict__ cmap = nullptr,
-                                           int32_t* __restrict__ cdec = nullptr) {
+                                           int32_t* __restrict__ cdec = nullptr, SelCtl* ctl = nullptr,
+                                           unsigned long long cond = 0ull) {
   __shared__ uint64_t s_lo[kMaxInvSeg], s_end[kMaxInvSeg];   // list start, inclusive prefix end
   __shared__ const uint32_t* s_inv[kMaxInvSeg];
-  __shared__ uint32_t s_nseg, s_limit;
+  __shared__ uint32_t s_nseg, s_limit, s_stop;
   const uint32_t sub = threadIdx.x & 7;
+  // bounded greedy (IMM estimation rounds, SelCtl): gains never increase, so after the argmax of
+  // step j the final covered count is at most cov_j + (kk - j) * gain_j with cov_j = the gains of
+  // steps < j. Below cstar the round's test (Alg. 2 l.7) fails whatever the remaining steps pick:
+  // the selection stops here (every CTA evaluates the same bound from the same keys).
+  uint32_t stop_now = 0;
+  if (ctl != nullptr) {
+    if (*(volatile const uint32_t*)&ctl->stop) return;
+    const unsigned long long cstar = ctl->cstar;
+    if (cstar != 0ull && threadIdx.x < 32) {
+      unsigned long long sum = 0;
+      for (int t = (int)threadIdx.x; t < j; t += 32) sum += keys[t] >> 32;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(kFull, sum, off);
+      const unsigned long long bound = sum + (unsigned long long)(ctl->kk - (uint32_t)j) * (keys[j] >> 32);
+      stop_now = bound < cstar ? 1u : 0u;
+    }
+  }
   // u_known: the pick computed by this CTA itself (cooperative selection; the pick is excluded
   // from later argmaxes there, not retired in cnt, which other CTAs may still be reading)
   const uint32_t u = u_known != kEmpty ? u_known : ~(uint32_t)keys[j];
@@ -467,6 +491,12 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
     if (l == 0) {
       s_nseg = __popc(used);
       s_limit = lim;
+      s_stop = stop_now;
+      if (stop_now && blockIdx.x == 0) {
+        ctl->stop = 1u;
+        // graph replay: the remaining steps are IF nodes on this handle and are skipped whole
+        if (cond != 0ull) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, 0u);
+      }
     }
   }
   // MRIM (R27): the pick that gives round t = u / n its k-th seed closes the round: every pair of
@@ -482,6 +512,7 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
     if (threadIdx.x == 0) s_close = picks == mr.k ? 1u : 0u;
   }
   __syncthreads();
+  if (s_stop) return;
   if (mr.rounds > 1u && s_close) {
     const uint32_t t = u / mr.n;
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < mr.n; v += gridDim.x * blockDim.x)
@@ -531,15 +562,14 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
 
 template <bool LIMIT>
 __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restrict__ keys, int j,
-                                               const InvSegDev* __restrict__ segs,
-                                               const uint32_t* __restrict__ nseg_ptr_unused,
+                                               const InvSegDev* __restrict__ segs, SelCtl* ctl,
                                                const uint64_t* __restrict__ offsets,
                                                const uint32_t* __restrict__ pool,
                                                uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
-                                               int32_t* __restrict__ dec, MrimSel mr) {
+                                               int32_t* __restrict__ dec, MrimSel mr, unsigned long long cond) {
   pdl_wait();
   pdl_trigger();
-  cover_step<LIMIT>(keys, j, segs, offsets, pool, covered, cnt, dec, mr);
+  cover_step<LIMIT>(keys, j, segs, offsets, pool, covered, cnt, dec, mr, kEmpty, nullptr, nullptr, ctl, cond);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -788,8 +818,17 @@ cudaError_t launch_scan_u32_to32(const uint32_t* in, uint64_t count, uint32_t* o
 }
 
 cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, uint32_t set0, uint32_t set1,
-                               uint32_t* end, uint32_t* inv, int grid, cudaStream_t s) {
-  k_inv_scatter<<<grid, 256, 0, s>>>(offsets, pool, set0, set1, end, inv);
+                               uint32_t* end, uint32_t* inv, int grid, cudaStream_t s, uint32_t n, int passes,
+                               int* launches) {
+  const uint32_t span = (uint32_t)(((uint64_t)n + passes - 1) / passes);
+  *launches = 0;
+  for (int q = 0; q < passes; ++q) {
+    const uint32_t lo = (uint32_t)std::min<uint64_t>((uint64_t)q * span, n);
+    const uint32_t len = (uint32_t)std::min<uint64_t>(span, (uint64_t)n - lo);
+    if (len == 0) break;
+    k_inv_scatter<<<grid, 256, 0, s>>>(offsets, pool, set0, set1, end, inv, lo, len);
+    ++*launches;
+  }
   return cudaGetLastError();
 }
 
@@ -839,8 +878,19 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t
 }
 
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
-                          const uint32_t* tau_p1, int grid, cudaStream_t s, bool excl, uint32_t id_base) {
-  return launch_pdl(k_argmax, grid, 256, s, cnt, dec, n, keys, j, tau_p1, excl ? 0x80000000u : 0u, id_base);
+                          const uint32_t* tau_p1, int grid, cudaStream_t s, bool excl, uint32_t id_base,
+                          const SelCtl* ctl) {
+  return launch_pdl(k_argmax, grid, 256, s, cnt, dec, n, keys, j, tau_p1, excl ? 0x80000000u : 0u, id_base, ctl);
+}
+
+__global__ void k_sel_ctl(SelCtl* ctl, unsigned long long cstar, uint32_t kk) {
+  ctl->cstar = cstar;
+  ctl->stop = 0u;
+  ctl->kk = kk;
+}
+cudaError_t launch_sel_ctl(SelCtl* ctl, unsigned long long cstar, uint32_t kk, cudaStream_t s) {
+  k_sel_ctl<<<1, 1, 0, s>>>(ctl, cstar, kk);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_rs_pack(const unsigned long long* local_keys, int j, uint32_t rank, uint32_t world,
@@ -865,8 +915,8 @@ cudaError_t launch_cand_setup(const uint32_t* cnt, uint32_t n, uint32_t kmax, un
 }
 
 cudaError_t launch_argmax_cand(const uint32_t* cnt, const uint32_t* cand, const unsigned int* ncand,
-                               unsigned long long* keys, int j, int grid, cudaStream_t s) {
-  return launch_pdl(k_argmax_cand, grid, 256, s, cnt, cand, ncand, keys, j);
+                               unsigned long long* keys, int j, int grid, cudaStream_t s, const SelCtl* ctl) {
+  return launch_pdl(k_argmax_cand, grid, 256, s, cnt, cand, ncand, keys, j, ctl);
 }
 
 cudaError_t launch_select_persistent(uint32_t* cnt, uint32_t n, unsigned long long* keys, int kk,
@@ -930,13 +980,13 @@ cudaError_t launch_select_coop(const uint32_t* cnt, const uint32_t* cand, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, const uint32_t* nseg,
+cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, SelCtl* ctl,
                          const uint64_t* offsets, const uint32_t* pool,
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s, bool limit,
-                         const MrimSel* mr) {
+                         const MrimSel* mr, unsigned long long cond) {
   const MrimSel m = mr ? *mr : MrimSel{1u, 0u, 0u};
-  if (limit) return launch_pdl(k_cover<true>, grid, 256, s, keys, j, segs, nseg, offsets, pool, covered, cnt, dec, m);
-  return launch_pdl(k_cover<false>, grid, 256, s, keys, j, segs, nseg, offsets, pool, covered, cnt, dec, m);
+  if (limit) return launch_pdl(k_cover<true>, grid, 256, s, keys, j, segs, ctl, offsets, pool, covered, cnt, dec, m, cond);
+  return launch_pdl(k_cover<false>, grid, 256, s, keys, j, segs, ctl, offsets, pool, covered, cnt, dec, m, cond);
 }
 
 }  // namespace gim

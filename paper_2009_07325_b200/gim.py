@@ -24,7 +24,7 @@ LIB_PATH = os.environ.get("GIM_LIB_PATH") or os.path.join(_HERE, "libgim.so")
 GIM_OK, GIM_EINVAL, GIM_ESTATE, GIM_ENOMEM, GIM_ECUDA, GIM_ECOLL, GIM_ELTWEIGHT = range(7)
 IC, LT = 0, 1
 W_EXPLICIT, W_WC, W_UNIFORM = 0, 1, 2
-OPT_FORCE_GIANT, OPT_QUEUE_CAP, OPT_PROFILE, OPT_STAGING_CAP, OPT_SELECT_GRAPH, OPT_INV_SEGMENTS, OPT_ARGMAX_CAND, OPT_IC_LANE, OPT_SPECULATE, OPT_MB_CHAINS, OPT_PDL, OPT_GIANT_NT, OPT_FRESH_FINAL, OPT_SELECT_PERSISTENT, OPT_SKIP, OPT_SPILL, OPT_SELECT_FUSED, OPT_FUSED_CTAS, OPT_FORCE_COLLECTIVES, OPT_GIANT_SHARED, OPT_SKIP_LANE_CAP, OPT_SELECT_COOP = 1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23
+OPT_FORCE_GIANT, OPT_QUEUE_CAP, OPT_PROFILE, OPT_STAGING_CAP, OPT_SELECT_GRAPH, OPT_INV_SEGMENTS, OPT_ARGMAX_CAND, OPT_IC_LANE, OPT_SPECULATE, OPT_MB_CHAINS, OPT_PDL, OPT_GIANT_NT, OPT_FRESH_FINAL, OPT_SELECT_PERSISTENT, OPT_SKIP, OPT_SPILL, OPT_SELECT_FUSED, OPT_FUSED_CTAS, OPT_FORCE_COLLECTIVES, OPT_GIANT_SHARED, OPT_SKIP_LANE_CAP, OPT_SELECT_COOP, OPT_IMM_EARLY_EXIT, OPT_COND_GRAPH, OPT_INV_PASSES = 1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23, 24, 25, 26
 
 _STATUS = {0: "GIM_OK", 1: "GIM_EINVAL", 2: "GIM_ESTATE", 3: "GIM_ENOMEM", 4: "GIM_ECUDA",
            5: "GIM_ECOLL", 6: "GIM_ELTWEIGHT"}
@@ -43,7 +43,7 @@ class ImmResultC(ctypes.Structure):
     _fields_ = [("ell_eff", _dbl), ("eps_prime", _dbl), ("lambda_prime", _dbl),
                 ("lambda_star", _dbl), ("LB", _dbl), ("theta", _dbl), ("rounds", _u32),
                 ("theta_i", _u64 * 64), ("cov_i", _u64 * 64), ("theta_i_real", _dbl * 64),
-                ("R_final", _u64), ("covered", _u64), ("spread_est", _dbl)]
+                ("R_final", _u64), ("covered", _u64), ("spread_est", _dbl), ("sel_steps_i", _u32 * 64)]
 
 
 class StatsC(ctypes.Structure):
@@ -53,7 +53,8 @@ class StatsC(ctypes.Structure):
                 ("allreduces", _u64), ("ms_rr", _dbl), ("ms_giant", _dbl), ("ms_store", _dbl),
                 ("ms_inv", _dbl), ("ms_select", _dbl), ("n_rr_launches", _u64),
                 ("n_giant_launches", _u64), ("n_syncs", _u64), ("n_allocs", _u64),
-                ("host_ms_sync", _dbl), ("host_ms_api", _dbl), ("fused_fallbacks", _u64)]
+                ("host_ms_sync", _dbl), ("host_ms_api", _dbl), ("fused_fallbacks", _u64),
+                ("probe_stops", _u64)]
 
 
 # name -> (restype, argtypes); exactly the functions declared in include/gim.h
@@ -119,6 +120,7 @@ class ImmResult:
     R_final: int
     covered: int
     spread_est: float
+    sel_steps_i: np.ndarray = None   # greedy steps run per round (< k: bounded-greedy early exit)
 
 
 def _ptr(a: Optional[np.ndarray]):
@@ -243,7 +245,8 @@ class Gim:
                          theta=r.theta, rounds=nr, theta_i=np.array(r.theta_i[:nr], dtype=np.uint64),
                          theta_i_real=np.array(r.theta_i_real[:nr]),
                          cov_i=np.array(r.cov_i[:nr], dtype=np.uint64), R_final=int(r.R_final),
-                         covered=int(r.covered), spread_est=r.spread_est)
+                         covered=int(r.covered), spread_est=r.spread_est,
+                         sel_steps_i=np.array(r.sel_steps_i[:nr], dtype=np.uint32))
 
     def rr_export(self, sort_each_set: bool = True):
         ns, pl = _u64(), _u64()

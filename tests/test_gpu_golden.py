@@ -16,6 +16,7 @@ import numpy as np
 import pytest
 
 import gim_inputs as gi
+from tests.imm_trace import check_cov_trace
 
 pytestmark = pytest.mark.gpu
 
@@ -35,8 +36,11 @@ def _rel(a, b):
     return abs(a - b) <= 1e-12 * max(abs(b), 1e-300)
 
 
-@pytest.mark.parametrize("key", ["C1", "C2", "C3", "C4", "C5"])
-def test_imm_golden(key):
+@pytest.mark.parametrize("key,early", [("C1", 1), ("C2", 1), ("C3", 1), ("C4", 1), ("C5", 1),
+                                       ("C1", 0), ("C3", 0)])
+def test_imm_golden(key, early):
+    """early = 1: the default bounded greedy in the estimation rounds (stopped rounds checked by
+    tests/imm_trace.py); early = 0: every round's k steps, cov_i exactly as the oracle's."""
     gd = json.load(open(os.path.join(GOLDEN, f"imm_{key}.json")))
     w = gi.WORKLOADS[key]
     g = gi.workload_graph(key)
@@ -44,11 +48,15 @@ def test_imm_golden(key):
     c = P.Gim(0)
     try:
         c.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme, p_uniform=w.p_uniform)
+        c.set_option(P.OPT_IMM_EARLY_EXIT, early)
         r = c.imm(w.k, w.eps, w.ell, w.rr_seed)
         assert _rel(r.ell_eff, gd["ell_eff"]) and _rel(r.eps_prime, gd["eps_prime"])
         assert _rel(r.lambda_prime, gd["lambda_prime"]) and _rel(r.lambda_star, gd["lambda_star"])
         assert r.rounds == gd["rounds"]
-        assert r.theta_i.tolist() == gd["T_i"] and r.cov_i.tolist() == gd["cov_i"]
+        assert r.theta_i.tolist() == gd["T_i"]
+        stopped = check_cov_trace(r, gd["T_i"], gd["cov_i"], g.n, gd["eps_prime"], w.k)
+        if not early:
+            assert stopped == 0 and r.cov_i.tolist() == gd["cov_i"]
         assert all(_rel(a, b) for a, b in zip(r.theta_i_real.tolist(), gd["theta_i"]))
         assert _rel(r.LB, gd["LB"]) and _rel(r.theta, gd["theta"])
         assert r.R_final == gd["R_final"] and r.covered == gd["cov"]

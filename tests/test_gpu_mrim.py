@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import gim_inputs as gi
+from tests.imm_trace import check_cov_trace, oracle_round_gains
 import oracle
 from tests.test_gpu_parity import _ctx, _variants
 
@@ -117,7 +118,9 @@ def test_mrim_imm_parity(key, model, k, T, eps):
     ro = o.mrim(k, T, eps, w.ell, w.rr_seed)
     rel = lambda a, b: abs(a - b) <= 1e-12 * max(abs(b), 1e-300)
     assert rel(r.lambda_prime, ro.lambda_prime) and rel(r.lambda_star, ro.lambda_star)
-    assert r.rounds == ro.rounds and np.array_equal(r.theta_i, ro.T_i) and np.array_equal(r.cov_i, ro.cov_i)
+    assert r.rounds == ro.rounds and np.array_equal(r.theta_i, ro.T_i)
+    check_cov_trace(r, ro.T_i, ro.cov_i, g.n, ro.eps_prime, k * T,
+                    oracle_round_gains(oracle.Oracle(g, model, w.scheme), ro.T_i, k, w.rr_seed, mrim_T=T))
     assert rel(r.LB, ro.LB) and rel(r.theta, ro.theta)
     assert r.R_final == ro.R_final and r.covered == ro.cov
     assert np.array_equal(r.seeds, ro.seeds), (r.seeds, ro.seeds)

@@ -60,6 +60,9 @@ def test_multiprocess_vs_oracle(world, proto):
     ooff, onodes, _ = o.export()
     oseeds, ogains, ocov = o.select(k)
     oimm = oracle.Oracle(g, w.model, w.scheme).imm(k, w.eps, w.ell, w.rr_seed)
+    import torch
+    if torch.cuda.is_initialized():          # cached memory of earlier tests back to the device
+        torch.cuda.empty_cache()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()

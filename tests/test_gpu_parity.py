@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 import gim_inputs as gi
+from tests.imm_trace import check_cov_trace, oracle_round_gains
 import oracle
 
 pytestmark = pytest.mark.gpu
@@ -109,15 +110,20 @@ def test_pool_parity_C1_invariance(opts):
         assert c.stats()["giant_sets"] == T
 
 
-@pytest.mark.parametrize("graph,segs,cand", [(1, 1, 1), (0, 1, 2), (1, 0, 1), (1, 1, 0), (1, 1, 2)])
-def test_pool_parity_C2_and_select(graph, segs, cand):
-    """k = 50 selection through the argmax/cover launches replayed from a CUDA graph (default)
-    and launched one by one; pool generated in several calls (several index segments)."""
+@pytest.mark.parametrize("graph,segs,cand,extra", [
+    (1, 1, 1, {}), (0, 1, 2, {}), (1, 0, 1, {}), (1, 1, 0, {}), (1, 1, 2, {}),
+    (1, 1, 1, {"OPT_INV_PASSES": 7}), (1, 0, 2, {"OPT_INV_PASSES": 3, "OPT_COND_GRAPH": 0}),
+    (0, 1, 1, {"OPT_INV_PASSES": 64}), (1, 1, 0, {"OPT_COND_GRAPH": 0})])
+def test_pool_parity_C2_and_select(graph, segs, cand, extra):
+    """k = 50 selection through the argmax/cover launches replayed from a CUDA graph (default:
+    one conditional IF node per step; or a plain graph) and launched one by one; pool generated
+    in several calls (several index segments), index scattered in 1..64 node-range passes."""
     w = gi.WORKLOADS["C2"]
     g = gi.workload_graph("C2")
     T = 30011
-    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_GRAPH: graph, P.OPT_INV_SEGMENTS: segs,
-                                         P.OPT_ARGMAX_CAND: cand})
+    opts = {P.OPT_SELECT_GRAPH: graph, P.OPT_INV_SEGMENTS: segs, P.OPT_ARGMAX_CAND: cand}
+    opts.update({getattr(P, k): v for k, v in extra.items()})
+    c = _ctx(g, w.model, w.scheme, opts=opts)
     for t in (1000, 7000, 7001, 20000):
         c.generate_rr(t, w.rr_seed)
     c.generate_rr(T, w.rr_seed)
@@ -224,7 +230,9 @@ def _imm_parity(key, k=None, eps=None):
     assert rel(r.ell_eff, ro.ell_eff) and rel(r.eps_prime, ro.eps_prime)
     assert r.rounds == ro.rounds
     assert all(rel(a, b) for a, b in zip(r.theta_i_real, ro.theta_i))
-    assert np.array_equal(r.theta_i, ro.T_i) and np.array_equal(r.cov_i, ro.cov_i)
+    assert np.array_equal(r.theta_i, ro.T_i)
+    check_cov_trace(r, ro.T_i, ro.cov_i, g.n, ro.eps_prime, k,
+                    oracle_round_gains(oracle.Oracle(g, w.model, w.scheme, w.p_uniform), ro.T_i, k, w.rr_seed))
     assert rel(r.LB, ro.LB) and rel(r.theta, ro.theta)
     assert r.R_final == ro.R_final and r.covered == ro.cov
     assert np.array_equal(r.seeds, ro.seeds), (r.seeds, ro.seeds)
@@ -258,7 +266,9 @@ def test_imm_parity_BA_small():
     c = _ctx(g, gi.IC, gi.W_WC)
     r = c.imm(20, 0.3, 1.0, 5)
     ro = oracle.Oracle(g, gi.IC, gi.W_WC).imm(20, 0.3, 1.0, 5)
-    assert r.rounds == ro.rounds and np.array_equal(r.theta_i, ro.T_i) and np.array_equal(r.cov_i, ro.cov_i)
+    assert r.rounds == ro.rounds and np.array_equal(r.theta_i, ro.T_i)
+    check_cov_trace(r, ro.T_i, ro.cov_i, g.n, ro.eps_prime, 20,
+                    oracle_round_gains(oracle.Oracle(g, gi.IC, gi.W_WC), ro.T_i, 20, 5))
     assert r.R_final == ro.R_final and r.covered == ro.cov
     assert np.array_equal(r.seeds, ro.seeds), (r.seeds, ro.seeds)
 
@@ -342,7 +352,10 @@ def test_imm_fresh_final_parity(key, rounds):
         ro = o.imm(k, w.eps, w.ell, w.rr_seed)
     r = c.imm(k, w.eps, w.ell, w.rr_seed)
     rel = lambda a, b: abs(a - b) <= 1e-12 * max(abs(b), 1e-300)
-    assert r.rounds == ro.rounds and np.array_equal(r.theta_i, ro.T_i) and np.array_equal(r.cov_i, ro.cov_i)
+    assert r.rounds == ro.rounds and np.array_equal(r.theta_i, ro.T_i)
+    o2 = oracle.Oracle(g, w.model, w.scheme)
+    check_cov_trace(r, ro.T_i, ro.cov_i, g.n, ro.eps_prime, k * rounds,
+                    oracle_round_gains(o2, ro.T_i, k, w.rr_seed, mrim_T=rounds if rounds > 1 else None))
     assert rel(r.LB, ro.LB) and rel(r.theta, ro.theta)
     assert r.R_final == ro.R_final == math.ceil(ro.theta) and r.covered == ro.cov
     assert np.array_equal(r.seeds, ro.seeds)
@@ -451,5 +464,6 @@ def test_coop_selection_imm_golden(key):
     g = gi.workload_graph(key)
     c = _ctx(g, w.model, w.scheme, w.p_uniform, {P.OPT_SELECT_COOP: 4096})
     r = c.imm(w.k, w.eps, w.ell, w.rr_seed)
-    assert r.seeds.tolist() == gd["seeds"] and r.cov_i.tolist() == gd["cov_i"] and r.R_final == gd["R_final"]
+    assert r.seeds.tolist() == gd["seeds"] and r.R_final == gd["R_final"]
+    check_cov_trace(r, gd["T_i"], gd["cov_i"], g.n, gd["eps_prime"], w.k)
     c.close()

@@ -289,7 +289,9 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                         (falls back to the plain graph where conditional nodes are refused).
  *  GIM_OPT_INV_PASSES   = P (0 = auto: one pass per 32 MB of per-node cursors, 1..64): the
  *                         inverted-index scatter runs P node-range passes over the new sets so
- *                         each pass's cursor atomics stay in the L2 (results identical). */
+ *                         each pass's cursor atomics stay in the L2 (results identical).
+ *  GIM_OPT_L2_PERSIST   = 1 (default) / 0: an L2 persisting access-policy window on the library
+ *                         stream over the row pointers (+ WC thresholds), read at every BFS level. */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -315,7 +317,8 @@ typedef enum {
   GIM_OPT_SELECT_COOP = 23,
   GIM_OPT_IMM_EARLY_EXIT = 24,
   GIM_OPT_COND_GRAPH = 25,
-  GIM_OPT_INV_PASSES = 26
+  GIM_OPT_INV_PASSES = 26,
+  GIM_OPT_L2_PERSIST = 27
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 
@@ -340,6 +343,8 @@ typedef struct {
   double host_ms_api;           /* host wall time inside gim_generate_rr/select/imm       */
   uint64_t fused_fallbacks;     /* fused selections redone unfused (uncertified argmax)   */
   uint64_t probe_stops;         /* gim_imm rounds settled by the first-step probe alone   */
+  uint64_t cond_graph;          /* selection graph form: 1 = IF node per step, 0 = none yet,
+                                   2 + the failing stage * 1000 + cudaError = plain-graph fallback */
 } gim_stats;
 gim_status gim_get_stats(gim_ctx* ctx, gim_stats* out);
 gim_status gim_reset_stats(gim_ctx* ctx);

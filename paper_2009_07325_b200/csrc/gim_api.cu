@@ -64,7 +64,9 @@ struct gim_ctx {
   int model = 0, scheme = 0;
   float p_uniform = 0.f;
   uint64_t thr_uniform = 0;
-  DevBuf row_ptr, src, thr_edge, thr_node;
+  DevBuf row_ptr, src, thr_edge;   // row_ptr holds [n + 1] row pointers, then (WC) [n + 1] thresholds
+  uint32_t* thr_node = nullptr;     // WC threshold per node: row_ptr + n + 1 (one L2 window covers both)
+  int l2_persist = 1;               // GIM_OPT_L2_PERSIST
   DevBuf out_ptr, out_dst, out_in, thr_wc;   // out-CSR for gim_mc_spread (built on first use)
   bool out_valid = false;
   // MRIM (readings R26-R28): rounds T; pair ids t*n + u index the count / index / selection
@@ -143,9 +145,10 @@ struct gim_ctx {
   DevBuf cmap, cdec;            // cooperative selection: node -> candidate index (kEmpty), decrement rings
   DevBuf sel_ctl;               // SelCtl of the bounded greedy (IMM estimation rounds)
   DevBuf probe;                 // first-step argmax key of gim_imm's probe
+  DevBuf cond_handles;          // IF-node handles of the conditional selection graph (one per step)
   uint64_t sel_cstar = 0;       // smallest passing covered count of the running round (0 = off)
   uint32_t last_sel_steps = 0;  // greedy steps the last selection ran
-  int cond_graph = 1;           // selection graph as IF nodes per step (0: unsupported / off)
+  int cond_graph = 0;           // GIM_OPT_COND_GRAPH: selection graph as IF nodes per step (measured slower)
   int inv_passes = 0;           // GIM_OPT_INV_PASSES: node-range passes of the index scatter (0 = auto)
   bool sel_cond_used = false;   // the pending selection replays a conditional graph
   int sel_per_step = 2;         // kernels per greedy step of the pending graph replay
@@ -413,12 +416,37 @@ gim_status ensure_giant_slots(gim_ctx* c, uint32_t want) {
   return GIM_OK;
 }
 
+// L2 persisting window over the row pointers (+ WC thresholds): every BFS level of every RR set
+// starts with these loads, on the critical path of deep sets; src (read only for live edges) and
+// the pool stream through the rest of the L2. Window and set-aside capped by the device limits;
+// hitRatio scales down when the rows exceed the set-aside (C5: 333 MB).
+void set_l2_window(gim_ctx* c) {
+  cudaStreamAttrValue v{};
+  if (c->l2_persist && c->graph) {
+    int max_win = 0, max_persist = 0;
+    cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device);
+    const size_t bytes = std::min<size_t>(c->row_ptr.bytes, (size_t)std::max(max_win, 0));
+    if (bytes > 0 && max_persist > 0) {
+      const size_t persist = std::min<size_t>(bytes, (size_t)max_persist);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist);
+      v.accessPolicyWindow.base_ptr = c->row_ptr.p;
+      v.accessPolicyWindow.num_bytes = bytes;
+      v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)persist / (double)bytes);
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    }
+  }
+  cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v);   // num_bytes 0: off
+  cudaGetLastError();
+}
+
 RRParams base_params(gim_ctx* c) {
   RRParams p{};
   p.n = c->n;
   p.row_ptr = c->row_ptr.as<uint32_t>();
   p.src = c->src.as<uint32_t>();
-  p.thr_node = c->thr_node.as<uint32_t>();
+  p.thr_node = c->thr_node;
   p.thr_edge = c->thr_edge.as<uint64_t>();
   p.thr_uniform = c->thr_uniform;
   p.p_uniform = c->p_uniform;
@@ -1080,7 +1108,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
                                         (uintptr_t)c->offsets.p, (uintptr_t)c->pool.p, (uintptr_t)c->covered.p,
                                         (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n, (uintptr_t)limited,
                                         (uintptr_t)c->rounds, (uintptr_t)ctl};
-    auto step = [&](uint32_t j, unsigned long long h) {
+    auto step = [&](uint32_t j, const unsigned long long* h) {
       if (cand) launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream, ctl);
       launch_argmax(c->cnt.as<uint32_t>(), nullptr, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * kArgmaxCtasPerSM, c->stream,
                     mr != nullptr, 0u, ctl);
@@ -1096,40 +1124,60 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
       if (c->cond_graph) {
         // one IF node per greedy step on one handle (reset to 1 at every replay): the cover that
         // stops a bounded greedy clears it and the graph skips the remaining steps itself
+        int stage = 1;
         cudaError_t e = cudaGraphCreate(&graph, 0);
-        cudaGraphConditionalHandle h = 0;
-        if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, graph, 1u, cudaGraphCondAssignDefault);
+        // one handle per IF node (a handle serves a single conditional node), all default 1 at
+        // every replay; the handles go to the device for the cover kernels
+        std::vector<unsigned long long> hs(kk, 0ull);
+        for (uint32_t j = 0; j < kk && e == cudaSuccess; ++j) {
+          stage = 2;
+          cudaGraphConditionalHandle h = 0;
+          e = cudaGraphConditionalHandleCreate(&h, graph, 1u, cudaGraphCondAssignDefault);
+          hs[j] = (unsigned long long)h;
+        }
+        if (e == cudaSuccess) { stage = 3; e = (cudaError_t)(ensure(c, c->cond_handles, (uint64_t)kk * 8) == GIM_OK ? 0 : 2); }
+        if (e == cudaSuccess) e = cudaMemcpy(c->cond_handles.p, hs.data(), (uint64_t)kk * 8, cudaMemcpyHostToDevice);
+        const unsigned long long* dh = c->cond_handles.as<unsigned long long>();
+        // a conditional node cannot be a root of the graph (measured: cudaErrorInvalidValue):
+        // the IF chain hangs off an empty root node
         cudaGraphNode_t prev = nullptr;
+        if (e == cudaSuccess) { stage = 4; e = cudaGraphAddEmptyNode(&prev, graph, nullptr, 0); }
         for (uint32_t j = 0; j < kk && e == cudaSuccess; ++j) {
           cudaGraphNodeParams cp = {};
           cp.type = cudaGraphNodeTypeConditional;
-          cp.conditional.handle = h;
+          cp.conditional.handle = (cudaGraphConditionalHandle)hs[j];
           cp.conditional.type = cudaGraphCondTypeIf;
           cp.conditional.size = 1;
           cudaGraphNode_t node = nullptr;
-          e = cudaGraphAddNode(&node, graph, prev ? &prev : nullptr, prev ? 1 : 0, &cp);
+          stage = 5;
+          e = cudaGraphAddNode(&node, graph, &prev, 1, &cp);
           if (e != cudaSuccess) break;
           cudaGraph_t body = cp.conditional.phGraph_out[0];
+          stage = 6;
           e = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
           if (e != cudaSuccess) break;
-          step(j, (unsigned long long)h);
+          step(j, dh);
           const cudaError_t le = cudaGetLastError();
+          stage = 7;
           e = cudaStreamEndCapture(c->stream, &body);
-          if (e == cudaSuccess) e = le;
+          if (e == cudaSuccess && le != cudaSuccess) e = le;
           prev = node;
         }
-        if (e == cudaSuccess) e = cudaGraphInstantiate(&c->sel_exec, graph, 0);
+        if (e == cudaSuccess) { stage = 9; e = cudaGraphInstantiate(&c->sel_exec, graph, 0); }
         if (graph) cudaGraphDestroy(graph);
         graph = nullptr;
         if (e != cudaSuccess) {                  // no conditional nodes here: plain graph below
+          c->st.cond_graph = 2 + (uint64_t)stage * 1000 + (uint64_t)e;
           cudaGetLastError();
           c->sel_exec = nullptr;
           c->cond_graph = 0;
+        } else {
+          c->st.cond_graph = 1;
         }
       }
       if (!c->sel_exec) {
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        for (uint32_t j = 0; j < kk; ++j) step(j, 0ull);
+        for (uint32_t j = 0; j < kk; ++j) step(j, nullptr);
         CK(cudaStreamEndCapture(c->stream, &graph));
         const cudaError_t ie = cudaGraphInstantiate(&c->sel_exec, graph, 0);
         cudaGraphDestroy(graph);
@@ -1304,9 +1352,9 @@ void gim_destroy(gim_ctx* c) {
                     &c->sizes, &c->soff, &c->giant_list, &c->giant2_list, &c->retry_list, &c->item_list, &c->scan_out,
                     &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->spill, &c->lane_spill, &c->skip_tab, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
-                    &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->thr_node, &c->ag_small,
+                    &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->ag_small,
                     &c->ag_send, &c->ag_recv, &c->sel_bar, &c->rs_gcnt, &c->rs_dshard, &c->rs_keys, &c->rs_kx,
-                    &c->sel_ctl, &c->cmap, &c->cdec, &c->sel_done, &c->probe};
+                    &c->sel_ctl, &c->cmap, &c->cdec, &c->sel_done, &c->probe, &c->cond_handles};
   for (auto& sg : c->iseg) {
     dfree(c, sg.off);
     dfree(c, sg.inv);
@@ -1391,10 +1439,9 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
   if (c->skip && ((int)model != MODEL_IC || (int)scheme == W_EXPLICIT)) c->skip = 0;   // R31 needs IC + WC/uniform
   c->p_uniform = p_uniform;
   c->thr_uniform = (uint64_t)std::ceil((double)p_uniform * 4294967296.0);
-  TRY(dalloc(c, c->row_ptr, ((uint64_t)n + 1) * 4));
+  TRY(dalloc(c, c->row_ptr, ((uint64_t)n + 1) * 4 * (scheme == GIM_W_WC ? 2 : 1)));
   TRY(dalloc(c, c->src, std::max<uint64_t>(m, 1) * 4));
-  if (scheme == GIM_W_WC) TRY(dalloc(c, c->thr_node, ((uint64_t)n + 1) * 4));
-  else dfree(c, c->thr_node);
+  c->thr_node = scheme == GIM_W_WC ? c->row_ptr.as<uint32_t>() + n + 1 : nullptr;
   {
     // upload (pinned host buffers DMA directly), validate + convert row pointers on the device
     DevBuf rp64;
@@ -1406,7 +1453,7 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
     CK(cudaMemsetAsync(flags + 1, 0xFF, 4, c->stream));
     CK(cudaMemsetAsync(flags + 2, 0, 8, c->stream));                 // max in-degree
     TRY(launched(c, launch_validate_csr(rp64.as<uint64_t>(), n, m, c->src.as<uint32_t>(), c->row_ptr.as<uint32_t>(),
-                                        flags, flags + 1, scheme == GIM_W_WC ? c->thr_node.as<uint32_t>() : nullptr,
+                                        flags, flags + 1, c->thr_node,
                                         c->num_sms * 8, c->stream), "k_validate_csr"));
     CK(cudaMemcpyAsync(c->h_u64, flags, 16, cudaMemcpyDeviceToHost, c->stream));
     TRY(sync(c));
@@ -1450,6 +1497,7 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
     CK(cudaMemcpyAsync(c->thr_edge.p, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, c->stream));
   }
   c->graph = true;
+  set_l2_window(c);
   c->have_seed = false;
   TRY(reset_pool(c, 0));
   c->have_seed = false;
@@ -1799,6 +1847,10 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     }
     case GIM_OPT_SELECT_PERSISTENT: c->sel_persistent = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_IMM_EARLY_EXIT: c->imm_early_exit = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_L2_PERSIST:
+      c->l2_persist = value ? 1 : 0;
+      set_l2_window(c);
+      return GIM_OK;
     case GIM_OPT_INV_PASSES: c->inv_passes = (value < 0 || value > 64) ? 0 : (int)value; return GIM_OK;
     case GIM_OPT_COND_GRAPH:
       c->cond_graph = value ? 1 : 0;

@@ -42,23 +42,7 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const uint32_t* src) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// A newly visited node is expanded at the next BFS step, whose first act is loading its row
-// pointers (and WC threshold): start pulling those lines into the L2 now, so that the next
-// step's loads hit the L2 instead of HBM (one DRAM latency less per BFS level on the critical
-// path of deep sets). No register result, no wait.
-#ifndef GIM_PREFETCH
-#define GIM_PREFETCH 1
-#endif
-__device__ __forceinline__ void prefetch_l2(const void* ptr) {
-  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(ptr));
-}
-template <int SCHEME>
-__device__ __forceinline__ void prefetch_node(const RRParams& p, uint32_t u) {
-  if (GIM_PREFETCH) {
-    prefetch_l2(p.row_ptr + u);
-    if (SCHEME == W_WC) prefetch_l2(p.thr_node + u);
-  }
-}
+
 
 // LT: index of the chosen in-edge of v (0..d-1) or d if none (reading R18). Warp-collective.
 template <int SCHEME>
@@ -404,10 +388,7 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
             __syncwarp();
           }
           if (tail + total > (spilled ? p.spill_cap : p.qcap)) { ok = false; break; }
-          if (isnew) {
-            (spilled ? gq : q)[tail + __popc(has & ((1u << lane) - 1u))] = u;
-            prefetch_node<SCHEME>(p, u);
-          }
+          if (isnew) (spilled ? gq : q)[tail + __popc(has & ((1u << lane) - 1u))] = u;
           tail += total;
         }
         npend = 0;
@@ -1105,10 +1086,7 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
       uint32_t b0 = 0;
       if (lane == 0 && total) b0 = atomicAdd(&s_tail, total);
       b0 = __shfl_sync(kFull, b0, 0);
-      if (isnew) {
-        prefetch_node<SCHEME>(p, u);
-        qwrite(b0 + __popc(has & ((1u << lane) - 1u)), u);
-      }
+      if (isnew) qwrite(b0 + __popc(has & ((1u << lane) - 1u)), u);
     }
     npend = 0;
     __syncwarp();

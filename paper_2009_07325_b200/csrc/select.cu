@@ -439,7 +439,7 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
                                            int32_t* __restrict__ dec, MrimSel mr,
                                            uint32_t u_known = kEmpty, const uint32_t* __restrict__ cmap = nullptr,
                                            int32_t* __restrict__ cdec = nullptr, SelCtl* ctl = nullptr,
-                                           unsigned long long cond = 0ull) {
+                                           const unsigned long long* cond = nullptr) {
   __shared__ uint64_t s_lo[kMaxInvSeg], s_end[kMaxInvSeg];   // list start, inclusive prefix end
   __shared__ const uint32_t* s_inv[kMaxInvSeg];
   __shared__ uint32_t s_nseg, s_limit, s_stop;
@@ -494,8 +494,10 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
       s_stop = stop_now;
       if (stop_now && blockIdx.x == 0) {
         ctl->stop = 1u;
-        // graph replay: the remaining steps are IF nodes on this handle and are skipped whole
-        if (cond != 0ull) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, 0u);
+        // graph replay: every later step is an IF node with its own handle (a handle serves one
+        // conditional node): cleared here, the graph skips those steps whole
+        if (cond != nullptr)
+          for (uint32_t t = (uint32_t)j + 1; t < ctl->kk; ++t) cudaGraphSetConditional((cudaGraphConditionalHandle)cond[t], 0u);
       }
     }
   }
@@ -566,7 +568,7 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
                                                const uint64_t* __restrict__ offsets,
                                                const uint32_t* __restrict__ pool,
                                                uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
-                                               int32_t* __restrict__ dec, MrimSel mr, unsigned long long cond) {
+                                               int32_t* __restrict__ dec, MrimSel mr, const unsigned long long* cond) {
   pdl_wait();
   pdl_trigger();
   cover_step<LIMIT>(keys, j, segs, offsets, pool, covered, cnt, dec, mr, kEmpty, nullptr, nullptr, ctl, cond);
@@ -983,7 +985,7 @@ cudaError_t launch_select_coop(const uint32_t* cnt, const uint32_t* cand, const 
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, SelCtl* ctl,
                          const uint64_t* offsets, const uint32_t* pool,
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s, bool limit,
-                         const MrimSel* mr, unsigned long long cond) {
+                         const MrimSel* mr, const unsigned long long* cond) {
   const MrimSel m = mr ? *mr : MrimSel{1u, 0u, 0u};
   if (limit) return launch_pdl(k_cover<true>, grid, 256, s, keys, j, segs, ctl, offsets, pool, covered, cnt, dec, m, cond);
   return launch_pdl(k_cover<false>, grid, 256, s, keys, j, segs, ctl, offsets, pool, covered, cnt, dec, m, cond);

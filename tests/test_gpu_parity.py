@@ -112,8 +112,8 @@ def test_pool_parity_C1_invariance(opts):
 
 @pytest.mark.parametrize("graph,segs,cand,extra", [
     (1, 1, 1, {}), (0, 1, 2, {}), (1, 0, 1, {}), (1, 1, 0, {}), (1, 1, 2, {}),
-    (1, 1, 1, {"OPT_INV_PASSES": 7}), (1, 0, 2, {"OPT_INV_PASSES": 3, "OPT_COND_GRAPH": 0}),
-    (0, 1, 1, {"OPT_INV_PASSES": 64}), (1, 1, 0, {"OPT_COND_GRAPH": 0})])
+    (1, 1, 1, {"OPT_INV_PASSES": 7}), (1, 0, 2, {"OPT_INV_PASSES": 3, "OPT_COND_GRAPH": 1}),
+    (0, 1, 1, {"OPT_INV_PASSES": 64}), (1, 1, 0, {"OPT_COND_GRAPH": 1})])
 def test_pool_parity_C2_and_select(graph, segs, cand, extra):
     """k = 50 selection through the argmax/cover launches replayed from a CUDA graph (default:
     one conditional IF node per step; or a plain graph) and launched one by one; pool generated

@@ -283,18 +283,15 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                         fallbacks): the grid barrier costs more than the launch it replaces.
  *  GIM_OPT_IMM_EARLY_EXIT = 1 (default) / 0: bounded greedy in gim_imm's estimation rounds (see
  *                         gim_imm_result.sel_steps_i); 0 runs every round's k steps.
- *  GIM_OPT_COND_GRAPH   = 0 (default) / 1: the replayed selection graph is one conditional (IF)
- *                         node per greedy step (one handle each: a handle serves one node), so
- *                         the steps after a bounded-greedy stop are skipped by the graph instead
- *                         of launching kernels that return at once (falls back to the plain
- *                         graph where conditional nodes are refused; gim_stats.cond_graph).
- *                         Results identical; measured slower: C1 selection 2.20 vs 1.18 ms, C3
- *                         3.65 vs 2.46 ms (each IF body costs more than two no-op launches).
  *  GIM_OPT_INV_PASSES   = P (0 = auto: one pass per 32 MB of per-node cursors, 1..64): the
  *                         inverted-index scatter runs P node-range passes over the new sets so
  *                         each pass's cursor atomics stay in the L2 (results identical).
  *  GIM_OPT_L2_PERSIST   = 1 (default) / 0: an L2 persisting access-policy window on the library
- *                         stream over the row pointers (+ WC thresholds), read at every BFS level. */
+ *                         stream over the row pointers (+ WC thresholds), read at every BFS level.
+ *  GIM_OPT_SELECT_CTA   = 1 (default) / 0: for P = 1 (or a replicated pool), standard IM and
+ *                         n <= 51,200 (the counts fit in 200 KB of shared memory), the k greedy
+ *                         steps run in ONE 1024-thread CTA: argmax over shared counts, decrements
+ *                         as shared atomics, no launch or grid barrier per step. */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -319,9 +316,10 @@ typedef enum {
   GIM_OPT_SKIP_LANE_CAP = 22,
   GIM_OPT_SELECT_COOP = 23,
   GIM_OPT_IMM_EARLY_EXIT = 24,
-  GIM_OPT_COND_GRAPH = 25,
+  /* 25: retired (conditional IF-node selection graph; measured slower) */
   GIM_OPT_INV_PASSES = 26,
-  GIM_OPT_L2_PERSIST = 27
+  GIM_OPT_L2_PERSIST = 27,
+  GIM_OPT_SELECT_CTA = 28
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 
@@ -346,8 +344,6 @@ typedef struct {
   double host_ms_api;           /* host wall time inside gim_generate_rr/select/imm       */
   uint64_t fused_fallbacks;     /* fused selections redone unfused (uncertified argmax)   */
   uint64_t probe_stops;         /* gim_imm rounds settled by the first-step probe alone   */
-  uint64_t cond_graph;          /* selection graph form: 1 = IF node per step, 0 = none yet,
-                                   2 + the failing stage * 1000 + cudaError = plain-graph fallback */
 } gim_stats;
 gim_status gim_get_stats(gim_ctx* ctx, gim_stats* out);
 gim_status gim_reset_stats(gim_ctx* ctx);

@@ -145,14 +145,11 @@ struct gim_ctx {
   DevBuf cmap, cdec;            // cooperative selection: node -> candidate index (kEmpty), decrement rings
   DevBuf sel_ctl;               // SelCtl of the bounded greedy (IMM estimation rounds)
   DevBuf probe;                 // first-step argmax key of gim_imm's probe
-  DevBuf cond_handles;          // IF-node handles of the conditional selection graph (one per step)
   uint64_t sel_cstar = 0;       // smallest passing covered count of the running round (0 = off)
   uint32_t last_sel_steps = 0;  // greedy steps the last selection ran
-  int cond_graph = 0;           // GIM_OPT_COND_GRAPH: selection graph as IF nodes per step (measured slower)
   int inv_passes = 0;           // GIM_OPT_INV_PASSES: node-range passes of the index scatter (0 = auto)
-  bool sel_cond_used = false;   // the pending selection replays a conditional graph
-  int sel_per_step = 2;         // kernels per greedy step of the pending graph replay
   int imm_early_exit = 1;       // GIM_OPT_IMM_EARLY_EXIT
+  int sel_small = 1;            // GIM_OPT_SELECT_CTA: single-CTA selection when the counts fit in shared memory
   uint64_t cmap_n = 0;          // nodes covered by cmap (kEmpty-initialised)
   // options
   int force_giant = 0, profile = 0;
@@ -167,7 +164,6 @@ struct gim_ctx {
   // CUDA graph of the k-step selection loop (P = 1), valid while its key is unchanged
   cudaGraphExec_t sel_exec = nullptr;
   std::vector<uintptr_t> sel_key;
-  bool sel_cond = false;        // sel_exec is the conditional (IF node per step) graph
   int use_graph = 1;
 };
 
@@ -1101,6 +1097,12 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
                                              c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                                              c->covered.as<uint8_t>(), mr, limited, c->sel_bar.as<unsigned int>(),
                                              c->num_sms, c->stream), "k_select_persistent"));
+  } else if (!dec && !cand && c->rounds == 1 && c->sel_small && n <= select_cta_max_n() && !c->speculate) {
+    // small graphs: every greedy step in one CTA, counts in shared memory (no launch per step)
+    Prof pf(c, CLS_SELECT);
+    TRY(launched(c, launch_select_cta(c->count_total.as<uint32_t>(), (uint32_t)n, keys, (int)kk, segd,
+                                      c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), c->covered.as<uint8_t>(),
+                                      ctl, limited, c->stream), "k_select_cta"));
   } else if (!dec && c->use_graph) {
     // P = 1: the 2k argmax/cover launches replayed from a CUDA graph (captured once per set of
     // buffer pointers; steady-state IMM runs reuse it), so the GPU runs them back to back.
@@ -1108,87 +1110,30 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
                                         (uintptr_t)c->offsets.p, (uintptr_t)c->pool.p, (uintptr_t)c->covered.p,
                                         (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n, (uintptr_t)limited,
                                         (uintptr_t)c->rounds, (uintptr_t)ctl};
-    auto step = [&](uint32_t j, const unsigned long long* h) {
+    auto step = [&](uint32_t j) {
       if (cand) launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream, ctl);
       launch_argmax(c->cnt.as<uint32_t>(), nullptr, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * kArgmaxCtasPerSM, c->stream,
                     mr != nullptr, 0u, ctl);
       launch_cover(keys, (int)j, segd, ctl, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                    c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * kCoverCtasPerSM, c->stream,
-                   limited, mr, h);
+                   limited, mr);
     };
     if (!c->sel_exec || key != c->sel_key) {
       if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
       c->sel_exec = nullptr;
       c->sel_key.clear();
       cudaGraph_t graph = nullptr;
-      if (c->cond_graph) {
-        // one IF node per greedy step on one handle (reset to 1 at every replay): the cover that
-        // stops a bounded greedy clears it and the graph skips the remaining steps itself
-        int stage = 1;
-        cudaError_t e = cudaGraphCreate(&graph, 0);
-        // one handle per IF node (a handle serves a single conditional node), all default 1 at
-        // every replay; the handles go to the device for the cover kernels
-        std::vector<unsigned long long> hs(kk, 0ull);
-        for (uint32_t j = 0; j < kk && e == cudaSuccess; ++j) {
-          stage = 2;
-          cudaGraphConditionalHandle h = 0;
-          e = cudaGraphConditionalHandleCreate(&h, graph, 1u, cudaGraphCondAssignDefault);
-          hs[j] = (unsigned long long)h;
-        }
-        if (e == cudaSuccess) { stage = 3; e = (cudaError_t)(ensure(c, c->cond_handles, (uint64_t)kk * 8) == GIM_OK ? 0 : 2); }
-        if (e == cudaSuccess) e = cudaMemcpy(c->cond_handles.p, hs.data(), (uint64_t)kk * 8, cudaMemcpyHostToDevice);
-        const unsigned long long* dh = c->cond_handles.as<unsigned long long>();
-        // a conditional node cannot be a root of the graph (measured: cudaErrorInvalidValue):
-        // the IF chain hangs off an empty root node
-        cudaGraphNode_t prev = nullptr;
-        if (e == cudaSuccess) { stage = 4; e = cudaGraphAddEmptyNode(&prev, graph, nullptr, 0); }
-        for (uint32_t j = 0; j < kk && e == cudaSuccess; ++j) {
-          cudaGraphNodeParams cp = {};
-          cp.type = cudaGraphNodeTypeConditional;
-          cp.conditional.handle = (cudaGraphConditionalHandle)hs[j];
-          cp.conditional.type = cudaGraphCondTypeIf;
-          cp.conditional.size = 1;
-          cudaGraphNode_t node = nullptr;
-          stage = 5;
-          e = cudaGraphAddNode(&node, graph, &prev, 1, &cp);
-          if (e != cudaSuccess) break;
-          cudaGraph_t body = cp.conditional.phGraph_out[0];
-          stage = 6;
-          e = cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
-          if (e != cudaSuccess) break;
-          step(j, dh);
-          const cudaError_t le = cudaGetLastError();
-          stage = 7;
-          e = cudaStreamEndCapture(c->stream, &body);
-          if (e == cudaSuccess && le != cudaSuccess) e = le;
-          prev = node;
-        }
-        if (e == cudaSuccess) { stage = 9; e = cudaGraphInstantiate(&c->sel_exec, graph, 0); }
-        if (graph) cudaGraphDestroy(graph);
-        graph = nullptr;
-        if (e != cudaSuccess) {                  // no conditional nodes here: plain graph below
-          c->st.cond_graph = 2 + (uint64_t)stage * 1000 + (uint64_t)e;
-          cudaGetLastError();
-          c->sel_exec = nullptr;
-          c->cond_graph = 0;
-        } else {
-          c->st.cond_graph = 1;
-        }
-      }
       if (!c->sel_exec) {
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        for (uint32_t j = 0; j < kk; ++j) step(j, nullptr);
+        for (uint32_t j = 0; j < kk; ++j) step(j);
         CK(cudaStreamEndCapture(c->stream, &graph));
         const cudaError_t ie = cudaGraphInstantiate(&c->sel_exec, graph, 0);
         cudaGraphDestroy(graph);
         if (ie != cudaSuccess) return fail_cuda(c, "cudaGraphInstantiate", ie);
       }
-      c->sel_cond = c->cond_graph != 0;
       c->sel_key = key;
     }
     Prof pf(c, CLS_SELECT);
-    c->sel_cond_used = c->sel_cond;
-    c->sel_per_step = cand ? 3 : 2;
     TRY(launched(c, cudaGraphLaunch(c->sel_exec, c->stream), "selection graph", (cand ? 3 : 2) * (int)kk));
   } else {
     for (uint32_t j = 0; j < kk; ++j) {
@@ -1237,8 +1182,6 @@ gim_status select_finish(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gain
   }
   uint64_t cov = 0;
   uint32_t steps = 0;                   // a step that ran has a nonzero key (k <= n: a pick exists)
-  const bool cond_used = c->sel_cond_used;
-  c->sel_cond_used = false;
   for (uint32_t j = 0; j < k * c->rounds; ++j) {
     steps += c->h_keys[j] != 0ull;
     seeds[j] = ~(uint32_t)(c->h_keys[j] & 0xFFFFFFFFull);
@@ -1248,7 +1191,6 @@ gim_status select_finish(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gain
   }
   if (covered) *covered = cov;
   c->last_sel_steps = steps;
-  if (cond_used) c->st.launches -= (uint64_t)c->sel_per_step * (k * c->rounds - steps);   // skipped IF bodies
   c->st.selects++;
   return GIM_OK;
 }
@@ -1354,7 +1296,7 @@ void gim_destroy(gim_ctx* c) {
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
                     &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->ag_small,
                     &c->ag_send, &c->ag_recv, &c->sel_bar, &c->rs_gcnt, &c->rs_dshard, &c->rs_keys, &c->rs_kx,
-                    &c->sel_ctl, &c->cmap, &c->cdec, &c->sel_done, &c->probe, &c->cond_handles};
+                    &c->sel_ctl, &c->cmap, &c->cdec, &c->sel_done, &c->probe};
   for (auto& sg : c->iseg) {
     dfree(c, sg.off);
     dfree(c, sg.inv);
@@ -1847,16 +1789,12 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     }
     case GIM_OPT_SELECT_PERSISTENT: c->sel_persistent = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_IMM_EARLY_EXIT: c->imm_early_exit = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_SELECT_CTA: c->sel_small = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_L2_PERSIST:
       c->l2_persist = value ? 1 : 0;
       set_l2_window(c);
       return GIM_OK;
     case GIM_OPT_INV_PASSES: c->inv_passes = (value < 0 || value > 64) ? 0 : (int)value; return GIM_OK;
-    case GIM_OPT_COND_GRAPH:
-      c->cond_graph = value ? 1 : 0;
-      if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);   // recapture in the new form
-      c->sel_exec = nullptr;
-      return GIM_OK;
     case GIM_OPT_GIANT_NT:
       if (value != 0 && value != kGiantThreads && value != kGiantThreadsNarrow)
         return fail(c, GIM_EINVAL, "giant CTA width must be 0 (auto), 256 or 128");

@@ -87,7 +87,12 @@ cudaError_t launch_select_persistent(uint32_t* cnt, uint32_t n, unsigned long lo
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, SelCtl* ctl,
                          const uint64_t* offsets, const uint32_t* pool,
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s,
-                         bool limit, const MrimSel* mr = nullptr, const unsigned long long* cond = nullptr);
+                         bool limit, const MrimSel* mr = nullptr);
+// small graphs (P = 1): all k steps in one CTA, counts in shared memory (n <= select_cta_max_n())
+uint32_t select_cta_max_n();
+cudaError_t launch_select_cta(const uint32_t* count_total, uint32_t n, unsigned long long* keys, int kk,
+                              const InvSegDev* segs, const uint64_t* offsets, const uint32_t* pool,
+                              uint8_t* covered, SelCtl* ctl, bool limit, cudaStream_t s);
 // fused greedy steps (P = 1): candidate argmax of step 0, then per step cover + next argmax
 cudaError_t launch_select_fused(unsigned long long* keys, int kk, const InvSegDev* segs, const uint64_t* offsets,
                                 const uint32_t* pool, uint8_t* covered, uint32_t* cnt, const uint32_t* cand,

@@ -186,7 +186,12 @@ __device__ __forceinline__ void argmax_step(uint32_t* __restrict__ cnt, int32_t*
                                             uint32_t n, unsigned long long* __restrict__ keys, int j,
                                             const uint32_t* __restrict__ tau_p1, uint32_t excl,
                                             uint32_t id_base = 0, const SelCtl* ctl = nullptr) {
-  if (ctl != nullptr && *(volatile const uint32_t*)&ctl->stop) return;   // bounded greedy stopped
+  // bounded greedy stopped (SelCtl): no pick from here on, keys[j] stays 0. Large n: test first
+  // and skip the scan; small n: the flag load overlaps the (cheap) scan and only the final
+  // atomicMax is skipped — no serial load at the head of every greedy step
+  const bool test_first = ctl != nullptr && n >= (1u << 20);
+  if (test_first && *(volatile const uint32_t*)&ctl->stop) return;
+  const uint32_t stopped = (ctl != nullptr && !test_first) ? *(volatile const uint32_t*)&ctl->stop : 0u;
   // candidate mode: the candidate argmax already found a count >= tau_p1, which no node outside
   // the candidate list can reach (their counts started below it and only decrease)
   if (tau_p1 != nullptr && (uint32_t)(keys[j] >> 32) >= *tau_p1 && keys[j] != 0ull) return;
@@ -249,7 +254,7 @@ __device__ __forceinline__ void argmax_step(uint32_t* __restrict__ cnt, int32_t*
       const unsigned long long o = __shfl_xor_sync(kFull, best, off);
       best = o > best ? o : best;
     }
-    if (threadIdx.x == 0 && best) atomicMax(keys + j, best);
+    if (threadIdx.x == 0 && best && !stopped) atomicMax(keys + j, best);
   }
 }
 
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(256) k_argmax_cand(const uint32_t* __restrict_
   __shared__ unsigned long long s_best[8];
   pdl_wait();
   pdl_trigger();
-  if (ctl != nullptr && *(volatile const uint32_t*)&ctl->stop) return;
+  if (ctl != nullptr && *(volatile const uint32_t*)&ctl->stop) return;   // large n only (C5)
   const uint32_t nc = *ncand;
   unsigned long long best = 0;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
@@ -438,8 +443,7 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
                                            uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
                                            int32_t* __restrict__ dec, MrimSel mr,
                                            uint32_t u_known = kEmpty, const uint32_t* __restrict__ cmap = nullptr,
-                                           int32_t* __restrict__ cdec = nullptr, SelCtl* ctl = nullptr,
-                                           const unsigned long long* cond = nullptr) {
+                                           int32_t* __restrict__ cdec = nullptr, SelCtl* ctl = nullptr) {
   __shared__ uint64_t s_lo[kMaxInvSeg], s_end[kMaxInvSeg];   // list start, inclusive prefix end
   __shared__ const uint32_t* s_inv[kMaxInvSeg];
   __shared__ uint32_t s_nseg, s_limit, s_stop;
@@ -448,27 +452,27 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
   // step j the final covered count is at most cov_j + (kk - j) * gain_j with cov_j = the gains of
   // steps < j. Below cstar the round's test (Alg. 2 l.7) fails whatever the remaining steps pick:
   // the selection stops here (every CTA evaluates the same bound from the same keys).
-  uint32_t stop_now = 0;
-  if (ctl != nullptr) {
-    if (*(volatile const uint32_t*)&ctl->stop) return;
-    const unsigned long long cstar = ctl->cstar;
-    if (cstar != 0ull && threadIdx.x < 32) {
-      unsigned long long sum = 0;
-      for (int t = (int)threadIdx.x; t < j; t += 32) sum += keys[t] >> 32;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(kFull, sum, off);
-      const unsigned long long bound = sum + (unsigned long long)(ctl->kk - (uint32_t)j) * (keys[j] >> 32);
-      stop_now = bound < cstar ? 1u : 0u;
-    }
-  }
   // u_known: the pick computed by this CTA itself (cooperative selection; the pick is excluded
-  // from later argmaxes there, not retired in cnt, which other CTAs may still be reading)
-  const uint32_t u = u_known != kEmpty ? u_known : ~(uint32_t)keys[j];
-  if (u_known == kEmpty && blockIdx.x == 0 && threadIdx.x == 0) cnt[u] = kSent;   // retire the pick
+  // from later argmaxes there, not retired in cnt, which other CTAs may still be reading).
+  // keys[j] == 0: the selection stopped at an earlier step (its argmax made no pick)
+  const unsigned long long kj = u_known != kEmpty ? 0ull : keys[j];
+  const bool dead = u_known == kEmpty && kj == 0ull;
+  const uint32_t u = u_known != kEmpty ? u_known : ~(uint32_t)kj;
+  if (!dead && u_known == kEmpty && blockIdx.x == 0 && threadIdx.x == 0) cnt[u] = kSent;   // retire the pick
+  uint32_t stop_now = dead ? 1u : 0u;
   if (threadIdx.x < 32) {                     // lanes load the segments' list bounds in parallel
     const uint32_t l = threadIdx.x;
     InvSegDev sg{nullptr, nullptr};
-    if (l < (uint32_t)kMaxInvSeg) sg = segs[l];  // unused slots are null: no dependency on nseg
+    if (l < (uint32_t)kMaxInvSeg && !dead) sg = segs[l];  // unused slots are null: no dependency on nseg
+    if (ctl != nullptr && !dead) {             // bound: loads in parallel with the list bounds
+      const unsigned long long cstar = ctl->cstar;
+      unsigned long long sum = 0;
+      for (int t = (int)l; t < j; t += 32) sum += keys[t] >> 32;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(kFull, sum, off);
+      const unsigned long long bound = sum + (unsigned long long)(ctl->kk - (uint32_t)j) * (kj >> 32);
+      stop_now = (cstar != 0ull && bound < cstar) ? 1u : 0u;
+    }
     // set-id limit (only after a tail truncation), loaded alongside the descriptors
     const uint32_t lim = (LIMIT && l == 0) ? reinterpret_cast<const uint32_t*>(segs + kMaxInvSeg)[1] : 0u;
     uint64_t lo = 0, len = 0;
@@ -492,13 +496,7 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
       s_nseg = __popc(used);
       s_limit = lim;
       s_stop = stop_now;
-      if (stop_now && blockIdx.x == 0) {
-        ctl->stop = 1u;
-        // graph replay: every later step is an IF node with its own handle (a handle serves one
-        // conditional node): cleared here, the graph skips those steps whole
-        if (cond != nullptr)
-          for (uint32_t t = (uint32_t)j + 1; t < ctl->kk; ++t) cudaGraphSetConditional((cudaGraphConditionalHandle)cond[t], 0u);
-      }
+      if (stop_now && !dead && blockIdx.x == 0) ctl->stop = 1u;
     }
   }
   // MRIM (R27): the pick that gives round t = u / n its k-th seed closes the round: every pair of
@@ -568,10 +566,10 @@ __global__ void __launch_bounds__(256) k_cover(const unsigned long long* __restr
                                                const uint64_t* __restrict__ offsets,
                                                const uint32_t* __restrict__ pool,
                                                uint8_t* __restrict__ covered, uint32_t* __restrict__ cnt,
-                                               int32_t* __restrict__ dec, MrimSel mr, const unsigned long long* cond) {
+                                               int32_t* __restrict__ dec, MrimSel mr) {
   pdl_wait();
   pdl_trigger();
-  cover_step<LIMIT>(keys, j, segs, offsets, pool, covered, cnt, dec, mr, kEmpty, nullptr, nullptr, ctl, cond);
+  cover_step<LIMIT>(keys, j, segs, offsets, pool, covered, cnt, dec, mr, kEmpty, nullptr, nullptr, ctl);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -789,6 +787,124 @@ __global__ void __launch_bounds__(1024, 1) k_select_persistent(uint32_t* __restr
 }
 
 // ------------------------------------------------------------------------------------------
+// Small-graph NodeSelection (P = 1, standard IM, n counts fit in shared memory): all k greedy
+// steps in ONE CTA of 1024 threads — the count vector lives in shared memory (argmax = a scan of
+// shared memory, decrements = shared atomics), the covered flags / inverted lists / pool in
+// global memory (L2-resident at these sizes). Between argmax and cover only __syncthreads: no
+// kernel boundary and no grid barrier per step (Alg. 1 l.6-10, Alg. 7; bounded greedy
+// of SelCtl as in cover_step).
+// ------------------------------------------------------------------------------------------
+constexpr int kSmallSelThreads = 1024;
+template <bool LIMIT>
+__global__ void __launch_bounds__(kSmallSelThreads, 1) k_select_cta(const uint32_t* __restrict__ count_total,
+                                                                   uint32_t n, unsigned long long* __restrict__ keys,
+                                                                   int kk, const InvSegDev* __restrict__ segs,
+                                                                   const uint64_t* __restrict__ offsets,
+                                                                   const uint32_t* __restrict__ pool,
+                                                                   uint8_t* __restrict__ covered, SelCtl* ctl) {
+  extern __shared__ uint32_t s_cnt[];                 // [n]
+  __shared__ unsigned long long s_wbest[kSmallSelThreads / 32];
+  __shared__ uint64_t s_lo[kMaxInvSeg], s_end[kMaxInvSeg];
+  __shared__ const uint32_t* s_inv[kMaxInvSeg];
+  __shared__ const uint32_t* s_endp[kMaxInvSeg];
+  __shared__ uint32_t s_u, s_stop, s_nseg, s_limit;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (uint32_t v = tid; v < n; v += kSmallSelThreads) s_cnt[v] = count_total[v];
+  if (tid < 32) {
+    InvSegDev sg{nullptr, nullptr};
+    if (tid < kMaxInvSeg) sg = segs[tid];
+    if (tid < kMaxInvSeg) {
+      s_inv[tid] = sg.inv;
+      s_endp[tid] = sg.end;
+    }
+    const uint32_t used = __ballot_sync(kFull, sg.end != nullptr);
+    if (tid == 0) {
+      s_nseg = __popc(used);
+      s_limit = LIMIT ? reinterpret_cast<const uint32_t*>(segs + kMaxInvSeg)[1] : 0xFFFFFFFFu;
+    }
+  }
+  const unsigned long long cstar = ctl ? ctl->cstar : 0ull;
+  unsigned long long cov = 0;                         // thread 0: gains of the steps so far
+  __syncthreads();
+  const uint32_t nseg = s_nseg, limit = s_limit;
+  const uint32_t sub = tid & 7;
+  for (int j = 0; j < kk; ++j) {
+    // argmax over the shared counts (4 independent loads per thread per round)
+    unsigned long long best = 0;
+    for (uint32_t v = tid; v < n; v += kSmallSelThreads) argmax_one(s_cnt[v], v, best, 0u);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+      best = o > best ? o : best;
+    }
+    if (lane == 0) s_wbest[warp] = best;
+    __syncthreads();
+    if (warp == 0) {
+      best = s_wbest[lane];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+        best = o > best ? o : best;
+      }
+      const uint32_t u = ~(uint32_t)best;
+      // lane q < nseg: list bounds of u in segment q, inclusive prefix over the segments
+      uint64_t lo = 0, len = 0;
+      if ((uint32_t)lane < nseg) {
+        const uint32_t* e = s_endp[lane];
+        lo = u ? e[u - 1] : 0u;
+        len = e[u] - lo;
+      }
+      uint64_t incl = len;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t y = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += y;
+      }
+      if (lane < kMaxInvSeg) {
+        s_lo[lane] = lo;
+        s_end[lane] = (uint32_t)lane < nseg ? incl : ~0ull;
+      }
+      if (lane == 0) {
+        keys[j] = best;
+        const unsigned long long g = best >> 32;
+        // bounded greedy: the remaining kk - j steps gain at most g each
+        const bool stop = cstar != 0ull && cov + (unsigned long long)(kk - j) * g < cstar;
+        cov += g;
+        s_stop = stop ? 1u : 0u;
+        if (stop) ctl->stop = 1u;
+        s_u = u;
+        s_cnt[u] = kSent;                             // retire the pick
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+    const uint32_t u = s_u;
+    const uint64_t total = (nseg && limit) ? s_end[nseg - 1] : 0ull;
+    // cover: one 8-lane group per inverted-list entry of u (as cover_step)
+    uint32_t q = 0;
+    for (uint64_t t = tid >> 3; t < total; t += kSmallSelThreads / 8) {
+      while (t >= s_end[q]) ++q;
+      const uint64_t pos = s_lo[q] + (t - (q ? s_end[q - 1] : 0));
+      const uint32_t r0 = s_inv[q][pos];
+      const uint32_t r = LIMIT ? min(r0, limit - 1u) : r0;
+      const uint8_t cv = covered[r];
+      const uint64_t a = offsets[r], b = offsets[r + 1];
+      if (cv || (LIMIT && r0 != r)) continue;
+      if (sub == 0) covered[r] = 1;
+      for (uint64_t e = a + sub; e < b; e += 8 * 8) {
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = (e + 8 * i < b) ? pool[e + 8 * i] : u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (w[i] != u) atomicSub(&s_cnt[w[i]], 1u);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Host launch wrappers
 // ------------------------------------------------------------------------------------------
 int g_pdl = 0;   // GIM_OPT_PDL (process-wide: the launch wrappers carry no ctx)
@@ -982,13 +1098,33 @@ cudaError_t launch_select_coop(const uint32_t* cnt, const uint32_t* cand, const 
   return cudaGetLastError();
 }
 
+uint32_t select_cta_max_n() { return (uint32_t)((200u << 10) / 4); }   // counts in <= 200 KB of shared memory
+
+cudaError_t launch_select_cta(const uint32_t* count_total, uint32_t n, unsigned long long* keys, int kk,
+                              const InvSegDev* segs, const uint64_t* offsets, const uint32_t* pool,
+                              uint8_t* covered, SelCtl* ctl, bool limit, cudaStream_t s) {
+  const int smem = (int)(n * 4u);
+  static std::atomic<uint64_t> attr{0};
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  if (!(attr.load() & (1ull << (dev & 63)))) {
+    const int cap = (int)(select_cta_max_n() * 4u);
+    if (cudaError_t e = cudaFuncSetAttribute((const void*)k_select_cta<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap)) return e;
+    if (cudaError_t e = cudaFuncSetAttribute((const void*)k_select_cta<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cap)) return e;
+    attr.fetch_or(1ull << (dev & 63));
+  }
+  if (limit) k_select_cta<true><<<1, kSmallSelThreads, smem, s>>>(count_total, n, keys, kk, segs, offsets, pool, covered, ctl);
+  else k_select_cta<false><<<1, kSmallSelThreads, smem, s>>>(count_total, n, keys, kk, segs, offsets, pool, covered, ctl);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, SelCtl* ctl,
                          const uint64_t* offsets, const uint32_t* pool,
                          uint8_t* covered, uint32_t* cnt, int32_t* dec, int grid, cudaStream_t s, bool limit,
-                         const MrimSel* mr, const unsigned long long* cond) {
+                         const MrimSel* mr) {
   const MrimSel m = mr ? *mr : MrimSel{1u, 0u, 0u};
-  if (limit) return launch_pdl(k_cover<true>, grid, 256, s, keys, j, segs, ctl, offsets, pool, covered, cnt, dec, m, cond);
-  return launch_pdl(k_cover<false>, grid, 256, s, keys, j, segs, ctl, offsets, pool, covered, cnt, dec, m, cond);
+  if (limit) return launch_pdl(k_cover<true>, grid, 256, s, keys, j, segs, ctl, offsets, pool, covered, cnt, dec, m);
+  return launch_pdl(k_cover<false>, grid, 256, s, keys, j, segs, ctl, offsets, pool, covered, cnt, dec, m);
 }
 
 }  // namespace gim

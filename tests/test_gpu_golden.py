@@ -37,11 +37,10 @@ def _rel(a, b):
 
 
 @pytest.mark.parametrize("key,early", [("C1", 1), ("C2", 1), ("C3", 1), ("C4", 1), ("C5", 1),
-                                       ("C1", 0), ("C3", 0), ("C1", 2), ("C3", 2)])
+                                       ("C1", 0), ("C3", 0)])
 def test_imm_golden(key, early):
     """early = 1: the default bounded greedy in the estimation rounds (stopped rounds checked by
-    tests/imm_trace.py); early = 2: the same with the selection replayed as conditional graph
-    nodes; early = 0: every round's k steps, cov_i exactly as the oracle's."""
+    tests/imm_trace.py); early = 0: every round's k steps, cov_i exactly as the oracle's."""
     gd = json.load(open(os.path.join(GOLDEN, f"imm_{key}.json")))
     w = gi.WORKLOADS[key]
     g = gi.workload_graph(key)
@@ -49,9 +48,7 @@ def test_imm_golden(key, early):
     c = P.Gim(0)
     try:
         c.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme, p_uniform=w.p_uniform)
-        c.set_option(P.OPT_IMM_EARLY_EXIT, 1 if early else 0)
-        if early == 2:
-            c.set_option(P.OPT_COND_GRAPH, 1)
+        c.set_option(P.OPT_IMM_EARLY_EXIT, early)
         r = c.imm(w.k, w.eps, w.ell, w.rr_seed)
         assert _rel(r.ell_eff, gd["ell_eff"]) and _rel(r.eps_prime, gd["eps_prime"])
         assert _rel(r.lambda_prime, gd["lambda_prime"]) and _rel(r.lambda_star, gd["lambda_star"])
@@ -60,8 +57,6 @@ def test_imm_golden(key, early):
         stopped = check_cov_trace(r, gd["T_i"], gd["cov_i"], g.n, gd["eps_prime"], w.k)
         if not early:
             assert stopped == 0 and r.cov_i.tolist() == gd["cov_i"]
-        if early == 2:
-            assert c.stats()["cond_graph"] == 1, c.stats()["cond_graph"]
         assert all(_rel(a, b) for a, b in zip(r.theta_i_real.tolist(), gd["theta_i"]))
         assert _rel(r.LB, gd["LB"]) and _rel(r.theta, gd["theta"])
         assert r.R_final == gd["R_final"] and r.covered == gd["cov"]

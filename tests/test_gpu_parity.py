@@ -112,8 +112,8 @@ def test_pool_parity_C1_invariance(opts):
 
 @pytest.mark.parametrize("graph,segs,cand,extra", [
     (1, 1, 1, {}), (0, 1, 2, {}), (1, 0, 1, {}), (1, 1, 0, {}), (1, 1, 2, {}),
-    (1, 1, 1, {"OPT_INV_PASSES": 7}), (1, 0, 2, {"OPT_INV_PASSES": 3, "OPT_COND_GRAPH": 1}),
-    (0, 1, 1, {"OPT_INV_PASSES": 64}), (1, 1, 0, {"OPT_COND_GRAPH": 1})])
+    (1, 1, 1, {"OPT_INV_PASSES": 7}), (1, 0, 2, {"OPT_INV_PASSES": 3}),
+    (0, 1, 1, {"OPT_INV_PASSES": 64})])
 def test_pool_parity_C2_and_select(graph, segs, cand, extra):
     """k = 50 selection through the argmax/cover launches replayed from a CUDA graph (default:
     one conditional IF node per step; or a plain graph) and launched one by one; pool generated
@@ -466,4 +466,34 @@ def test_coop_selection_imm_golden(key):
     r = c.imm(w.k, w.eps, w.ell, w.rr_seed)
     assert r.seeds.tolist() == gd["seeds"] and r.R_final == gd["R_final"]
     check_cov_trace(r, gd["T_i"], gd["cov_i"], g.n, gd["eps_prime"], w.k)
+    c.close()
+
+
+@pytest.mark.parametrize("small", [1, 0])
+def test_select_small_cta_equals_oracle(small):
+    """Single-CTA selection (counts in shared memory, GIM_OPT_SELECT_CTA, default for n <= 51,200)
+    and the multi-CTA graph replay both equal the oracle: C1 pool in several generate calls
+    (several index segments), k = 50 and k = 200, a truncated pool (cut sets skipped), and the full
+    IMM with its bounded-greedy trace."""
+    w = gi.WORKLOADS["C1"]
+    g = gi.workload_graph("C1")
+    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_CTA: small})
+    o = oracle.Oracle(g, w.model, w.scheme)
+    for T in (5000, 12001, 40013):
+        c.generate_rr(T, w.rr_seed)
+    o.generate(40013, w.rr_seed)
+    for k in (50, 200):
+        s, gn, cov = c.select(k)
+        os_, ogn, ocov = o.select(k)
+        assert np.array_equal(s, os_) and np.array_equal(gn, ogn) and cov == ocov
+    c.generate_rr(30011, w.rr_seed)                    # truncation: sets >= 30011 are cut
+    o.generate(30011, w.rr_seed)
+    s, gn, cov = c.select(50)
+    os_, ogn, ocov = o.select(50)
+    assert np.array_equal(s, os_) and np.array_equal(gn, ogn) and cov == ocov
+    r = c.imm(w.k, w.eps, w.ell, w.rr_seed)
+    ro = oracle.Oracle(g, w.model, w.scheme).imm(w.k, w.eps, w.ell, w.rr_seed)
+    assert np.array_equal(r.seeds, ro.seeds) and r.R_final == ro.R_final and r.covered == ro.cov
+    check_cov_trace(r, ro.T_i, ro.cov_i, g.n, ro.eps_prime, w.k,
+                    oracle_round_gains(oracle.Oracle(g, w.model, w.scheme), ro.T_i, w.k, w.rr_seed))
     c.close()

@@ -283,15 +283,19 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                         fallbacks): the grid barrier costs more than the launch it replaces.
  *  GIM_OPT_IMM_EARLY_EXIT = 1 (default) / 0: bounded greedy in gim_imm's estimation rounds (see
  *                         gim_imm_result.sel_steps_i); 0 runs every round's k steps.
- *  GIM_OPT_INV_PASSES   = P (0 = auto: one pass per 32 MB of per-node cursors, 1..64): the
- *                         inverted-index scatter runs P node-range passes over the new sets so
- *                         each pass's cursor atomics stay in the L2 (results identical).
- *  GIM_OPT_L2_PERSIST   = 1 (default) / 0: an L2 persisting access-policy window on the library
- *                         stream over the row pointers (+ WC thresholds), read at every BFS level.
+ *  GIM_OPT_INV_PASSES   = P (0 = default 1, 1..64): the inverted-index scatter runs P node-range
+ *                         passes over the new sets so each pass's cursor atomics stay in the L2
+ *                         (results identical; measured slower on C5: 6.19 vs 5.66 ms at P = 6).
+ *  GIM_OPT_L2_PERSIST   = 0 (default) / 1: an L2 persisting access-policy window on the library
+ *                         stream over the row pointers (+ WC thresholds), read at every BFS level
+ *                         (measured: C3 neutral; C5 store 3.8 -> 5.9 ms, index 6.2 -> 10.5 ms).
  *  GIM_OPT_SELECT_CTA   = 1 (default) / 0: for P = 1 (or a replicated pool), standard IM and
  *                         n <= 51,200 (the counts fit in 200 KB of shared memory), the k greedy
  *                         steps run in ONE 1024-thread CTA: argmax over shared counts, decrements
- *                         as shared atomics, no launch or grid barrier per step. */
+ *                         as shared atomics, no launch or grid barrier per step.
+ *  GIM_OPT_INV_SORT     = -1 (default: auto, when n * 4 > 64 MB) / 0 / 1: build each index
+ *                         segment by a stable radix sort of its (node, set) pairs by node instead
+ *                         of the cursor scatter (lists in ascending set order; same lists). */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -319,7 +323,8 @@ typedef enum {
   /* 25: retired (conditional IF-node selection graph; measured slower) */
   GIM_OPT_INV_PASSES = 26,
   GIM_OPT_L2_PERSIST = 27,
-  GIM_OPT_SELECT_CTA = 28
+  GIM_OPT_SELECT_CTA = 28,
+  GIM_OPT_INV_SORT = 29
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

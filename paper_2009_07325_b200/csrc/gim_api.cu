@@ -66,7 +66,7 @@ struct gim_ctx {
   uint64_t thr_uniform = 0;
   DevBuf row_ptr, src, thr_edge;   // row_ptr holds [n + 1] row pointers, then (WC) [n + 1] thresholds
   uint32_t* thr_node = nullptr;     // WC threshold per node: row_ptr + n + 1 (one L2 window covers both)
-  int l2_persist = 1;               // GIM_OPT_L2_PERSIST
+  int l2_persist = 0;               // GIM_OPT_L2_PERSIST (measured: C5 store 3.8 -> 5.9 ms, index 6.2 -> 10.5 ms with it)
   DevBuf out_ptr, out_dst, out_in, thr_wc;   // out-CSR for gim_mc_spread (built on first use)
   bool out_valid = false;
   // MRIM (readings R26-R28): rounds T; pair ids t*n + u index the count / index / selection
@@ -102,6 +102,7 @@ struct gim_ctx {
   int sel_persistent = 0;           // GIM_OPT_SELECT_PERSISTENT: k steps in one cooperative launch
   DevBuf sel_bar;
   double giant_per_slot = 0.0;      // giant sets per default slot in the previous chunk
+  bool dense_sets = false;          // some chunk had >= 12 giant sets per slot (sticky: spill tier on)
   bool giant_cap_reached = false;
   uint64_t stage_cap = 0;
   int lt_bps = 0;                  // resident K-LT CTAs per SM on this context's device
@@ -148,6 +149,8 @@ struct gim_ctx {
   uint64_t sel_cstar = 0;       // smallest passing covered count of the running round (0 = off)
   uint32_t last_sel_steps = 0;  // greedy steps the last selection ran
   int inv_passes = 0;           // GIM_OPT_INV_PASSES: node-range passes of the index scatter (0 = auto)
+  int inv_sort = -1;            // GIM_OPT_INV_SORT: -1 auto (n * 4 > 64 MB), 0 scatter, 1 sort
+  DevBuf isort_keys, isort_vals, isort_tmp;   // sort-based segments: sorted keys, set ids, CUB scratch
   int imm_early_exit = 1;       // GIM_OPT_IMM_EARLY_EXIT
   int sel_small = 1;            // GIM_OPT_SELECT_CTA: single-CTA selection when the counts fit in shared memory
   uint64_t cmap_n = 0;          // nodes covered by cmap (kEmpty-initialised)
@@ -336,11 +339,27 @@ gim_status build_inv_segment(gim_ctx* c, uint64_t set0, uint64_t set1, uint64_t 
   cudaError_t e = launch_scan_u32_to32(c->cursor.as<uint32_t>(), n, sg.off.as<uint32_t>(), c->scan_tmp.as<uint64_t>(),
                                        c->scan_tmp.as<uint64_t>() + scan_tiles(n) + 1, c->stream, &nl);
   TRY(launched(c, e, "scan(segment counts)", nl));
-  if (set1 > set0) {
-    // node-range passes: each keeps <= kInvPassBytes of cursors (+ its inv range) in the L2
-    const uint64_t kInvPassBytes = 32ull << 20;
-    const int passes = c->inv_passes > 0 ? c->inv_passes
-                                         : (int)std::max<uint64_t>(1, (n * 4 + kInvPassBytes - 1) / kInvPassBytes);
+  // sort-based segment (GIM_OPT_INV_SORT; auto: when the per-node cursors exceed 64 MB, i.e. far
+  // beyond the L2, so that each scatter step would be a random DRAM read-modify-write)
+  const bool sort_mode = c->inv_sort == 1 || (c->inv_sort == -1 && n * 4 > (64ull << 20));
+  if (set1 > set0 && sort_mode) {
+    const uint64_t E = e1 - e0;
+    uint32_t nbits = 1;
+    while (nbits < 32 && (1ull << nbits) < n) ++nbits;
+    const size_t cub_bytes = inv_sort_tmp_bytes(E, nbits);
+    TRY(ensure(c, c->isort_keys, E * 4));
+    TRY(ensure(c, c->isort_vals, E * 4));
+    TRY(ensure(c, c->isort_tmp, cub_bytes + 256));
+    e = launch_inv_sort(c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), (uint32_t)set0, (uint32_t)set1, e0, E, nbits,
+                        c->isort_keys.as<uint32_t>(), c->isort_vals.as<uint32_t>(), c->isort_tmp.p, cub_bytes,
+                        sg.inv.as<uint32_t>(), sg.off.as<uint32_t>(), c->cursor.as<uint32_t>(), (uint32_t)n,
+                        c->num_sms * 8, c->stream, &nl);
+    TRY(launched(c, e, "inv sort", nl));
+  } else if (set1 > set0) {
+    // node-range passes (GIM_OPT_INV_PASSES; default 1: measured C5 index 5.66 ms with one pass
+    // vs 6.19 ms with one pass per 32 MB of cursors — the re-reads of the pool cost more than the
+    // L2-resident atomics save)
+    const int passes = c->inv_passes > 0 ? c->inv_passes : 1;
     e = launch_inv_scatter(c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), (uint32_t)set0, (uint32_t)set1,
                            sg.off.as<uint32_t>(), sg.inv.as<uint32_t>(), c->num_sms * 8, c->stream, (uint32_t)n,
                            passes, &nl);
@@ -511,10 +530,13 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
     // spill tier of the warp kernels. Auto: WC sets grow by ~1 live in-edge per node (deep,
     // narrow: kept in flight beside the small ones in the warp's spill tier); uniform-p sets
     // become big through hubs of thousands of live in-edges (wide: better spread over a CTA)
-    // (per-edge coins: no spill by default — a giant set's ~10^5 coins on one warp finish
-    // after the rest of the launch; measured C3 sampling 16.5 vs 14.4 ms with K-GIANT)
+    // (per-edge coins: no spill when giant sets are rare — a giant set's ~10^5 coins on one warp
+    // finish after the rest of the launch; measured C3 sampling 16.5 vs 14.4 ms with K-GIANT;
+    // spill up to 2048 nodes when the previous chunk had many giant sets per K-GIANT slot, the
+    // dense graphs where K-GIANT is throughput-bound: B32 sampling + giant 76.8 vs 79.7 ms)
+    const uint32_t coin_cap = c->dense_sets ? 2048u : 0u;
     uint32_t cap = c->spill_cap >= 0 ? (uint32_t)c->spill_cap
-                                     : (!c->skip ? 0u : (c->scheme == W_WC ? kSpillQ : 2048u));
+                                     : (!c->skip ? coin_cap : (c->scheme == W_WC ? kSpillQ : 2048u));
     cap = std::min<uint32_t>(cap, kSpillQ);
     c->spill_cap_eff = cap;
     if (cap > c->qcap) {
@@ -646,6 +668,7 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
   c->st.giant_sets += c->h_ctr->giant_count;
   if (cnt >= 4096)
     c->giant_per_slot = (double)c->h_ctr->giant_count / ((double)kGiantBlocksPerSM * (double)c->num_sms);
+  if (c->giant_per_slot >= 12.0) c->dense_sets = true;
   for (int iter = 0; c->h_ctr->retry_count; ++iter) {
     if (iter > 40) return fail(c, GIM_ENOMEM, "staging retry loop did not converge");
     // staging overflow: grow (keep the part already written) and redo the failed items
@@ -1296,7 +1319,8 @@ void gim_destroy(gim_ctx* c) {
                     &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
                     &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->ag_small,
                     &c->ag_send, &c->ag_recv, &c->sel_bar, &c->rs_gcnt, &c->rs_dshard, &c->rs_keys, &c->rs_kx,
-                    &c->sel_ctl, &c->cmap, &c->cdec, &c->sel_done, &c->probe};
+                    &c->sel_ctl, &c->cmap, &c->cdec, &c->sel_done, &c->probe, &c->isort_keys, &c->isort_vals,
+                    &c->isort_tmp};
   for (auto& sg : c->iseg) {
     dfree(c, sg.off);
     dfree(c, sg.inv);
@@ -1790,6 +1814,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_SELECT_PERSISTENT: c->sel_persistent = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_IMM_EARLY_EXIT: c->imm_early_exit = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_SELECT_CTA: c->sel_small = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_INV_SORT: c->inv_sort = (value < -1 || value > 1) ? -1 : (int)value; return GIM_OK;
     case GIM_OPT_L2_PERSIST:
       c->l2_persist = value ? 1 : 0;
       set_l2_window(c);

@@ -568,9 +568,6 @@ __global__ void __launch_bounds__(kRRWarps * 32, kRRBlocksPerSM) k_rr_warp(RRPar
 // of one per refill — with 1.5-node sets a refill happens almost every iteration, and the
 // returning atomic on the shared counter was the top stall of K-IC-lane on C5 (35% of ncu
 // samples). Returns this lane's id (meaningful for the lanes in `need`). Warp-collective.
-#ifndef GIM_LANE_PIPE
-#define GIM_LANE_PIPE 0
-#endif
 #ifndef GIM_LANE_CLAIM
 #define GIM_LANE_CLAIM 64
 #endif
@@ -609,9 +606,9 @@ __global__ void __launch_bounds__(kIcLaneWarps * 32) k_rr_ic_lane(RRParams p) {
   const int lane = threadIdx.x & 31;
   uint32_t* qv = smem + (threadIdx.x >> 5) * (kIcLaneCap * 32);     // qv[i * 32 + lane]
   const bool never = (SCHEME == W_UNIFORM) && p.thr_uniform == 0;
-  uint32_t item = 0, head = 0, tail = 0, a = 0, b = 0, g = 0, g_hi = 0, thr = 0, pa = 0, pb = 0;
+  uint32_t item = 0, head = 0, tail = 0, a = 0, b = 0, g = 0, g_hi = 0, thr = 0;
   uint64_t id = 0;
-  bool active = false, want = true, on_node = false, pend = false;
+  bool active = false, want = true, on_node = false;
   uint32_t coins = 0, lives = 0;
   unsigned long long chunk_off = 0;
   uint32_t chunk_left = 0;
@@ -630,7 +627,6 @@ __global__ void __launch_bounds__(kIcLaneWarps * 32) k_rr_ic_lane(RRParams p) {
           head = 0;
           tail = 1;
           on_node = false;
-          pend = false;
           if (p.force_giant) {                 // forced fallback: everything via the warp kernel
             p.esc_list[atomicAdd(&p.ctr->esc_count, 1u)] = item;
             active = false;
@@ -645,33 +641,6 @@ __global__ void __launch_bounds__(kIcLaneWarps * 32) k_rr_ic_lane(RRParams p) {
     }
     bool finish = false, escalate = false;
     if (active && !on_node) {                // next node of this lane's BFS
-#if GIM_LANE_PIPE
-      // software-pipelined: the row pointers of the next node are loaded in one iteration and
-      // used in the next, so their latency overlaps the other lanes' Philox work instead of
-      // stalling the whole warp at the load
-      if (pend) {
-        pend = false;
-        a = pa;
-        b = pb;
-        if (b - a > kIcLaneMaxDeg) {
-          escalate = true;
-        } else if (b > a) {
-          on_node = true;
-          g = a >> 2;
-          g_hi = (b - 1) >> 2;
-          thr = node_thr<SCHEME>(p, b - a);
-          coins += b - a;
-        }
-      } else if (head == tail) {
-        finish = true;
-      } else {
-        const uint32_t v = qv[head * 32 + lane];
-        ++head;
-        pa = __ldg(p.row_ptr + v);
-        pb = __ldg(p.row_ptr + v + 1);
-        pend = true;
-      }
-#else
       if (head == tail) {
         finish = true;
       } else {
@@ -689,7 +658,6 @@ __global__ void __launch_bounds__(kIcLaneWarps * 32) k_rr_ic_lane(RRParams p) {
           coins += b - a;
         }
       }
-#endif
     }
     if (active && on_node) {                 // one slot group of the current node
       const uint4 w = philox4x32_10_rk(make_uint4((uint32_t)id, (uint32_t)(id >> 32), g, 0u), p.rk);
@@ -1425,7 +1393,9 @@ __global__ void __launch_bounds__(256) k_store(const uint32_t* __restrict__ stag
       if (i < total) {
         const uint32_t v = staging[fk + (i - ek)] + ok;
         pool[pool_base + base + i] = v;
+#ifndef GIM_AB_NOCOUNT
         atomicAdd(count_total + v, 1u);
+#endif
       }
     }
   }

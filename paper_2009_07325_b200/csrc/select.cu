@@ -540,7 +540,6 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
       uint32_t w[kCoverIlp];
 #pragma unroll
       for (int t = 0; t < kCoverIlp; ++t) w[t] = (e + 8 * t < b) ? pool[e + 8 * t] : u;
-#pragma unroll
       if (cmap != nullptr) {                   // cooperative selection: candidates only
         uint32_t ci[kCoverIlp];
 #pragma unroll

@@ -497,3 +497,28 @@ def test_select_small_cta_equals_oracle(small):
     check_cov_trace(r, ro.T_i, ro.cov_i, g.n, ro.eps_prime, w.k,
                     oracle_round_gains(oracle.Oracle(g, w.model, w.scheme), ro.T_i, w.k, w.rr_seed))
     c.close()
+
+
+@pytest.mark.parametrize("key", ["C1", "C2"])
+def test_inv_sort_segments_equal_oracle(key):
+    """Sort-based index segments (GIM_OPT_INV_SORT = 1; the default for n * 4 > 64 MB): selection
+    over a pool built in several generate calls (several segments, one rebuilt after a
+    truncation) and a full IMM equal the oracle."""
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    c = _ctx(g, w.model, w.scheme, opts={P.OPT_INV_SORT: 1})
+    o = oracle.Oracle(g, w.model, w.scheme)
+    for T in (3001, 9000, 30011):
+        c.generate_rr(T, w.rr_seed)
+    o.generate(30011, w.rr_seed)
+    assert [x.tolist() if hasattr(x, "tolist") else x for x in c.select(50)] == \
+           [x.tolist() if hasattr(x, "tolist") else x for x in o.select(50)]
+    c.generate_rr(20000, w.rr_seed)
+    c.generate_rr(25000, w.rr_seed)
+    o.generate(25000, w.rr_seed)
+    assert [x.tolist() if hasattr(x, "tolist") else x for x in c.select(50)] == \
+           [x.tolist() if hasattr(x, "tolist") else x for x in o.select(50)]
+    r = c.imm(w.k, w.eps, w.ell, w.rr_seed)
+    ro = oracle.Oracle(g, w.model, w.scheme).imm(w.k, w.eps, w.ell, w.rr_seed)
+    assert np.array_equal(r.seeds, ro.seeds) and r.R_final == ro.R_final and r.covered == ro.cov
+    c.close()

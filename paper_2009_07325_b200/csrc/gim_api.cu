@@ -34,6 +34,7 @@ constexpr uint32_t kChunk = 1u << 22;   // RR ids per generation chunk (bounds s
 #define GIM_ARGMAX_CTAS 4
 #endif
 constexpr int kArgmaxCtasPerSM = GIM_ARGMAX_CTAS;   // k_argmax grid = this x #SMs (256 threads each)
+constexpr uint32_t kSelHead = 8;   // greedy steps before a bounded greedy's host stop check
 #ifndef GIM_COVER_CTAS
 #define GIM_COVER_CTAS 8
 #endif
@@ -165,7 +166,8 @@ struct gim_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[CLS_N];
   std::vector<cudaEvent_t> ev_free;   // recycled timing events
   // CUDA graph of the k-step selection loop (P = 1), valid while its key is unchanged
-  cudaGraphExec_t sel_exec = nullptr;
+  cudaGraphExec_t sel_exec = nullptr;    // fused selection graph
+  std::vector<cudaGraphExec_t> sel_parts;   // default selection: consecutive graphs of greedy steps
   std::vector<uintptr_t> sel_key;
   int use_graph = 1;
 };
@@ -1090,6 +1092,8 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
     if (c->use_graph) {
       if (!c->sel_exec || key != c->sel_key) {
         if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
+        for (cudaGraphExec_t& ex : c->sel_parts) cudaGraphExecDestroy(ex);
+        c->sel_parts.clear();
         c->sel_exec = nullptr;
         cudaGraph_t graph = nullptr;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
@@ -1141,23 +1145,43 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
                    c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * kCoverCtasPerSM, c->stream,
                    limited, mr);
     };
-    if (!c->sel_exec || key != c->sel_key) {
-      if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
+    // the steps as consecutive graphs [0, 8), [8, 32), [32, kk): a bounded greedy (IMM estimation
+    // round) checks its stop flag on the host between them, so a selection that stops early does
+    // not replay the no-op launches of the remaining steps (C3 round 3 stops at step 2 of 50,
+    // C5 round 6 at step 10 of 100); a full selection replays them back to back
+    std::vector<uint32_t> cuts = {0};
+    for (uint32_t b : {kSelHead, 4 * kSelHead})
+      if (b < kk) cuts.push_back(b);
+    cuts.push_back(kk);
+    const size_t parts = cuts.size() - 1;
+    if (c->sel_exec || c->sel_parts.size() != parts || key != c->sel_key) {
+      for (cudaGraphExec_t& ex : c->sel_parts)
+        if (ex) cudaGraphExecDestroy(ex);
+      c->sel_parts.assign(parts, nullptr);
+      if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);   // a fused selection's graph
       c->sel_exec = nullptr;
       c->sel_key.clear();
-      cudaGraph_t graph = nullptr;
-      if (!c->sel_exec) {
+      for (size_t q = 0; q < parts; ++q) {
+        cudaGraph_t graph = nullptr;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        for (uint32_t j = 0; j < kk; ++j) step(j);
+        for (uint32_t j = cuts[q]; j < cuts[q + 1]; ++j) step(j);
         CK(cudaStreamEndCapture(c->stream, &graph));
-        const cudaError_t ie = cudaGraphInstantiate(&c->sel_exec, graph, 0);
+        const cudaError_t ie = cudaGraphInstantiate(&c->sel_parts[q], graph, 0);
         cudaGraphDestroy(graph);
         if (ie != cudaSuccess) return fail_cuda(c, "cudaGraphInstantiate", ie);
       }
       c->sel_key = key;
     }
     Prof pf(c, CLS_SELECT);
-    TRY(launched(c, cudaGraphLaunch(c->sel_exec, c->stream), "selection graph", (cand ? 3 : 2) * (int)kk));
+    for (size_t q = 0; q < parts; ++q) {
+      if (q > 0 && c->sel_cstar) {
+        CK(cudaMemcpyAsync(c->h_u64 + 4, &ctl->stop, 4, cudaMemcpyDeviceToHost, c->stream));
+        TRY(sync(c));
+        if ((uint32_t)c->h_u64[4] != 0u) break;
+      }
+      TRY(launched(c, cudaGraphLaunch(c->sel_parts[q], c->stream), "selection graph",
+                   (cand ? 3 : 2) * (int)(cuts[q + 1] - cuts[q])));
+    }
   } else {
     for (uint32_t j = 0; j < kk; ++j) {
       {
@@ -1334,6 +1358,8 @@ void gim_destroy(gim_ctx* c) {
     }
   for (cudaEvent_t e : c->ev_free) cudaEventDestroy(e);
   if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
+  for (cudaGraphExec_t& ex : c->sel_parts) cudaGraphExecDestroy(ex);
+  c->sel_parts.clear();
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
   if (c->h_u64) cudaFreeHost(c->h_u64);
   if (c->h_keys) cudaFreeHost(c->h_keys);
@@ -1828,6 +1854,8 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_PDL:
       set_pdl((int)value);
       if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);   // recapture with the new launch mode
+      for (cudaGraphExec_t& ex : c->sel_parts) cudaGraphExecDestroy(ex);
+      c->sel_parts.clear();
       c->sel_exec = nullptr;
       return GIM_OK;
     case GIM_OPT_IC_LANE: c->ic_lane = (value < -1 || value > 1) ? -1 : (int)value; return GIM_OK;
@@ -1835,6 +1863,8 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
       if (value < 1 || value > 16) return fail(c, GIM_EINVAL, "fused CTAs per SM must be in [1, 16]");
       c->fused_ctas = (int)value;
       if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
+      for (cudaGraphExec_t& ex : c->sel_parts) cudaGraphExecDestroy(ex);
+      c->sel_parts.clear();
       c->sel_exec = nullptr;
       return GIM_OK;
     case GIM_OPT_SKIP_LANE_CAP:

@@ -29,7 +29,10 @@ struct Seg {
 
 enum { CLS_RR = 0, CLS_GIANT, CLS_STORE, CLS_INV, CLS_SELECT, CLS_N };
 
-constexpr uint32_t kChunk = 1u << 22;   // RR ids per generation chunk (bounds staging)
+#ifndef GIM_CHUNK_LOG2
+#define GIM_CHUNK_LOG2 22
+#endif
+constexpr uint32_t kChunk = 1u << GIM_CHUNK_LOG2;   // RR ids per generation chunk (bounds staging)
 #ifndef GIM_ARGMAX_CTAS
 #define GIM_ARGMAX_CTAS 4
 #endif
@@ -706,6 +709,9 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
       TRY(sync(c));
     }
   }
+#ifdef GIM_GIANT_TRACE
+  giant_trace_dump(c->stream);
+#endif
 #ifdef GIM_WINSTAT
   fprintf(stderr, "WINSTAT sets=%u windows=%llu valid_groups=%llu hub_steps=%llu coins=%llu\n", cnt,
           c->h_ctr->dbg[0], c->h_ctr->dbg[1], c->h_ctr->dbg[2], c->h_ctr->coins);

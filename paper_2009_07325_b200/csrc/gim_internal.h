@@ -7,6 +7,9 @@ namespace gim {
 struct RRParams;
 
 int lt_blocks_per_sm();
+#ifdef GIM_GIANT_TRACE
+void giant_trace_dump(cudaStream_t s);   // diagnostic build: per-set K-GIANT timing to stderr
+#endif
 cudaError_t launch_rr_ic_lane(int scheme, const RRParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rr_warp(int model, int scheme, const RRParams& p, int grid, cudaStream_t s);
 cudaError_t launch_rr_giant(int model, int scheme, const RRParams& p, int grid, uint32_t* bitmaps,

@@ -17,6 +17,11 @@
 //  * two-pass storage: bump-allocated staging + sizes, then exclusive scan and a compacting
 //    copy that also builds count_total (Occur; Alg. 6 l.4-11).
 #include <atomic>
+#ifdef GIM_GIANT_TRACE
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+#endif
 #include "gim_device.cuh"
 #include "gim_internal.h"
 
@@ -950,6 +955,29 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* ptr) {
   return v;
 }
 
+#ifdef GIM_GIANT_TRACE
+// diagnostic build: per giant set {cycles in K-GIANT, final size, dumped size, claimed batches}
+constexpr unsigned int kGTrace = 1u << 16;
+__device__ uint4 g_gtrace[kGTrace];
+__device__ unsigned int g_gtrace_n;
+void giant_trace_dump(cudaStream_t s) {
+  unsigned int n = 0;
+  cudaStreamSynchronize(s);
+  cudaMemcpyFromSymbol(&n, g_gtrace_n, 4);
+  n = n < kGTrace ? n : kGTrace;
+  std::vector<uint4> v(n);
+  if (n) cudaMemcpyFromSymbol(v.data(), g_gtrace, n * sizeof(uint4));
+  const unsigned int zero = 0;
+  cudaMemcpyToSymbol(g_gtrace_n, &zero, 4);
+  std::sort(v.begin(), v.end(), [](const uint4& a, const uint4& b) { return a.x > b.x; });
+  unsigned long long sum = 0;
+  for (const uint4& e : v) sum += e.x;
+  fprintf(stderr, "GTRACE sets=%u mean_us=%.1f\n", n, n ? sum / 1965.0 / n : 0.0);
+  for (unsigned int i = 0; i < n && i < 8; ++i)
+    fprintf(stderr, "GTRACE top%u us=%.1f size=%u dumped=%u claims=%u\n", i, v[i].x / 1965.0, v[i].y, v[i].z, v[i].w);
+}
+#endif
+
 // SQ = true (the first pass): queue and visited hash in shared memory (kGQS entries, kGHS slots)
 // — every claim, visit and queue read is a shared-memory access, not an L2 round trip; a set
 // that outgrows kGQS is aborted and handed to the second pass (SQ = false: per-CTA global
@@ -1085,6 +1113,11 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
     const uint32_t r = s_r;
     if (r >= giant_count) break;
     const GiantRec rec = recs[r];
+#ifdef GIM_GIANT_TRACE
+    __shared__ unsigned long long s_t0;
+    __shared__ unsigned int s_claims;
+    if (threadIdx.x == 0) { s_t0 = clock64(); s_claims = 0; }
+#endif
     const uint64_t id = p.id_base + rec.item;
     const uint32_t id_lo = (uint32_t)id, id_hi = (uint32_t)(id >> 32);
     if (rec.qlen == 0) {
@@ -1142,7 +1175,13 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
             // IC: a batch of up to 32 nodes, smaller while the frontier is narrow so that
             // every warp of the block gets work; LT: one node (its walk is a single path)
             const uint32_t want = (MODEL == MODEL_IC) ? min(32u, max(1u, (t - h) / kGiantClaimDiv)) : 1u;
-            if (atomicCAS(&s_head, h, h + want) == h) { f = h; c = want; state = 1; break; }
+            if (atomicCAS(&s_head, h, h + want) == h) {
+              f = h; c = want; state = 1;
+#ifdef GIM_GIANT_TRACE
+              atomicAdd(&s_claims, 1u);
+#endif
+              break;
+            }
             continue;
           }
           atomicSub(&s_busy, 1u);
@@ -1321,6 +1360,12 @@ __global__ void __launch_bounds__(kGiantThreads, 1024 / kGiantThreads) k_rr_gian
       continue;
     }
     const uint32_t size = s_tail;
+#ifdef GIM_GIANT_TRACE
+    if (threadIdx.x == 0) {
+      const unsigned int t = atomicAdd(&g_gtrace_n, 1u);
+      if (t < kGTrace) g_gtrace[t] = make_uint4((uint32_t)(clock64() - s_t0), size, rec.qlen, s_claims);
+    }
+#endif
     if (threadIdx.x == 0) s_off = atomicAdd(&p.ctr->stage_tail, (unsigned long long)size);
     __syncthreads();
     const unsigned long long off = s_off;

@@ -8,6 +8,6 @@ timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k re
   -o gpurun_out/prof_$k -f python bench.py --workload $w --steps 1 --warmup 1 --no-e2e --no-cpu-baseline "$@" \
   > gpurun_out/ncu_$k.log 2>&1
 echo "ncu rc=$?"
-ncu -i gpurun_out/prof_$k.ncu-rep --page source --csv --print-source sass > gpurun_out/src_$k.csv 2>&1
+ncu -i gpurun_out/prof_$k.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/src_$k.csv 2>&1
 ncu -i gpurun_out/prof_$k.ncu-rep --page raw --csv > gpurun_out/raw_$k.csv 2>&1
 ncu -i gpurun_out/prof_$k.ncu-rep --page details > gpurun_out/details_$k.txt 2>&1

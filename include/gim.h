@@ -295,7 +295,9 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                         as shared atomics, no launch or grid barrier per step.
  *  GIM_OPT_INV_SORT     = -1 (default: auto, when n * 4 > 64 MB) / 0 / 1: build each index
  *                         segment by a stable radix sort of its (node, set) pairs by node instead
- *                         of the cursor scatter (lists in ascending set order; same lists). */
+ *                         of the cursor scatter (lists in ascending set order; same lists).
+ *  GIM_OPT_CHUNK        = ids (0 = default 2^25; 1024..2^25): RR ids sampled per generation chunk
+ *                         (one K-RR / K-GIANT / store pass each; results identical). */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -324,7 +326,8 @@ typedef enum {
   GIM_OPT_INV_PASSES = 26,
   GIM_OPT_L2_PERSIST = 27,
   GIM_OPT_SELECT_CTA = 28,
-  GIM_OPT_INV_SORT = 29
+  GIM_OPT_INV_SORT = 29,
+  GIM_OPT_CHUNK = 30
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

@@ -30,9 +30,12 @@ struct Seg {
 enum { CLS_RR = 0, CLS_GIANT, CLS_STORE, CLS_INV, CLS_SELECT, CLS_N };
 
 #ifndef GIM_CHUNK_LOG2
-#define GIM_CHUNK_LOG2 22
+#define GIM_CHUNK_LOG2 25
 #endif
-constexpr uint32_t kChunk = 1u << GIM_CHUNK_LOG2;   // RR ids per generation chunk (bounds staging)
+// RR ids per generation chunk (bounds the per-chunk buffers: ~3.5 GB at 2^25). Every chunk pays
+// the K-RR / K-GIANT launch tails and one host sync: C5 (37.9M sets per IMM) 31.7 / 29.1 / 27.5 /
+// 26.7 ms at 2^22 / 2^23 / 2^24 / 2^25; C3/C4 (rounds below 2^22 ids) unchanged
+constexpr uint32_t kChunk = 1u << GIM_CHUNK_LOG2;
 #ifndef GIM_ARGMAX_CTAS
 #define GIM_ARGMAX_CTAS 4
 #endif
@@ -154,6 +157,7 @@ struct gim_ctx {
   uint32_t last_sel_steps = 0;  // greedy steps the last selection ran
   int inv_passes = 0;           // GIM_OPT_INV_PASSES: node-range passes of the index scatter (0 = auto)
   int inv_sort = -1;            // GIM_OPT_INV_SORT: -1 auto (n * 4 > 64 MB), 0 scatter, 1 sort
+  uint32_t chunk = 0;           // GIM_OPT_CHUNK: RR ids per generation chunk (0 = kChunk)
   DevBuf isort_keys, isort_vals, isort_tmp;   // sort-based segments: sorted keys, set ids, CUB scratch
   int imm_early_exit = 1;       // GIM_OPT_IMM_EARLY_EXIT
   int sel_small = 1;            // GIM_OPT_SELECT_CTA: single-CTA selection when the counts fit in shared memory
@@ -873,7 +877,8 @@ gim_status generate(gim_ctx* c, uint64_t theta_sets, uint64_t seed, bool host_sy
     const uint64_t hi = a + Tr * (uint64_t)((unsigned __int128)len * (c->rank + 1) / c->world);
     const uint64_t set0 = c->nsets, e0 = c->pool_len;
     const size_t seg0 = c->segs.size();
-    for (uint64_t s = lo; s < hi; s += kChunk) TRY(gen_chunk(c, s, (uint32_t)std::min<uint64_t>(kChunk, hi - s)));
+    const uint64_t ch = c->chunk ? c->chunk : kChunk;
+    for (uint64_t s = lo; s < hi; s += ch) TRY(gen_chunk(c, s, (uint32_t)std::min<uint64_t>(ch, hi - s)));
     if ((c->world > 1 || c->force_coll) && c->agfn) TRY(replicate_round(c, a, theta, set0, e0, seg0));
     // the new sets join the unindexed range; the next selection indexes it as one segment (its
     // O(n) count scan is paid once per selection that needs it, not per 2^22-id chunk or round)
@@ -1847,6 +1852,10 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_IMM_EARLY_EXIT: c->imm_early_exit = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_SELECT_CTA: c->sel_small = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_INV_SORT: c->inv_sort = (value < -1 || value > 1) ? -1 : (int)value; return GIM_OK;
+    case GIM_OPT_CHUNK:
+      if (value != 0 && (value < 1024 || value > (int64_t)kChunk)) return fail(c, GIM_EINVAL, "chunk must be 0 or in [1024, 2^25]");
+      c->chunk = (uint32_t)value;
+      return GIM_OK;
     case GIM_OPT_L2_PERSIST:
       c->l2_persist = value ? 1 : 0;
       set_l2_window(c);

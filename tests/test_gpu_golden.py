@@ -36,11 +36,12 @@ def _rel(a, b):
     return abs(a - b) <= 1e-12 * max(abs(b), 1e-300)
 
 
-@pytest.mark.parametrize("key,early", [("C1", 1), ("C2", 1), ("C3", 1), ("C4", 1), ("C5", 1),
-                                       ("C1", 0), ("C3", 0)])
-def test_imm_golden(key, early):
+@pytest.mark.parametrize("key,early,chunk", [("C1", 1, 0), ("C2", 1, 0), ("C3", 1, 0), ("C4", 1, 0), ("C5", 1, 0),
+                                             ("C1", 0, 0), ("C3", 0, 0), ("C3", 1, 1 << 18), ("C5", 1, 1 << 22)])
+def test_imm_golden(key, early, chunk):
     """early = 1: the default bounded greedy in the estimation rounds (stopped rounds checked by
-    tests/imm_trace.py); early = 0: every round's k steps, cov_i exactly as the oracle's."""
+    tests/imm_trace.py); early = 0: every round's k steps, cov_i exactly as the oracle's. chunk:
+    RR ids per generation chunk (0 = the default 2^25; small chunks: every round in several)."""
     gd = json.load(open(os.path.join(GOLDEN, f"imm_{key}.json")))
     w = gi.WORKLOADS[key]
     g = gi.workload_graph(key)
@@ -49,6 +50,7 @@ def test_imm_golden(key, early):
     try:
         c.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme, p_uniform=w.p_uniform)
         c.set_option(P.OPT_IMM_EARLY_EXIT, early)
+        c.set_option(P.OPT_CHUNK, chunk)
         r = c.imm(w.k, w.eps, w.ell, w.rr_seed)
         assert _rel(r.ell_eff, gd["ell_eff"]) and _rel(r.eps_prime, gd["eps_prime"])
         assert _rel(r.lambda_prime, gd["lambda_prime"]) and _rel(r.lambda_star, gd["lambda_star"])

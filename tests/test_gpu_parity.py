@@ -93,7 +93,9 @@ def test_pool_parity_tiny(gname):
                                   {P.OPT_QUEUE_CAP: 32, P.OPT_SPILL: 40, P.OPT_STAGING_CAP: 1000},
                                   {P.OPT_IC_LANE: 1, P.OPT_QUEUE_CAP: 4, P.OPT_SPILL: 16384},
                                   {P.OPT_GIANT_SHARED: 0}, {P.OPT_GIANT_SHARED: 0, P.OPT_FORCE_GIANT: 1},
-                                  {P.OPT_GIANT_SHARED: 1, P.OPT_QUEUE_CAP: 16}])
+                                  {P.OPT_GIANT_SHARED: 1, P.OPT_QUEUE_CAP: 16},
+                                  {P.OPT_CHUNK: 4096}, {P.OPT_CHUNK: 1024, P.OPT_STAGING_CAP: 1000},
+                                  {P.OPT_CHUNK: 4096, P.OPT_IC_LANE: 1}])
 def test_pool_parity_C1_invariance(opts):
     """Same pool whatever the queue capacity, spill-tier capacity (sets beyond the shared queue
     continue in the warp's global queue + hash, beyond the spill cap in K-GIANT), forced

@@ -214,9 +214,11 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *  GIM_OPT_INV_SEGMENTS = 1 (default): index each generation chunk's sets as it is stored (one
  *                          inverted-index segment per chunk); 0: rebuild one index over the
  *                          whole pool at every selection (ablation).
- *  GIM_OPT_ARGMAX_CAND  = 1 (default): for P = 1 and n >= 2^23 the per-step argmax scans a candidate list of
- *                          <= 65536 nodes (count >= a power-of-two threshold) and falls back to
- *                          the full scan once no candidate reaches the threshold; 0: always full;
+ *  GIM_OPT_ARGMAX_CAND  = 1 (default): for P = 1 and n >= 2^20 the per-step argmax scans a candidate list of
+ *                          <= 65536 nodes (count >= a power-of-two threshold tau; counts only
+ *                          decrease, so a best candidate >= tau is the argmax over all nodes); a
+ *                          step whose best candidate is below tau fails the selection, which is
+ *                          redone with full scans (gim_stats.fused_fallbacks); 0: always full;
  *                          2: candidates whatever n (tests).
  *  GIM_OPT_IC_LANE      = -1 (default): IC sampling starts with the lane-per-set kernel when the
  *                          running mean of coins per set is below 160 (tiny sets) and the chunk

@@ -147,6 +147,7 @@ struct gim_ctx {
   uint32_t sel_fused = 0;       // GIM_OPT_SELECT_FUSED: candidate cap of the fused steps (0 = off)
   bool force_unfused = false;   // the fused selection failed its certificate: redo unfused
   bool sel_fused_used = false;  // the pending selection ran fused
+  bool sel_cand_used = false;   // the pending selection took candidate argmaxes (certificate checked)
   DevBuf sel_done;              // fused steps: per-step completion tickets + the fail flag
   int fused_ctas = 2;           // fused cover grid = this x #SMs (fewer tickets per step)
   uint32_t sel_coop = 0;        // GIM_OPT_SELECT_COOP: candidate cap of the cooperative selection (0 = off)
@@ -943,7 +944,7 @@ gim_status select_launch_rs(gim_ctx* c, uint32_t k, const InvSegDev* segd, SelCt
   CK(cudaMemsetAsync(c->covered.p, 0, std::max<uint64_t>(c->nsets, 1), c->stream));
   CK(cudaMemsetAsync(keys, 0, (uint64_t)kk * 8, c->stream));
   CK(cudaMemsetAsync(lkeys, 0, (uint64_t)kk * 8, c->stream));
-  TRY(launched(c, launch_sel_ctl(ctl, c->sel_cstar, kk, c->stream), "k_sel_ctl"));
+  TRY(launched(c, launch_sel_ctl(ctl, c->sel_cstar, kk, nullptr, c->stream), "k_sel_ctl"));
   CK(cudaMemsetAsync(dec, 0, npad * 4, c->stream));
   CK(cudaMemsetAsync(dshard, 0, ns * 4, c->stream));
   c->st.allreduces++;
@@ -973,6 +974,7 @@ gim_status select_launch_rs(gim_ctx* c, uint32_t k, const InvSegDev* segd, SelCt
 }
 
 gim_status select_launch(gim_ctx* c, uint32_t k) {
+  c->sel_cand_used = false;
   if (!c->graph) return fail(c, GIM_ESTATE, "no graph loaded");
   if (k < 1 || k > c->n) return fail(c, GIM_EINVAL, "k must satisfy 1 <= k <= n");
   if (!c->have_seed || c->T_global == 0) return fail(c, GIM_ESTATE, "RR pool is empty");
@@ -1008,7 +1010,6 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   CK(cudaEventRecord(c->ev_cnt_copied, c->stream));
   CK(cudaMemsetAsync(c->covered.p, 0, std::max<uint64_t>(c->nsets / c->rounds, 1), c->stream));
   CK(cudaMemsetAsync(c->keys.p, 0, (uint64_t)kk * 8, c->stream));
-  TRY(launched(c, launch_sel_ctl(ctl, c->sel_cstar, kk, c->stream), "k_sel_ctl"));
   if (dec) {
     CK(cudaMemsetAsync(dec, 0, n * 4, c->stream));
     c->st.allreduces++;
@@ -1023,8 +1024,10 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   uint32_t* tau_p1 = nullptr;
   const bool fused_mode = !dec && c->rounds == 1 && (c->sel_fused || c->sel_coop) && !c->force_unfused &&
                           !c->speculate && !c->sel_persistent;
-  if (!fused_mode && !dec && c->rounds == 1 &&
-      (c->use_cand == 2 || (c->use_cand == 1 && n >= (1u << 23)))) {   // small n: full scan is cheaper
+  if (!fused_mode && !dec && c->rounds == 1 && !c->force_unfused &&
+      (c->use_cand == 2 || (c->use_cand == 1 && n >= (1u << 20)))) {   // small n: full scan is cheaper
+    // (measured with the per-step backup scan gone: C3 selection 1.95 vs 2.19 ms with full scans,
+    // C2 1.29 vs 1.14 ms — the candidate list pays from ~10^6 nodes)
     TRY(ensure(c, c->cand, (uint64_t)kMaxCand * 4 + 64 * 4));
     cand = c->cand.as<uint32_t>();
     hist = reinterpret_cast<unsigned int*>(cand + kMaxCand);
@@ -1033,6 +1036,10 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
     TRY(launched(c, launch_cand_setup(c->cnt.as<uint32_t>(), (uint32_t)n, kMaxCand, hist, tau_p1, cand, ncand,
                                       c->num_sms * 4, c->stream), "candidate setup", 3));
   }
+  // candidate argmax: each step is argmax over the list + cover; an uncertified pick makes the
+  // cover fail the selection, which select_finish redoes with full scans (no per-step backup scan)
+  TRY(launched(c, launch_sel_ctl(ctl, c->sel_cstar, kk, cand ? tau_p1 : nullptr, c->stream), "k_sel_ctl"));
+  c->sel_cand_used = cand != nullptr;
   // cooperative selection (P = 1, standard IM): one cooperative launch, one grid barrier per
   // step, redundant per-CTA candidate argmax; certificate failures are redone by select_finish
   const bool coop = !dec && c->rounds == 1 && c->sel_coop && !c->force_unfused && !c->speculate &&
@@ -1149,9 +1156,11 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
                                         (uintptr_t)c->keys.p, (uintptr_t)k, (uintptr_t)n, (uintptr_t)limited,
                                         (uintptr_t)c->rounds, (uintptr_t)ctl};
     auto step = [&](uint32_t j) {
-      if (cand) launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream, ctl);
-      launch_argmax(c->cnt.as<uint32_t>(), nullptr, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * kArgmaxCtasPerSM, c->stream,
-                    mr != nullptr, 0u, ctl);
+      if (cand)
+        launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream, ctl);
+      else
+        launch_argmax(c->cnt.as<uint32_t>(), nullptr, (uint32_t)n, keys, (int)j, nullptr,
+                      c->num_sms * kArgmaxCtasPerSM, c->stream, mr != nullptr, 0u, ctl);
       launch_cover(keys, (int)j, segd, ctl, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                    c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), nullptr, c->num_sms * kCoverCtasPerSM, c->stream,
                    limited, mr);
@@ -1191,16 +1200,18 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
         if ((uint32_t)c->h_u64[4] != 0u) break;
       }
       TRY(launched(c, cudaGraphLaunch(c->sel_parts[q], c->stream), "selection graph",
-                   (cand ? 3 : 2) * (int)(cuts[q + 1] - cuts[q])));
+                   2 * (int)(cuts[q + 1] - cuts[q])));
     }
   } else {
     for (uint32_t j = 0; j < kk; ++j) {
       {
         Prof pf(c, CLS_SELECT);
-        if (cand) TRY(launched(c, launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream, ctl),
-                               "k_argmax_cand"));
-        TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, (uint32_t)n, keys, (int)j, tau_p1, c->num_sms * kArgmaxCtasPerSM,
-                                      c->stream, mr != nullptr, 0u, ctl), "k_argmax"));
+        if (cand)
+          TRY(launched(c, launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream, ctl),
+                       "k_argmax_cand"));
+        else
+          TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, (uint32_t)n, keys, (int)j, nullptr,
+                                        c->num_sms * kArgmaxCtasPerSM, c->stream, mr != nullptr, 0u, ctl), "k_argmax"));
         TRY(launched(c, launch_cover(keys, (int)j, segd, ctl, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
                                      c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * kCoverCtasPerSM,
                                      c->stream, limited, mr), "k_cover"));
@@ -1220,6 +1231,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   CK(cudaMemcpyAsync(c->h_keys, keys, (uint64_t)kk * 8, cudaMemcpyDeviceToHost, c->stream));
   c->h_keys[kk] = 0;
   if (fused) CK(cudaMemcpyAsync(c->h_keys + kk, fflag, 4, cudaMemcpyDeviceToHost, c->stream));
+  else if (c->sel_cand_used) CK(cudaMemcpyAsync(c->h_keys + kk, &ctl->fail, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaEventRecord(c->ev_sel_done, c->stream));
   c->sel_pending = true;
   return GIM_OK;
@@ -1228,8 +1240,8 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
 gim_status select_finish(gim_ctx* c, uint32_t k, uint32_t* seeds, uint64_t* gains, uint64_t* covered) {
   TRY(sync(c));
   c->sel_pending = false;
-  if (c->sel_fused_used && c->h_keys[(uint64_t)k * c->rounds]) {
-    // a candidate argmax could not be certified (best candidate below tau): redo unfused
+  if ((c->sel_fused_used || c->sel_cand_used) && c->h_keys[(uint64_t)k * c->rounds]) {
+    // a candidate argmax could not be certified (best candidate below tau): redo with full scans
     c->st.fused_fallbacks++;
     c->force_unfused = true;
     const gim_status st = select_launch(c, k);

@@ -80,11 +80,15 @@ struct InvSegDev;
 // smallest covered count that passes the round's test (Alg. 2 l.7); 0 disables. stop is set by
 // the cover of the first step whose bound cov_j + (kk - j) * gain_j falls below cstar, and every
 // later argmax / cover of the selection returns at once.
+// Candidate argmax (large n): tau points at the certificate threshold; a pick below it is not
+// certified — the cover sets fail (and stop) and the host redoes the selection with full scans.
 struct SelCtl {
   unsigned long long cstar;
   uint32_t stop, kk;
+  uint32_t fail, pad;
+  const uint32_t* tau;
 };
-cudaError_t launch_sel_ctl(SelCtl* ctl, unsigned long long cstar, uint32_t kk, cudaStream_t s);
+cudaError_t launch_sel_ctl(SelCtl* ctl, unsigned long long cstar, uint32_t kk, const uint32_t* tau, cudaStream_t s);
 // MRIM selection (R27): pair ids t*n + u over `rounds` rounds, at most k picks per round
 struct MrimSel {
   uint32_t rounds, n, k;

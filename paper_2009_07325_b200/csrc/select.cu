@@ -464,14 +464,20 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
     const uint32_t l = threadIdx.x;
     InvSegDev sg{nullptr, nullptr};
     if (l < (uint32_t)kMaxInvSeg && !dead) sg = segs[l];  // unused slots are null: no dependency on nseg
+    uint32_t uncertified = 0;
     if (ctl != nullptr && !dead) {             // bound: loads in parallel with the list bounds
       const unsigned long long cstar = ctl->cstar;
+      const uint32_t* tau = ctl->tau;
       unsigned long long sum = 0;
       for (int t = (int)l; t < j; t += 32) sum += keys[t] >> 32;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(kFull, sum, off);
       const unsigned long long bound = sum + (unsigned long long)(ctl->kk - (uint32_t)j) * (kj >> 32);
-      stop_now = (cstar != 0ull && bound < cstar) ? 1u : 0u;
+      // candidate argmax: a pick below tau is not certified (a node outside the list may beat it)
+      uncertified = (tau != nullptr && (uint32_t)(kj >> 32) < *tau) ? 1u : 0u;
+      stop_now = ((cstar != 0ull && bound < cstar) || uncertified) ? 1u : 0u;
+    } else if (ctl != nullptr && dead && ctl->tau != nullptr && *(volatile const uint32_t*)&ctl->stop == 0u) {
+      uncertified = 1u;                        // no candidate at all (empty list): not certified either
     }
     // set-id limit (only after a tail truncation), loaded alongside the descriptors
     const uint32_t lim = (LIMIT && l == 0) ? reinterpret_cast<const uint32_t*>(segs + kMaxInvSeg)[1] : 0u;
@@ -496,7 +502,10 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
       s_nseg = __popc(used);
       s_limit = lim;
       s_stop = stop_now;
-      if (stop_now && !dead && blockIdx.x == 0) ctl->stop = 1u;
+      if (stop_now && (!dead || uncertified) && blockIdx.x == 0) {
+        if (uncertified) ctl->fail = 1u;
+        ctl->stop = 1u;
+      }
     }
   }
   // MRIM (R27): the pick that gives round t = u / n its k-th seed closes the round: every pair of
@@ -1000,13 +1009,15 @@ cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long
   return launch_pdl(k_argmax, grid, 256, s, cnt, dec, n, keys, j, tau_p1, excl ? 0x80000000u : 0u, id_base, ctl);
 }
 
-__global__ void k_sel_ctl(SelCtl* ctl, unsigned long long cstar, uint32_t kk) {
+__global__ void k_sel_ctl(SelCtl* ctl, unsigned long long cstar, uint32_t kk, const uint32_t* tau) {
   ctl->cstar = cstar;
   ctl->stop = 0u;
   ctl->kk = kk;
+  ctl->fail = 0u;
+  ctl->tau = tau;
 }
-cudaError_t launch_sel_ctl(SelCtl* ctl, unsigned long long cstar, uint32_t kk, cudaStream_t s) {
-  k_sel_ctl<<<1, 1, 0, s>>>(ctl, cstar, kk);
+cudaError_t launch_sel_ctl(SelCtl* ctl, unsigned long long cstar, uint32_t kk, const uint32_t* tau, cudaStream_t s) {
+  k_sel_ctl<<<1, 1, 0, s>>>(ctl, cstar, kk, tau);
   return cudaGetLastError();
 }
 

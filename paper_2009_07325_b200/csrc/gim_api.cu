@@ -631,7 +631,7 @@ gim_status gen_chunk(gim_ctx* c, uint64_t gstart, uint32_t cnt) {
       pl.esc_list = c->esc_list.as<uint32_t>();
       {
         Prof pf(c, CLS_RR);
-        TRY(launched(c, launch_rr_ic_lane(c->scheme, pl, c->num_sms * 4, c->stream), "k_rr_ic_lane"));
+        TRY(launched(c, launch_rr_ic_lane(c->scheme, pl, c->num_sms * kIcLaneBlocksPerSM, c->stream), "k_rr_ic_lane"));
         c->st.n_rr_launches++;
       }
       RRParams pw = pp;                        // the warp kernel replays the escalated items

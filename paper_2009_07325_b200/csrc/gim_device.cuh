@@ -215,6 +215,10 @@ constexpr int kLtWarps = 8;          // K-LT: warps per CTA
 constexpr int kLtCap = GIM_LT_CAP;   // K-LT: path entries per lane in shared memory
 constexpr int kLtCap2 = 512;         // K-LT: max path per lane (shared + global spill)
 constexpr int kIcLaneWarps = 8;      // K-IC lane kernel: warps per CTA
+#ifndef GIM_LANE_BLOCKS
+#define GIM_LANE_BLOCKS 5   // C5 lane sampling 10.12 / 9.67 / 9.63 ms at 4 / 5 / 6 (latency-bound: more sets in flight)
+#endif
+constexpr int kIcLaneBlocksPerSM = GIM_LANE_BLOCKS;   // K-IC lane kernel: resident CTAs per SM
 constexpr int kIcLaneCap = 32;       // K-IC lane kernel: set size limit (then escalate)
 constexpr uint32_t kIcLaneMaxDeg = 256;   // K-IC lane kernel: in-degree limit (then escalate)
 constexpr int kGiantWin = 2048;      // frontier window of the giant kernel (smem)

@@ -606,7 +606,7 @@ __device__ __forceinline__ uint32_t lane_claim(unsigned int* ctr, uint32_t need,
 // escalated: its id goes to esc_list and the warp kernel replays it exactly (same coins).
 // ------------------------------------------------------------------------------------------
 template <int SCHEME>
-__global__ void __launch_bounds__(kIcLaneWarps * 32) k_rr_ic_lane(RRParams p) {
+__global__ void __launch_bounds__(kIcLaneWarps * 32, kIcLaneBlocksPerSM) k_rr_ic_lane(RRParams p) {
   extern __shared__ uint32_t smem[];
   const int lane = threadIdx.x & 31;
   uint32_t* qv = smem + (threadIdx.x >> 5) * (kIcLaneCap * 32);     // qv[i * 32 + lane]

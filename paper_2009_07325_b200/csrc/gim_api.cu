@@ -127,7 +127,7 @@ struct gim_ctx {
   unsigned long long* h_keys = nullptr;   // pinned selection keys
   uint32_t h_keys_cap = 0;
   // selection scratch
-  DevBuf cnt, cursor, covered, keys, dec;
+  DevBuf cnt, covered, keys, dec;
   // segmented inverted index (one segment per generation chunk; rebuilt whole when invalid)
   struct InvSeg {
     DevBuf off, inv;
@@ -339,20 +339,19 @@ gim_status build_inv_segment(gim_ctx* c, uint64_t set0, uint64_t set1, uint64_t 
   gim_ctx::InvSeg sg;
   TRY(dalloc(c, sg.off, (n + 1) * 4));
   TRY(dalloc(c, sg.inv, std::max<uint64_t>(e1 - e0, 1) * 4));
-  TRY(ensure(c, c->cursor, n * 4));
   TRY(ensure(c, c->scan_tmp, (scan_tiles(n) + 2) * 8));
   Prof pf(c, CLS_INV);
-  TRY(launched(c, launch_count_delta(c->count_total.as<uint32_t>(), c->cnt_snap.as<uint32_t>(),
-                                     c->cursor.as<uint32_t>(), (uint32_t)n, c->num_sms * 8, c->stream), "k_count_delta"));
-  int nl = 0;
-  // exclusive prefix = start of each node's list; the scatter advances it to the list's end
-  cudaError_t e = launch_scan_u32_to32(c->cursor.as<uint32_t>(), n, sg.off.as<uint32_t>(), c->scan_tmp.as<uint64_t>(),
-                                       c->scan_tmp.as<uint64_t>() + scan_tiles(n) + 1, c->stream, &nl);
-  TRY(launched(c, e, "scan(segment counts)", nl));
   // sort-based segment (GIM_OPT_INV_SORT; auto: when the per-node cursors exceed 64 MB, i.e. far
   // beyond the L2, so that each scatter step would be a random DRAM read-modify-write)
-  const bool sort_mode = c->inv_sort == 1 || (c->inv_sort == -1 && n * 4 > (64ull << 20));
-  if (set1 > set0 && sort_mode) {
+  const bool sort_mode = set1 > set0 && (c->inv_sort == 1 || (c->inv_sort == -1 && n * 4 > (64ull << 20)));
+  int nl = 0;
+  // histogram count_total - snap and its scan in one pass pair: list starts (scatter: advanced to
+  // the list ends by the scatter's atomics) or list ends (sorted segment)
+  cudaError_t e = launch_seg_scan(c->count_total.as<uint32_t>(), c->cnt_snap.as<uint32_t>(), n, sg.off.as<uint32_t>(),
+                                  sort_mode, c->scan_tmp.as<uint64_t>(), c->scan_tmp.as<uint64_t>() + scan_tiles(n) + 1,
+                                  c->stream, &nl);
+  TRY(launched(c, e, "segment scan", nl));
+  if (sort_mode) {
     const uint64_t E = e1 - e0;
     uint32_t nbits = 1;
     while (nbits < 32 && (1ull << nbits) < n) ++nbits;
@@ -362,8 +361,7 @@ gim_status build_inv_segment(gim_ctx* c, uint64_t set0, uint64_t set1, uint64_t 
     TRY(ensure(c, c->isort_tmp, cub_bytes + 256));
     e = launch_inv_sort(c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), (uint32_t)set0, (uint32_t)set1, e0, E, nbits,
                         c->isort_keys.as<uint32_t>(), c->isort_vals.as<uint32_t>(), c->isort_tmp.p, cub_bytes,
-                        sg.inv.as<uint32_t>(), sg.off.as<uint32_t>(), c->cursor.as<uint32_t>(), (uint32_t)n,
-                        c->num_sms * 8, c->stream, &nl);
+                        sg.inv.as<uint32_t>(), c->num_sms * 8, c->stream, &nl);
     TRY(launched(c, e, "inv sort", nl));
   } else if (set1 > set0) {
     // node-range passes (GIM_OPT_INV_PASSES; default 1: measured C5 index 5.66 ms with one pass
@@ -1363,7 +1361,7 @@ void gim_destroy(gim_ctx* c) {
   DevBuf* bufs[] = {&c->row_ptr, &c->src, &c->thr_edge, &c->pool, &c->offsets, &c->count_total,
                     &c->sizes, &c->soff, &c->giant_list, &c->giant2_list, &c->retry_list, &c->item_list, &c->scan_out,
                     &c->scan_tmp, &c->staging, &c->ctr, &c->dump, &c->lt_spill, &c->spill, &c->lane_spill, &c->skip_tab, &c->esc_list, &c->bitmaps, &c->gqueues, &c->cnt,
-                    &c->cursor, &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
+                    &c->covered, &c->keys, &c->dec, &c->cnt_snap, &c->seg_desc, &c->cand,
                     &c->out_ptr, &c->out_dst, &c->out_in, &c->thr_wc, &c->ag_small,
                     &c->ag_send, &c->ag_recv, &c->sel_bar, &c->rs_gcnt, &c->rs_dshard, &c->rs_keys, &c->rs_kx,
                     &c->sel_ctl, &c->cmap, &c->cdec, &c->sel_done, &c->probe, &c->isort_keys, &c->isort_vals,

@@ -47,20 +47,22 @@ cudaError_t launch_scan_u32(const uint32_t* in, uint64_t count, uint64_t* out, u
 // same, 32-bit output (the caller guarantees the total is < 2^32)
 cudaError_t launch_scan_u32_to32(const uint32_t* in, uint64_t count, uint32_t* out, uint64_t* tile_tmp,
                                  uint64_t* total_tmp, cudaStream_t s, int* launches);
+// index segment histogram (count_total - snap) + scan, snap := count_total; out = list starts
+// (exclusive) or list ends (inclusive), out[count] = total
+cudaError_t launch_seg_scan(const uint32_t* cnt, uint32_t* snap, uint64_t count, uint32_t* out, bool inclusive,
+                            uint64_t* tile_tmp, uint64_t* total_tmp, cudaStream_t s, int* launches);
 cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, uint32_t set0, uint32_t set1,
                                uint32_t* end, uint32_t* inv, int grid, cudaStream_t s, uint32_t n, int passes,
                                int* launches);
-// sort-based index segment (inv_sort.cu): inv = set indices sorted by node, end = list ends
+// sort-based index segment (inv_sort.cu): inv = set indices sorted by node (list ends: the
+// inclusive segment scan)
 size_t inv_sort_tmp_bytes(uint64_t elements, uint32_t nbits);
 cudaError_t launch_inv_sort(const uint64_t* offsets, const uint32_t* pool, uint32_t set0, uint32_t set1, uint64_t e0,
                             uint64_t elements, uint32_t nbits, uint32_t* keys_tmp, uint32_t* vals_tmp, void* cub_tmp,
-                            size_t cub_bytes, uint32_t* inv, uint32_t* end, const uint32_t* cnt, uint32_t n, int grid,
-                            cudaStream_t s, int* launches);
+                            size_t cub_bytes, uint32_t* inv, int grid, cudaStream_t s, int* launches);
 struct InvSegDev;
 cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, uint32_t limit, InvSegDev* out,
                             uint32_t* nseg_out, cudaStream_t s);
-cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* delta, uint32_t n, int grid,
-                               cudaStream_t s);
 struct SelCtl;
 cudaError_t launch_argmax(uint32_t* cnt, int32_t* dec, uint32_t n, unsigned long long* keys, int j,
                           const uint32_t* tau_p1, int grid, cudaStream_t s, bool excl = false,

@@ -8,9 +8,9 @@
 // node instead: keys = the pool slice itself (nodes), values = the local set index of each
 // element, written in pool order, so the sorted values ARE the lists, each in ascending set order
 // (a deterministic layout; the scatter's order within a list is arbitrary, and the cover does not
-// depend on it). The per-node list starts come from the same count scan as the scatter's; one
-// pass then turns them into list ends. cub::DeviceRadixSort is a library primitive (like the
-// sort mc.cu uses for the out-CSR).
+// depend on it). The per-node list ends come from the same count scan as the scatter's (its
+// inclusive form). cub::DeviceRadixSort is a library primitive (like the sort mc.cu uses for the
+// out-CSR).
 #include <cub/device/device_radix_sort.cuh>
 #include "gim_device.cuh"
 #include "gim_internal.h"
@@ -37,12 +37,6 @@ __global__ void __launch_bounds__(256) k_set_ids(const uint64_t* __restrict__ of
   }
 }
 
-// end[v] += cnt[v]: list starts (exclusive scan) -> list ends, as the cover reads them.
-__global__ void __launch_bounds__(256) k_end_add(uint32_t* __restrict__ end, const uint32_t* __restrict__ cnt,
-                                                 uint32_t n) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) end[v] += cnt[v];
-}
-
 size_t inv_sort_tmp_bytes(uint64_t elements, uint32_t nbits) {
   size_t bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
@@ -52,8 +46,7 @@ size_t inv_sort_tmp_bytes(uint64_t elements, uint32_t nbits) {
 
 cudaError_t launch_inv_sort(const uint64_t* offsets, const uint32_t* pool, uint32_t set0, uint32_t set1, uint64_t e0,
                             uint64_t elements, uint32_t nbits, uint32_t* keys_tmp, uint32_t* vals_tmp, void* cub_tmp,
-                            size_t cub_bytes, uint32_t* inv, uint32_t* end, const uint32_t* cnt, uint32_t n, int grid,
-                            cudaStream_t s, int* launches) {
+                            size_t cub_bytes, uint32_t* inv, int grid, cudaStream_t s, int* launches) {
   *launches = 0;
   k_set_ids<<<grid, 256, 0, s>>>(offsets, set0, set1, e0, vals_tmp);
   ++*launches;
@@ -63,8 +56,6 @@ cudaError_t launch_inv_sort(const uint64_t* offsets, const uint32_t* pool, uint3
                                                       (int64_t)elements, 0, (int)nbits, s))
     return e;
   *launches += 4;                                        // onesweep passes (launch accounting only)
-  k_end_add<<<grid, 256, 0, s>>>(end, cnt, n);
-  ++*launches;
   return cudaGetLastError();
 }
 

@@ -65,6 +65,50 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_sums(const uint32_t* __re
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = s_total;
 }
 
+// Index segment histogram + scan in one pass pair (no separate delta array): the segment's count
+// of node v is cnt[v] - snap[v] (count_total minus its value at the previous segment); phase 1
+// sums it per tile, phase 3 writes the exclusive (scatter: list starts) or inclusive (sorted
+// segment: list ends) prefix and sets snap := cnt.
+__global__ void __launch_bounds__(kScanThreads) k_seg_sums(const uint32_t* __restrict__ cnt,
+                                                           const uint32_t* __restrict__ snap, uint64_t count,
+                                                           uint64_t* __restrict__ tile_sums) {
+  __shared__ uint64_t s_total;
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanPerThread;
+  uint64_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanPerThread; ++j)
+    if (base + j < count) s += cnt[base + j] - snap[base + j];
+  block_excl_scan(s, &s_total);
+  __syncthreads();
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = s_total;
+}
+__global__ void __launch_bounds__(kScanThreads) k_seg_apply(const uint32_t* __restrict__ cnt,
+                                                            uint32_t* __restrict__ snap, uint64_t count,
+                                                            const uint64_t* __restrict__ tile_sums,
+                                                            const uint64_t* __restrict__ grand_total,
+                                                            uint32_t* __restrict__ out, int inclusive) {
+  __shared__ uint64_t s_total;
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanPerThread;
+  uint32_t v[kScanPerThread], c[kScanPerThread];
+  uint64_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanPerThread; ++j) {
+    c[j] = (base + j < count) ? cnt[base + j] : 0u;
+    v[j] = (base + j < count) ? c[j] - snap[base + j] : 0u;
+    s += v[j];
+  }
+  uint64_t ex = block_excl_scan(s, &s_total) + tile_sums[blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kScanPerThread; ++j) {
+    if (base + j < count) {
+      out[base + j] = (uint32_t)(inclusive ? ex + v[j] : ex);
+      snap[base + j] = c[j];
+    }
+    ex += v[j];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[count] = (uint32_t)*grand_total;
+}
+
 // Phase 2: exclusive scan of the tile sums by one CTA (loops over chunks of 1024).
 __global__ void __launch_bounds__(kScanThreads) k_scan_tiles(uint64_t* __restrict__ tile_sums, uint64_t ntiles,
                                                              uint64_t* __restrict__ grand_total) {
@@ -153,15 +197,6 @@ __global__ void __launch_bounds__(256) k_inv_scatter(const uint64_t* __restrict_
   }
 }
 
-// Per-segment histogram without atomics: delta[v] = count_total[v] - snap[v]; snap := count_total.
-__global__ void __launch_bounds__(256) k_count_delta(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ snap,
-                                                     uint32_t* __restrict__ delta, uint32_t n) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    const uint32_t c = cnt[v];
-    delta[v] = c - snap[v];
-    snap[v] = c;
-  }
-}
 
 // ------------------------------------------------------------------------------------------
 // K-ARGMAX: keys[j] = max over v of (selected ? 0 : count[v] << 32 | ~v). Applies the
@@ -942,6 +977,16 @@ cudaError_t launch_scan_u32_to32(const uint32_t* in, uint64_t count, uint32_t* o
                                  uint64_t* total_tmp, cudaStream_t s, int* launches) {
   return launch_scan_impl<uint32_t>(in, count, out, tile_tmp, total_tmp, s, launches);
 }
+cudaError_t launch_seg_scan(const uint32_t* cnt, uint32_t* snap, uint64_t count, uint32_t* out, bool inclusive,
+                            uint64_t* tile_tmp, uint64_t* total_tmp, cudaStream_t s, int* launches) {
+  const uint64_t nt = scan_tiles(count);
+  if (nt > 0) k_seg_sums<<<(unsigned)nt, kScanThreads, 0, s>>>(cnt, snap, count, tile_tmp);
+  k_scan_tiles<<<1, kScanThreads, 0, s>>>(tile_tmp, nt, total_tmp);
+  k_seg_apply<<<(unsigned)(nt > 0 ? nt : 1), kScanThreads, 0, s>>>(cnt, snap, count, tile_tmp, total_tmp, out,
+                                                                    inclusive ? 1 : 0);
+  *launches = nt > 0 ? 3 : 2;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_inv_scatter(const uint64_t* offsets, const uint32_t* pool, uint32_t set0, uint32_t set1,
                                uint32_t* end, uint32_t* inv, int grid, cudaStream_t s, uint32_t n, int passes,
@@ -981,11 +1026,6 @@ cudaError_t launch_set_segs(const InvSegDev* segs, uint32_t nseg, uint32_t limit
   return cudaGetLastError();
 }
 
-cudaError_t launch_count_delta(const uint32_t* cnt, uint32_t* snap, uint32_t* delta, uint32_t n, int grid,
-                               cudaStream_t s) {
-  k_count_delta<<<grid, 256, 0, s>>>(cnt, snap, delta, n);
-  return cudaGetLastError();
-}
 
 // Launch with programmatic stream serialization (see pdl_wait / pdl_trigger).
 template <typename... KArgs, typename... Args>

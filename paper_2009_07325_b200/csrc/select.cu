@@ -469,6 +469,11 @@ __global__ void __launch_bounds__(256) k_argmax_cand(const uint32_t* __restrict_
 #define GIM_COVER_ILP 16
 #endif
 constexpr int kCoverIlp = GIM_COVER_ILP;
+#ifndef GIM_COVER_BIG
+#define GIM_COVER_BIG 256
+#endif
+constexpr uint32_t kCoverBig = 32;                  // big sets queued per CTA (more: the group does it)
+constexpr uint64_t kCoverBigMin = GIM_COVER_BIG;    // members above which the whole CTA decrements
 
 template <bool LIMIT>
 __device__ __forceinline__ void cover_step(const unsigned long long* __restrict__ keys, int j,
@@ -565,6 +570,13 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
   const uint32_t ns = s_nseg, limit = LIMIT ? s_limit : 0xFFFFFFFFu;
   const uint64_t total = (ns && limit) ? s_end[kMaxInvSeg - 1] : 0;   // limit 0: every set cut
   const uint64_t ngroups = (uint64_t)gridDim.x * (blockDim.x >> 3);
+  // big covered sets (the first greedy steps cover hub-rich sets of up to thousands of members):
+  // their members are decremented by the whole CTA after its entries, not by one 8-lane group —
+  // a 2,793-member set was 22 dependent load rounds of one group
+  __shared__ uint64_t s_big_a[kCoverBig], s_big_b[kCoverBig];
+  __shared__ uint32_t s_nbig;
+  if (threadIdx.x == 0) s_nbig = 0;
+  __syncthreads();
   uint32_t q = 0;
   for (uint64_t t = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3); t < total; t += ngroups) {
     while (t >= s_end[q]) ++q;                 // t increases monotonically per group
@@ -578,6 +590,15 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
     const uint64_t b = offsets[mr.rounds > 1u ? ci * mr.rounds + mr.rounds : r + 1];
     if (cov || (LIMIT && r0 != r)) continue;
     if (sub == 0) covered[ci] = 1;     // each set appears once across the lists of u: no race
+    if (cmap == nullptr && b - a > kCoverBigMin) {
+      uint32_t slot = kCoverBig;
+      if (sub == 0) slot = atomicAdd(&s_nbig, 1u);
+      slot = __shfl_sync(0xFFu << (threadIdx.x & 24), slot, threadIdx.x & 24);
+      if (slot < kCoverBig) {
+        if (sub == 0) { s_big_a[slot] = a; s_big_b[slot] = b; }
+        continue;
+      }
+    }
     // members: kCoverIlp loads in flight per lane (big sets would otherwise serialise one L2
     // round trip per 8 members), then fire-and-forget decrements; u itself is skipped
     for (uint64_t e = a + sub; e < b; e += 8 * kCoverIlp) {
@@ -595,6 +616,22 @@ __device__ __forceinline__ void cover_step(const unsigned long long* __restrict_
       }
 #pragma unroll
       for (int t = 0; t < kCoverIlp; ++t) {
+        if (w[t] == u) continue;
+        if (dec == nullptr) atomicSub(cnt + w[t], 1u);
+        else atomicAdd(dec + w[t], 1);
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t nbig = min(s_nbig, (uint32_t)kCoverBig);
+  for (uint32_t i = 0; i < nbig; ++i) {
+    const uint64_t a = s_big_a[i], b = s_big_b[i];
+    for (uint64_t e = a + threadIdx.x; e < b; e += (uint64_t)blockDim.x * 4) {
+      uint32_t w[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) w[t] = (e + (uint64_t)blockDim.x * t < b) ? pool[e + (uint64_t)blockDim.x * t] : u;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
         if (w[t] == u) continue;
         if (dec == nullptr) atomicSub(cnt + w[t], 1u);
         else atomicAdd(dec + w[t], 1);

@@ -11,10 +11,11 @@ namespace gim {
 __global__ void __launch_bounds__(256) k_validate_csr(const uint64_t* __restrict__ rp64, uint32_t n,
                                                       uint64_t m, const uint32_t* __restrict__ src,
                                                       uint32_t* __restrict__ rp32, uint32_t* err,
-                                                      uint32_t* bad_row, uint32_t* __restrict__ thr_node) {
+                                                      uint32_t* bad_row, uint32_t* __restrict__ thr_node,
+                                                      uint32_t v0, uint32_t v1) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-  for (uint32_t v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); v < n; v += nwarps) {
+  for (uint32_t v = v0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); v < v1; v += nwarps) {
     const uint64_t a = rp64[v], b = rp64[v + 1];
     uint32_t e_bits = 0;
     if (b < a || b > m) {
@@ -40,13 +41,15 @@ __global__ void __launch_bounds__(256) k_validate_csr(const uint64_t* __restrict
       }
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) rp32[n] = (uint32_t)m;
+  if (v1 == n && blockIdx.x == 0 && threadIdx.x == 0) rp32[n] = (uint32_t)m;
 }
 
+// Rows [v0, v1) (their sources must be resident: gim_load_graph validates each row range as soon
+// as its slice of src has arrived, overlapping the rest of the upload).
 cudaError_t launch_validate_csr(const uint64_t* rp64, uint32_t n, uint64_t m, const uint32_t* src,
                                 uint32_t* rp32, uint32_t* err, uint32_t* bad_row, uint32_t* thr_node, int grid,
-                                cudaStream_t s) {
-  k_validate_csr<<<grid, 256, 0, s>>>(rp64, n, m, src, rp32, err, bad_row, thr_node);
+                                cudaStream_t s, uint32_t v0, uint32_t v1) {
+  k_validate_csr<<<grid, 256, 0, s>>>(rp64, n, m, src, rp32, err, bad_row, thr_node, v0, v1);
   return cudaGetLastError();
 }
 

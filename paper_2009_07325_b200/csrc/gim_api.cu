@@ -1461,15 +1461,51 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
     TRY(dalloc(c, rp64, ((uint64_t)n + 1) * 8 + 16));
     uint32_t* flags = reinterpret_cast<uint32_t*>(rp64.as<uint64_t>() + n + 1);
     CK(cudaMemcpyAsync(rp64.p, rp, ((uint64_t)n + 1) * 8, cudaMemcpyHostToDevice, c->stream));
-    if (m) CK(cudaMemcpyAsync(c->src.p, src, m * 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(flags, 0, 4, c->stream));
     CK(cudaMemsetAsync(flags + 1, 0xFF, 4, c->stream));
     CK(cudaMemsetAsync(flags + 2, 0, 8, c->stream));                 // max in-degree
-    TRY(launched(c, launch_validate_csr(rp64.as<uint64_t>(), n, m, c->src.as<uint32_t>(), c->row_ptr.as<uint32_t>(),
-                                        flags, flags + 1, c->thr_node,
-                                        c->num_sms * 8, c->stream), "k_validate_csr"));
+    // src arrives in row-aligned slices on `stream`; each slice's rows are validated on stream2
+    // as soon as it has landed, so the validation overlaps the rest of the PCIe upload. The row
+    // pointers are read on the host only where they are monotone (a bad row_ptr is reported by
+    // the validation itself and the slicing falls back to one slice).
+    const int K = m >= (1u << 23) ? 8 : 1;
+    std::vector<uint32_t> cut = {0};
+    bool mono = true;
+    for (int k = 1; k < K; ++k) {
+      const uint64_t target = m * (uint64_t)k / K;
+      uint32_t lo = cut.back(), hi = n;                  // first row with rp >= target
+      while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (rp[mid] >= target) hi = mid; else lo = mid + 1;
+      }
+      if (lo > cut.back() && lo < n) cut.push_back(lo);
+    }
+    cut.push_back(n);
+    for (size_t q = 1; q < cut.size(); ++q) mono = mono && rp[cut[q - 1]] <= rp[cut[q]] && rp[cut[q]] <= m;
+    if (!mono) cut = {0, n};
+    std::vector<cudaEvent_t> evs;
+    for (size_t q = 0; q + 1 < cut.size(); ++q) {
+      const uint64_t e0 = rp[cut[q]], e1 = (q + 2 == cut.size()) ? m : rp[cut[q + 1]];
+      if (e1 > e0) CK(cudaMemcpyAsync(c->src.as<uint32_t>() + e0, src + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, c->stream));
+      cudaEvent_t ev;
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      evs.push_back(ev);
+      CK(cudaEventRecord(ev, c->stream));
+      CK(cudaStreamWaitEvent(c->stream2, ev, 0));
+      TRY(launched(c, launch_validate_csr(rp64.as<uint64_t>(), n, m, c->src.as<uint32_t>(), c->row_ptr.as<uint32_t>(),
+                                          flags, flags + 1, c->thr_node, c->num_sms * 8, c->stream2, cut[q],
+                                          cut[q + 1]), "k_validate_csr"));
+    }
+    {
+      cudaEvent_t ev;
+      CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      evs.push_back(ev);
+      CK(cudaEventRecord(ev, c->stream2));
+      CK(cudaStreamWaitEvent(c->stream, ev, 0));
+    }
     CK(cudaMemcpyAsync(c->h_u64, flags, 16, cudaMemcpyDeviceToHost, c->stream));
     TRY(sync(c));
+    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
     dfree(c, rp64);
     c->max_deg = (uint32_t)c->h_u64[1];
     c->skip_tab_valid = false;

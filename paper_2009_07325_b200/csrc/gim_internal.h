@@ -122,7 +122,7 @@ cudaError_t launch_select_coop(const uint32_t* cnt, const uint32_t* cand, const 
                                cudaStream_t s);
 cudaError_t launch_validate_csr(const uint64_t* rp64, uint32_t n, uint64_t m, const uint32_t* src,
                                 uint32_t* rp32, uint32_t* err, uint32_t* bad_row, uint32_t* thr_node, int grid,
-                                cudaStream_t s);
+                                cudaStream_t s, uint32_t v0, uint32_t v1);
 // forward Monte-Carlo (mc.cu)
 cudaError_t build_out_csr(const uint32_t* row_ptr, const uint32_t* src, uint32_t n, uint64_t m, int scheme,
                           uint32_t* out_ptr, uint32_t* out_dst, uint32_t* out_in, uint32_t* thr_wc,

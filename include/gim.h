@@ -299,7 +299,14 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                         segment by a stable radix sort of its (node, set) pairs by node instead
  *                         of the cursor scatter (lists in ascending set order; same lists).
  *  GIM_OPT_CHUNK        = ids (0 = default 2^25; 1024..2^25): RR ids sampled per generation chunk
- *                         (one K-RR / K-GIANT / store pass each; results identical). */
+ *                         (one K-RR / K-GIANT / store pass each; results identical).
+ *  GIM_OPT_SELECT_CLUSTER = 0 (default) / 1: with GIM_OPT_SELECT_CTA, graphs of 51,200 < n <=
+ *                         409,600 run the k greedy steps in one launch on a thread-block cluster of
+ *                         2..8 CTAs whose shared memories hold the counts (DSMEM exchange of the
+ *                         partial argmaxes, DSMEM atomics for the decrements). Results identical;
+ *                         measured slower on C2 (selection 5.31 vs 1.16 ms): a few SMs cannot
+ *                         carry the covers of a 358K-set pool, which the graph path spreads over
+ *                         all 148. */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -329,7 +336,8 @@ typedef enum {
   GIM_OPT_L2_PERSIST = 27,
   GIM_OPT_SELECT_CTA = 28,
   GIM_OPT_INV_SORT = 29,
-  GIM_OPT_CHUNK = 30
+  GIM_OPT_CHUNK = 30,
+  GIM_OPT_SELECT_CLUSTER = 31
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 

@@ -162,6 +162,7 @@ struct gim_ctx {
   DevBuf isort_keys, isort_vals, isort_tmp;   // sort-based segments: sorted keys, set ids, CUB scratch
   int imm_early_exit = 1;       // GIM_OPT_IMM_EARLY_EXIT
   int sel_small = 1;            // GIM_OPT_SELECT_CTA: single-CTA selection when the counts fit in shared memory
+  int sel_cluster = 0;          // GIM_OPT_SELECT_CLUSTER: the cluster version for n up to 8x that (measured slower)
   uint64_t cmap_n = 0;          // nodes covered by cmap (kEmpty-initialised)
   // options
   int force_giant = 0, profile = 0;
@@ -1146,6 +1147,13 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
     TRY(launched(c, launch_select_cta(c->count_total.as<uint32_t>(), (uint32_t)n, keys, (int)kk, segd,
                                       c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), c->covered.as<uint8_t>(),
                                       ctl, limited, c->stream), "k_select_cta"));
+  } else if (!dec && !cand && c->rounds == 1 && c->sel_small && c->sel_cluster && n <= select_cluster_max_n() &&
+             !c->speculate) {
+    // mid-size graphs: the same on a thread-block cluster, counts in the CTAs' shared memories
+    Prof pf(c, CLS_SELECT);
+    TRY(launched(c, launch_select_cluster(c->count_total.as<uint32_t>(), (uint32_t)n, keys, (int)kk, segd,
+                                          c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(), c->covered.as<uint8_t>(),
+                                          ctl, limited, c->stream), "k_select_cluster"));
   } else if (!dec && c->use_graph) {
     // P = 1: the 2k argmax/cover launches replayed from a CUDA graph (captured once per set of
     // buffer pointers; steady-state IMM runs reuse it), so the GPU runs them back to back.
@@ -1897,6 +1905,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_SELECT_PERSISTENT: c->sel_persistent = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_IMM_EARLY_EXIT: c->imm_early_exit = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_SELECT_CTA: c->sel_small = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_SELECT_CLUSTER: c->sel_cluster = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_INV_SORT: c->inv_sort = (value < -1 || value > 1) ? -1 : (int)value; return GIM_OK;
     case GIM_OPT_CHUNK:
       if (value != 0 && (value < 1024 || value > (int64_t)kChunk)) return fail(c, GIM_EINVAL, "chunk must be 0 or in [1024, 2^25]");

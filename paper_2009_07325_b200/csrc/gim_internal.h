@@ -108,6 +108,12 @@ uint32_t select_cta_max_n();
 cudaError_t launch_select_cta(const uint32_t* count_total, uint32_t n, unsigned long long* keys, int kk,
                               const InvSegDev* segs, const uint64_t* offsets, const uint32_t* pool,
                               uint8_t* covered, SelCtl* ctl, bool limit, cudaStream_t s);
+// mid-size graphs (P = 1): the same on a cluster of 2..8 CTAs, counts split over their shared
+// memories (DSMEM atomics for the decrements)
+uint32_t select_cluster_max_n();
+cudaError_t launch_select_cluster(const uint32_t* count_total, uint32_t n, unsigned long long* keys, int kk,
+                                  const InvSegDev* segs, const uint64_t* offsets, const uint32_t* pool,
+                                  uint8_t* covered, SelCtl* ctl, bool limit, cudaStream_t s);
 // fused greedy steps (P = 1): candidate argmax of step 0, then per step cover + next argmax
 cudaError_t launch_select_fused(unsigned long long* keys, int kk, const InvSegDev* segs, const uint64_t* offsets,
                                 const uint32_t* pool, uint8_t* covered, uint32_t* cnt, const uint32_t* cand,

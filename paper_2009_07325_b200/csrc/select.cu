@@ -12,6 +12,7 @@
 // atomicMax per CTA; the previous pick is retired inside the same pass (count = sentinel).
 #include <atomic>
 #include <algorithm>
+#include <cooperative_groups.h>
 
 #include "gim_device.cuh"
 #include "gim_internal.h"
@@ -985,6 +986,142 @@ __global__ void __launch_bounds__(kSmallSelThreads, 1) k_select_cta(const uint32
 }
 
 // ------------------------------------------------------------------------------------------
+// Mid-size graphs (n <= 8 x 51,200): the same single-launch selection on a thread-block CLUSTER
+// of CS CTAs (one per SM): CTA r keeps the counts of nodes [r ns, (r+1) ns) in its shared memory;
+// the argmax is a local scan + an exchange of the CS partial bests through distributed shared
+// memory, the cover is split over all CTAs of the cluster and decrements a member's count with an
+// atomic on its owner's shared memory (DSMEM); two cluster barriers per greedy step, no launch.
+// ------------------------------------------------------------------------------------------
+template <bool LIMIT>
+__global__ void __launch_bounds__(kSmallSelThreads, 1) k_select_cluster(const uint32_t* __restrict__ count_total,
+                                                                       uint32_t n, uint32_t ns,
+                                                                       unsigned long long* __restrict__ keys, int kk,
+                                                                       const InvSegDev* __restrict__ segs,
+                                                                       const uint64_t* __restrict__ offsets,
+                                                                       const uint32_t* __restrict__ pool,
+                                                                       uint8_t* __restrict__ covered, SelCtl* ctl) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ uint32_t s_cnt[];                 // [ns]: counts of this CTA's node range
+  __shared__ unsigned long long s_wbest[kSmallSelThreads / 32];
+  __shared__ unsigned long long s_mybest;             // read by every CTA of the cluster
+  __shared__ uint64_t s_lo[kMaxInvSeg], s_end[kMaxInvSeg];
+  __shared__ const uint32_t* s_inv[kMaxInvSeg];
+  __shared__ const uint32_t* s_endp[kMaxInvSeg];
+  __shared__ uint32_t s_u, s_stop, s_nseg, s_limit;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t rank = cluster.block_rank(), cs = cluster.num_blocks();
+  const uint32_t v0 = rank * ns, v1 = min(n, v0 + ns);
+  for (uint32_t i = tid; i < ns; i += kSmallSelThreads) s_cnt[i] = (v0 + i < v1) ? count_total[v0 + i] : kSent;
+  if (tid < 32) {
+    InvSegDev sg{nullptr, nullptr};
+    if (tid < kMaxInvSeg) sg = segs[tid];
+    if (tid < kMaxInvSeg) {
+      s_inv[tid] = sg.inv;
+      s_endp[tid] = sg.end;
+    }
+    const uint32_t used = __ballot_sync(kFull, sg.end != nullptr);
+    if (tid == 0) {
+      s_nseg = __popc(used);
+      s_limit = LIMIT ? reinterpret_cast<const uint32_t*>(segs + kMaxInvSeg)[1] : 0xFFFFFFFFu;
+    }
+  }
+  const unsigned long long cstar = ctl ? ctl->cstar : 0ull;
+  unsigned long long cov = 0;                         // thread 0: gains of the steps so far
+  cluster.sync();                                     // every CTA's counts are in place
+  const uint32_t nseg = s_nseg, limit = s_limit;
+  const uint32_t sub = tid & 7;
+  for (int j = 0; j < kk; ++j) {
+    unsigned long long best = 0;
+    for (uint32_t i = tid; i < v1 - v0; i += kSmallSelThreads) argmax_one(s_cnt[i], v0 + i, best, 0u);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+      best = o > best ? o : best;
+    }
+    if (lane == 0) s_wbest[warp] = best;
+    __syncthreads();
+    if (warp == 0) {
+      best = s_wbest[lane];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+        best = o > best ? o : best;
+      }
+      if (lane == 0) s_mybest = best;
+    }
+    cluster.sync();                                   // partial bests published
+    if (warp == 0) {
+      best = 0;
+      if ((uint32_t)lane < cs) best = *cluster.map_shared_rank(&s_mybest, (unsigned)lane);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(kFull, best, off);
+        best = o > best ? o : best;
+      }
+      const uint32_t u = ~(uint32_t)best;
+      uint64_t lo = 0, len = 0;
+      if ((uint32_t)lane < nseg) {
+        const uint32_t* e = s_endp[lane];
+        lo = u ? e[u - 1] : 0u;
+        len = e[u] - lo;
+      }
+      uint64_t incl = len;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t y = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += y;
+      }
+      if (lane < kMaxInvSeg) {
+        s_lo[lane] = lo;
+        s_end[lane] = (uint32_t)lane < nseg ? incl : ~0ull;
+      }
+      if (lane == 0) {
+        const unsigned long long g = best >> 32;
+        const bool stop = cstar != 0ull && cov + (unsigned long long)(kk - j) * g < cstar;
+        cov += g;
+        s_stop = stop ? 1u : 0u;
+        s_u = u;
+        if (rank == 0) {
+          keys[j] = best;
+          if (stop) ctl->stop = 1u;
+        }
+        if (u - v0 < v1 - v0) s_cnt[u - v0] = kSent;   // the owner retires the pick
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;                                // the same decision in every CTA
+    const uint32_t u = s_u;
+    const uint64_t total = (nseg && limit) ? s_end[nseg - 1] : 0ull;
+    uint32_t q = 0;
+    const uint64_t gstride = (uint64_t)cs * (kSmallSelThreads / 8);
+    for (uint64_t t = (uint64_t)rank * (kSmallSelThreads / 8) + (tid >> 3); t < total; t += gstride) {
+      while (t >= s_end[q]) ++q;
+      const uint64_t pos = s_lo[q] + (t - (q ? s_end[q - 1] : 0));
+      const uint32_t r0 = s_inv[q][pos];
+      const uint32_t r = LIMIT ? min(r0, limit - 1u) : r0;
+      const uint8_t cv = covered[r];
+      const uint64_t a = offsets[r], b = offsets[r + 1];
+      if (cv || (LIMIT && r0 != r)) continue;
+      if (sub == 0) covered[r] = 1;
+      for (uint64_t e = a + sub; e < b; e += 8 * 8) {
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = (e + 8 * i < b) ? pool[e + 8 * i] : u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (w[i] == u) continue;
+          const uint32_t owner = w[i] / ns;
+          atomicSub(cluster.map_shared_rank(s_cnt, owner) + (w[i] - owner * ns), 1u);
+        }
+      }
+    }
+    cluster.sync();                                   // every decrement landed before the next argmax
+  }
+  cluster.sync();                                     // no CTA leaves while others may touch its smem
+}
+
+// ------------------------------------------------------------------------------------------
 // Host launch wrappers
 // ------------------------------------------------------------------------------------------
 int g_pdl = 0;   // GIM_OPT_PDL (process-wide: the launch wrappers carry no ctx)
@@ -1203,6 +1340,42 @@ cudaError_t launch_select_cta(const uint32_t* count_total, uint32_t n, unsigned 
   if (limit) k_select_cta<true><<<1, kSmallSelThreads, smem, s>>>(count_total, n, keys, kk, segs, offsets, pool, covered, ctl);
   else k_select_cta<false><<<1, kSmallSelThreads, smem, s>>>(count_total, n, keys, kk, segs, offsets, pool, covered, ctl);
   return cudaGetLastError();
+}
+
+uint32_t select_cluster_max_n() { return 8u * select_cta_max_n(); }
+
+cudaError_t launch_select_cluster(const uint32_t* count_total, uint32_t n, unsigned long long* keys, int kk,
+                                  const InvSegDev* segs, const uint64_t* offsets, const uint32_t* pool,
+                                  uint8_t* covered, SelCtl* ctl, bool limit, cudaStream_t s) {
+  const uint32_t cs = (n + select_cta_max_n() - 1) / select_cta_max_n();   // 2..8 CTAs
+  const uint32_t ns = (n + cs - 1) / cs;
+  const int smem = (int)(ns * 4u);
+  static std::atomic<uint64_t> attr{0};
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  if (!(attr.load() & (1ull << (dev & 63)))) {
+    const int cap = (int)(select_cta_max_n() * 4u);
+    for (const void* f : {(const void*)k_select_cluster<true>, (const void*)k_select_cluster<false>}) {
+      if (cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, cap)) return e;
+      if (cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 0)) return e;
+    }
+    attr.fetch_or(1ull << (dev & 63));
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(kSmallSelThreads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (limit)
+    return cudaLaunchKernelEx(&cfg, k_select_cluster<true>, count_total, n, ns, keys, kk, segs, offsets, pool, covered, ctl);
+  return cudaLaunchKernelEx(&cfg, k_select_cluster<false>, count_total, n, ns, keys, kk, segs, offsets, pool, covered, ctl);
 }
 
 cudaError_t launch_cover(const unsigned long long* keys, int j, const InvSegDev* segs, SelCtl* ctl,

@@ -471,15 +471,17 @@ def test_coop_selection_imm_golden(key):
     c.close()
 
 
-@pytest.mark.parametrize("small", [1, 0])
-def test_select_small_cta_equals_oracle(small):
-    """Single-CTA selection (counts in shared memory, GIM_OPT_SELECT_CTA, default for n <= 51,200)
-    and the multi-CTA graph replay both equal the oracle: C1 pool in several generate calls
-    (several index segments), k = 50 and k = 200, a truncated pool (cut sets skipped), and the full
-    IMM with its bounded-greedy trace."""
-    w = gi.WORKLOADS["C1"]
-    g = gi.workload_graph("C1")
-    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_CTA: small})
+@pytest.mark.parametrize("key,small", [("C1", 1), ("C1", 0), ("C2", 2), ("C2", 0)])
+def test_select_small_cta_equals_oracle(key, small):
+    """Single-launch selection — one CTA (C1, n <= 51,200) or a thread-block cluster with the counts
+    in its CTAs' shared memories (C2: 2 CTAs, DSMEM atomics) — and the multi-CTA graph replay
+    (small = 0) all equal the oracle (small = 2: GIM_OPT_SELECT_CLUSTER, off by default): a pool in
+    several generate calls (several index segments),
+    k = 50 and k = 200, a truncated pool (cut sets skipped), and the full IMM with its
+    bounded-greedy trace."""
+    w = gi.WORKLOADS[key]
+    g = gi.workload_graph(key)
+    c = _ctx(g, w.model, w.scheme, opts={P.OPT_SELECT_CTA: min(small, 1), P.OPT_SELECT_CLUSTER: int(small == 2)})
     o = oracle.Oracle(g, w.model, w.scheme)
     for T in (5000, 12001, 40013):
         c.generate_rr(T, w.rr_seed)

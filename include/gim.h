@@ -306,7 +306,14 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                         partial argmaxes, DSMEM atomics for the decrements). Results identical;
  *                         measured slower on C2 (selection 5.31 vs 1.16 ms): a few SMs cannot
  *                         carry the covers of a 358K-set pool, which the graph path spreads over
- *                         all 148. */
+ *                         all 148.
+ *  GIM_OPT_IMM_LOOKAHEAD = 1 (default) / 0: in gim_imm, after a round the probe settled (bound
+ *                         fraction u = k gain_0 / T_i), the following rounds whose passing fraction
+ *                         (1 + eps') / 2^m exceeds u / 0.8 are sampled in the same generate call and
+ *                         probed on the counts of their own prefix of T_m sets; a round the probe
+ *                         does not settle truncates the pool to its T_m (gim_stats.lookahead_drops).
+ *                         The trace, LB, theta, R_final and the seeds are unchanged. 2: two rounds
+ *                         ahead whatever u (tests: exercises the drop path). */
 typedef enum {
   GIM_OPT_FORCE_GIANT = 1,
   GIM_OPT_QUEUE_CAP = 2,
@@ -337,7 +344,8 @@ typedef enum {
   GIM_OPT_SELECT_CTA = 28,
   GIM_OPT_INV_SORT = 29,
   GIM_OPT_CHUNK = 30,
-  GIM_OPT_SELECT_CLUSTER = 31
+  GIM_OPT_SELECT_CLUSTER = 31,
+  GIM_OPT_IMM_LOOKAHEAD = 32
 } gim_option;
 gim_status gim_set_option(gim_ctx* ctx, gim_option opt, int64_t value);
 
@@ -362,6 +370,7 @@ typedef struct {
   double host_ms_api;           /* host wall time inside gim_generate_rr/select/imm       */
   uint64_t fused_fallbacks;     /* fused selections redone unfused (uncertified argmax)   */
   uint64_t probe_stops;         /* gim_imm rounds settled by the first-step probe alone   */
+  uint64_t lookahead_drops;     /* lookahead sets dropped because a round needed selection */
 } gim_stats;
 gim_status gim_get_stats(gim_ctx* ctx, gim_stats* out);
 gim_status gim_reset_stats(gim_ctx* ctx);

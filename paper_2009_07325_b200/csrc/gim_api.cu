@@ -41,6 +41,7 @@ constexpr uint32_t kChunk = 1u << GIM_CHUNK_LOG2;
 #endif
 constexpr int kArgmaxCtasPerSM = GIM_ARGMAX_CTAS;   // k_argmax grid = this x #SMs (256 threads each)
 constexpr uint32_t kSelHead = 8;   // greedy steps before a bounded greedy's host stop check
+constexpr double kLookSafety = 0.8;   // lookahead: u_prev below this fraction of a round's passing fraction
 #ifndef GIM_COVER_CTAS
 #define GIM_COVER_CTAS 8
 #endif
@@ -161,6 +162,7 @@ struct gim_ctx {
   uint32_t chunk = 0;           // GIM_OPT_CHUNK: RR ids per generation chunk (0 = kChunk)
   DevBuf isort_keys, isort_vals, isort_tmp;   // sort-based segments: sorted keys, set ids, CUB scratch
   int imm_early_exit = 1;       // GIM_OPT_IMM_EARLY_EXIT
+  int imm_lookahead = 1;        // GIM_OPT_IMM_LOOKAHEAD
   int sel_small = 1;            // GIM_OPT_SELECT_CTA: single-CTA selection when the counts fit in shared memory
   int sel_cluster = 0;          // GIM_OPT_SELECT_CLUSTER: the cluster version for n up to 8x that (measured slower)
   uint64_t cmap_n = 0;          // nodes covered by cmap (kEmpty-initialised)
@@ -1646,13 +1648,39 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
   std::vector<uint32_t> tmp((size_t)k * c->rounds);
   auto R_sets = [c]() { return c->T_global / c->rounds; };     // sets in API units
   const int i_max = (int)std::floor(std::log2(n)) - 1;       // reading R5
+  const bool global_counts = !(c->world > 1 || c->force_coll) || c->agfn;
+  // lookahead sampling (GIM_OPT_IMM_LOOKAHEAD): after a round the probe settled with
+  // k * gain_0 / T = u_prev, the next rounds whose passing fraction (1 + eps') / 2^m is well above
+  // u_prev are sampled in the same generate call (one sampling pass instead of several); each of
+  // them then probes the counts of its own prefix of T_m sets. A round the probe does not settle
+  // truncates the pool back to its T_m (the extra sets are dropped) and continues as usual.
+  const bool can_look = c->imm_lookahead && c->imm_early_exit && c->rounds == 1 && c->world == 1 &&
+                        !c->force_coll && !c->speculate;
+  double u_prev = -1.0;
+  uint64_t la_end = 0;                                       // pool size sampled ahead (0: none)
   for (int i = 1; i <= i_max && i <= 64; ++i) {              // Alg. 2 l.2
     const double x = n / std::ldexp(1.0, i);                 // l.3
     const double theta_i = K.lambda_p / x;                   // l.4 (f = lambda', reading R1)
     const uint64_t T = (uint64_t)std::ceil(theta_i);
-    const uint64_t R = std::max<uint64_t>(R_sets(), T);      // l.5 (reading R4)
-    TRY(generate(c, R, seed, false));
-    if (R_sets() > R) TRY(truncate_pool(c, R * c->rounds));  // drop excess speculation
+    uint64_t R;
+    if (la_end > T) {
+      R = T;                                                 // this round's prefix of the pool
+    } else {
+      la_end = 0;
+      R = std::max<uint64_t>(R_sets(), T);                   // l.5 (reading R4)
+      uint64_t target = R;
+      if (can_look && u_prev >= 0.0 && R_sets() < T)
+        for (int m = i + 1; m <= i_max; ++m) {
+          // (GIM_OPT_IMM_LOOKAHEAD = 2, tests: two rounds ahead whatever u_prev, to exercise drops)
+          const bool ahead = c->imm_lookahead == 2 ? m <= i + 2
+                                                   : u_prev < kLookSafety * (1.0 + K.eps_p) / std::ldexp(1.0, m);
+          if (!ahead) break;
+          target = (uint64_t)std::ceil(K.lambda_p / (n / std::ldexp(1.0, m)));
+        }
+      TRY(generate(c, target, seed, false));
+      if (target > R) la_end = target;
+      else if (R_sets() > R) TRY(truncate_pool(c, R * c->rounds));   // drop excess speculation
+    }
     // speculative target while this round's selection runs: the next round's T if the test
     // fails, capped by ceil(lambda*/x), the largest theta a passing test can produce
     const uint64_t spec = std::min<uint64_t>(
@@ -1675,13 +1703,22 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
     // (one pick, cov = gain_0) is known without indexing the new sets or launching the
     // selection — their index segment is built later, merged with the next rounds' sets
     bool probed = false;
-    const bool global_counts = !(c->world > 1 || c->force_coll) || c->agfn;
-    if (c->sel_cstar && c->inv_pending && global_counts && !c->speculate) {
+    const bool prefix = la_end > R;                          // the pool holds sets beyond this round
+    if (c->sel_cstar && (c->inv_pending || prefix) && global_counts && !c->speculate) {
       TRY(ensure(c, c->probe, 8));
       CK(cudaMemsetAsync(c->probe.p, 0, 8, c->stream));
+      const uint32_t* counts = c->count_total.as<uint32_t>();
+      if (prefix) {                                          // counts of the first R sets only
+        TRY(ensure(c, c->cnt, nsp(c) * 4));
+        CK(cudaMemcpyAsync(c->cnt.p, c->count_total.p, nsp(c) * 4, cudaMemcpyDeviceToDevice, c->stream));
+        TRY(launched(c, launch_count_sub_range(c->pool.as<uint32_t>(), c->offsets.as<uint64_t>() + R,
+                                               c->offsets.as<uint64_t>() + c->nsets, c->cnt.as<uint32_t>(),
+                                               c->num_sms * 8, c->stream), "k_count_sub_range"));
+        counts = c->cnt.as<uint32_t>();
+      }
       {
         Prof pf(c, CLS_SELECT);
-        TRY(launched(c, launch_argmax(c->count_total.as<uint32_t>(), nullptr, (uint32_t)nsp(c),
+        TRY(launched(c, launch_argmax(const_cast<uint32_t*>(counts), nullptr, (uint32_t)nsp(c),
                                       c->probe.as<unsigned long long>(), 0, nullptr, c->num_sms * kArgmaxCtasPerSM,
                                       c->stream, c->rounds > 1), "k_argmax(probe)"));
       }
@@ -1694,6 +1731,14 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
         c->last_sel_steps = 1;
         c->st.probe_stops++;
       }
+      u_prev = probed ? (double)((uint64_t)k * c->rounds * g0) / (double)R : -1.0;
+    } else {
+      u_prev = -1.0;
+    }
+    if (!probed && prefix) {                                 // lookahead mispredicted: back to T
+      TRY(truncate_pool(c, R * c->rounds));
+      la_end = 0;
+      c->st.lookahead_drops++;
     }
     if (!probed) {
       const gim_status sst = select_launch(c, k);             // l.6 (reading R9)
@@ -1905,6 +1950,7 @@ gim_status gim_set_option(gim_ctx* c, gim_option opt, int64_t value) {
     case GIM_OPT_SELECT_PERSISTENT: c->sel_persistent = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_IMM_EARLY_EXIT: c->imm_early_exit = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_SELECT_CTA: c->sel_small = value ? 1 : 0; return GIM_OK;
+    case GIM_OPT_IMM_LOOKAHEAD: c->imm_lookahead = (value < 0 || value > 2) ? 1 : (int)value; return GIM_OK;
     case GIM_OPT_SELECT_CLUSTER: c->sel_cluster = value ? 1 : 0; return GIM_OK;
     case GIM_OPT_INV_SORT: c->inv_sort = (value < -1 || value > 1) ? -1 : (int)value; return GIM_OK;
     case GIM_OPT_CHUNK:

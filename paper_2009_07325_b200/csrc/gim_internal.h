@@ -36,6 +36,8 @@ cudaError_t launch_offsets_of(const uint64_t* scan, uint64_t cnt, uint64_t base,
                               cudaStream_t s);
 cudaError_t launch_count_sub(const uint32_t* pool, uint64_t e0, uint64_t e1, uint32_t* count_total,
                              int grid, cudaStream_t s);
+cudaError_t launch_count_sub_range(const uint32_t* pool, const uint64_t* e0p, const uint64_t* e1p, uint32_t* cnt,
+                                   int grid, cudaStream_t s);
 
 cudaError_t launch_philox_bench(uint64_t seed, uint32_t per_thread, uint32_t* sink, int grid, cudaStream_t s,
                                 int chains);

@@ -1447,6 +1447,20 @@ __global__ void __launch_bounds__(256) k_store(const uint32_t* __restrict__ stag
   if (blockIdx.x == 0 && threadIdx.x == 0) offsets_out[count] = pool_base + scan[count];
 }
 
+// cnt[v] -= 1 for every element of pool[*e0, *e1) (bounds read on the device: the prefix counts
+// of a lookahead round, gim_imm).
+__global__ void k_count_sub_range(const uint32_t* __restrict__ pool, const uint64_t* __restrict__ e0p,
+                                  const uint64_t* __restrict__ e1p, uint32_t* __restrict__ cnt) {
+  const uint64_t e0 = *e0p, e1 = *e1p;
+  for (uint64_t t = e0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < e1; t += (uint64_t)gridDim.x * blockDim.x)
+    atomicSub(cnt + pool[t], 1u);
+}
+cudaError_t launch_count_sub_range(const uint32_t* pool, const uint64_t* e0p, const uint64_t* e1p, uint32_t* cnt,
+                                   int grid, cudaStream_t s) {
+  k_count_sub_range<<<grid, 256, 0, s>>>(pool, e0p, e1p, cnt);
+  return cudaGetLastError();
+}
+
 // count_total[v] += 1 for every element of pool[e0, e1) (replicated pool: the gathered round).
 __global__ void k_count_add(const uint32_t* __restrict__ pool, uint64_t e0, uint64_t e1,
                             uint32_t* __restrict__ count_total) {

@@ -24,7 +24,7 @@ LIB_PATH = os.environ.get("GIM_LIB_PATH") or os.path.join(_HERE, "libgim.so")
 GIM_OK, GIM_EINVAL, GIM_ESTATE, GIM_ENOMEM, GIM_ECUDA, GIM_ECOLL, GIM_ELTWEIGHT = range(7)
 IC, LT = 0, 1
 W_EXPLICIT, W_WC, W_UNIFORM = 0, 1, 2
-OPT_FORCE_GIANT, OPT_QUEUE_CAP, OPT_PROFILE, OPT_STAGING_CAP, OPT_SELECT_GRAPH, OPT_INV_SEGMENTS, OPT_ARGMAX_CAND, OPT_IC_LANE, OPT_SPECULATE, OPT_MB_CHAINS, OPT_PDL, OPT_GIANT_NT, OPT_FRESH_FINAL, OPT_SELECT_PERSISTENT, OPT_SKIP, OPT_SPILL, OPT_SELECT_FUSED, OPT_FUSED_CTAS, OPT_FORCE_COLLECTIVES, OPT_GIANT_SHARED, OPT_SKIP_LANE_CAP, OPT_SELECT_COOP, OPT_IMM_EARLY_EXIT, OPT_INV_PASSES, OPT_L2_PERSIST, OPT_SELECT_CTA, OPT_INV_SORT, OPT_CHUNK, OPT_SELECT_CLUSTER = 1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23, 24, 26, 27, 28, 29, 30, 31
+OPT_FORCE_GIANT, OPT_QUEUE_CAP, OPT_PROFILE, OPT_STAGING_CAP, OPT_SELECT_GRAPH, OPT_INV_SEGMENTS, OPT_ARGMAX_CAND, OPT_IC_LANE, OPT_SPECULATE, OPT_MB_CHAINS, OPT_PDL, OPT_GIANT_NT, OPT_FRESH_FINAL, OPT_SELECT_PERSISTENT, OPT_SKIP, OPT_SPILL, OPT_SELECT_FUSED, OPT_FUSED_CTAS, OPT_FORCE_COLLECTIVES, OPT_GIANT_SHARED, OPT_SKIP_LANE_CAP, OPT_SELECT_COOP, OPT_IMM_EARLY_EXIT, OPT_INV_PASSES, OPT_L2_PERSIST, OPT_SELECT_CTA, OPT_INV_SORT, OPT_CHUNK, OPT_SELECT_CLUSTER, OPT_IMM_LOOKAHEAD = 1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23, 24, 26, 27, 28, 29, 30, 31, 32
 
 _STATUS = {0: "GIM_OK", 1: "GIM_EINVAL", 2: "GIM_ESTATE", 3: "GIM_ENOMEM", 4: "GIM_ECUDA",
            5: "GIM_ECOLL", 6: "GIM_ELTWEIGHT"}
@@ -54,7 +54,7 @@ class StatsC(ctypes.Structure):
                 ("ms_inv", _dbl), ("ms_select", _dbl), ("n_rr_launches", _u64),
                 ("n_giant_launches", _u64), ("n_syncs", _u64), ("n_allocs", _u64),
                 ("host_ms_sync", _dbl), ("host_ms_api", _dbl), ("fused_fallbacks", _u64),
-                ("probe_stops", _u64)]
+                ("probe_stops", _u64), ("lookahead_drops", _u64)]
 
 
 # name -> (restype, argtypes); exactly the functions declared in include/gim.h

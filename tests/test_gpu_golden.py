@@ -37,10 +37,12 @@ def _rel(a, b):
 
 
 @pytest.mark.parametrize("key,early,chunk", [("C1", 1, 0), ("C2", 1, 0), ("C3", 1, 0), ("C4", 1, 0), ("C5", 1, 0),
-                                             ("C1", 0, 0), ("C3", 0, 0), ("C3", 1, 1 << 18), ("C5", 1, 1 << 22)])
+                                             ("C1", 0, 0), ("C3", 0, 0), ("C3", 1, 1 << 18), ("C5", 1, 1 << 22),
+                                             ("C3", 2, 0), ("C5", 2, 0)])
 def test_imm_golden(key, early, chunk):
     """early = 1: the default bounded greedy in the estimation rounds (stopped rounds checked by
-    tests/imm_trace.py); early = 0: every round's k steps, cov_i exactly as the oracle's. chunk:
+    tests/imm_trace.py); early = 0: every round's k steps, cov_i exactly as the oracle's; early = 2:
+    lookahead sampling forced one round ahead (its drop path runs when a round needs selection). chunk:
     RR ids per generation chunk (0 = the default 2^25; small chunks: every round in several)."""
     gd = json.load(open(os.path.join(GOLDEN, f"imm_{key}.json")))
     w = gi.WORKLOADS[key]
@@ -49,7 +51,8 @@ def test_imm_golden(key, early, chunk):
     c = P.Gim(0)
     try:
         c.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme, p_uniform=w.p_uniform)
-        c.set_option(P.OPT_IMM_EARLY_EXIT, early)
+        c.set_option(P.OPT_IMM_EARLY_EXIT, min(early, 1))
+        c.set_option(P.OPT_IMM_LOOKAHEAD, 2 if early == 2 else 1)
         c.set_option(P.OPT_CHUNK, chunk)
         r = c.imm(w.k, w.eps, w.ell, w.rr_seed)
         assert _rel(r.ell_eff, gd["ell_eff"]) and _rel(r.eps_prime, gd["eps_prime"])
@@ -59,6 +62,8 @@ def test_imm_golden(key, early, chunk):
         stopped = check_cov_trace(r, gd["T_i"], gd["cov_i"], g.n, gd["eps_prime"], w.k)
         if not early:
             assert stopped == 0 and r.cov_i.tolist() == gd["cov_i"]
+        if early == 2 and key == "C3":
+            assert c.stats()["lookahead_drops"] >= 1      # round 3 needed its selection
         assert all(_rel(a, b) for a, b in zip(r.theta_i_real.tolist(), gd["theta_i"]))
         assert _rel(r.LB, gd["LB"]) and _rel(r.theta, gd["theta"])
         assert r.R_final == gd["R_final"] and r.covered == gd["cov"]

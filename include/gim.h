@@ -309,7 +309,7 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *                         all 148.
  *  GIM_OPT_IMM_LOOKAHEAD = 1 (default) / 0: in gim_imm, after a round the probe settled (bound
  *                         fraction u = k gain_0 / T_i), the following rounds whose passing fraction
- *                         (1 + eps') / 2^m exceeds u / 0.8 are sampled in the same generate call and
+ *                         (1 + eps') / 2^m exceeds u / 1.2 are sampled in the same generate call and
  *                         probed on the counts of their own prefix of T_m sets; a round the probe
  *                         does not settle truncates the pool to its T_m (gim_stats.lookahead_drops).
  *                         The trace, LB, theta, R_final and the seeds are unchanged. 2: two rounds

@@ -1026,7 +1026,7 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
   }
   auto* keys = reinterpret_cast<unsigned long long*>(c->keys.p);
   // P = 1: candidate list for the argmax (at most kMaxCand nodes whose initial count reaches
-  // tau_p1); the full-scan argmax runs only once no candidate reaches tau_p1
+  // tau_p1; counts only decrease, so a pick >= tau_p1 is the argmax over all nodes)
   const uint32_t kMaxCand = 1u << 16;
   uint32_t* cand = nullptr;
   unsigned int *hist = nullptr, *ncand = nullptr;

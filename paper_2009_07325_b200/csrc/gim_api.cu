@@ -1501,7 +1501,13 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
     cut.push_back(n);
     for (size_t q = 1; q < cut.size(); ++q) mono = mono && rp[cut[q - 1]] <= rp[cut[q]] && rp[cut[q]] <= m;
     if (!mono) cut = {0, n};
-    std::vector<cudaEvent_t> evs;
+    struct Events {                                    // destroyed on every exit path
+      std::vector<cudaEvent_t> v;
+      ~Events() {
+        for (cudaEvent_t e : v) cudaEventDestroy(e);
+      }
+    } ev_guard;
+    std::vector<cudaEvent_t>& evs = ev_guard.v;
     for (size_t q = 0; q + 1 < cut.size(); ++q) {
       const uint64_t e0 = rp[cut[q]], e1 = (q + 2 == cut.size()) ? m : rp[cut[q + 1]];
       if (e1 > e0) CK(cudaMemcpyAsync(c->src.as<uint32_t>() + e0, src + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, c->stream));
@@ -1523,7 +1529,6 @@ gim_status gim_load_graph(gim_ctx* c, uint32_t n, uint64_t m, const uint64_t* rp
     }
     CK(cudaMemcpyAsync(c->h_u64, flags, 16, cudaMemcpyDeviceToHost, c->stream));
     TRY(sync(c));
-    for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
     dfree(c, rp64);
     c->max_deg = (uint32_t)c->h_u64[1];
     c->skip_tab_valid = false;

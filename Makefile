@@ -7,13 +7,13 @@ ARCH    := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -lineinfo $(ARCH) -std=c++17 -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
            -Xcompiler -fno-fast-math -Xptxas -warn-spills
 PKG     := paper_2009_07325_b200
-SRCS    := $(PKG)/csrc/gim_api.cu $(PKG)/csrc/rr.cu $(PKG)/csrc/select.cu $(PKG)/csrc/csr.cu $(PKG)/csrc/mc.cu $(PKG)/csrc/skip.cu $(PKG)/csrc/inv_sort.cu
+SRCS    := $(PKG)/csrc/gim_api.cu $(PKG)/csrc/rr.cu $(PKG)/csrc/select.cu $(PKG)/csrc/csr.cu $(PKG)/csrc/mc.cu $(PKG)/csrc/skip.cu $(PKG)/csrc/inv_sort.cu $(PKG)/csrc/nccl_ex.cu
 HDRS    := $(PKG)/csrc/gim_device.cuh $(PKG)/csrc/gim_internal.h include/gim.h
 
 all: $(PKG)/libgim.so oracle/liboracle.so gim_inputs/libplg.so
 
 $(PKG)/libgim.so: $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -ldl
 
 oracle/liboracle.so: oracle/gim_oracle.c
 	gcc -O2 -std=c11 -D_DEFAULT_SOURCE -ffp-contract=off -fno-fast-math -fPIC -shared $< -o $@ -lm

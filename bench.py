@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo + --same-device: functional multi-rank test on 1 GPU)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (functional testing)")
+    ap.add_argument("--torch-collectives", action="store_true",
+                    help="exchange through torch.distributed callbacks instead of the library's own NCCL communicator")
     ap.add_argument("--skip", action="store_true",
                     help="geometric-skip RNG contract (reading R31, GIM_OPT_SKIP) instead of one coin per in-edge")
     ap.add_argument("--protocol", default="replicated", choices=["replicated", "allreduce", "reducescatter"],
@@ -276,14 +278,26 @@ def run_gim(args, w):
     ctx.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme, weights=g.weights, p_uniform=w.p_uniform)
     if args.rounds > 1:
         ctx.set_rounds(args.rounds)
+    exchange = {"kind": "none"}
+
     def hooks(cx):
         if world > 1 or args.force_collectives:
             cx.set_shard(rank, world)
-            cx.set_allreduce(P.torch_allreduce())
-            if args.protocol == "replicated":      # no per-step collectives
-                cx.set_allgather(P.torch_allgather())
-            elif args.protocol == "reducescatter":
-                cx.set_reducescatter(P.torch_reducescatter())
+            native = not args.torch_collectives and args.backend == "nccl"
+            if native:
+                try:          # the library's own NCCL communicator (gim_set_nccl): no Python per step
+                    P.setup_nccl(cx, rank, world, args.protocol)
+                    exchange["kind"] = "native NCCL (gim_set_nccl)"
+                except Exception as ex:   # noqa: BLE001 — fall back to the torch.distributed callbacks
+                    exchange["fallback"] = str(ex)[:120]
+                    native = False
+            if not native:
+                cx.set_allreduce(P.torch_allreduce())
+                if args.protocol == "replicated":      # no per-step collectives
+                    cx.set_allgather(P.torch_allgather())
+                elif args.protocol == "reducescatter":
+                    cx.set_reducescatter(P.torch_reducescatter())
+                exchange["kind"] = "torch.distributed callbacks"
             if args.force_collectives:
                 cx.set_option(P.OPT_FORCE_COLLECTIVES, 1)
     hooks(ctx)
@@ -502,7 +516,8 @@ def run_gim(args, w):
                 "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
                 "config": {**config_of(w, world, args.rounds, args.protocol, args.force_collectives),
                            "rng": ("geometric-skip contract (reading R31, GIM_OPT_SKIP)" if args.skip else
-                                   "Philox4x32-10 coin per in-edge slot (reading R16, north_star)")},
+                                   "Philox4x32-10 coin per in-edge slot (reading R16, north_star)"),
+                           **({"exchange": exchange} if exchange["kind"] != "none" else {})},
                 "imm_time_s": ms / args.steps / 1000.0,
                 "rr_sets_per_step": r0.R_final, "theta": r0.theta, "LB": r0.LB, "rounds": r0.rounds,
                 "spread_est": r0.spread_est,

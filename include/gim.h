@@ -110,6 +110,17 @@ typedef int (*gim_reducescatter_fn)(void* dev_send, void* dev_recv, uint64_t rec
                                     void* user);
 gim_status gim_set_reducescatter(gim_ctx* ctx, gim_reducescatter_fn fn, void* user);
 
+/* Native NCCL exchange: instead of callbacks, the library issues the protocol's collectives
+ * itself on its stream through an NCCL communicator it creates and owns (NCCL over NVLink /
+ * NVSwitch; the libnccl.so.2 already loaded in the process, e.g. torch's, else the system's).
+ * gim_nccl_unique_id fills a 128-byte ncclUniqueId on one rank; the caller broadcasts it; every
+ * rank then calls gim_set_nccl collectively (after gim_set_shard; rank / world must match).
+ * protocol: 0 = dense per-step all-reduce, 1 = replicated pool (all-gather), 2 = node-sharded
+ * (reduce-scatter + all-reduce) — the same protocols as the callback hooks, same results.
+ * GIM_ECOLL when NCCL cannot be loaded or the communicator cannot be created. */
+gim_status gim_nccl_unique_id(void* id_out);
+gim_status gim_set_nccl(gim_ctx* ctx, const void* id, int rank, int world, int protocol);
+
 /* Route every device allocation of ctx through the caller (e.g. torch's caching allocator).
  * Must be called before gim_load_graph. alloc_fn returns NULL on failure. */
 typedef void* (*gim_alloc_fn)(uint64_t bytes, void* cuda_stream, void* user);

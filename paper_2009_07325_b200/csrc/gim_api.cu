@@ -90,6 +90,7 @@ struct gim_ctx {
   uint32_t rounds = 1;
   // sharding
   int rank = 0, world = 1;
+  void* nccl = nullptr;              // communicator owned by the ctx (gim_set_nccl)
   gim_allreduce_fn arfn = nullptr;
   void* aruser = nullptr;
   gim_allgather_fn agfn = nullptr;   // set: replicated-pool protocol (no per-step collectives)
@@ -1407,6 +1408,7 @@ void gim_destroy(gim_ctx* c) {
   cudaStreamDestroy(c->stream2);
   cudaEventDestroy(c->ev_cnt_copied);
   cudaEventDestroy(c->ev_sel_done);
+  if (c->nccl) nccl_comm_destroy(c->nccl);
   // the default pool keeps freed memory (release threshold = max, set in gim_create): hand the
   // unused part back so other processes on this GPU can use it
   cudaMemPool_t mp;
@@ -1602,6 +1604,30 @@ gim_status gim_set_reducescatter(gim_ctx* c, gim_reducescatter_fn fn, void* user
   c->err.clear();
   c->rsfn = fn;
   c->rsuser = user;
+  return GIM_OK;
+}
+
+gim_status gim_nccl_unique_id(void* id_out) {
+  if (!id_out) return GIM_EINVAL;
+  return nccl_unique_id(id_out) ? GIM_ECOLL : GIM_OK;
+}
+
+gim_status gim_set_nccl(gim_ctx* c, const void* id, int rank, int world, int protocol) {
+  if (!c) return GIM_EINVAL;
+  c->err.clear();
+  if (!id || protocol < 0 || protocol > 2) return fail(c, GIM_EINVAL, "id required; protocol 0 (all-reduce), 1 (replicated), 2 (node-sharded)");
+  if (rank != c->rank || world != c->world) return fail(c, GIM_EINVAL, "rank / world must match gim_set_shard");
+  if (!nccl_available()) return fail(c, GIM_ECOLL, "libnccl.so.2 not found");
+  DeviceGuard g(c->device);
+  if (c->nccl) nccl_comm_destroy(c->nccl);
+  c->nccl = nullptr;
+  if (nccl_comm_init(&c->nccl, id, rank, world)) return fail(c, GIM_ECOLL, "ncclCommInitRank failed");
+  c->arfn = nccl_allreduce_i32;
+  c->aruser = c->nccl;
+  c->agfn = protocol == 1 ? nccl_allgather_bytes : nullptr;
+  c->aguser = protocol == 1 ? c->nccl : nullptr;
+  c->rsfn = protocol == 2 ? nccl_reducescatter_i32 : nullptr;
+  c->rsuser = protocol == 2 ? c->nccl : nullptr;
   return GIM_OK;
 }
 

@@ -7,6 +7,14 @@ namespace gim {
 struct RRParams;
 
 int lt_blocks_per_sm();
+// native NCCL exchange (nccl_ex.cu): dlopen'ed NCCL; hooks with the gim_*_fn signatures
+bool nccl_available();
+int nccl_unique_id(void* out128);
+int nccl_comm_init(void** comm, const void* id128, int rank, int world);
+void nccl_comm_destroy(void* comm);
+int nccl_allreduce_i32(void* buf, uint64_t count, void* stream, void* comm);
+int nccl_allgather_bytes(const void* send, uint64_t bytes, void* recv, void* stream, void* comm);
+int nccl_reducescatter_i32(void* send, void* recv, uint64_t recv_count, void* stream, void* comm);
 #ifdef GIM_GIANT_TRACE
 void giant_trace_dump(cudaStream_t s);   // diagnostic build: per-set K-GIANT timing to stderr
 #endif

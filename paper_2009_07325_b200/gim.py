@@ -67,6 +67,8 @@ SIGNATURES = {
     "gim_set_allreduce": (_i32, [_p, ALLREDUCE_FN, _p]),
     "gim_set_allgather": (_i32, [_p, ALLGATHER_FN, _p]),
     "gim_set_reducescatter": (_i32, [_p, REDUCESCATTER_FN, _p]),
+    "gim_nccl_unique_id": (_i32, [_p]),
+    "gim_set_nccl": (_i32, [_p, _p, _i32, _i32, _i32]),
     "gim_set_allocator": (_i32, [_p, ALLOC_FN, FREE_FN, _p]),
     "gim_generate_rr": (_i32, [_p, _u64, _u64]),
     "gim_select": (_i32, [_p, _u32, _p, _p, _p]),
@@ -203,6 +205,14 @@ class Gim:
         self._keep.append(cb)
         self._check(self._lib.gim_set_allgather(self._h, cb, None))
 
+    def set_nccl(self, nccl_id: bytes, rank: int, world: int, protocol: str = "allreduce"):
+        """Native NCCL exchange (include/gim.h gim_set_nccl): the library creates its own NCCL
+        communicator from the 128-byte id (same on every rank, see nccl_unique_id / setup_nccl)
+        and issues the protocol's collectives on its stream itself; collective over the world."""
+        proto = {"allreduce": 0, "replicated": 1, "reducescatter": 2}[protocol]
+        buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        self._check(self._lib.gim_set_nccl(self._h, buf, rank, world, proto))
+
     def set_reducescatter(self, fn: Callable[[int, int, int, int], int]):
         """fn(send_ptr, recv_ptr, recv_count_int32, cuda_stream) -> 0: SUM reduce-scatter of int32
         (this rank's block of the sum). With set_allreduce (and no all-gather), world > 1
@@ -301,6 +311,28 @@ class Gim:
         ms = _dbl()
         self._check(self._lib.gim_microbench_philox(self._h, groups, ctypes.byref(ms)))
         return ms.value
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (include/gim.h gim_nccl_unique_id)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    st = lib.gim_nccl_unique_id(buf)
+    if st != GIM_OK:
+        raise GimError(st, "ncclGetUniqueId failed (libnccl.so.2 not loadable?)")
+    return buf.raw
+
+
+def setup_nccl(ctx: "Gim", rank: int, world: int, protocol: str = "allreduce", group=None):
+    """Rank 0 draws the NCCL id, torch.distributed broadcasts it (any backend), every rank then
+    hands it to ctx.set_nccl: from there on the library runs its own NCCL collectives."""
+    nid = nccl_unique_id() if rank == 0 else bytes(128)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [nid]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        nid = obj[0]
+    ctx.set_nccl(nid, rank, world, protocol)
 
 
 def torch_allreduce(group=None, device: str = "cuda"):

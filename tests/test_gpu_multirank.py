@@ -244,3 +244,34 @@ def test_nccl_world1_protocols():
             c.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("proto", ["allreduce", "replicated", "reducescatter"])
+def test_native_nccl_world1_protocols(proto):
+    """The library's own NCCL communicator (gim_set_nccl: collectives issued by libgim on its
+    stream, no Python per step) at world 1 with GIM_OPT_FORCE_COLLECTIVES: every protocol's code
+    path runs through real NCCL collectives and the results equal the oracle's (the RR sets of the
+    pool element by element, the selection, the full IMM)."""
+    w = gi.WORKLOADS["C2"]
+    g = gi.workload_graph("C2")
+    T, k = 20011, 20
+    o = oracle.Oracle(g, w.model, w.scheme)
+    o.generate(T, w.rr_seed)
+    ooff, onodes, _ = o.export()
+    oseeds, ogains, ocov = o.select(k)
+    oimm = oracle.Oracle(g, w.model, w.scheme).imm(k, w.eps, w.ell, w.rr_seed)
+    c = P.Gim(0)
+    c.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme)
+    c.set_shard(0, 1)
+    P.setup_nccl(c, 0, 1, proto)
+    c.set_option(P.OPT_FORCE_COLLECTIVES, 1)
+    c.reset_stats()
+    c.generate_rr(T, w.rr_seed)
+    ids, off, nodes = c.rr_export(sort_each_set=True)
+    assert np.array_equal(off, ooff) and np.array_equal(nodes, onodes)
+    seeds, gains, cov = c.select(k)
+    assert c.stats()["allreduces"] > 0 or proto == "replicated"
+    assert seeds.tolist() == oseeds.tolist() and gains.tolist() == ogains.tolist() and cov == ocov
+    r = c.imm(k, w.eps, w.ell, w.rr_seed)
+    assert r.seeds.tolist() == oimm.seeds.tolist() and r.R_final == oimm.R_final and r.LB == oimm.LB, proto
+    c.close()

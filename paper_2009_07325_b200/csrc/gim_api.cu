@@ -188,6 +188,8 @@ struct gim_ctx {
   // CUDA graph of the k-step selection loop (P = 1), valid while its key is unchanged
   cudaGraphExec_t sel_exec = nullptr;    // fused selection graph
   std::vector<cudaGraphExec_t> sel_parts;   // default selection: consecutive graphs of greedy steps
+  cudaGraphExec_t p_exec = nullptr;      // P > 1 selection loop with the native NCCL exchange
+  std::vector<uintptr_t> p_key;
   std::vector<uintptr_t> sel_key;
   int use_graph = 1;
 };
@@ -910,6 +912,32 @@ gim_status generate(gim_ctx* c, uint64_t theta_sets, uint64_t seed, bool host_sy
 }
 
 // ---- NodeSelection (O7) ---------------------------------------------------------------------
+// Replays the enqueue sequence `body` (kernels + the library's own NCCL collectives, which stream
+// capture supports) from a CUDA graph cached under `key`: the k-step loops of the P > 1
+// protocols then cost one graph launch instead of a host round of launches per step.
+template <class Body>
+gim_status replay_captured(gim_ctx* c, const std::vector<uintptr_t>& key, Body body, int launches) {
+  if (!c->p_exec || key != c->p_key) {
+    if (c->p_exec) cudaGraphExecDestroy(c->p_exec);
+    c->p_exec = nullptr;
+    c->p_key.clear();
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const gim_status st = body();
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (st != GIM_OK) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (e != cudaSuccess) return fail_cuda(c, "stream capture (P > 1 selection)", e);
+    const cudaError_t ie = cudaGraphInstantiate(&c->p_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) return fail_cuda(c, "cudaGraphInstantiate (P > 1 selection)", ie);
+    c->p_key = key;
+  }
+  return launched(c, cudaGraphLaunch(c->p_exec, c->stream), "selection graph (P > 1)", launches);
+}
+
 gim_status read_keys(gim_ctx* c, uint32_t kk) {
   if (c->h_keys_cap < kk + 1) {
     if (c->h_keys) cudaFreeHost(c->h_keys);
@@ -960,21 +988,33 @@ gim_status select_launch_rs(gim_ctx* c, uint32_t k, const InvSegDev* segd, SelCt
   c->st.allreduces++;
   if (c->rsfn(c->cnt.p, gcnt, ns, c->stream, c->rsuser)) return fail(c, GIM_ECOLL, "reduce-scatter(count) failed");
   Prof pf(c, CLS_SELECT);
-  for (uint32_t j = 0; j < kk; ++j) {
-    TRY(launched(c, launch_argmax(gcnt, dshard, ns_valid, lkeys, (int)j, nullptr, c->num_sms * kArgmaxCtasPerSM,
-                                  c->stream, false, id_base, ctl), "k_argmax(shard)"));
-    TRY(launched(c, launch_rs_pack(lkeys, (int)j, r, W, kx, c->stream), "k_rs_pack"));
-    c->st.allreduces++;
-    if (c->arfn(kx, 2ull * W, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(keys) failed");
-    TRY(launched(c, launch_rs_pick(kx, W, keys, (int)j, gcnt, id_base, ns_valid, c->stream), "k_rs_pick"));
-    TRY(launched(c, launch_cover(keys, (int)j, segd, ctl, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
-                                 c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * kCoverCtasPerSM,
-                                 c->stream, limited, nullptr), "k_cover"));
-    if (j + 1 < kk) {
+  auto loop = [&]() -> gim_status {
+    for (uint32_t j = 0; j < kk; ++j) {
+      TRY(launched(c, launch_argmax(gcnt, dshard, ns_valid, lkeys, (int)j, nullptr, c->num_sms * kArgmaxCtasPerSM,
+                                    c->stream, false, id_base, ctl), "k_argmax(shard)"));
+      TRY(launched(c, launch_rs_pack(lkeys, (int)j, r, W, kx, c->stream), "k_rs_pack"));
       c->st.allreduces++;
-      if (c->rsfn(dec, dshard, ns, c->stream, c->rsuser)) return fail(c, GIM_ECOLL, "reduce-scatter(dec) failed");
-      CK(cudaMemsetAsync(dec, 0, npad * 4, c->stream));
+      if (c->arfn(kx, 2ull * W, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(keys) failed");
+      TRY(launched(c, launch_rs_pick(kx, W, keys, (int)j, gcnt, id_base, ns_valid, c->stream), "k_rs_pick"));
+      TRY(launched(c, launch_cover(keys, (int)j, segd, ctl, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
+                                   c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * kCoverCtasPerSM,
+                                   c->stream, limited, nullptr), "k_cover"));
+      if (j + 1 < kk) {
+        c->st.allreduces++;
+        if (c->rsfn(dec, dshard, ns, c->stream, c->rsuser)) return fail(c, GIM_ECOLL, "reduce-scatter(dec) failed");
+        CK(cudaMemsetAsync(dec, 0, npad * 4, c->stream));
+      }
     }
+    return GIM_OK;
+  };
+  if (c->nccl && c->use_graph) {
+    const std::vector<uintptr_t> key = {1, (uintptr_t)c->nccl, (uintptr_t)gcnt, (uintptr_t)dshard, (uintptr_t)lkeys,
+                                        (uintptr_t)kx, (uintptr_t)keys, (uintptr_t)segd, (uintptr_t)c->offsets.p,
+                                        (uintptr_t)c->pool.p, (uintptr_t)c->covered.p, (uintptr_t)c->cnt.p,
+                                        (uintptr_t)dec, (uintptr_t)ctl, kk, (uintptr_t)n, (uintptr_t)limited};
+    TRY(replay_captured(c, key, loop, 4 * (int)kk));
+  } else {
+    TRY(loop());
   }
   c->sel_fused_used = false;
   TRY(read_keys(c, kk));
@@ -1220,23 +1260,37 @@ gim_status select_launch(gim_ctx* c, uint32_t k) {
                    2 * (int)(cuts[q + 1] - cuts[q])));
     }
   } else {
-    for (uint32_t j = 0; j < kk; ++j) {
-      {
-        Prof pf(c, CLS_SELECT);
-        if (cand)
-          TRY(launched(c, launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream, ctl),
-                       "k_argmax_cand"));
-        else
-          TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, (uint32_t)n, keys, (int)j, nullptr,
-                                        c->num_sms * kArgmaxCtasPerSM, c->stream, mr != nullptr, 0u, ctl), "k_argmax"));
-        TRY(launched(c, launch_cover(keys, (int)j, segd, ctl, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
-                                     c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * kCoverCtasPerSM,
-                                     c->stream, limited, mr), "k_cover"));
+    auto loop = [&]() -> gim_status {
+      for (uint32_t j = 0; j < kk; ++j) {
+        {
+          Prof pf(c, CLS_SELECT);
+          if (cand)
+            TRY(launched(c, launch_argmax_cand(c->cnt.as<uint32_t>(), cand, ncand, keys, (int)j, 64, c->stream, ctl),
+                         "k_argmax_cand"));
+          else
+            TRY(launched(c, launch_argmax(c->cnt.as<uint32_t>(), dec, (uint32_t)n, keys, (int)j, nullptr,
+                                          c->num_sms * kArgmaxCtasPerSM, c->stream, mr != nullptr, 0u, ctl), "k_argmax"));
+          TRY(launched(c, launch_cover(keys, (int)j, segd, ctl, c->offsets.as<uint64_t>(), c->pool.as<uint32_t>(),
+                                       c->covered.as<uint8_t>(), c->cnt.as<uint32_t>(), dec, c->num_sms * kCoverCtasPerSM,
+                                       c->stream, limited, mr), "k_cover"));
+        }
+        if (dec && j + 1 < kk) {
+          c->st.allreduces++;
+          if (c->arfn(dec, n, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(dec) failed");
+        }
       }
-      if (dec && j + 1 < kk) {
-        c->st.allreduces++;
-        if (c->arfn(dec, n, c->stream, c->aruser)) return fail(c, GIM_ECOLL, "all-reduce(dec) failed");
-      }
+      return GIM_OK;
+    };
+    if (dec && c->nccl && c->use_graph && !c->profile) {
+      // dense all-reduce protocol with the native exchange: the whole k-step loop as one graph
+      const std::vector<uintptr_t> key = {2, (uintptr_t)c->nccl, (uintptr_t)c->cnt.p, (uintptr_t)dec, (uintptr_t)keys,
+                                          (uintptr_t)segd, (uintptr_t)c->offsets.p, (uintptr_t)c->pool.p,
+                                          (uintptr_t)c->covered.p, (uintptr_t)ctl, kk, (uintptr_t)n, (uintptr_t)limited,
+                                          (uintptr_t)c->rounds};
+      Prof pf(c, CLS_SELECT);
+      TRY(replay_captured(c, key, loop, 3 * (int)kk));
+    } else {
+      TRY(loop());
     }
   }
   if (c->h_keys_cap < kk + 1) {
@@ -1400,6 +1454,7 @@ void gim_destroy(gim_ctx* c) {
   if (c->sel_exec) cudaGraphExecDestroy(c->sel_exec);
   for (cudaGraphExec_t& ex : c->sel_parts) cudaGraphExecDestroy(ex);
   c->sel_parts.clear();
+  if (c->p_exec) cudaGraphExecDestroy(c->p_exec);
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
   if (c->h_u64) cudaFreeHost(c->h_u64);
   if (c->h_keys) cudaFreeHost(c->h_keys);

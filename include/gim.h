@@ -221,10 +221,13 @@ gim_status gim_set_rounds(gim_ctx* ctx, uint32_t rounds);
  *  GIM_OPT_PROFILE      = 1: time every kernel class with CUDA events (see gim_get_stats).
  *  GIM_OPT_STAGING_CAP  = elements of staging memory to start from (forces retries if tiny).
  *  GIM_OPT_SELECT_GRAPH = 1 (default): for P = 1 replay the 2k argmax/cover launches of a
- *                          NodeSelection from a captured CUDA graph; 0: launch them one by one.
- *  GIM_OPT_INV_SEGMENTS = 1 (default): index each generation chunk's sets as it is stored (one
- *                          inverted-index segment per chunk); 0: rebuild one index over the
- *                          whole pool at every selection (ablation).
+ *                          NodeSelection from captured CUDA graphs of consecutive steps ([0, 8),
+ *                          [8, 32), [32, k); a bounded greedy checks its stop flag between them;
+ *                          with gim_set_nccl also the P > 1 step loops); 0: launch them one by one.
+ *  GIM_OPT_INV_SEGMENTS = 1 (default): the sets generated since the last selection are indexed
+ *                          as one new inverted-index segment when a selection needs them (rounds
+ *                          settled by gim_imm's probe are merged into the next segment); 0:
+ *                          rebuild one index over the whole pool at every selection (ablation).
  *  GIM_OPT_ARGMAX_CAND  = 1 (default): for P = 1 and n >= 2^20 the per-step argmax scans a candidate list of
  *                          <= 65536 nodes (count >= a power-of-two threshold tau; counts only
  *                          decrease, so a best candidate >= tau is the argmax over all nodes); a

@@ -1754,6 +1754,9 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
                         !c->force_coll && !c->speculate;
   double u_prev = -1.0;
   uint64_t la_end = 0;                                       // pool size sampled ahead (0: none)
+  // the probe's bound fraction u is about the same from round to round while the passing
+  // fraction halves: once a probe did not settle its round, later ones will not either
+  bool probe_on = true;
   for (int i = 1; i <= i_max && i <= 64; ++i) {              // Alg. 2 l.2
     const double x = n / std::ldexp(1.0, i);                 // l.3
     const double theta_i = K.lambda_p / x;                   // l.4 (f = lambda', reading R1)
@@ -1800,7 +1803,7 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
     // selection — their index segment is built later, merged with the next rounds' sets
     bool probed = false;
     const bool prefix = la_end > R;                          // the pool holds sets beyond this round
-    if (c->sel_cstar && (c->inv_pending || prefix) && global_counts && !c->speculate) {
+    if (c->sel_cstar && (c->inv_pending || prefix) && global_counts && !c->speculate && (probe_on || prefix)) {
       TRY(ensure(c, c->probe, 8));
       CK(cudaMemsetAsync(c->probe.p, 0, 8, c->stream));
       const uint32_t* counts = c->count_total.as<uint32_t>();
@@ -1828,6 +1831,7 @@ gim_status gim_imm(gim_ctx* c, uint32_t k, double eps, double ell, uint64_t seed
         c->st.probe_stops++;
       }
       u_prev = probed ? (double)((uint64_t)k * c->rounds * g0) / (double)R : -1.0;
+      if (!probed) probe_on = false;
     } else {
       u_prev = -1.0;
     }

@@ -275,3 +275,21 @@ def test_native_nccl_world1_protocols(proto):
     r = c.imm(k, w.eps, w.ell, w.rr_seed)
     assert r.seeds.tolist() == oimm.seeds.tolist() and r.R_final == oimm.R_final and r.LB == oimm.LB, proto
     c.close()
+
+
+def test_native_nccl_errors():
+    """gim_set_nccl validates its arguments before touching NCCL: rank / world must match
+    gim_set_shard, the protocol must be 0..2, an id is required."""
+    g = gi.workload_graph("C1")
+    w = gi.WORKLOADS["C1"]
+    c = P.Gim(0)
+    c.load_graph(g.n, g.row_ptr, g.src, w.model, w.scheme)
+    c.set_shard(0, 1)
+    nid = P.nccl_unique_id()
+    assert len(nid) == 128
+    with pytest.raises(P.GimError, match="GIM_EINVAL"):
+        c.set_nccl(nid, 0, 2, "allreduce")             # world differs from gim_set_shard
+    with pytest.raises(KeyError):
+        c.set_nccl(nid, 0, 1, "bogus")
+    c.set_nccl(nid, 0, 1, "replicated")                # valid: a world-1 communicator
+    c.close()
